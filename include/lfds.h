@@ -1,0 +1,155 @@
+/*
+ * lfds.h — C ABI of the B200-native blocked separable Helmholtz solver
+ * (layered-medium fast direct solver, arXiv 1909.01299, Druskin & Zaslavsky).
+ *
+ * Operation (Eq. (fd); Kronecker form Eq. (fdmtr) PAPER.md:38-40 with
+ * reading R1 of DESIGN.md):  for unknown nodes (i,j,k), 1<=i<=nx, 1<=j<=ny, 1<=k<=nz,
+ *
+ *   sigma_k [ (u_{i+1}-u_i)/hx_i - (u_i-u_{i-1})/hx_{i-1} ] hy^_j hz^_k
+ * + sigma_k [ (u_{j+1}-u_j)/hy_j - (u_j-u_{j-1})/hy_{j-1} ] hx^_i hz^_k
+ * + [ sigma_{k+1/2}(u_{k+1}-u_k)/hz_k - sigma_{k-1/2}(u_k-u_{k-1})/hz_{k-1} ] hx^_i hy^_j
+ * + lambda u hx^_i hy^_j hz^_k  =  f hx^_i hy^_j hz^_k,
+ *
+ * hd^_i = (hd_{i-1} + hd_i)/2, homogeneous Dirichlet on all six faces
+ * (node 0 and node N+1 of every axis, reading R10).  lfds_solve returns the unique
+ * solution u by the paper's two-level blocked separable method (steps 1-7)
+ * on the device.  The method is direct: u = A^{-1} M f up to rounding.
+ *
+ * Data layout: fields f, u are [nrhs][nz][ny][nx] (x fastest), complex128 (interleaved
+ * re,im == torch.complex128 == cuDoubleComplex), or float64 when the plan was created
+ * with LFDS_F64 (all inputs real).
+ *
+ * Errors: every int-returning call returns an lfds_status; the message of the last error
+ * on the calling thread is lfds_last_error().  Nothing is ever silently regularised
+ * (SPEC S:303): a near-zero pivot is reported, not perturbed.
+ */
+#ifndef LFDS_H
+#define LFDS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lfds_plan lfds_plan;            /* opaque; owned by the library */
+typedef struct { double re, im; } lfds_z;      /* layout of complex128 */
+
+typedef enum {
+  LFDS_OK = 0,
+  LFDS_EINVAL = 1,        /* bad sizes/steps/partition/pointers (see lfds_setup_grid) */
+  LFDS_EEIG = 2,          /* 1D eigenbasis failed its residual / biorthonormality check */
+  LFDS_ERESONANCE = 3,    /* z-system pivot below 1e-14 x row norm (lambda resonant) */
+  LFDS_ENOMEM = 4,
+  LFDS_ECUDA = 5,
+  LFDS_ENCCL = 6,
+  LFDS_ENOTCONVERGED = 7, /* refinement did not reach the requested residual */
+  LFDS_ENODEVICE = 8      /* compute call on a host-only plan (options.device < 0) */
+} lfds_status;
+
+enum { LFDS_C128 = 0, LFDS_F64 = 1 };
+
+typedef struct {
+  int dtype;        /* LFDS_C128 or LFDS_F64 (real steps, sigma, lambda and f required)   */
+  int refine;       /* refinement passes after the first solve pass: 0..8, or -1 = auto   */
+                    /* (repeat while the residual improves 2x and exceeds refine_tol)     */
+  double refine_tol;/* auto mode: stop when ||Au - Mf||/||Mf|| <= refine_tol (e.g. 1e-13)  */
+  int residual_dd;  /* 1: refinement residual in double-double (reading R13), 0: fp64      */
+  int device;       /* CUDA device ordinal; <0 = host-only plan (setup/basis queries only) */
+  int rhs_chunk;    /* max right-hand sides processed per pipeline pass (0 = all)          */
+} lfds_options;
+
+/* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0. */
+void lfds_default_options(lfds_options* opt);
+
+/*
+ * Setup (timed separately from the solve; north_star): control volumes,
+ * per-block and global 1D generalized eigenpairs A_d W = M_d W Lambda, W^T M_d W = I
+ * (transpose reading R4), block classification (U = uniform real
+ * steps -> exact sine modes; R = real; C = complex), z tables, device upload.
+ *
+ *  hx[nx+1], hy[ny+1], hz[nz+1]  host, complex steps h_0..h_N (h_t joins node t and t+1);
+ *                                Re(h) > 0 required.
+ *  sigma_node[nz]                host, sigma_k at nodes k = 1..nz (Re > 0).
+ *  sigma_edge[nz+1]              host, sigma_{k+1/2} for k = 0..nz (Re > 0).
+ *  lambda                        the shift of Eq. (wave2) (complex accepted, reading R11).
+ *  if_x[n_if_x], if_y[n_if_y]    host, sorted 1-based interface nodes (width-1 planes,
+ *                                reading R9); 2 <= node <= N-1, consecutive nodes >= 2 apart.
+ *                                n_if = 0 gives a single block (the global separable solve).
+ *  opt                           may be NULL (defaults).
+ *  *out                          receives the plan; release with lfds_destroy.
+ * Returns LFDS_EINVAL on bad input, LFDS_EEIG if an eigenbasis fails its checks,
+ * LFDS_ECUDA / LFDS_ENOMEM on device errors.  All host arrays are only read.
+ */
+int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, const lfds_z* hz,
+                    const lfds_z* sigma_node, const lfds_z* sigma_edge, lfds_z lambda,
+                    int n_if_x, const int* if_x, int n_if_y, const int* if_y,
+                    const lfds_options* opt, lfds_plan** out);
+
+/* Device workspace (bytes, 256-B aligned) that lfds_solve needs for nrhs right-hand sides. */
+size_t lfds_workspace_bytes(const lfds_plan* plan, int nrhs);
+
+/*
+ * Solve A u = M f for nrhs right-hand sides on `cuda_stream` (a cudaStream_t; NULL =
+ * legacy default stream).  f_dev, u_dev: device pointers, [nrhs][nz][ny][nx], 16-byte
+ * aligned; u may alias f.  ws_dev: caller-owned device workspace of >= lfds_workspace_bytes.
+ * Stream-ordered: the call returns after enqueueing, except when refinement is on (it
+ * reads the residual norm back, which synchronises the stream).  The caller owns f, u, ws.
+ */
+int lfds_solve(lfds_plan* plan, const void* f_dev, void* u_dev, int nrhs,
+               void* ws_dev, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * End-to-end variant with HOST buffers (pinned or pageable): copies f to the device
+ * (inside ws: lfds_workspace_bytes_host), solves, copies u back, synchronises the stream.
+ */
+size_t lfds_workspace_bytes_host(const lfds_plan* plan, int nrhs);
+int lfds_solve_host(lfds_plan* plan, const void* f_host, void* u_host, int nrhs,
+                    void* ws_dev, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * Residual r = M f - A u (b-units, PAPER.md Eq. (fdmtr)) on the device; f_dev may be NULL
+ * (then r = -A u).  dd = 1 evaluates in double-double and rounds once.  r_dev is
+ * complex128 [nrhs][nz][ny][nx] even for LFDS_F64 plans.  If norms != NULL it receives
+ * 2*nrhs doubles (||r||_2, ||M f||_2 per rhs), which synchronises the stream.
+ */
+int lfds_residual(lfds_plan* plan, const void* u_dev, const void* f_dev, lfds_z* r_dev, int nrhs,
+                  int dd, double* norms, void* cuda_stream);
+
+typedef struct {
+  int passes;                  /* solve passes in the last lfds_solve (1 + refinements)     */
+  double rel_residual[9];      /* ||Au-Mf||/||Mf|| after each pass (max over rhs), if known */
+  double min_pivot_ratio;      /* min |pivot| / row-norm over all z-sweeps of the last call  */
+  int n_kernel_launches;       /* kernels enqueued by the last lfds_solve                   */
+} lfds_report;
+int lfds_get_report(const lfds_plan* plan, lfds_report* rep);
+
+typedef struct {
+  int nx, ny, nz;
+  int nbx, nby;                /* blocks per axis                                          */
+  int n_if_x, n_if_y;
+  int real_z;                  /* 1 if the z tables are real                                */
+  double setup_seconds;        /* host wall time of lfds_setup_grid                          */
+  double eig_max_residual;     /* max over all bases of ||AW-MWL||/(||A|| ||W||)              */
+  double eig_max_biorth;       /* max over all bases of ||W^T M W - I||_max                   */
+  size_t device_table_bytes;
+} lfds_info;
+int lfds_get_info(const lfds_plan* plan, lfds_info* info);
+
+/*
+ * Basis query (for tests): axis 0 = x, 1 = y; block = -1 for the global basis, else the
+ * block index along that axis.  *n receives the size; kind receives 0 = U (sine), 1 = R
+ * (real), 2 = C (complex); lam (n) and W (n*n, row-major W[p*n + l]) may be NULL.
+ */
+int lfds_get_basis(const lfds_plan* plan, int axis, int block, int* n, int* kind, int* lo,
+                   lfds_z* lam, lfds_z* W);
+
+void lfds_destroy(lfds_plan* plan);
+const char* lfds_last_error(void);
+const char* lfds_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LFDS_H */

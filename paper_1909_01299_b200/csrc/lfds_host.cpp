@@ -1,0 +1,832 @@
+// Host orchestration and C ABI (include/lfds.h) of the blocked separable solve
+// (arXiv 1909.01299).  Setup builds every table once (timed separately);
+// lfds_solve enqueues the seven steps as stream-ordered kernels:
+//
+//   pass 1 (per block S^ij)   step 1  f~ = (F_x (x) F_y (x) I) f,  F = W^T M      (k_gemm x2)
+//                             step 2  T_lm v~_lm = f~_lm (z-solves)               (k_zsolve_block<1>)
+//                             step 3  v at the rows next to every block face      (k_gemm x4)
+//   interface                 step 4  r_b = b - A v on the interface planes       (k_iface_res)
+//                             step 5  w on the planes via the global bases        (k_gemm, k_gsweep)
+//   pass 2 (per block)        step 6  w~ from the Dirichlet lifting of w          (k_gemm, k_zsolve_block<2>)
+//                             step 7  u = (W_x (x) W_y (x) I)(v~ + w~), u = w on planes (k_gemm x2, k_write_iface)
+//
+// optional refinement: r = M f - A u in double-double (k_residual), u += solve(r).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/lfds.h"
+#include "lfds_eig.h"
+#include "lfds_internal.h"
+
+using namespace lfds;
+
+static thread_local std::string g_err;
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+#define CUDA_TRY(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t _e = (x);                                                                    \
+    if (_e != cudaSuccess) return fail(LFDS_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+namespace {
+
+struct AxisBlock {
+  int lo, n;         // first node (1-based), interior size
+  Basis B;
+  int64_t F = 0, W = 0, lam = 0;  // TAB offsets: F[l*n+p] = W[p][l] hh_p, W[p*n+l], lam[l]
+};
+
+struct Axis {
+  int N = 0;
+  std::vector<zc> h, hh;
+  std::vector<int> iface;
+  std::vector<AxisBlock> blocks;
+  std::vector<int> blk_of;  // per node (0-based): block index or -1 (interface)
+  Basis G;                  // global basis
+  int64_t Wg = 0, lamg = 0, WI = 0, hoff = 0, hhoff = 0;
+};
+
+struct StageDescs {
+  int64_t off = 0;  // index of the first desc in the device desc array
+  int n = 0, maxM = 0;
+  int64_t maxN = 0;
+};
+
+struct PassPlan {  // descriptors for one (R, in_real, out_real)
+  GemmDesc* d_descs = nullptr;
+  ZBlock* d_zb = nullptr;
+  StageDescs s1x, s1y, s3g, s3h, s3x, s3y, s5r1, s5r2, s5p1, s5p2, s5wx, s5wy, s6f, s7y, s7x;
+  int max_systems = 0;
+  // workspace layout (bytes)
+  size_t off_ms = 0, off_t1 = 0, off_if = 0, off_red = 0, off_res = 0, total = 0;
+  int64_t g_off = 0, h_off = 0, vx_off = 0, vy_off = 0, rx = 0, ry = 0, r1 = 0, r2 = 0, p1 = 0, p2 = 0, wx = 0,
+          wy = 0, gf = 0;
+};
+
+}  // namespace
+
+struct lfds_plan {
+  lfds_options opt;
+  Axis ax[2];
+  int nz = 0;
+  std::vector<zc> hz, hhz, sig_node, sig_edge;
+  zc lam;
+  bool real_z = true;
+  int nbx = 0, nby = 0, mpad = 0, lpad = 0, fpad = 0;
+  // device tables
+  double2* d_tab = nullptr;
+  size_t tab_elems = 0;
+  ZTab zt_scaled{}, zt_plain{};
+  int64_t t_hz = 0, t_hhz = 0, t_sig = 0, t_sige = 0, t_ifx = 0, t_ify = 0, t_bx = 0, t_by = 0, t_xlo = 0, t_ylo = 0;
+  std::map<std::tuple<int, int, int>, PassPlan> passes;
+  lfds_report report{};
+  lfds_info info{};
+  int launches = 0;
+};
+
+namespace {
+
+int64_t align4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+// ------------------------------------------------------------------ device tables
+struct TabBuilder {
+  std::vector<double2> v;
+  int64_t put(const std::vector<zc>& a) {
+    int64_t off = (int64_t)v.size();
+    for (auto& z : a) v.push_back(make_double2(z.real(), z.imag()));
+    return off;
+  }
+  int64_t put_ints(const std::vector<int>& a) {
+    int64_t off = (int64_t)v.size();
+    size_t slots = (a.size() + 3) / 4;
+    v.resize(v.size() + (slots ? slots : 1), make_double2(0, 0));
+    if (!a.empty()) std::memcpy(&v[off], a.data(), a.size() * sizeof(int));
+    return off;
+  }
+};
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+GemmDesc gd(int64_t a_off, int64_t sAi, int64_t sAj, int M, int K, int b_buf, int64_t b_off, int64_t sBj, int64_t sB1,
+            int64_t sB2, int c_buf, int64_t c_off, int64_t sCi, int64_t sC1, int64_t sC2, int N1, int N2, int flags) {
+  GemmDesc d{};
+  d.a_off = a_off; d.sAi = sAi; d.sAj = sAj;
+  d.b_off = b_off; d.sBj = sBj; d.sB1 = sB1; d.sB2 = sB2;
+  d.c_off = c_off; d.sCi = sCi; d.sC1 = sC1; d.sC2 = sC2;
+  d.M = M; d.K = K; d.N1 = N1; d.N2 = N2;
+  d.b_buf = b_buf; d.c_buf = c_buf; d.flags = flags;
+  return d;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ pass plan (descriptors + workspace layout)
+static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& pp) {
+  const Axis& X = P->ax[0];
+  const Axis& Y = P->ax[1];
+  const int Nx = X.N, Ny = Y.N, Nz = P->nz;
+  const int nbx = P->nbx, nby = P->nby, nblk = nbx * nby;
+  const int nifx = (int)X.iface.size(), nify = (int)Y.iface.size();
+  // block mode-space offsets
+  std::vector<int64_t> ms(nblk), t1(nblk);
+  int64_t acc = 0;
+  int maxsys = 0;
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i) {
+      int b = j * nbx + i;
+      ms[b] = acc;
+      t1[b] = acc;
+      acc += (int64_t)X.blocks[i].n * Y.blocks[j].n * Nz * R;
+      maxsys = std::max(maxsys, X.blocks[i].n * Y.blocks[j].n * R);
+    }
+  const int64_t ms_elems = acc;
+  const int64_t t1_elems = std::max(acc, (int64_t)Nx * Ny * Nz * R);
+  // interface buffer layout (complex elements)
+  int64_t o = 0;
+  pp.g_off = o; o += align4((int64_t)nblk * R * 2 * P->mpad * Nz);
+  pp.h_off = o; o += align4((int64_t)nblk * R * 2 * P->lpad * Nz);
+  pp.vx_off = o; o += align4((int64_t)nblk * R * 2 * Nz * P->mpad);
+  pp.vy_off = o; o += align4((int64_t)nblk * R * 2 * Nz * P->lpad);
+  pp.rx = o; o += align4((int64_t)nifx * R * Nz * Ny);
+  pp.ry = o; o += align4((int64_t)nify * R * Nz * Nx);
+  pp.r1 = o; o += align4((int64_t)nifx * R * Ny * Nz);
+  pp.r2 = o; o += align4((int64_t)nify * R * Nx * Nz);
+  pp.p1 = o; o += align4((int64_t)nifx * R * Ny * Nz);
+  pp.p2 = o; o += align4((int64_t)nify * R * Nx * Nz);
+  pp.wx = o; o += align4((int64_t)nifx * R * Nz * Ny);
+  pp.wy = o; o += align4((int64_t)nify * R * Nz * Nx);
+  pp.gf = o; o += align4((int64_t)nblk * 4 * R * P->fpad * Nz);
+  const int64_t if_elems = o;
+  size_t off = 0;
+  pp.off_ms = off; off = al256(off + ms_elems * 16);
+  pp.off_t1 = off; off = al256(off + t1_elems * 16);
+  pp.off_if = off; off = al256(off + if_elems * 16);
+  pp.off_red = off; off = al256(off + (size_t)(2 * R + 8) * 8);
+  pp.off_res = off;
+  if (P->opt.refine != 0) off = al256(off + (size_t)Nx * Ny * Nz * R * 16);
+  pp.total = off;
+  pp.max_systems = maxsys;
+
+  std::vector<GemmDesc> D;
+  auto stage = [&](StageDescs& s, std::vector<GemmDesc>&& v) {
+    s.off = (int64_t)D.size();
+    s.n = (int)v.size();
+    s.maxM = 0;
+    s.maxN = 0;
+    for (auto& d : v) {
+      s.maxM = std::max(s.maxM, d.M);
+      s.maxN = std::max(s.maxN, (int64_t)d.N1 * d.N2);
+      D.push_back(d);
+    }
+  };
+  const int inF = in_real ? G_BREAL : 0, outF = out_real ? G_CREAL : 0;
+  std::vector<GemmDesc> v;
+  // step 1: x-forward per block, then y-forward per (block, r) into [r][m][l][k]
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+      int b = j * nbx + i;
+      v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_F, (int64_t)(by.lo - 1) * Nx + (bx.lo - 1), 1, (int64_t)Nx * Ny, Nx,
+                     B_T1, t1[b], 1, (int64_t)by.n * bx.n, bx.n, R * Nz, by.n, inF));
+    }
+  stage(pp.s1x, std::move(v)); v.clear();
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i)
+      for (int r = 0; r < R; ++r) {
+        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+        int b = j * nbx + i;
+        int64_t vol = (int64_t)bx.n * by.n * Nz;
+        v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_T1, t1[b] + r * vol, bx.n, (int64_t)bx.n * by.n, 1, B_MS,
+                       ms[b] + r * vol, (int64_t)bx.n * Nz, 1, Nz, Nz, bx.n, 0));
+      }
+  stage(pp.s1y, std::move(v)); v.clear();
+  // step 3: G[b][r][e][m][k] = sum_l Wx[e_row, l] v~[r][m][l][k];  H[b][r][e][l][k] = sum_m Wy[e_row, m] v~
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i)
+      for (int r = 0; r < R; ++r) {
+        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+        int b = j * nbx + i;
+        int64_t vol = (int64_t)bx.n * by.n * Nz;
+        v.push_back(gd(bx.W, (int64_t)(bx.n - 1) * bx.n, 1, 2, bx.n, B_MS, ms[b] + r * vol, Nz, (int64_t)bx.n * Nz, 1,
+                       B_IF, pp.g_off + ((int64_t)b * R + r) * 2 * P->mpad * Nz, (int64_t)P->mpad * Nz, Nz, 1, by.n,
+                       Nz, 0));
+      }
+  stage(pp.s3g, std::move(v)); v.clear();
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i)
+      for (int r = 0; r < R; ++r) {
+        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+        int b = j * nbx + i;
+        int64_t vol = (int64_t)bx.n * by.n * Nz;
+        v.push_back(gd(by.W, (int64_t)(by.n - 1) * by.n, 1, 2, by.n, B_MS, ms[b] + r * vol, (int64_t)bx.n * Nz, Nz, 1,
+                       B_IF, pp.h_off + ((int64_t)b * R + r) * 2 * P->lpad * Nz, (int64_t)P->lpad * Nz, Nz, 1, bx.n,
+                       Nz, 0));
+      }
+  stage(pp.s3h, std::move(v)); v.clear();
+  // VX[b][r][e][k][q] = sum_m Wy[q,m] G[..][e][m][k];  VY[b][r][e][k][p] = sum_l Wx[p,l] H[..][e][l][k]
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i)
+      for (int r = 0; r < R; ++r) {
+        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+        int b = j * nbx + i;
+        v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_IF, pp.g_off + ((int64_t)b * R + r) * 2 * P->mpad * Nz, Nz,
+                       (int64_t)P->mpad * Nz, 1, B_IF, pp.vx_off + ((int64_t)b * R + r) * 2 * Nz * P->mpad, 1,
+                       (int64_t)Nz * P->mpad, P->mpad, 2, Nz, 0));
+      }
+  stage(pp.s3x, std::move(v)); v.clear();
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i)
+      for (int r = 0; r < R; ++r) {
+        const AxisBlock &bx = X.blocks[i];
+        int b = j * nbx + i;
+        v.push_back(gd(bx.W, bx.n, 1, bx.n, bx.n, B_IF, pp.h_off + ((int64_t)b * R + r) * 2 * P->lpad * Nz, Nz,
+                       (int64_t)P->lpad * Nz, 1, B_IF, pp.vy_off + ((int64_t)b * R + r) * 2 * Nz * P->lpad, 1,
+                       (int64_t)Nz * P->lpad, P->lpad, 2, Nz, 0));
+      }
+  stage(pp.s3y, std::move(v)); v.clear();
+  // step 5: R1 = W_y^T RX, R2 = W_x^T RY  (b-units: no mass)
+  if (nifx) v.push_back(gd(Y.Wg, 1, Ny, Ny, Ny, B_IF, pp.rx, 1, (int64_t)Nz * Ny, Ny, B_IF, pp.r1, Nz, (int64_t)Ny * Nz, 1,
+                           nifx * R, Nz, 0));
+  stage(pp.s5r1, std::move(v)); v.clear();
+  if (nify) v.push_back(gd(X.Wg, 1, Nx, Nx, Nx, B_IF, pp.ry, 1, (int64_t)Nz * Nx, Nx, B_IF, pp.r2, Nz, (int64_t)Nx * Nz, 1,
+                           nify * R, Nz, 0));
+  stage(pp.s5r2, std::move(v)); v.clear();
+  // P1[a][r][m][k] = sum_l Wx[I_a, l] W^[r][m][l][k];  P2[b][r][l][k] = sum_m Wy[I_b, m] W^[r][m][l][k]
+  if (nifx) v.push_back(gd(X.WI, Nx, 1, nifx, Nx, B_T1, 0, Nz, (int64_t)Nx * Nz, 1, B_IF, pp.p1, (int64_t)R * Ny * Nz, Nz, 1,
+                           R * Ny, Nz, 0));
+  stage(pp.s5p1, std::move(v)); v.clear();
+  if (nify) v.push_back(gd(Y.WI, Ny, 1, nify, Ny, B_T1, 0, (int64_t)Nx * Nz, (int64_t)Ny * Nx * Nz, 1, B_IF, pp.p2,
+                           (int64_t)R * Nx * Nz, (int64_t)Nx * Nz, 1, R, Nx * Nz, 0));
+  stage(pp.s5p2, std::move(v)); v.clear();
+  // w on the planes: WX[a][r][k][q] = sum_m Wy[q,m] P1[a][r][m][k];  WY[b][r][k][p] = sum_l Wx[p,l] P2[b][r][l][k]
+  if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, Nz, (int64_t)Ny * Nz, 1, B_IF, pp.wx, 1, (int64_t)Nz * Ny, Ny,
+                           nifx * R, Nz, 0));
+  stage(pp.s5wx, std::move(v)); v.clear();
+  if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, Nz, (int64_t)Nx * Nz, 1, B_IF, pp.wy, 1, (int64_t)Nz * Nx, Nx,
+                           nify * R, Nz, 0));
+  stage(pp.s5wy, std::move(v)); v.clear();
+  // step 6: face transforms GF[b][face][r][mode][k] (faces L, R, B, T)
+  std::vector<ZBlock> zb(nblk);
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+      int b = j * nbx + i;
+      ZBlock& z = zb[b];
+      z.ms_off = ms[b];
+      z.nx = bx.n;
+      z.ny = by.n;
+      z.lamx = bx.lam;
+      z.lamy = by.lam;
+      z.wx0 = bx.W;                                  // row p = 0:   W[0*n + l]
+      z.wx1 = bx.W + (int64_t)(bx.n - 1) * bx.n;     // row p = n-1
+      z.wy0 = by.W;
+      z.wy1 = by.W + (int64_t)(by.n - 1) * by.n;
+      z.gL = z.gR = z.gB = z.gT = -1;
+      z.cL = z.cR = z.cB = z.cT = make_double2(0, 0);
+      auto face_off = [&](int face) { return pp.gf + ((int64_t)b * 4 + face) * R * P->fpad * Nz; };
+      const int x1 = bx.lo + bx.n - 1, y1 = by.lo + by.n - 1;
+      if (i > 0) {  // left face: x-interface a = i-1 at node bx.lo-1
+        int a = i - 1;
+        v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_IF, pp.wx + (int64_t)a * R * Nz * Ny + (by.lo - 1), 1, (int64_t)Nz * Ny,
+                       Ny, B_IF, face_off(0), Nz, (int64_t)by.n * Nz, 1, R, Nz, 0));
+        z.gL = face_off(0);
+        zc c = 1.0 / X.h[bx.lo - 1];
+        z.cL = make_double2(c.real(), c.imag());
+      }
+      if (i < nbx - 1) {  // right face: interface a = i at node x1+1
+        int a = i;
+        v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_IF, pp.wx + (int64_t)a * R * Nz * Ny + (by.lo - 1), 1, (int64_t)Nz * Ny,
+                       Ny, B_IF, face_off(1), Nz, (int64_t)by.n * Nz, 1, R, Nz, 0));
+        z.gR = face_off(1);
+        zc c = 1.0 / X.h[x1];
+        z.cR = make_double2(c.real(), c.imag());
+      }
+      if (j > 0) {
+        int bb = j - 1;
+        v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_IF, pp.wy + (int64_t)bb * R * Nz * Nx + (bx.lo - 1), 1,
+                       (int64_t)Nz * Nx, Nx, B_IF, face_off(2), Nz, (int64_t)bx.n * Nz, 1, R, Nz, 0));
+        z.gB = face_off(2);
+        zc c = 1.0 / Y.h[by.lo - 1];
+        z.cB = make_double2(c.real(), c.imag());
+      }
+      if (j < nby - 1) {
+        int bb = j;
+        v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_IF, pp.wy + (int64_t)bb * R * Nz * Nx + (bx.lo - 1), 1,
+                       (int64_t)Nz * Nx, Nx, B_IF, face_off(3), Nz, (int64_t)bx.n * Nz, 1, R, Nz, 0));
+        z.gT = face_off(3);
+        zc c = 1.0 / Y.h[y1];
+        z.cT = make_double2(c.real(), c.imag());
+      }
+    }
+  stage(pp.s6f, std::move(v)); v.clear();
+  // step 7: y-inverse [r][m][l][k] -> [r][k][q][l], x-inverse -> u
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i)
+      for (int r = 0; r < R; ++r) {
+        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+        int b = j * nbx + i;
+        int64_t vol = (int64_t)bx.n * by.n * Nz;
+        v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_MS, ms[b] + r * vol, (int64_t)bx.n * Nz, Nz, 1, B_T1, t1[b] + r * vol,
+                       bx.n, 1, (int64_t)bx.n * by.n, bx.n, Nz, 0));
+      }
+  stage(pp.s7y, std::move(v)); v.clear();
+  for (int j = 0; j < nby; ++j)
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+      int b = j * nbx + i;
+      v.push_back(gd(bx.W, bx.n, 1, bx.n, bx.n, B_T1, t1[b], 1, (int64_t)by.n * bx.n, bx.n, B_U,
+                     (int64_t)(by.lo - 1) * Nx + (bx.lo - 1), 1, (int64_t)Nx * Ny, Nx, R * Nz, by.n, outF));
+    }
+  stage(pp.s7x, std::move(v)); v.clear();
+
+  CUDA_TRY(cudaMalloc(&pp.d_descs, sizeof(GemmDesc) * std::max<size_t>(1, D.size())));
+  CUDA_TRY(cudaMemcpy(pp.d_descs, D.data(), sizeof(GemmDesc) * D.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&pp.d_zb, sizeof(ZBlock) * nblk));
+  CUDA_TRY(cudaMemcpy(pp.d_zb, zb.data(), sizeof(ZBlock) * nblk, cudaMemcpyHostToDevice));
+  return LFDS_OK;
+}
+
+static int get_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan** out) {
+  auto key = std::make_tuple(R, in_real, out_real);
+  auto it = P->passes.find(key);
+  if (it == P->passes.end()) {
+    PassPlan pp;
+    int rc = build_pass(P, R, in_real, out_real, pp);
+    if (rc) return rc;
+    it = P->passes.emplace(key, pp).first;
+  }
+  *out = &it->second;
+  return LFDS_OK;
+}
+
+// ------------------------------------------------------------------ one pipeline pass (steps 1-7)
+static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, int out_dtype, cudaStream_t st) {
+  const Axis& X = P->ax[0];
+  const Axis& Y = P->ax[1];
+  const int Nx = X.N, Ny = Y.N, Nz = P->nz;
+  const int nifx = (int)X.iface.size(), nify = (int)Y.iface.size();
+  const int nblk = P->nbx * P->nby;
+  double* minpiv = reinterpret_cast<double*>(bufs.p[B_RED]);
+  auto gemm = [&](const StageDescs& s) -> int {
+    if (!s.n) return LFDS_OK;
+    CUDA_TRY(launch_gemm(pp.d_descs + s.off, s.n, s.maxM, (int)std::min<int64_t>(s.maxN, INT32_MAX), 0, bufs, st));
+    P->launches += (s.n + 65534) / 65535;
+    return LFDS_OK;
+  };
+  int rc;
+  // pass 1
+  if ((rc = gemm(pp.s1x))) return rc;
+  if ((rc = gemm(pp.s1y))) return rc;
+  CUDA_TRY(launch_zsolve_block(1, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st));
+  P->launches++;
+  if (nifx + nify > 0) {
+    if ((rc = gemm(pp.s3g))) return rc;
+    if ((rc = gemm(pp.s3h))) return rc;
+    if ((rc = gemm(pp.s3x))) return rc;
+    if ((rc = gemm(pp.s3y))) return rc;
+    // step 4
+    IfaceRes ir{};
+    ir.nx = Nx; ir.ny = Ny; ir.nz = Nz; ir.R = R; ir.nifx = nifx; ir.nify = nify; ir.dtype = in_dtype;
+    ir.ifx = P->t_ifx; ir.ify = P->t_ify;
+    ir.hx = X.hoff; ir.hy = Y.hoff; ir.hhx = X.hhoff; ir.hhy = Y.hhoff; ir.hhz = P->t_hhz; ir.sig = P->t_sig;
+    ir.rx = pp.rx; ir.ry = pp.ry; ir.vxo = pp.vx_off; ir.vyo = pp.vy_off;
+    ir.blk_of_x = P->t_bx; ir.blk_of_y = P->t_by; ir.xlo = P->t_xlo; ir.ylo = P->t_ylo;
+    ir.nbx = P->nbx; ir.nby = P->nby; ir.qpad = P->mpad; ir.ppad = P->lpad;
+    CUDA_TRY(launch_iface_residual(ir, bufs, st));
+    P->launches++;
+    // step 5
+    if ((rc = gemm(pp.s5r1))) return rc;
+    if ((rc = gemm(pp.s5r2))) return rc;
+    GSweep g{};
+    g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
+    g.lamx = X.lamg; g.lamy = Y.lamg; g.wxi = X.WI; g.wyi = Y.WI; g.r1 = pp.r1; g.r2 = pp.r2; g.what = 0;
+    CUDA_TRY(launch_gsweep(g, P->zt_plain, bufs, minpiv, st));
+    P->launches++;
+    if ((rc = gemm(pp.s5p1))) return rc;
+    if ((rc = gemm(pp.s5p2))) return rc;
+    if ((rc = gemm(pp.s5wx))) return rc;
+    if ((rc = gemm(pp.s5wy))) return rc;
+    // step 6
+    if ((rc = gemm(pp.s6f))) return rc;
+    CUDA_TRY(launch_zsolve_block(2, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st));
+    P->launches++;
+  }
+  // step 7
+  if ((rc = gemm(pp.s7y))) return rc;
+  if ((rc = gemm(pp.s7x))) return rc;
+  if (nifx + nify > 0) {
+    CUDA_TRY(launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st));
+    P->launches++;
+  }
+  return LFDS_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+void lfds_default_options(lfds_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->dtype = LFDS_C128;
+  o->refine = 0;
+  o->refine_tol = 1e-13;
+  o->residual_dd = 1;
+  o->device = 0;
+  o->rhs_chunk = 0;
+}
+
+const char* lfds_last_error(void) { return g_err.c_str(); }
+const char* lfds_version(void) { return "lfds 0.1 (sm_100a)"; }
+
+static int setup_axis(Axis& A, int N, const lfds_z* h, int nif, const int* iface, bool need_global, const char* name) {
+  A.N = N;
+  A.h.resize(N + 1);
+  for (int t = 0; t <= N; ++t) {
+    A.h[t] = zc(h[t].re, h[t].im);
+    if (!(A.h[t].real() > 0)) return fail(LFDS_EINVAL, "%s: step h_%d has Re(h) <= 0", name, t);
+  }
+  A.hh.resize(N);
+  for (int i = 0; i < N; ++i) A.hh[i] = 0.5 * (A.h[i] + A.h[i + 1]);
+  A.iface.assign(iface, iface + nif);
+  for (int a = 0; a < nif; ++a) {
+    int v = A.iface[a];
+    if (v < 2 || v > N - 1) return fail(LFDS_EINVAL, "%s: interface node %d outside 2..N-1", name, v);
+    if (a > 0 && v < A.iface[a - 1] + 2) return fail(LFDS_EINVAL, "%s: interfaces must be sorted and >= 2 apart", name);
+  }
+  A.blk_of.assign(N, -1);
+  std::vector<int> cuts;
+  cuts.push_back(0);
+  for (int v : A.iface) cuts.push_back(v);
+  cuts.push_back(N + 1);
+  for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+    AxisBlock b;
+    b.lo = cuts[c] + 1;
+    b.n = cuts[c + 1] - 1 - cuts[c];
+    for (int p = 0; p < b.n; ++p) A.blk_of[b.lo - 1 + p] = (int)A.blocks.size();
+    A.blocks.push_back(b);
+  }
+  std::string err;
+  for (auto& b : A.blocks) {
+    std::vector<zc> hs(A.h.begin() + (b.lo - 1), A.h.begin() + (b.lo + b.n));
+    if (!pencil_basis(hs, b.B, err)) return fail(LFDS_EEIG, "%s block at node %d: %s", name, b.lo, err.c_str());
+  }
+  if (need_global) {
+    if (!pencil_basis(A.h, A.G, err)) return fail(LFDS_EEIG, "%s global basis: %s", name, err.c_str());
+  }
+  return LFDS_OK;
+}
+
+int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, const lfds_z* hz,
+                    const lfds_z* sigma_node, const lfds_z* sigma_edge, lfds_z lambda, int n_if_x, const int* if_x,
+                    int n_if_y, const int* if_y, const lfds_options* opt, lfds_plan** out) {
+  auto t0 = std::chrono::steady_clock::now();
+  if (!out) return fail(LFDS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (nx < 1 || ny < 1 || nz < 1) return fail(LFDS_EINVAL, "sizes must be >= 1 (nx=%d ny=%d nz=%d)", nx, ny, nz);
+  if (nz > 512) return fail(LFDS_EINVAL, "nz=%d > 512 is not supported by the warp z-solver", nz);
+  if (!hx || !hy || !hz || !sigma_node || !sigma_edge) return fail(LFDS_EINVAL, "NULL input array");
+  if ((n_if_x && !if_x) || (n_if_y && !if_y) || n_if_x < 0 || n_if_y < 0) return fail(LFDS_EINVAL, "bad interface arrays");
+  std::unique_ptr<lfds_plan> P(new lfds_plan());
+  if (opt) P->opt = *opt;
+  else lfds_default_options(&P->opt);
+  if (P->opt.refine < -1 || P->opt.refine > 8) return fail(LFDS_EINVAL, "refine must be -1..8");
+  int rc;
+  const bool need_global = n_if_x + n_if_y > 0;
+  if ((rc = setup_axis(P->ax[0], nx, hx, n_if_x, if_x, need_global, "x"))) return rc;
+  if ((rc = setup_axis(P->ax[1], ny, hy, n_if_y, if_y, need_global, "y"))) return rc;
+  P->nz = nz;
+  P->hz.resize(nz + 1);
+  P->sig_edge.resize(nz + 1);
+  P->sig_node.resize(nz);
+  for (int k = 0; k <= nz; ++k) {
+    P->hz[k] = zc(hz[k].re, hz[k].im);
+    P->sig_edge[k] = zc(sigma_edge[k].re, sigma_edge[k].im);
+    if (!(P->hz[k].real() > 0)) return fail(LFDS_EINVAL, "z: step h_%d has Re(h) <= 0", k);
+    if (!(P->sig_edge[k].real() > 0)) return fail(LFDS_EINVAL, "sigma_edge[%d] has Re <= 0", k);
+  }
+  for (int k = 0; k < nz; ++k) {
+    P->sig_node[k] = zc(sigma_node[k].re, sigma_node[k].im);
+    if (!(P->sig_node[k].real() > 0)) return fail(LFDS_EINVAL, "sigma_node[%d] has Re <= 0", k);
+  }
+  P->lam = zc(lambda.re, lambda.im);
+  P->hhz.resize(nz);
+  for (int k = 0; k < nz; ++k) P->hhz[k] = 0.5 * (P->hz[k] + P->hz[k + 1]);
+  if (P->opt.dtype == LFDS_F64) {
+    bool ok = P->lam.imag() == 0;
+    for (auto& a : P->ax)
+      for (auto& z : a.h) ok = ok && z.imag() == 0;
+    for (auto& z : P->hz) ok = ok && z.imag() == 0;
+    for (auto& z : P->sig_edge) ok = ok && z.imag() == 0;
+    for (auto& z : P->sig_node) ok = ok && z.imag() == 0;
+    if (!ok) return fail(LFDS_EINVAL, "LFDS_F64 requires real steps, sigma and lambda");
+  }
+  Axis& X = P->ax[0];
+  Axis& Y = P->ax[1];
+  P->nbx = (int)X.blocks.size();
+  P->nby = (int)Y.blocks.size();
+  P->mpad = 0;
+  P->lpad = 0;
+  for (auto& b : Y.blocks) P->mpad = std::max(P->mpad, b.n);
+  for (auto& b : X.blocks) P->lpad = std::max(P->lpad, b.n);
+  P->fpad = std::max(P->mpad, P->lpad);
+  // eigen diagnostics
+  double mres = 0, mbio = 0;
+  for (auto& a : P->ax) {
+    for (auto& b : a.blocks) { mres = std::max(mres, b.B.residual); mbio = std::max(mbio, b.B.biorth); }
+    if (a.G.n) { mres = std::max(mres, a.G.residual); mbio = std::max(mbio, a.G.biorth); }
+  }
+  if (!(mres < 1e-8) || !(mbio < 1e-3))
+    return fail(LFDS_EEIG, "eigenbasis check failed: residual %.3e, biorthonormality %.3e", mres, mbio);
+  // ---- device tables
+  TabBuilder T;
+  for (auto& a : P->ax) {
+    for (auto& b : a.blocks) {
+      const int n = b.n;
+      std::vector<zc> F((size_t)n * n);
+      for (int l = 0; l < n; ++l)
+        for (int p = 0; p < n; ++p) F[(size_t)l * n + p] = b.B.W[(size_t)p * n + l] * a.hh[b.lo - 1 + p];
+      b.F = T.put(F);
+      b.W = T.put(b.B.W);
+      b.lam = T.put(b.B.lam);
+    }
+    if (a.G.n) {
+      a.Wg = T.put(a.G.W);
+      a.lamg = T.put(a.G.lam);
+      std::vector<zc> WI((size_t)a.iface.size() * a.N);
+      for (size_t q = 0; q < a.iface.size(); ++q)
+        for (int l = 0; l < a.N; ++l) WI[q * a.N + l] = a.G.W[(size_t)(a.iface[q] - 1) * a.N + l];
+      a.WI = T.put(WI);
+    }
+    a.hoff = T.put(a.h);
+    a.hhoff = T.put(a.hh);
+  }
+  // z tables: T(s) row k = a_k x_{k-1} + (g_k + s e_k) x_k + c_k x_{k+1}
+  std::vector<zc> za(nz), zg(nz), zcv(nz), ze(nz), sa(nz), sg(nz), scv(nz), se(nz);
+  for (int k = 0; k < nz; ++k) {
+    zc lo = P->sig_edge[k] / P->hz[k], hi = P->sig_edge[k + 1] / P->hz[k + 1];
+    za[k] = k > 0 ? lo : zc(0);
+    zcv[k] = k + 1 < nz ? hi : zc(0);
+    zg[k] = -(lo + hi) + P->lam * P->hhz[k];
+    ze[k] = P->sig_node[k] * P->hhz[k];
+    sa[k] = za[k] / P->hhz[k];
+    scv[k] = zcv[k] / P->hhz[k];
+    sg[k] = zg[k] / P->hhz[k];
+    se[k] = P->sig_node[k];
+    for (auto* z : {&za[k], &zg[k], &zcv[k], &ze[k]})
+      if (z->imag() != 0) P->real_z = false;
+  }
+  P->zt_plain = ZTab{T.put(za), T.put(zg), T.put(zcv), T.put(ze)};
+  P->zt_scaled = ZTab{T.put(sa), T.put(sg), T.put(scv), T.put(se)};
+  P->t_hz = T.put(P->hz);
+  P->t_hhz = T.put(P->hhz);
+  P->t_sig = T.put(P->sig_node);
+  P->t_sige = T.put(P->sig_edge);
+  P->t_ifx = T.put_ints(X.iface);
+  P->t_ify = T.put_ints(Y.iface);
+  P->t_bx = T.put_ints(X.blk_of);
+  P->t_by = T.put_ints(Y.blk_of);
+  std::vector<int> xlo, ylo;
+  for (auto& b : X.blocks) xlo.push_back(b.lo);
+  for (auto& b : Y.blocks) ylo.push_back(b.lo);
+  P->t_xlo = T.put_ints(xlo);
+  P->t_ylo = T.put_ints(ylo);
+  P->tab_elems = T.v.size();
+  if (P->opt.device >= 0) {
+    CUDA_TRY(cudaSetDevice(P->opt.device));
+    CUDA_TRY(cudaMalloc(&P->d_tab, T.v.size() * sizeof(double2)));
+    CUDA_TRY(cudaMemcpy(P->d_tab, T.v.data(), T.v.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  lfds_info& I = P->info;
+  I.nx = nx; I.ny = ny; I.nz = nz; I.nbx = P->nbx; I.nby = P->nby; I.n_if_x = n_if_x; I.n_if_y = n_if_y;
+  I.real_z = P->real_z ? 1 : 0;
+  I.setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+  I.eig_max_residual = mres;
+  I.eig_max_biorth = mbio;
+  I.device_table_bytes = T.v.size() * sizeof(double2);
+  *out = P.release();
+  return LFDS_OK;
+}
+
+static int chunk_of(const lfds_plan* P, int nrhs) {
+  int c = P->opt.rhs_chunk > 0 ? P->opt.rhs_chunk : nrhs;
+  return std::max(1, std::min(c, nrhs));
+}
+
+size_t lfds_workspace_bytes(const lfds_plan* cp, int nrhs) {
+  lfds_plan* P = const_cast<lfds_plan*>(cp);
+  if (!P || nrhs < 1 || !P->d_tab) return 0;
+  int R = chunk_of(P, nrhs);
+  int in_real = P->opt.dtype == LFDS_F64;
+  PassPlan* pp;
+  if (get_pass(P, R, in_real, in_real, &pp)) return 0;
+  return pp->total;
+}
+
+size_t lfds_workspace_bytes_host(const lfds_plan* P, int nrhs) {
+  size_t ws = lfds_workspace_bytes(P, nrhs);
+  if (!ws) return 0;
+  size_t el = P->opt.dtype == LFDS_F64 ? 8 : 16;
+  size_t vol = (size_t)P->ax[0].N * P->ax[1].N * P->nz * nrhs * el;
+  return ws + 2 * al256(vol);
+}
+
+static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int R = chunk_of(P, nrhs);
+  const int dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
+  const size_t el = dt ? 8 : 16;
+  const int64_t vol = (int64_t)P->ax[0].N * P->ax[1].N * P->nz;
+  P->launches = 0;
+  P->report = lfds_report{};
+  P->report.min_pivot_ratio = 1.0;
+  double maxres[9] = {0};
+  int passes_done = 0;
+  for (int r0 = 0; r0 < nrhs; r0 += R) {
+    const int Rc = std::min(R, nrhs - r0);
+    PassPlan *pp_main, *pp_ref = nullptr;
+    int rc;
+    if ((rc = get_pass(P, Rc, dt, dt, &pp_main))) return rc;
+    if (P->opt.refine != 0 && (rc = get_pass(P, Rc, 0, 0, &pp_ref))) return rc;
+    if (ws_bytes < pp_main->total) return fail(LFDS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, pp_main->total);
+    char* w = reinterpret_cast<char*>(ws);
+    Bufs b{};
+    b.p[B_TAB] = P->d_tab;
+    b.p[B_F] = const_cast<char*>(reinterpret_cast<const char*>(f_dev)) + (size_t)r0 * vol * el;
+    b.p[B_U] = reinterpret_cast<char*>(u_dev) + (size_t)r0 * vol * el;
+    b.p[B_MS] = w + pp_main->off_ms;
+    b.p[B_T1] = w + pp_main->off_t1;
+    b.p[B_IF] = w + pp_main->off_if;
+    b.p[B_RED] = w + pp_main->off_red;
+    double* red = reinterpret_cast<double*>(b.p[B_RED]);
+    CUDA_TRY(launch_fill_minpiv(red, st));
+    if ((rc = run_pass(P, *pp_main, b, Rc, dt, dt, st))) return rc;
+    int passes = 1;
+    if (P->opt.refine != 0) {
+      double2* res = reinterpret_cast<double2*>(w + pp_main->off_res);
+      double* norms = red + 8;
+      const Axis& X = P->ax[0];
+      const Axis& Y = P->ax[1];
+      double prev = 1e300;
+      const int maxref = P->opt.refine < 0 ? 8 : P->opt.refine;
+      for (int it = 0; it <= maxref; ++it) {
+        CUDA_TRY(cudaMemsetAsync(norms, 0, sizeof(double) * 2 * Rc, st));
+        CUDA_TRY(launch_residual(X.N, Y.N, P->nz, Rc, dt, P->opt.residual_dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff,
+                                 Y.hhoff, P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()),
+                                 b.p[B_U], b.p[B_F], res, 1, norms, b, st));
+        P->launches++;
+        std::vector<double> hn(2 * Rc);
+        CUDA_TRY(cudaMemcpyAsync(hn.data(), norms, sizeof(double) * 2 * Rc, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        double worst = 0;
+        for (int r = 0; r < Rc; ++r) worst = std::max(worst, hn[2 * r + 1] > 0 ? std::sqrt(hn[2 * r] / hn[2 * r + 1]) : 0.0);
+        if (it < 9) maxres[it] = std::max(maxres[it], worst);
+        if (it == maxref) break;
+        if (P->opt.refine < 0 && (worst <= P->opt.refine_tol || worst > 0.5 * prev)) break;
+        prev = worst;
+        Bufs rb = b;
+        rb.p[B_F] = res;
+        rb.p[B_U] = res;
+        if ((rc = run_pass(P, *pp_ref, rb, Rc, 0, 0, st))) return rc;
+        CUDA_TRY(launch_axpy_u(vol * Rc, dt, res, b.p[B_U], st));
+        P->launches++;
+        passes++;
+      }
+    }
+    passes_done = std::max(passes_done, passes);
+    if (P->opt.refine != 0) {  // the stream is already synchronised by the refinement loop
+      double mp = 1.0;
+      CUDA_TRY(cudaMemcpyAsync(&mp, red, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      P->report.min_pivot_ratio = std::min(P->report.min_pivot_ratio, mp);
+    } else {
+      P->report.min_pivot_ratio = -1.0;  // not read back (would synchronise the stream)
+    }
+  }
+  P->report.passes = passes_done;
+  for (int i = 0; i < 9; ++i) P->report.rel_residual[i] = maxres[i];
+  P->report.n_kernel_launches = P->launches;
+  return LFDS_OK;
+}
+
+int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes, void* stream) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  if (nrhs < 1 || !f_dev || !u_dev || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
+  if (((uintptr_t)f_dev | (uintptr_t)u_dev | (uintptr_t)ws) & 15) return fail(LFDS_EINVAL, "pointers must be 16-byte aligned");
+  return solve_impl(P, f_dev, u_dev, nrhs, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lfds_solve_host(lfds_plan* P, const void* f_host, void* u_host, int nrhs, void* ws, size_t ws_bytes, void* stream) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  if (nrhs < 1 || !f_host || !u_host || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
+  size_t need = lfds_workspace_bytes_host(P, nrhs);
+  if (ws_bytes < need) return fail(LFDS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
+  size_t el = P->opt.dtype == LFDS_F64 ? 8 : 16;
+  size_t vol = (size_t)P->ax[0].N * P->ax[1].N * P->nz * nrhs * el;
+  size_t base = lfds_workspace_bytes(P, nrhs);
+  char* w = reinterpret_cast<char*>(ws);
+  void* fd = w + base;
+  void* ud = w + base + al256(vol);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaMemcpyAsync(fd, f_host, vol, cudaMemcpyHostToDevice, st));
+  int rc = solve_impl(P, fd, ud, nrhs, ws, base, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(u_host, ud, vol, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return LFDS_OK;
+}
+
+int lfds_residual(lfds_plan* P, const void* u_dev, const void* f_dev, lfds_z* r_dev, int nrhs, int dd, double* norms,
+                  void* stream) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  if (!u_dev || nrhs < 1) return fail(LFDS_EINVAL, "bad residual arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
+  double* d_norms = nullptr;
+  if (norms) CUDA_TRY(cudaMallocAsync(&d_norms, sizeof(double) * 2 * nrhs, st));
+  if (d_norms) CUDA_TRY(cudaMemsetAsync(d_norms, 0, sizeof(double) * 2 * nrhs, st));
+  Bufs b{};
+  b.p[B_TAB] = P->d_tab;
+  const Axis& X = P->ax[0];
+  const Axis& Y = P->ax[1];
+  CUDA_TRY(launch_residual(X.N, Y.N, P->nz, nrhs, dt, dd, f_dev != nullptr, X.hoff, Y.hoff, P->t_hz, X.hhoff, Y.hhoff,
+                           P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()), u_dev, f_dev,
+                           reinterpret_cast<double2*>(r_dev), 0, d_norms, b, st));
+  if (norms) {
+    CUDA_TRY(cudaMemcpyAsync(norms, d_norms, sizeof(double) * 2 * nrhs, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int r = 0; r < nrhs; ++r) { norms[2 * r] = std::sqrt(norms[2 * r]); norms[2 * r + 1] = std::sqrt(norms[2 * r + 1]); }
+    CUDA_TRY(cudaFree(d_norms));
+  }
+  return LFDS_OK;
+}
+
+int lfds_get_report(const lfds_plan* P, lfds_report* rep) {
+  if (!P || !rep) return fail(LFDS_EINVAL, "NULL argument");
+  *rep = P->report;
+  return LFDS_OK;
+}
+
+int lfds_get_info(const lfds_plan* P, lfds_info* info) {
+  if (!P || !info) return fail(LFDS_EINVAL, "NULL argument");
+  *info = P->info;
+  return LFDS_OK;
+}
+
+int lfds_get_basis(const lfds_plan* P, int axis, int block, int* n, int* kind, int* lo, lfds_z* lam, lfds_z* W) {
+  if (!P || axis < 0 || axis > 1) return fail(LFDS_EINVAL, "bad axis");
+  const Axis& A = P->ax[axis];
+  const Basis* B;
+  int l0 = 1;
+  if (block < 0) {
+    if (A.iface.empty()) {
+      if (A.blocks.size() != 1) return fail(LFDS_EINVAL, "no global basis");
+      B = &A.blocks[0].B;  // single block == global
+    } else {
+      B = &A.G;
+    }
+  } else {
+    if (block >= (int)A.blocks.size()) return fail(LFDS_EINVAL, "block index out of range");
+    B = &A.blocks[block].B;
+    l0 = A.blocks[block].lo;
+  }
+  if (n) *n = B->n;
+  if (kind) *kind = B->kind;
+  if (lo) *lo = l0;
+  if (lam) for (int i = 0; i < B->n; ++i) lam[i] = lfds_z{B->lam[i].real(), B->lam[i].imag()};
+  if (W) for (size_t q = 0; q < (size_t)B->n * B->n; ++q) W[q] = lfds_z{B->W[q].real(), B->W[q].imag()};
+  return LFDS_OK;
+}
+
+void lfds_destroy(lfds_plan* P) {
+  if (!P) return;
+  for (auto& kv : P->passes) {
+    cudaFree(kv.second.d_descs);
+    cudaFree(kv.second.d_zb);
+  }
+  if (P->d_tab) cudaFree(P->d_tab);
+  delete P;
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// Internal declarations shared by the host orchestration (lfds_host.cpp) and the
+// sm_100a kernels (lfds_kernels.cu).  Not part of the public ABI (include/lfds.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lfds {
+
+// Device buffers addressed by descriptors (offsets are in elements of the buffer's type:
+// complex128 everywhere except B_F / B_U of an LFDS_F64 plan, which are float64).
+enum BufId { B_TAB = 0, B_F = 1, B_U = 2, B_MS = 3, B_T1 = 4, B_IF = 5, B_RED = 6, NBUF = 8 };
+
+struct Bufs {
+  void* p[NBUF];
+};
+
+// Strided batched complex GEMM  C(i, n) (+)= sum_j A(i, j) * B(j, n),  n = (n1, n2).
+//   A(i,j) = TAB[a_off + i*sAi + j*sAj]            (always complex, in the plan tables)
+//   B(j,n) = buf[b_buf][b_off + j*sBj + n1*sB1 + n2*sB2]
+//   C(i,n) = buf[c_buf][c_off + i*sCi + n1*sC1 + n2*sC2]
+// All four transform passes of a block, the sparse global transforms
+// of step 5, the interface-adjacent evaluations of step 3 and the
+// face transforms of step 6 are instances of this one contraction.
+enum GemmFlags { G_BREAL = 1, G_CREAL = 2, G_ACCUM = 4 };
+struct GemmDesc {
+  int64_t a_off, sAi, sAj;
+  int64_t b_off, sBj, sB1, sB2;
+  int64_t c_off, sCi, sC1, sC2;
+  int M, K, N1, N2;
+  int b_buf, c_buf, flags, pad;
+};
+
+// z-tables: per row k the tridiagonal row (a_k x_{k-1} + (g_k + s e_k) x_k + c_k x_{k+1})
+// of T(s) = A_z + lambda M_z + s M_z^sigma (reading R1); 'row-scaled' tables are divided
+// by hz^_k so that the RHS of a block z-solve is the f-unit transform (no M_z factor).
+struct ZTab {
+  int64_t a, g, c, e;  // offsets in TAB (nz complex each)
+};
+
+// One block for the block-pass z-solves.
+struct ZBlock {
+  int64_t ms_off;              // offset of this block's mode space [r][m][l][k] in B_MS
+  int nx, ny;                  // interior sizes (modes)
+  int64_t lamx, lamy;          // eigenvalue offsets in TAB
+  // pass-2 lifting (reading R8): l~[l,m,k] = -sigma_k (cL Wx[0,l] GL[m,k] + cR Wx[n-1,l] GR[m,k]
+  //                                               + cB Wy[0,m] GB[l,k] + cT Wy[n-1,m] GT[l,k])
+  int64_t wx0, wx1, wy0, wy1;  // offsets in TAB of W rows (first / last interior node)
+  int64_t gL, gR, gB, gT;      // offsets in B_IF of the face transforms, [r][m or l][k]; -1 = none
+  double2 cL, cR, cB, cT;      // coupling coefficients 1/h across each face (0 at outer boundary)
+};
+
+// Step-5 global sweep parameters (Eq. (fdmtrprjfrerr)).
+struct GSweep {
+  int nx, ny, nifx, nify, nz, R;
+  int64_t lamx, lamy;          // global eigenvalues (TAB)
+  int64_t wxi, wyi;            // W_x[I_a, l] (nifx x nx), W_y[I_b, m] (nify x ny)  (TAB)
+  int64_t r1, r2;              // R1[a][r][m][k], R2[b][r][l][k]  (B_IF)
+  int64_t what;                // W^[r][m][l][k] output (B_T1)
+};
+
+// Interface residual (step 4).
+struct IfaceRes {
+  int nx, ny, nz, R, nifx, nify, dtype;
+  int64_t ifx, ify;            // int arrays (device) of 1-based interface nodes
+  int64_t hx, hy, hhx, hhy, hhz, sig;   // TAB offsets (steps, control volumes, sigma_k)
+  int64_t rx, ry;              // out: RX[a][r][k][q] (all q), RY[b][r][k][p] (0 at p in I_x) (B_IF)
+  int64_t vxo, vyo;            // in: v at interface-adjacent nodes, see lfds_host.cpp
+  int64_t blk_of_x, blk_of_y;  // int arrays: block index along the axis for each node (or -1)
+  int64_t xlo, ylo;            // int arrays: first node of each block along the axis
+  int nbx, nby;
+  int qpad, ppad;              // padded row lengths of the step-3 arrays VX / VY
+};
+
+// launchers (lfds_kernels.cu); return cudaGetLastError()
+cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, int ldB_hint,
+                        const Bufs& bufs, cudaStream_t st);
+cudaError_t launch_zsolve_block(int mode, const ZBlock* d_blocks, int nblocks, int max_systems,
+                                int R, int nz, ZTab tab, int64_t sig_off, const Bufs& bufs,
+                                double* d_minpiv, cudaStream_t st);
+cudaError_t launch_gsweep(const GSweep& g, ZTab tab, const Bufs& bufs, double* d_minpiv, cudaStream_t st);
+cudaError_t launch_iface_residual(const IfaceRes& p, const Bufs& bufs, cudaStream_t st);
+cudaError_t launch_write_iface_u(int nx, int ny, int nz, int R, int dtype, int nifx, int nify,
+                                 int64_t ifx, int64_t ify, int64_t wx, int64_t wy,
+                                 const Bufs& bufs, cudaStream_t st);
+cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, int has_f,
+                            int64_t hx, int64_t hy, int64_t hz, int64_t hhx, int64_t hhy, int64_t hhz,
+                            int64_t sig, int64_t sige, double2 lam, const void* u, const void* f,
+                            double2* r, int to_f_units, double* d_norms, const Bufs& bufs, cudaStream_t st);
+cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st);
+cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
+
+}  // namespace lfds

@@ -1,0 +1,730 @@
+// sm_100a kernels of the blocked separable Helmholtz solve (arXiv 1909.01299).
+//
+//  k_gemm          strided batched complex contraction: block forward/inverse transforms
+//                  (steps 1 and 7), interface-adjacent evaluation (step 3), sparse global
+//                  transforms (step 5), face transforms for the Dirichlet lifting (step 6).
+//  k_zsolve_block  per-mode z tridiagonal solves of a block pass (steps 2 and 6), one warp
+//                  per system: Thomas sweeps inside each lane's chunk of rows + parallel
+//                  cyclic reduction of the 2-per-lane interface system over warp shuffles.
+//  k_gsweep        step 5's global per-mode z-solves with the rank-|I| right-hand side
+//                  built on the fly from the transformed interface residual.
+//  k_iface_res     step 4: residual b - A v on the interface planes.
+//  k_write_iface   u = w on the interface planes (last sentence).
+//  k_residual      r = M f - A u (Eq. (fd)), fp64 or double-double (refinement, reading R13).
+#include "lfds_internal.h"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lfds {
+
+// ---------------------------------------------------------------- complex helpers
+struct cplx {
+  double x, y;
+};
+__device__ __forceinline__ cplx mk(double a, double b) { return cplx{a, b}; }
+__device__ __forceinline__ cplx ld(const double2* p) {
+  double2 v = __ldg(p);
+  return cplx{v.x, v.y};
+}
+__device__ __forceinline__ cplx operator+(cplx a, cplx b) { return cplx{a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cplx operator-(cplx a, cplx b) { return cplx{a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cplx operator-(cplx a) { return cplx{-a.x, -a.y}; }
+__device__ __forceinline__ cplx operator*(cplx a, cplx b) {
+  return cplx{fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
+}
+__device__ __forceinline__ cplx operator*(double s, cplx b) { return cplx{s * b.x, s * b.y}; }
+__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {  // a*b + c
+  return cplx{fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y))};
+}
+__device__ __forceinline__ cplx cinv(cplx a) {
+  double n = 1.0 / fma(a.x, a.x, a.y * a.y);
+  return cplx{a.x * n, -a.y * n};
+}
+__device__ __forceinline__ double cabs1(cplx a) { return fabs(a.x) + fabs(a.y); }
+__device__ __forceinline__ cplx shfl_up(cplx v, int d) {
+  return cplx{__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d)};
+}
+__device__ __forceinline__ cplx shfl_down(cplx v, int d) {
+  return cplx{__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d)};
+}
+
+// minimum of positive doubles through their ordered bit patterns
+__device__ __forceinline__ void atomic_min_pos(double* addr, double v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// ---------------------------------------------------------------- generic contraction
+// C(i, n) (+)= sum_j A(i, j) B(j, n); 256 threads, tile TM x TN outputs, TK-deep chunks.
+constexpr int GTM = 32, GTN = 64, GTK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm(const GemmDesc* __restrict__ descs, Bufs bufs) {
+  const GemmDesc& D = descs[blockIdx.z];
+  const int M = D.M, K = D.K, N2 = D.N2;
+  const int64_t N = (int64_t)D.N1 * N2;
+  const int i0 = blockIdx.y * GTM;
+  const int64_t n0 = (int64_t)blockIdx.x * GTN;
+  if (i0 >= M || n0 >= N) return;
+  __shared__ double2 smem[(GTK * (GTM + 1) + GTK * (GTN + 1)) > (GTM * (GTN + 1)) ? (GTK * (GTM + 1) + GTK * (GTN + 1)) : (GTM * (GTN + 1))];
+  double2* As = smem;                       // [GTK][GTM+1]
+  double2* Bs = smem + GTK * (GTM + 1);     // [GTK][GTN+1]
+  const double2* A = reinterpret_cast<const double2*>(bufs.p[B_TAB]) + D.a_off;
+  const bool breal = D.flags & G_BREAL;
+  const char* Bb = reinterpret_cast<const char*>(bufs.p[D.b_buf]);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool jfast = (D.sBj == 1);
+  cplx acc[2][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = mk(0, 0);
+
+  for (int j0 = 0; j0 < K; j0 += GTK) {
+    for (int e = tid; e < GTM * GTK; e += 256) {
+      int jj = e % GTK, ii = e / GTK;
+      int i = i0 + ii, j = j0 + jj;
+      double2 v = make_double2(0, 0);
+      if (i < M && j < K) v = __ldg(A + i * D.sAi + j * D.sAj);
+      As[jj * (GTM + 1) + ii] = v;
+    }
+    for (int e = tid; e < GTK * GTN; e += 256) {
+      int jj, nn;
+      if (jfast) { jj = e % GTK; nn = e / GTK; } else { nn = e % GTN; jj = e / GTN; }
+      int64_t n = n0 + nn;
+      int j = j0 + jj;
+      double2 v = make_double2(0, 0);
+      if (n < N && j < K) {
+        int64_t n1 = n / N2, n2 = n - n1 * N2;
+        int64_t off = D.b_off + (int64_t)j * D.sBj + n1 * D.sB1 + n2 * D.sB2;
+        if (breal) v.x = __ldg(reinterpret_cast<const double*>(Bb) + off);
+        else v = __ldg(reinterpret_cast<const double2*>(Bb) + off);
+      }
+      Bs[jj * (GTN + 1) + nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < GTK; ++jj) {
+      cplx a0, a1, b[4];
+      double2 t = As[jj * (GTM + 1) + ty]; a0 = mk(t.x, t.y);
+      t = As[jj * (GTM + 1) + ty + 16]; a1 = mk(t.x, t.y);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { t = Bs[jj * (GTN + 1) + tx + 16 * q]; b[q] = mk(t.x, t.y); }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { acc[0][q] = cfma(a0, b[q], acc[0][q]); acc[1][q] = cfma(a1, b[q], acc[1][q]); }
+    }
+    __syncthreads();
+  }
+  // stage the tile in shared memory, then store with the C-contiguous index fastest
+  double2* Cs = smem;  // [GTM][GTN+1]
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Cs[(ty + 16 * a) * (GTN + 1) + tx + 16 * q] = make_double2(acc[a][q].x, acc[a][q].y);
+  __syncthreads();
+  const bool ifast = (D.sCi == 1);
+  const bool creal = D.flags & G_CREAL, accum = D.flags & G_ACCUM;
+  char* Cb = reinterpret_cast<char*>(bufs.p[D.c_buf]);
+  for (int e = tid; e < GTM * GTN; e += 256) {
+    int ii, nn;
+    if (ifast) { ii = e % GTM; nn = e / GTM; } else { nn = e % GTN; ii = e / GTN; }
+    int i = i0 + ii;
+    int64_t n = n0 + nn;
+    if (i >= M || n >= N) continue;
+    int64_t n1 = n / N2, n2 = n - n1 * N2;
+    int64_t off = D.c_off + (int64_t)i * D.sCi + n1 * D.sC1 + n2 * D.sC2;
+    double2 v = Cs[ii * (GTN + 1) + nn];
+    if (creal) {
+      double* c = reinterpret_cast<double*>(Cb) + off;
+      *c = accum ? *c + v.x : v.x;
+    } else {
+      double2* c = reinterpret_cast<double2*>(Cb) + off;
+      if (accum) { double2 o = *c; v.x += o.x; v.y += o.y; }
+      *c = v;
+    }
+  }
+}
+
+cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, int, const Bufs& bufs,
+                        cudaStream_t st) {
+  if (ndesc <= 0) return cudaSuccess;
+  for (int z0 = 0; z0 < ndesc; z0 += 65535) {
+    int nz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
+    dim3 grid((unsigned)((maxN + GTN - 1) / GTN), (unsigned)((maxM + GTM - 1) / GTM), (unsigned)nz);
+    k_gemm<<<grid, 256, 0, st>>>(d_descs + z0, bufs);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- warp tridiagonal solver
+// Solves a_k x_{k-1} + (g_k + s e_k) x_k + c_k x_{k+1} = d_k, k = 0..nz-1, one system per
+// warp; lane t owns rows t*K .. t*K+K-1 (rows >= nz are identity rows).  Each lane first
+// eliminates inside its chunk (a downward sweep expressing rows through the chunk's first
+// unknown, an upward sweep expressing the first row through the chunk's last unknown),
+// leaving a tridiagonal system of 2 unknowns per lane (64 total) that parallel cyclic
+// reduction solves in 6 shuffle levels; a back-substitution recovers the chunk interior.
+// No pivoting (reading R15); |pivot| / row-norm is monitored into minpiv.
+struct ZRow {
+  const double2 *a, *g, *c, *e;
+};
+
+template <int K>
+__device__ __forceinline__ void warp_tridiag(cplx (&d)[K], int nz, const ZRow& T, cplx s, int lane,
+                                             double& minpiv) {
+  const int k0 = lane * K;
+  cplx al[K], ga[K], de[K];
+  auto coef = [&](int j, cplx& a, cplx& b, cplx& c) {
+    int k = k0 + j;
+    if (k < nz) {
+      a = ld(T.a + k); c = ld(T.c + k);
+      b = cfma(s, ld(T.e + k), ld(T.g + k));
+    } else {
+      a = mk(0, 0); c = mk(0, 0); b = mk(1, 0);
+    }
+  };
+  // downward sweep, rows 1..K-1, left boundary x_s (= row 0 of the chunk)
+  {
+    cplx a, b, c;
+    coef(1, a, b, c);
+    double rn = cabs1(a) + cabs1(b) + cabs1(c);
+    minpiv = fmin(minpiv, cabs1(b) / rn);
+    cplx inv = cinv(b);
+    al[1] = a * inv; ga[1] = c * inv; de[1] = d[1] * inv;
+#pragma unroll
+    for (int j = 2; j < K; ++j) {
+      coef(j, a, b, c);
+      cplx r = b - a * ga[j - 1];
+      minpiv = fmin(minpiv, cabs1(r) / (cabs1(a) + cabs1(b) + cabs1(c)));
+      inv = cinv(r);
+      al[j] = -(a * al[j - 1]) * inv;
+      ga[j] = c * inv;
+      de[j] = (d[j] - a * de[j - 1]) * inv;
+    }
+  }
+  // upward sweep for row 0 with right boundary x_e (= row K-1)
+  cplx ua, uc, ud;
+  {
+    cplx a, b, c;
+    coef(K - 2, a, b, c);
+    double rn = cabs1(a) + cabs1(b) + cabs1(c);
+    minpiv = fmin(minpiv, cabs1(b) / rn);
+    cplx inv = cinv(b);
+    ua = a * inv; uc = c * inv; ud = d[K - 2] * inv;
+#pragma unroll
+    for (int j = K - 3; j >= 0; --j) {
+      coef(j, a, b, c);
+      cplx r = b - c * ua;
+      minpiv = fmin(minpiv, cabs1(r) / (cabs1(a) + cabs1(b) + cabs1(c)));
+      inv = cinv(r);
+      cplx nua = a * inv;
+      uc = -(c * uc) * inv;
+      ud = (d[j] - c * ud) * inv;
+      ua = nua;
+    }
+  }
+  // reduced system, normalised rows (B = 1):  S: ua x_{e,t-1} + x_{s,t} + uc x_{e,t} = ud
+  //                                           E: al x_{s,t} + x_{e,t} + ga x_{s,t+1} = de
+  cplx sA = ua, sC = uc, sD = ud;
+  cplx eA = al[K - 1], eC = ga[K - 1], eD = de[K - 1];
+  // level 1: S uses (E of lane-1) on the left and own E on the right; E uses own S and S of lane+1.
+  {
+    cplx lA = shfl_up(eA, 1), lC = shfl_up(eC, 1), lD = shfl_up(eD, 1);
+    if (lane == 0) { lA = mk(0, 0); lC = mk(0, 0); lD = mk(0, 0); }
+    cplx rA = shfl_down(sA, 1), rC = shfl_down(sC, 1), rD = shfl_down(sD, 1);
+    if (lane == 31) { rA = mk(0, 0); rC = mk(0, 0); rD = mk(0, 0); }
+    // S' = S - sA*Eleft - sC*Eown
+    cplx nsA = -(sA * lA);
+    cplx nsB = mk(1, 0) - sA * lC - sC * eA;
+    cplx nsC = -(sC * eC);
+    cplx nsD = sD - sA * lD - sC * eD;
+    // E' = E - eA*Sown - eC*Sright
+    cplx neA = -(eA * sA);
+    cplx neB = mk(1, 0) - eA * sC - eC * rA;
+    cplx neC = -(eC * rC);
+    cplx neD = eD - eA * sD - eC * rD;
+    cplx is = cinv(nsB), ie = cinv(neB);
+    sA = nsA * is; sC = nsC * is; sD = nsD * is;
+    eA = neA * ie; eC = neC * ie; eD = neD * ie;
+  }
+  // levels 2..: S couples S of lanes t-+delta, E couples E of lanes t-+delta
+#pragma unroll
+  for (int dl = 1; dl < 32; dl <<= 1) {
+    cplx lsA = shfl_up(sA, dl), lsC = shfl_up(sC, dl), lsD = shfl_up(sD, dl);
+    cplx rsA = shfl_down(sA, dl), rsC = shfl_down(sC, dl), rsD = shfl_down(sD, dl);
+    cplx leA = shfl_up(eA, dl), leC = shfl_up(eC, dl), leD = shfl_up(eD, dl);
+    cplx reA = shfl_down(eA, dl), reC = shfl_down(eC, dl), reD = shfl_down(eD, dl);
+    if (lane < dl) { lsA = lsC = lsD = leA = leC = leD = mk(0, 0); }
+    if (lane + dl > 31) { rsA = rsC = rsD = reA = reC = reD = mk(0, 0); }
+    cplx nsB = mk(1, 0) - sA * lsC - sC * rsA;
+    cplx nsA = -(sA * lsA), nsC = -(sC * rsC), nsD = sD - sA * lsD - sC * rsD;
+    cplx neB = mk(1, 0) - eA * leC - eC * reA;
+    cplx neA = -(eA * leA), neC = -(eC * reC), neD = eD - eA * leD - eC * reD;
+    cplx is = cinv(nsB), ie = cinv(neB);
+    sA = nsA * is; sC = nsC * is; sD = nsD * is;
+    eA = neA * ie; eC = neC * ie; eD = neD * ie;
+  }
+  const cplx xs = sD, xe = eD;
+  d[K - 1] = xe;
+#pragma unroll
+  for (int j = K - 2; j >= 1; --j) d[j] = de[j] - al[j] * xs - ga[j] * d[j + 1];
+  d[0] = xs;
+}
+
+__device__ __forceinline__ void warp_min_commit(double v, double* out) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && out) atomic_min_pos(out, v);
+}
+
+// mode 1: pass-1 solve in place (RHS = transformed f).  mode 2: pass-2 Dirichlet lifting
+// (RHS built from the face transforms), solution ADDED to the stored v~ (u~ = v~ + w~).
+template <int K, int MODE>
+__global__ void __launch_bounds__(128) k_zsolve_block(const ZBlock* __restrict__ blocks, int R, int nz,
+                                                      ZTab tab, int64_t sig_off, Bufs bufs, double* minpiv_out) {
+  const ZBlock& B = blocks[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int64_t nsys = (int64_t)B.nx * B.ny * R;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  double2* MS = reinterpret_cast<double2*>(bufs.p[B_MS]);
+  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
+  ZRow T{TAB + tab.a, TAB + tab.g, TAB + tab.c, TAB + tab.e};
+  double minpiv = 1.0;
+  const int warps = blockDim.x >> 5;
+  for (int64_t sidx = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); sidx < nsys;
+       sidx += (int64_t)gridDim.x * warps) {
+    const int l = (int)(sidx % B.nx);
+    const int64_t rm = sidx / B.nx;
+    const int m = (int)(rm % B.ny);
+    const int r = (int)(rm / B.ny);
+    const cplx s = ld(TAB + B.lamx + l) + ld(TAB + B.lamy + m);
+    double2* line = MS + B.ms_off + sidx * nz;
+    cplx d[K];
+    if (MODE == 1) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        int k = lane * K + j;
+        d[j] = (k < nz) ? cplx{line[k].x, line[k].y} : mk(0, 0);
+      }
+    } else {
+      const cplx wx0 = ld(TAB + B.wx0 + l), wx1 = ld(TAB + B.wx1 + l);
+      const cplx wy0 = ld(TAB + B.wy0 + m), wy1 = ld(TAB + B.wy1 + m);
+      const cplx cL = mk(B.cL.x, B.cL.y) * wx0, cR = mk(B.cR.x, B.cR.y) * wx1;
+      const cplx cB = mk(B.cB.x, B.cB.y) * wy0, cT = mk(B.cT.x, B.cT.y) * wy1;
+      // face transforms stored [r][mode][k] with the mode stride padded to Bx.ny / nx
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        int k = lane * K + j;
+        cplx acc = mk(0, 0);
+        if (k < nz) {
+          if (B.gL >= 0) acc = cfma(cL, ld(IF + B.gL + ((int64_t)r * B.ny + m) * nz + k), acc);
+          if (B.gR >= 0) acc = cfma(cR, ld(IF + B.gR + ((int64_t)r * B.ny + m) * nz + k), acc);
+          if (B.gB >= 0) acc = cfma(cB, ld(IF + B.gB + ((int64_t)r * B.nx + l) * nz + k), acc);
+          if (B.gT >= 0) acc = cfma(cT, ld(IF + B.gT + ((int64_t)r * B.nx + l) * nz + k), acc);
+          acc = -(ld(TAB + sig_off + k) * acc);
+        }
+        d[j] = acc;
+      }
+    }
+    warp_tridiag<K>(d, nz, T, s, lane, minpiv);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      int k = lane * K + j;
+      if (k < nz) {
+        if (MODE == 1) line[k] = make_double2(d[j].x, d[j].y);
+        else { double2 o = line[k]; line[k] = make_double2(o.x + d[j].x, o.y + d[j].y); }
+      }
+    }
+  }
+  warp_min_commit(minpiv, minpiv_out);
+}
+
+template <int MODE>
+static cudaError_t zsb_dispatch(int K, dim3 grid, cudaStream_t st, const ZBlock* b, int R, int nz, ZTab tab,
+                                int64_t sig, const Bufs& bufs, double* mp) {
+  switch (K) {
+#define ZK(KK) case KK: k_zsolve_block<KK, MODE><<<grid, 128, 0, st>>>(b, R, nz, tab, sig, bufs, mp); break;
+    ZK(2) ZK(3) ZK(4) ZK(5) ZK(6) ZK(7) ZK(8) ZK(9) ZK(10) ZK(11) ZK(12) ZK(13) ZK(14) ZK(15) ZK(16)
+#undef ZK
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+static int rows_per_lane(int nz) {
+  int K = (nz + 31) / 32;
+  return K < 2 ? 2 : K;
+}
+
+cudaError_t launch_zsolve_block(int mode, const ZBlock* d_blocks, int nblocks, int max_systems, int R, int nz,
+                                ZTab tab, int64_t sig_off, const Bufs& bufs, double* d_minpiv, cudaStream_t st) {
+  int K = rows_per_lane(nz);
+  if (K > 16) return cudaErrorInvalidValue;
+  int64_t want = ((int64_t)max_systems + 3) / 4;
+  dim3 grid((unsigned)(want > 65535 ? 65535 : (want < 1 ? 1 : want)), (unsigned)nblocks);
+  return mode == 1 ? zsb_dispatch<1>(K, grid, st, d_blocks, R, nz, tab, sig_off, bufs, d_minpiv)
+                   : zsb_dispatch<2>(K, grid, st, d_blocks, R, nz, tab, sig_off, bufs, d_minpiv);
+}
+
+// ---------------------------------------------------------------- step 5 global sweep
+template <int K>
+__global__ void __launch_bounds__(128) k_gsweep(GSweep G, ZTab tab, Bufs bufs, double* minpiv_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nsys = (int64_t)G.nx * G.ny * G.R;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
+  double2* WH = reinterpret_cast<double2*>(bufs.p[B_T1]) + G.what;
+  ZRow T{TAB + tab.a, TAB + tab.g, TAB + tab.c, TAB + tab.e};
+  const int nz = G.nz;
+  double minpiv = 1.0;
+  const int warps = blockDim.x >> 5;
+  for (int64_t sidx = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); sidx < nsys;
+       sidx += (int64_t)gridDim.x * warps) {
+    const int l = (int)(sidx % G.nx);
+    const int64_t rm = sidx / G.nx;
+    const int m = (int)(rm % G.ny);
+    const int r = (int)(rm / G.ny);
+    const cplx s = ld(TAB + G.lamx + l) + ld(TAB + G.lamy + m);
+    cplx d[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) d[j] = mk(0, 0);
+    // r^[l,m,k] = sum_a W_x[I_a,l] R1[a][r][m][k] + sum_b W_y[I_b,m] R2[b][r][l][k]
+    for (int a = 0; a < G.nifx; ++a) {
+      const cplx w = ld(TAB + G.wxi + (int64_t)a * G.nx + l);
+      const double2* src = IF + G.r1 + (((int64_t)a * G.R + r) * G.ny + m) * nz;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        int k = lane * K + j;
+        if (k < nz) d[j] = cfma(w, ld(src + k), d[j]);
+      }
+    }
+    for (int b = 0; b < G.nify; ++b) {
+      const cplx w = ld(TAB + G.wyi + (int64_t)b * G.ny + m);
+      const double2* src = IF + G.r2 + (((int64_t)b * G.R + r) * G.nx + l) * nz;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        int k = lane * K + j;
+        if (k < nz) d[j] = cfma(w, ld(src + k), d[j]);
+      }
+    }
+    warp_tridiag<K>(d, nz, T, s, lane, minpiv);
+    double2* line = WH + sidx * nz;  // W^[r][m][l][k]
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      int k = lane * K + j;
+      if (k < nz) line[k] = make_double2(d[j].x, d[j].y);
+    }
+  }
+  warp_min_commit(minpiv, minpiv_out);
+}
+
+cudaError_t launch_gsweep(const GSweep& g, ZTab tab, const Bufs& bufs, double* d_minpiv, cudaStream_t st) {
+  int K = rows_per_lane(g.nz);
+  int64_t nsys = (int64_t)g.nx * g.ny * g.R;
+  int64_t want = (nsys + 3) / 4;
+  dim3 grid((unsigned)(want > 1048576 ? 1048576 : want));
+  switch (K) {
+#define GK(KK) case KK: k_gsweep<KK><<<grid, 128, 0, st>>>(g, tab, bufs, d_minpiv); break;
+    GK(2) GK(3) GK(4) GK(5) GK(6) GK(7) GK(8) GK(9) GK(10) GK(11) GK(12) GK(13) GK(14) GK(15) GK(16)
+#undef GK
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- step 4 interface residual
+// x-plane a (node P): r = b - (1/hx_{P-1}) hy^_q s_k hz^_k v(P-1,q,k) - (1/hx_P) hy^_q s_k hz^_k v(P+1,q,k)
+// for q not on a y-interface, r = b on the intersection lines (v = 0 on every neighbour).
+// v at the interface-adjacent rows comes from step 3: VX[blk][r][e][k][qpad], VY[blk][r][e][k][ppad].
+__device__ __forceinline__ cplx load_f(const void* f, int dtype, int64_t off) {
+  if (dtype == 1) return mk(__ldg(reinterpret_cast<const double*>(f) + off), 0.0);
+  return ld(reinterpret_cast<const double2*>(f) + off);
+}
+
+__global__ void k_iface_res(IfaceRes P, Bufs bufs) {
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  double2* IF = reinterpret_cast<double2*>(bufs.p[B_IF]);
+  const int* ifx = reinterpret_cast<const int*>(TAB + P.ifx);
+  const int* ify = reinterpret_cast<const int*>(TAB + P.ify);
+  const int* bx = reinterpret_cast<const int*>(TAB + P.blk_of_x);
+  const int* by = reinterpret_cast<const int*>(TAB + P.blk_of_y);
+  const int* xlo = reinterpret_cast<const int*>(TAB + P.xlo);
+  const int* ylo = reinterpret_cast<const int*>(TAB + P.ylo);
+  const void* f = bufs.p[B_F];
+  const int nx = P.nx, ny = P.ny, nz = P.nz, R = P.R;
+  const int64_t nxplane = (int64_t)P.nifx * R * nz * ny;
+  const int64_t total = nxplane + (int64_t)P.nify * R * nz * nx;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < nxplane) {
+      const int q = (int)(t % ny);              // 0-based global y index
+      int64_t rest = t / ny;
+      const int k = (int)(rest % nz); rest /= nz;
+      const int r = (int)(rest % R);
+      const int a = (int)(rest / R);
+      const int Pn = ifx[a];                    // 1-based node
+      const int64_t fo = (((int64_t)r * nz + k) * ny + q) * nx + (Pn - 1);
+      cplx hh = ld(TAB + P.hhx + Pn - 1) * ld(TAB + P.hhy + q) * ld(TAB + P.hhz + k);
+      cplx res = hh * load_f(f, P.dtype, fo);
+      const int jb = by[q];
+      if (jb >= 0) {
+        const int ql = q + 1 - ylo[jb];
+        const cplx wgt = ld(TAB + P.hhy + q) * ld(TAB + P.sig + k) * ld(TAB + P.hhz + k);
+        // left block column a, its last row (e=1); right block column a+1, its first row (e=0)
+        const int bl = jb * P.nbx + a, br = jb * P.nbx + a + 1;
+        const cplx vl = ld(IF + P.vxo + ((((int64_t)bl * R + r) * 2 + 1) * nz + k) * P.qpad + ql);
+        const cplx vr = ld(IF + P.vxo + ((((int64_t)br * R + r) * 2 + 0) * nz + k) * P.qpad + ql);
+        res = res - (cinv(ld(TAB + P.hx + Pn - 1)) * wgt) * vl - (cinv(ld(TAB + P.hx + Pn)) * wgt) * vr;
+      }
+      IF[P.rx + t] = make_double2(res.x, res.y);  // RX[a][r][k][q]
+    } else {
+      const int64_t u = t - nxplane;
+      const int p = (int)(u % nx);
+      int64_t rest = u / nx;
+      const int k = (int)(rest % nz); rest /= nz;
+      const int r = (int)(rest % R);
+      const int b = (int)(rest / R);
+      const int Qn = ify[b];
+      const int ib = bx[p];
+      cplx res = mk(0, 0);
+      if (ib >= 0) {  // nodes on x-interfaces are owned by RX
+        const int64_t fo = (((int64_t)r * nz + k) * ny + (Qn - 1)) * nx + p;
+        cplx hh = ld(TAB + P.hhx + p) * ld(TAB + P.hhy + Qn - 1) * ld(TAB + P.hhz + k);
+        res = hh * load_f(f, P.dtype, fo);
+        const int pl = p + 1 - xlo[ib];
+        const cplx wgt = ld(TAB + P.hhx + p) * ld(TAB + P.sig + k) * ld(TAB + P.hhz + k);
+        const int bb = b * P.nbx + ib, bt = (b + 1) * P.nbx + ib;
+        const cplx vb = ld(IF + P.vyo + ((((int64_t)bb * R + r) * 2 + 1) * nz + k) * P.ppad + pl);
+        const cplx vt = ld(IF + P.vyo + ((((int64_t)bt * R + r) * 2 + 0) * nz + k) * P.ppad + pl);
+        res = res - (cinv(ld(TAB + P.hy + Qn - 1)) * wgt) * vb - (cinv(ld(TAB + P.hy + Qn)) * wgt) * vt;
+      }
+      IF[P.ry + u] = make_double2(res.x, res.y);  // RY[b][r][k][p]
+    }
+  }
+}
+
+cudaError_t launch_iface_residual(const IfaceRes& p, const Bufs& bufs, cudaStream_t st) {
+  int64_t total = (int64_t)p.nifx * p.R * p.nz * p.ny + (int64_t)p.nify * p.R * p.nz * p.nx;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  k_iface_res<<<(unsigned)(blocks > 65535 * 16 ? 65535 * 16 : blocks), 256, 0, st>>>(p, bufs);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- u = w on the interface planes
+__global__ void k_write_iface(int nx, int ny, int nz, int R, int dtype, int nifx, int nify, int64_t ifxo,
+                              int64_t ifyo, int64_t wx, int64_t wy, Bufs bufs) {
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
+  const int* ifx = reinterpret_cast<const int*>(TAB + ifxo);
+  const int* ify = reinterpret_cast<const int*>(TAB + ifyo);
+  void* u = bufs.p[B_U];
+  const int64_t nxp = (int64_t)nifx * R * nz * ny;
+  const int64_t total = nxp + (int64_t)nify * R * nz * nx;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t uo;
+    double2 v;
+    if (t < nxp) {
+      const int q = (int)(t % ny);
+      int64_t rest = t / ny;
+      const int k = (int)(rest % nz); rest /= nz;
+      const int r = (int)(rest % R);
+      const int a = (int)(rest / R);
+      uo = (((int64_t)r * nz + k) * ny + q) * nx + (ifx[a] - 1);
+      v = IF[wx + t];
+    } else {
+      const int64_t s = t - nxp;
+      const int p = (int)(s % nx);
+      int64_t rest = s / nx;
+      const int k = (int)(rest % nz); rest /= nz;
+      const int r = (int)(rest % R);
+      const int b = (int)(rest / R);
+      // intersection lines are written by the x-plane values only
+      bool on_x = false;
+      for (int a = 0; a < nifx; ++a) on_x |= (ifx[a] - 1 == p);
+      if (on_x) continue;
+      uo = (((int64_t)r * nz + k) * ny + (ify[b] - 1)) * nx + p;
+      v = IF[wy + s];
+    }
+    if (dtype == 1) reinterpret_cast<double*>(u)[uo] = v.x;
+    else reinterpret_cast<double2*>(u)[uo] = v;
+  }
+}
+
+cudaError_t launch_write_iface_u(int nx, int ny, int nz, int R, int dtype, int nifx, int nify, int64_t ifx,
+                                 int64_t ify, int64_t wx, int64_t wy, const Bufs& bufs, cudaStream_t st) {
+  int64_t total = (int64_t)nifx * R * nz * ny + (int64_t)nify * R * nz * nx;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  k_write_iface<<<(unsigned)(blocks > 1048576 ? 1048576 : blocks), 256, 0, st>>>(nx, ny, nz, R, dtype, nifx, nify,
+                                                                                  ifx, ify, wx, wy, bufs);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- residual (fp64 / double-double)
+// double-double primitives (error-free transformations with FMA)
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = a + b, bb = s - a;
+  return dd{s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  double lo = s.lo + a.lo + b.lo;
+  double hi = s.hi + lo;
+  return dd{hi, lo - (hi - s.hi)};
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  double p = a.hi * b.hi;
+  double e = fma(a.hi, b.hi, -p);
+  e = fma(a.hi, b.lo, fma(a.lo, b.hi, e));
+  double hi = p + e;
+  return dd{hi, e - (hi - p)};
+}
+__device__ __forceinline__ dd dd_neg(dd a) { return dd{-a.hi, -a.lo}; }
+struct zdd {
+  dd x, y;
+};
+__device__ __forceinline__ zdd zadd(zdd a, zdd b) { return zdd{dd_add(a.x, b.x), dd_add(a.y, b.y)}; }
+__device__ __forceinline__ zdd zsub(zdd a, zdd b) { return zdd{dd_add(a.x, dd_neg(b.x)), dd_add(a.y, dd_neg(b.y))}; }
+__device__ __forceinline__ zdd zmul(zdd a, zdd b) {
+  return zdd{dd_add(dd_mul(a.x, b.x), dd_neg(dd_mul(a.y, b.y))), dd_add(dd_mul(a.x, b.y), dd_mul(a.y, b.x))};
+}
+__device__ __forceinline__ zdd zfrom(cplx a) { return zdd{dd{a.x, 0}, dd{a.y, 0}}; }
+// 1/h in double-double (Newton step on the fp64 reciprocal)
+__device__ __forceinline__ zdd zinv_dd(cplx h) {
+  zdd H = zfrom(h);
+  cplx r0 = cinv(h);
+  zdd R0 = zfrom(r0);
+  // r1 = r0 + r0 (1 - h r0)
+  zdd e = zsub(zdd{dd{1.0, 0}, dd{0, 0}}, zmul(H, R0));
+  return zadd(R0, zmul(R0, e));
+}
+
+struct ResParams {
+  int nx, ny, nz, R, dtype, dd, has_f, to_f;
+  int64_t hx, hy, hz, hhx, hhy, hhz, sig, sige;
+  double2 lam;
+};
+
+__device__ __forceinline__ cplx load_u(const void* u, int dtype, int64_t off) {
+  if (dtype == 1) return mk(reinterpret_cast<const double*>(u)[off], 0.0);
+  double2 v = reinterpret_cast<const double2*>(u)[off];
+  return mk(v.x, v.y);
+}
+
+__global__ void k_residual(ResParams P, const void* __restrict__ u, const void* __restrict__ f, double2* __restrict__ rout,
+                           double* norms, Bufs bufs) {
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const int nx = P.nx, ny = P.ny, nz = P.nz;
+  const int64_t plane = (int64_t)nx * ny, vol = plane * nz, total = vol * P.R;
+  double acc_r = 0, acc_b = 0;
+  int rcur = -1;
+  auto flush = [&](int rr) {
+    if (rr >= 0 && norms) {
+      atomicAdd(norms + 2 * rr, acc_r);
+      atomicAdd(norms + 2 * rr + 1, acc_b);
+    }
+    acc_r = acc_b = 0;
+  };
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % nx);
+    const int j = (int)((t / nx) % ny);
+    const int k = (int)((t / plane) % nz);
+    const int r = (int)(t / vol);
+    if (r != rcur) { flush(rcur); rcur = r; }
+    const cplx uc = load_u(u, P.dtype, t);
+    const cplx ul = i > 0 ? load_u(u, P.dtype, t - 1) : mk(0, 0);
+    const cplx ur = i < nx - 1 ? load_u(u, P.dtype, t + 1) : mk(0, 0);
+    const cplx us = j > 0 ? load_u(u, P.dtype, t - nx) : mk(0, 0);
+    const cplx un = j < ny - 1 ? load_u(u, P.dtype, t + nx) : mk(0, 0);
+    const cplx ub = k > 0 ? load_u(u, P.dtype, t - plane) : mk(0, 0);
+    const cplx ut = k < nz - 1 ? load_u(u, P.dtype, t + plane) : mk(0, 0);
+    const cplx hx0 = ld(TAB + P.hx + i), hx1 = ld(TAB + P.hx + i + 1);
+    const cplx hy0 = ld(TAB + P.hy + j), hy1 = ld(TAB + P.hy + j + 1);
+    const cplx hz0 = ld(TAB + P.hz + k), hz1 = ld(TAB + P.hz + k + 1);
+    const cplx cx = ld(TAB + P.hhx + i), cy = ld(TAB + P.hhy + j), cz = ld(TAB + P.hhz + k);
+    const cplx sg = ld(TAB + P.sig + k), se0 = ld(TAB + P.sige + k), se1 = ld(TAB + P.sige + k + 1);
+    const cplx lam = mk(P.lam.x, P.lam.y);
+    cplx fv = P.has_f ? load_f(f, P.dtype, t) : mk(0, 0);
+    cplx res, bnorm;
+    if (!P.dd) {
+      cplx tx = (ur - uc) * cinv(hx1) - (uc - ul) * cinv(hx0);
+      cplx ty = (un - uc) * cinv(hy1) - (uc - us) * cinv(hy0);
+      cplx tz = se1 * (ut - uc) * cinv(hz1) - se0 * (uc - ub) * cinv(hz0);
+      cplx Au = sg * tx * cy * cz + sg * ty * cx * cz + tz * cx * cy + lam * uc * cx * cy * cz;
+      cplx b = fv * cx * cy * cz;
+      res = b - Au;
+      bnorm = b;
+      if (P.to_f) res = res * cinv(cx * cy * cz);
+    } else {
+      // every product and sum in double-double, rounded once at the end
+      const zdd Uc = zfrom(uc);
+      zdd tx = zsub(zmul(zsub(zfrom(ur), Uc), zinv_dd(hx1)), zmul(zsub(Uc, zfrom(ul)), zinv_dd(hx0)));
+      zdd ty = zsub(zmul(zsub(zfrom(un), Uc), zinv_dd(hy1)), zmul(zsub(Uc, zfrom(us)), zinv_dd(hy0)));
+      zdd tz = zsub(zmul(zmul(zfrom(se1), zsub(zfrom(ut), Uc)), zinv_dd(hz1)),
+                    zmul(zmul(zfrom(se0), zsub(Uc, zfrom(ub))), zinv_dd(hz0)));
+      // control volumes (h_{i-1}+h_i)/2 exactly in dd
+      zdd Cx = zmul(zadd(zfrom(hx0), zfrom(hx1)), zdd{dd{0.5, 0}, dd{0, 0}});
+      zdd Cy = zmul(zadd(zfrom(hy0), zfrom(hy1)), zdd{dd{0.5, 0}, dd{0, 0}});
+      zdd Cz = zmul(zadd(zfrom(hz0), zfrom(hz1)), zdd{dd{0.5, 0}, dd{0, 0}});
+      zdd S = zfrom(sg);
+      zdd Au = zmul(zmul(S, tx), zmul(Cy, Cz));
+      Au = zadd(Au, zmul(zmul(S, ty), zmul(Cx, Cz)));
+      Au = zadd(Au, zmul(tz, zmul(Cx, Cy)));
+      zdd V = zmul(Cx, zmul(Cy, Cz));
+      Au = zadd(Au, zmul(zmul(zfrom(lam), Uc), V));
+      zdd b = zmul(zfrom(fv), V);
+      zdd rr = zsub(b, Au);
+      res = mk(rr.x.hi + rr.x.lo, rr.y.hi + rr.y.lo);
+      bnorm = mk(b.x.hi, b.y.hi);
+      if (P.to_f) res = res * cinv(cx * cy * cz);
+    }
+    if (rout) rout[t] = make_double2(res.x, res.y);
+    if (norms) {
+      cplx rb = P.to_f ? res * (cx * cy * cz) : res;
+      acc_r += rb.x * rb.x + rb.y * rb.y;
+      acc_b += bnorm.x * bnorm.x + bnorm.y * bnorm.y;
+    }
+  }
+  flush(rcur);
+}
+
+cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int ddm, int has_f, int64_t hx, int64_t hy,
+                            int64_t hz, int64_t hhx, int64_t hhy, int64_t hhz, int64_t sig, int64_t sige, double2 lam,
+                            const void* u, const void* f, double2* r, int to_f_units, double* d_norms, const Bufs& bufs,
+                            cudaStream_t st) {
+  ResParams P{nx, ny, nz, R, dtype, ddm, has_f, to_f_units, hx, hy, hz, hhx, hhy, hhz, sig, sige, lam};
+  int64_t total = (int64_t)nx * ny * nz * R;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  k_residual<<<(unsigned)blocks, 256, 0, st>>>(P, u, f, r, d_norms, bufs);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- u += delta
+__global__ void k_axpy(int64_t n, int dtype, const double2* __restrict__ dlt, void* u) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    double2 d = dlt[t];
+    if (dtype == 1) reinterpret_cast<double*>(u)[t] += d.x;
+    else {
+      double2* p = reinterpret_cast<double2*>(u) + t;
+      double2 o = *p;
+      *p = make_double2(o.x + d.x, o.y + d.y);
+    }
+  }
+}
+
+cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  k_axpy<<<(unsigned)blocks, 256, 0, st>>>(n, dtype, delta, u);
+  return cudaGetLastError();
+}
+
+__global__ void k_fill_one(double* p) { *p = 1.0; }
+cudaError_t launch_fill_minpiv(double* p, cudaStream_t st) {
+  k_fill_one<<<1, 1, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace lfds

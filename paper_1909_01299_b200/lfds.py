@@ -1,0 +1,234 @@
+"""Thin ctypes binding of the C ABI in include/lfds.h (argument marshalling only).
+
+Every step of the solve runs in the sm_100a kernels of ``_lib/liblfds.so``; PyTorch only
+provides device memory (tensors, the workspace) and the CUDA stream.  There is no
+fallback: if the library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "liblfds.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"liblfds.so not built ({_LIB_PATH}); run __graft_entry__.build() "
+                      "or python paper_1909_01299_b200/build.py")
+_lib = ctypes.CDLL(_LIB_PATH)
+
+LFDS_C128, LFDS_F64 = 0, 1
+STATUS = {0: "OK", 1: "EINVAL", 2: "EEIG", 3: "ERESONANCE", 4: "ENOMEM", 5: "ECUDA", 6: "ENCCL",
+          7: "ENOTCONVERGED", 8: "ENODEVICE"}
+
+
+class LfdsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"lfds {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Z(ctypes.Structure):
+    _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int), ("refine", ctypes.c_int), ("refine_tol", ctypes.c_double),
+                ("residual_dd", ctypes.c_int), ("device", ctypes.c_int), ("rhs_chunk", ctypes.c_int)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("passes", ctypes.c_int), ("rel_residual", ctypes.c_double * 9),
+                ("min_pivot_ratio", ctypes.c_double), ("n_kernel_launches", ctypes.c_int)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("nbx", ctypes.c_int),
+                ("nby", ctypes.c_int), ("n_if_x", ctypes.c_int), ("n_if_y", ctypes.c_int), ("real_z", ctypes.c_int),
+                ("setup_seconds", ctypes.c_double), ("eig_max_residual", ctypes.c_double),
+                ("eig_max_biorth", ctypes.c_double), ("device_table_bytes", ctypes.c_size_t)]
+
+
+_P = ctypes.c_void_p
+_lib.lfds_default_options.argtypes = [ctypes.POINTER(Options)]
+_lib.lfds_setup_grid.argtypes = [ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P, _P, _Z,
+                                 ctypes.c_int, _P, ctypes.c_int, _P, ctypes.POINTER(Options), ctypes.POINTER(_P)]
+_lib.lfds_workspace_bytes.argtypes = [_P, ctypes.c_int]
+_lib.lfds_workspace_bytes.restype = ctypes.c_size_t
+_lib.lfds_workspace_bytes_host.argtypes = [_P, ctypes.c_int]
+_lib.lfds_workspace_bytes_host.restype = ctypes.c_size_t
+_lib.lfds_solve.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
+_lib.lfds_solve_host.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
+_lib.lfds_residual.argtypes = [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P]
+_lib.lfds_get_report.argtypes = [_P, ctypes.POINTER(Report)]
+_lib.lfds_get_info.argtypes = [_P, ctypes.POINTER(Info)]
+_lib.lfds_get_basis.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _P, _P]
+_lib.lfds_destroy.argtypes = [_P]
+_lib.lfds_last_error.restype = ctypes.c_char_p
+_lib.lfds_version.restype = ctypes.c_char_p
+
+EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
+            "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_residual", "lfds_get_report",
+            "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version"]
+
+
+def _check(rc):
+    if rc != 0:
+        raise LfdsError(rc, _lib.lfds_last_error().decode())
+
+
+def _zarr(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+    return a, a.ctypes.data_as(_P)
+
+
+def version() -> str:
+    return _lib.lfds_version().decode()
+
+
+class Plan:
+    """A setup_grid plan (per-grid tables resident on the device)."""
+
+    def __init__(self, hx, hy, hz, sigma_node, sigma_edge, lam, iface_x: Sequence[int] = (),
+                 iface_y: Sequence[int] = (), *, dtype: str = "c128", refine: int = 0,
+                 refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0):
+        opt = Options()
+        _lib.lfds_default_options(ctypes.byref(opt))
+        opt.dtype = LFDS_F64 if dtype in ("f64", "float64") else LFDS_C128
+        opt.refine, opt.refine_tol, opt.residual_dd = int(refine), float(refine_tol), int(bool(residual_dd))
+        opt.device, opt.rhs_chunk = int(device), int(rhs_chunk)
+        self.dtype = opt.dtype
+        hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
+        sn_, psn = _zarr(sigma_node); se_, pse = _zarr(sigma_edge)
+        ix = np.ascontiguousarray(np.asarray(list(iface_x), dtype=np.int32))
+        iy = np.ascontiguousarray(np.asarray(list(iface_y), dtype=np.int32))
+        lam = complex(lam)
+        h = _P()
+        _check(_lib.lfds_setup_grid(len(hx_) - 1, px, len(hy_) - 1, py, len(hz_) - 1, pz, psn, pse,
+                                    _Z(lam.real, lam.imag), len(ix), ix.ctypes.data_as(_P), len(iy),
+                                    iy.ctypes.data_as(_P), ctypes.byref(opt), ctypes.byref(h)))
+        self._h = h
+        self.shape = (len(hz_) - 1, len(hy_) - 1, len(hx_) - 1)
+        self._ws = {}
+
+    @classmethod
+    def from_problem(cls, p, **kw):
+        """Plan for a workloads.Problem (seeded synthetic config)."""
+        if p.real and "dtype" not in kw:
+            kw["dtype"] = "f64"
+        return cls(p.hx, p.hy, p.hz, p.sigma_node, p.sigma_edge, p.lam, p.iface_x, p.iface_y, **kw)
+
+    # ------------------------------------------------------------------ queries
+    def workspace_bytes(self, nrhs: int = 1) -> int:
+        return int(_lib.lfds_workspace_bytes(self._h, nrhs))
+
+    def workspace_bytes_host(self, nrhs: int = 1) -> int:
+        return int(_lib.lfds_workspace_bytes_host(self._h, nrhs))
+
+    def info(self) -> dict:
+        i = Info()
+        _check(_lib.lfds_get_info(self._h, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in Info._fields_}
+
+    def report(self) -> dict:
+        r = Report()
+        _check(_lib.lfds_get_report(self._h, ctypes.byref(r)))
+        return {"passes": r.passes, "rel_residual": list(r.rel_residual)[:max(r.passes, 1)],
+                "min_pivot_ratio": r.min_pivot_ratio, "n_kernel_launches": r.n_kernel_launches}
+
+    def basis(self, axis: int, block: int = -1):
+        """(lam, W, kind, lo) of a block (or the global, block=-1) basis: A W = M W diag(lam)."""
+        n, kind, lo = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(_lib.lfds_get_basis(self._h, axis, block, ctypes.byref(n), ctypes.byref(kind), ctypes.byref(lo),
+                                   None, None))
+        lam = np.empty(n.value, np.complex128)
+        W = np.empty((n.value, n.value), np.complex128)
+        _check(_lib.lfds_get_basis(self._h, axis, block, None, None, None, lam.ctypes.data_as(_P),
+                                   W.ctypes.data_as(_P)))
+        return lam, W, kind.value, lo.value
+
+    # ------------------------------------------------------------------ compute
+    def _torch(self):
+        import torch
+        return torch
+
+    def workspace(self, nrhs: int, host: bool = False):
+        torch = self._torch()
+        key = (nrhs, host)
+        nb = self.workspace_bytes_host(nrhs) if host else self.workspace_bytes(nrhs)
+        if nb == 0:
+            raise LfdsError(5, _lib.lfds_last_error().decode() or "workspace query failed")
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nb:
+            ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            self._ws[key] = ws
+        return ws
+
+    def _fdtype(self):
+        torch = self._torch()
+        return torch.float64 if self.dtype == LFDS_F64 else torch.complex128
+
+    def solve(self, f, out=None, stream=None):
+        """u = A^{-1} M f for f of shape (nrhs, nz, ny, nx) or (nz, ny, nx), on the device."""
+        torch = self._torch()
+        single = f.dim() == 3
+        F = f.unsqueeze(0) if single else f
+        if not (F.is_cuda and F.is_contiguous() and F.dtype == self._fdtype()):
+            raise ValueError(f"f must be a contiguous CUDA {self._fdtype()} tensor")
+        if tuple(F.shape[1:]) != self.shape:
+            raise ValueError(f"f shape {tuple(F.shape)} does not match grid {self.shape}")
+        nrhs = F.shape[0]
+        U = torch.empty_like(F) if out is None else (out.unsqueeze(0) if single else out)
+        ws = self.workspace(nrhs)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _check(_lib.lfds_solve(self._h, _P(F.data_ptr()), _P(U.data_ptr()), nrhs, _P(ws.data_ptr()),
+                               ws.numel(), _P(st)))
+        return U[0] if single else U
+
+    def solve_host(self, f_host, out=None, stream=None):
+        """End-to-end: host f (pinned CPU tensor) -> device -> solve -> host u."""
+        torch = self._torch()
+        single = f_host.dim() == 3
+        F = f_host.unsqueeze(0) if single else f_host
+        if F.is_cuda or not F.is_contiguous() or F.dtype != self._fdtype():
+            raise ValueError("f_host must be a contiguous CPU tensor of the plan dtype")
+        nrhs = F.shape[0]
+        U = torch.empty_like(F, pin_memory=F.is_pinned()) if out is None else (out.unsqueeze(0) if single else out)
+        ws = self.workspace(nrhs, host=True)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _check(_lib.lfds_solve_host(self._h, _P(F.data_ptr()), _P(U.data_ptr()), nrhs, _P(ws.data_ptr()),
+                                    ws.numel(), _P(st)))
+        return U[0] if single else U
+
+    def residual(self, u, f=None, dd: bool = True, stream=None):
+        """(r, norms): r = M f - A u (complex128), norms[r] = (||r||_2, ||M f||_2)."""
+        torch = self._torch()
+        single = u.dim() == 3
+        U = u.unsqueeze(0) if single else u
+        F = None if f is None else (f.unsqueeze(0) if single else f)
+        nrhs = U.shape[0]
+        r = torch.empty(U.shape, dtype=torch.complex128, device=U.device)
+        norms = np.zeros(2 * nrhs, np.float64)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _check(_lib.lfds_residual(self._h, _P(U.data_ptr()), None if F is None else _P(F.data_ptr()),
+                                  _P(r.data_ptr()), nrhs, int(dd), norms.ctypes.data_as(_P), _P(st)))
+        return (r[0] if single else r), norms.reshape(nrhs, 2)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lfds_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def setup_grid(hx, hy, hz, sigma_node, sigma_edge, lam, iface_x=(), iface_y=(), **kw) -> Plan:
+    """Python name of lfds_setup_grid."""
+    return Plan(hx, hy, hz, sigma_node, sigma_edge, lam, iface_x, iface_y, **kw)

@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): ||u_gpu - u_ref|| / ||u_ref|| <= 1e-9 (complex128) and relative
+residual ||A u - M f|| / ||M f|| <= 1e-10 on well-conditioned cases.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import make_problem, shrunken
+from workloads.configs import Problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _lib():
+    from paper_1909_01299_b200 import Plan
+    return Plan
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def gpu_solve(p, F, **kw):
+    Plan = _lib()
+    plan = Plan.from_problem(p, **kw)
+    dt = torch.float64 if p.real else torch.complex128
+    f = torch.from_numpy(np.ascontiguousarray(F)).to(device="cuda", dtype=dt)
+    u = plan.solve(f)
+    torch.cuda.synchronize()
+    return plan, u.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_shrunken_configs_single_pass(name):
+    """Two-level GPU solve vs oracle (i) sparse LU, no refinement."""
+    p = shrunken(name)
+    F = p.rhs_all()
+    plan, U = gpu_solve(p, F)
+    for r in range(p.nrhs):
+        ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[r]))
+        assert rel(U[r], ref) < TOL, (name, r, rel(U[r], ref))
+        assert oracle.rel_residual(p, U[r], F[r], np.clongdouble) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_shrunken_refined(name):
+    p = shrunken(name)
+    F = p.rhs_all()
+    plan, U = gpu_solve(p, F, refine=-1, refine_tol=1e-15)
+    rep = plan.report()
+    assert rep["passes"] >= 1
+    for r in range(p.nrhs):
+        ref = oracle.solve(p, F[r])
+        assert rel(U[r], ref) < 1e-12
+        assert oracle.rel_residual(p, U[r], F[r], np.clongdouble) < 1e-14
+
+
+def test_single_block_is_global_separable_solve():
+    p = shrunken("c3").with_partition([], [])
+    F = p.rhs_all()
+    _, U = gpu_solve(p, F)
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
+    assert rel(U[0], ref) < TOL
+
+
+def test_partition_independence_and_one_axis_split():
+    p = shrunken("c5")
+    F = p.rhs(0)[None]
+    _, U1 = gpu_solve(p, F)
+    _, U2 = gpu_solve(p.with_partition([7, 19, 33], []), F)
+    _, U3 = gpu_solve(p.with_partition([], [11, 30]), F)
+    assert rel(U2[0], U1[0]) < TOL and rel(U3[0], U1[0]) < TOL
+
+
+def test_multi_rhs_chunking_matches_batched():
+    p = shrunken("c5", nrhs=5)
+    F = p.rhs_all()
+    _, U1 = gpu_solve(p, F)
+    _, U2 = gpu_solve(p, F, rhs_chunk=2)
+    for r in range(5):
+        assert rel(U2[r], U1[r]) < 1e-14
+        ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[r]))
+        assert rel(U1[r], ref) < TOL
+
+
+def test_solve_host_matches_device():
+    Plan = _lib()
+    p = shrunken("c2")
+    F = p.rhs_all()
+    plan = Plan.from_problem(p)
+    f_host = torch.from_numpy(F).pin_memory()
+    u_host = plan.solve_host(f_host)
+    _, U = gpu_solve(p, F)
+    assert rel(u_host.numpy(), U) < 1e-15
+
+
+def test_residual_kernel_matches_oracle_stencil():
+    Plan = _lib()
+    p = shrunken("c4")
+    plan = Plan.from_problem(p)
+    rng = np.random.default_rng(4)
+    u = rng.standard_normal(p.shape) + 1j * rng.standard_normal(p.shape)
+    f = p.rhs(0)
+    ut = torch.from_numpy(u).cuda()
+    ft = torch.from_numpy(f).cuda()
+    for dd in (False, True):
+        r, norms = plan.residual(ut, ft, dd=dd)
+        ref = oracle.mass_rhs(p, f) - oracle.apply_stencil(p, u)
+        assert rel(r.cpu().numpy(), ref) < 1e-14
+        assert abs(norms[0, 0] / np.linalg.norm(ref) - 1) < 1e-12
+
+
+@pytest.mark.parametrize("nz", [1, 2, 3, 33, 70])
+def test_edge_sizes(nz):
+    """Degenerate and ragged z sizes (identity padding rows in the warp solver), blocks of 1 node."""
+    rng = np.random.default_rng(nz)
+    nx, ny = 9, 7
+    hx = rng.uniform(0.5, 2, nx + 1) + 0.3j * rng.uniform(0, 1, nx + 1)
+    hy = rng.uniform(0.5, 2, ny + 1)
+    hz = rng.uniform(0.5, 2, nz + 1)
+    se = rng.uniform(0.3, 3, nz + 1)
+    k = np.arange(1, nz + 1)
+    sn = (hz[k - 1] * se[k - 1] + hz[k] * se[k]) / (hz[k - 1] + hz[k])
+    p = Problem(name="edge", hx=hx.astype(complex), hy=hy.astype(complex), hz=hz.astype(complex),
+                sigma_edge=se.astype(complex), sigma_node=sn.astype(complex), lam=0.2, iface_x=[2, 4, 8],
+                iface_y=[3], nrhs=1, real=False, _rhs=None)
+    F = (rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape))
+    _, U = gpu_solve(p, F)
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
+    assert rel(U[0], ref) < TOL
+
+
+def test_zero_rhs_gives_zero():
+    p = shrunken("c3")
+    _, U = gpu_solve(p, np.zeros((1,) + p.shape, complex))
+    assert np.abs(U).max() == 0.0
+
+
+def test_bad_partition_raises():
+    from paper_1909_01299_b200 import LfdsError
+    p = shrunken("c3")
+    with pytest.raises(LfdsError):
+        _lib().from_problem(p.with_partition([5, 6], []))
+    with pytest.raises(LfdsError):
+        _lib().from_problem(p.with_partition([1], []))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_full_size_configs_vs_oracle(name):
+    """Full BASELINE.json sizes (c1-c3): GPU vs oracle (ii) with refinement, element by element."""
+    p = make_problem(name)
+    F = p.rhs_all()
+    plan, U = gpu_solve(p, F, refine=(-1 if name == "c2" else 0))
+    ref = oracle.solve(p, F[0])
+    assert rel(U[0], ref) < TOL, rel(U[0], ref)
