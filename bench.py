@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark: unknowns solved per second of the blocked separable Helmholtz solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One *step* = one lfds_solve of the whole hot path (steps 1-7 of PAPER.md:63-73, plus the
+refinement passes the config needs) over one batch of right-hand sides already resident
+in HBM.  Default workload: BASELINE.json configs[3] ("c4", 1024 x 1024 x 256, 8 x 8
+blocks, complex128) — the largest config, the one north_star's roofline and scaling
+targets are quoted on; it fits one GPU (4.3 GB per array, larger than the 126 MB L2, so
+no L2 flush is needed between steps).  N > 1 (torchrun): every rank solves its own
+right-hand side of the same grid (RHS sharding: independent problems, no data-path
+collective, "scaling": "weak"); the time is the max over ranks.
+
+The reference arm (--impl reference) is the CPU oracle (oracle/, test infrastructure) on
+the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import make_problem  # noqa: E402
+
+METRIC = "unknowns solved/sec (complex128 direct solve)"
+UNIT = "unknowns/s"
+# refinement passes each config needs for the 1e-9 parity bar: C2's BJ-fixed
+# quadratic PML profile has cond(V) ~ 1e5 -> one refinement pass; the others need none.
+REFINE = {"c1": 0, "c2": 1, "c3": 0, "c4": 0, "c5": 0}
+# FP64 peaks: derived 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 TF/s;
+# measured on this pool (profiles/r01_fp64_peaks.log): DMMA 37.1, DFMA 34.2 TF/s.
+FP64_PEAK_TFLOPS = 37.2
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mp = json.load(fh)
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def sample_problem(p, nz_sample: int):
+    """The same x/y grid, partition, lambda and sigma recipe with N_z reduced (CPU sample)."""
+    from workloads.configs import sigma_layers
+    nz = p.nz
+    # keep the layer structure: resample the cell -> layer map onto nz_sample + 1 cells
+    layer_vals = []
+    for c in range(nz + 1):
+        v = complex(p.sigma_edge[c]).real
+        if not layer_vals or layer_vals[-1] != v:
+            layer_vals.append(v)
+    hz, se, sn = sigma_layers(nz_sample, np.array(layer_vals))
+    rng = np.random.default_rng(np.random.SeedSequence([1909, 1299, 900, nz_sample]))
+    shape = (nz_sample, p.ny, p.nx)
+
+    def rhs(r):
+        out = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / math.sqrt(2)
+        return out
+
+    return dataclasses.replace(p, hz=hz, sigma_edge=se, sigma_node=sn, nrhs=1, _rhs=rhs,
+                               name=p.name + f"_nz{nz_sample}")
+
+
+def cpu_oracle_sample(p, nz_sample: int, steps: int = 1):
+    """Time the oracle's global separable solve (ii) (setup excluded) on the sample."""
+    import oracle
+    from oracle.solve import global_bases
+    ps = sample_problem(p, nz_sample)
+    g = global_bases(ps)
+    f = ps.rhs(0)
+    b = oracle.mass_rhs(ps, f)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.solve_separable(ps, b, g)
+        times.append(time.perf_counter() - t0)
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    return ps, times, threads
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def stage_algorithmic(p, R: int):
+    """Algorithmic FLOPs and bytes per stage (DESIGN.md §5 table)."""
+    def sizes(n, iface):
+        cuts = [0] + list(iface) + [n + 1]
+        return [cuts[i + 1] - cuts[i] - 1 for i in range(len(cuts) - 1)]
+    bx, by = sizes(p.nx, p.iface_x), sizes(p.ny, p.iface_y)
+    nz = p.nz
+    fl_x = sum(8.0 * nx * nx * ny * nz * R for nx in bx for ny in by)
+    fl_y = sum(8.0 * ny * ny * nx * nz * R for nx in bx for ny in by)
+    el_blk = sum(nx * ny * nz * R for nx in bx for ny in by)
+    el_all = p.nx * p.ny * nz * R
+    nif = len(p.iface_x) + len(p.iface_y)
+    return {
+        "step1_x_forward": ("tensor", fl_x, 32.0 * el_blk),
+        "step1_y_forward": ("tensor", fl_y, 32.0 * el_blk),
+        "step2_zsolve": ("hbm", None, 32.0 * el_blk),
+        "step5_global_zsolve": ("hbm", 8.0 * nif * el_all, 16.0 * el_all),
+        "step5_projection": ("hbm", 8.0 * nif * el_all, 32.0 * el_all),
+        "step6_zsolve_lift": ("hbm", None, 32.0 * el_blk),
+        "step7_y_inverse": ("tensor", fl_y, 32.0 * el_blk),
+        "step7_x_inverse": ("tensor", fl_x, 32.0 * el_blk),
+    }
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    p = make_problem(args.config)
+    nz_s = args.cpu_nz
+    ps, ts, threads = cpu_oracle_sample(p, nz_s, args.warmup + args.steps)
+    t = statistics.mean(ts[args.warmup:])
+    val = ps.unknowns / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": args.config, "sample": f"{p.name} with N_z={nz_s} (same x/y grid, blocks, lambda, "
+                   f"sigma layers), 1 RHS, oracle (ii) solve only", "nx": p.nx, "ny": p.ny, "nz": nz_s},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"{p.name} x/y grid with N_z={nz_s}: {ps.unknowns} unknowns per step"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1909_01299_b200 import Plan
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p = make_problem(args.config)
+    # RHS sharding: rank r solves right-hand sides [r*nrhs, (r+1)*nrhs) of the same grid
+    nrhs = p.nrhs if args.nrhs <= 0 else args.nrhs
+    pw = dataclasses.replace(p, nrhs=nrhs * world)
+    refine = REFINE.get(args.config, 0) if args.refine is None else args.refine
+    t0 = time.perf_counter()
+    plan = Plan.from_problem(p, device=local_rank, refine=refine, profile=True)
+    setup_s = time.perf_counter() - t0
+    info = plan.info()
+    dt = torch.float64 if p.real else torch.complex128
+    host = np.stack([pw.rhs(rank * nrhs + r) for r in range(nrhs)])
+    f = torch.from_numpy(host).to(device=dev, dtype=dt)
+    u = torch.empty_like(f)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.solve(f, out=u)
+    torch.cuda.synchronize()
+    plan.stage_times()  # reset
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.solve(f, out=u)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    stages = plan.stage_times()
+    launches_per_step = plan.report()["n_kernel_launches"]
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    units = p.unknowns * nrhs * world
+    value = units / (ms_max * 1e-3)
+    # correctness of what was timed: relative residual in double-double
+    _, norms = plan.residual(u, f, dd=True)
+    rel_res = float(max(norms[:, 0] / norms[:, 1]))
+    # e2e: host (pinned) buffers through lfds_solve_host, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        fh = torch.from_numpy(host).to(dtype=dt).pin_memory()
+        uh = torch.empty_like(fh).pin_memory()
+        plan.solve_host(fh, out=uh)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        k2 = max(1, min(args.steps, 3))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k2):
+            plan.solve_host(fh, out=uh)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / k2], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        nbytes = fh.numel() * fh.element_size()
+        e2e = {"value": units / (float(t.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item())}
+    # roofline of the dominant stage
+    alg = stage_algorithmic(p, nrhs)
+    hbm_peak, hbm_src = _peaks()
+    dom = max(stages.items(), key=lambda kv: kv[1][0])
+    name, (st_ms, st_launch) = dom
+    per_launch_ms = st_ms / max(1, args.steps)
+    kind, flops, nbytes = alg.get(name, ("hbm", None, None))
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
+            traffic = json.load(fh_).get(args.config, {}).get(name)
+    except Exception:
+        pass
+    if kind == "tensor" and flops:
+        achieved = flops / (per_launch_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "kernel": name,
+                "peak_source": "FP64 derived from unit counts x max clock (DESIGN.md §5); DMMA measured 37.1"}
+    else:
+        achieved = (nbytes or 0) / (per_launch_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "kernel": name,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
+    roof["stage_ms_per_step"] = {k: v[0] / max(1, args.steps) for k, v in stages.items() if v[1]}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ps, ts, threads = cpu_oracle_sample(p, args.cpu_nz, 1)
+        cpu = {"value": ps.unknowns / ts[0], "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"{p.name} x/y grid, N_z={args.cpu_nz}, 1 RHS, oracle (ii) solve only "
+                         f"({ps.unknowns} unknowns, {ts[0]:.1f} s)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128" if not p.real else "f64", "data": "synthetic",
+            "config": {"workload": args.config, "nx": p.nx, "ny": p.ny, "nz": p.nz,
+                       "blocks": [len(p.iface_x) + 1, len(p.iface_y) + 1], "nrhs_per_gpu": nrhs,
+                       "refine_passes": refine, "parallelism": f"rhs-sharded x{world}" if world > 1 else "1 gpu",
+                       "l2": "inputs larger than L2 (no flush)" if p.unknowns * 16 > 126e6 else "L2-resident",
+                       "setup_s": setup_s, "rel_residual_dd": rel_res},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nrhs", type=int, default=0, help="RHS per GPU (0 = the config's)")
+    ap.add_argument("--refine", type=int, default=None)
+    ap.add_argument("--cpu-nz", type=int, default=16, dest="cpu_nz")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

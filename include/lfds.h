@@ -58,6 +58,7 @@ typedef struct {
   int residual_dd;  /* 1: refinement residual in double-double (reading R13), 0: fp64      */
   int device;       /* CUDA device ordinal; <0 = host-only plan (setup/basis queries only) */
   int rhs_chunk;    /* max right-hand sides processed per pipeline pass (0 = all)          */
+  int profile;      /* 1: record CUDA events around every stage on the solve stream        */
 } lfds_options;
 
 /* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0. */
@@ -144,6 +145,16 @@ int lfds_get_info(const lfds_plan* plan, lfds_info* info);
  */
 int lfds_get_basis(const lfds_plan* plan, int axis, int block, int* n, int* kind, int* lo,
                    lfds_z* lam, lfds_z* W);
+
+/*
+ * Stage timing (options.profile = 1): device milliseconds per pipeline stage, measured with
+ * CUDA events recorded on the solve stream around each stage, accumulated over all solves
+ * since the previous call (which this call resets; it synchronises those events).
+ * ms[i] and launches[i] for i < lfds_stage_count(); names from lfds_stage_name(i).
+ */
+int lfds_stage_count(void);
+const char* lfds_stage_name(int stage);
+int lfds_stage_times(lfds_plan* plan, double* ms, int* launches);
 
 void lfds_destroy(lfds_plan* plan);
 const char* lfds_last_error(void);

@@ -65,6 +65,25 @@ struct Axis {
   int64_t Wg = 0, lamg = 0, WI = 0, hoff = 0, hhoff = 0;
 };
 
+enum Stage { ST_X1, ST_Y1, ST_Z1, ST_EDGE, ST_IFRES, ST_GFWD, ST_GSWEEP, ST_GPROJ, ST_GPLANE, ST_FACE, ST_Z2, ST_Y7,
+             ST_X7, ST_WRITE, ST_RESID, ST_AXPY, ST_COUNT };
+const char* kStageNames[ST_COUNT] = {
+    "step1_x_forward", "step1_y_forward", "step2_zsolve", "step3_edge_values", "step4_iface_residual",
+    "step5_global_forward", "step5_global_zsolve", "step5_projection", "step5_plane_inverse", "step6_face_transform",
+    "step6_zsolve_lift", "step7_y_inverse", "step7_x_inverse", "step7_write_iface", "refine_residual", "refine_axpy"};
+
+struct Profiler {
+  struct Rec { int stage, launches; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double ms[ST_COUNT] = {0};
+  int launches[ST_COUNT] = {0};
+  cudaEvent_t get() {
+    if (pool.empty()) { cudaEvent_t e; cudaEventCreate(&e); return e; }
+    cudaEvent_t e = pool.back(); pool.pop_back(); return e;
+  }
+};
+
 struct StageDescs {
   int64_t off = 0;  // index of the first desc in the device desc array
   int n = 0, maxM = 0;
@@ -101,6 +120,7 @@ struct lfds_plan {
   lfds_report report{};
   lfds_info info{};
   int launches = 0;
+  Profiler prof;
 };
 
 namespace {
@@ -199,92 +219,81 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     }
   };
   const int inF = in_real ? G_BREAL : 0, outF = out_real ? G_CREAL : 0;
+  const int64_t RZ = (int64_t)R * Nz;  // merged (r, k) row index
   std::vector<GemmDesc> v;
-  // step 1: x-forward per block, then y-forward per (block, r) into [r][m][l][k]
+  // Layouts (complex elements): T1 and MS per block [r][k][q|m][l] (l fastest), so a block's
+  // mode space is [rk][m][l] and every z-line (fixed m, l) is strided by nx*ny.
+  // step 1: x-forward  T1[rk][q][l] = sum_p F_x[l][p] f[rk][y0+q][x0+p]
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
       int b = j * nbx + i;
       v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_F, (int64_t)(by.lo - 1) * Nx + (bx.lo - 1), 1, (int64_t)Nx * Ny, Nx,
-                     B_T1, t1[b], 1, (int64_t)by.n * bx.n, bx.n, R * Nz, by.n, inF));
+                     B_T1, t1[b], 1, (int64_t)by.n * bx.n, bx.n, (int)RZ, by.n, inF));
     }
   stage(pp.s1x, std::move(v)); v.clear();
+  //         y-forward  MS[rk][m][l] = sum_q F_y[m][q] T1[rk][q][l]
   for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i)
-      for (int r = 0; r < R; ++r) {
-        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
-        int b = j * nbx + i;
-        int64_t vol = (int64_t)bx.n * by.n * Nz;
-        v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_T1, t1[b] + r * vol, bx.n, (int64_t)bx.n * by.n, 1, B_MS,
-                       ms[b] + r * vol, (int64_t)bx.n * Nz, 1, Nz, Nz, bx.n, 0));
-      }
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+      int b = j * nbx + i;
+      const int64_t pl = (int64_t)bx.n * by.n;
+      v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_T1, t1[b], bx.n, pl, 1, B_MS, ms[b], bx.n, pl, 1, (int)RZ, bx.n, 0));
+    }
   stage(pp.s1y, std::move(v)); v.clear();
-  // step 3: G[b][r][e][m][k] = sum_l Wx[e_row, l] v~[r][m][l][k];  H[b][r][e][l][k] = sum_m Wy[e_row, m] v~
+  // step 3: G[b][e][rk][m] = sum_l W_x[e_row][l] v~[rk][m][l];  H[b][e][rk][l] = sum_m W_y[e_row][m] v~[rk][m][l]
   for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i)
-      for (int r = 0; r < R; ++r) {
-        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
-        int b = j * nbx + i;
-        int64_t vol = (int64_t)bx.n * by.n * Nz;
-        v.push_back(gd(bx.W, (int64_t)(bx.n - 1) * bx.n, 1, 2, bx.n, B_MS, ms[b] + r * vol, Nz, (int64_t)bx.n * Nz, 1,
-                       B_IF, pp.g_off + ((int64_t)b * R + r) * 2 * P->mpad * Nz, (int64_t)P->mpad * Nz, Nz, 1, by.n,
-                       Nz, 0));
-      }
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+      int b = j * nbx + i;
+      const int64_t pl = (int64_t)bx.n * by.n;
+      v.push_back(gd(bx.W, (int64_t)(bx.n - 1) * bx.n, 1, 2, bx.n, B_MS, ms[b], 1, pl, bx.n, B_IF,
+                     pp.g_off + (int64_t)b * 2 * RZ * P->mpad, RZ * P->mpad, P->mpad, 1, (int)RZ, by.n, 0));
+    }
   stage(pp.s3g, std::move(v)); v.clear();
   for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i)
-      for (int r = 0; r < R; ++r) {
-        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
-        int b = j * nbx + i;
-        int64_t vol = (int64_t)bx.n * by.n * Nz;
-        v.push_back(gd(by.W, (int64_t)(by.n - 1) * by.n, 1, 2, by.n, B_MS, ms[b] + r * vol, (int64_t)bx.n * Nz, Nz, 1,
-                       B_IF, pp.h_off + ((int64_t)b * R + r) * 2 * P->lpad * Nz, (int64_t)P->lpad * Nz, Nz, 1, bx.n,
-                       Nz, 0));
-      }
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+      int b = j * nbx + i;
+      const int64_t pl = (int64_t)bx.n * by.n;
+      v.push_back(gd(by.W, (int64_t)(by.n - 1) * by.n, 1, 2, by.n, B_MS, ms[b], bx.n, pl, 1, B_IF,
+                     pp.h_off + (int64_t)b * 2 * RZ * P->lpad, RZ * P->lpad, P->lpad, 1, (int)RZ, bx.n, 0));
+    }
   stage(pp.s3h, std::move(v)); v.clear();
-  // VX[b][r][e][k][q] = sum_m Wy[q,m] G[..][e][m][k];  VY[b][r][e][k][p] = sum_l Wx[p,l] H[..][e][l][k]
+  // VX[b][e][rk][q] = sum_m W_y[q][m] G[b][e][rk][m];  VY[b][e][rk][p] = sum_l W_x[p][l] H[b][e][rk][l]
   for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i)
-      for (int r = 0; r < R; ++r) {
-        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
-        int b = j * nbx + i;
-        v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_IF, pp.g_off + ((int64_t)b * R + r) * 2 * P->mpad * Nz, Nz,
-                       (int64_t)P->mpad * Nz, 1, B_IF, pp.vx_off + ((int64_t)b * R + r) * 2 * Nz * P->mpad, 1,
-                       (int64_t)Nz * P->mpad, P->mpad, 2, Nz, 0));
-      }
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock& by = Y.blocks[j];
+      int b = j * nbx + i;
+      v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_IF, pp.g_off + (int64_t)b * 2 * RZ * P->mpad, 1, P->mpad, 0, B_IF,
+                     pp.vx_off + (int64_t)b * 2 * RZ * P->mpad, 1, P->mpad, 0, (int)(2 * RZ), 1, 0));
+    }
   stage(pp.s3x, std::move(v)); v.clear();
   for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i)
-      for (int r = 0; r < R; ++r) {
-        const AxisBlock &bx = X.blocks[i];
-        int b = j * nbx + i;
-        v.push_back(gd(bx.W, bx.n, 1, bx.n, bx.n, B_IF, pp.h_off + ((int64_t)b * R + r) * 2 * P->lpad * Nz, Nz,
-                       (int64_t)P->lpad * Nz, 1, B_IF, pp.vy_off + ((int64_t)b * R + r) * 2 * Nz * P->lpad, 1,
-                       (int64_t)Nz * P->lpad, P->lpad, 2, Nz, 0));
-      }
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock& bx = X.blocks[i];
+      int b = j * nbx + i;
+      v.push_back(gd(bx.W, bx.n, 1, bx.n, bx.n, B_IF, pp.h_off + (int64_t)b * 2 * RZ * P->lpad, 1, P->lpad, 0, B_IF,
+                     pp.vy_off + (int64_t)b * 2 * RZ * P->lpad, 1, P->lpad, 0, (int)(2 * RZ), 1, 0));
+    }
   stage(pp.s3y, std::move(v)); v.clear();
-  // step 5: R1 = W_y^T RX, R2 = W_x^T RY  (b-units: no mass)
-  if (nifx) v.push_back(gd(Y.Wg, 1, Ny, Ny, Ny, B_IF, pp.rx, 1, (int64_t)Nz * Ny, Ny, B_IF, pp.r1, Nz, (int64_t)Ny * Nz, 1,
-                           nifx * R, Nz, 0));
+  // step 5: R1[a][rk][m] = sum_q W_y[q][m] RX[a][rk][q];  R2[b][rk][l] = sum_p W_x[p][l] RY[b][rk][p]  (b-units)
+  if (nifx) v.push_back(gd(Y.Wg, 1, Ny, Ny, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
   stage(pp.s5r1, std::move(v)); v.clear();
-  if (nify) v.push_back(gd(X.Wg, 1, Nx, Nx, Nx, B_IF, pp.ry, 1, (int64_t)Nz * Nx, Nx, B_IF, pp.r2, Nz, (int64_t)Nx * Nz, 1,
-                           nify * R, Nz, 0));
+  if (nify) v.push_back(gd(X.Wg, 1, Nx, Nx, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2, 1, Nx, 0, (int)(nify * RZ), 1, 0));
   stage(pp.s5r2, std::move(v)); v.clear();
-  // P1[a][r][m][k] = sum_l Wx[I_a, l] W^[r][m][l][k];  P2[b][r][l][k] = sum_m Wy[I_b, m] W^[r][m][l][k]
-  if (nifx) v.push_back(gd(X.WI, Nx, 1, nifx, Nx, B_T1, 0, Nz, (int64_t)Nx * Nz, 1, B_IF, pp.p1, (int64_t)R * Ny * Nz, Nz, 1,
-                           R * Ny, Nz, 0));
+  // P1[a][rk][m] = sum_l W_x[I_a][l] W^[rk][m][l];  P2[b][rk][l] = sum_m W_y[I_b][m] W^[rk][m][l]
+  if (nifx) v.push_back(gd(X.WI, Nx, 1, nifx, Nx, B_T1, 0, 1, Nx, 0, B_IF, pp.p1, RZ * Ny, 1, 0, (int)(RZ * Ny), 1, 0));
   stage(pp.s5p1, std::move(v)); v.clear();
-  if (nify) v.push_back(gd(Y.WI, Ny, 1, nify, Ny, B_T1, 0, (int64_t)Nx * Nz, (int64_t)Ny * Nx * Nz, 1, B_IF, pp.p2,
-                           (int64_t)R * Nx * Nz, (int64_t)Nx * Nz, 1, R, Nx * Nz, 0));
+  if (nify) v.push_back(gd(Y.WI, Ny, 1, nify, Ny, B_T1, 0, Nx, (int64_t)Ny * Nx, 1, B_IF, pp.p2, RZ * Nx, Nx, 1,
+                           (int)RZ, Nx, 0));
   stage(pp.s5p2, std::move(v)); v.clear();
-  // w on the planes: WX[a][r][k][q] = sum_m Wy[q,m] P1[a][r][m][k];  WY[b][r][k][p] = sum_l Wx[p,l] P2[b][r][l][k]
-  if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, Nz, (int64_t)Ny * Nz, 1, B_IF, pp.wx, 1, (int64_t)Nz * Ny, Ny,
-                           nifx * R, Nz, 0));
+  // w on the planes: WX[a][rk][q] = sum_m W_y[q][m] P1[a][rk][m];  WY[b][rk][p] = sum_l W_x[p][l] P2[b][rk][l]
+  if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, 1, Ny, 0, B_IF, pp.wx, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
   stage(pp.s5wx, std::move(v)); v.clear();
-  if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, Nz, (int64_t)Nx * Nz, 1, B_IF, pp.wy, 1, (int64_t)Nz * Nx, Nx,
-                           nify * R, Nz, 0));
+  if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, 1, Nx, 0, B_IF, pp.wy, 1, Nx, 0, (int)(nify * RZ), 1, 0));
   stage(pp.s5wy, std::move(v)); v.clear();
-  // step 6: face transforms GF[b][face][r][mode][k] (faces L, R, B, T)
+  // step 6: face transforms GF[b][face][rk][mode] (faces L, R, B, T), e.g. GL = F_y w_L
   std::vector<ZBlock> zb(nblk);
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
@@ -301,60 +310,47 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
       z.wy0 = by.W;
       z.wy1 = by.W + (int64_t)(by.n - 1) * by.n;
       z.gL = z.gR = z.gB = z.gT = -1;
+      z.fstride = P->fpad;
       z.cL = z.cR = z.cB = z.cT = make_double2(0, 0);
-      auto face_off = [&](int face) { return pp.gf + ((int64_t)b * 4 + face) * R * P->fpad * Nz; };
+      auto face_off = [&](int face) { return pp.gf + ((int64_t)b * 4 + face) * RZ * P->fpad; };
       const int x1 = bx.lo + bx.n - 1, y1 = by.lo + by.n - 1;
-      if (i > 0) {  // left face: x-interface a = i-1 at node bx.lo-1
-        int a = i - 1;
-        v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_IF, pp.wx + (int64_t)a * R * Nz * Ny + (by.lo - 1), 1, (int64_t)Nz * Ny,
-                       Ny, B_IF, face_off(0), Nz, (int64_t)by.n * Nz, 1, R, Nz, 0));
-        z.gL = face_off(0);
-        zc c = 1.0 / X.h[bx.lo - 1];
-        z.cL = make_double2(c.real(), c.imag());
+      // x faces: GL[rk][m] = sum_q F_y[m][q] WX[a][rk][y0+q]
+      for (int side = 0; side < 2; ++side) {
+        if (side == 0 ? i == 0 : i == nbx - 1) continue;
+        const int a = side == 0 ? i - 1 : i;
+        v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_IF, pp.wx + (int64_t)a * RZ * Ny + (by.lo - 1), 1, Ny, 0, B_IF,
+                       face_off(side), 1, P->fpad, 0, (int)RZ, 1, 0));
+        zc c = 1.0 / X.h[side == 0 ? bx.lo - 1 : x1];
+        if (side == 0) { z.gL = face_off(0); z.cL = make_double2(c.real(), c.imag()); }
+        else { z.gR = face_off(1); z.cR = make_double2(c.real(), c.imag()); }
       }
-      if (i < nbx - 1) {  // right face: interface a = i at node x1+1
-        int a = i;
-        v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_IF, pp.wx + (int64_t)a * R * Nz * Ny + (by.lo - 1), 1, (int64_t)Nz * Ny,
-                       Ny, B_IF, face_off(1), Nz, (int64_t)by.n * Nz, 1, R, Nz, 0));
-        z.gR = face_off(1);
-        zc c = 1.0 / X.h[x1];
-        z.cR = make_double2(c.real(), c.imag());
-      }
-      if (j > 0) {
-        int bb = j - 1;
-        v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_IF, pp.wy + (int64_t)bb * R * Nz * Nx + (bx.lo - 1), 1,
-                       (int64_t)Nz * Nx, Nx, B_IF, face_off(2), Nz, (int64_t)bx.n * Nz, 1, R, Nz, 0));
-        z.gB = face_off(2);
-        zc c = 1.0 / Y.h[by.lo - 1];
-        z.cB = make_double2(c.real(), c.imag());
-      }
-      if (j < nby - 1) {
-        int bb = j;
-        v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_IF, pp.wy + (int64_t)bb * R * Nz * Nx + (bx.lo - 1), 1,
-                       (int64_t)Nz * Nx, Nx, B_IF, face_off(3), Nz, (int64_t)bx.n * Nz, 1, R, Nz, 0));
-        z.gT = face_off(3);
-        zc c = 1.0 / Y.h[y1];
-        z.cT = make_double2(c.real(), c.imag());
+      // y faces: GB[rk][l] = sum_p F_x[l][p] WY[b][rk][x0+p]
+      for (int side = 0; side < 2; ++side) {
+        if (side == 0 ? j == 0 : j == nby - 1) continue;
+        const int bb = side == 0 ? j - 1 : j;
+        v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_IF, pp.wy + (int64_t)bb * RZ * Nx + (bx.lo - 1), 1, Nx, 0, B_IF,
+                       face_off(2 + side), 1, P->fpad, 0, (int)RZ, 1, 0));
+        zc c = 1.0 / Y.h[side == 0 ? by.lo - 1 : y1];
+        if (side == 0) { z.gB = face_off(2); z.cB = make_double2(c.real(), c.imag()); }
+        else { z.gT = face_off(3); z.cT = make_double2(c.real(), c.imag()); }
       }
     }
   stage(pp.s6f, std::move(v)); v.clear();
-  // step 7: y-inverse [r][m][l][k] -> [r][k][q][l], x-inverse -> u
+  // step 7: y-inverse T1[rk][q][l] = sum_m W_y[q][m] MS[rk][m][l];  x-inverse u[rk][y0+q][x0+p] = sum_l W_x[p][l] T1
   for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i)
-      for (int r = 0; r < R; ++r) {
-        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
-        int b = j * nbx + i;
-        int64_t vol = (int64_t)bx.n * by.n * Nz;
-        v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_MS, ms[b] + r * vol, (int64_t)bx.n * Nz, Nz, 1, B_T1, t1[b] + r * vol,
-                       bx.n, 1, (int64_t)bx.n * by.n, bx.n, Nz, 0));
-      }
+    for (int i = 0; i < nbx; ++i) {
+      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+      int b = j * nbx + i;
+      const int64_t pl = (int64_t)bx.n * by.n;
+      v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_MS, ms[b], bx.n, pl, 1, B_T1, t1[b], bx.n, pl, 1, (int)RZ, bx.n, 0));
+    }
   stage(pp.s7y, std::move(v)); v.clear();
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
       int b = j * nbx + i;
       v.push_back(gd(bx.W, bx.n, 1, bx.n, bx.n, B_T1, t1[b], 1, (int64_t)by.n * bx.n, bx.n, B_U,
-                     (int64_t)(by.lo - 1) * Nx + (bx.lo - 1), 1, (int64_t)Nx * Ny, Nx, R * Nz, by.n, outF));
+                     (int64_t)(by.lo - 1) * Nx + (bx.lo - 1), 1, (int64_t)Nx * Ny, Nx, (int)RZ, by.n, outF));
     }
   stage(pp.s7x, std::move(v)); v.clear();
 
@@ -386,6 +382,22 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   const int nifx = (int)X.iface.size(), nify = (int)Y.iface.size();
   const int nblk = P->nbx * P->nby;
   double* minpiv = reinterpret_cast<double*>(bufs.p[B_RED]);
+  const bool prof = P->opt.profile != 0;
+  int cur_stage = -1, cur_launch0 = 0;
+  cudaEvent_t ev_a = nullptr;
+  auto begin = [&](int stg) {
+    cur_stage = stg;
+    cur_launch0 = P->launches;
+    if (prof) { ev_a = P->prof.get(); cudaEventRecord(ev_a, st); }
+  };
+  auto end = [&]() {
+    if (prof && cur_stage >= 0) {
+      cudaEvent_t b = P->prof.get();
+      cudaEventRecord(b, st);
+      P->prof.recs.push_back({cur_stage, P->launches - cur_launch0, ev_a, b});
+    }
+    cur_stage = -1;
+  };
   auto gemm = [&](const StageDescs& s) -> int {
     if (!s.n) return LFDS_OK;
     CUDA_TRY(launch_gemm(pp.d_descs + s.off, s.n, s.maxM, (int)std::min<int64_t>(s.maxN, INT32_MAX), 0, bufs, st));
@@ -394,15 +406,21 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   };
   int rc;
   // pass 1
+  begin(ST_X1);
   if ((rc = gemm(pp.s1x))) return rc;
+  end(); begin(ST_Y1);
   if ((rc = gemm(pp.s1y))) return rc;
+  end(); begin(ST_Z1);
   CUDA_TRY(launch_zsolve_block(1, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st));
   P->launches++;
+  end();
   if (nifx + nify > 0) {
+    begin(ST_EDGE);
     if ((rc = gemm(pp.s3g))) return rc;
     if ((rc = gemm(pp.s3h))) return rc;
     if ((rc = gemm(pp.s3x))) return rc;
     if ((rc = gemm(pp.s3y))) return rc;
+    end(); begin(ST_IFRES);
     // step 4
     IfaceRes ir{};
     ir.nx = Nx; ir.ny = Ny; ir.nz = Nz; ir.R = R; ir.nifx = nifx; ir.nify = nify; ir.dtype = in_dtype;
@@ -413,29 +431,41 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     ir.nbx = P->nbx; ir.nby = P->nby; ir.qpad = P->mpad; ir.ppad = P->lpad;
     CUDA_TRY(launch_iface_residual(ir, bufs, st));
     P->launches++;
+    end(); begin(ST_GFWD);
     // step 5
     if ((rc = gemm(pp.s5r1))) return rc;
     if ((rc = gemm(pp.s5r2))) return rc;
+    end(); begin(ST_GSWEEP);
     GSweep g{};
     g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
     g.lamx = X.lamg; g.lamy = Y.lamg; g.wxi = X.WI; g.wyi = Y.WI; g.r1 = pp.r1; g.r2 = pp.r2; g.what = 0;
     CUDA_TRY(launch_gsweep(g, P->zt_plain, bufs, minpiv, st));
     P->launches++;
+    end(); begin(ST_GPROJ);
     if ((rc = gemm(pp.s5p1))) return rc;
     if ((rc = gemm(pp.s5p2))) return rc;
+    end(); begin(ST_GPLANE);
     if ((rc = gemm(pp.s5wx))) return rc;
     if ((rc = gemm(pp.s5wy))) return rc;
+    end(); begin(ST_FACE);
     // step 6
     if ((rc = gemm(pp.s6f))) return rc;
+    end(); begin(ST_Z2);
     CUDA_TRY(launch_zsolve_block(2, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st));
     P->launches++;
+    end();
   }
   // step 7
+  begin(ST_Y7);
   if ((rc = gemm(pp.s7y))) return rc;
+  end(); begin(ST_X7);
   if ((rc = gemm(pp.s7x))) return rc;
+  end();
   if (nifx + nify > 0) {
+    begin(ST_WRITE);
     CUDA_TRY(launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st));
     P->launches++;
+    end();
   }
   return LFDS_OK;
 }
@@ -452,6 +482,31 @@ void lfds_default_options(lfds_options* o) {
   o->residual_dd = 1;
   o->device = 0;
   o->rhs_chunk = 0;
+  o->profile = 0;
+}
+
+int lfds_stage_count(void) { return ST_COUNT; }
+const char* lfds_stage_name(int i) { return (i >= 0 && i < ST_COUNT) ? kStageNames[i] : ""; }
+
+int lfds_stage_times(lfds_plan* P, double* ms, int* launches) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  for (auto& r : P->prof.recs) {
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float t = 0;
+    CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    P->prof.ms[r.stage] += t;
+    P->prof.launches[r.stage] += r.launches;
+    P->prof.pool.push_back(r.a);
+    P->prof.pool.push_back(r.b);
+  }
+  P->prof.recs.clear();
+  for (int i = 0; i < ST_COUNT; ++i) {
+    if (ms) ms[i] = P->prof.ms[i];
+    if (launches) launches[i] = P->prof.launches[i];
+    P->prof.ms[i] = 0;
+    P->prof.launches[i] = 0;
+  }
+  return LFDS_OK;
 }
 
 const char* lfds_last_error(void) { return g_err.c_str(); }
@@ -689,10 +744,13 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
       const int maxref = P->opt.refine < 0 ? 8 : P->opt.refine;
       for (int it = 0; it <= maxref; ++it) {
         CUDA_TRY(cudaMemsetAsync(norms, 0, sizeof(double) * 2 * Rc, st));
+        cudaEvent_t ra = nullptr;
+        if (P->opt.profile) { ra = P->prof.get(); cudaEventRecord(ra, st); }
         CUDA_TRY(launch_residual(X.N, Y.N, P->nz, Rc, dt, P->opt.residual_dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff,
                                  Y.hhoff, P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()),
                                  b.p[B_U], b.p[B_F], res, 1, norms, b, st));
         P->launches++;
+        if (P->opt.profile) { cudaEvent_t rb2 = P->prof.get(); cudaEventRecord(rb2, st); P->prof.recs.push_back({ST_RESID, 1, ra, rb2}); }
         std::vector<double> hn(2 * Rc);
         CUDA_TRY(cudaMemcpyAsync(hn.data(), norms, sizeof(double) * 2 * Rc, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
@@ -706,8 +764,11 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         rb.p[B_F] = res;
         rb.p[B_U] = res;
         if ((rc = run_pass(P, *pp_ref, rb, Rc, 0, 0, st))) return rc;
+        cudaEvent_t xa = nullptr;
+        if (P->opt.profile) { xa = P->prof.get(); cudaEventRecord(xa, st); }
         CUDA_TRY(launch_axpy_u(vol * Rc, dt, res, b.p[B_U], st));
         P->launches++;
+        if (P->opt.profile) { cudaEvent_t xb = P->prof.get(); cudaEventRecord(xb, st); P->prof.recs.push_back({ST_AXPY, 1, xa, xb}); }
         passes++;
       }
     }
@@ -826,6 +887,8 @@ void lfds_destroy(lfds_plan* P) {
     cudaFree(kv.second.d_zb);
   }
   if (P->d_tab) cudaFree(P->d_tab);
+  for (auto& r : P->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : P->prof.pool) cudaEventDestroy(e);
   delete P;
 }
 

@@ -40,13 +40,14 @@ struct ZTab {
 
 // One block for the block-pass z-solves.
 struct ZBlock {
-  int64_t ms_off;              // offset of this block's mode space [r][m][l][k] in B_MS
+  int64_t ms_off;              // offset of this block's mode space [r][k][m][l] in B_MS (and T1)
   int nx, ny;                  // interior sizes (modes)
   int64_t lamx, lamy;          // eigenvalue offsets in TAB
   // pass-2 lifting (reading R8): l~[l,m,k] = -sigma_k (cL Wx[0,l] GL[m,k] + cR Wx[n-1,l] GR[m,k]
   //                                               + cB Wy[0,m] GB[l,k] + cT Wy[n-1,m] GT[l,k])
   int64_t wx0, wx1, wy0, wy1;  // offsets in TAB of W rows (first / last interior node)
-  int64_t gL, gR, gB, gT;      // offsets in B_IF of the face transforms, [r][m or l][k]; -1 = none
+  int64_t gL, gR, gB, gT;      // offsets in B_IF of the face transforms, [r*nz + k][m or l]; -1 = none
+  int64_t fstride;             // row stride of the face-transform arrays
   double2 cL, cR, cB, cT;      // coupling coefficients 1/h across each face (0 at outer boundary)
 };
 
@@ -55,8 +56,8 @@ struct GSweep {
   int nx, ny, nifx, nify, nz, R;
   int64_t lamx, lamy;          // global eigenvalues (TAB)
   int64_t wxi, wyi;            // W_x[I_a, l] (nifx x nx), W_y[I_b, m] (nify x ny)  (TAB)
-  int64_t r1, r2;              // R1[a][r][m][k], R2[b][r][l][k]  (B_IF)
-  int64_t what;                // W^[r][m][l][k] output (B_T1)
+  int64_t r1, r2;              // R1[a][r][k][m], R2[b][r][k][l]  (B_IF)
+  int64_t what;                // W^[r][k][m][l] output (B_T1)
 };
 
 // Interface residual (step 4).
@@ -65,7 +66,7 @@ struct IfaceRes {
   int64_t ifx, ify;            // int arrays (device) of 1-based interface nodes
   int64_t hx, hy, hhx, hhy, hhz, sig;   // TAB offsets (steps, control volumes, sigma_k)
   int64_t rx, ry;              // out: RX[a][r][k][q] (all q), RY[b][r][k][p] (0 at p in I_x) (B_IF)
-  int64_t vxo, vyo;            // in: v at interface-adjacent nodes, see lfds_host.cpp
+  int64_t vxo, vyo;            // in: v next to the faces, VX[blk][e][r][k][qpad], VY[blk][e][r][k][ppad]
   int64_t blk_of_x, blk_of_y;  // int arrays: block index along the axis for each node (or -1)
   int64_t xlo, ylo;            // int arrays: first node of each block along the axis
   int nbx, nby;

@@ -3,9 +3,8 @@
 //  k_gemm          strided batched complex contraction: block forward/inverse transforms
 //                  (steps 1 and 7), interface-adjacent evaluation (step 3), sparse global
 //                  transforms (step 5), face transforms for the Dirichlet lifting (step 6).
-//  k_zsolve_block  per-mode z tridiagonal solves of a block pass (steps 2 and 6), one warp
-//                  per system: Thomas sweeps inside each lane's chunk of rows + parallel
-//                  cyclic reduction of the 2-per-lane interface system over warp shuffles.
+//  k_zsolve_block  per-mode z tridiagonal solves of a block pass (steps 2 and 6): one thread
+//                  per system, Thomas with shared-memory checkpoints of c' (coalesced rows).
 //  k_gsweep        step 5's global per-mode z-solves with the rank-|I| right-hand side
 //                  built on the fly from the transformed interface residual.
 //  k_iface_res     step 4: residual b - A v on the interface planes.
@@ -155,278 +154,220 @@ cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, 
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- warp tridiagonal solver
-// Solves a_k x_{k-1} + (g_k + s e_k) x_k + c_k x_{k+1} = d_k, k = 0..nz-1, one system per
-// warp; lane t owns rows t*K .. t*K+K-1 (rows >= nz are identity rows).  Each lane first
-// eliminates inside its chunk (a downward sweep expressing rows through the chunk's first
-// unknown, an upward sweep expressing the first row through the chunk's last unknown),
-// leaving a tridiagonal system of 2 unknowns per lane (64 total) that parallel cyclic
-// reduction solves in 6 shuffle levels; a back-substitution recovers the chunk interior.
-// No pivoting (reading R15); |pivot| / row-norm is monitored into minpiv.
-struct ZRow {
-  const double2 *a, *g, *c, *e;
+// ---------------------------------------------------------------- z tridiagonal solves
+// One thread per system ("split into multiple tridiagonal systems ... O(N_z)").
+// Mode space is [r][k][mode] (mode contiguous), so every row access of a warp is one
+// coalesced 512-byte transaction.  Thomas elimination without pivoting (reading R15):
+//   forward   r_k = b_k - a_k c'_{k-1},  c'_k = c_k / r_k,  d'_k = (d_k - a_k d'_{k-1}) / r_k
+//   backward  x_k = d'_k - c'_k x_{k+1}
+// d' is stored in place in the output line (it is overwritten by x on the way back);
+// c' is not stored: every ZSEG-th value is checkpointed in shared memory and the segment
+// is recomputed into registers for the backward pass.  |r_k| / row-norm is monitored.
+// The tridiagonal row k of T(s) = A_z + lambda M_z + s M_z^sigma is a_k, g_k + s e_k, c_k
+// (tables staged in shared memory; row-scaled tables for the block passes, reading R1).
+constexpr int ZSEG = 16;
+constexpr int ZTHREADS = 128;
+
+struct ZLine {
+  double2* out;     // d' / x storage (MS or T1)
+  int64_t stride;   // elements between consecutive k
 };
 
-template <int K>
-__device__ __forceinline__ void warp_tridiag(cplx (&d)[K], int nz, const ZRow& T, cplx s, int lane,
-                                             double& minpiv) {
-  const int k0 = lane * K;
-  cplx al[K], ga[K], de[K];
-  auto coef = [&](int j, cplx& a, cplx& b, cplx& c) {
-    int k = k0 + j;
-    if (k < nz) {
-      a = ld(T.a + k); c = ld(T.c + k);
-      b = cfma(s, ld(T.e + k), ld(T.g + k));
-    } else {
-      a = mk(0, 0); c = mk(0, 0); b = mk(1, 0);
-    }
-  };
-  // downward sweep, rows 1..K-1, left boundary x_s (= row 0 of the chunk)
-  {
-    cplx a, b, c;
-    coef(1, a, b, c);
-    double rn = cabs1(a) + cabs1(b) + cabs1(c);
-    minpiv = fmin(minpiv, cabs1(b) / rn);
-    cplx inv = cinv(b);
-    al[1] = a * inv; ga[1] = c * inv; de[1] = d[1] * inv;
-#pragma unroll
-    for (int j = 2; j < K; ++j) {
-      coef(j, a, b, c);
-      cplx r = b - a * ga[j - 1];
-      minpiv = fmin(minpiv, cabs1(r) / (cabs1(a) + cabs1(b) + cabs1(c)));
-      inv = cinv(r);
-      al[j] = -(a * al[j - 1]) * inv;
-      ga[j] = c * inv;
-      de[j] = (d[j] - a * de[j - 1]) * inv;
-    }
+template <class RHS, class STORE>
+__device__ __forceinline__ void thomas_line(int nz, const double2* __restrict__ sa, const double2* __restrict__ sg,
+                                            const double2* __restrict__ sc, const double2* __restrict__ se, cplx s,
+                                            double2* __restrict__ ck, double2* __restrict__ dst, int64_t stride,
+                                            RHS rhs, STORE store, double& minpiv) {
+  const int tid = threadIdx.x;
+  cplx cp = mk(0, 0), dp = mk(0, 0);
+  for (int k = 0; k < nz; ++k) {
+    if (k % ZSEG == 0) ck[(k / ZSEG) * ZTHREADS + tid] = make_double2(cp.x, cp.y);
+    const double2 a2 = sa[k], g2 = sg[k], c2 = sc[k], e2 = se[k];
+    const cplx a = mk(a2.x, a2.y), c = mk(c2.x, c2.y);
+    const cplx b = cfma(s, mk(e2.x, e2.y), mk(g2.x, g2.y));
+    const cplx r = b - a * cp;
+    minpiv = fmin(minpiv, cabs1(r) / (cabs1(a) + cabs1(b) + cabs1(c)));
+    const cplx inv = cinv(r);
+    cp = c * inv;
+    dp = (rhs(k) - a * dp) * inv;
+    dst[k * stride] = make_double2(dp.x, dp.y);
   }
-  // upward sweep for row 0 with right boundary x_e (= row K-1)
-  cplx ua, uc, ud;
-  {
-    cplx a, b, c;
-    coef(K - 2, a, b, c);
-    double rn = cabs1(a) + cabs1(b) + cabs1(c);
-    minpiv = fmin(minpiv, cabs1(b) / rn);
-    cplx inv = cinv(b);
-    ua = a * inv; uc = c * inv; ud = d[K - 2] * inv;
+  cplx x = mk(0, 0);
+  const int nseg = (nz + ZSEG - 1) / ZSEG;
+  for (int sgi = nseg - 1; sgi >= 0; --sgi) {
+    const int k0 = sgi * ZSEG;
+    cplx cs[ZSEG];
+    double2 c0 = ck[sgi * ZTHREADS + tid];
+    cplx cc = mk(c0.x, c0.y);
 #pragma unroll
-    for (int j = K - 3; j >= 0; --j) {
-      coef(j, a, b, c);
-      cplx r = b - c * ua;
-      minpiv = fmin(minpiv, cabs1(r) / (cabs1(a) + cabs1(b) + cabs1(c)));
-      inv = cinv(r);
-      cplx nua = a * inv;
-      uc = -(c * uc) * inv;
-      ud = (d[j] - c * ud) * inv;
-      ua = nua;
+    for (int j = 0; j < ZSEG; ++j) {
+      const int k = k0 + j;
+      if (k < nz) {
+        const double2 a2 = sa[k], g2 = sg[k], c2 = sc[k], e2 = se[k];
+        const cplx b = cfma(s, mk(e2.x, e2.y), mk(g2.x, g2.y));
+        cc = mk(c2.x, c2.y) * cinv(b - mk(a2.x, a2.y) * cc);
+      }
+      cs[j] = cc;
+    }
+#pragma unroll
+    for (int j = ZSEG - 1; j >= 0; --j) {
+      const int k = k0 + j;
+      if (k < nz) {
+        const double2 d2 = dst[k * stride];
+        x = mk(d2.x, d2.y) - cs[j] * x;
+        store(k, x);
+      }
     }
   }
-  // reduced system, normalised rows (B = 1):  S: ua x_{e,t-1} + x_{s,t} + uc x_{e,t} = ud
-  //                                           E: al x_{s,t} + x_{e,t} + ga x_{s,t+1} = de
-  cplx sA = ua, sC = uc, sD = ud;
-  cplx eA = al[K - 1], eC = ga[K - 1], eD = de[K - 1];
-  // level 1: S uses (E of lane-1) on the left and own E on the right; E uses own S and S of lane+1.
-  {
-    cplx lA = shfl_up(eA, 1), lC = shfl_up(eC, 1), lD = shfl_up(eD, 1);
-    if (lane == 0) { lA = mk(0, 0); lC = mk(0, 0); lD = mk(0, 0); }
-    cplx rA = shfl_down(sA, 1), rC = shfl_down(sC, 1), rD = shfl_down(sD, 1);
-    if (lane == 31) { rA = mk(0, 0); rC = mk(0, 0); rD = mk(0, 0); }
-    // S' = S - sA*Eleft - sC*Eown
-    cplx nsA = -(sA * lA);
-    cplx nsB = mk(1, 0) - sA * lC - sC * eA;
-    cplx nsC = -(sC * eC);
-    cplx nsD = sD - sA * lD - sC * eD;
-    // E' = E - eA*Sown - eC*Sright
-    cplx neA = -(eA * sA);
-    cplx neB = mk(1, 0) - eA * sC - eC * rA;
-    cplx neC = -(eC * rC);
-    cplx neD = eD - eA * sD - eC * rD;
-    cplx is = cinv(nsB), ie = cinv(neB);
-    sA = nsA * is; sC = nsC * is; sD = nsD * is;
-    eA = neA * ie; eC = neC * ie; eD = neD * ie;
-  }
-  // levels 2..: S couples S of lanes t-+delta, E couples E of lanes t-+delta
-#pragma unroll
-  for (int dl = 1; dl < 32; dl <<= 1) {
-    cplx lsA = shfl_up(sA, dl), lsC = shfl_up(sC, dl), lsD = shfl_up(sD, dl);
-    cplx rsA = shfl_down(sA, dl), rsC = shfl_down(sC, dl), rsD = shfl_down(sD, dl);
-    cplx leA = shfl_up(eA, dl), leC = shfl_up(eC, dl), leD = shfl_up(eD, dl);
-    cplx reA = shfl_down(eA, dl), reC = shfl_down(eC, dl), reD = shfl_down(eD, dl);
-    if (lane < dl) { lsA = lsC = lsD = leA = leC = leD = mk(0, 0); }
-    if (lane + dl > 31) { rsA = rsC = rsD = reA = reC = reD = mk(0, 0); }
-    cplx nsB = mk(1, 0) - sA * lsC - sC * rsA;
-    cplx nsA = -(sA * lsA), nsC = -(sC * rsC), nsD = sD - sA * lsD - sC * rsD;
-    cplx neB = mk(1, 0) - eA * leC - eC * reA;
-    cplx neA = -(eA * leA), neC = -(eC * reC), neD = eD - eA * leD - eC * reD;
-    cplx is = cinv(nsB), ie = cinv(neB);
-    sA = nsA * is; sC = nsC * is; sD = nsD * is;
-    eA = neA * ie; eC = neC * ie; eD = neD * ie;
-  }
-  const cplx xs = sD, xe = eD;
-  d[K - 1] = xe;
-#pragma unroll
-  for (int j = K - 2; j >= 1; --j) d[j] = de[j] - al[j] * xs - ga[j] * d[j + 1];
-  d[0] = xs;
 }
 
-__device__ __forceinline__ void warp_min_commit(double v, double* out) {
+__device__ __forceinline__ void stage_ztab(ZTab tab, const double2* TAB, int nz, double2* sa, double2* sg,
+                                           double2* sc, double2* se) {
+  for (int k = threadIdx.x; k < nz; k += blockDim.x) {
+    sa[k] = TAB[tab.a + k];
+    sg[k] = TAB[tab.g + k];
+    sc[k] = TAB[tab.c + k];
+    se[k] = TAB[tab.e + k];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void block_min_commit(double v, double* out) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((threadIdx.x & 31) == 0 && out) atomic_min_pos(out, v);
 }
 
-// mode 1: pass-1 solve in place (RHS = transformed f).  mode 2: pass-2 Dirichlet lifting
-// (RHS built from the face transforms), solution ADDED to the stored v~ (u~ = v~ + w~).
-template <int K, int MODE>
-__global__ void __launch_bounds__(128) k_zsolve_block(const ZBlock* __restrict__ blocks, int R, int nz,
-                                                      ZTab tab, int64_t sig_off, Bufs bufs, double* minpiv_out) {
-  const ZBlock& B = blocks[blockIdx.y];
-  const int lane = threadIdx.x & 31;
-  const int64_t nsys = (int64_t)B.nx * B.ny * R;
-  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
-  double2* MS = reinterpret_cast<double2*>(bufs.p[B_MS]);
-  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
-  ZRow T{TAB + tab.a, TAB + tab.g, TAB + tab.c, TAB + tab.e};
-  double minpiv = 1.0;
-  const int warps = blockDim.x >> 5;
-  for (int64_t sidx = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); sidx < nsys;
-       sidx += (int64_t)gridDim.x * warps) {
-    const int l = (int)(sidx % B.nx);
-    const int64_t rm = sidx / B.nx;
-    const int m = (int)(rm % B.ny);
-    const int r = (int)(rm / B.ny);
-    const cplx s = ld(TAB + B.lamx + l) + ld(TAB + B.lamy + m);
-    double2* line = MS + B.ms_off + sidx * nz;
-    cplx d[K];
-    if (MODE == 1) {
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        int k = lane * K + j;
-        d[j] = (k < nz) ? cplx{line[k].x, line[k].y} : mk(0, 0);
-      }
-    } else {
-      const cplx wx0 = ld(TAB + B.wx0 + l), wx1 = ld(TAB + B.wx1 + l);
-      const cplx wy0 = ld(TAB + B.wy0 + m), wy1 = ld(TAB + B.wy1 + m);
-      const cplx cL = mk(B.cL.x, B.cL.y) * wx0, cR = mk(B.cR.x, B.cR.y) * wx1;
-      const cplx cB = mk(B.cB.x, B.cB.y) * wy0, cT = mk(B.cT.x, B.cT.y) * wy1;
-      // face transforms stored [r][mode][k] with the mode stride padded to Bx.ny / nx
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        int k = lane * K + j;
-        cplx acc = mk(0, 0);
-        if (k < nz) {
-          if (B.gL >= 0) acc = cfma(cL, ld(IF + B.gL + ((int64_t)r * B.ny + m) * nz + k), acc);
-          if (B.gR >= 0) acc = cfma(cR, ld(IF + B.gR + ((int64_t)r * B.ny + m) * nz + k), acc);
-          if (B.gB >= 0) acc = cfma(cB, ld(IF + B.gB + ((int64_t)r * B.nx + l) * nz + k), acc);
-          if (B.gT >= 0) acc = cfma(cT, ld(IF + B.gT + ((int64_t)r * B.nx + l) * nz + k), acc);
-          acc = -(ld(TAB + sig_off + k) * acc);
-        }
-        d[j] = acc;
-      }
-    }
-    warp_tridiag<K>(d, nz, T, s, lane, minpiv);
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      int k = lane * K + j;
-      if (k < nz) {
-        if (MODE == 1) line[k] = make_double2(d[j].x, d[j].y);
-        else { double2 o = line[k]; line[k] = make_double2(o.x + d[j].x, o.y + d[j].y); }
-      }
-    }
-  }
-  warp_min_commit(minpiv, minpiv_out);
+static size_t zsmem_bytes(int nz) {
+  return (size_t)4 * nz * sizeof(double2) + (size_t)((nz + ZSEG - 1) / ZSEG) * ZTHREADS * sizeof(double2);
 }
 
+// mode 1: pass-1 solve in place in MS (RHS = transformed f, steps 2).  mode 2: pass-2
+// Dirichlet lifting (step 6): RHS built from the face transforms, d' kept in T1, the
+// solution ADDED to the stored v~ (u~ = v~ + w~).
 template <int MODE>
-static cudaError_t zsb_dispatch(int K, dim3 grid, cudaStream_t st, const ZBlock* b, int R, int nz, ZTab tab,
-                                int64_t sig, const Bufs& bufs, double* mp) {
-  switch (K) {
-#define ZK(KK) case KK: k_zsolve_block<KK, MODE><<<grid, 128, 0, st>>>(b, R, nz, tab, sig, bufs, mp); break;
-    ZK(2) ZK(3) ZK(4) ZK(5) ZK(6) ZK(7) ZK(8) ZK(9) ZK(10) ZK(11) ZK(12) ZK(13) ZK(14) ZK(15) ZK(16)
-#undef ZK
-    default: return cudaErrorInvalidValue;
+__global__ void __launch_bounds__(ZTHREADS) k_zsolve_block(const ZBlock* __restrict__ blocks, int R, int nz, ZTab tab,
+                                                          int64_t sig_off, Bufs bufs, double* minpiv_out) {
+  extern __shared__ double2 zsm[];
+  double2 *sa = zsm, *sg = zsm + nz, *sc = zsm + 2 * nz, *se = zsm + 3 * nz, *ck = zsm + 4 * nz;
+  const ZBlock& B = blocks[blockIdx.y];
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  stage_ztab(tab, TAB, nz, sa, sg, sc, se);
+  const int nxy = B.nx * B.ny;
+  const int64_t sys = (int64_t)blockIdx.x * ZTHREADS + threadIdx.x;
+  double minpiv = 1.0;
+  if (sys < (int64_t)nxy * R) {
+    const int r = (int)(sys / nxy);
+    const int mode = (int)(sys - (int64_t)r * nxy);
+    const int l = mode % B.nx, m = mode / B.nx;
+    const cplx s = ld(TAB + B.lamx + l) + ld(TAB + B.lamy + m);
+    double2* MS = reinterpret_cast<double2*>(bufs.p[B_MS]) + B.ms_off + (int64_t)r * nz * nxy + mode;
+    if (MODE == 1) {
+      thomas_line(nz, sa, sg, sc, se, s, ck, MS, nxy,
+                  [&](int k) { double2 v = MS[(int64_t)k * nxy]; return mk(v.x, v.y); },
+                  [&](int k, cplx x) { MS[(int64_t)k * nxy] = make_double2(x.x, x.y); }, minpiv);
+    } else {
+      const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
+      double2* T1 = reinterpret_cast<double2*>(bufs.p[B_T1]) + B.ms_off + (int64_t)r * nz * nxy + mode;
+      const cplx cL = mk(B.cL.x, B.cL.y) * ld(TAB + B.wx0 + l), cR = mk(B.cR.x, B.cR.y) * ld(TAB + B.wx1 + l);
+      const cplx cB = mk(B.cB.x, B.cB.y) * ld(TAB + B.wy0 + m), cT = mk(B.cT.x, B.cT.y) * ld(TAB + B.wy1 + m);
+      const int64_t rk0 = (int64_t)r * nz;
+      auto rhs = [&](int k) {
+        const int64_t row = (rk0 + k) * B.fstride;
+        cplx acc = mk(0, 0);
+        if (B.gL >= 0) acc = cfma(cL, ld(IF + B.gL + row + m), acc);
+        if (B.gR >= 0) acc = cfma(cR, ld(IF + B.gR + row + m), acc);
+        if (B.gB >= 0) acc = cfma(cB, ld(IF + B.gB + row + l), acc);
+        if (B.gT >= 0) acc = cfma(cT, ld(IF + B.gT + row + l), acc);
+        return -(ld(TAB + sig_off + k) * acc);
+      };
+      thomas_line(nz, sa, sg, sc, se, s, ck, T1, nxy, rhs,
+                  [&](int k, cplx x) {
+                    double2 o = MS[(int64_t)k * nxy];
+                    MS[(int64_t)k * nxy] = make_double2(o.x + x.x, o.y + x.y);
+                  },
+                  minpiv);
+    }
   }
-  return cudaGetLastError();
-}
-
-static int rows_per_lane(int nz) {
-  int K = (nz + 31) / 32;
-  return K < 2 ? 2 : K;
+  block_min_commit(minpiv, minpiv_out);
 }
 
 cudaError_t launch_zsolve_block(int mode, const ZBlock* d_blocks, int nblocks, int max_systems, int R, int nz,
                                 ZTab tab, int64_t sig_off, const Bufs& bufs, double* d_minpiv, cudaStream_t st) {
-  int K = rows_per_lane(nz);
-  if (K > 16) return cudaErrorInvalidValue;
-  int64_t want = ((int64_t)max_systems + 3) / 4;
-  dim3 grid((unsigned)(want > 65535 ? 65535 : (want < 1 ? 1 : want)), (unsigned)nblocks);
-  return mode == 1 ? zsb_dispatch<1>(K, grid, st, d_blocks, R, nz, tab, sig_off, bufs, d_minpiv)
-                   : zsb_dispatch<2>(K, grid, st, d_blocks, R, nz, tab, sig_off, bufs, d_minpiv);
+  (void)R;
+  size_t sm = zsmem_bytes(nz);
+  dim3 grid((unsigned)((max_systems + ZTHREADS - 1) / ZTHREADS), (unsigned)nblocks);
+  if (mode == 1) {
+    cudaFuncSetAttribute(k_zsolve_block<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_zsolve_block<1><<<grid, ZTHREADS, sm, st>>>(d_blocks, R, nz, tab, sig_off, bufs, d_minpiv);
+  } else {
+    cudaFuncSetAttribute(k_zsolve_block<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_zsolve_block<2><<<grid, ZTHREADS, sm, st>>>(d_blocks, R, nz, tab, sig_off, bufs, d_minpiv);
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- step 5 global sweep
-template <int K>
-__global__ void __launch_bounds__(128) k_gsweep(GSweep G, ZTab tab, Bufs bufs, double* minpiv_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nsys = (int64_t)G.nx * G.ny * G.R;
-  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
-  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
-  double2* WH = reinterpret_cast<double2*>(bufs.p[B_T1]) + G.what;
-  ZRow T{TAB + tab.a, TAB + tab.g, TAB + tab.c, TAB + tab.e};
+// One thread per global mode (l, m): r^_k = sum_a W_x[I_a,l] R1[a][r][k][m] + sum_b W_y[I_b,m]
+// R2[b][r][k][l] (the sparse forward transform of the interface residual),
+// then the z-solve with the global eigenvalues; W^ in [r][k][m][l] (B_T1).
+constexpr int GMAXIF = 32;
+template <int NIF>
+__global__ void __launch_bounds__(ZTHREADS) k_gsweep(GSweep G, ZTab tab, Bufs bufs, double* minpiv_out) {
+  extern __shared__ double2 zsm[];
   const int nz = G.nz;
+  double2 *sa = zsm, *sg = zsm + nz, *sc = zsm + 2 * nz, *se = zsm + 3 * nz, *ck = zsm + 4 * nz;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  stage_ztab(tab, TAB, nz, sa, sg, sc, se);
+  const int nxy = G.nx * G.ny;
+  const int64_t sys = (int64_t)blockIdx.x * ZTHREADS + threadIdx.x;
   double minpiv = 1.0;
-  const int warps = blockDim.x >> 5;
-  for (int64_t sidx = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); sidx < nsys;
-       sidx += (int64_t)gridDim.x * warps) {
-    const int l = (int)(sidx % G.nx);
-    const int64_t rm = sidx / G.nx;
-    const int m = (int)(rm % G.ny);
-    const int r = (int)(rm / G.ny);
+  if (sys < (int64_t)nxy * G.R) {
+    const int r = (int)(sys / nxy);
+    const int mode = (int)(sys - (int64_t)r * nxy);
+    const int l = mode % G.nx, m = mode / G.nx;
     const cplx s = ld(TAB + G.lamx + l) + ld(TAB + G.lamy + m);
-    cplx d[K];
+    const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
+    cplx wa[NIF], wb[NIF];
 #pragma unroll
-    for (int j = 0; j < K; ++j) d[j] = mk(0, 0);
-    // r^[l,m,k] = sum_a W_x[I_a,l] R1[a][r][m][k] + sum_b W_y[I_b,m] R2[b][r][l][k]
-    for (int a = 0; a < G.nifx; ++a) {
-      const cplx w = ld(TAB + G.wxi + (int64_t)a * G.nx + l);
-      const double2* src = IF + G.r1 + (((int64_t)a * G.R + r) * G.ny + m) * nz;
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        int k = lane * K + j;
-        if (k < nz) d[j] = cfma(w, ld(src + k), d[j]);
-      }
+    for (int a = 0; a < NIF; ++a) {
+      wa[a] = a < G.nifx ? ld(TAB + G.wxi + (int64_t)a * G.nx + l) : mk(0, 0);
+      wb[a] = a < G.nify ? ld(TAB + G.wyi + (int64_t)a * G.ny + m) : mk(0, 0);
     }
-    for (int b = 0; b < G.nify; ++b) {
-      const cplx w = ld(TAB + G.wyi + (int64_t)b * G.ny + m);
-      const double2* src = IF + G.r2 + (((int64_t)b * G.R + r) * G.nx + l) * nz;
+    const int64_t rk0 = (int64_t)r * nz;
+    const int64_t sa1 = (int64_t)G.R * nz * G.ny, sa2 = (int64_t)G.R * nz * G.nx;
+    auto rhs = [&](int k) {
+      cplx acc = mk(0, 0);
+      const double2* p1 = IF + G.r1 + (rk0 + k) * G.ny + m;
+      const double2* p2 = IF + G.r2 + (rk0 + k) * G.nx + l;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        int k = lane * K + j;
-        if (k < nz) d[j] = cfma(w, ld(src + k), d[j]);
-      }
-    }
-    warp_tridiag<K>(d, nz, T, s, lane, minpiv);
-    double2* line = WH + sidx * nz;  // W^[r][m][l][k]
+      for (int a = 0; a < NIF; ++a)
+        if (a < G.nifx) acc = cfma(wa[a], ld(p1 + a * sa1), acc);
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      int k = lane * K + j;
-      if (k < nz) line[k] = make_double2(d[j].x, d[j].y);
-    }
+      for (int b = 0; b < NIF; ++b)
+        if (b < G.nify) acc = cfma(wb[b], ld(p2 + b * sa2), acc);
+      return acc;
+    };
+    double2* W = reinterpret_cast<double2*>(bufs.p[B_T1]) + G.what + (int64_t)r * nz * nxy + mode;
+    thomas_line(nz, sa, sg, sc, se, s, ck, W, nxy, rhs,
+                [&](int k, cplx x) { W[(int64_t)k * nxy] = make_double2(x.x, x.y); }, minpiv);
   }
-  warp_min_commit(minpiv, minpiv_out);
+  block_min_commit(minpiv, minpiv_out);
 }
 
 cudaError_t launch_gsweep(const GSweep& g, ZTab tab, const Bufs& bufs, double* d_minpiv, cudaStream_t st) {
-  int K = rows_per_lane(g.nz);
+  if (g.nifx > GMAXIF || g.nify > GMAXIF) return cudaErrorInvalidValue;
+  size_t sm = zsmem_bytes(g.nz);
   int64_t nsys = (int64_t)g.nx * g.ny * g.R;
-  int64_t want = (nsys + 3) / 4;
-  dim3 grid((unsigned)(want > 1048576 ? 1048576 : want));
-  switch (K) {
-#define GK(KK) case KK: k_gsweep<KK><<<grid, 128, 0, st>>>(g, tab, bufs, d_minpiv); break;
-    GK(2) GK(3) GK(4) GK(5) GK(6) GK(7) GK(8) GK(9) GK(10) GK(11) GK(12) GK(13) GK(14) GK(15) GK(16)
-#undef GK
-    default: return cudaErrorInvalidValue;
+  const int nif = g.nifx > g.nify ? g.nifx : g.nify;
+  const unsigned grid = (unsigned)((nsys + ZTHREADS - 1) / ZTHREADS);
+#define GS(NN)                                                                              \
+  {                                                                                         \
+    cudaFuncSetAttribute(k_gsweep<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_gsweep<NN><<<grid, ZTHREADS, sm, st>>>(g, tab, bufs, d_minpiv);                        \
   }
+  if (nif <= 4) GS(4) else if (nif <= 8) GS(8) else if (nif <= 16) GS(16) else GS(32)
+#undef GS
   return cudaGetLastError();
 }
 
@@ -469,8 +410,8 @@ __global__ void k_iface_res(IfaceRes P, Bufs bufs) {
         const cplx wgt = ld(TAB + P.hhy + q) * ld(TAB + P.sig + k) * ld(TAB + P.hhz + k);
         // left block column a, its last row (e=1); right block column a+1, its first row (e=0)
         const int bl = jb * P.nbx + a, br = jb * P.nbx + a + 1;
-        const cplx vl = ld(IF + P.vxo + ((((int64_t)bl * R + r) * 2 + 1) * nz + k) * P.qpad + ql);
-        const cplx vr = ld(IF + P.vxo + ((((int64_t)br * R + r) * 2 + 0) * nz + k) * P.qpad + ql);
+        const cplx vl = ld(IF + P.vxo + ((((int64_t)bl * 2 + 1) * R + r) * nz + k) * P.qpad + ql);
+        const cplx vr = ld(IF + P.vxo + ((((int64_t)br * 2 + 0) * R + r) * nz + k) * P.qpad + ql);
         res = res - (cinv(ld(TAB + P.hx + Pn - 1)) * wgt) * vl - (cinv(ld(TAB + P.hx + Pn)) * wgt) * vr;
       }
       IF[P.rx + t] = make_double2(res.x, res.y);  // RX[a][r][k][q]
@@ -491,8 +432,8 @@ __global__ void k_iface_res(IfaceRes P, Bufs bufs) {
         const int pl = p + 1 - xlo[ib];
         const cplx wgt = ld(TAB + P.hhx + p) * ld(TAB + P.sig + k) * ld(TAB + P.hhz + k);
         const int bb = b * P.nbx + ib, bt = (b + 1) * P.nbx + ib;
-        const cplx vb = ld(IF + P.vyo + ((((int64_t)bb * R + r) * 2 + 1) * nz + k) * P.ppad + pl);
-        const cplx vt = ld(IF + P.vyo + ((((int64_t)bt * R + r) * 2 + 0) * nz + k) * P.ppad + pl);
+        const cplx vb = ld(IF + P.vyo + ((((int64_t)bb * 2 + 1) * R + r) * nz + k) * P.ppad + pl);
+        const cplx vt = ld(IF + P.vyo + ((((int64_t)bt * 2 + 0) * R + r) * nz + k) * P.ppad + pl);
         res = res - (cinv(ld(TAB + P.hy + Qn - 1)) * wgt) * vb - (cinv(ld(TAB + P.hy + Qn)) * wgt) * vt;
       }
       IF[P.ry + u] = make_double2(res.x, res.y);  // RY[b][r][k][p]

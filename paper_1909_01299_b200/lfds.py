@@ -36,7 +36,8 @@ class _Z(ctypes.Structure):
 
 class Options(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("refine", ctypes.c_int), ("refine_tol", ctypes.c_double),
-                ("residual_dd", ctypes.c_int), ("device", ctypes.c_int), ("rhs_chunk", ctypes.c_int)]
+                ("residual_dd", ctypes.c_int), ("device", ctypes.c_int), ("rhs_chunk", ctypes.c_int),
+                ("profile", ctypes.c_int)]
 
 
 class Report(ctypes.Structure):
@@ -67,12 +68,17 @@ _lib.lfds_get_info.argtypes = [_P, ctypes.POINTER(Info)]
 _lib.lfds_get_basis.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _P, _P]
 _lib.lfds_destroy.argtypes = [_P]
+_lib.lfds_stage_count.restype = ctypes.c_int
+_lib.lfds_stage_name.argtypes = [ctypes.c_int]
+_lib.lfds_stage_name.restype = ctypes.c_char_p
+_lib.lfds_stage_times.argtypes = [_P, _P, _P]
 _lib.lfds_last_error.restype = ctypes.c_char_p
 _lib.lfds_version.restype = ctypes.c_char_p
 
 EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
             "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_residual", "lfds_get_report",
-            "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version"]
+            "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version",
+            "lfds_stage_count", "lfds_stage_name", "lfds_stage_times"]
 
 
 def _check(rc):
@@ -94,12 +100,13 @@ class Plan:
 
     def __init__(self, hx, hy, hz, sigma_node, sigma_edge, lam, iface_x: Sequence[int] = (),
                  iface_y: Sequence[int] = (), *, dtype: str = "c128", refine: int = 0,
-                 refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0):
+                 refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0,
+                 profile: bool = False):
         opt = Options()
         _lib.lfds_default_options(ctypes.byref(opt))
         opt.dtype = LFDS_F64 if dtype in ("f64", "float64") else LFDS_C128
         opt.refine, opt.refine_tol, opt.residual_dd = int(refine), float(refine_tol), int(bool(residual_dd))
-        opt.device, opt.rhs_chunk = int(device), int(rhs_chunk)
+        opt.device, opt.rhs_chunk, opt.profile = int(device), int(rhs_chunk), int(bool(profile))
         self.dtype = opt.dtype
         hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
         sn_, psn = _zarr(sigma_node); se_, pse = _zarr(sigma_edge)
@@ -149,6 +156,14 @@ class Plan:
         _check(_lib.lfds_get_basis(self._h, axis, block, None, None, None, lam.ctypes.data_as(_P),
                                    W.ctypes.data_as(_P)))
         return lam, W, kind.value, lo.value
+
+    def stage_times(self) -> dict:
+        """{stage: (device ms, launches)} accumulated since the last call (profile=True plans)."""
+        n = _lib.lfds_stage_count()
+        ms = np.zeros(n, np.float64)
+        la = np.zeros(n, np.int32)
+        _check(_lib.lfds_stage_times(self._h, ms.ctypes.data_as(_P), la.ctypes.data_as(_P)))
+        return {_lib.lfds_stage_name(i).decode(): (float(ms[i]), int(la[i])) for i in range(n)}
 
     # ------------------------------------------------------------------ compute
     def _torch(self):
