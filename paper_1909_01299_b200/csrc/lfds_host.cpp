@@ -6,7 +6,7 @@
 //                             step 2  T_lm v~_lm = f~_lm (z-solves)               (k_zsolve_block<1>)
 //                             step 3  v at the rows next to every block face      (k_gemm x4)
 //   interface                 step 4  r_b = b - A v on the interface planes       (k_iface_res)
-//                             step 5  w on the planes via the global bases        (k_gemm, k_gsweep)
+//                             step 5  w on the planes via the global bases        (k_gemm, k_grank, k_zsolve_block)
 //   pass 2 (per block)        step 6  w~ from the Dirichlet lifting of w          (k_gemm, k_zsolve_block<2>)
 //                             step 7  u = (W_x (x) W_y (x) I)(v~ + w~), u = w on planes (k_gemm x2, k_write_iface)
 //
@@ -53,6 +53,7 @@ struct AxisBlock {
   int lo, n;         // first node (1-based), interior size
   Basis B;
   int64_t F = 0, W = 0, lam = 0;  // TAB offsets: F[l*n+p] = W[p][l] hh_p, W[p*n+l], lam[l]
+  int64_t Fr = -1, Wr = -1;       // real copies (offsets in doubles) when the basis is real (U, R)
 };
 
 struct Axis {
@@ -94,9 +95,12 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   GemmDesc* d_descs = nullptr;
   ZBlock* d_zb = nullptr;
   StageDescs s1x, s1y, s3g, s3h, s3x, s3y, s5r1, s5r2, s5p1, s5p2, s5wx, s5wy, s6f, s7y, s7x;
-  int max_systems = 0;
+  StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
+  StageDescs m3g, m3h, m5p1, m5p2;                    // few-row DMMA contractions (<= 8 rows each)
+  bool use_xform = false;
+  int max_systems = 0, max_systems_global = 0;
   // workspace layout (bytes)
-  size_t off_ms = 0, off_t1 = 0, off_if = 0, off_red = 0, off_res = 0, total = 0;
+  size_t off_ms = 0, off_t1 = 0, off_if = 0, off_red = 0, off_ck = 0, off_res = 0, total = 0;
   int64_t g_off = 0, h_off = 0, vx_off = 0, vy_off = 0, rx = 0, ry = 0, r1 = 0, r2 = 0, p1 = 0, p2 = 0, wx = 0,
           wy = 0, gf = 0;
 };
@@ -134,6 +138,12 @@ struct TabBuilder {
     int64_t off = (int64_t)v.size();
     for (auto& z : a) v.push_back(make_double2(z.real(), z.imag()));
     return off;
+  }
+  int64_t put_real(const std::vector<zc>& a) {  // real parts packed two per slot; offset in doubles
+    int64_t off = (int64_t)v.size();
+    for (size_t i = 0; i < a.size(); i += 2)
+      v.push_back(make_double2(a[i].real(), i + 1 < a.size() ? a[i + 1].real() : 0.0));
+    return 2 * off;
   }
   int64_t put_ints(const std::vector<int>& a) {
     int64_t off = (int64_t)v.size();
@@ -201,6 +211,8 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   pp.off_t1 = off; off = al256(off + t1_elems * 16);
   pp.off_if = off; off = al256(off + if_elems * 16);
   pp.off_red = off; off = al256(off + (size_t)(2 * R + 8) * 8);
+  pp.off_ck = off;
+  off = al256(off + std::max(zsolve_checkpoint_bytes(nblk, maxsys, Nz), zsolve_checkpoint_bytes(1, Nx * Ny * R, Nz)));
   pp.off_res = off;
   if (P->opt.refine != 0) off = al256(off + (size_t)Nx * Ny * Nz * R * 16);
   pp.total = off;
@@ -301,6 +313,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
       int b = j * nbx + i;
       ZBlock& z = zb[b];
       z.ms_off = ms[b];
+      z.buf = B_MS;
       z.nx = bx.n;
       z.ny = by.n;
       z.lamx = bx.lam;
@@ -354,10 +367,66 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     }
   stage(pp.s7x, std::move(v)); v.clear();
 
+  // few-row contractions (step 3 edge rows, step 5 projections): split into <= 8-row slices
+  {
+    std::vector<GemmDesc> vm;
+    auto split8 = [&](StageDescs& dst, const StageDescs& src) {
+      for (int q = 0; q < src.n; ++q) {
+        const GemmDesc d0 = D[src.off + q];
+        for (int r0 = 0; r0 < d0.M; r0 += 8) {
+          GemmDesc d = d0;
+          d.M = std::min(8, d0.M - r0);
+          d.a_off += (int64_t)r0 * d0.sAi;
+          d.c_off += (int64_t)r0 * d0.sCi;
+          vm.push_back(d);
+        }
+      }
+      stage(dst, std::move(vm)); vm.clear();
+    };
+    split8(pp.m3g, pp.s3g);
+    split8(pp.m3h, pp.s3h);
+    split8(pp.m5p1, pp.s5p1);
+    split8(pp.m5p2, pp.s5p2);
+  }
+  // DMMA transform passes: the same contractions, split by real / complex eigenvector matrix
+  pp.use_xform = !in_real && !out_real;
+  if (pp.use_xform) {
+    std::vector<GemmDesc> vc, vr;
+    auto split = [&](StageDescs& sc, StageDescs& sr, const StageDescs& src, bool xaxis, bool fwd) {
+      for (int q = 0; q < src.n; ++q) {
+        GemmDesc d = D[src.off + q];
+        // recover the block of this descriptor: stages s1x/s7x have one desc per block, s1y/s7y too
+        const int b = q;
+        const AxisBlock& ab = xaxis ? X.blocks[b % nbx] : Y.blocks[b / nbx];
+        const int64_t roff = fwd ? ab.Fr : ab.Wr;
+        if (roff >= 0) { d.a_off = roff; vr.push_back(d); }
+        else vc.push_back(d);
+      }
+      stage(sc, std::move(vc)); vc.clear();
+      stage(sr, std::move(vr)); vr.clear();
+    };
+    split(pp.x1c, pp.x1r, pp.s1x, true, true);
+    split(pp.y1c, pp.y1r, pp.s1y, false, true);
+    split(pp.y7c, pp.y7r, pp.s7y, false, false);
+    split(pp.x7c, pp.x7r, pp.s7x, true, false);
+  }
+
   CUDA_TRY(cudaMalloc(&pp.d_descs, sizeof(GemmDesc) * std::max<size_t>(1, D.size())));
   CUDA_TRY(cudaMemcpy(pp.d_descs, D.data(), sizeof(GemmDesc) * D.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMalloc(&pp.d_zb, sizeof(ZBlock) * nblk));
-  CUDA_TRY(cudaMemcpy(pp.d_zb, zb.data(), sizeof(ZBlock) * nblk, cudaMemcpyHostToDevice));
+  {  // the step-5 global z-solve as one more 'block': all Nx x Ny global modes, in place in T1
+    ZBlock g{};
+    g.ms_off = 0;
+    g.buf = B_T1;
+    g.nx = Nx;
+    g.ny = Ny;
+    g.lamx = X.lamg;
+    g.lamy = Y.lamg;
+    g.gL = g.gR = g.gB = g.gT = -1;
+    zb.push_back(g);
+    pp.max_systems_global = Nx * Ny * R;
+  }
+  CUDA_TRY(cudaMalloc(&pp.d_zb, sizeof(ZBlock) * zb.size()));
+  CUDA_TRY(cudaMemcpy(pp.d_zb, zb.data(), sizeof(ZBlock) * zb.size(), cudaMemcpyHostToDevice));
   return LFDS_OK;
 }
 
@@ -404,20 +473,38 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     P->launches += (s.n + 65534) / 65535;
     return LFDS_OK;
   };
+  auto m8 = [&](const StageDescs& s, bool kcontig) -> int {
+    if (!s.n) return LFDS_OK;
+    CUDA_TRY(launch_xform_m8(pp.d_descs + s.off, s.n, s.maxN, kcontig, bufs, st));
+    P->launches += (s.n + 65534) / 65535;
+    return LFDS_OK;
+  };
+  auto xform = [&](const StageDescs& sc, const StageDescs& sr, const StageDescs& generic, bool kcontig) -> int {
+    if (!pp.use_xform) return gemm(generic);
+    if (sc.n) {
+      CUDA_TRY(launch_xform(pp.d_descs + sc.off, sc.n, sc.maxM, sc.maxN, false, kcontig, bufs, st));
+      P->launches += (sc.n + 65534) / 65535;
+    }
+    if (sr.n) {
+      CUDA_TRY(launch_xform(pp.d_descs + sr.off, sr.n, sr.maxM, sr.maxN, true, kcontig, bufs, st));
+      P->launches += (sr.n + 65534) / 65535;
+    }
+    return LFDS_OK;
+  };
   int rc;
   // pass 1
   begin(ST_X1);
-  if ((rc = gemm(pp.s1x))) return rc;
+  if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true))) return rc;
   end(); begin(ST_Y1);
-  if ((rc = gemm(pp.s1y))) return rc;
+  if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false))) return rc;
   end(); begin(ST_Z1);
-  CUDA_TRY(launch_zsolve_block(1, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st));
+  CUDA_TRY(launch_zsolve_block(1, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st, P->real_z));
   P->launches++;
   end();
   if (nifx + nify > 0) {
     begin(ST_EDGE);
-    if ((rc = gemm(pp.s3g))) return rc;
-    if ((rc = gemm(pp.s3h))) return rc;
+    if ((rc = m8(pp.m3g, true))) return rc;
+    if ((rc = m8(pp.m3h, false))) return rc;
     if ((rc = gemm(pp.s3x))) return rc;
     if ((rc = gemm(pp.s3y))) return rc;
     end(); begin(ST_IFRES);
@@ -433,33 +520,35 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     P->launches++;
     end(); begin(ST_GFWD);
     // step 5
-    if ((rc = gemm(pp.s5r1))) return rc;
-    if ((rc = gemm(pp.s5r2))) return rc;
+    if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true))) return rc;
+    if ((rc = xform(pp.s5r2, StageDescs{}, pp.s5r2, true))) return rc;
     end(); begin(ST_GSWEEP);
     GSweep g{};
     g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
     g.lamx = X.lamg; g.lamy = Y.lamg; g.wxi = X.WI; g.wyi = Y.WI; g.r1 = pp.r1; g.r2 = pp.r2; g.what = 0;
-    CUDA_TRY(launch_gsweep(g, P->zt_plain, bufs, minpiv, st));
-    P->launches++;
+    CUDA_TRY(launch_grank(g, bufs, st));
+    CUDA_TRY(launch_zsolve_block(1, pp.d_zb + nblk, 1, pp.max_systems_global, R, Nz, P->zt_plain, P->t_sig, bufs,
+                                 minpiv, st, P->real_z));
+    P->launches += 2;
     end(); begin(ST_GPROJ);
-    if ((rc = gemm(pp.s5p1))) return rc;
-    if ((rc = gemm(pp.s5p2))) return rc;
+    if ((rc = m8(pp.m5p1, true))) return rc;
+    if ((rc = m8(pp.m5p2, false))) return rc;
     end(); begin(ST_GPLANE);
-    if ((rc = gemm(pp.s5wx))) return rc;
-    if ((rc = gemm(pp.s5wy))) return rc;
+    if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true))) return rc;
+    if ((rc = xform(pp.s5wy, StageDescs{}, pp.s5wy, true))) return rc;
     end(); begin(ST_FACE);
     // step 6
     if ((rc = gemm(pp.s6f))) return rc;
     end(); begin(ST_Z2);
-    CUDA_TRY(launch_zsolve_block(2, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st));
+    CUDA_TRY(launch_zsolve_block(2, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st, P->real_z));
     P->launches++;
     end();
   }
   // step 7
   begin(ST_Y7);
-  if ((rc = gemm(pp.s7y))) return rc;
+  if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false))) return rc;
   end(); begin(ST_X7);
-  if ((rc = gemm(pp.s7x))) return rc;
+  if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true))) return rc;
   end();
   if (nifx + nify > 0) {
     begin(ST_WRITE);
@@ -622,6 +711,14 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
       b.F = T.put(F);
       b.W = T.put(b.B.W);
       b.lam = T.put(b.B.lam);
+      if (b.B.kind != 2) {
+        bool real = true;
+        for (auto& z : F) real = real && z.imag() == 0;
+        if (real) {
+          b.Fr = T.put_real(F);
+          b.Wr = T.put_real(b.B.W);
+        }
+      }
     }
     if (a.G.n) {
       a.Wg = T.put(a.G.W);
@@ -731,6 +828,7 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
     b.p[B_T1] = w + pp_main->off_t1;
     b.p[B_IF] = w + pp_main->off_if;
     b.p[B_RED] = w + pp_main->off_red;
+    b.p[B_CK] = w + pp_main->off_ck;
     double* red = reinterpret_cast<double*>(b.p[B_RED]);
     CUDA_TRY(launch_fill_minpiv(red, st));
     if ((rc = run_pass(P, *pp_main, b, Rc, dt, dt, st))) return rc;

@@ -9,7 +9,7 @@ namespace lfds {
 
 // Device buffers addressed by descriptors (offsets are in elements of the buffer's type:
 // complex128 everywhere except B_F / B_U of an LFDS_F64 plan, which are float64).
-enum BufId { B_TAB = 0, B_F = 1, B_U = 2, B_MS = 3, B_T1 = 4, B_IF = 5, B_RED = 6, NBUF = 8 };
+enum BufId { B_TAB = 0, B_F = 1, B_U = 2, B_MS = 3, B_T1 = 4, B_IF = 5, B_RED = 6, B_CK = 7, NBUF = 8 };
 
 struct Bufs {
   void* p[NBUF];
@@ -42,6 +42,7 @@ struct ZTab {
 struct ZBlock {
   int64_t ms_off;              // offset of this block's mode space [r][k][m][l] in B_MS (and T1)
   int nx, ny;                  // interior sizes (modes)
+  int buf, pad_;               // buffer holding the mode space of a mode-1 solve (B_MS, or B_T1 for step 5)
   int64_t lamx, lamy;          // eigenvalue offsets in TAB
   // pass-2 lifting (reading R8): l~[l,m,k] = -sigma_k (cL Wx[0,l] GL[m,k] + cR Wx[n-1,l] GR[m,k]
   //                                               + cB Wy[0,m] GB[l,k] + cT Wy[n-1,m] GT[l,k])
@@ -76,10 +77,14 @@ struct IfaceRes {
 // launchers (lfds_kernels.cu); return cudaGetLastError()
 cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, int ldB_hint,
                         const Bufs& bufs, cudaStream_t st);
+cudaError_t launch_xform(const GemmDesc* d_descs, int ndesc, int maxM, int64_t maxN, bool real_s, bool kcontig,
+                         const Bufs& bufs, cudaStream_t st);
+cudaError_t launch_xform_m8(const GemmDesc* d_descs, int ndesc, int64_t maxN, bool kcontig, const Bufs& bufs,
+                            cudaStream_t st);
 cudaError_t launch_zsolve_block(int mode, const ZBlock* d_blocks, int nblocks, int max_systems,
                                 int R, int nz, ZTab tab, int64_t sig_off, const Bufs& bufs,
-                                double* d_minpiv, cudaStream_t st);
-cudaError_t launch_gsweep(const GSweep& g, ZTab tab, const Bufs& bufs, double* d_minpiv, cudaStream_t st);
+                                double* d_minpiv, cudaStream_t st, bool realz);
+cudaError_t launch_grank(const GSweep& g, const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_iface_residual(const IfaceRes& p, const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_write_iface_u(int nx, int ny, int nz, int R, int dtype, int nifx, int nify,
                                  int64_t ifx, int64_t ify, int64_t wx, int64_t wy,
@@ -90,5 +95,6 @@ cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, in
                             double2* r, int to_f_units, double* d_norms, const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st);
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
+size_t zsolve_checkpoint_bytes(int nblocks, int max_systems, int nz);
 
 }  // namespace lfds

@@ -1,0 +1,370 @@
+// Block transform passes on the FP64 tensor pipe (DMMA, mma.sync.m8n8k4.f64 -> SASS DMMA.8).
+//
+// Steps 1 and 7 of PAPER.md:66/:72 apply a small n x n eigenvector matrix S (F = W^T M
+// forward, W inverse) along x or along y of every block:
+//     C(i, n) = sum_j S(i, j) B(j, n)                          (GemmDesc addressing)
+// with S in the plan tables and B, C the data (n = every other index of the block).
+// sm_100a has no tcgen05 kind for f64, so the tensor path is the legacy warp-level DMMA
+// (8x8x4, one double per thread for A and B); on B200 it runs at the same 37 TF/s as DFMA
+// (profiles/r01_fp64_peaks.log) but with 8x fewer issued instructions per FMA.
+//
+//  * complex S (C blocks): 4 real MMAs per complex 8x8x4 step (re*re - im*im, re*im + im*re)
+//  * real S (U, R blocks; also exact sine modes): the complex data is viewed as a real matrix
+//    with interleaved (re, im) columns, so C = S B is ONE real GEMM — half the flops.
+// Tiles: CTA 64 (S rows) x 64 (complex data columns), K chunks of 16 double-buffered in
+// shared memory with cp.async (16-byte copies, zero-fill outside the ragged edges).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lfds_internal.h"
+
+namespace lfds {
+
+namespace {
+
+constexpr int XT_M = 64, XT_N = 64, XT_K = 16, XT_THREADS = 128;
+constexpr int LDA_C = XT_M + 2;   // complex A tile row stride (16-B units) == 2 mod 8
+constexpr int LDA_R = XT_M + 4;   // real A tile row stride (8-B units) == 4 mod 16
+constexpr int LDB_C = XT_N + 2;   // complex B tile row stride == 2 mod 8 (real view 2*LDB_C == 4 mod 16)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool REAL_S>
+struct XSmem {
+  static constexpr int A_ELEMS = REAL_S ? XT_K * LDA_R : XT_K * LDA_C * 2;  // in doubles
+  static constexpr int B_ELEMS = XT_K * LDB_C * 2;                          // in doubles
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr size_t BYTES = (size_t)2 * STAGE * sizeof(double);
+};
+
+template <bool REAL_S, bool KCONTIG>
+__global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict__ descs, Bufs bufs) {
+  extern __shared__ __align__(16) double xsm[];
+  const GemmDesc& D = descs[blockIdx.z];
+  const int M = D.M, K = D.K;
+  const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
+  const int i0 = blockIdx.y * XT_M;
+  const int64_t n0 = (int64_t)blockIdx.x * XT_N;
+  if (i0 >= M || n0 >= N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp tile origin (complex columns)
+  const int g = lane >> 2, q = lane & 3;
+
+  const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off;
+  // ---- per-thread load assignments (fixed across K chunks)
+  // A (S): 64 x 16 elements, thread -> row ai = tid/2, 8 consecutive j
+  const int ai = tid >> 1, aj0 = (tid & 1) * 8;
+  const bool arow_ok = (i0 + ai) < M;
+  // B (data): 16 x 64 complex.  Coalesced mappings: K-contiguous data -> 16 threads cover
+  // one 256-byte column segment (8 columns per instruction); otherwise 64 consecutive
+  // threads cover 64 consecutive columns of one row (2 rows per instruction).
+  int64_t bcol[8];
+  int bj, bn0;
+  if (KCONTIG) {  // thread -> j = tid % 16, columns tid/16 + 8e
+    bj = tid & 15;
+    bn0 = tid >> 4;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int64_t n = n0 + bn0 + 8 * e;
+      const int64_t n1 = n / N2, n2 = n - n1 * N2;
+      bcol[e] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
+    }
+  } else {        // thread -> column tid % 64, rows tid/64 + 2e
+    bj = tid >> 6;
+    bn0 = tid & 63;
+    const int64_t n = n0 + bn0;
+    const int64_t n1 = n / N2, n2 = n - n1 * N2;
+    bcol[0] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
+  }
+
+  auto load_chunk = [&](int stage, int j0) {
+    double* As = xsm + stage * XSmem<REAL_S>::STAGE;
+    double2* Bs = reinterpret_cast<double2*>(As + XSmem<REAL_S>::A_ELEMS);
+    if (REAL_S) {
+      const double* A = reinterpret_cast<const double*>(bufs.p[B_TAB]) + D.a_off;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = j0 + aj0 + e;
+        const bool ok = arow_ok && j < K;
+        cp_async8(As + (aj0 + e) * LDA_R + ai, ok ? A + (int64_t)(i0 + ai) * D.sAi + (int64_t)j * D.sAj : A, ok);
+      }
+    } else {
+      const double2* A = reinterpret_cast<const double2*>(bufs.p[B_TAB]) + D.a_off;
+      double2* As2 = reinterpret_cast<double2*>(As);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = j0 + aj0 + e;
+        const bool ok = arow_ok && j < K;
+        cp_async16(As2 + (aj0 + e) * LDA_C + ai, ok ? A + (int64_t)(i0 + ai) * D.sAi + (int64_t)j * D.sAj : A, ok);
+      }
+    }
+    if (KCONTIG) {
+      const int j = j0 + bj;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool ok = bcol[e] >= 0 && j < K;
+        cp_async16(Bs + bj * LDB_C + bn0 + 8 * e, ok ? B + bcol[e] + j : B, ok);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = j0 + bj + 2 * e;
+        const bool ok = bcol[0] >= 0 && j < K;
+        cp_async16(Bs + (bj + 2 * e) * LDB_C + bn0, ok ? B + bcol[0] + (int64_t)j * D.sBj : B, ok);
+      }
+    }
+  };
+
+  // accumulators: complex S -> [4 row tiles][4 col tiles][re/im][2]; real S -> [4][8][2] over
+  // the real view (8 real column tiles of 8 = 32 complex columns)
+  double acc[4][8][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  const int nchunks = (K + XT_K - 1) / XT_K;
+  load_chunk(0, 0);
+  cp_commit();
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) load_chunk((c + 1) & 1, (c + 1) * XT_K);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const double* As = xsm + (c & 1) * XSmem<REAL_S>::STAGE;
+    const double* Bs = As + XSmem<REAL_S>::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < XT_K; kk += 4) {
+      if (REAL_S) {
+        double a[4], b[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[(kk + q) * LDA_R + wm + 8 * i + g];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) b[j] = Bs[(kk + q) * (2 * LDB_C) + 2 * wn + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      } else {
+        const double2* As2 = reinterpret_cast<const double2*>(As);
+        const double2* Bs2 = reinterpret_cast<const double2*>(Bs);
+        double2 a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As2[(kk + q) * LDA_C + wm + 8 * i + g];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs2[(kk + q) * LDB_C + wn + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double nai = -a[i].y;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            // acc[i][2j] = re part, acc[i][2j+1] = im part
+            dmma(acc[i][2 * j][0], acc[i][2 * j][1], a[i].x, b[j].x);
+            dmma(acc[i][2 * j][0], acc[i][2 * j][1], nai, b[j].y);
+            dmma(acc[i][2 * j + 1][0], acc[i][2 * j + 1][1], a[i].x, b[j].y);
+            dmma(acc[i][2 * j + 1][0], acc[i][2 * j + 1][1], a[i].y, b[j].x);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+
+  // ---- epilogue: thread holds C rows (wm + 8i + g), columns 2q, 2q+1 of each 8-wide tile
+  double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
+  auto store = [&](int i, int64_t n, double re, double im) {
+    if (i >= M || n >= N) return;
+    const int64_t n1 = n / N2, n2 = n - n1 * N2;
+    C[(int64_t)i * D.sCi + n1 * D.sC1 + n2 * D.sC2] = make_double2(re, im);
+  };
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i0 + wm + 8 * i + g;
+    if (REAL_S) {
+      // real column 2*wn + 8j + 2q (+1) == complex column wn + 4j + q, (re, im)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) store(row, n0 + wn + 4 * j + q, acc[i][j][0], acc[i][j][1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t col = n0 + wn + 8 * j + 2 * q;
+        store(row, col, acc[i][2 * j][0], acc[i][2 * j + 1][0]);
+        store(row, col + 1, acc[i][2 * j][1], acc[i][2 * j + 1][1]);
+      }
+    }
+  }
+}
+
+template <bool REAL_S, bool KCONTIG>
+cudaError_t launch_one(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
+  const size_t sm = XSmem<REAL_S>::BYTES;
+  cudaError_t e = cudaFuncSetAttribute(k_xform<REAL_S, KCONTIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  for (int z0 = 0; z0 < ndesc; z0 += 65535) {
+    const int nzz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
+    dim3 grid((unsigned)((maxN + XT_N - 1) / XT_N), (unsigned)((maxM + XT_M - 1) / XT_M), (unsigned)nzz);
+    k_xform<REAL_S, KCONTIG><<<grid, XT_THREADS, sm, st>>>(d + z0, bufs);
+  }
+  return cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------- few-row contractions (M <= 8)
+// Step 3 (v on the rows next to the block faces: 2 rows of W) and the step-5 projections
+// (W_x[I_a, l], W_y[I_b, m]: |I| <= 8 rows) contract a whole mode array with at most 8
+// weight rows.  One 8-row DMMA tile, 4 warps across 128 complex data columns; the data
+// stream dominates, so the kernel is HBM-bound by design.
+constexpr int X8_N = 128, X8_K = 16;
+constexpr int LDB8 = X8_N + 2;
+
+template <bool KCONTIG>
+__global__ void __launch_bounds__(XT_THREADS) k_xform_m8(const GemmDesc* __restrict__ descs, Bufs bufs) {
+  extern __shared__ __align__(16) double2 x8sm[];
+  double2 (*As)[X8_K][8 + 2] = reinterpret_cast<double2 (*)[X8_K][8 + 2]>(x8sm);
+  double2 (*Bs)[X8_K][LDB8] = reinterpret_cast<double2 (*)[X8_K][LDB8]>(x8sm + 2 * X8_K * (8 + 2));
+  const GemmDesc& D = descs[blockIdx.z];
+  const int M = D.M, K = D.K;
+  const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
+  const int64_t n0 = (int64_t)blockIdx.x * X8_N;
+  if (n0 >= N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const double2* A = reinterpret_cast<const double2*>(bufs.p[B_TAB]) + D.a_off;
+  const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off;
+  // B loads: 16 x 128 complex = 2048, 16 per thread, coalesced as in k_xform
+  int64_t bcol[16];
+  int bj, bn0;
+  if (KCONTIG) {  // thread -> j = tid % 16, columns tid/16 + 8e
+    bj = tid & 15;
+    bn0 = tid >> 4;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t n = n0 + bn0 + 8 * e;
+      const int64_t n1 = n / N2, n2 = n - n1 * N2;
+      bcol[e] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
+    }
+  } else {        // thread -> column tid, all 16 rows
+    bj = 0;
+    bn0 = tid;
+    const int64_t n = n0 + bn0;
+    const int64_t n1 = n / N2, n2 = n - n1 * N2;
+    bcol[0] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
+  }
+  auto load_chunk = [&](int st, int j0) {
+    if (tid < 8 * X8_K) {  // A: 8 x 16
+      const int i = tid >> 4, j = tid & 15;
+      const bool ok = i < M && j0 + j < K;
+      cp_async16(&As[st][j][i], ok ? A + (int64_t)i * D.sAi + (int64_t)(j0 + j) * D.sAj : A, ok);
+    }
+    if (KCONTIG) {
+      const int j = j0 + bj;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const bool ok = bcol[e] >= 0 && j < K;
+        cp_async16(&Bs[st][bj][bn0 + 8 * e], ok ? B + bcol[e] + j : B, ok);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int j = j0 + e;
+        const bool ok = bcol[0] >= 0 && j < K;
+        cp_async16(&Bs[st][e][bn0], ok ? B + bcol[0] + (int64_t)j * D.sBj : B, ok);
+      }
+    }
+  };
+  double acc[8][2];  // 4 complex column tiles x (re, im)
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int wn = warp * 32;
+  const int nchunks = (K + X8_K - 1) / X8_K;
+  load_chunk(0, 0);
+  cp_commit();
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) load_chunk((c + 1) & 1, (c + 1) * X8_K);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const int st = c & 1;
+#pragma unroll
+    for (int kk = 0; kk < X8_K; kk += 4) {
+      const double2 a = As[st][kk + q][g];
+      const double nai = -a.y;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 b = Bs[st][kk + q][wn + 8 * j + g];
+        dmma(acc[2 * j][0], acc[2 * j][1], a.x, b.x);
+        dmma(acc[2 * j][0], acc[2 * j][1], nai, b.y);
+        dmma(acc[2 * j + 1][0], acc[2 * j + 1][1], a.x, b.y);
+        dmma(acc[2 * j + 1][0], acc[2 * j + 1][1], a.y, b.x);
+      }
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
+  const int row = g;
+  if (row < M) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t n = n0 + wn + 8 * j + 2 * q + h;
+        if (n < N) {
+          const int64_t n1 = n / N2, n2 = n - n1 * N2;
+          C[(int64_t)row * D.sCi + n1 * D.sC1 + n2 * D.sC2] = make_double2(acc[2 * j][h], acc[2 * j + 1][h]);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_xform_m8(const GemmDesc* d_descs, int ndesc, int64_t maxN, bool kcontig, const Bufs& bufs,
+                            cudaStream_t st) {
+  if (ndesc <= 0) return cudaSuccess;
+  for (int z0 = 0; z0 < ndesc; z0 += 65535) {
+    const int nzz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
+    dim3 grid((unsigned)((maxN + X8_N - 1) / X8_N), 1, (unsigned)nzz);
+    const size_t sm = (size_t)2 * X8_K * (8 + 2 + LDB8) * sizeof(double2);
+    if (kcontig) {
+      cudaFuncSetAttribute(k_xform_m8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_xform_m8<true><<<grid, XT_THREADS, sm, st>>>(d_descs + z0, bufs);
+    } else {
+      cudaFuncSetAttribute(k_xform_m8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_xform_m8<false><<<grid, XT_THREADS, sm, st>>>(d_descs + z0, bufs);
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xform(const GemmDesc* d_descs, int ndesc, int maxM, int64_t maxN, bool real_s, bool kcontig,
+                         const Bufs& bufs, cudaStream_t st) {
+  if (ndesc <= 0) return cudaSuccess;
+  if (real_s) return kcontig ? launch_one<true, true>(d_descs, ndesc, maxM, maxN, bufs, st)
+                             : launch_one<true, false>(d_descs, ndesc, maxM, maxN, bufs, st);
+  return kcontig ? launch_one<false, true>(d_descs, ndesc, maxM, maxN, bufs, st)
+                 : launch_one<false, false>(d_descs, ndesc, maxM, maxN, bufs, st);
+}
+
+}  // namespace lfds
