@@ -1,0 +1,153 @@
+"""CPU-side tests of the C-ABI library: it loads, exports every symbol include/lfds.h declares,
+validates its inputs, and its host eigensolver (setup) meets the paper's
+closed forms and the pencil invariants — compared with the oracle's independent LAPACK route.
+No compute call is made (host-only plans, options.device = -1)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.eig import gen_eig
+from oracle.operator import axis_pencil
+from workloads import make_problem, shrunken
+from workloads.configs import axis_steps
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lfds():
+    import paper_1909_01299_b200.lfds as m
+    return m
+
+
+def test_library_exports_every_header_symbol(lfds):
+    with open(os.path.join(ROOT, "include", "lfds.h")) as fh:
+        hdr = fh.read()
+    declared = set(re.findall(r"\b(lfds_[a-z_0-9]+)\s*\(", hdr))
+    assert "lfds_solve" in declared and "lfds_setup_grid" in declared
+    lib = ctypes.CDLL(lfds._LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), name
+    assert declared == set(lfds.EXPORTED)
+    assert "sm_100a" in lfds.version()
+
+
+def test_library_is_built_for_sm100a(lfds):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lfds._LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def host_plan(p, **kw):
+    from paper_1909_01299_b200 import Plan
+    return Plan.from_problem(p, device=-1, **kw)
+
+
+def test_host_only_plan_refuses_compute(lfds):
+    """A host-only plan returns LFDS_ENODEVICE from the C ABI before touching any pointer."""
+    plan = host_plan(shrunken("c2"))
+    P = ctypes.c_void_p
+    rc = lfds._lib.lfds_solve(plan._h, P(256), P(512), 1, P(1024), 4096, None)
+    assert rc == 8 and b"host-only" in lfds._lib.lfds_last_error()
+    assert lfds._lib.lfds_workspace_bytes(plan._h, 1) == 0
+
+
+@pytest.mark.parametrize("bad", [dict(iface_x=[5, 6]), dict(iface_x=[1]), dict(iface_x=[44]),
+                                 dict(iface_x=[9, 4])])
+def test_setup_rejects_bad_partitions(lfds, bad):
+    p = shrunken("c3")
+    with pytest.raises(lfds.LfdsError) as e:
+        host_plan(p.with_partition(bad.get("iface_x", []), []))
+    assert e.value.code == 1
+
+
+def test_setup_rejects_nonpositive_steps(lfds):
+    from paper_1909_01299_b200 import Plan
+    p = shrunken("c2")
+    hx = p.hx.copy()
+    hx[3] = -1.0
+    with pytest.raises(lfds.LfdsError):
+        Plan(hx, p.hy, p.hz, p.sigma_node, p.sigma_edge, p.lam, p.iface_x, p.iface_y, device=-1)
+    with pytest.raises(lfds.LfdsError):
+        Plan(p.hx, p.hy, p.hz, -p.sigma_node, p.sigma_edge, p.lam, p.iface_x, p.iface_y, device=-1)
+
+
+def test_f64_plan_requires_real_inputs(lfds):
+    from paper_1909_01299_b200 import Plan
+    p = shrunken("c2")
+    with pytest.raises(lfds.LfdsError):
+        Plan(p.hx, p.hy, p.hz, p.sigma_node, p.sigma_edge, p.lam, p.iface_x, p.iface_y, device=-1, dtype="f64")
+
+
+@pytest.mark.parametrize("n,h", [(15, 1.0), (127, 1.0), (96, 0.5)])
+def test_uniform_blocks_are_exact_sine_modes(n, h):
+    """Kind U (uniform real steps) uses the closed form of PAPER.md:47/:75."""
+    from paper_1909_01299_b200 import Plan
+    one = np.ones(3)
+    plan = Plan(np.full(n + 1, h), one, one, [1.0, 1.0], [1.0, 1.0, 1.0], 0.3, device=-1)
+    lam, W, kind, lo = plan.basis(0, 0)
+    assert kind == 0 and lo == 1
+    i = np.arange(1, n + 1)
+    lam_cf = np.sort(-(4.0 / h ** 2) * np.sin(np.pi * i / (2 * (n + 1))) ** 2)
+    np.testing.assert_allclose(lam.real, lam_cf, atol=1e-13 / h ** 2)
+    for c in range(n):
+        l = n - c
+        w = np.sqrt(2.0 / (h * (n + 1))) * np.sin(np.pi * i * l / (n + 1))
+        s = np.sign(np.dot(W[:, c].real, w))
+        assert np.abs(s * W[:, c] - w).max() < 4e-14
+
+
+CASES = {
+    "c2_pml_quad": axis_steps(96, 0, 1.0, 16, "quad"),
+    "c3_graded_pml": axis_steps(192, 24, 1.2, 8, "quad"),
+    "c4_pml_const": axis_steps(960, 0, 1.0, 32, "const"),
+    "c4_edge_block": axis_steps(960, 0, 1.0, 32, "const")[:128],
+    "c5_jittered": make_problem("c5").hx,
+    "random_real": np.random.default_rng(7).uniform(0.5, 2.0, 61),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_host_eigensolver_invariants_and_oracle_agreement(case):
+    """A W = M W Lambda, W^T M W = I, and the spectrum agrees with the oracle's LAPACK route."""
+    from paper_1909_01299_b200 import Plan
+    h = CASES[case]
+    one = np.ones(3)
+    plan = Plan(h, one, one, [1.0, 1.0], [1.0, 1.0, 1.0], 0.3, device=-1)
+    lam, W, kind, _ = plan.basis(0, 0)
+    A, m = axis_pencil(h)
+    res = np.abs(A @ W - (m[:, None] * W) * lam[None, :]).max() / (np.abs(A).max() * np.abs(W).max())
+    bio = np.abs(W.T @ (m[:, None] * W) - np.eye(len(m))).max()
+    assert res < 1e-13, res
+    assert bio < 1e-9, bio
+    lo, _ = gen_eig(h)
+    # eigenvalues are simple here; compare as sorted sets (ordering convention R14)
+    d = np.abs(np.sort_complex(lam) - np.sort_complex(lo)).max() / np.abs(lo).max()
+    assert d < 1e-9, d
+
+
+def test_partition_blocks_and_kinds():
+    """C2: blocks 31,31,31,32 with kinds C U U C."""
+    plan = host_plan(make_problem("c2"))
+    info = plan.info()
+    assert (info["nbx"], info["nby"], info["n_if_x"]) == (4, 4, 3)
+    kinds, sizes = [], []
+    for b in range(4):
+        lam, W, kind, lo = plan.basis(0, b)
+        kinds.append(kind)
+        sizes.append(len(lam))
+    assert sizes == [31, 31, 31, 32] and kinds == [2, 0, 0, 2]
+    assert info["eig_max_residual"] < 1e-13 and info["eig_max_biorth"] < 1e-10
+
+
+def test_single_block_global_basis_equals_block_basis():
+    p = shrunken("c3").with_partition([], [])
+    plan = host_plan(p)
+    lam_g, W_g, _, _ = plan.basis(0, -1)
+    lam_b, W_b, _, _ = plan.basis(0, 0)
+    assert np.array_equal(lam_g, lam_b) and np.array_equal(W_g, W_b)
