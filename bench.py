@@ -166,10 +166,15 @@ def stage_algorithmic(p, R: int, plan=None):
     bx, by = sizes(p.nx, p.iface_x), sizes(p.ny, p.iface_y)
     kx = [plan.basis(0, i)[2] if plan else 2 for i in range(len(bx))]
     ky = [plan.basis(1, j)[2] if plan else 2 for j in range(len(by))]
-    fm = lambda kind: 8.0 if kind == 2 else 4.0
     nz = p.nz
-    fl_x = sum(fm(kx[i]) * bx[i] ** 2 * by[j] * nz * R for i in range(len(bx)) for j in range(len(by)))
-    fl_y = sum(fm(ky[j]) * by[j] ** 2 * bx[i] * nz * R for i in range(len(bx)) for j in range(len(by)))
+
+    def fl(kind, n):  # per element of the transformed direction
+        if kind == 0 and (2 * (n + 1)) in (16, 32, 64, 128, 256, 512):
+            L = 2 * (n + 1)   # fast sine transform: complex FFT of the odd extension, 5 L log2 L / n
+            return 5.0 * L * math.log2(L) / n
+        return (8.0 if kind == 2 else 4.0) * n  # dense complex / real eigenvector matrix
+    fl_x = sum(fl(kx[i], bx[i]) * bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by)))
+    fl_y = sum(fl(ky[j], by[j]) * bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by)))
     el_blk = sum(nx * ny * nz * R for nx in bx for ny in by)
     el_all = p.nx * p.ny * nz * R
     nif = len(p.iface_x) + len(p.iface_y)

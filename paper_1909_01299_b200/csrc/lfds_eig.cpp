@@ -277,9 +277,10 @@ bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err) {
     const long double hs = h[0].real();
     const long double pi = 3.141592653589793238462643383279502884L;
     const long double sc = std::sqrt(2.0L / (hs * (n + 1)));
-    // ascending eigenvalue order: column c holds sine mode l = n - c
+    // natural mode order: column c holds sine mode l = c + 1, so that the forward and
+    // inverse transforms of a U block are plain DST-I (the fast sine-transform kernel)
     for (int c = 0; c < n; ++c) {
-      int l = n - c;
+      int l = c + 1;
       long double sl = std::sin(pi * l / (2.0L * (n + 1)));
       lamL[c] = lc(-(4.0L / (hs * hs)) * sl * sl, 0);
       for (int p = 0; p < n; ++p) WL[(size_t)p * n + c] = lc(sc * std::sin(pi * (long double)(p + 1) * l / (n + 1)), 0);

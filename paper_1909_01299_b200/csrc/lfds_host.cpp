@@ -54,6 +54,8 @@ struct AxisBlock {
   Basis B;
   int64_t F = 0, W = 0, lam = 0;  // TAB offsets: F[l*n+p] = W[p][l] hh_p, W[p*n+l], lam[l]
   int64_t Fr = -1, Wr = -1;       // real copies (offsets in doubles) when the basis is real (U, R)
+  bool dst = false;               // U block with 2(n+1) a supported FFT length: fast sine transform
+  double dst_fwd = 0, dst_inv = 0;  // DST-I scale factors sqrt(2h/N), sqrt(2/(hN))
 };
 
 struct Axis {
@@ -96,6 +98,7 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   ZBlock* d_zb = nullptr;
   StageDescs s1x, s1y, s3g, s3h, s3x, s3y, s5r1, s5r2, s5p1, s5p2, s5wx, s5wy, s6f, s7y, s7x;
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
+  std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
   StageDescs m3g, m3h, m5p1, m5p2;                    // few-row DMMA contractions (<= 8 rows each)
   bool use_xform = false;
   int max_systems = 0, max_systems_global = 0;
@@ -392,23 +395,31 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   pp.use_xform = !in_real && !out_real;
   if (pp.use_xform) {
     std::vector<GemmDesc> vc, vr;
-    auto split = [&](StageDescs& sc, StageDescs& sr, const StageDescs& src, bool xaxis, bool fwd) {
+    auto split = [&](StageDescs& sc, StageDescs& sr, std::vector<std::pair<int, StageDescs>>& sd,
+                     const StageDescs& src, bool xaxis, bool fwd) {
+      std::map<int, std::vector<GemmDesc>> vd;  // DST descriptors grouped by block length
       for (int q = 0; q < src.n; ++q) {
         GemmDesc d = D[src.off + q];
-        // recover the block of this descriptor: stages s1x/s7x have one desc per block, s1y/s7y too
+        // stages s1x/s7x/s1y/s7y hold one descriptor per block, in block order
         const int b = q;
         const AxisBlock& ab = xaxis ? X.blocks[b % nbx] : Y.blocks[b / nbx];
         const int64_t roff = fwd ? ab.Fr : ab.Wr;
-        if (roff >= 0) { d.a_off = roff; vr.push_back(d); }
+        if (ab.dst) { d.scale = fwd ? ab.dst_fwd : ab.dst_inv; vd[ab.n].push_back(d); }
+        else if (roff >= 0) { d.a_off = roff; vr.push_back(d); }
         else vc.push_back(d);
       }
       stage(sc, std::move(vc)); vc.clear();
       stage(sr, std::move(vr)); vr.clear();
+      for (auto& kv : vd) {
+        StageDescs t;
+        stage(t, std::move(kv.second));
+        sd.emplace_back(kv.first, t);
+      }
     };
-    split(pp.x1c, pp.x1r, pp.s1x, true, true);
-    split(pp.y1c, pp.y1r, pp.s1y, false, true);
-    split(pp.y7c, pp.y7r, pp.s7y, false, false);
-    split(pp.x7c, pp.x7r, pp.s7x, true, false);
+    split(pp.x1c, pp.x1r, pp.x1s, pp.s1x, true, true);
+    split(pp.y1c, pp.y1r, pp.y1s, pp.s1y, false, true);
+    split(pp.y7c, pp.y7r, pp.y7s, pp.s7y, false, false);
+    split(pp.x7c, pp.x7r, pp.x7s, pp.s7x, true, false);
   }
 
   CUDA_TRY(cudaMalloc(&pp.d_descs, sizeof(GemmDesc) * std::max<size_t>(1, D.size())));
@@ -479,8 +490,14 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     P->launches += (s.n + 65534) / 65535;
     return LFDS_OK;
   };
-  auto xform = [&](const StageDescs& sc, const StageDescs& sr, const StageDescs& generic, bool kcontig) -> int {
+  auto xform = [&](const StageDescs& sc, const StageDescs& sr, const StageDescs& generic, bool kcontig,
+                   const std::vector<std::pair<int, StageDescs>>* sd = nullptr) -> int {
     if (!pp.use_xform) return gemm(generic);
+    if (sd)
+      for (auto& kv : *sd) {
+        CUDA_TRY(launch_dst(pp.d_descs + kv.second.off, kv.second.n, kv.first, kv.second.maxN, kcontig, bufs, st));
+        P->launches += (kv.second.n + 65534) / 65535;
+      }
     if (sc.n) {
       CUDA_TRY(launch_xform(pp.d_descs + sc.off, sc.n, sc.maxM, sc.maxN, false, kcontig, bufs, st));
       P->launches += (sc.n + 65534) / 65535;
@@ -494,9 +511,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   int rc;
   // pass 1
   begin(ST_X1);
-  if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true))) return rc;
+  if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s))) return rc;
   end(); begin(ST_Y1);
-  if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false))) return rc;
+  if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s))) return rc;
   end(); begin(ST_Z1);
   CUDA_TRY(launch_zsolve_block(1, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st, P->real_z));
   P->launches++;
@@ -546,9 +563,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   }
   // step 7
   begin(ST_Y7);
-  if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false))) return rc;
+  if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false, &pp.y7s))) return rc;
   end(); begin(ST_X7);
-  if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true))) return rc;
+  if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s))) return rc;
   end();
   if (nifx + nify > 0) {
     begin(ST_WRITE);
@@ -711,6 +728,12 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
       b.F = T.put(F);
       b.W = T.put(b.B.W);
       b.lam = T.put(b.B.lam);
+      if (b.B.kind == 0 && dst_supported(b.n)) {
+        const double h = a.h[b.lo - 1].real(), Nn = b.n + 1.0;
+        b.dst = true;
+        b.dst_fwd = std::sqrt(2.0 * h / Nn);
+        b.dst_inv = std::sqrt(2.0 / (h * Nn));
+      }
       if (b.B.kind != 2) {
         bool real = true;
         for (auto& z : F) real = real && z.imag() == 0;

@@ -29,6 +29,7 @@ struct GemmDesc {
   int64_t c_off, sCi, sC1, sC2;
   int M, K, N1, N2;
   int b_buf, c_buf, flags, pad;
+  double scale;                // used by the sine-transform kernel (alpha)
 };
 
 // z-tables: per row k the tridiagonal row (a_k x_{k-1} + (g_k + s e_k) x_k + c_k x_{k+1})
@@ -81,6 +82,9 @@ cudaError_t launch_xform(const GemmDesc* d_descs, int ndesc, int maxM, int64_t m
                          const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_xform_m8(const GemmDesc* d_descs, int ndesc, int64_t maxN, bool kcontig, const Bufs& bufs,
                             cudaStream_t st);
+bool dst_supported(int n);
+cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, bool kcontig, const Bufs& bufs,
+                       cudaStream_t st);
 cudaError_t launch_zsolve_block(int mode, const ZBlock* d_blocks, int nblocks, int max_systems,
                                 int R, int nz, ZTab tab, int64_t sig_off, const Bufs& bufs,
                                 double* d_minpiv, cudaStream_t st, bool realz);

@@ -636,21 +636,32 @@ __global__ void k_residual(ResParams P, const void* __restrict__ u, const void* 
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const int nx = P.nx, ny = P.ny, nz = P.nz;
   const int64_t plane = (int64_t)nx * ny, vol = plane * nz, total = vol * P.R;
+  // per-rhs partial norms: registers -> block reduction in shared memory -> one atomic per
+  // block and rhs (a per-thread atomic on two addresses serialises the whole kernel)
   double acc_r = 0, acc_b = 0;
   int rcur = -1;
   auto flush = [&](int rr) {
-    if (rr >= 0 && norms) {
-      atomicAdd(norms + 2 * rr, acc_r);
-      atomicAdd(norms + 2 * rr + 1, acc_b);
+    if (!norms) return;
+    double a = acc_r, b2 = acc_b;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b2 += __shfl_xor_sync(0xffffffffu, b2, o);
+    }
+    if (rr >= 0 && (threadIdx.x & 31) == 0) {
+      atomicAdd(norms + 2 * rr, a);
+      atomicAdd(norms + 2 * rr + 1, b2);
     }
     acc_r = acc_b = 0;
   };
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(t % nx);
-    const int j = (int)((t / nx) % ny);
-    const int k = (int)((t / plane) % nz);
-    const int r = (int)(t / vol);
-    if (r != rcur) { flush(rcur); rcur = r; }
+  (void)total;
+  for (int r = 0; r < P.R; ++r) {
+  rcur = r;
+  for (int64_t tl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; tl < vol; tl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = (int64_t)r * vol + tl;
+    const int i = (int)(tl % nx);
+    const int j = (int)((tl / nx) % ny);
+    const int k = (int)(tl / plane);
     const cplx uc = load_u(u, P.dtype, t);
     const cplx ul = i > 0 ? load_u(u, P.dtype, t - 1) : mk(0, 0);
     const cplx ur = i < nx - 1 ? load_u(u, P.dtype, t + 1) : mk(0, 0);
@@ -706,6 +717,7 @@ __global__ void k_residual(ResParams P, const void* __restrict__ u, const void* 
     }
   }
   flush(rcur);
+  }
 }
 
 cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int ddm, int has_f, int64_t hx, int64_t hy,

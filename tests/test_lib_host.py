@@ -93,10 +93,10 @@ def test_uniform_blocks_are_exact_sine_modes(n, h):
     lam, W, kind, lo = plan.basis(0, 0)
     assert kind == 0 and lo == 1
     i = np.arange(1, n + 1)
-    lam_cf = np.sort(-(4.0 / h ** 2) * np.sin(np.pi * i / (2 * (n + 1))) ** 2)
+    lam_cf = -(4.0 / h ** 2) * np.sin(np.pi * i / (2 * (n + 1))) ** 2
     np.testing.assert_allclose(lam.real, lam_cf, atol=1e-13 / h ** 2)
     for c in range(n):
-        l = n - c
+        l = c + 1  # natural sine order for U blocks (the fast sine transform's order)
         w = np.sqrt(2.0 / (h * (n + 1))) * np.sin(np.pi * i * l / (n + 1))
         s = np.sign(np.dot(W[:, c].real, w))
         assert np.abs(s * W[:, c] - w).max() < 4e-14
