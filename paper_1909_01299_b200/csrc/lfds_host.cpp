@@ -3,11 +3,11 @@
 // lfds_solve enqueues the seven steps as stream-ordered kernels:
 //
 //   pass 1 (per block S^ij)   step 1  f~ = (F_x (x) F_y (x) I) f,  F = W^T M      (k_gemm x2)
-//                             step 2  T_lm v~_lm = f~_lm (z-solves)               (k_zsolve_block<1>)
+//                             step 2  T_lm v~_lm = f~_lm (z-solves)               (k_zs<1>)
 //                             step 3  v at the rows next to every block face      (k_gemm x4)
 //   interface                 step 4  r_b = b - A v on the interface planes       (k_iface_res)
-//                             step 5  w on the planes via the global bases        (k_gemm, k_grank, k_zsolve_block)
-//   pass 2 (per block)        step 6  w~ from the Dirichlet lifting of w          (k_gemm, k_zsolve_block<2>)
+//                             step 5  w on the planes via the global bases        (k_xform, k_zs<3>, k_xform_m8)
+//   pass 2 (per block)        step 6  w~ from the Dirichlet lifting of w          (k_gemm, k_zs<2>)
 //                             step 7  u = (W_x (x) W_y (x) I)(v~ + w~), u = w on planes (k_gemm x2, k_write_iface)
 //
 // optional refinement: r = M f - A u in double-double (k_residual), u += solve(r).
@@ -96,10 +96,12 @@ struct StageDescs {
 struct PassPlan {  // descriptors for one (R, in_real, out_real)
   GemmDesc* d_descs = nullptr;
   ZBlock* d_zb = nullptr;
+  PDesc* d_pd = nullptr;     // step-3 two-sided edge projections, one per block
+  int n_pd3 = 0;
   StageDescs s1x, s1y, s3g, s3h, s3x, s3y, s5r1, s5r2, s5p1, s5p2, s5wx, s5wy, s6f, s7y, s7x;
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
   std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
-  StageDescs m3g, m3h, m5p1, m5p2;                    // few-row DMMA contractions (<= 8 rows each)
+  StageDescs m5p1, m5p2;                    // few-row DMMA contractions (<= 8 rows each)
   bool use_xform = false;
   int max_systems = 0, max_systems_global = 0;
   // workspace layout (bytes)
@@ -215,7 +217,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   pp.off_if = off; off = al256(off + if_elems * 16);
   pp.off_red = off; off = al256(off + (size_t)(2 * R + 8) * 8);
   pp.off_ck = off;
-  off = al256(off + std::max(zsolve_checkpoint_bytes(nblk, maxsys, Nz), zsolve_checkpoint_bytes(1, Nx * Ny * R, Nz)));
+  off = al256(off + std::max(zsolve_checkpoint_bytes(nblk, P->lpad, P->mpad, R, Nz), zsolve_checkpoint_bytes(1, Nx, Ny, R, Nz)));
   pp.off_res = off;
   if (P->opt.refine != 0) off = al256(off + (size_t)Nx * Ny * Nz * R * 16);
   pp.total = off;
@@ -386,8 +388,6 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
       }
       stage(dst, std::move(vm)); vm.clear();
     };
-    split8(pp.m3g, pp.s3g);
-    split8(pp.m3h, pp.s3h);
     split8(pp.m5p1, pp.s5p1);
     split8(pp.m5p2, pp.s5p2);
   }
@@ -435,6 +435,36 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     g.gL = g.gR = g.gB = g.gT = -1;
     zb.push_back(g);
     pp.max_systems_global = Nx * Ny * R;
+  }
+  {  // step 3: G = (edge rows of W_x) v~, H = (edge rows of W_y) v~, one read of v~ per block
+    std::vector<PDesc> pd;
+    for (int j = 0; j < nby; ++j)
+      for (int i = 0; i < nbx; ++i) {
+        const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
+        const int b = j * nbx + i;
+        PDesc d{};
+        d.x_off = ms[b];
+        d.ps = (int64_t)bx.n * by.n;
+        d.x_buf = B_MS;
+        d.nx = bx.n;
+        d.ny = by.n;
+        d.nplanes = (int)RZ;
+        d.E1 = d.E2 = 2;
+        d.wr = bx.W;                                 // rows p = 0 and p = n-1 of W_x
+        d.wr_es = (int64_t)(bx.n - 1) * bx.n;
+        d.wc = by.W;
+        d.wc_es = (int64_t)(by.n - 1) * by.n;
+        d.g_off = pp.g_off + (int64_t)b * 2 * RZ * P->mpad;  // G[b][e][rk][m]
+        d.g_es = RZ * P->mpad;
+        d.g_ps = P->mpad;
+        d.h_off = pp.h_off + (int64_t)b * 2 * RZ * P->lpad;  // H[b][e][rk][l]
+        d.h_es = RZ * P->lpad;
+        d.h_ps = P->lpad;
+        pd.push_back(d);
+      }
+    pp.n_pd3 = (int)pd.size();
+    CUDA_TRY(cudaMalloc(&pp.d_pd, sizeof(PDesc) * std::max<size_t>(1, pd.size())));
+    CUDA_TRY(cudaMemcpy(pp.d_pd, pd.data(), sizeof(PDesc) * pd.size(), cudaMemcpyHostToDevice));
   }
   CUDA_TRY(cudaMalloc(&pp.d_zb, sizeof(ZBlock) * zb.size()));
   CUDA_TRY(cudaMemcpy(pp.d_zb, zb.data(), sizeof(ZBlock) * zb.size(), cudaMemcpyHostToDevice));
@@ -515,13 +545,13 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   end(); begin(ST_Y1);
   if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s))) return rc;
   end(); begin(ST_Z1);
-  CUDA_TRY(launch_zsolve_block(1, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st, P->real_z));
+  CUDA_TRY(launch_zsolve(1, pp.d_zb, nblk, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv, st, P->real_z));
   P->launches++;
   end();
   if (nifx + nify > 0) {
     begin(ST_EDGE);
-    if ((rc = m8(pp.m3g, true))) return rc;
-    if ((rc = m8(pp.m3h, false))) return rc;
+    CUDA_TRY(launch_proj(pp.d_pd, pp.n_pd3, P->lpad, 2, R * Nz, st, bufs));
+    P->launches++;
     if ((rc = gemm(pp.s3x))) return rc;
     if ((rc = gemm(pp.s3y))) return rc;
     end(); begin(ST_IFRES);
@@ -543,10 +573,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     GSweep g{};
     g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
     g.lamx = X.lamg; g.lamy = Y.lamg; g.wxi = X.WI; g.wyi = Y.WI; g.r1 = pp.r1; g.r2 = pp.r2; g.what = 0;
-    CUDA_TRY(launch_grank(g, bufs, st));
-    CUDA_TRY(launch_zsolve_block(1, pp.d_zb + nblk, 1, pp.max_systems_global, R, Nz, P->zt_plain, P->t_sig, bufs,
-                                 minpiv, st, P->real_z));
-    P->launches += 2;
+    CUDA_TRY(launch_zsolve(3, pp.d_zb + nblk, 1, Nx, Ny, R, Nz, P->zt_plain, P->t_sig, &g, bufs, minpiv, st,
+                           P->real_z));
+    P->launches += 1;
     end(); begin(ST_GPROJ);
     if ((rc = m8(pp.m5p1, true))) return rc;
     if ((rc = m8(pp.m5p2, false))) return rc;
@@ -557,7 +586,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     // step 6
     if ((rc = gemm(pp.s6f))) return rc;
     end(); begin(ST_Z2);
-    CUDA_TRY(launch_zsolve_block(2, pp.d_zb, nblk, pp.max_systems, R, Nz, P->zt_scaled, P->t_sig, bufs, minpiv, st, P->real_z));
+    CUDA_TRY(launch_zsolve(2, pp.d_zb, nblk, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv, st, P->real_z));
     P->launches++;
     end();
   }
@@ -1006,6 +1035,7 @@ void lfds_destroy(lfds_plan* P) {
   for (auto& kv : P->passes) {
     cudaFree(kv.second.d_descs);
     cudaFree(kv.second.d_zb);
+    cudaFree(kv.second.d_pd);
   }
   if (P->d_tab) cudaFree(P->d_tab);
   for (auto& r : P->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

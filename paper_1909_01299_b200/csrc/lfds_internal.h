@@ -75,6 +75,20 @@ struct IfaceRes {
   int qpad, ppad;              // padded row lengths of the step-3 arrays VX / VY
 };
 
+// Two-sided projection of mode planes (lfds_proj.cu): G[e][p][m] = sum_l Wr[e][l] X[p][m][l],
+// H[e][p][l] = sum_m Wc[e][m] X[p][m][l] (step 3 edge values, E1 = E2 = 2).
+struct PDesc {
+  int64_t x_off, ps;           // plane p of X at x_off + p*ps in buffer x_buf; row m at + m*nx
+  int x_buf, nx, ny, nplanes;
+  int E1, E2, pad0, pad1;
+  int64_t wr, wr_es;           // TAB: Wr[e][l] at wr + e*wr_es + l
+  int64_t wc, wc_es;           // TAB: Wc[e][m] at wc + e*wc_es + m
+  int64_t g_off, g_es, g_ps;   // IF: G[e][p][m] at g_off + e*g_es + p*g_ps + m
+  int64_t h_off, h_es, h_ps;   // IF: H[e][p][l] at h_off + e*h_es + p*h_ps + l
+};
+cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, int maxplanes, cudaStream_t st,
+                        const Bufs& bufs);
+
 // launchers (lfds_kernels.cu); return cudaGetLastError()
 cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, int ldB_hint,
                         const Bufs& bufs, cudaStream_t st);
@@ -85,10 +99,11 @@ cudaError_t launch_xform_m8(const GemmDesc* d_descs, int ndesc, int64_t maxN, bo
 bool dst_supported(int n);
 cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, bool kcontig, const Bufs& bufs,
                        cudaStream_t st);
-cudaError_t launch_zsolve_block(int mode, const ZBlock* d_blocks, int nblocks, int max_systems,
-                                int R, int nz, ZTab tab, int64_t sig_off, const Bufs& bufs,
-                                double* d_minpiv, cudaStream_t st, bool realz);
-cudaError_t launch_grank(const GSweep& g, const Bufs& bufs, cudaStream_t st);
+// z-solves (lfds_zsolve.cu): mode 1 = in place (step 2), 2 = Dirichlet lifting added to v~
+// (step 6), 3 = step-5 global modes with the rank-|I| RHS built from R1/R2 (g != NULL)
+cudaError_t launch_zsolve(int mode, const ZBlock* d_blocks, int nblocks, int max_nx, int max_ny, int R, int nz,
+                          ZTab tab, int64_t sig_off, const GSweep* g, const Bufs& bufs, double* d_minpiv,
+                          cudaStream_t st, bool realz);
 cudaError_t launch_iface_residual(const IfaceRes& p, const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_write_iface_u(int nx, int ny, int nz, int R, int dtype, int nifx, int nify,
                                  int64_t ifx, int64_t ify, int64_t wx, int64_t wy,
@@ -99,6 +114,6 @@ cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, in
                             double2* r, int to_f_units, double* d_norms, const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st);
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
-size_t zsolve_checkpoint_bytes(int nblocks, int max_systems, int nz);
+size_t zsolve_checkpoint_bytes(int nblocks, int max_nx, int max_ny, int R, int nz);
 
 }  // namespace lfds

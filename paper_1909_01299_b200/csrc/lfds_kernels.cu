@@ -3,10 +3,7 @@
 //  k_gemm          strided batched complex contraction: block forward/inverse transforms
 //                  (steps 1 and 7), interface-adjacent evaluation (step 3), sparse global
 //                  transforms (step 5), face transforms for the Dirichlet lifting (step 6).
-//  k_zsolve_block  per-mode z tridiagonal solves of a block pass (steps 2 and 6): one thread
-//                  per system, Thomas with shared-memory checkpoints of c' (coalesced rows).
-//  k_grank         step 5's rank-|I| right-hand side for every global mode (then solved
-//                  in place by k_zsolve_block<1> with the global eigenvalues).
+//  (z-solves of steps 2, 5 and 6: lfds_zsolve.cu)
 //  k_iface_res     step 4: residual b - A v on the interface planes.
 //  k_write_iface   u = w on the interface planes (last sentence).
 //  k_residual      r = M f - A u (Eq. (fd)), fp64 or double-double (refinement, reading R13).
@@ -165,287 +162,6 @@ cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, 
     dim3 grid((unsigned)((maxN + GTN - 1) / GTN), (unsigned)((maxM + GTM - 1) / GTM), (unsigned)nz);
     k_gemm<<<grid, 256, 0, st>>>(d_descs + z0, bufs);
   }
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------- z tridiagonal solves
-// One thread per system ("split into multiple tridiagonal systems ... O(N_z)").
-// Mode space is [r][k][mode] (mode contiguous), so every row access of a warp is one
-// coalesced 512-byte transaction.  Thomas elimination without pivoting (reading R15):
-//   forward   r_k = b_k - a_k c'_{k-1},  c'_k = c_k / r_k,  d'_k = (d_k - a_k d'_{k-1}) / r_k
-//   backward  x_k = d'_k - c'_k x_{k+1}
-// Neither c' nor d' goes to memory: the forward sweep keeps a (c', d') checkpoint at the
-// start of every ZSEG-row segment (a coalesced global scratch, 4 B per row, which keeps
-// shared memory and registers small enough for 4 CTAs per SM); the backward sweep recomputes each
-// segment into registers from its checkpoint and back-substitutes.  RHS(k) is therefore
-// evaluated twice per row (a re-read of the input line, or an L2-resident expression).
-// A pivot monitor keeps min |r_k|^2 / (|b_k|^2 + (|a_k|+|c_k|)^2) (reported as its sqrt).
-// The z tables of every config are real (real sigma, h_z, lambda): REALZ specialises
-// a, c, g, e to real numbers, halving the arithmetic of the recurrence.
-constexpr int ZSEG = 8;
-constexpr int ZTHREADS = 128;
-
-struct ZSmem {      // staged tables: real -> ag[k] = (a, g), ce[k] = (c, e), m2[k] = (|a|+|c|)^2
-  double2 *ag, *ce; // complex -> sa, sg, sc, se (4 arrays of nz double2), m2 unused
-  double2 *sa, *sg, *sc, *se;
-  double* m2;
-  double2* ck;       // checkpoints: ck[(2 seg + {0: c', 1: d'}) * cks]
-  int64_t cks;       // checkpoint stride (systems per launch slot)
-};
-
-template <bool REALZ>
-__device__ __forceinline__ void zrow(const ZSmem& T, int k, cplx s, cplx& a, cplx& b, cplx& c, double& m2) {
-  if (REALZ) {
-    const double2 ag = T.ag[k], ce = T.ce[k];
-    a = mk(ag.x, 0); c = mk(ce.x, 0);
-    b = mk(fma(s.x, ce.y, ag.y), s.y * ce.y);
-    m2 = T.m2[k];
-  } else {
-    const double2 a2 = T.sa[k], g2 = T.sg[k], c2 = T.sc[k], e2 = T.se[k];
-    a = mk(a2.x, a2.y); c = mk(c2.x, c2.y);
-    b = cfma(s, mk(e2.x, e2.y), mk(g2.x, g2.y));
-    const double t = cabs1(a) + cabs1(c);
-    m2 = t * t;
-  }
-}
-
-// one Thomas row: in/out (cp, dp); real a, c use 2 multiplies instead of 4
-template <bool REALZ>
-__device__ __forceinline__ cplx thomas_step(cplx a, cplx b, cplx c, cplx d, cplx& cp, cplx& dp) {
-  cplx r, t;
-  if (REALZ) {
-    r = mk(fma(-a.x, cp.x, b.x), fma(-a.x, cp.y, b.y));
-    t = mk(fma(-a.x, dp.x, d.x), fma(-a.x, dp.y, d.y));
-  } else {
-    r = b - a * cp;
-    t = d - a * dp;
-  }
-  const double n2 = fma(r.x, r.x, r.y * r.y);
-  const double in = fast_rcp(n2);
-  const cplx inv = mk(r.x * in, -r.y * in);
-  cp = REALZ ? mk(c.x * inv.x, c.x * inv.y) : c * inv;
-  dp = t * inv;
-  return mk(n2, 0);
-}
-
-template <bool REALZ, bool FULL, bool ADD, class RHS>
-__device__ __forceinline__ void thomas_line(int nz, const ZSmem& T, cplx s, double2* __restrict__ dst, int64_t stride,
-                                            RHS rhs, double2* __restrict__ acc_line, float& minpiv) {
-  const int nseg = (nz + ZSEG - 1) / ZSEG;
-  cplx cp = mk(0, 0), dp = mk(0, 0);
-  for (int sgi = 0; sgi < nseg; ++sgi) {
-    const int k0 = sgi * ZSEG;
-    T.ck[(2 * sgi) * T.cks] = make_double2(cp.x, cp.y);
-    T.ck[(2 * sgi + 1) * T.cks] = make_double2(dp.x, dp.y);
-    cplx rb[ZSEG];
-#pragma unroll
-    for (int j = 0; j < ZSEG; ++j) rb[j] = (FULL || k0 + j < nz) ? rhs(k0 + j) : mk(0, 0);
-#pragma unroll
-    for (int j = 0; j < ZSEG; ++j) {
-      const int k = k0 + j;
-      if (FULL || k < nz) {
-        cplx a, b, c;
-        double m2;
-        zrow<REALZ>(T, k, s, a, b, c, m2);
-        const double n2 = thomas_step<REALZ>(a, b, c, rb[j], cp, dp).x;
-        minpiv = fminf(minpiv, __fdividef((float)n2, (float)(fma(b.x, b.x, fma(b.y, b.y, m2)))));
-      }
-    }
-  }
-  cplx x = mk(0, 0);
-  for (int sgi = nseg - 1; sgi >= 0; --sgi) {
-    const int k0 = sgi * ZSEG;
-    cplx rb[ZSEG], cs[ZSEG];
-#pragma unroll
-    for (int j = 0; j < ZSEG; ++j) rb[j] = (FULL || k0 + j < nz) ? rhs(k0 + j) : mk(0, 0);
-    double2 t = T.ck[(2 * sgi) * T.cks];
-    cplx cc = mk(t.x, t.y);
-    t = T.ck[(2 * sgi + 1) * T.cks];
-    cplx dd = mk(t.x, t.y);
-#pragma unroll
-    for (int j = 0; j < ZSEG; ++j) {  // rb[j] becomes d'_j, cs[j] = c'_j
-      const int k = k0 + j;
-      if (FULL || k < nz) {
-        cplx a, b, c;
-        double m2;
-        zrow<REALZ>(T, k, s, a, b, c, m2);
-        thomas_step<REALZ>(a, b, c, rb[j], cc, dd);
-      }
-      cs[j] = cc;
-      rb[j] = dd;
-    }
-#pragma unroll
-    for (int j = ZSEG - 1; j >= 0; --j) {
-      const int k = k0 + j;
-      if (FULL || k < nz) {
-        x = rb[j] - cs[j] * x;
-        if (ADD) {
-          const double2 o = acc_line[k * stride];
-          acc_line[k * stride] = make_double2(o.x + x.x, o.y + x.y);
-        } else {
-          dst[k * stride] = make_double2(x.x, x.y);
-        }
-      }
-    }
-  }
-}
-
-template <bool REALZ>
-__device__ __forceinline__ ZSmem stage_ztab(ZTab tab, const double2* TAB, int nz, double2* zsm) {
-  ZSmem T{};
-  if (REALZ) {
-    T.ag = zsm;
-    T.ce = zsm + nz;
-    T.m2 = reinterpret_cast<double*>(zsm + 2 * nz);
-    for (int k = threadIdx.x; k < nz; k += blockDim.x) {
-      const double a = TAB[tab.a + k].x, c = TAB[tab.c + k].x;
-      T.ag[k] = make_double2(a, TAB[tab.g + k].x);
-      T.ce[k] = make_double2(c, TAB[tab.e + k].x);
-      T.m2[k] = (fabs(a) + fabs(c)) * (fabs(a) + fabs(c));
-    }
-  } else {
-    T.sa = zsm; T.sg = zsm + nz; T.sc = zsm + 2 * nz; T.se = zsm + 3 * nz;
-    for (int k = threadIdx.x; k < nz; k += blockDim.x) {
-      T.sa[k] = TAB[tab.a + k]; T.sg[k] = TAB[tab.g + k]; T.sc[k] = TAB[tab.c + k]; T.se[k] = TAB[tab.e + k];
-    }
-  }
-  __syncthreads();
-  return T;
-}
-
-__device__ __forceinline__ void block_min_commit(float v, double* out) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0 && out) atomic_min_pos(out, (double)sqrtf(v));
-}
-
-static size_t zsmem_bytes(int nz, bool realz) {
-  return realz ? (size_t)(2 * nz + (nz + 1) / 2) * sizeof(double2) : (size_t)4 * nz * sizeof(double2);
-}
-
-// mode 1: solve in place (step 2: RHS = transformed f; step 5: RHS = k_grank output).
-// mode 2: pass-2 Dirichlet lifting (step 6): RHS built from the face transforms, solution
-// ADDED to the stored v~ (u~ = v~ + w~).
-template <int MODE, bool REALZ, bool FULL>
-__global__ void __launch_bounds__(ZTHREADS, 4) k_zsolve_block(const ZBlock* __restrict__ blocks, int R, int nz,
-                                                             ZTab tab, int64_t sig_off, Bufs bufs, double* minpiv_out) {
-  extern __shared__ double2 zsm[];
-  const ZBlock B = blocks[blockIdx.y];  // by value: no reloads after the stores below
-  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
-  ZSmem T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
-  const int nxy = B.nx * B.ny;
-  const int64_t sys = (int64_t)blockIdx.x * ZTHREADS + threadIdx.x;
-  T.cks = (int64_t)gridDim.x * ZTHREADS;
-  T.ck = reinterpret_cast<double2*>(bufs.p[B_CK]) + (int64_t)blockIdx.y * 2 * ((nz + ZSEG - 1) / ZSEG) * T.cks + sys;
-  float minpiv = 1.0f;
-  if (sys < (int64_t)nxy * R) {
-    const int r = (int)(sys / nxy);
-    const int mode = (int)(sys - (int64_t)r * nxy);
-    const int l = mode % B.nx, m = mode / B.nx;
-    const cplx s = ld(TAB + B.lamx + l) + ld(TAB + B.lamy + m);
-    double2* MS = reinterpret_cast<double2*>(bufs.p[MODE == 1 ? B.buf : B_MS]) + B.ms_off + (int64_t)r * nz * nxy + mode;
-    if (MODE == 1) {
-      thomas_line<REALZ, FULL, false>(nz, T, s, MS, nxy,
-                                      [&](int k) { const double2 v = MS[(int64_t)k * nxy]; return mk(v.x, v.y); },
-                                      nullptr, minpiv);
-    } else {
-      const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
-      const cplx cL = mk(B.cL.x, B.cL.y) * ld(TAB + B.wx0 + l), cR = mk(B.cR.x, B.cR.y) * ld(TAB + B.wx1 + l);
-      const cplx cB = mk(B.cB.x, B.cB.y) * ld(TAB + B.wy0 + m), cT = mk(B.cT.x, B.cT.y) * ld(TAB + B.wy1 + m);
-      const double2* gL = B.gL >= 0 ? IF + B.gL + (int64_t)r * nz * B.fstride + m : nullptr;
-      const double2* gR = B.gR >= 0 ? IF + B.gR + (int64_t)r * nz * B.fstride + m : nullptr;
-      const double2* gB = B.gB >= 0 ? IF + B.gB + (int64_t)r * nz * B.fstride + l : nullptr;
-      const double2* gT = B.gT >= 0 ? IF + B.gT + (int64_t)r * nz * B.fstride + l : nullptr;
-      const double2* sig = TAB + sig_off;
-      const int64_t fs = B.fstride;
-      auto rhs = [&](int k) {
-        cplx acc = mk(0, 0);
-        if (gL) acc = cfma(cL, ld(gL + k * fs), acc);
-        if (gR) acc = cfma(cR, ld(gR + k * fs), acc);
-        if (gB) acc = cfma(cB, ld(gB + k * fs), acc);
-        if (gT) acc = cfma(cT, ld(gT + k * fs), acc);
-        return -(ld(sig + k) * acc);
-      };
-      thomas_line<REALZ, FULL, true>(nz, T, s, nullptr, nxy, rhs, MS, minpiv);
-    }
-  }
-  block_min_commit(minpiv, minpiv_out);
-}
-
-template <int MODE, bool REALZ, bool FULL>
-static cudaError_t zlaunch(dim3 grid, size_t sm, cudaStream_t st, const ZBlock* b, int R, int nz, ZTab tab, int64_t sig,
-                           const Bufs& bufs, double* mp) {
-  cudaFuncSetAttribute(k_zsolve_block<MODE, REALZ, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_zsolve_block<MODE, REALZ, FULL><<<grid, ZTHREADS, sm, st>>>(b, R, nz, tab, sig, bufs, mp);
-  return cudaGetLastError();
-}
-
-size_t zsolve_checkpoint_bytes(int nblocks, int max_systems, int nz) {
-  const size_t msys = (size_t)((max_systems + ZTHREADS - 1) / ZTHREADS) * ZTHREADS;
-  return (size_t)nblocks * 2 * ((nz + ZSEG - 1) / ZSEG) * msys * sizeof(double2);
-}
-
-cudaError_t launch_zsolve_block(int mode, const ZBlock* d_blocks, int nblocks, int max_systems, int R, int nz,
-                                ZTab tab, int64_t sig_off, const Bufs& bufs, double* d_minpiv, cudaStream_t st,
-                                bool realz) {
-  const size_t sm = zsmem_bytes(nz, realz);
-  const bool full = nz % ZSEG == 0;
-  dim3 grid((unsigned)((max_systems + ZTHREADS - 1) / ZTHREADS), (unsigned)nblocks);
-#define ZL(M, RZ, F) return zlaunch<M, RZ, F>(grid, sm, st, d_blocks, R, nz, tab, sig_off, bufs, d_minpiv)
-  if (mode == 1) {
-    if (realz) { if (full) ZL(1, true, true); ZL(1, true, false); }
-    if (full) ZL(1, false, true);
-    ZL(1, false, false);
-  }
-  if (realz) { if (full) ZL(2, true, true); ZL(2, true, false); }
-  if (full) ZL(2, false, true);
-  ZL(2, false, false);
-#undef ZL
-}
-
-// ---------------------------------------------------------------- step 5 right-hand side
-// r^[rk][m][l] = sum_a W_x[I_a,l] R1[a][rk][m] + sum_b W_y[I_b,m] R2[b][rk][l]: the sparse
-// forward transform of the interface residual ("thanks to the sparsity of r"),
-// written into the global mode array that the step-5 z-solve then solves in place.
-// Thread = l (coalesced), loop over a chunk of m; the l-dependent factors stay in registers.
-constexpr int GR_M = 32;
-template <int NIF>
-__global__ void __launch_bounds__(128) k_grank(GSweep G, Bufs bufs) {
-  const int l = blockIdx.x * 128 + threadIdx.x;
-  const int64_t rk = blockIdx.y;
-  const int m0 = blockIdx.z * GR_M;
-  if (l >= G.nx) return;
-  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
-  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
-  const int64_t RZ = (int64_t)G.R * G.nz;
-  cplx wx[NIF], r2[NIF];
-#pragma unroll
-  for (int a = 0; a < NIF; ++a) {
-    wx[a] = a < G.nifx ? ld(TAB + G.wxi + (int64_t)a * G.nx + l) : mk(0, 0);
-    r2[a] = a < G.nify ? ld(IF + G.r2 + ((int64_t)a * RZ + rk) * G.nx + l) : mk(0, 0);
-  }
-  double2* W = reinterpret_cast<double2*>(bufs.p[B_T1]) + G.what + rk * G.nx * (int64_t)G.ny + l;
-  const int m1 = m0 + GR_M < G.ny ? m0 + GR_M : G.ny;
-  for (int m = m0; m < m1; ++m) {
-    cplx acc = mk(0, 0);
-#pragma unroll
-    for (int a = 0; a < NIF; ++a)
-      if (a < G.nifx) acc = cfma(wx[a], ld(IF + G.r1 + ((int64_t)a * RZ + rk) * G.ny + m), acc);
-#pragma unroll
-    for (int b = 0; b < NIF; ++b)
-      if (b < G.nify) acc = cfma(ld(TAB + G.wyi + (int64_t)b * G.ny + m), r2[b], acc);
-    W[(int64_t)m * G.nx] = make_double2(acc.x, acc.y);
-  }
-}
-
-cudaError_t launch_grank(const GSweep& g, const Bufs& bufs, cudaStream_t st) {
-  const int nif = g.nifx > g.nify ? g.nifx : g.nify;
-  if (nif > 32) return cudaErrorInvalidValue;
-  dim3 grid((unsigned)((g.nx + 127) / 128), (unsigned)(g.R * g.nz), (unsigned)((g.ny + GR_M - 1) / GR_M));
-  if (nif <= 4) k_grank<4><<<grid, 128, 0, st>>>(g, bufs);
-  else if (nif <= 8) k_grank<8><<<grid, 128, 0, st>>>(g, bufs);
-  else if (nif <= 16) k_grank<16><<<grid, 128, 0, st>>>(g, bufs);
-  else k_grank<32><<<grid, 128, 0, st>>>(g, bufs);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,701 @@
+// Batched z tridiagonal solves of the blocked separable method (arXiv 1909.01299):
+//   step 2  T_lm v~_lm = f~_lm in every block, in place      (k_zs1)
+//   step 6    T_lm w~_lm = l~_lm (Dirichlet lifting, reading R8),
+//                              solution added to v~ in place                      (k_zs2)
+//   step 5    T_lm w^_lm = r^_lm for every global mode, with the
+//                              rank-|I| right side r^ built on the fly            (k_zs3)
+// with T_lm = A_z + lambda M_z + (lambda_l + mu_m) M_z^sigma (reading R1).
+//
+// One thread per z-line; a CTA covers a TL x TM tile of (l, m) modes (l fastest), so a
+// warp's row access is TL consecutive complex numbers (one 512-B segment for TL = 32).
+// Mode space is [r][k][m][l]: a z-line is strided by nx*ny.
+//
+// Thomas elimination without pivoting (reading R15):
+//   forward   r_k = b_k - a_k c'_{k-1},  c'_k = c_k / r_k,  d'_k = (d_k - a_k d'_{k-1}) / r_k
+//   backward  x_k = d'_k - c'_k x_{k+1}
+// c' and d' never go to memory in full: the forward sweep stores a (c', d') checkpoint at
+// the start of every ZSEG-row segment (global scratch, L2-resident while the CTA lives);
+// the backward sweep recomputes a segment from its checkpoint into registers.
+//   k_zs1 re-reads the RHS in the backward sweep (48 B/unknown of HBM traffic);
+//   k_zs2 rebuilds its RHS from the four face transforms and reads/writes v~ once
+//         (32 B/unknown);
+//   k_zs3 builds its RHS once, stores d' in the global mode array (the only copy of the
+//         line) and only recomputes c' backwards (48 B/unknown, no separate RHS pass).
+// Rows of a thread's own line come through per-thread cp.async copies into a private
+// shared-memory ring, NSTAGE-1 segments ahead.  Rows shared by the CTA (face transforms,
+// interface residual rows) are staged cooperatively, double-buffered, one segment ahead,
+// so no load sits inside a dependency chain.  k_zs3 forms its right-hand side tile
+//   r^[k][m][l] = sum_a R1[a][k][m] W_x[I_a][l] + sum_b W_y[I_b][m] R2[b][k][l]
+// (a rank-|I| complex contraction) on the DMMA tensor pipe from the staged rows.
+// A pivot monitor keeps min |r_k|^2 / (|b_k|^2 + (|a_k|+|c_k|)^2) (reported as its sqrt).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "lfds_internal.h"
+
+namespace lfds {
+namespace {
+
+struct cplx {
+  double x, y;
+};
+__device__ __forceinline__ cplx mk(double a, double b) { return cplx{a, b}; }
+__device__ __forceinline__ cplx mk(double2 v) { return cplx{v.x, v.y}; }
+__device__ __forceinline__ cplx ld(const double2* p) {
+  const double2 v = __ldg(p);
+  return cplx{v.x, v.y};
+}
+__device__ __forceinline__ cplx operator+(cplx a, cplx b) { return cplx{a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cplx operator-(cplx a, cplx b) { return cplx{a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cplx operator*(cplx a, cplx b) {
+  return cplx{fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
+}
+__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {  // a*b + c
+  return cplx{fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y))};
+}
+__device__ __forceinline__ double cabs1(cplx a) { return fabs(a.x) + fabs(a.y); }
+// reciprocal from the MUFU.RCP64H seed and two Newton steps (full fp64 accuracy)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ void atomic_min_pos(double* addr, double v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int ZT = 256;  // threads per CTA
+
+// staged z tables (real tables: ag[k] = (a, g), ce[k] = (c, e), m2[k] = (|a|+|c|)^2;
+// complex tables: sa, sg, sc, se)
+struct ZTabS {
+  const double2 *ag, *ce, *sa, *sg, *sc, *se;
+  const double* m2;
+};
+
+template <bool REALZ>
+__device__ __forceinline__ void zrow(const ZTabS& T, int k, cplx s, cplx& a, cplx& b, cplx& c, double& m2) {
+  if (REALZ) {
+    const double2 ag = T.ag[k], ce = T.ce[k];
+    a = mk(ag.x, 0);
+    c = mk(ce.x, 0);
+    b = mk(fma(s.x, ce.y, ag.y), s.y * ce.y);
+    m2 = T.m2[k];
+  } else {
+    const double2 a2 = T.sa[k], g2 = T.sg[k], c2 = T.sc[k], e2 = T.se[k];
+    a = mk(a2.x, a2.y);
+    c = mk(c2.x, c2.y);
+    b = cfma(s, mk(e2.x, e2.y), mk(g2.x, g2.y));
+    const double t = cabs1(a) + cabs1(c);
+    m2 = t * t;
+  }
+}
+
+// one forward elimination row; returns |r|^2
+template <bool REALZ>
+__device__ __forceinline__ double elim(cplx a, cplx b, cplx c, cplx d, cplx& cp, cplx& dp) {
+  cplx r, t;
+  if (REALZ) {
+    r = mk(fma(-a.x, cp.x, b.x), fma(-a.x, cp.y, b.y));
+    t = mk(fma(-a.x, dp.x, d.x), fma(-a.x, dp.y, d.y));
+  } else {
+    r = b - a * cp;
+    t = d - a * dp;
+  }
+  const double n2 = fma(r.x, r.x, r.y * r.y);
+  const double in = fast_rcp(n2);
+  const cplx inv = mk(r.x * in, -r.y * in);
+  cp = REALZ ? mk(c.x * inv.x, c.x * inv.y) : c * inv;
+  dp = t * inv;
+  return n2;
+}
+// c' only (k_zs3 backward recompute)
+template <bool REALZ>
+__device__ __forceinline__ void elim_c(cplx a, cplx b, cplx c, cplx& cp) {
+  cplx r;
+  if (REALZ) r = mk(fma(-a.x, cp.x, b.x), fma(-a.x, cp.y, b.y));
+  else r = b - a * cp;
+  const double in = fast_rcp(fma(r.x, r.x, r.y * r.y));
+  const cplx inv = mk(r.x * in, -r.y * in);
+  cp = REALZ ? mk(c.x * inv.x, c.x * inv.y) : c * inv;
+}
+
+__host__ __device__ __forceinline__ int ztab_slots(int nz, bool realz) {  // in double2 units
+  return realz ? 2 * nz + (nz + 1) / 2 : 4 * nz;
+}
+
+template <bool REALZ>
+__device__ __forceinline__ ZTabS stage_ztab(ZTab tab, const double2* TAB, int nz, double2* zsm) {
+  ZTabS T{};
+  if (REALZ) {
+    double2* ag = zsm;
+    double2* ce = zsm + nz;
+    double* m2 = reinterpret_cast<double*>(zsm + 2 * nz);
+    for (int k = threadIdx.x; k < nz; k += blockDim.x) {
+      const double a = TAB[tab.a + k].x, c = TAB[tab.c + k].x;
+      ag[k] = make_double2(a, TAB[tab.g + k].x);
+      ce[k] = make_double2(c, TAB[tab.e + k].x);
+      m2[k] = (fabs(a) + fabs(c)) * (fabs(a) + fabs(c));
+    }
+    T.ag = ag; T.ce = ce; T.m2 = m2;
+  } else {
+    double2* s = zsm;
+    for (int k = threadIdx.x; k < nz; k += blockDim.x) {
+      s[k] = TAB[tab.a + k];
+      s[nz + k] = TAB[tab.g + k];
+      s[2 * nz + k] = TAB[tab.c + k];
+      s[3 * nz + k] = TAB[tab.e + k];
+    }
+    T.sa = s; T.sg = s + nz; T.sc = s + 2 * nz; T.se = s + 3 * nz;
+  }
+  return T;
+}
+
+// per-thread ring of ZSEG-row segments of one z-line
+template <int ZSEG, int NSTAGE>
+struct Ring {
+  double2* s;  // s[(slot * ZSEG + j) * ZT + tid]
+  const double2* line;
+  int64_t stride;
+  int nz;
+  bool active;
+  __device__ __forceinline__ void issue(int seg) const {
+    if (active && seg >= 0) {
+      double2* d = s + (seg % NSTAGE) * ZSEG * ZT + threadIdx.x;
+      const int k0 = seg * ZSEG;
+#pragma unroll
+      for (int j = 0; j < ZSEG; ++j)
+        if (k0 + j < nz) cp16(d + j * ZT, line + (int64_t)(k0 + j) * stride);
+    }
+    cp_commit();
+  }
+  __device__ __forceinline__ cplx get(int seg, int j) const {
+    return mk(s[((seg % NSTAGE) * ZSEG + j) * ZT + threadIdx.x]);
+  }
+};
+
+struct Tile {  // the CTA's (l, m) tile and this thread's line
+  int l0, m0, l, m;
+  bool active;
+};
+template <int TL>
+__device__ __forceinline__ bool make_tile(const ZBlock& B, Tile& t) {
+  constexpr int TM = ZT / TL;
+  const int tiles_l = (B.nx + TL - 1) / TL;
+  const int tl = blockIdx.x % tiles_l, tm = blockIdx.x / tiles_l;
+  t.l0 = tl * TL;
+  t.m0 = tm * TM;
+  if (t.m0 >= B.ny) return false;
+  t.l = t.l0 + (int)(threadIdx.x % TL);
+  t.m = t.m0 + (int)(threadIdx.x / TL);
+  t.active = t.l < B.nx && t.m < B.ny;
+  return true;
+}
+
+__device__ __forceinline__ void commit_minpiv(float v, double* out) {
+  if (!out) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomic_min_pos(out, (double)sqrtf(v));
+}
+
+__device__ __forceinline__ double2* ck_base(const Bufs& bufs) {
+  return reinterpret_cast<double2*>(bufs.p[B_CK]) +
+         (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * ZT + threadIdx.x;
+}
+
+// ===================================================================== step 2
+template <bool REALZ, int TL>
+__global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks, int nz, ZTab tab, Bufs bufs,
+                                               double* minpiv_out) {
+  constexpr int ZSEG = 8, NSTAGE = 3;
+  extern __shared__ __align__(16) double2 zsm[];
+  const ZBlock B = blocks[blockIdx.y];
+  Tile t;
+  if (!make_tile<TL>(B, t)) return;  // whole CTA, before any barrier
+  const int r = blockIdx.z;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
+  const int64_t nxy = (int64_t)B.nx * B.ny;
+  double2* line = reinterpret_cast<double2*>(bufs.p[B.buf]) + B.ms_off + (int64_t)r * nz * nxy +
+                  (int64_t)(t.active ? t.m : 0) * B.nx + (t.active ? t.l : 0);
+  const Ring<ZSEG, NSTAGE> ring{zsm + ztab_slots(nz, REALZ), line, nxy, nz, t.active};
+  const int nseg = (nz + ZSEG - 1) / ZSEG;
+  const int64_t nslot = (int64_t)gridDim.x * gridDim.y * gridDim.z * ZT;
+  double2* ck = ck_base(bufs);
+  __syncthreads();
+  float minpiv = 1.0f;
+  const cplx s = t.active ? ld(TAB + B.lamx + t.l) + ld(TAB + B.lamy + t.m) : mk(0, 0);
+  cplx cp = mk(0, 0), dp = mk(0, 0);
+#pragma unroll
+  for (int q = 0; q < NSTAGE - 1; ++q) ring.issue(q < nseg ? q : -1);
+  for (int sg = 0; sg < nseg; ++sg) {
+    const int k0 = sg * ZSEG;
+    ring.issue(sg + NSTAGE - 1 < nseg ? sg + NSTAGE - 1 : -1);
+    cp_wait<NSTAGE - 1>();
+    if (!t.active) continue;
+    ck[(int64_t)(2 * sg) * nslot] = make_double2(cp.x, cp.y);
+    ck[(int64_t)(2 * sg + 1) * nslot] = make_double2(dp.x, dp.y);
+#pragma unroll
+    for (int j = 0; j < ZSEG; ++j) {
+      const int k = k0 + j;
+      if (k < nz) {
+        cplx a, b, c;
+        double m2;
+        zrow<REALZ>(T, k, s, a, b, c, m2);
+        const double n2 = elim<REALZ>(a, b, c, ring.get(sg, j), cp, dp);
+        minpiv = fminf(minpiv, __fdividef((float)n2, (float)fma(b.x, b.x, fma(b.y, b.y, m2))));
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NSTAGE - 1; ++q) ring.issue(nseg - 1 - q);
+  cplx x = mk(0, 0);
+  for (int sg = nseg - 1; sg >= 0; --sg) {
+    const int k0 = sg * ZSEG;
+    ring.issue(sg - (NSTAGE - 1));
+    cp_wait<NSTAGE - 1>();
+    if (!t.active) continue;
+    cplx rb[ZSEG], cs[ZSEG];
+    cplx cc = mk(ck[(int64_t)(2 * sg) * nslot]), dd = mk(ck[(int64_t)(2 * sg + 1) * nslot]);
+#pragma unroll
+    for (int j = 0; j < ZSEG; ++j) {
+      const int k = k0 + j;
+      rb[j] = mk(0, 0);
+      if (k < nz) {
+        cplx a, b, c;
+        double m2;
+        zrow<REALZ>(T, k, s, a, b, c, m2);
+        elim<REALZ>(a, b, c, ring.get(sg, j), cc, dd);
+        rb[j] = dd;
+      }
+      cs[j] = cc;
+    }
+#pragma unroll
+    for (int j = ZSEG - 1; j >= 0; --j) {
+      const int k = k0 + j;
+      if (k < nz) {
+        x = rb[j] - cs[j] * x;
+        line[(int64_t)k * nxy] = make_double2(x.x, x.y);
+      }
+    }
+  }
+  cp_wait<0>();
+  commit_minpiv(minpiv, minpiv_out);
+}
+
+// ===================================================================== step 6
+// Face rows staged per segment: per row j, GL[TM], GR[TM] (indexed by m), GB[TL], GT[TL]
+// (indexed by l) and sigma_k.
+template <int TL, int ZSEG>
+struct FaceStage {
+  static constexpr int TM = ZT / TL;
+  static constexpr int ROW = 2 * TM + 2 * TL + 1;
+  static constexpr int SLOTS = ZSEG * ROW;  // double2 per stage
+};
+
+template <bool REALZ, int TL>
+__global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks, int nz, ZTab tab, int64_t sig_off,
+                                               Bufs bufs, double* minpiv_out) {
+  constexpr int ZSEG = 8, NSTAGE = 2, TM = ZT / TL;
+  using FS = FaceStage<TL, ZSEG>;
+  extern __shared__ __align__(16) double2 zsm[];
+  const ZBlock B = blocks[blockIdx.y];
+  Tile t;
+  if (!make_tile<TL>(B, t)) return;
+  const int r = blockIdx.z;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
+  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
+  double2* fsm = zsm + ztab_slots(nz, REALZ);  // [2][FS::SLOTS]
+  const int64_t nxy = (int64_t)B.nx * B.ny;
+  double2* line = reinterpret_cast<double2*>(bufs.p[B_MS]) + B.ms_off + (int64_t)r * nz * nxy +
+                  (int64_t)(t.active ? t.m : 0) * B.nx + (t.active ? t.l : 0);
+  const Ring<ZSEG, NSTAGE> ring{fsm + 2 * FS::SLOTS, line, nxy, nz, t.active};
+  const int nseg = (nz + ZSEG - 1) / ZSEG;
+  const int64_t nslot = (int64_t)gridDim.x * gridDim.y * gridDim.z * ZT;
+  double2* ck = ck_base(bufs);
+  // face f row k at IF[base_f + (r*nz + k)*fs + index]
+  const int64_t fs = B.fstride, ro = (int64_t)r * nz * fs;
+  const bool hL = B.gL >= 0, hR = B.gR >= 0, hB = B.gB >= 0, hT = B.gT >= 0;
+  auto stage = [&](int sg) {  // cooperative copy of segment sg into slot sg&1
+    if (sg >= 0 && sg < nseg) {
+      double2* d = fsm + (sg & 1) * FS::SLOTS;
+      const int k0 = sg * ZSEG;
+      for (int c = threadIdx.x; c < FS::SLOTS; c += ZT) {
+        const int j = c / FS::ROW, w = c - j * FS::ROW, k = k0 + j;
+        if (k >= nz) continue;
+        const double2* src = nullptr;
+        if (w < TM) {
+          if (hL && t.m0 + w < B.ny) src = IF + B.gL + ro + k * fs + t.m0 + w;
+        } else if (w < 2 * TM) {
+          if (hR && t.m0 + w - TM < B.ny) src = IF + B.gR + ro + k * fs + t.m0 + w - TM;
+        } else if (w < 2 * TM + TL) {
+          if (hB && t.l0 + w - 2 * TM < B.nx) src = IF + B.gB + ro + k * fs + t.l0 + w - 2 * TM;
+        } else if (w < 2 * TM + 2 * TL) {
+          if (hT && t.l0 + w - 2 * TM - TL < B.nx) src = IF + B.gT + ro + k * fs + t.l0 + w - 2 * TM - TL;
+        } else {
+          src = TAB + sig_off + k;
+        }
+        if (src) cp16(d + c, src);
+      }
+    }
+    cp_commit();
+  };
+  const cplx cL = hL && t.active ? mk(B.cL) * ld(TAB + B.wx0 + t.l) : mk(0, 0);
+  const cplx cR = hR && t.active ? mk(B.cR) * ld(TAB + B.wx1 + t.l) : mk(0, 0);
+  const cplx cB = hB && t.active ? mk(B.cB) * ld(TAB + B.wy0 + t.m) : mk(0, 0);
+  const cplx cT = hT && t.active ? mk(B.cT) * ld(TAB + B.wy1 + t.m) : mk(0, 0);
+  const int tx = threadIdx.x % TL, ty = threadIdx.x / TL;
+  // l~(k) = -sigma_k (cL_l GL[k][m] + cR_l GR[k][m] + cB_m GB[k][l] + cT_m GT[k][l])
+  auto lift = [&](int sg, int j) {
+    const double2* d = fsm + (sg & 1) * FS::SLOTS + j * FS::ROW;
+    cplx acc = mk(0, 0);
+    if (hL) acc = cfma(cL, mk(d[ty]), acc);
+    if (hR) acc = cfma(cR, mk(d[TM + ty]), acc);
+    if (hB) acc = cfma(cB, mk(d[2 * TM + tx]), acc);
+    if (hT) acc = cfma(cT, mk(d[2 * TM + TL + tx]), acc);
+    const cplx sg2 = mk(d[2 * TM + 2 * TL]);
+    return mk(-(sg2.x * acc.x - sg2.y * acc.y), -(sg2.x * acc.y + sg2.y * acc.x));
+  };
+  __syncthreads();  // z tables
+  float minpiv = 1.0f;
+  const cplx s = t.active ? ld(TAB + B.lamx + t.l) + ld(TAB + B.lamy + t.m) : mk(0, 0);
+  // ---- forward sweep
+  cplx cp = mk(0, 0), dp = mk(0, 0);
+  stage(0);
+  for (int sg = 0; sg < nseg; ++sg) {
+    const int k0 = sg * ZSEG;
+    stage(sg + 1);
+    cp_wait<1>();
+    __syncthreads();  // segment sg staged by every thread
+    if (t.active) {
+      ck[(int64_t)(2 * sg) * nslot] = make_double2(cp.x, cp.y);
+      ck[(int64_t)(2 * sg + 1) * nslot] = make_double2(dp.x, dp.y);
+#pragma unroll
+      for (int j = 0; j < ZSEG; ++j) {
+        const int k = k0 + j;
+        if (k < nz) {
+          cplx a, b, c;
+          double m2;
+          zrow<REALZ>(T, k, s, a, b, c, m2);
+          const double n2 = elim<REALZ>(a, b, c, lift(sg, j), cp, dp);
+          minpiv = fminf(minpiv, __fdividef((float)n2, (float)fma(b.x, b.x, fma(b.y, b.y, m2))));
+        }
+      }
+    }
+    __syncthreads();  // slot sg&1 consumed before it is refilled with segment sg+2
+  }
+  // ---- backward sweep: faces staged again in reverse order, v~ through the ring
+  cp_wait<0>();
+  stage(nseg - 1);
+  ring.issue(nseg - 1);
+  cplx x = mk(0, 0);
+  for (int sg = nseg - 1; sg >= 0; --sg) {
+    const int k0 = sg * ZSEG;
+    stage(sg - 1);
+    ring.issue(sg - 1);
+    cp_wait<2>();  // this segment's faces and ring rows, issued one iteration earlier
+    __syncthreads();
+    if (t.active) {
+      cplx rb[ZSEG], cs[ZSEG];
+      cplx cc = mk(ck[(int64_t)(2 * sg) * nslot]), dd = mk(ck[(int64_t)(2 * sg + 1) * nslot]);
+#pragma unroll
+      for (int j = 0; j < ZSEG; ++j) {
+        const int k = k0 + j;
+        rb[j] = mk(0, 0);
+        if (k < nz) {
+          cplx a, b, c;
+          double m2;
+          zrow<REALZ>(T, k, s, a, b, c, m2);
+          elim<REALZ>(a, b, c, lift(sg, j), cc, dd);
+          rb[j] = dd;
+        }
+        cs[j] = cc;
+      }
+#pragma unroll
+      for (int j = ZSEG - 1; j >= 0; --j) {
+        const int k = k0 + j;
+        if (k < nz) {
+          x = rb[j] - cs[j] * x;
+          const cplx o = ring.get(sg, j);
+          line[(int64_t)k * nxy] = make_double2(o.x + x.x, o.y + x.y);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  commit_minpiv(minpiv, minpiv_out);
+}
+
+// ===================================================================== step 5
+// Per ZSEG-row segment the CTA stages R1[a][k][m0..m0+TM) and R2[b][k][l0..l0+TL) and
+// forms the RHS tile with DMMA: for row j,  C[m][l] = sum_{a<KA} A1[m][a] B1[a][l]
+//   + sum_{b<KA} A2[m][b] B2[b][l],  A1 = R1^T (staged), B1 = W_x[I, tile] (smem, fixed),
+//   A2 = W_y[I, tile]^T (smem, fixed), B2 = R2 (staged);  KA = |I| padded to 4.
+template <int TL, int NIF>
+struct RankStage {
+  static constexpr int TM = ZT / TL, ZSEG = 4, KA = (NIF + 3) / 4 * 4;
+  static constexpr int R1S = ZSEG * KA * TM, R2S = ZSEG * KA * TL;  // per stage (double2)
+  static constexpr int STAGE = R1S + R2S;
+  static constexpr int RHS = ZSEG * ZT;                            // RHS tile [j][tid]
+  static constexpr int WX = KA * TL, WY = KA * TM;                  // fixed weights
+  static constexpr int FWD = 2 * STAGE + RHS + WX + WY;             // forward smem
+  static constexpr int BWD = 3 * ZSEG * ZT;                         // backward ring
+  static constexpr int SLOTS = FWD > BWD ? FWD : BWD;
+};
+
+template <bool REALZ, int TL, int NIF>
+__global__ void __launch_bounds__(ZT, 2) k_zs3(const ZBlock* __restrict__ blocks, int nz, ZTab tab, GSweep G,
+                                               Bufs bufs, double* minpiv_out) {
+  using RS = RankStage<TL, NIF>;
+  constexpr int ZSEG = RS::ZSEG, TM = RS::TM, KA = RS::KA, NSTAGE = 3;
+  extern __shared__ __align__(16) double2 zsm[];
+  const ZBlock B = blocks[blockIdx.y];
+  Tile t;
+  if (!make_tile<TL>(B, t)) return;
+  const int r = blockIdx.z;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
+  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
+  double2* wsm = zsm + ztab_slots(nz, REALZ);  // union: forward staging / backward ring
+  double2* R1s = wsm;                           // [2][ZSEG][KA][TM]
+  double2* R2s = wsm + 2 * RS::R1S;             // [2][ZSEG][KA][TL]
+  double2* RH = wsm + 2 * RS::STAGE;            // [ZSEG][ZT]
+  double2* WXs = RH + RS::RHS;                  // [KA][TL]
+  double2* WYs = WXs + RS::WX;                  // [KA][TM]
+  const int64_t nxy = (int64_t)B.nx * B.ny;
+  double2* line = reinterpret_cast<double2*>(bufs.p[B.buf]) + B.ms_off + (int64_t)r * nz * nxy +
+                  (int64_t)(t.active ? t.m : 0) * B.nx + (t.active ? t.l : 0);
+  const int nseg = (nz + ZSEG - 1) / ZSEG;
+  const int64_t nslot = (int64_t)gridDim.x * gridDim.y * gridDim.z * ZT;
+  double2* ck = ck_base(bufs);
+  const int64_t RZ = (int64_t)G.R * nz;
+  // fixed weights (zero beyond |I| and outside the grid); staged rows zero-filled once so
+  // that entries never copied (a >= |I|, outside the grid) are finite zeros
+  for (int c = threadIdx.x; c < RS::WX + RS::WY; c += ZT) {
+    double2 v = make_double2(0, 0);
+    if (c < RS::WX) {
+      const int a = c / TL, l = t.l0 + c % TL;
+      if (a < G.nifx && l < G.nx) v = TAB[G.wxi + (int64_t)a * G.nx + l];
+    } else {
+      const int b = (c - RS::WX) / TM, m = t.m0 + (c - RS::WX) % TM;
+      if (b < G.nify && m < G.ny) v = TAB[G.wyi + (int64_t)b * G.ny + m];
+    }
+    WXs[c] = v;
+  }
+  for (int c = threadIdx.x; c < 2 * RS::STAGE; c += ZT) wsm[c] = make_double2(0, 0);
+  __syncthreads();
+  auto stage = [&](int sg) {
+    if (sg >= 0 && sg < nseg) {
+      double2* d1 = R1s + (sg & 1) * RS::R1S;
+      double2* d2 = R2s + (sg & 1) * RS::R2S;
+      const int k0 = sg * ZSEG;
+      for (int c = threadIdx.x; c < RS::STAGE; c += ZT) {
+        if (c < RS::R1S) {  // R1[a][r*nz + k][m]
+          const int j = c / (KA * TM), a = (c / TM) % KA, mm = t.m0 + c % TM, k = k0 + j;
+          if (a < G.nifx && mm < G.ny && k < nz)
+            cp16(d1 + c, IF + G.r1 + ((int64_t)a * RZ + (int64_t)r * nz + k) * G.ny + mm);
+        } else {  // R2[b][r*nz + k][l]
+          const int c2 = c - RS::R1S;
+          const int j = c2 / (KA * TL), b = (c2 / TL) % KA, ll = t.l0 + c2 % TL, k = k0 + j;
+          if (b < G.nify && ll < G.nx && k < nz)
+            cp16(d2 + c2, IF + G.r2 + ((int64_t)b * RZ + (int64_t)r * nz + k) * G.nx + ll);
+        }
+      }
+    }
+    cp_commit();
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  // warp -> row j = warp % ZSEG of the segment and (m-tile, l-tile) pairs warp / ZSEG + WPR*i
+  constexpr int NT = TL / 8, MT = TM / 8, NPAIR = NT * MT, WPR = 8 / ZSEG, PPW = NPAIR / WPR;
+  auto rhs_tile = [&](int sg) {
+    const int j = warp % ZSEG;
+    const double2* a1 = R1s + (sg & 1) * RS::R1S + j * KA * TM;  // [a][m]
+    const double2* b2 = R2s + (sg & 1) * RS::R2S + j * KA * TL;  // [b][l]
+#pragma unroll
+    for (int pi = 0; pi < PPW; ++pi) {
+      const int pr = warp / ZSEG + WPR * pi, mt = pr / NT, nt = pr % NT;
+      double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
+#pragma unroll
+      for (int ks = 0; ks < KA / 4; ++ks) {
+        const int kk = 4 * ks + q;
+        const double2 A = a1[kk * TM + mt * 8 + g], Bv = WXs[kk * TL + nt * 8 + g];
+        dmma(cr0, cr1, A.x, Bv.x);
+        dmma(cr0, cr1, -A.y, Bv.y);
+        dmma(ci0, ci1, A.x, Bv.y);
+        dmma(ci0, ci1, A.y, Bv.x);
+        const double2 A2 = WYs[kk * TM + mt * 8 + g], B2 = b2[kk * TL + nt * 8 + g];
+        dmma(cr0, cr1, A2.x, B2.x);
+        dmma(cr0, cr1, -A2.y, B2.y);
+        dmma(ci0, ci1, A2.x, B2.y);
+        dmma(ci0, ci1, A2.y, B2.x);
+      }
+      // C[m = mt*8 + g][l = nt*8 + 2q (+1)] -> the slot of thread (tx = l, ty = m)
+      const int mm = mt * 8 + g, ll = nt * 8 + 2 * q;
+      RH[j * ZT + mm * TL + ll] = make_double2(cr0, ci0);
+      RH[j * ZT + mm * TL + ll + 1] = make_double2(cr1, ci1);
+    }
+  };
+  float minpiv = 1.0f;
+  const cplx s = t.active ? ld(TAB + B.lamx + t.l) + ld(TAB + B.lamy + t.m) : mk(0, 0);
+  // ---- forward sweep: RHS tile per segment, d' stored in the line
+  cplx cp = mk(0, 0), dp = mk(0, 0);
+  stage(0);
+  for (int sg = 0; sg < nseg; ++sg) {
+    const int k0 = sg * ZSEG;
+    stage(sg + 1);
+    cp_wait<1>();
+    __syncthreads();  // segment sg staged
+    rhs_tile(sg);
+    __syncthreads();  // RHS tile complete; staging slot sg&1 free for segment sg+2
+    if (t.active) {
+      ck[(int64_t)sg * nslot] = make_double2(cp.x, cp.y);
+#pragma unroll
+      for (int j = 0; j < ZSEG; ++j) {
+        const int k = k0 + j;
+        if (k < nz) {
+          cplx a, b, c;
+          double m2;
+          zrow<REALZ>(T, k, s, a, b, c, m2);
+          const double n2 = elim<REALZ>(a, b, c, mk(RH[j * ZT + threadIdx.x]), cp, dp);
+          minpiv = fminf(minpiv, __fdividef((float)n2, (float)fma(b.x, b.x, fma(b.y, b.y, m2))));
+          line[(int64_t)k * nxy] = make_double2(dp.x, dp.y);  // d'
+        }
+      }
+    }
+    __syncthreads();  // RH consumed before the next tile overwrites it
+  }
+  cp_wait<0>();
+  __threadfence_block();  // own d' stores precede the cp.async re-reads
+  __syncthreads();        // the forward staging area becomes the backward ring
+  const Ring<ZSEG, NSTAGE> ring{wsm, line, nxy, nz, t.active};
+#pragma unroll
+  for (int qq = 0; qq < NSTAGE - 1; ++qq) ring.issue(nseg - 1 - qq);
+  cplx x = mk(0, 0);
+  for (int sg = nseg - 1; sg >= 0; --sg) {
+    const int k0 = sg * ZSEG;
+    ring.issue(sg - (NSTAGE - 1));
+    cp_wait<NSTAGE - 1>();
+    if (!t.active) continue;
+    cplx cs[ZSEG];
+    cplx cc = mk(ck[(int64_t)sg * nslot]);
+#pragma unroll
+    for (int j = 0; j < ZSEG; ++j) {
+      const int k = k0 + j;
+      if (k < nz) {
+        cplx a, b, c;
+        double m2;
+        zrow<REALZ>(T, k, s, a, b, c, m2);
+        elim_c<REALZ>(a, b, c, cc);
+      }
+      cs[j] = cc;
+    }
+#pragma unroll
+    for (int j = ZSEG - 1; j >= 0; --j) {
+      const int k = k0 + j;
+      if (k < nz) {
+        x = ring.get(sg, j) - cs[j] * x;
+        line[(int64_t)k * nxy] = make_double2(x.x, x.y);
+      }
+    }
+  }
+  cp_wait<0>();
+  commit_minpiv(minpiv, minpiv_out);
+}
+
+// ===================================================================== launch
+int tile_l(int mode, int max_nx, int nif) {
+  if (mode == 3 && nif > 8) return 16;  // keeps the 16-row staging of k_zs3 within 2 CTAs/SM
+  return max_nx > 16 ? 32 : 16;
+}
+
+dim3 zs_grid(int nblocks, int max_nx, int max_ny, int R, int tl) {
+  const int tm = ZT / tl;
+  const int tiles = ((max_nx + tl - 1) / tl) * ((max_ny + tm - 1) / tm);
+  return dim3((unsigned)tiles, (unsigned)nblocks, (unsigned)R);
+}
+
+template <class K>
+cudaError_t prep(K kern, size_t sm) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+}
+
+template <bool REALZ, int TL>
+cudaError_t launch_tl(int mode, dim3 grid, cudaStream_t st, const ZBlock* b, int nz, ZTab tab, int64_t sig,
+                      const GSweep& g, const Bufs& bufs, double* mp) {
+  const size_t zt = (size_t)ztab_slots(nz, REALZ) * sizeof(double2);
+  cudaError_t e;
+  if (mode == 1) {
+    const size_t sm = zt + (size_t)3 * 8 * ZT * sizeof(double2);
+    if ((e = prep(k_zs1<REALZ, TL>, sm)) != cudaSuccess) return e;
+    k_zs1<REALZ, TL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs, mp);
+  } else if (mode == 2) {
+    const size_t sm = zt + (size_t)(2 * FaceStage<TL, 8>::SLOTS + 2 * 8 * ZT) * sizeof(double2);
+    if ((e = prep(k_zs2<REALZ, TL>, sm)) != cudaSuccess) return e;
+    k_zs2<REALZ, TL><<<grid, ZT, sm, st>>>(b, nz, tab, sig, bufs, mp);
+  } else {
+    const int nif = g.nifx > g.nify ? g.nifx : g.nify;
+#define Z3(N)                                                                 \
+  {                                                                           \
+    const size_t sm = zt + (size_t)RankStage<TL, N>::SLOTS * sizeof(double2); \
+    if ((e = prep(k_zs3<REALZ, TL, N>, sm)) != cudaSuccess) return e;         \
+    k_zs3<REALZ, TL, N><<<grid, ZT, sm, st>>>(b, nz, tab, g, bufs, mp);       \
+  }
+    if (nif <= 4) Z3(4)
+    else if (nif <= 8) Z3(8)
+    else if (nif <= 16) Z3(16)
+    else return cudaErrorInvalidValue;
+#undef Z3
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t zsolve_checkpoint_bytes(int nblocks, int max_nx, int max_ny, int R, int nz) {
+  // steps 2/6: (c', d') every 8 rows; step 5: c' every 4 rows; either tile shape
+  size_t slots = 0;
+  for (int tl : {16, 32}) {
+    const dim3 g = zs_grid(nblocks, max_nx, max_ny, R, tl);
+    slots = std::max(slots, (size_t)g.x * g.y * g.z * ZT);
+  }
+  const size_t per = (size_t)((nz + 3) / 4 + 1);
+  return slots * per * sizeof(double2);
+}
+
+cudaError_t launch_zsolve(int mode, const ZBlock* d_blocks, int nblocks, int max_nx, int max_ny, int R, int nz,
+                          ZTab tab, int64_t sig_off, const GSweep* g, const Bufs& bufs, double* d_minpiv,
+                          cudaStream_t st, bool realz) {
+  if (R > 65535 || nblocks > 65535) return cudaErrorInvalidValue;
+  GSweep G{};
+  if (g) G = *g;
+  const int tl = tile_l(mode, max_nx, G.nifx > G.nify ? G.nifx : G.nify);
+  const dim3 grid = zs_grid(nblocks, max_nx, max_ny, R, tl);
+  if (realz) return tl == 32 ? launch_tl<true, 32>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv)
+                             : launch_tl<true, 16>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv);
+  return tl == 32 ? launch_tl<false, 32>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv)
+                  : launch_tl<false, 16>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv);
+}
+
+}  // namespace lfds
