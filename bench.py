@@ -40,6 +40,9 @@ UNIT = "unknowns/s"
 # refinement passes each config needs for the 1e-9 parity bar: C2's BJ-fixed
 # quadratic PML profile has cond(V) ~ 1e5 -> one refinement pass; the others need none.
 REFINE = {"c1": 0, "c2": 1, "c3": 0, "c4": 0, "c5": 0}
+# right-hand sides per pipeline pass (workspace scales with it): C5's 64 RHS x 0.84 GB per
+# array do not fit next to f and u in one pass; 16 per pass keeps the workspace at ~35 GB
+RHS_CHUNK = {"c5": 16}
 # FP64 peaks: derived 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 TF/s;
 # measured on this pool (profiles/r01_fp64_peaks.log): DMMA 37.1, DFMA 34.2 TF/s.
 FP64_PEAK_TFLOPS = 37.2
@@ -225,12 +228,15 @@ def run_ours(args, rank, world, local_rank):
     pw = dataclasses.replace(p, nrhs=nrhs * world)
     refine = REFINE.get(args.config, 0) if args.refine is None else args.refine
     t0 = time.perf_counter()
-    plan = Plan.from_problem(p, device=local_rank, refine=refine, profile=True)
+    plan = Plan.from_problem(p, device=local_rank, refine=refine, profile=True,
+                             rhs_chunk=RHS_CHUNK.get(args.config, 0))
     setup_s = time.perf_counter() - t0
     info = plan.info()
     dt = torch.float64 if p.real else torch.complex128
-    host = np.stack([pw.rhs(rank * nrhs + r) for r in range(nrhs)])
-    f = torch.from_numpy(host).to(device=dev, dtype=dt)
+    # right-hand sides generated one at a time straight into device memory (C5: 64 x 0.84 GB)
+    f = torch.empty((nrhs,) + p.shape, dtype=dt, device=dev)
+    for r in range(nrhs):
+        f[r].copy_(torch.from_numpy(pw.rhs(rank * nrhs + r)))
     u = torch.empty_like(f)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -264,7 +270,9 @@ def run_ours(args, rank, world, local_rank):
     # e2e: host (pinned) buffers through lfds_solve_host, copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        fh = torch.from_numpy(host).to(dtype=dt).pin_memory()
+        # e2e: host (pinned) buffers; at most E2E_RHS right-hand sides (host memory bound)
+        ne = min(nrhs, args.e2e_rhs)
+        fh = f[:ne].cpu().pin_memory()
         uh = torch.empty_like(fh).pin_memory()
         plan.solve_host(fh, out=uh)
         torch.cuda.synchronize()
@@ -281,8 +289,9 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         nbytes = fh.numel() * fh.element_size()
-        e2e = {"value": units / (float(t.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item())}
+        e2e = {"value": p.unknowns * ne * world / (float(t.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item()),
+               "nrhs_per_gpu": ne}
     # roofline of the dominant stage
     alg = stage_algorithmic(p, nrhs, plan)
     hbm_peak, hbm_src = _peaks()
@@ -341,6 +350,7 @@ def main():
     ap.add_argument("--refine", type=int, default=None)
     ap.add_argument("--cpu-nz", type=int, default=16, dest="cpu_nz")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-rhs", type=int, default=8, dest="e2e_rhs", help="RHS per e2e step (host memory)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

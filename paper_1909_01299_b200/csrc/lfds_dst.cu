@@ -6,6 +6,7 @@
 //   alpha = sqrt(2h/N) (forward) or sqrt(2/(hN)) (inverse).
 // DST-I via the odd extension y (length L = 2N: y_q = x_q, y_{L-q} = -x_q, y_0 = y_N = 0):
 //   DFT_L(y)_k = -2i S(x)_k   =>   S(x)_k = (i/2) DFT_L(y)_k.
+// The twiddles W_L^j = exp(-2 pi i j / L) come from the plan tables (GemmDesc.a_off).
 // The length-L DFT uses the four-step split L = R1 * R2: R2 threads per column each run an
 // R1-point FFT in registers, multiply by W_L^{n2 k1}, exchange through shared memory, then R1
 // threads run R2-point FFTs.  Only the outputs k = 1..N-1 are kept.  FP64 CUDA-core
@@ -60,7 +61,7 @@ __device__ __forceinline__ void fft_reg(zc2 (&v)[R], const double2* __restrict__
   }
 }
 
-constexpr int DST_THREADS = 256;
+constexpr int DST_THREADS = 128;  // 8 columns per CTA at L = 256: small CTAs, many resident per SM
 
 __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
@@ -85,11 +86,7 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
   const int64_t c0 = (int64_t)blockIdx.x * CPB;
   if (c0 >= NC) return;
   const int tid = threadIdx.x;
-  for (int j = tid; j < L; j += DST_THREADS) {
-    double s, c;
-    sincospi(-2.0 * j / L, &s, &c);
-    twl[j] = make_double2(c, s);
-  }
+  for (int j = tid; j < L; j += DST_THREADS) twl[j] = __ldg(reinterpret_cast<const double2*>(bufs.p[B_TAB]) + D.a_off + j);
   if (tid < CPB) {
     const int64_t col = c0 + tid;
     const int64_t n1 = col / N2, n2 = col - n1 * N2;

@@ -124,6 +124,7 @@ struct lfds_plan {
   double2* d_tab = nullptr;
   size_t tab_elems = 0;
   ZTab zt_scaled{}, zt_plain{};
+  std::map<int, int64_t> t_tw;  // FFT twiddle tables per length L
   int64_t t_hz = 0, t_hhz = 0, t_sig = 0, t_sige = 0, t_ifx = 0, t_ify = 0, t_bx = 0, t_by = 0, t_xlo = 0, t_ylo = 0;
   std::map<std::tuple<int, int, int>, PassPlan> passes;
   lfds_report report{};
@@ -404,7 +405,11 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
         const int b = q;
         const AxisBlock& ab = xaxis ? X.blocks[b % nbx] : Y.blocks[b / nbx];
         const int64_t roff = fwd ? ab.Fr : ab.Wr;
-        if (ab.dst) { d.scale = fwd ? ab.dst_fwd : ab.dst_inv; vd[ab.n].push_back(d); }
+        if (ab.dst) {
+          d.scale = fwd ? ab.dst_fwd : ab.dst_inv;
+          d.a_off = P->t_tw.at(2 * (ab.n + 1));  // twiddles W_L^j of the odd-extension FFT
+          vd[ab.n].push_back(d);
+        }
         else if (roff >= 0) { d.a_off = roff; vr.push_back(d); }
         else vc.push_back(d);
       }
@@ -800,6 +805,14 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
   }
   P->zt_plain = ZTab{T.put(za), T.put(zg), T.put(zcv), T.put(ze)};
   P->zt_scaled = ZTab{T.put(sa), T.put(sg), T.put(scv), T.put(se)};
+  for (int L = 16; L <= 512; L *= 2) {  // FFT twiddles W_L^j = exp(-2 pi i j/L) for the sine transforms
+    std::vector<zc> tw(L);
+    for (int j = 0; j < L; ++j) {
+      const long double a = -2.0L * 3.141592653589793238462643383279502884L * j / L;
+      tw[j] = zc((double)std::cos(a), (double)std::sin(a));
+    }
+    P->t_tw[L] = T.put(tw);
+  }
   P->t_hz = T.put(P->hz);
   P->t_hhz = T.put(P->hhz);
   P->t_sig = T.put(P->sig_node);
