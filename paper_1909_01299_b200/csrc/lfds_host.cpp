@@ -106,6 +106,7 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   int max_systems = 0, max_systems_global = 0;
   // workspace layout (bytes)
   size_t off_ms = 0, off_t1 = 0, off_if = 0, off_red = 0, off_ck = 0, off_res = 0, total = 0;
+  int64_t gp = 0;  // step-5 P1 partials per l-chunk
   int64_t g_off = 0, h_off = 0, vx_off = 0, vy_off = 0, rx = 0, ry = 0, r1 = 0, r2 = 0, p1 = 0, p2 = 0, wx = 0,
           wy = 0, gf = 0;
 };
@@ -207,6 +208,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   pp.r1 = o; o += align4((int64_t)nifx * R * Ny * Nz);
   pp.r2 = o; o += align4((int64_t)nify * R * Nx * Nz);
   pp.p1 = o; o += align4((int64_t)nifx * R * Ny * Nz);
+  pp.gp = o; o += align4((int64_t)(projm_chunks(Nx) > 1 ? projm_chunks(Nx) : 0) * nifx * R * Ny * Nz);
   pp.p2 = o; o += align4((int64_t)nify * R * Nx * Nz);
   pp.wx = o; o += align4((int64_t)nifx * R * Nz * Ny);
   pp.wy = o; o += align4((int64_t)nify * R * Nz * Nx);
@@ -582,8 +584,18 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
                            P->real_z));
     P->launches += 1;
     end(); begin(ST_GPROJ);
-    if ((rc = m8(pp.m5p1, true))) return rc;
-    if ((rc = m8(pp.m5p2, false))) return rc;
+    {
+      ProjM pm{};
+      pm.nx = Nx; pm.ny = Ny; pm.nplanes = R * Nz; pm.E1 = nifx; pm.E2 = nify; pm.nlc = projm_chunks(Nx);
+      pm.x_buf = B_T1; pm.x_off = 0; pm.wr = X.WI; pm.wc = Y.WI;
+      const int64_t RZ = (int64_t)R * Nz;
+      pm.g_es = RZ * Ny; pm.g_ps = Ny; pm.p1_off = pp.p1; pm.p1_es = RZ * Ny;
+      if (pm.nlc > 1) { pm.g_off = pp.gp; pm.g_lcs = (int64_t)nifx * RZ * Ny; }
+      else { pm.g_off = pp.p1; pm.g_lcs = 0; }
+      pm.h_off = pp.p2; pm.h_es = RZ * Nx; pm.h_ps = Nx;
+      CUDA_TRY(launch_projm(pm, bufs, st));
+      P->launches += pm.nlc > 1 ? 2 : 1;
+    }
     end(); begin(ST_GPLANE);
     if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true))) return rc;
     if ((rc = xform(pp.s5wy, StageDescs{}, pp.s5wy, true))) return rc;

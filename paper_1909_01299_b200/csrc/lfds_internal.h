@@ -89,6 +89,20 @@ struct PDesc {
 cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, int maxplanes, cudaStream_t st,
                         const Bufs& bufs);
 
+// Step-5 projections of the global correction (lfds_proj.cu, DMMA): P1 = W_x[I,:] w^ (over l),
+// P2 = W_y[I,:] w^ (over m), one read of w^[p][m][l] (plane stride nx*ny).  P1 partials per
+// l-chunk of 256 columns at g_off + lc*g_lcs + e*g_es + p*g_ps + m, summed into p1_off.
+struct ProjM {
+  int nx, ny, nplanes, E1, E2, nlc, x_buf, pad;
+  int64_t x_off;
+  int64_t wr, wc;              // TAB: Wr[e][l] (row stride nx), Wc[e][m] (row stride ny)
+  int64_t g_off, g_lcs, g_es, g_ps;
+  int64_t p1_off, p1_es;
+  int64_t h_off, h_es, h_ps;
+};
+int projm_chunks(int nx);
+cudaError_t launch_projm(const ProjM& P, const Bufs& bufs, cudaStream_t st);
+
 // launchers (lfds_kernels.cu); return cudaGetLastError()
 cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, int ldB_hint,
                         const Bufs& bufs, cudaStream_t st);

@@ -181,4 +181,186 @@ cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, i
   return launch_l<2>(maxE, d_descs, ndesc, maxplanes, threads, st, bufs);
 }
 
+
+// ============================================================================================
+// Step-5 projections on the DMMA pipe (one read of the global correction w^):
+//   P1[a][p][m] = sum_l W_x[I_a][l] w^[p][m][l],   P2[b][p][l] = sum_m W_y[I_b][m] w^[p][m][l]
+// (w on the interface planes needs only these rows of the inverse transform).
+// CTA = one l-chunk of up to 256 columns of one plane p, all rows m in tiles of 8 staged by
+// cp.async (double-buffered).  Per tile and warp (32 columns):
+//   P2 (K = m):  C[e][l] += Wc[e][m] X[m][l]   — accumulated in registers over all m
+//   P1 (K = l):  C[m][e] += X[m][l] Wr[e][l]   — reduced over the warps in shared memory and
+//                over l-chunks by k_projm_sum in a fixed order (deterministic)
+// Complex products use the 3-multiplication form (T1 = ar br, T2 = ai bi, T3 = (ar+ai)(br+bi)).
+namespace {
+
+__device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp16p(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+struct C3 {  // 3M accumulators of one 8x8 complex tile (2 values per thread)
+  double t1[2], t2[2], t3[2];
+  __device__ __forceinline__ void zero() { t1[0] = t1[1] = t2[0] = t2[1] = t3[0] = t3[1] = 0.0; }
+  __device__ __forceinline__ void mma(double2 a, double2 b) {
+    dmma8(t1[0], t1[1], a.x, b.x);
+    dmma8(t2[0], t2[1], a.y, b.y);
+    dmma8(t3[0], t3[1], a.x + a.y, b.x + b.y);
+  }
+  __device__ __forceinline__ double2 get(int h) const {
+    return make_double2(t1[h] - t2[h], t3[h] - t1[h] - t2[h]);
+  }
+};
+
+constexpr int PM_LC = 256, PM_LDX = PM_LC + 4;  // columns per CTA; padded row (== 4 mod 8)
+
+template <int ET>
+__global__ void __launch_bounds__(256) k_projm(ProjM P, Bufs bufs) {
+  extern __shared__ __align__(16) double2 psm[];
+  double2* Xs = psm;                    // [2][8][PM_LDX]
+  double2* Wrs = Xs + 2 * 8 * PM_LDX;   // [8*ET][PM_LDX]
+  double2* red = Wrs + 8 * ET * PM_LDX; // [NW][ET][8 m][8 e]
+  const int lc = blockIdx.x, p = blockIdx.y;
+  const int lb = lc * PM_LC;
+  const int NW = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const double2* X = reinterpret_cast<const double2*>(bufs.p[P.x_buf]) + P.x_off + (int64_t)p * P.nx * P.ny;
+  double2* IF = reinterpret_cast<double2*>(bufs.p[B_IF]);
+  for (int c = threadIdx.x; c < 8 * ET * PM_LDX; c += blockDim.x) {
+    const int e = c / PM_LDX, li = c % PM_LDX, l = lb + li;
+    Wrs[c] = (e < P.E1 && li < PM_LC && l < P.nx) ? TAB[P.wr + (int64_t)e * P.nx + l] : make_double2(0, 0);
+  }
+  const int ntile = (P.ny + 7) / 8;
+  auto stage = [&](int it) {
+    if (it < ntile) {
+      double2* d = Xs + (it & 1) * 8 * PM_LDX;
+      const int m0 = it * 8;
+      for (int c = threadIdx.x; c < 8 * PM_LC; c += blockDim.x) {
+        const int r = c / PM_LC, li = c % PM_LC, m = m0 + r, l = lb + li;
+        const bool ok = m < P.ny && l < P.nx;
+        cp16p(d + r * PM_LDX + li, ok ? X + (int64_t)m * P.nx + l : X, ok);  // zero-fill outside
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  C3 h[ET][4];
+#pragma unroll
+  for (int et = 0; et < ET; ++et)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) h[et][nt].zero();
+  const int lw = warp * 32;  // warp's columns within the chunk
+  stage(0);
+  for (int it = 0; it < ntile; ++it) {
+    stage(it + 1);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    const double2* x = Xs + (it & 1) * 8 * PM_LDX;
+    const int m0 = it * 8;
+    // P2: C[e][l] += Wc[e][m] X[m][l]  (A = Wc 8e x 4m, B = X 4m x 8l)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int m = m0 + 4 * ks + q;
+#pragma unroll
+      for (int et = 0; et < ET; ++et) {
+        const int e = et * 8 + g;
+        const double2 a = (e < P.E2 && m < P.ny) ? __ldg(TAB + P.wc + (int64_t)e * P.ny + m) : make_double2(0, 0);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) h[et][nt].mma(a, x[(4 * ks + q) * PM_LDX + lw + 8 * nt + g]);
+      }
+    }
+    // P1 partial: C[m][e] += X[m][l] Wr[e][l]  (A = X 8m x 4l, B = Wr^T 4l x 8e), K = warp's 32 l
+    C3 gacc[ET];
+#pragma unroll
+    for (int et = 0; et < ET; ++et) gacc[et].zero();
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const double2 a = x[g * PM_LDX + lw + 4 * ks + q];
+#pragma unroll
+      for (int et = 0; et < ET; ++et) gacc[et].mma(a, Wrs[(et * 8 + g) * PM_LDX + lw + 4 * ks + q]);
+    }
+    // C fragment: thread holds C[m = g][e = 2q, 2q+1]
+#pragma unroll
+    for (int et = 0; et < ET; ++et)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) red[((warp * ET + et) * 8 + g) * 8 + 2 * q + hh] = gacc[et].get(hh);
+    __syncthreads();
+    for (int t = threadIdx.x; t < ET * 64; t += blockDim.x) {
+      const int et = t / 64, m = m0 + (t / 8) % 8, e = et * 8 + t % 8;
+      if (m < P.ny && e < P.E1) {
+        double2 acc = make_double2(0, 0);
+        for (int w = 0; w < NW; ++w) {
+          const double2 v = red[((w * ET + et) * 8 + (t / 8) % 8) * 8 + t % 8];
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        IF[P.g_off + (int64_t)lc * P.g_lcs + (int64_t)e * P.g_es + (int64_t)p * P.g_ps + m] = acc;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  // P2: thread holds C[e = et*8 + g][l = lw + 8nt + 2q (+1)]
+#pragma unroll
+  for (int et = 0; et < ET; ++et) {
+    const int e = et * 8 + g;
+    if (e >= P.E2) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int l = lb + lw + 8 * nt + 2 * q + hh;
+        if (lw + 8 * nt + 2 * q + hh < PM_LC && l < P.nx)
+          IF[P.h_off + (int64_t)e * P.h_es + (int64_t)p * P.h_ps + l] = h[et][nt].get(hh);
+      }
+  }
+}
+
+// P1 = sum over l-chunks of the partials (fixed order)
+__global__ void k_projm_sum(ProjM P, Bufs bufs) {
+  double2* IF = reinterpret_cast<double2*>(bufs.p[B_IF]);
+  const int64_t n = (int64_t)P.E1 * P.nplanes * P.ny;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i % P.ny);
+    const int64_t rest = i / P.ny;
+    const int p = (int)(rest % P.nplanes), e = (int)(rest / P.nplanes);
+    double2 acc = make_double2(0, 0);
+    for (int lc = 0; lc < P.nlc; ++lc) {
+      const double2 v = IF[P.g_off + (int64_t)lc * P.g_lcs + (int64_t)e * P.g_es + (int64_t)p * P.g_ps + m];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    IF[P.p1_off + (int64_t)e * P.p1_es + (int64_t)p * P.g_ps + m] = acc;
+  }
+}
+
+}  // namespace
+
+int projm_chunks(int nx) { return (nx + PM_LC - 1) / PM_LC; }
+
+cudaError_t launch_projm(const ProjM& P, const Bufs& bufs, cudaStream_t st) {
+  if (P.nplanes <= 0 || P.nplanes > 65535) return P.nplanes <= 0 ? cudaSuccess : cudaErrorInvalidValue;
+  const int E = P.E1 > P.E2 ? P.E1 : P.E2;
+  const int threads = P.nx >= PM_LC ? PM_LC : ((P.nx + 31) / 32) * 32;
+  const int nw = threads / 32;
+  const dim3 grid((unsigned)P.nlc, (unsigned)P.nplanes);
+  cudaError_t e;
+  if (E <= 8) {
+    const size_t sm = (size_t)((2 * 8 + 8) * PM_LDX + nw * 64) * sizeof(double2);
+    if ((e = cudaFuncSetAttribute(k_projm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
+    k_projm<1><<<grid, threads, sm, st>>>(P, bufs);
+  } else if (E <= 16) {
+    const size_t sm = (size_t)((2 * 8 + 16) * PM_LDX + nw * 128) * sizeof(double2);
+    if ((e = cudaFuncSetAttribute(k_projm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
+    k_projm<2><<<grid, threads, sm, st>>>(P, bufs);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  if (P.nlc > 1 && P.E1 > 0) k_projm_sum<<<148 * 8, 256, 0, st>>>(P, bufs);
+  return cudaGetLastError();
+}
+
 }  // namespace lfds

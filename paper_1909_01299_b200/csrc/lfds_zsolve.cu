@@ -270,13 +270,18 @@ __global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks
 #pragma unroll
   for (int q = 0; q < NSTAGE - 1; ++q) ring.issue(nseg - 1 - q);
   cplx x = mk(0, 0);
+  double2 nc = ck[(int64_t)(2 * (nseg - 1)) * nslot], nd = ck[(int64_t)(2 * (nseg - 1) + 1) * nslot];
   for (int sg = nseg - 1; sg >= 0; --sg) {
     const int k0 = sg * ZSEG;
     ring.issue(sg - (NSTAGE - 1));
     cp_wait<NSTAGE - 1>();
     if (!t.active) continue;
     cplx rb[ZSEG], cs[ZSEG];
-    cplx cc = mk(ck[(int64_t)(2 * sg) * nslot]), dd = mk(ck[(int64_t)(2 * sg + 1) * nslot]);
+    cplx cc = mk(nc), dd = mk(nd);
+    if (sg > 0) {  // next segment's checkpoint in flight while this one is solved
+      nc = ck[(int64_t)(2 * sg - 2) * nslot];
+      nd = ck[(int64_t)(2 * sg - 1) * nslot];
+    }
 #pragma unroll
     for (int j = 0; j < ZSEG; ++j) {
       const int k = k0 + j;
@@ -304,13 +309,14 @@ __global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks
 }
 
 // ===================================================================== step 6
-// Face rows staged per segment: per row j, GL[TM], GR[TM] (indexed by m), GB[TL], GT[TL]
-// (indexed by l) and sigma_k.
+// Face rows staged per segment, separate arrays per face: GL[j][TM], GR[j][TM] (indexed
+// by m), GB[j][TL], GT[j][TL] (indexed by l), sigma[j].  Every thread owns fixed copy slots
+// (shift/mask index math only): 2*ZSEG*(TL+TM) + ZSEG copies over ZT threads.
 template <int TL, int ZSEG>
 struct FaceStage {
   static constexpr int TM = ZT / TL;
-  static constexpr int ROW = 2 * TM + 2 * TL + 1;
-  static constexpr int SLOTS = ZSEG * ROW;  // double2 per stage
+  static constexpr int GB = 0, GT = ZSEG * TL, GL = 2 * ZSEG * TL, GR = GL + ZSEG * TM, SG = GR + ZSEG * TM;
+  static constexpr int SLOTS = SG + ZSEG;  // double2 per stage
 };
 
 template <bool REALZ, int TL>
@@ -337,24 +343,26 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
   // face f row k at IF[base_f + (r*nz + k)*fs + index]
   const int64_t fs = B.fstride, ro = (int64_t)r * nz * fs;
   const bool hL = B.gL >= 0, hR = B.gR >= 0, hB = B.gB >= 0, hT = B.gT >= 0;
-  auto stage = [&](int sg) {  // cooperative copy of segment sg into slot sg&1
+  // cooperative copy of segment sg into slot sg&1: copy c -> (face, row j, index)
+  auto stage = [&](int sg) {
     if (sg >= 0 && sg < nseg) {
       double2* d = fsm + (sg & 1) * FS::SLOTS;
       const int k0 = sg * ZSEG;
-      for (int c = threadIdx.x; c < FS::SLOTS; c += ZT) {
-        const int j = c / FS::ROW, w = c - j * FS::ROW, k = k0 + j;
-        if (k >= nz) continue;
+#pragma unroll
+      for (int i = 0; i < (FS::SLOTS + ZT - 1) / ZT; ++i) {
+        const int c = threadIdx.x + i * ZT;
+        if (c >= FS::SLOTS) break;
         const double2* src = nullptr;
-        if (w < TM) {
-          if (hL && t.m0 + w < B.ny) src = IF + B.gL + ro + k * fs + t.m0 + w;
-        } else if (w < 2 * TM) {
-          if (hR && t.m0 + w - TM < B.ny) src = IF + B.gR + ro + k * fs + t.m0 + w - TM;
-        } else if (w < 2 * TM + TL) {
-          if (hB && t.l0 + w - 2 * TM < B.nx) src = IF + B.gB + ro + k * fs + t.l0 + w - 2 * TM;
-        } else if (w < 2 * TM + 2 * TL) {
-          if (hT && t.l0 + w - 2 * TM - TL < B.nx) src = IF + B.gT + ro + k * fs + t.l0 + w - 2 * TM - TL;
+        if (c < FS::GL) {  // GB / GT rows, TL entries each
+          const int f = c / (ZSEG * TL), j = (c / TL) % ZSEG, li = c % TL, k = k0 + j;
+          if (k < nz && t.l0 + li < B.nx && (f ? hT : hB)) src = IF + (f ? B.gT : B.gB) + ro + k * fs + t.l0 + li;
+        } else if (c < FS::SG) {  // GL / GR rows, TM entries each
+          const int c2 = c - FS::GL;
+          const int f = c2 / (ZSEG * TM), j = (c2 / TM) % ZSEG, mi = c2 % TM, k = k0 + j;
+          if (k < nz && t.m0 + mi < B.ny && (f ? hR : hL)) src = IF + (f ? B.gR : B.gL) + ro + k * fs + t.m0 + mi;
         } else {
-          src = TAB + sig_off + k;
+          const int k = k0 + c - FS::SG;
+          if (k < nz) src = TAB + sig_off + k;
         }
         if (src) cp16(d + c, src);
       }
@@ -368,13 +376,13 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
   const int tx = threadIdx.x % TL, ty = threadIdx.x / TL;
   // l~(k) = -sigma_k (cL_l GL[k][m] + cR_l GR[k][m] + cB_m GB[k][l] + cT_m GT[k][l])
   auto lift = [&](int sg, int j) {
-    const double2* d = fsm + (sg & 1) * FS::SLOTS + j * FS::ROW;
+    const double2* d = fsm + (sg & 1) * FS::SLOTS;
     cplx acc = mk(0, 0);
-    if (hL) acc = cfma(cL, mk(d[ty]), acc);
-    if (hR) acc = cfma(cR, mk(d[TM + ty]), acc);
-    if (hB) acc = cfma(cB, mk(d[2 * TM + tx]), acc);
-    if (hT) acc = cfma(cT, mk(d[2 * TM + TL + tx]), acc);
-    const cplx sg2 = mk(d[2 * TM + 2 * TL]);
+    if (hL) acc = cfma(cL, mk(d[FS::GL + j * TM + ty]), acc);
+    if (hR) acc = cfma(cR, mk(d[FS::GR + j * TM + ty]), acc);
+    if (hB) acc = cfma(cB, mk(d[FS::GB + j * TL + tx]), acc);
+    if (hT) acc = cfma(cT, mk(d[FS::GT + j * TL + tx]), acc);
+    const cplx sg2 = mk(d[FS::SG + j]);
     return mk(-(sg2.x * acc.x - sg2.y * acc.y), -(sg2.x * acc.y + sg2.y * acc.x));
   };
   __syncthreads();  // z tables
@@ -410,6 +418,7 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
   stage(nseg - 1);
   ring.issue(nseg - 1);
   cplx x = mk(0, 0);
+  double2 nc = ck[(int64_t)(2 * (nseg - 1)) * nslot], nd = ck[(int64_t)(2 * (nseg - 1) + 1) * nslot];
   for (int sg = nseg - 1; sg >= 0; --sg) {
     const int k0 = sg * ZSEG;
     stage(sg - 1);
@@ -418,7 +427,11 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
     __syncthreads();
     if (t.active) {
       cplx rb[ZSEG], cs[ZSEG];
-      cplx cc = mk(ck[(int64_t)(2 * sg) * nslot]), dd = mk(ck[(int64_t)(2 * sg + 1) * nslot]);
+      cplx cc = mk(nc), dd = mk(nd);
+      if (sg > 0) {
+        nc = ck[(int64_t)(2 * sg - 2) * nslot];
+        nd = ck[(int64_t)(2 * sg - 1) * nslot];
+      }
 #pragma unroll
       for (int j = 0; j < ZSEG; ++j) {
         const int k = k0 + j;
@@ -458,7 +471,7 @@ struct RankStage {
   static constexpr int TM = ZT / TL, ZSEG = 4, KA = (NIF + 3) / 4 * 4;
   static constexpr int R1S = ZSEG * KA * TM, R2S = ZSEG * KA * TL;  // per stage (double2)
   static constexpr int STAGE = R1S + R2S;
-  static constexpr int RHS = ZSEG * ZT;                            // RHS tile [j][tid]
+  static constexpr int RHS = ZSEG * TM * (TL + 1);                 // RHS tile [j][m][TL+1]
   static constexpr int WX = KA * TL, WY = KA * TM;                  // fixed weights
   static constexpr int FWD = 2 * STAGE + RHS + WX + WY;             // forward smem
   static constexpr int BWD = 3 * ZSEG * ZT;                         // backward ring
@@ -481,7 +494,7 @@ __global__ void __launch_bounds__(ZT, 2) k_zs3(const ZBlock* __restrict__ blocks
   double2* wsm = zsm + ztab_slots(nz, REALZ);  // union: forward staging / backward ring
   double2* R1s = wsm;                           // [2][ZSEG][KA][TM]
   double2* R2s = wsm + 2 * RS::R1S;             // [2][ZSEG][KA][TL]
-  double2* RH = wsm + 2 * RS::STAGE;            // [ZSEG][ZT]
+  double2* RH = wsm + 2 * RS::STAGE;            // [ZSEG][TM][TL+1] (padded: conflict-free)
   double2* WXs = RH + RS::RHS;                  // [KA][TL]
   double2* WYs = WXs + RS::WX;                  // [KA][TM]
   const int64_t nxy = (int64_t)B.nx * B.ny;
@@ -527,6 +540,7 @@ __global__ void __launch_bounds__(ZT, 2) k_zs3(const ZBlock* __restrict__ blocks
     cp_commit();
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int tx = threadIdx.x % TL, ty = threadIdx.x / TL;
   // warp -> row j = warp % ZSEG of the segment and (m-tile, l-tile) pairs warp / ZSEG + WPR*i
   constexpr int NT = TL / 8, MT = TM / 8, NPAIR = NT * MT, WPR = 8 / ZSEG, PPW = NPAIR / WPR;
   auto rhs_tile = [&](int sg) {
@@ -553,8 +567,8 @@ __global__ void __launch_bounds__(ZT, 2) k_zs3(const ZBlock* __restrict__ blocks
       }
       // C[m = mt*8 + g][l = nt*8 + 2q (+1)] -> the slot of thread (tx = l, ty = m)
       const int mm = mt * 8 + g, ll = nt * 8 + 2 * q;
-      RH[j * ZT + mm * TL + ll] = make_double2(cr0, ci0);
-      RH[j * ZT + mm * TL + ll + 1] = make_double2(cr1, ci1);
+      RH[(j * TM + mm) * (TL + 1) + ll] = make_double2(cr0, ci0);
+      RH[(j * TM + mm) * (TL + 1) + ll + 1] = make_double2(cr1, ci1);
     }
   };
   float minpiv = 1.0f;
@@ -578,7 +592,7 @@ __global__ void __launch_bounds__(ZT, 2) k_zs3(const ZBlock* __restrict__ blocks
           cplx a, b, c;
           double m2;
           zrow<REALZ>(T, k, s, a, b, c, m2);
-          const double n2 = elim<REALZ>(a, b, c, mk(RH[j * ZT + threadIdx.x]), cp, dp);
+          const double n2 = elim<REALZ>(a, b, c, mk(RH[(j * TM + ty) * (TL + 1) + tx]), cp, dp);
           minpiv = fminf(minpiv, __fdividef((float)n2, (float)fma(b.x, b.x, fma(b.y, b.y, m2))));
           line[(int64_t)k * nxy] = make_double2(dp.x, dp.y);  // d'
         }
@@ -593,13 +607,15 @@ __global__ void __launch_bounds__(ZT, 2) k_zs3(const ZBlock* __restrict__ blocks
 #pragma unroll
   for (int qq = 0; qq < NSTAGE - 1; ++qq) ring.issue(nseg - 1 - qq);
   cplx x = mk(0, 0);
+  double2 nc = ck[(int64_t)(nseg - 1) * nslot];
   for (int sg = nseg - 1; sg >= 0; --sg) {
     const int k0 = sg * ZSEG;
     ring.issue(sg - (NSTAGE - 1));
     cp_wait<NSTAGE - 1>();
     if (!t.active) continue;
     cplx cs[ZSEG];
-    cplx cc = mk(ck[(int64_t)sg * nslot]);
+    cplx cc = mk(nc);
+    if (sg > 0) nc = ck[(int64_t)(sg - 1) * nslot];
 #pragma unroll
     for (int j = 0; j < ZSEG; ++j) {
       const int k = k0 + j;
