@@ -159,10 +159,13 @@ class ClockSampler:
 
 
 def stage_algorithmic(p, R: int, plan=None):
-    """Algorithmic FLOPs and bytes per stage (DESIGN.md §5 table).
+    """Algorithmic (flops, bytes) per launch of each timed stage (DESIGN.md §5 table).
 
-    A transform along an axis costs 8 flops per complex MAC with a complex eigenvector
-    matrix (C blocks) and 4 with a real one (U, R blocks: real matrix x complex data)."""
+    Dense transform stages: a complex eigenvector matrix (C blocks) costs 8 flops per complex
+    MAC, a real one (R blocks) 4 (real matrix x complex data); each element moves 32 B.
+    Sine stages (uniform blocks, FFT-based DST): HBM-bound, 32 B per element.
+    z-solves: 32 B per unknown (read + write).  Step 5: the rank-|I| contraction costs
+    8 (|I_x| + |I_y|) flops per global unknown (RHS build and projection each)."""
     def sizes(n, iface):
         cuts = [0] + list(iface) + [n + 1]
         return [cuts[i + 1] - cuts[i] - 1 for i in range(len(cuts) - 1)]
@@ -171,26 +174,45 @@ def stage_algorithmic(p, R: int, plan=None):
     ky = [plan.basis(1, j)[2] if plan else 2 for j in range(len(by))]
     nz = p.nz
 
-    def fl(kind, n):  # per element of the transformed direction
-        if kind == 0 and (2 * (n + 1)) in (16, 32, 64, 128, 256, 512):
-            L = 2 * (n + 1)   # fast sine transform: complex FFT of the odd extension, 5 L log2 L / n
-            return 5.0 * L * math.log2(L) / n
-        return (8.0 if kind == 2 else 4.0) * n  # dense complex / real eigenvector matrix
-    fl_x = sum(fl(kx[i], bx[i]) * bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by)))
-    fl_y = sum(fl(ky[j], by[j]) * bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by)))
+    def is_sine(kind, n):
+        return kind == 0 and (2 * (n + 1)) in (16, 32, 64, 128, 256, 512)
+
+    def dense(kinds, sz, axis):
+        fl, el = 0.0, 0.0
+        for i in range(len(bx)):
+            for j in range(len(by)):
+                k, n = (kinds[i], bx[i]) if axis == 0 else (kinds[j], by[j])
+                if not is_sine(k, n):
+                    e = bx[i] * by[j] * nz * R
+                    fl += (8.0 if k == 2 else 4.0) * n * e
+                    el += e
+        return fl, 32.0 * el
+
+    def sine(kinds, axis):
+        el = 0.0
+        for i in range(len(bx)):
+            for j in range(len(by)):
+                k, n = (kinds[i], bx[i]) if axis == 0 else (kinds[j], by[j])
+                if is_sine(k, n):
+                    el += bx[i] * by[j] * nz * R
+        return None, 32.0 * el
     el_blk = sum(nx * ny * nz * R for nx in bx for ny in by)
     el_all = p.nx * p.ny * nz * R
-    nif = len(p.iface_x) + len(p.iface_y)
+    nifx, nify = len(p.iface_x), len(p.iface_y)
+    nif = nifx + nify
+    plane = 8.0 * (nifx * p.ny * p.ny + nify * p.nx * p.nx) * nz * R
+    xd, yd = dense(kx, bx, 0), dense(ky, by, 1)
+    xs, ys = sine(kx, 0), sine(ky, 1)
     return {
-        "step1_x_forward": ("tensor", fl_x, 32.0 * el_blk),
-        "step1_y_forward": ("tensor", fl_y, 32.0 * el_blk),
-        "step2_zsolve": ("hbm", None, 32.0 * el_blk),
-        "step3_edge_values": ("hbm", None, 32.0 * el_blk),
-        "step5_global_zsolve": ("hbm", 8.0 * nif * el_all, 32.0 * el_all),
-        "step5_projection": ("hbm", 8.0 * nif * el_all, 32.0 * el_all),
-        "step6_zsolve_lift": ("hbm", None, 32.0 * el_blk),
-        "step7_y_inverse": ("tensor", fl_y, 32.0 * el_blk),
-        "step7_x_inverse": ("tensor", fl_x, 32.0 * el_blk),
+        "step1_x_sine": xs, "step1_x_dense": xd, "step1_y_sine": ys, "step1_y_dense": yd,
+        "step2_zsolve": (None, 32.0 * el_blk),
+        "step3_edge_projection": (None, 16.0 * el_blk),
+        "step5_plane_forward": (plane, None),
+        "step5_global_zsolve": (8.0 * nif * el_all, 16.0 * el_all),
+        "step5_projection": (8.0 * nif * el_all, 16.0 * el_all),
+        "step5_plane_inverse": (plane, None),
+        "step6_zsolve_lift": (None, 32.0 * el_blk),
+        "step7_y_sine": ys, "step7_y_dense": yd, "step7_x_sine": xs, "step7_x_dense": xd,
     }
 
 
@@ -292,29 +314,38 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": p.unknowns * ne * world / (float(t.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item()),
                "nrhs_per_gpu": ne}
-    # roofline of the dominant stage
+    # roofline of the dominant stage (the kernel kind with the largest device time per step);
+    # governing bound = whichever of flops/peak and bytes/peak is the larger time
     alg = stage_algorithmic(p, nrhs, plan)
     hbm_peak, hbm_src = _peaks()
     dom = max(stages.items(), key=lambda kv: kv[1][0])
     name, (st_ms, st_launch) = dom
-    per_launch_ms = st_ms / max(1, args.steps)
-    kind, flops, nbytes = alg.get(name, ("hbm", None, None))
+    per_step_ms = st_ms / max(1, args.steps)
+    flops, nbytes = alg.get(name, (None, None))
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
             traffic = json.load(fh_).get(args.config, {}).get(name)
     except Exception:
         pass
-    if kind == "tensor" and flops:
-        achieved = flops / (per_launch_ms * 1e-3) / 1e12
+    t_tensor = (flops or 0) / (FP64_PEAK_TFLOPS * 1e12)
+    t_hbm = (nbytes or 0) / (hbm_peak * 1e9)
+    if t_tensor >= t_hbm and flops:
+        achieved = flops / (per_step_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "kernel": name,
-                "peak_source": "FP64 derived from unit counts x max clock (DESIGN.md §5); DMMA measured 37.1"}
+                "peak_source": "FP64 tensor (DMMA) = 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5); "
+                               "measured DMMA 37.1 TF/s (profiles/r01_fp64_peaks.log)"}
     else:
-        achieved = (nbytes or 0) / (per_launch_ms * 1e-3) / 1e9
+        achieved = (nbytes or 0) / (per_step_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic, "kernel": name,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
+    # whole-solve roofline: T_roof = max(64 B/unknown / HBM, F_alg / FP64)
+    f_alg = sum(v[0] or 0 for k, v in alg.items() if "dense" in k or k.startswith("step5_"))
+    b_alg = (64.0 if not p.real else 32.0) * p.unknowns * nrhs
+    t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (FP64_PEAK_TFLOPS * 1e12)) * 1e3
+    roof["solve"] = {"t_roof_ms": t_roof, "frac": t_roof / ms_max, "alg_bytes": b_alg, "alg_flops": f_alg}
     roof["stage_ms_per_step"] = {k: v[0] / max(1, args.steps) for k, v in stages.items() if v[1]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

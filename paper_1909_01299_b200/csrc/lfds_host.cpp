@@ -68,12 +68,14 @@ struct Axis {
   int64_t Wg = 0, lamg = 0, WI = 0, hoff = 0, hhoff = 0;
 };
 
-enum Stage { ST_X1, ST_Y1, ST_Z1, ST_EDGE, ST_IFRES, ST_GFWD, ST_GSWEEP, ST_GPROJ, ST_GPLANE, ST_FACE, ST_Z2, ST_Y7,
-             ST_X7, ST_WRITE, ST_RESID, ST_AXPY, ST_COUNT };
+// one stage per kernel kind (sine = FFT-based DST on uniform blocks, dense = DMMA contraction)
+enum Stage { ST_X1S, ST_X1D, ST_Y1S, ST_Y1D, ST_Z1, ST_EPROJ, ST_EDGE, ST_IFRES, ST_GFWD, ST_GSWEEP, ST_GPROJ,
+             ST_GPLANE, ST_FACE, ST_Z2, ST_Y7S, ST_Y7D, ST_X7S, ST_X7D, ST_WRITE, ST_RESID, ST_AXPY, ST_COUNT };
 const char* kStageNames[ST_COUNT] = {
-    "step1_x_forward", "step1_y_forward", "step2_zsolve", "step3_edge_values", "step4_iface_residual",
-    "step5_global_forward", "step5_global_zsolve", "step5_projection", "step5_plane_inverse", "step6_face_transform",
-    "step6_zsolve_lift", "step7_y_inverse", "step7_x_inverse", "step7_write_iface", "refine_residual", "refine_axpy"};
+    "step1_x_sine", "step1_x_dense", "step1_y_sine", "step1_y_dense", "step2_zsolve", "step3_edge_projection",
+    "step3_edge_values", "step4_iface_residual", "step5_plane_forward", "step5_global_zsolve", "step5_projection",
+    "step5_plane_inverse", "step6_face_transform", "step6_zsolve_lift", "step7_y_sine", "step7_y_dense",
+    "step7_x_sine", "step7_x_dense", "step7_write_iface", "refine_residual", "refine_axpy"};
 
 struct Profiler {
   struct Rec { int stage, launches; cudaEvent_t a, b; };
@@ -527,14 +529,24 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     P->launches += (s.n + 65534) / 65535;
     return LFDS_OK;
   };
+  // transform pass: sine-transform launches timed as stage st_s, dense ones as st_d
   auto xform = [&](const StageDescs& sc, const StageDescs& sr, const StageDescs& generic, bool kcontig,
-                   const std::vector<std::pair<int, StageDescs>>* sd = nullptr) -> int {
-    if (!pp.use_xform) return gemm(generic);
-    if (sd)
+                   const std::vector<std::pair<int, StageDescs>>* sd, int st_s, int st_d) -> int {
+    if (!pp.use_xform) {
+      begin(st_d);
+      int r = gemm(generic);
+      end();
+      return r;
+    }
+    if (sd && !sd->empty()) {
+      begin(st_s);
       for (auto& kv : *sd) {
         CUDA_TRY(launch_dst(pp.d_descs + kv.second.off, kv.second.n, kv.first, kv.second.maxN, kcontig, bufs, st));
         P->launches += (kv.second.n + 65534) / 65535;
       }
+      end();
+    }
+    begin(st_d);
     if (sc.n) {
       CUDA_TRY(launch_xform(pp.d_descs + sc.off, sc.n, sc.maxM, sc.maxN, false, kcontig, bufs, st));
       P->launches += (sc.n + 65534) / 65535;
@@ -543,22 +555,22 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
       CUDA_TRY(launch_xform(pp.d_descs + sr.off, sr.n, sr.maxM, sr.maxN, true, kcontig, bufs, st));
       P->launches += (sr.n + 65534) / 65535;
     }
+    end();
     return LFDS_OK;
   };
   int rc;
   // pass 1
-  begin(ST_X1);
-  if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s))) return rc;
-  end(); begin(ST_Y1);
-  if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s))) return rc;
-  end(); begin(ST_Z1);
+  if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s, ST_X1S, ST_X1D))) return rc;
+  if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s, ST_Y1S, ST_Y1D))) return rc;
+  begin(ST_Z1);
   CUDA_TRY(launch_zsolve(1, pp.d_zb, nblk, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv, st, P->real_z));
   P->launches++;
   end();
   if (nifx + nify > 0) {
-    begin(ST_EDGE);
+    begin(ST_EPROJ);
     CUDA_TRY(launch_proj(pp.d_pd, pp.n_pd3, P->lpad, 2, R * Nz, st, bufs));
     P->launches++;
+    end(); begin(ST_EDGE);
     if ((rc = gemm(pp.s3x))) return rc;
     if ((rc = gemm(pp.s3y))) return rc;
     end(); begin(ST_IFRES);
@@ -572,11 +584,11 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     ir.nbx = P->nbx; ir.nby = P->nby; ir.qpad = P->mpad; ir.ppad = P->lpad;
     CUDA_TRY(launch_iface_residual(ir, bufs, st));
     P->launches++;
-    end(); begin(ST_GFWD);
+    end();
     // step 5
-    if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true))) return rc;
-    if ((rc = xform(pp.s5r2, StageDescs{}, pp.s5r2, true))) return rc;
-    end(); begin(ST_GSWEEP);
+    if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
+    if ((rc = xform(pp.s5r2, StageDescs{}, pp.s5r2, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
+    begin(ST_GSWEEP);
     GSweep g{};
     g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
     g.lamx = X.lamg; g.lamy = Y.lamg; g.wxi = X.WI; g.wyi = Y.WI; g.r1 = pp.r1; g.r2 = pp.r2; g.what = 0;
@@ -596,10 +608,10 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
       CUDA_TRY(launch_projm(pm, bufs, st));
       P->launches += pm.nlc > 1 ? 2 : 1;
     }
-    end(); begin(ST_GPLANE);
-    if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true))) return rc;
-    if ((rc = xform(pp.s5wy, StageDescs{}, pp.s5wy, true))) return rc;
-    end(); begin(ST_FACE);
+    end();
+    if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
+    if ((rc = xform(pp.s5wy, StageDescs{}, pp.s5wy, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
+    begin(ST_FACE);
     // step 6
     if ((rc = gemm(pp.s6f))) return rc;
     end(); begin(ST_Z2);
@@ -608,11 +620,8 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     end();
   }
   // step 7
-  begin(ST_Y7);
-  if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false, &pp.y7s))) return rc;
-  end(); begin(ST_X7);
-  if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s))) return rc;
-  end();
+  if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false, &pp.y7s, ST_Y7S, ST_Y7D))) return rc;
+  if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s, ST_X7S, ST_X7D))) return rc;
   if (nifx + nify > 0) {
     begin(ST_WRITE);
     CUDA_TRY(launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st));

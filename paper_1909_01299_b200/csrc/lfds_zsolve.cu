@@ -479,7 +479,7 @@ struct RankStage {
 };
 
 template <bool REALZ, int TL, int NIF>
-__global__ void __launch_bounds__(ZT, 2) k_zs3(const ZBlock* __restrict__ blocks, int nz, ZTab tab, GSweep G,
+__global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks, int nz, ZTab tab, GSweep G,
                                                Bufs bufs, double* minpiv_out) {
   using RS = RankStage<TL, NIF>;
   constexpr int ZSEG = RS::ZSEG, TM = RS::TM, KA = RS::KA, NSTAGE = 3;
