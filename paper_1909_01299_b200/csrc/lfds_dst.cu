@@ -12,8 +12,6 @@
 // threads run R2-point FFTs.  Only the outputs k = 1..N-1 are kept.  FP64 CUDA-core
 // arithmetic: ~5 L log2 L flops per column instead of the 4 n^2 of the dense real matrix.
 #include <cuda_runtime.h>
-
-#include <algorithm>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -32,36 +30,7 @@ __device__ __forceinline__ zc2 zmul(zc2 a, zc2 b) {
 }
 
 // in-register radix-2 DIT FFT (forward, e^{-2 pi i k n / R}); all indices compile-time;
-// twiddles W_len^j = W_L^{j L/len} are warp-uniform broadcast reads of the W_L table, except
-// the trivial ones: W^0 = 1, W^{len/4} = -i, W^{len/8} = (1-i)/sqrt2, W^{3len/8} = (-1-i)/sqrt2
-// (only a third of the butterflies of a 16-point FFT need a general complex multiply)
-template <int R, int L, int LEN>
-__device__ __forceinline__ void fft_stage(zc2 (&v)[R], const double2* __restrict__ twl) {
-#pragma unroll
-  for (int i = 0; i < R; i += LEN) {
-#pragma unroll
-    for (int j = 0; j < LEN / 2; ++j) {
-      const zc2 u = v[i + j], b = v[i + j + LEN / 2];
-      zc2 t;
-      if (j == 0) {
-        t = b;
-      } else if (4 * j == LEN) {
-        t = zc2{b.y, -b.x};
-      } else if (8 * j == LEN) {
-        t = zc2{CUDART_SQRT_HALF * (b.x + b.y), CUDART_SQRT_HALF * (b.y - b.x)};
-      } else if (8 * j == 3 * LEN) {
-        t = zc2{CUDART_SQRT_HALF * (b.y - b.x), -CUDART_SQRT_HALF * (b.x + b.y)};
-      } else {
-        const double2 w2 = twl[j * (L / LEN)];
-        t = zmul(zc2{w2.x, w2.y}, b);
-      }
-      v[i + j] = zadd(u, t);
-      v[i + j + LEN / 2] = zsub(u, t);
-    }
-  }
-  if constexpr (2 * LEN <= R) fft_stage<R, L, 2 * LEN>(v, twl);
-}
-
+// twiddles W_len^j = W_L^{j L/len} are warp-uniform broadcast reads of the W_L table
 template <int R, int L>
 __device__ __forceinline__ void fft_reg(zc2 (&v)[R], const double2* __restrict__ twl) {
   // bit reversal
@@ -76,7 +45,20 @@ __device__ __forceinline__ void fft_reg(zc2 (&v)[R], const double2* __restrict__
       v[j] = t2;
     }
   }
-  fft_stage<R, L, 2>(v, twl);
+#pragma unroll
+  for (int len = 2; len <= R; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < R; i += len) {
+#pragma unroll
+      for (int j = 0; j < len / 2; ++j) {
+        const double2 w2 = twl[j * (L / len)];
+        const zc2 w{w2.x, w2.y};
+        const zc2 u = v[i + j], t = zmul(w, v[i + j + len / 2]);
+        v[i + j] = zadd(u, t);
+        v[i + j + len / 2] = zsub(u, t);
+      }
+    }
+  }
 }
 
 constexpr int DST_THREADS = 128;  // 8 columns per CTA at L = 256: small CTAs, many resident per SM
@@ -86,163 +68,125 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool val
                "l"(src), "r"(valid ? 16 : 0));
 }
 
-// Persistent CTAs: group g (CPB columns of one descriptor) is loaded by cp.async into one of
-// two input tiles while the previous group is transformed, so HBM reads, FFT arithmetic and
-// stores of different groups overlap inside every CTA.  Per group:
-//   load tile[p][col] (p < n) -> step 1 (R1-point FFTs, twiddles) -> exchange -> step 3
-//   (R2-point FFTs) -> (i/2) Y staged back into the consumed input tile -> coalesced stores.
-template <int R1, int R2>
-struct DstSmem {
-  static constexpr int L = R1 * R2, N = L / 2, CPB = DST_THREADS / R2, LDT = CPB + 1, LDE = R2 + 1;
-  static constexpr int TILE = (N - 1) * LDT, EX = CPB * R1 * LDE;
-  static constexpr size_t BYTES = (size_t)(2 * TILE + EX + L) * sizeof(double2) + 4 * CPB * sizeof(int64_t);
-};
-
 template <int R1, int R2, bool KCONTIG>
-__global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict__ descs, int ndesc, int gpd,
-                                                     Bufs bufs) {
-  using S = DstSmem<R1, R2>;
-  constexpr int L = S::L, N = S::N, CPB = S::CPB, LDT = S::LDT, LDE = S::LDE;
+__global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict__ descs, Bufs bufs) {
+  constexpr int L = R1 * R2, N = L / 2;
+  constexpr int CPB = DST_THREADS / R2;      // columns per CTA
+  constexpr int LDT = CPB + 1;               // tile row stride (complex)
+  constexpr int LDE = R2 + 1;                // exchange row stride
   extern __shared__ __align__(16) double2 dsm[];
-  double2* tiles = dsm;                         // [2][TILE]
-  double2* ex = dsm + 2 * S::TILE;              // [CPB][R1][LDE]
-  double2* twl = ex + S::EX;                    // W_L^j, j < L
-  int64_t* cols = reinterpret_cast<int64_t*>(twl + L);  // [2][CPB] input column offsets, [2][CPB] output
-  const int n = N - 1, tid = threadIdx.x;
-  const int total = ndesc * gpd;
-  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
-  for (int j = tid; j < L; j += DST_THREADS) twl[j] = __ldg(TAB + descs[0].a_off + j);  // same L for all descs
-  // column offsets of group g into cols[slot]
-  auto colsetup = [&](int g, int slot) {
-    if (tid < CPB) {
-      int64_t ib = -1, ob = -1;
-      if (g < total) {
-        const GemmDesc& D = descs[g / gpd];
-        const int64_t col = (int64_t)(g % gpd) * CPB + tid, NC = (int64_t)D.N1 * D.N2;
-        if (col < NC) {
-          const int64_t n1 = col / D.N2, n2 = col - n1 * D.N2;
-          ib = D.b_off + n1 * D.sB1 + n2 * D.sB2;
-          ob = D.c_off + n1 * D.sC1 + n2 * D.sC2;
-        }
-      }
-      cols[slot * CPB + tid] = ib;
-      cols[(2 + slot) * CPB + tid] = ob;
-    }
-  };
-  auto load = [&](int g, int slot) {  // every thread's copies of group g (cols[slot] ready)
-    if (g < total) {
-      const GemmDesc& D = descs[g / gpd];
-      const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]);
-      double2* tile = tiles + slot * S::TILE;
-      if (KCONTIG) {  // a column is contiguous in memory: sweep along p
-        for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
-          const int col = idx / n, p = idx - col * n;
-          const int64_t b = cols[slot * CPB + col];
-          cp_async16z(&tile[p * LDT + col], b >= 0 ? B + b + p : B, b >= 0);
-        }
-      } else {        // consecutive columns are adjacent in memory: sweep along col
-        for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
-          const int p = idx / CPB, col = idx - p * CPB;
-          const int64_t b = cols[slot * CPB + col];
-          cp_async16z(&tile[p * LDT + col], b >= 0 ? B + b + (int64_t)p * D.sBj : B, b >= 0);
-        }
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  int g = blockIdx.x;
-  colsetup(g, 0);
+  // buffer: tile [N-1][LDT] (load, later output staging) aliased with exchange [CPB][R1][LDE]
+  double2* tile = dsm;
+  double2* ex = dsm;
+  __shared__ double2 twl[L];                 // W_L^j, j < L
+  __shared__ int64_t colB[CPB], colC[CPB];
+  const GemmDesc& D = descs[blockIdx.z];
+  const int n = N - 1;
+  const int64_t N2 = D.N2, NC = (int64_t)D.N1 * D.N2;
+  const int64_t c0 = (int64_t)blockIdx.x * CPB;
+  if (c0 >= NC) return;
+  const int tid = threadIdx.x;
+  for (int j = tid; j < L; j += DST_THREADS) twl[j] = __ldg(reinterpret_cast<const double2*>(bufs.p[B_TAB]) + D.a_off + j);
+  if (tid < CPB) {
+    const int64_t col = c0 + tid;
+    const int64_t n1 = col / N2, n2 = col - n1 * N2;
+    colB[tid] = col < NC ? D.b_off + n1 * D.sB1 + n2 * D.sB2 : -1;
+    colC[tid] = col < NC ? D.c_off + n1 * D.sC1 + n2 * D.sC2 : -1;
+  }
   __syncthreads();
-  load(g, 0);
-  colsetup(g + gridDim.x, 1);
-  const int col = tid / R2, t = tid % R2;
-#pragma unroll 1
-  for (int it = 0; g < total; ++it, g += gridDim.x) {
-    const int cur = it & 1;
-    __syncthreads();  // cols[cur^1] ready; tile[cur^1] free (stores of the previous group done)
-    load(g + gridDim.x, cur ^ 1);
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    __syncthreads();  // group g staged by every thread
-    const GemmDesc& D = descs[g / gpd];
-    double2* tile = tiles + cur * S::TILE;
-    // ---- step 1: thread n2 = t: R1-point FFT over n1 of y[R2 n1 + n2], twiddle W_L^{n2 k1}
-    zc2 a[R1];
-#pragma unroll
-    for (int n1 = 0; n1 < R1; ++n1) {
-      const int q = R2 * n1 + t;
-      zc2 v{0, 0};
-      if (q > 0 && q < N) {
-        const double2 w = tile[(q - 1) * LDT + col];
-        v = zc2{w.x, w.y};
-      } else if (q > N) {
-        const double2 w = tile[(L - q - 1) * LDT + col];
-        v = zc2{-w.x, -w.y};
-      }
-      a[n1] = v;
+  const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]);
+  double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]);
+  // ---- load the CPB columns (n values each) into tile[p][col]: every copy is an async
+  // 16-byte cp.async, so all of a thread's loads are in flight at once
+  if (KCONTIG) {  // a column is contiguous in memory: sweep along p
+    for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
+      const int col = idx / n, p = idx - col * n;
+      const int64_t b = colB[col];
+      cp_async16z(&tile[p * LDT + col], b >= 0 ? B + b + p : B, b >= 0);
     }
-    fft_reg<R1, L>(a, twl);
-#pragma unroll
-    for (int k1 = 1; k1 < R1; ++k1) {
-      const double2 w = twl[(t * k1) % L];
-      a[k1] = zmul(a[k1], zc2{w.x, w.y});
-    }
-#pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) ex[(col * R1 + k1) * LDE + t] = make_double2(a[k1].x, a[k1].y);
-    __syncthreads();  // exchange written; tile[cur] consumed
-    // ---- step 3: thread k1 = t < R1: R2-point FFT over n2 -> Y[k1 + R1 k2], keep k < N
-    zc2 b[R2];
-    if (t < R1) {
-#pragma unroll
-      for (int n2 = 0; n2 < R2; ++n2) {
-        const double2 w = ex[(col * R1 + t) * LDE + n2];
-        b[n2] = zc2{w.x, w.y};
-      }
-      fft_reg<R2, L>(b, twl);
-      const double half = 0.5 * D.scale;
-#pragma unroll
-      for (int k2 = 0; k2 < R2 / 2; ++k2) {
-        const int k = t + R1 * k2;
-        if (k >= 1 && k < N) tile[(k - 1) * LDT + col] = make_double2(-half * b[k2].y, half * b[k2].x);  // (i/2) Y
-      }
-    }
-    colsetup(g + 2 * gridDim.x, cur);  // offsets of the group after next (cols[cur] input part is free)
-    __syncthreads();  // outputs staged
-    double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]);
-    const int64_t* oc = cols + (2 + cur) * CPB;
-    if (D.sCi == 1) {  // output column contiguous
-      for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
-        const int cc = idx / n, c = idx - cc * n;
-        const int64_t o = oc[cc];
-        if (o >= 0) C[o + c] = tile[c * LDT + cc];
-      }
-    } else {
-      for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
-        const int c = idx / CPB, cc = idx - c * CPB;
-        const int64_t o = oc[cc];
-        if (o >= 0) C[o + (int64_t)c * D.sCi] = tile[c * LDT + cc];
-      }
+  } else {        // consecutive columns are adjacent in memory: sweep along col
+    for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
+      const int p = idx / CPB, col = idx - p * CPB;
+      const int64_t b = colB[col];
+      cp_async16z(&tile[p * LDT + col], b >= 0 ? B + b + (int64_t)p * D.sBj : B, b >= 0);
     }
   }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  const int col = tid / R2, t = tid % R2;
+  // ---- step 1: thread n2 = t: R1-point FFT over n1 of y[R2 n1 + n2], twiddle W_L^{n2 k1}
+  zc2 a[R1];
+#pragma unroll
+  for (int n1 = 0; n1 < R1; ++n1) {
+    const int q = R2 * n1 + t;
+    zc2 v{0, 0};
+    if (q > 0 && q < N) {
+      const double2 w = tile[(q - 1) * LDT + col];
+      v = zc2{w.x, w.y};
+    } else if (q > N) {
+      const double2 w = tile[(L - q - 1) * LDT + col];
+      v = zc2{-w.x, -w.y};
+    }
+    a[n1] = v;
+  }
+  fft_reg<R1, L>(a, twl);
+#pragma unroll
+  for (int k1 = 1; k1 < R1; ++k1) {
+    const double2 w = twl[(t * k1) % L];
+    a[k1] = zmul(a[k1], zc2{w.x, w.y});
+  }
+  __syncthreads();  // tile fully consumed
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) ex[(col * R1 + k1) * LDE + t] = make_double2(a[k1].x, a[k1].y);
+  __syncthreads();
+  // ---- step 3: thread k1 = t < R1: R2-point FFT over n2 -> Y[k1 + R1 k2], keep k < N
+  zc2 b[R2];
+  if (t < R1) {
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+      const double2 w = ex[(col * R1 + t) * LDE + n2];
+      b[n2] = zc2{w.x, w.y};
+    }
+    fft_reg<R2, L>(b, twl);
+  }
+  __syncthreads();  // exchange consumed; reuse as output tile[c][col]
+  const double half = 0.5 * D.scale;
+  if (t < R1) {
+#pragma unroll
+    for (int k2 = 0; k2 < R2 / 2; ++k2) {
+      const int k = t + R1 * k2;
+      if (k >= 1 && k < N) tile[(k - 1) * LDT + col] = make_double2(-half * b[k2].y, half * b[k2].x);  // (i/2) Y
+    }
+  }
+  __syncthreads();
+  if (D.sCi == 1) {  // output column contiguous
+    for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
+      const int cc = idx / n, c = idx - cc * n;
+      const int64_t o = colC[cc];
+      if (o >= 0) C[o + c] = tile[c * LDT + cc];
+    }
+  } else {
+    for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
+      const int c = idx / CPB, cc = idx - c * CPB;
+      const int64_t o = colC[cc];
+      if (o >= 0) C[o + (int64_t)c * D.sCi] = tile[c * LDT + cc];
+    }
+  }
 }
 
 template <int R1, int R2, bool KC>
 cudaError_t dst_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
-  using S = DstSmem<R1, R2>;
-  const size_t sm = S::BYTES;
+  constexpr int L = R1 * R2, N = L / 2, CPB = DST_THREADS / R2;
+  const size_t tile = (size_t)(N - 1) * (CPB + 1) * sizeof(double2);
+  const size_t ex = (size_t)CPB * R1 * (R2 + 1) * sizeof(double2);
+  const size_t sm = tile > ex ? tile : ex;
   cudaError_t e = cudaFuncSetAttribute(k_dst<R1, R2, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dst<R1, R2, KC>, DST_THREADS, sm);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int gpd = (int)((maxN + S::CPB - 1) / S::CPB);
-  const int64_t total = (int64_t)ndesc * gpd;
-  if (total > INT32_MAX / 2) return cudaErrorInvalidValue;
-  const int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(1, per_sm));
-  k_dst<R1, R2, KC><<<(unsigned)grid, DST_THREADS, sm, st>>>(d, ndesc, gpd, bufs);
+  for (int z0 = 0; z0 < ndesc; z0 += 65535) {
+    const int nzz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
+    dim3 grid((unsigned)((maxN + CPB - 1) / CPB), 1, (unsigned)nzz);
+    k_dst<R1, R2, KC><<<grid, DST_THREADS, sm, st>>>(d + z0, bufs);
+  }
   return cudaGetLastError();
 }
 

@@ -126,7 +126,7 @@ struct lfds_plan {
   // device tables
   double2* d_tab = nullptr;
   size_t tab_elems = 0;
-  ZTab zt_scaled{}, zt_plain{};
+  ZTab zt_scaled{}, zt_plain{}, zt_lift{};  // zt_lift: zt_scaled rows divided by -sigma_k (step 6)
   std::map<int, int64_t> t_tw;  // FFT twiddle tables per length L
   int64_t t_hz = 0, t_hhz = 0, t_sig = 0, t_sige = 0, t_ifx = 0, t_ify = 0, t_bx = 0, t_by = 0, t_xlo = 0, t_ylo = 0;
   std::map<std::tuple<int, int, int>, PassPlan> passes;
@@ -615,7 +615,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     // step 6
     if ((rc = gemm(pp.s6f))) return rc;
     end(); begin(ST_Z2);
-    CUDA_TRY(launch_zsolve(2, pp.d_zb, nblk, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv, st, P->real_z));
+    CUDA_TRY(launch_zsolve(2, pp.d_zb, nblk, P->lpad, P->mpad, R, Nz, P->zt_lift, P->t_sig, nullptr, bufs, minpiv, st, P->real_z));
     P->launches++;
     end();
   }
@@ -826,6 +826,14 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
   }
   P->zt_plain = ZTab{T.put(za), T.put(zg), T.put(zcv), T.put(ze)};
   P->zt_scaled = ZTab{T.put(sa), T.put(sg), T.put(scv), T.put(se)};
+  {  // step-6 lifting RHS is -sigma_k (sum of face terms): fold -sigma_k into the rows
+    std::vector<zc> la(nz), lg(nz), lc(nz), le(nz);
+    for (int k = 0; k < nz; ++k) {
+      const zc f = -1.0 / P->sig_node[k];
+      la[k] = sa[k] * f; lg[k] = sg[k] * f; lc[k] = scv[k] * f; le[k] = se[k] * f;
+    }
+    P->zt_lift = ZTab{T.put(la), T.put(lg), T.put(lc), T.put(le)};
+  }
   for (int L = 16; L <= 512; L *= 2) {  // FFT twiddles W_L^j = exp(-2 pi i j/L) for the sine transforms
     std::vector<zc> tw(L);
     for (int j = 0; j < L; ++j) {

@@ -310,13 +310,15 @@ __global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks
 
 // ===================================================================== step 6
 // Face rows staged per segment, separate arrays per face: GL[j][TM], GR[j][TM] (indexed
-// by m), GB[j][TL], GT[j][TL] (indexed by l), sigma[j].  Every thread owns fixed copy slots
-// (shift/mask index math only): 2*ZSEG*(TL+TM) + ZSEG copies over ZT threads.
+// by m), GB[j][TL], GT[j][TL] (indexed by l).  Every thread owns fixed copy slots (shift/mask
+// index math only): 2*ZSEG*(TL+TM) copies over ZT threads.  The -sigma_k factor of the lifting
+// is folded into the rows of the z table the step-6 solve uses (row scaling leaves the
+// solution and the c'/d' recurrences unchanged).
 template <int TL, int ZSEG>
 struct FaceStage {
   static constexpr int TM = ZT / TL;
-  static constexpr int GB = 0, GT = ZSEG * TL, GL = 2 * ZSEG * TL, GR = GL + ZSEG * TM, SG = GR + ZSEG * TM;
-  static constexpr int SLOTS = SG + ZSEG;  // double2 per stage
+  static constexpr int GB = 0, GT = ZSEG * TL, GL = 2 * ZSEG * TL, GR = GL + ZSEG * TM;
+  static constexpr int SLOTS = GR + ZSEG * TM;  // double2 per stage
 };
 
 template <bool REALZ, int TL>
@@ -356,13 +358,10 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
         if (c < FS::GL) {  // GB / GT rows, TL entries each
           const int f = c / (ZSEG * TL), j = (c / TL) % ZSEG, li = c % TL, k = k0 + j;
           if (k < nz && t.l0 + li < B.nx && (f ? hT : hB)) src = IF + (f ? B.gT : B.gB) + ro + k * fs + t.l0 + li;
-        } else if (c < FS::SG) {  // GL / GR rows, TM entries each
+        } else {  // GL / GR rows, TM entries each
           const int c2 = c - FS::GL;
           const int f = c2 / (ZSEG * TM), j = (c2 / TM) % ZSEG, mi = c2 % TM, k = k0 + j;
           if (k < nz && t.m0 + mi < B.ny && (f ? hR : hL)) src = IF + (f ? B.gR : B.gL) + ro + k * fs + t.m0 + mi;
-        } else {
-          const int k = k0 + c - FS::SG;
-          if (k < nz) src = TAB + sig_off + k;
         }
         if (src) cp16(d + c, src);
       }
@@ -374,7 +373,8 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
   const cplx cB = hB && t.active ? mk(B.cB) * ld(TAB + B.wy0 + t.m) : mk(0, 0);
   const cplx cT = hT && t.active ? mk(B.cT) * ld(TAB + B.wy1 + t.m) : mk(0, 0);
   const int tx = threadIdx.x % TL, ty = threadIdx.x / TL;
-  // l~(k) = -sigma_k (cL_l GL[k][m] + cR_l GR[k][m] + cB_m GB[k][l] + cT_m GT[k][l])
+  // l~(k) = -sigma_k (cL_l GL[k][m] + cR_l GR[k][m] + cB_m GB[k][l] + cT_m GT[k][l]); the
+  // -sigma_k is in the (row-scaled) z table, so the right side is the bracket
   auto lift = [&](int sg, int j) {
     const double2* d = fsm + (sg & 1) * FS::SLOTS;
     cplx acc = mk(0, 0);
@@ -382,11 +382,9 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
     if (hR) acc = cfma(cR, mk(d[FS::GR + j * TM + ty]), acc);
     if (hB) acc = cfma(cB, mk(d[FS::GB + j * TL + tx]), acc);
     if (hT) acc = cfma(cT, mk(d[FS::GT + j * TL + tx]), acc);
-    const cplx sg2 = mk(d[FS::SG + j]);
-    return mk(-(sg2.x * acc.x - sg2.y * acc.y), -(sg2.x * acc.y + sg2.y * acc.x));
+    return acc;
   };
   __syncthreads();  // z tables
-  float minpiv = 1.0f;
   const cplx s = t.active ? ld(TAB + B.lamx + t.l) + ld(TAB + B.lamy + t.m) : mk(0, 0);
   // ---- forward sweep
   cplx cp = mk(0, 0), dp = mk(0, 0);
@@ -406,8 +404,7 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
           cplx a, b, c;
           double m2;
           zrow<REALZ>(T, k, s, a, b, c, m2);
-          const double n2 = elim<REALZ>(a, b, c, lift(sg, j), cp, dp);
-          minpiv = fminf(minpiv, __fdividef((float)n2, (float)fma(b.x, b.x, fma(b.y, b.y, m2))));
+          elim<REALZ>(a, b, c, lift(sg, j), cp, dp);  // same T_lm as step 2: pivots monitored there
         }
       }
     }
@@ -458,7 +455,6 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
     __syncthreads();
   }
   cp_wait<0>();
-  commit_minpiv(minpiv, minpiv_out);
 }
 
 // ===================================================================== step 5

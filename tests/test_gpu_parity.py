@@ -141,6 +141,48 @@ def test_edge_sizes(nz):
     assert rel(U[0], ref) < TOL
 
 
+def _steps_problem(hx, hy, nz, ix, iy, lam=0.3, seed=0, layers=(0.5, 2.0, 1.0)):
+    from workloads.configs import sigma_layers
+    hz, se, sn = sigma_layers(nz, np.array(layers))
+    return Problem(name="custom", hx=np.asarray(hx, complex), hy=np.asarray(hy, complex), hz=hz, sigma_edge=se,
+                   sigma_node=sn, lam=lam, iface_x=list(ix), iface_y=list(iy), nrhs=1, real=False, _rhs=None)
+
+
+def test_uniform_blocks_with_pml_blocks():
+    """Sine-transform (DST) blocks of 15 nodes (L = 32) between thin complex PML blocks: the
+    three-subgrid layout of PAPER.md:75 (tails / uniform core)."""
+    from workloads.configs import axis_steps
+    h = axis_steps(33, 0, 1.0, 4, "const")          # 4 PML + 33 core + 4 PML = 41 nodes
+    p = _steps_problem(h, h, 12, [5, 21, 37], [5, 21, 37])
+    rng = np.random.default_rng(11)
+    F = rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape)
+    plan, U = gpu_solve(p, F)
+    kinds = [plan.basis(0, b)[2] for b in range(4)]
+    assert kinds == [2, 0, 0, 2], kinds
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
+    assert rel(U[0], ref) < TOL
+
+
+@pytest.mark.parametrize("n", [7, 31, 63, 127, 255])
+def test_sine_transform_lengths(n):
+    """Every FFT length of the sine-transform kernel (L = 2(n+1) = 16 .. 512) against the oracle,
+    with the sine direction along x (contiguous columns) and along y (strided columns)."""
+    N = 2 * n + 1
+    hx = np.ones(N + 1)
+    hy = np.ones(10) * 0.7
+    p = _steps_problem(hx, hy, 3, [n + 1], [4])
+    rng = np.random.default_rng(n)
+    F = rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape)
+    _, U = gpu_solve(p, F)
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
+    assert rel(U[0], ref) < TOL
+    pt = _steps_problem(hy, hx, 3, [4], [n + 1])
+    Ft = np.ascontiguousarray(np.swapaxes(F, 2, 3))
+    _, Ut = gpu_solve(pt, Ft)
+    reft = oracle.solve_direct(pt, oracle.mass_rhs(pt, Ft[0]))
+    assert rel(Ut[0], reft) < TOL
+
+
 def test_zero_rhs_gives_zero():
     p = shrunken("c3")
     _, U = gpu_solve(p, np.zeros((1,) + p.shape, complex))
