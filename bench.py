@@ -9,8 +9,10 @@ in HBM.  Default workload: BASELINE.json configs[3] ("c4", 1024 x 1024 x 256, 8 
 blocks, complex128) — the largest config, the one north_star's roofline and scaling
 targets are quoted on; it fits one GPU (4.3 GB per array, larger than the 126 MB L2, so
 no L2 flush is needed between steps).  N > 1 (torchrun): every rank solves its own
-right-hand side of the same grid (RHS sharding: independent problems, no data-path
-collective, "scaling": "weak"); the time is the max over ranks.
+share of the blocks S^ij of the same problem (block sharding, north_star: LPT block ownership,
+step-5 global modes split by x-mode, two NCCL all-reduces for the interface exchange;
+"scaling": "strong"); C5's 64 right-hand sides are split across ranks instead (no collective,
+"weak").  The time is the max over ranks.
 
 The reference arm (--impl reference) is the CPU oracle (oracle/, test infrastructure) on
 the host cores, on a bounded sample of the same workload.
@@ -43,6 +45,9 @@ REFINE = {"c1": 0, "c2": 1, "c3": 0, "c4": 0, "c5": 0}
 # right-hand sides per pipeline pass (workspace scales with it): C5's 64 RHS x 0.84 GB per
 # array do not fit next to f and u in one pass; 16 per pass keeps the workspace at ~35 GB
 RHS_CHUNK = {"c5": 16}
+# multi-GPU split (north_star: blocks S^ij over the GPUs, NCCL for the interface exchange);
+# C5's 64 independent right-hand sides are split across GPUs instead (no exchange needed)
+DEFAULT_SHARD = {"c5": "rhs"}
 # FP64 peaks: derived 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 TF/s;
 # measured on this pool (profiles/r01_fp64_peaks.log): DMMA 37.1, DFMA 34.2 TF/s.
 FP64_PEAK_TFLOPS = 37.2
@@ -241,28 +246,43 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_1909_01299_b200 import Plan
+    from paper_1909_01299_b200 import dist as lfds_dist
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     p = make_problem(args.config)
-    # RHS sharding: rank r solves right-hand sides [r*nrhs, (r+1)*nrhs) of the same grid
+    shard = args.shard or DEFAULT_SHARD.get(args.config, "blocks")
+    blocks = shard == "blocks" and (world > 1 or args.shard == "blocks")  # --shard blocks: phased path at N=1 too
+    allreduce = None if world > 1 else (lambda t: None)
+    # blocks: every rank works on the same right-hand sides, owning a share of the blocks and
+    # of the step-5 modes (strong scaling); rhs: rank r solves its own right-hand sides
     nrhs = p.nrhs if args.nrhs <= 0 else args.nrhs
-    pw = dataclasses.replace(p, nrhs=nrhs * world)
+    pw = dataclasses.replace(p, nrhs=nrhs * (1 if blocks else world))
+    rhs0 = 0 if blocks else rank * nrhs
     refine = REFINE.get(args.config, 0) if args.refine is None else args.refine
+    if blocks and refine:
+        raise SystemExit("block-sharded solves do not refine; use --shard rhs for " + args.config)
     t0 = time.perf_counter()
     plan = Plan.from_problem(p, device=local_rank, refine=refine, profile=True,
-                             rhs_chunk=RHS_CHUNK.get(args.config, 0))
+                             rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0))
     setup_s = time.perf_counter() - t0
-    info = plan.info()
+    part = lfds_dist.shard(plan, rank, world) if blocks else None
     dt = torch.float64 if p.real else torch.complex128
     # right-hand sides generated one at a time straight into device memory (C5: 64 x 0.84 GB)
     f = torch.empty((nrhs,) + p.shape, dtype=dt, device=dev)
     for r in range(nrhs):
-        f[r].copy_(torch.from_numpy(pw.rhs(rank * nrhs + r)))
-    u = torch.empty_like(f)
+        f[r].copy_(torch.from_numpy(pw.rhs(rhs0 + r)))
+    u = torch.zeros_like(f)
+    ws = plan.workspace(nrhs) if blocks else None
+
+    def step():
+        if blocks:
+            lfds_dist.solve_sharded(plan, f, u, ws, allreduce)
+        else:
+            plan.solve(f, out=u)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        plan.solve(f, out=u)
+        step()
     torch.cuda.synchronize()
     plan.stage_times()  # reset
     if world > 1:
@@ -272,7 +292,7 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            plan.solve(f, out=u)
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -284,19 +304,35 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
-    units = p.unknowns * nrhs * world
+    units = p.unknowns * nrhs * (1 if blocks else world)
     value = units / (ms_max * 1e-3)
-    # correctness of what was timed: relative residual in double-double
+    # correctness of what was timed: relative residual in double-double (sharded: the ranks'
+    # parts of u are disjoint, their sum is the solution)
+    if blocks:
+        if world > 1:
+            dist.all_reduce(u)
+        plan.set_partition(None)
     _, norms = plan.residual(u, f, dd=True)
     rel_res = float(max(norms[:, 0] / norms[:, 1]))
-    # e2e: host (pinned) buffers through lfds_solve_host, copies inside the timed region
+    if blocks:
+        lfds_dist.shard(plan, rank, world)
+        ws = plan.workspace(nrhs)
+    # e2e: host (pinned) buffers through the public API, copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        # e2e: host (pinned) buffers; at most E2E_RHS right-hand sides (host memory bound)
-        ne = min(nrhs, args.e2e_rhs)
+        ne = min(nrhs, args.e2e_rhs) if not blocks else nrhs
         fh = f[:ne].cpu().pin_memory()
         uh = torch.empty_like(fh).pin_memory()
-        plan.solve_host(fh, out=uh)
+
+        def step_host():
+            if blocks:  # H2D of f, sharded solve, D2H of u (this rank's part)
+                f.copy_(fh, non_blocking=True)
+                lfds_dist.solve_sharded(plan, f, u, ws, allreduce)
+                uh.copy_(u, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            else:
+                plan.solve_host(fh, out=uh)
+        step_host()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -304,14 +340,14 @@ def run_ours(args, rank, world, local_rank):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(k2):
-            plan.solve_host(fh, out=uh)
+            step_host()
         b.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / k2], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         nbytes = fh.numel() * fh.element_size()
-        e2e = {"value": p.unknowns * ne * world / (float(t.item()) * 1e-3), "unit": UNIT,
+        e2e = {"value": p.unknowns * ne * (1 if blocks else world) / (float(t.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item()),
                "nrhs_per_gpu": ne}
     # roofline of the dominant stage (the kernel kind with the largest device time per step);
@@ -356,11 +392,14 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong" if blocks else "weak",
             "vs_baseline": None, "dtype": "c128" if not p.real else "f64", "data": "synthetic",
             "config": {"workload": args.config, "nx": p.nx, "ny": p.ny, "nz": p.nz,
                        "blocks": [len(p.iface_x) + 1, len(p.iface_y) + 1], "nrhs_per_gpu": nrhs,
-                       "refine_passes": refine, "parallelism": f"rhs-sharded x{world}" if world > 1 else "1 gpu",
+                       "refine_passes": refine,
+                       "parallelism": (f"block-sharded x{world} (LPT blocks, step-5 modes, 2 NCCL all-reduces)"
+                                       if blocks else f"rhs-sharded x{world}" if world > 1 else "1 gpu"),
                        "l2": "inputs larger than L2 (no flush)" if p.unknowns * 16 > 126e6 else "L2-resident",
                        "setup_s": setup_s, "rel_residual_dd": rel_res},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
@@ -381,6 +420,8 @@ def main():
     ap.add_argument("--refine", type=int, default=None)
     ap.add_argument("--cpu-nz", type=int, default=16, dest="cpu_nz")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", choices=["blocks", "rhs"], default=None,
+                    help="N > 1: block sharding with two NCCL exchanges (default) or RHS sharding")
     ap.add_argument("--e2e-rhs", type=int, default=8, dest="e2e_rhs", help="RHS per e2e step (host memory)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -118,6 +118,30 @@ int lfds_solve_host(lfds_plan* plan, const void* f_host, void* u_host, int nrhs,
 int lfds_residual(lfds_plan* plan, const void* u_dev, const void* f_dev, lfds_z* r_dev, int nrhs,
                   int dd, double* norms, void* cuda_stream);
 
+/*
+ * Block sharding across ranks (BASELINE.json north_star: "partitioned across the 8 B200s by
+ * blocks S^ij, with NCCL over NVLink only for the interface exchange").  Every rank builds the
+ * same plan, then lfds_set_partition tells it which blocks it computes in the two block passes
+ * (steps 1-3, 6-7), which global x-modes l in [l_begin, l_end) it
+ * sweeps in step 5, and whether it is the rank (exactly one) that adds the
+ * b = M f terms of the step-4 residual and writes u on the interface planes.
+ *  block_owned[nbx*nby]  host, row-major [block_y][block_x], nonzero = computed here;
+ *                        NULL restores the unpartitioned plan.
+ * A solve is then three phases on the caller's stream, with two sums over the ranks:
+ *   lfds_solve_phase(1) -> sum exchange 1 over ranks (in place, e.g. NCCL all-reduce)
+ *   lfds_solve_phase(2) -> sum exchange 2 over ranks
+ *   lfds_solve_phase(3)
+ * lfds_exchange_layout gives each exchange's byte offset inside the workspace and its length
+ * in doubles (exchange 1 = the interface residual on the planes, exchange 2 = the step-5
+ * correction projected onto the planes).  Afterwards u_dev holds u on this rank's blocks (and,
+ * for the rank0 rank, on the interface planes); other entries are not written.  Phased solves
+ * take all nrhs right-hand sides in one pass and do not refine (LFDS_EINVAL otherwise).
+ */
+int lfds_set_partition(lfds_plan* plan, const int* block_owned, int l_begin, int l_end, int rank0);
+int lfds_exchange_layout(const lfds_plan* plan, int nrhs, int which, size_t* byte_offset, size_t* n_doubles);
+int lfds_solve_phase(lfds_plan* plan, int phase, const void* f_dev, void* u_dev, int nrhs, void* ws,
+                     size_t ws_bytes, void* cuda_stream);
+
 typedef struct {
   int passes;                  /* solve passes in the last lfds_solve (1 + refinements)     */
   double rel_residual[9];      /* ||Au-Mf||/||Mf|| after each pass (max over rhs), if known */

@@ -99,11 +99,12 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   GemmDesc* d_descs = nullptr;
   ZBlock* d_zb = nullptr;
   PDesc* d_pd = nullptr;     // step-3 two-sided edge projections, one per block
+  int nzb = 0;               // owned blocks (entries of d_zb before the global one)
+  int* d_own = nullptr;      // per-block ownership flags (step-4 partial residual)
   int n_pd3 = 0;
-  StageDescs s1x, s1y, s3g, s3h, s3x, s3y, s5r1, s5r2, s5p1, s5p2, s5wx, s5wy, s6f, s7y, s7x;
+  StageDescs s1x, s1y, s3x, s3y, s5r1, s5r2, s5wx, s5wy, s6f, s7y, s7x;
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
   std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
-  StageDescs m5p1, m5p2;                    // few-row DMMA contractions (<= 8 rows each)
   bool use_xform = false;
   int max_systems = 0, max_systems_global = 0;
   // workspace layout (bytes)
@@ -134,6 +135,11 @@ struct lfds_plan {
   lfds_info info{};
   int launches = 0;
   Profiler prof;
+  // block sharding (lfds_set_partition): owned blocks, the global x-mode range of step 5,
+  // and whether this rank adds the b-terms of the interface residual and writes u on the planes
+  std::vector<char> own;
+  int l_begin = 0, l_end = -1, rank0 = 1;
+  bool sharded = false;
 };
 
 namespace {
@@ -185,13 +191,16 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   const int Nx = X.N, Ny = Y.N, Nz = P->nz;
   const int nbx = P->nbx, nby = P->nby, nblk = nbx * nby;
   const int nifx = (int)X.iface.size(), nify = (int)Y.iface.size();
-  // block mode-space offsets
-  std::vector<int64_t> ms(nblk), t1(nblk);
+  // blocks this plan computes (all, unless lfds_set_partition gave this rank a subset)
+  auto owned = [&](int b) { return P->own.empty() || P->own[b] != 0; };
+  // block mode-space offsets (owned blocks only, packed)
+  std::vector<int64_t> ms(nblk, 0), t1(nblk, 0);
   int64_t acc = 0;
   int maxsys = 0;
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
       int b = j * nbx + i;
+      if (!owned(b)) continue;
       ms[b] = acc;
       t1[b] = acc;
       acc += (int64_t)X.blocks[i].n * Y.blocks[j].n * Nz * R;
@@ -209,9 +218,9 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   pp.ry = o; o += align4((int64_t)nify * R * Nz * Nx);
   pp.r1 = o; o += align4((int64_t)nifx * R * Ny * Nz);
   pp.r2 = o; o += align4((int64_t)nify * R * Nx * Nz);
-  pp.p1 = o; o += align4((int64_t)nifx * R * Ny * Nz);
-  pp.gp = o; o += align4((int64_t)(projm_chunks(Nx) > 1 ? projm_chunks(Nx) : 0) * nifx * R * Ny * Nz);
+  pp.p1 = o; o += align4((int64_t)nifx * R * Ny * Nz);   // exchange 2 = [p1, p2] (contiguous)
   pp.p2 = o; o += align4((int64_t)nify * R * Nx * Nz);
+  pp.gp = o; o += align4((int64_t)(projm_chunks(Nx) > 1 ? projm_chunks(Nx) : 0) * nifx * R * Ny * Nz);
   pp.wx = o; o += align4((int64_t)nifx * R * Nz * Ny);
   pp.wy = o; o += align4((int64_t)nify * R * Nz * Nx);
   pp.gf = o; o += align4((int64_t)nblk * 4 * R * P->fpad * Nz);
@@ -246,10 +255,13 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   // Layouts (complex elements): T1 and MS per block [r][k][q|m][l] (l fastest), so a block's
   // mode space is [rk][m][l] and every z-line (fixed m, l) is strided by nx*ny.
   // step 1: x-forward  T1[rk][q][l] = sum_p F_x[l][p] f[rk][y0+q][x0+p]
+  std::vector<int> blk_ids;  // block of each descriptor of the per-block stages s1x, s1y, s7y, s7x
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
       int b = j * nbx + i;
+      if (!owned(b)) continue;
+      blk_ids.push_back(b);
       v.push_back(gd(bx.F, bx.n, 1, bx.n, bx.n, B_F, (int64_t)(by.lo - 1) * Nx + (bx.lo - 1), 1, (int64_t)Nx * Ny, Nx,
                      B_T1, t1[b], 1, (int64_t)by.n * bx.n, bx.n, (int)RZ, by.n, inF));
     }
@@ -259,34 +271,18 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
       int b = j * nbx + i;
+      if (!owned(b)) continue;
       const int64_t pl = (int64_t)bx.n * by.n;
       v.push_back(gd(by.F, by.n, 1, by.n, by.n, B_T1, t1[b], bx.n, pl, 1, B_MS, ms[b], bx.n, pl, 1, (int)RZ, bx.n, 0));
     }
   stage(pp.s1y, std::move(v)); v.clear();
-  // step 3: G[b][e][rk][m] = sum_l W_x[e_row][l] v~[rk][m][l];  H[b][e][rk][l] = sum_m W_y[e_row][m] v~[rk][m][l]
-  for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i) {
-      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
-      int b = j * nbx + i;
-      const int64_t pl = (int64_t)bx.n * by.n;
-      v.push_back(gd(bx.W, (int64_t)(bx.n - 1) * bx.n, 1, 2, bx.n, B_MS, ms[b], 1, pl, bx.n, B_IF,
-                     pp.g_off + (int64_t)b * 2 * RZ * P->mpad, RZ * P->mpad, P->mpad, 1, (int)RZ, by.n, 0));
-    }
-  stage(pp.s3g, std::move(v)); v.clear();
-  for (int j = 0; j < nby; ++j)
-    for (int i = 0; i < nbx; ++i) {
-      const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
-      int b = j * nbx + i;
-      const int64_t pl = (int64_t)bx.n * by.n;
-      v.push_back(gd(by.W, (int64_t)(by.n - 1) * by.n, 1, 2, by.n, B_MS, ms[b], bx.n, pl, 1, B_IF,
-                     pp.h_off + (int64_t)b * 2 * RZ * P->lpad, RZ * P->lpad, P->lpad, 1, (int)RZ, bx.n, 0));
-    }
-  stage(pp.s3h, std::move(v)); v.clear();
+  // step 3 (edge rows G, H of v~): k_proj descriptors below
   // VX[b][e][rk][q] = sum_m W_y[q][m] G[b][e][rk][m];  VY[b][e][rk][p] = sum_l W_x[p][l] H[b][e][rk][l]
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock& by = Y.blocks[j];
       int b = j * nbx + i;
+      if (!owned(b)) continue;
       v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_IF, pp.g_off + (int64_t)b * 2 * RZ * P->mpad, 1, P->mpad, 0, B_IF,
                      pp.vx_off + (int64_t)b * 2 * RZ * P->mpad, 1, P->mpad, 0, (int)(2 * RZ), 1, 0));
     }
@@ -295,6 +291,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock& bx = X.blocks[i];
       int b = j * nbx + i;
+      if (!owned(b)) continue;
       v.push_back(gd(bx.W, bx.n, 1, bx.n, bx.n, B_IF, pp.h_off + (int64_t)b * 2 * RZ * P->lpad, 1, P->lpad, 0, B_IF,
                      pp.vy_off + (int64_t)b * 2 * RZ * P->lpad, 1, P->lpad, 0, (int)(2 * RZ), 1, 0));
     }
@@ -304,24 +301,20 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   stage(pp.s5r1, std::move(v)); v.clear();
   if (nify) v.push_back(gd(X.Wg, 1, Nx, Nx, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2, 1, Nx, 0, (int)(nify * RZ), 1, 0));
   stage(pp.s5r2, std::move(v)); v.clear();
-  // P1[a][rk][m] = sum_l W_x[I_a][l] W^[rk][m][l];  P2[b][rk][l] = sum_m W_y[I_b][m] W^[rk][m][l]
-  if (nifx) v.push_back(gd(X.WI, Nx, 1, nifx, Nx, B_T1, 0, 1, Nx, 0, B_IF, pp.p1, RZ * Ny, 1, 0, (int)(RZ * Ny), 1, 0));
-  stage(pp.s5p1, std::move(v)); v.clear();
-  if (nify) v.push_back(gd(Y.WI, Ny, 1, nify, Ny, B_T1, 0, Nx, (int64_t)Ny * Nx, 1, B_IF, pp.p2, RZ * Nx, Nx, 1,
-                           (int)RZ, Nx, 0));
-  stage(pp.s5p2, std::move(v)); v.clear();
+  // P1, P2 (projections of w^ onto the planes): k_projm, see run_pass
   // w on the planes: WX[a][rk][q] = sum_m W_y[q][m] P1[a][rk][m];  WY[b][rk][p] = sum_l W_x[p][l] P2[b][rk][l]
   if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, 1, Ny, 0, B_IF, pp.wx, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
   stage(pp.s5wx, std::move(v)); v.clear();
   if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, 1, Nx, 0, B_IF, pp.wy, 1, Nx, 0, (int)(nify * RZ), 1, 0));
   stage(pp.s5wy, std::move(v)); v.clear();
   // step 6: face transforms GF[b][face][rk][mode] (faces L, R, B, T), e.g. GL = F_y w_L
-  std::vector<ZBlock> zb(nblk);
+  std::vector<ZBlock> zb;  // owned blocks (k_zs1, k_zs2), then the global 'block' (k_zs3)
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
       int b = j * nbx + i;
-      ZBlock& z = zb[b];
+      if (!owned(b)) continue;
+      ZBlock z{};
       z.ms_off = ms[b];
       z.buf = B_MS;
       z.nx = bx.n;
@@ -357,13 +350,16 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
         if (side == 0) { z.gB = face_off(2); z.cB = make_double2(c.real(), c.imag()); }
         else { z.gT = face_off(3); z.cT = make_double2(c.real(), c.imag()); }
       }
+      zb.push_back(z);
     }
+  pp.nzb = (int)zb.size();
   stage(pp.s6f, std::move(v)); v.clear();
   // step 7: y-inverse T1[rk][q][l] = sum_m W_y[q][m] MS[rk][m][l];  x-inverse u[rk][y0+q][x0+p] = sum_l W_x[p][l] T1
   for (int j = 0; j < nby; ++j)
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
       int b = j * nbx + i;
+      if (!owned(b)) continue;
       const int64_t pl = (int64_t)bx.n * by.n;
       v.push_back(gd(by.W, by.n, 1, by.n, by.n, B_MS, ms[b], bx.n, pl, 1, B_T1, t1[b], bx.n, pl, 1, (int)RZ, bx.n, 0));
     }
@@ -372,30 +368,12 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     for (int i = 0; i < nbx; ++i) {
       const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
       int b = j * nbx + i;
+      if (!owned(b)) continue;
       v.push_back(gd(bx.W, bx.n, 1, bx.n, bx.n, B_T1, t1[b], 1, (int64_t)by.n * bx.n, bx.n, B_U,
                      (int64_t)(by.lo - 1) * Nx + (bx.lo - 1), 1, (int64_t)Nx * Ny, Nx, (int)RZ, by.n, outF));
     }
   stage(pp.s7x, std::move(v)); v.clear();
 
-  // few-row contractions (step 3 edge rows, step 5 projections): split into <= 8-row slices
-  {
-    std::vector<GemmDesc> vm;
-    auto split8 = [&](StageDescs& dst, const StageDescs& src) {
-      for (int q = 0; q < src.n; ++q) {
-        const GemmDesc d0 = D[src.off + q];
-        for (int r0 = 0; r0 < d0.M; r0 += 8) {
-          GemmDesc d = d0;
-          d.M = std::min(8, d0.M - r0);
-          d.a_off += (int64_t)r0 * d0.sAi;
-          d.c_off += (int64_t)r0 * d0.sCi;
-          vm.push_back(d);
-        }
-      }
-      stage(dst, std::move(vm)); vm.clear();
-    };
-    split8(pp.m5p1, pp.s5p1);
-    split8(pp.m5p2, pp.s5p2);
-  }
   // DMMA transform passes: the same contractions, split by real / complex eigenvector matrix
   pp.use_xform = !in_real && !out_real;
   if (pp.use_xform) {
@@ -405,8 +383,8 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
       std::map<int, std::vector<GemmDesc>> vd;  // DST descriptors grouped by block length
       for (int q = 0; q < src.n; ++q) {
         GemmDesc d = D[src.off + q];
-        // stages s1x/s7x/s1y/s7y hold one descriptor per block, in block order
-        const int b = q;
+        // stages s1x/s7x/s1y/s7y hold one descriptor per owned block, in block order
+        const int b = blk_ids[q];
         const AxisBlock& ab = xaxis ? X.blocks[b % nbx] : Y.blocks[b / nbx];
         const int64_t roff = fwd ? ab.Fr : ab.Wr;
         if (ab.dst) {
@@ -451,6 +429,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
       for (int i = 0; i < nbx; ++i) {
         const AxisBlock &bx = X.blocks[i], &by = Y.blocks[j];
         const int b = j * nbx + i;
+        if (!owned(b)) continue;
         PDesc d{};
         d.x_off = ms[b];
         d.ps = (int64_t)bx.n * by.n;
@@ -475,6 +454,12 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     CUDA_TRY(cudaMalloc(&pp.d_pd, sizeof(PDesc) * std::max<size_t>(1, pd.size())));
     CUDA_TRY(cudaMemcpy(pp.d_pd, pd.data(), sizeof(PDesc) * pd.size(), cudaMemcpyHostToDevice));
   }
+  {
+    std::vector<int> own(nblk);
+    for (int b = 0; b < nblk; ++b) own[b] = owned(b) ? 1 : 0;
+    CUDA_TRY(cudaMalloc(&pp.d_own, sizeof(int) * nblk));
+    CUDA_TRY(cudaMemcpy(pp.d_own, own.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(cudaMalloc(&pp.d_zb, sizeof(ZBlock) * zb.size()));
   CUDA_TRY(cudaMemcpy(pp.d_zb, zb.data(), sizeof(ZBlock) * zb.size(), cudaMemcpyHostToDevice));
   return LFDS_OK;
@@ -494,7 +479,13 @@ static int get_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan** o
 }
 
 // ------------------------------------------------------------------ one pipeline pass (steps 1-7)
-static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, int out_dtype, cudaStream_t st) {
+// phases (bit mask): 1 = pass 1 (steps 1-3) and this rank's part of the step-4 residual;
+// 2 = step 5 on this rank's global x-modes; 4 = plane inverse, pass 2 (steps 6-7).  With block
+// sharding the caller sums exchange 1 ([RX, RY]) over the ranks between phases 1 and 2 and
+// exchange 2 ([P1, P2]) between phases 2 and 4 (lfds_exchange_layout).
+enum { PH_1 = 1, PH_2 = 2, PH_3 = 4, PH_ALL = 7 };
+static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, int out_dtype, cudaStream_t st,
+                    int phases = PH_ALL) {
   const Axis& X = P->ax[0];
   const Axis& Y = P->ax[1];
   const int Nx = X.N, Ny = Y.N, Nz = P->nz;
@@ -520,12 +511,6 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   auto gemm = [&](const StageDescs& s) -> int {
     if (!s.n) return LFDS_OK;
     CUDA_TRY(launch_gemm(pp.d_descs + s.off, s.n, s.maxM, (int)std::min<int64_t>(s.maxN, INT32_MAX), 0, bufs, st));
-    P->launches += (s.n + 65534) / 65535;
-    return LFDS_OK;
-  };
-  auto m8 = [&](const StageDescs& s, bool kcontig) -> int {
-    if (!s.n) return LFDS_OK;
-    CUDA_TRY(launch_xform_m8(pp.d_descs + s.off, s.n, s.maxN, kcontig, bufs, st));
     P->launches += (s.n + 65534) / 65535;
     return LFDS_OK;
   };
@@ -559,14 +544,21 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     return LFDS_OK;
   };
   int rc;
+  const bool has_if = nifx + nify > 0;
+  const int l_begin = P->sharded ? P->l_begin : 0, l_end = P->sharded ? P->l_end : Nx;
+  (void)nblk;
   // pass 1
+  if (phases & PH_1) {
   if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s, ST_X1S, ST_X1D))) return rc;
   if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s, ST_Y1S, ST_Y1D))) return rc;
   begin(ST_Z1);
-  CUDA_TRY(launch_zsolve(1, pp.d_zb, nblk, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv, st, P->real_z));
-  P->launches++;
+  if (pp.nzb) {
+    CUDA_TRY(launch_zsolve(1, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv,
+                           st, P->real_z));
+    P->launches++;
+  }
   end();
-  if (nifx + nify > 0) {
+  if (has_if) {
     begin(ST_EPROJ);
     CUDA_TRY(launch_proj(pp.d_pd, pp.n_pd3, P->lpad, 2, R * Nz, st, bufs));
     P->launches++;
@@ -582,9 +574,13 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     ir.rx = pp.rx; ir.ry = pp.ry; ir.vxo = pp.vx_off; ir.vyo = pp.vy_off;
     ir.blk_of_x = P->t_bx; ir.blk_of_y = P->t_by; ir.xlo = P->t_xlo; ir.ylo = P->t_ylo;
     ir.nbx = P->nbx; ir.nby = P->nby; ir.qpad = P->mpad; ir.ppad = P->lpad;
+    ir.own = pp.d_own; ir.with_b = P->sharded ? P->rank0 : 1;
     CUDA_TRY(launch_iface_residual(ir, bufs, st));
     P->launches++;
     end();
+  }
+  }
+  if ((phases & PH_2) && has_if) {
     // step 5
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     if ((rc = xform(pp.s5r2, StageDescs{}, pp.s5r2, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
@@ -592,15 +588,24 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     GSweep g{};
     g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
     g.lamx = X.lamg; g.lamy = Y.lamg; g.wxi = X.WI; g.wyi = Y.WI; g.r1 = pp.r1; g.r2 = pp.r2; g.what = 0;
-    CUDA_TRY(launch_zsolve(3, pp.d_zb + nblk, 1, Nx, Ny, R, Nz, P->zt_plain, P->t_sig, &g, bufs, minpiv, st,
+    g.l_begin = l_begin; g.l_end = l_end;
+    CUDA_TRY(launch_zsolve(3, pp.d_zb + pp.nzb, 1, Nx, Ny, R, Nz, P->zt_plain, P->t_sig, &g, bufs, minpiv, st,
                            P->real_z));
     P->launches += 1;
     end(); begin(ST_GPROJ);
     {
-      ProjM pm{};
-      pm.nx = Nx; pm.ny = Ny; pm.nplanes = R * Nz; pm.E1 = nifx; pm.E2 = nify; pm.nlc = projm_chunks(Nx);
-      pm.x_buf = B_T1; pm.x_off = 0; pm.wr = X.WI; pm.wc = Y.WI;
       const int64_t RZ = (int64_t)R * Nz;
+      if (l_begin >= l_end) {  // no x-modes on this rank: it contributes zero to exchange 2
+        CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.p1, 0,
+                                 sizeof(double2) * (size_t)(pp.gp - pp.p1), st));
+      } else if (l_begin > 0 || l_end < Nx) {  // P2 rows outside this rank's x-modes must sum to zero
+        CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.p2, 0,
+                                 sizeof(double2) * (size_t)nify * RZ * Nx, st));
+      }
+      ProjM pm{};
+      pm.nx = Nx; pm.ny = Ny; pm.nplanes = R * Nz; pm.E1 = nifx; pm.E2 = nify;
+      pm.l_begin = l_begin; pm.l_end = l_end; pm.nlc = projm_chunks(l_end - l_begin);
+      pm.x_buf = B_T1; pm.x_off = 0; pm.wr = X.WI; pm.wc = Y.WI;
       pm.g_es = RZ * Ny; pm.g_ps = Ny; pm.p1_off = pp.p1; pm.p1_es = RZ * Ny;
       if (pm.nlc > 1) { pm.g_off = pp.gp; pm.g_lcs = (int64_t)nifx * RZ * Ny; }
       else { pm.g_off = pp.p1; pm.g_lcs = 0; }
@@ -609,24 +614,31 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
       P->launches += pm.nlc > 1 ? 2 : 1;
     }
     end();
+  }
+  if (phases & PH_3) {
+  if (has_if) {
     if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
     if ((rc = xform(pp.s5wy, StageDescs{}, pp.s5wy, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
     begin(ST_FACE);
     // step 6
     if ((rc = gemm(pp.s6f))) return rc;
     end(); begin(ST_Z2);
-    CUDA_TRY(launch_zsolve(2, pp.d_zb, nblk, P->lpad, P->mpad, R, Nz, P->zt_lift, P->t_sig, nullptr, bufs, minpiv, st, P->real_z));
-    P->launches++;
+    if (pp.nzb) {
+      CUDA_TRY(launch_zsolve(2, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_lift, P->t_sig, nullptr, bufs, minpiv,
+                             st, P->real_z));
+      P->launches++;
+    }
     end();
   }
   // step 7
   if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false, &pp.y7s, ST_Y7S, ST_Y7D))) return rc;
   if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s, ST_X7S, ST_X7D))) return rc;
-  if (nifx + nify > 0) {
+  if (has_if && (!P->sharded || P->rank0)) {
     begin(ST_WRITE);
     CUDA_TRY(launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st));
     P->launches++;
     end();
+  }
   }
   return LFDS_OK;
 }
@@ -980,8 +992,87 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
   return LFDS_OK;
 }
 
+int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_end, int rank0) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  const int nblk = P->nbx * P->nby, Nx = P->ax[0].N;
+  if (!block_owned) {  // back to the whole problem on this device
+    P->own.clear();
+    P->sharded = false;
+    P->l_begin = 0;
+    P->l_end = -1;
+    P->rank0 = 1;
+  } else {
+    if (l_begin < 0 || l_end < l_begin || l_end > Nx) return fail(LFDS_EINVAL, "bad x-mode range [%d, %d) of %d", l_begin, l_end, Nx);
+    P->own.assign(block_owned, block_owned + nblk);
+    P->sharded = true;
+    P->l_begin = l_begin;
+    P->l_end = l_end;
+    P->rank0 = rank0 ? 1 : 0;
+  }
+  for (auto& kv : P->passes) {  // descriptors depend on the owned blocks: rebuild lazily
+    cudaFree(kv.second.d_descs);
+    cudaFree(kv.second.d_zb);
+    cudaFree(kv.second.d_pd);
+    cudaFree(kv.second.d_own);
+  }
+  P->passes.clear();
+  return LFDS_OK;
+}
+
+int lfds_exchange_layout(const lfds_plan* cp, int nrhs, int which, size_t* byte_offset, size_t* n_doubles) {
+  lfds_plan* P = const_cast<lfds_plan*>(cp);
+  if (!P || (which != 1 && which != 2) || !byte_offset || !n_doubles) return fail(LFDS_EINVAL, "bad arguments");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  const int R = chunk_of(P, nrhs);
+  if (R != nrhs) return fail(LFDS_EINVAL, "sharded solves take all right-hand sides in one pass (rhs_chunk)");
+  PassPlan* pp;
+  int rc = get_pass(P, R, P->opt.dtype == LFDS_F64, P->opt.dtype == LFDS_F64, &pp);
+  if (rc) return rc;
+  const int64_t lo = which == 1 ? pp->rx : pp->p1, hi = which == 1 ? pp->r1 : pp->gp;  // [RX, RY] / [P1, P2]
+  *byte_offset = pp->off_if + (size_t)lo * 16;
+  *n_doubles = (size_t)(hi - lo) * 2;
+  return LFDS_OK;
+}
+
+int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes,
+                     void* stream) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  if (phase < 1 || phase > 3) return fail(LFDS_EINVAL, "phase must be 1, 2 or 3");
+  if (nrhs < 1 || !f_dev || !u_dev || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
+  if (P->opt.refine != 0) return fail(LFDS_EINVAL, "phased (sharded) solves do not refine");
+  const int R = chunk_of(P, nrhs);
+  if (R != nrhs) return fail(LFDS_EINVAL, "phased solves take all right-hand sides in one pass (rhs_chunk)");
+  const int dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
+  PassPlan* pp;
+  int rc;
+  if ((rc = get_pass(P, R, dt, dt, &pp))) return rc;
+  if (ws_bytes < pp->total) return fail(LFDS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, pp->total);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* w = reinterpret_cast<char*>(ws);
+  Bufs b{};
+  b.p[B_TAB] = P->d_tab;
+  b.p[B_F] = const_cast<void*>(f_dev);
+  b.p[B_U] = u_dev;
+  b.p[B_MS] = w + pp->off_ms;
+  b.p[B_T1] = w + pp->off_t1;
+  b.p[B_IF] = w + pp->off_if;
+  b.p[B_RED] = w + pp->off_red;
+  b.p[B_CK] = w + pp->off_ck;
+  if (phase == 1) {
+    P->launches = 0;
+    CUDA_TRY(launch_fill_minpiv(reinterpret_cast<double*>(b.p[B_RED]), st));
+  }
+  if ((rc = run_pass(P, *pp, b, R, dt, dt, st, phase == 1 ? PH_1 : phase == 2 ? PH_2 : PH_3))) return rc;
+  P->report.passes = 1;
+  P->report.n_kernel_launches = P->launches;
+  P->report.min_pivot_ratio = -1.0;
+  return LFDS_OK;
+}
+
 int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes, void* stream) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (P->sharded) return fail(LFDS_EINVAL, "partitioned plan: use lfds_solve_phase with the two exchanges");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
   if (nrhs < 1 || !f_dev || !u_dev || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
   if (((uintptr_t)f_dev | (uintptr_t)u_dev | (uintptr_t)ws) & 15) return fail(LFDS_EINVAL, "pointers must be 16-byte aligned");
@@ -1078,6 +1169,7 @@ void lfds_destroy(lfds_plan* P) {
     cudaFree(kv.second.d_descs);
     cudaFree(kv.second.d_zb);
     cudaFree(kv.second.d_pd);
+    cudaFree(kv.second.d_own);
   }
   if (P->d_tab) cudaFree(P->d_tab);
   for (auto& r : P->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

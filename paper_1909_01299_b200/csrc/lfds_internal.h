@@ -60,6 +60,7 @@ struct GSweep {
   int64_t wxi, wyi;            // W_x[I_a, l] (nifx x nx), W_y[I_b, m] (nify x ny)  (TAB)
   int64_t r1, r2;              // R1[a][r][k][m], R2[b][r][k][l]  (B_IF)
   int64_t what;                // W^[r][k][m][l] output (B_T1)
+  int l_begin, l_end;          // global x-modes swept by this rank (block sharding); all: 0, nx
 };
 
 // Interface residual (step 4).
@@ -73,6 +74,8 @@ struct IfaceRes {
   int64_t xlo, ylo;            // int arrays: first node of each block along the axis
   int nbx, nby;
   int qpad, ppad;              // padded row lengths of the step-3 arrays VX / VY
+  const int* own;              // per block: 1 if this rank computed its v (block sharding)
+  int with_b;                  // 1: add the b = M f term (exactly one rank does)
 };
 
 // Two-sided projection of mode planes (lfds_proj.cu): G[e][p][m] = sum_l Wr[e][l] X[p][m][l],
@@ -94,6 +97,7 @@ cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, i
 // l-chunk of 256 columns at g_off + lc*g_lcs + e*g_es + p*g_ps + m, summed into p1_off.
 struct ProjM {
   int nx, ny, nplanes, E1, E2, nlc, x_buf, pad;
+  int l_begin, l_end;          // columns l in [l_begin, l_end) (block sharding: this rank's x-modes)
   int64_t x_off;
   int64_t wr, wc;              // TAB: Wr[e][l] (row stride nx), Wc[e][m] (row stride ny)
   int64_t g_off, g_lcs, g_es, g_ps;
@@ -108,8 +112,6 @@ cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, 
                         const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_xform(const GemmDesc* d_descs, int ndesc, int maxM, int64_t maxN, bool real_s, bool kcontig,
                          const Bufs& bufs, cudaStream_t st);
-cudaError_t launch_xform_m8(const GemmDesc* d_descs, int ndesc, int64_t maxN, bool kcontig, const Bufs& bufs,
-                            cudaStream_t st);
 bool dst_supported(int n);
 cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, bool kcontig, const Bufs& bufs,
                        cudaStream_t st);

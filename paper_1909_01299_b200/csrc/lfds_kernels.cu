@@ -197,16 +197,22 @@ __global__ void k_iface_res(IfaceRes P, Bufs bufs) {
       const int Pn = ifx[a];                    // 1-based node
       const int64_t fo = (((int64_t)r * nz + k) * ny + q) * nx + (Pn - 1);
       cplx hh = ld(TAB + P.hhx + Pn - 1) * ld(TAB + P.hhy + q) * ld(TAB + P.hhz + k);
-      cplx res = hh * load_f(f, P.dtype, fo);
+      cplx res = P.with_b ? hh * load_f(f, P.dtype, fo) : mk(0, 0);
       const int jb = by[q];
       if (jb >= 0) {
         const int ql = q + 1 - ylo[jb];
         const cplx wgt = ld(TAB + P.hhy + q) * ld(TAB + P.sig + k) * ld(TAB + P.hhz + k);
-        // left block column a, its last row (e=1); right block column a+1, its first row (e=0)
+        // left block column a, its last row (e=1); right block column a+1, its first row (e=0);
+        // with block sharding only the blocks this rank computed contribute
         const int bl = jb * P.nbx + a, br = jb * P.nbx + a + 1;
-        const cplx vl = ld(IF + P.vxo + ((((int64_t)bl * 2 + 1) * R + r) * nz + k) * P.qpad + ql);
-        const cplx vr = ld(IF + P.vxo + ((((int64_t)br * 2 + 0) * R + r) * nz + k) * P.qpad + ql);
-        res = res - (cinv(ld(TAB + P.hx + Pn - 1)) * wgt) * vl - (cinv(ld(TAB + P.hx + Pn)) * wgt) * vr;
+        if (P.own[bl]) {
+          const cplx vl = ld(IF + P.vxo + ((((int64_t)bl * 2 + 1) * R + r) * nz + k) * P.qpad + ql);
+          res = res - (cinv(ld(TAB + P.hx + Pn - 1)) * wgt) * vl;
+        }
+        if (P.own[br]) {
+          const cplx vr = ld(IF + P.vxo + ((((int64_t)br * 2 + 0) * R + r) * nz + k) * P.qpad + ql);
+          res = res - (cinv(ld(TAB + P.hx + Pn)) * wgt) * vr;
+        }
       }
       IF[P.rx + t] = make_double2(res.x, res.y);  // RX[a][r][k][q]
     } else {
@@ -222,13 +228,18 @@ __global__ void k_iface_res(IfaceRes P, Bufs bufs) {
       if (ib >= 0) {  // nodes on x-interfaces are owned by RX
         const int64_t fo = (((int64_t)r * nz + k) * ny + (Qn - 1)) * nx + p;
         cplx hh = ld(TAB + P.hhx + p) * ld(TAB + P.hhy + Qn - 1) * ld(TAB + P.hhz + k);
-        res = hh * load_f(f, P.dtype, fo);
+        if (P.with_b) res = hh * load_f(f, P.dtype, fo);
         const int pl = p + 1 - xlo[ib];
         const cplx wgt = ld(TAB + P.hhx + p) * ld(TAB + P.sig + k) * ld(TAB + P.hhz + k);
         const int bb = b * P.nbx + ib, bt = (b + 1) * P.nbx + ib;
-        const cplx vb = ld(IF + P.vyo + ((((int64_t)bb * 2 + 1) * R + r) * nz + k) * P.ppad + pl);
-        const cplx vt = ld(IF + P.vyo + ((((int64_t)bt * 2 + 0) * R + r) * nz + k) * P.ppad + pl);
-        res = res - (cinv(ld(TAB + P.hy + Qn - 1)) * wgt) * vb - (cinv(ld(TAB + P.hy + Qn)) * wgt) * vt;
+        if (P.own[bb]) {
+          const cplx vb = ld(IF + P.vyo + ((((int64_t)bb * 2 + 1) * R + r) * nz + k) * P.ppad + pl);
+          res = res - (cinv(ld(TAB + P.hy + Qn - 1)) * wgt) * vb;
+        }
+        if (P.own[bt]) {
+          const cplx vt = ld(IF + P.vyo + ((((int64_t)bt * 2 + 0) * R + r) * nz + k) * P.ppad + pl);
+          res = res - (cinv(ld(TAB + P.hy + Qn)) * wgt) * vt;
+        }
       }
       IF[P.ry + u] = make_double2(res.x, res.y);  // RY[b][r][k][p]
     }

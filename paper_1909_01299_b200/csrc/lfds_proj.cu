@@ -226,14 +226,14 @@ __global__ void __launch_bounds__(256) k_projm(ProjM P, Bufs bufs) {
   double2* Wrs = Xs + 2 * 8 * PM_LDX;   // [8*ET][PM_LDX]
   double2* red = Wrs + 8 * ET * PM_LDX; // [NW][ET][8 m][8 e]
   const int lc = blockIdx.x, p = blockIdx.y;
-  const int lb = lc * PM_LC;
+  const int lb = P.l_begin + lc * PM_LC;  // this chunk's first column
   const int NW = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const double2* X = reinterpret_cast<const double2*>(bufs.p[P.x_buf]) + P.x_off + (int64_t)p * P.nx * P.ny;
   double2* IF = reinterpret_cast<double2*>(bufs.p[B_IF]);
   for (int c = threadIdx.x; c < 8 * ET * PM_LDX; c += blockDim.x) {
     const int e = c / PM_LDX, li = c % PM_LDX, l = lb + li;
-    Wrs[c] = (e < P.E1 && li < PM_LC && l < P.nx) ? TAB[P.wr + (int64_t)e * P.nx + l] : make_double2(0, 0);
+    Wrs[c] = (e < P.E1 && li < PM_LC && l < P.l_end) ? TAB[P.wr + (int64_t)e * P.nx + l] : make_double2(0, 0);
   }
   const int ntile = (P.ny + 7) / 8;
   auto stage = [&](int it) {
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) k_projm(ProjM P, Bufs bufs) {
       const int m0 = it * 8;
       for (int c = threadIdx.x; c < 8 * PM_LC; c += blockDim.x) {
         const int r = c / PM_LC, li = c % PM_LC, m = m0 + r, l = lb + li;
-        const bool ok = m < P.ny && l < P.nx;
+        const bool ok = m < P.ny && l < P.l_end;
         cp16p(d + r * PM_LDX + li, ok ? X + (int64_t)m * P.nx + l : X, ok);  // zero-fill outside
       }
     }
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256) k_projm(ProjM P, Bufs bufs) {
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int l = lb + lw + 8 * nt + 2 * q + hh;
-        if (lw + 8 * nt + 2 * q + hh < PM_LC && l < P.nx)
+        if (lw + 8 * nt + 2 * q + hh < PM_LC && l < P.l_end)
           IF[P.h_off + (int64_t)e * P.h_es + (int64_t)p * P.h_ps + l] = h[et][nt].get(hh);
       }
   }
@@ -344,7 +344,9 @@ int projm_chunks(int nx) { return (nx + PM_LC - 1) / PM_LC; }
 cudaError_t launch_projm(const ProjM& P, const Bufs& bufs, cudaStream_t st) {
   if (P.nplanes <= 0 || P.nplanes > 65535) return P.nplanes <= 0 ? cudaSuccess : cudaErrorInvalidValue;
   const int E = P.E1 > P.E2 ? P.E1 : P.E2;
-  const int threads = P.nx >= PM_LC ? PM_LC : ((P.nx + 31) / 32) * 32;
+  const int width = P.l_end - P.l_begin;
+  if (width <= 0) return cudaSuccess;
+  const int threads = width >= PM_LC ? PM_LC : ((width + 31) / 32) * 32;
   const int nw = threads / 32;
   const dim3 grid((unsigned)P.nlc, (unsigned)P.nplanes);
   cudaError_t e;

@@ -373,134 +373,7 @@ cudaError_t launch_3m(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, cons
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- few-row contractions (M <= 8)
-// Step 3 (v on the rows next to the block faces: 2 rows of W) and the step-5 projections
-// (W_x[I_a, l], W_y[I_b, m]: |I| <= 8 rows) contract a whole mode array with at most 8
-// weight rows.  One 8-row DMMA tile, 4 warps across 128 complex data columns; the data
-// stream dominates, so the kernel is HBM-bound by design.
-constexpr int X8_N = 128, X8_K = 16;
-constexpr int LDB8 = X8_N + 2;
-
-template <bool KCONTIG>
-__global__ void __launch_bounds__(XT_THREADS) k_xform_m8(const GemmDesc* __restrict__ descs, Bufs bufs) {
-  extern __shared__ __align__(16) double2 x8sm[];
-  double2 (*As)[X8_K][8 + 2] = reinterpret_cast<double2 (*)[X8_K][8 + 2]>(x8sm);
-  double2 (*Bs)[X8_K][LDB8] = reinterpret_cast<double2 (*)[X8_K][LDB8]>(x8sm + 2 * X8_K * (8 + 2));
-  const GemmDesc& D = descs[blockIdx.z];
-  const int M = D.M, K = D.K;
-  const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
-  const int64_t n0 = (int64_t)blockIdx.x * X8_N;
-  if (n0 >= N) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, q = lane & 3;
-  const double2* A = reinterpret_cast<const double2*>(bufs.p[B_TAB]) + D.a_off;
-  const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off;
-  // B loads: 16 x 128 complex = 2048, 16 per thread, coalesced as in k_xform
-  int64_t bcol[16];
-  int bj, bn0;
-  if (KCONTIG) {  // thread -> j = tid % 16, columns tid/16 + 8e
-    bj = tid & 15;
-    bn0 = tid >> 4;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int64_t n = n0 + bn0 + 8 * e;
-      const int64_t n1 = n / N2, n2 = n - n1 * N2;
-      bcol[e] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
-    }
-  } else {        // thread -> column tid, all 16 rows
-    bj = 0;
-    bn0 = tid;
-    const int64_t n = n0 + bn0;
-    const int64_t n1 = n / N2, n2 = n - n1 * N2;
-    bcol[0] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
-  }
-  auto load_chunk = [&](int st, int j0) {
-    if (tid < 8 * X8_K) {  // A: 8 x 16
-      const int i = tid >> 4, j = tid & 15;
-      const bool ok = i < M && j0 + j < K;
-      cp_async16(&As[st][j][i], ok ? A + (int64_t)i * D.sAi + (int64_t)(j0 + j) * D.sAj : A, ok);
-    }
-    if (KCONTIG) {
-      const int j = j0 + bj;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const bool ok = bcol[e] >= 0 && j < K;
-        cp_async16(&Bs[st][bj][bn0 + 8 * e], ok ? B + bcol[e] + j : B, ok);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int j = j0 + e;
-        const bool ok = bcol[0] >= 0 && j < K;
-        cp_async16(&Bs[st][e][bn0], ok ? B + bcol[0] + (int64_t)j * D.sBj : B, ok);
-      }
-    }
-  };
-  double acc[8][2];  // 4 complex column tiles x (re, im)
-#pragma unroll
-  for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
-  const int wn = warp * 32;
-  const int nchunks = (K + X8_K - 1) / X8_K;
-  load_chunk(0, 0);
-  cp_commit();
-  for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) load_chunk((c + 1) & 1, (c + 1) * X8_K);
-    cp_commit();
-    cp_wait<1>();
-    __syncthreads();
-    const int st = c & 1;
-#pragma unroll
-    for (int kk = 0; kk < X8_K; kk += 4) {
-      const double2 a = As[st][kk + q][g];
-      const double nai = -a.y;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double2 b = Bs[st][kk + q][wn + 8 * j + g];
-        dmma(acc[2 * j][0], acc[2 * j][1], a.x, b.x);
-        dmma(acc[2 * j][0], acc[2 * j][1], nai, b.y);
-        dmma(acc[2 * j + 1][0], acc[2 * j + 1][1], a.x, b.y);
-        dmma(acc[2 * j + 1][0], acc[2 * j + 1][1], a.y, b.x);
-      }
-    }
-    __syncthreads();
-  }
-  cp_wait<0>();
-  double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
-  const int row = g;
-  if (row < M) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t n = n0 + wn + 8 * j + 2 * q + h;
-        if (n < N) {
-          const int64_t n1 = n / N2, n2 = n - n1 * N2;
-          C[(int64_t)row * D.sCi + n1 * D.sC1 + n2 * D.sC2] = make_double2(acc[2 * j][h], acc[2 * j + 1][h]);
-        }
-      }
-    }
-  }
-}
-
 }  // namespace
-
-cudaError_t launch_xform_m8(const GemmDesc* d_descs, int ndesc, int64_t maxN, bool kcontig, const Bufs& bufs,
-                            cudaStream_t st) {
-  if (ndesc <= 0) return cudaSuccess;
-  for (int z0 = 0; z0 < ndesc; z0 += 65535) {
-    const int nzz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
-    dim3 grid((unsigned)((maxN + X8_N - 1) / X8_N), 1, (unsigned)nzz);
-    const size_t sm = (size_t)2 * X8_K * (8 + 2 + LDB8) * sizeof(double2);
-    if (kcontig) {
-      cudaFuncSetAttribute(k_xform_m8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_xform_m8<true><<<grid, XT_THREADS, sm, st>>>(d_descs + z0, bufs);
-    } else {
-      cudaFuncSetAttribute(k_xform_m8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_xform_m8<false><<<grid, XT_THREADS, sm, st>>>(d_descs + z0, bufs);
-    }
-  }
-  return cudaGetLastError();
-}
 
 cudaError_t launch_xform(const GemmDesc* d_descs, int ndesc, int maxM, int64_t maxN, bool real_s, bool kcontig,
                          const Bufs& bufs, cudaStream_t st) {

@@ -482,7 +482,16 @@ __global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks
   extern __shared__ __align__(16) double2 zsm[];
   const ZBlock B = blocks[blockIdx.y];
   Tile t;
-  if (!make_tile<TL>(B, t)) return;
+  {  // tiles cover this rank's global x-modes [l_begin, l_end) (all of them on one GPU)
+    const int tiles_l = (G.l_end - G.l_begin + TL - 1) / TL;
+    const int tl = blockIdx.x % tiles_l, tm = blockIdx.x / tiles_l;
+    t.l0 = G.l_begin + tl * TL;
+    t.m0 = tm * TM;
+    if (t.m0 >= B.ny) return;
+    t.l = t.l0 + (int)(threadIdx.x % TL);
+    t.m = t.m0 + (int)(threadIdx.x / TL);
+    t.active = t.l < G.l_end && t.m < B.ny;
+  }
   const int r = blockIdx.z;
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
@@ -703,7 +712,8 @@ cudaError_t launch_zsolve(int mode, const ZBlock* d_blocks, int nblocks, int max
   GSweep G{};
   if (g) G = *g;
   const int tl = tile_l(mode, max_nx, G.nifx > G.nify ? G.nifx : G.nify);
-  const dim3 grid = zs_grid(nblocks, max_nx, max_ny, R, tl);
+  const dim3 grid = zs_grid(nblocks, mode == 3 ? G.l_end - G.l_begin : max_nx, max_ny, R, tl);
+  if (grid.x == 0) return cudaSuccess;
   if (realz) return tl == 32 ? launch_tl<true, 32>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv)
                              : launch_tl<true, 16>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv);
   return tl == 32 ? launch_tl<false, 32>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv)

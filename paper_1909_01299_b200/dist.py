@@ -1,0 +1,91 @@
+"""Block sharding of the two-level solve over ranks (BASELINE.json north_star: "Work is
+partitioned across the 8 B200s of one box by blocks S^ij, with NCCL over NVLink only for the
+interface exchange").
+
+Blocks S^ij are independent in the two block passes ("for each
+i,j"), so each rank computes a subset, chosen by longest-processing-time-first on a cost model
+(dense complex transform directions cost ~8n flops per element and direction, dense real ~4n,
+sine-transform directions ~O(log n)).  The interface step is one exchange: every rank adds the
+contributions of its own blocks to the residual on the interface planes and the
+residuals are summed over the ranks (exchange 1).  Step 5 is split by global
+x-modes l: each rank sweeps its l-range and the plane projections are summed (exchange 2).
+Both sums are `torch.distributed.all_reduce` on views of the library workspace (NCCL on GPUs);
+`allreduce` can be replaced (tests use an in-process emulation and gloo).
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+
+def block_costs(nx_blocks: Sequence[int], ny_blocks: Sequence[int], kinds_x: Sequence[int],
+                kinds_y: Sequence[int]) -> np.ndarray:
+    """Modelled cost of each block (row-major [j][i]): elements x per-direction transform cost
+    (+ the z-solves and edge work, ~60 units per element)."""
+    def dcost(kind, n):
+        if kind == 0 and (2 * (n + 1)) in (16, 32, 64, 128, 256, 512):
+            return 40.0                                   # sine transform, HBM-bound
+        return (8.0 if kind == 2 else 4.0) * n             # dense DMMA contraction
+    c = np.zeros((len(ny_blocks), len(nx_blocks)))
+    for j, (ny, ky) in enumerate(zip(ny_blocks, kinds_y)):
+        for i, (nx, kx) in enumerate(zip(nx_blocks, kinds_x)):
+            c[j, i] = nx * ny * (dcost(kx, nx) + dcost(ky, ny) + 60.0)
+    return c
+
+
+def lpt_partition(costs: np.ndarray, world: int) -> np.ndarray:
+    """Owner rank of every block: longest processing time first (deterministic tie-break)."""
+    flat = costs.ravel()
+    order = sorted(range(flat.size), key=lambda b: (-flat[b], b))
+    load = [0.0] * world
+    owner = np.zeros(flat.size, dtype=np.int32)
+    for b in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        owner[b] = r
+        load[r] += flat[b]
+    return owner.reshape(costs.shape)
+
+
+def mode_ranges(nx: int, world: int, align: int = 32) -> List[tuple]:
+    """Contiguous global x-mode ranges [l0, l1) per rank, aligned to warp tiles."""
+    units = (nx + align - 1) // align
+    out, start = [], 0
+    for r in range(world):
+        cnt = units // world + (1 if r < units % world else 0)
+        l0 = min(start * align, nx)
+        l1 = min((start + cnt) * align, nx)
+        out.append((l0, l1))
+        start += cnt
+    return out
+
+
+def shard(plan, rank: int, world: int) -> dict:
+    """Configure `plan` for `rank` of `world` (LPT block ownership, step-5 x-mode range)."""
+    info = plan.info()
+    nbx, nby = info["nbx"], info["nby"]
+    bx = [plan.basis(0, i) for i in range(nbx)]
+    by = [plan.basis(1, j) for j in range(nby)]
+    costs = block_costs([b[1].shape[0] for b in bx], [b[1].shape[0] for b in by], [b[2] for b in bx],
+                        [b[2] for b in by])
+    owner = lpt_partition(costs, world)
+    l0, l1 = mode_ranges(info["nx"], world)[rank]
+    plan.set_partition(owner == rank, l0, l1, rank == 0)
+    return {"owner": owner, "l_range": (l0, l1), "costs": costs}
+
+
+def solve_sharded(plan, f, u, ws, allreduce: Optional[Callable] = None, stream=None):
+    """One block-sharded solve: phase 1, sum of exchange 1, phase 2, sum of exchange 2, phase 3.
+    `allreduce(tensor)` sums in place over the ranks (default: torch.distributed.all_reduce)."""
+    if allreduce is None:
+        import torch.distributed as dist
+
+        def allreduce(t):
+            dist.all_reduce(t)
+    nrhs = f.shape[0]
+    plan.solve_phase(1, f, u, ws, stream)
+    allreduce(plan.exchange_view(ws, nrhs, 1))
+    plan.solve_phase(2, f, u, ws, stream)
+    allreduce(plan.exchange_view(ws, nrhs, 2))
+    plan.solve_phase(3, f, u, ws, stream)
+    return u

@@ -67,6 +67,10 @@ _lib.lfds_get_report.argtypes = [_P, ctypes.POINTER(Report)]
 _lib.lfds_get_info.argtypes = [_P, ctypes.POINTER(Info)]
 _lib.lfds_get_basis.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _P, _P]
+_lib.lfds_set_partition.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+_lib.lfds_exchange_layout.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
+                                      ctypes.POINTER(ctypes.c_size_t)]
+_lib.lfds_solve_phase.argtypes = [_P, ctypes.c_int, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
 _lib.lfds_destroy.argtypes = [_P]
 _lib.lfds_stage_count.restype = ctypes.c_int
 _lib.lfds_stage_name.argtypes = [ctypes.c_int]
@@ -78,7 +82,8 @@ _lib.lfds_version.restype = ctypes.c_char_p
 EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
             "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_residual", "lfds_get_report",
             "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version",
-            "lfds_stage_count", "lfds_stage_name", "lfds_stage_times"]
+            "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
+            "lfds_exchange_layout", "lfds_solve_phase"]
 
 
 def _check(rc):
@@ -217,6 +222,31 @@ class Plan:
         _check(_lib.lfds_solve_host(self._h, _P(F.data_ptr()), _P(U.data_ptr()), nrhs, _P(ws.data_ptr()),
                                     ws.numel(), _P(st)))
         return U[0] if single else U
+
+    # ------------------------------------------------------------------ block sharding
+    def set_partition(self, block_owned=None, l_begin: int = 0, l_end: int = -1, rank0: bool = True):
+        """Blocks this rank computes (flags [nby][nbx] or None for all), its global x-modes
+        [l_begin, l_end) of step 5, and whether it adds the b-terms / writes the planes."""
+        if block_owned is None:
+            _check(_lib.lfds_set_partition(self._h, None, 0, 0, 1))
+        else:
+            own = np.ascontiguousarray(np.asarray(block_owned, dtype=np.int32).ravel())
+            _check(_lib.lfds_set_partition(self._h, own.ctypes.data_as(_P), int(l_begin), int(l_end), int(rank0)))
+        self._ws = {}
+
+    def exchange_view(self, ws, nrhs: int, which: int):
+        """float64 view of exchange `which` (1: interface residual, 2: plane projections) in ws."""
+        torch = self._torch()
+        off, n = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(_lib.lfds_exchange_layout(self._h, nrhs, which, ctypes.byref(off), ctypes.byref(n)))
+        return ws[off.value:off.value + 8 * n.value].view(torch.float64)
+
+    def solve_phase(self, phase: int, f, u, ws, stream=None):
+        """One phase (1, 2, 3) of a sharded solve; f, u: (nrhs, nz, ny, nx) device tensors."""
+        torch = self._torch()
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _check(_lib.lfds_solve_phase(self._h, int(phase), _P(f.data_ptr()), _P(u.data_ptr()), f.shape[0],
+                                     _P(ws.data_ptr()), ws.numel(), _P(st)))
 
     def residual(self, u, f=None, dd: bool = True, stream=None):
         """(r, norms): r = M f - A u (complex128), norms[r] = (||r||_2, ||M f||_2)."""
