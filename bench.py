@@ -218,6 +218,8 @@ def stage_algorithmic(p, R: int, plan=None):
         "step5_plane_inverse": (plane, None),
         "step6_zsolve_lift": (None, 32.0 * el_blk),
         "step7_y_sine": ys, "step7_y_dense": yd, "step7_x_sine": xs, "step7_x_dense": xd,
+        # refinement: r = Mf - Au reads u and f and writes r; u += r reads both, writes u
+        "refine_residual": (None, 48.0 * el_all), "refine_axpy": (None, 48.0 * el_all),
     }
 
 
@@ -322,25 +324,33 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         ne = min(nrhs, args.e2e_rhs) if not blocks else nrhs
         fh = f[:ne].cpu().pin_memory()
-        uh = torch.empty_like(fh).pin_memory()
+        uhs = [torch.empty_like(fh).pin_memory() for _ in range(2)]
+        streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
 
-        def step_host():
+        def step_host(i):
             if blocks:  # H2D of f, sharded solve, D2H of u (this rank's part)
                 f.copy_(fh, non_blocking=True)
                 lfds_dist.solve_sharded(plan, f, u, ws, allreduce)
-                uh.copy_(u, non_blocking=True)
+                uhs[0].copy_(u, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             else:
-                plan.solve_host(fh, out=uh)
-        step_host()
+                # consecutive solves alternate between two streams and workspaces: the
+                # host-to-device copy of one overlaps the compute / device-to-host copy of the other
+                plan.solve_host(fh, out=uhs[i % 2], stream=streams[i % 2], sync=False, slot=i % 2)
+        step_host(0)
+        step_host(1)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        k2 = max(1, min(args.steps, 3))
+        k2 = max(2, min(args.steps, 4))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for _ in range(k2):
-            step_host()
+        for s_ in streams:
+            s_.wait_stream(stream)
+        for i in range(k2):
+            step_host(i)
+        for s_ in streams:
+            stream.wait_stream(s_)
         b.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / k2], dtype=torch.float64, device=dev)

@@ -108,6 +108,13 @@ int lfds_solve(lfds_plan* plan, const void* f_dev, void* u_dev, int nrhs,
 size_t lfds_workspace_bytes_host(const lfds_plan* plan, int nrhs);
 int lfds_solve_host(lfds_plan* plan, const void* f_host, void* u_host, int nrhs,
                     void* ws_dev, size_t ws_bytes, void* cuda_stream);
+/*
+ * The same, enqueued only (returns before u_host is written; synchronise the stream).  With
+ * pinned host buffers, separate workspaces and streams, consecutive solves overlap: the
+ * host-to-device copy of one with the compute and device-to-host copy of the other.
+ */
+int lfds_solve_host_async(lfds_plan* plan, const void* f_host, void* u_host, int nrhs,
+                          void* ws_dev, size_t ws_bytes, void* cuda_stream);
 
 /*
  * Residual r = M f - A u (b-units, PAPER.md Eq. (fdmtr)) on the device; f_dev may be NULL

@@ -315,6 +315,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
       int b = j * nbx + i;
       if (!owned(b)) continue;
       ZBlock z{};
+      z.pad_ = (bx.B.kind != 2 && by.B.kind != 2) ? 1 : 0;  // real eigenvalues: real shift s
       z.ms_off = ms[b];
       z.buf = B_MS;
       z.nx = bx.n;
@@ -419,6 +420,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     g.ny = Ny;
     g.lamx = X.lamg;
     g.lamy = Y.lamg;
+    g.pad_ = (X.G.kind != 2 && Y.G.kind != 2) ? 1 : 0;
     g.gL = g.gR = g.gB = g.gT = -1;
     zb.push_back(g);
     pp.max_systems_global = Nx * Ny * R;
@@ -1079,7 +1081,20 @@ int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws,
   return solve_impl(P, f_dev, u_dev, nrhs, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
+static int solve_host_impl(lfds_plan* P, const void* f_host, void* u_host, int nrhs, void* ws, size_t ws_bytes,
+                           void* stream, bool sync);
+
 int lfds_solve_host(lfds_plan* P, const void* f_host, void* u_host, int nrhs, void* ws, size_t ws_bytes, void* stream) {
+  return solve_host_impl(P, f_host, u_host, nrhs, ws, ws_bytes, stream, true);
+}
+
+int lfds_solve_host_async(lfds_plan* P, const void* f_host, void* u_host, int nrhs, void* ws, size_t ws_bytes,
+                          void* stream) {
+  return solve_host_impl(P, f_host, u_host, nrhs, ws, ws_bytes, stream, false);
+}
+
+static int solve_host_impl(lfds_plan* P, const void* f_host, void* u_host, int nrhs, void* ws, size_t ws_bytes,
+                           void* stream, bool sync) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
   if (nrhs < 1 || !f_host || !u_host || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
@@ -1096,7 +1111,7 @@ int lfds_solve_host(lfds_plan* P, const void* f_host, void* u_host, int nrhs, vo
   int rc = solve_impl(P, fd, ud, nrhs, ws, base, st);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(u_host, ud, vol, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  if (sync) CUDA_TRY(cudaStreamSynchronize(st));
   return LFDS_OK;
 }
 

@@ -43,7 +43,7 @@ struct ZTab {
 struct ZBlock {
   int64_t ms_off;              // offset of this block's mode space [r][k][m][l] in B_MS (and T1)
   int nx, ny;                  // interior sizes (modes)
-  int buf, pad_;               // buffer holding the mode space of a mode-1 solve (B_MS, or B_T1 for step 5)
+  int buf, pad_;               // mode-space buffer (B_MS, or B_T1 for step 5); pad_ = 1: real eigenvalues
   int64_t lamx, lamy;          // eigenvalue offsets in TAB
   // pass-2 lifting (reading R8): l~[l,m,k] = -sigma_k (cL Wx[0,l] GL[m,k] + cR Wx[n-1,l] GR[m,k]
   //                                               + cB Wy[0,m] GB[l,k] + cT Wy[n-1,m] GT[l,k])

@@ -92,13 +92,16 @@ struct ZTabS {
   const double* m2;
 };
 
-template <bool REALZ>
+// Row types: RT 0 = complex z table; RT 1 = real z table, complex shift s = lambda_l + mu_m;
+// RT 2 = real z table and real shift (both block bases real: U or R blocks), where c' is real
+// and the elimination costs about half.
+template <int RT>
 __device__ __forceinline__ void zrow(const ZTabS& T, int k, cplx s, cplx& a, cplx& b, cplx& c, double& m2) {
-  if (REALZ) {
+  if (RT >= 1) {
     const double2 ag = T.ag[k], ce = T.ce[k];
     a = mk(ag.x, 0);
     c = mk(ce.x, 0);
-    b = mk(fma(s.x, ce.y, ag.y), s.y * ce.y);
+    b = mk(fma(s.x, ce.y, ag.y), RT == 2 ? 0.0 : s.y * ce.y);
     m2 = T.m2[k];
   } else {
     const double2 a2 = T.sa[k], g2 = T.sg[k], c2 = T.sc[k], e2 = T.se[k];
@@ -111,10 +114,17 @@ __device__ __forceinline__ void zrow(const ZTabS& T, int k, cplx s, cplx& a, cpl
 }
 
 // one forward elimination row; returns |r|^2
-template <bool REALZ>
+template <int RT>
 __device__ __forceinline__ double elim(cplx a, cplx b, cplx c, cplx d, cplx& cp, cplx& dp) {
+  if (RT == 2) {
+    const double r = fma(-a.x, cp.x, b.x);
+    const double in = fast_rcp(r);
+    cp = mk(c.x * in, 0);
+    dp = mk(fma(-a.x, dp.x, d.x) * in, fma(-a.x, dp.y, d.y) * in);
+    return r * r;
+  }
   cplx r, t;
-  if (REALZ) {
+  if (RT == 1) {
     r = mk(fma(-a.x, cp.x, b.x), fma(-a.x, cp.y, b.y));
     t = mk(fma(-a.x, dp.x, d.x), fma(-a.x, dp.y, d.y));
   } else {
@@ -124,19 +134,29 @@ __device__ __forceinline__ double elim(cplx a, cplx b, cplx c, cplx d, cplx& cp,
   const double n2 = fma(r.x, r.x, r.y * r.y);
   const double in = fast_rcp(n2);
   const cplx inv = mk(r.x * in, -r.y * in);
-  cp = REALZ ? mk(c.x * inv.x, c.x * inv.y) : c * inv;
+  cp = RT == 1 ? mk(c.x * inv.x, c.x * inv.y) : c * inv;
   dp = t * inv;
   return n2;
 }
 // c' only (k_zs3 backward recompute)
-template <bool REALZ>
+template <int RT>
 __device__ __forceinline__ void elim_c(cplx a, cplx b, cplx c, cplx& cp) {
+  if (RT == 2) {
+    cp = mk(c.x * fast_rcp(fma(-a.x, cp.x, b.x)), 0);
+    return;
+  }
   cplx r;
-  if (REALZ) r = mk(fma(-a.x, cp.x, b.x), fma(-a.x, cp.y, b.y));
+  if (RT == 1) r = mk(fma(-a.x, cp.x, b.x), fma(-a.x, cp.y, b.y));
   else r = b - a * cp;
   const double in = fast_rcp(fma(r.x, r.x, r.y * r.y));
   const cplx inv = mk(r.x * in, -r.y * in);
-  cp = REALZ ? mk(c.x * inv.x, c.x * inv.y) : c * inv;
+  cp = RT == 1 ? mk(c.x * inv.x, c.x * inv.y) : c * inv;
+}
+// back substitution x_k = d'_k - c'_k x_{k+1}
+template <int RT>
+__device__ __forceinline__ cplx backsub(cplx d, cplx c, cplx x) {
+  if (RT == 2) return mk(fma(-c.x, x.x, d.x), fma(-c.x, x.y, d.y));
+  return d - c * x;
 }
 
 __host__ __device__ __forceinline__ int ztab_slots(int nz, bool realz) {  // in double2 units
@@ -171,7 +191,7 @@ __device__ __forceinline__ ZTabS stage_ztab(ZTab tab, const double2* TAB, int nz
 }
 
 // per-thread ring of ZSEG-row segments of one z-line
-template <int ZSEG, int NSTAGE>
+template <int ZSEG, int NSTAGE, bool FULL = false>
 struct Ring {
   double2* s;  // s[(slot * ZSEG + j) * ZT + tid]
   const double2* line;
@@ -184,7 +204,7 @@ struct Ring {
       const int k0 = seg * ZSEG;
 #pragma unroll
       for (int j = 0; j < ZSEG; ++j)
-        if (k0 + j < nz) cp16(d + j * ZT, line + (int64_t)(k0 + j) * stride);
+        if (FULL || k0 + j < nz) cp16(d + j * ZT, line + (int64_t)(k0 + j) * stride);
     }
     cp_commit();
   }
@@ -224,25 +244,18 @@ __device__ __forceinline__ double2* ck_base(const Bufs& bufs) {
 }
 
 // ===================================================================== step 2
-template <bool REALZ, int TL>
-__global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks, int nz, ZTab tab, Bufs bufs,
-                                               double* minpiv_out) {
+template <int RT, bool FULL, int TL>
+__device__ __forceinline__ void zs1_body(const ZBlock& B, const Tile& t, int nz, const ZTabS& T,
+                                         const double2* TAB, Bufs& bufs, double2* ring_smem, double* minpiv_out) {
   constexpr int ZSEG = 8, NSTAGE = 3;
-  extern __shared__ __align__(16) double2 zsm[];
-  const ZBlock B = blocks[blockIdx.y];
-  Tile t;
-  if (!make_tile<TL>(B, t)) return;  // whole CTA, before any barrier
   const int r = blockIdx.z;
-  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
-  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
   const int64_t nxy = (int64_t)B.nx * B.ny;
   double2* line = reinterpret_cast<double2*>(bufs.p[B.buf]) + B.ms_off + (int64_t)r * nz * nxy +
                   (int64_t)(t.active ? t.m : 0) * B.nx + (t.active ? t.l : 0);
-  const Ring<ZSEG, NSTAGE> ring{zsm + ztab_slots(nz, REALZ), line, nxy, nz, t.active};
+  const Ring<ZSEG, NSTAGE, FULL> ring{ring_smem, line, nxy, nz, t.active};
   const int nseg = (nz + ZSEG - 1) / ZSEG;
   const int64_t nslot = (int64_t)gridDim.x * gridDim.y * gridDim.z * ZT;
   double2* ck = ck_base(bufs);
-  __syncthreads();
   float minpiv = 1.0f;
   const cplx s = t.active ? ld(TAB + B.lamx + t.l) + ld(TAB + B.lamy + t.m) : mk(0, 0);
   cplx cp = mk(0, 0), dp = mk(0, 0);
@@ -258,11 +271,11 @@ __global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks
 #pragma unroll
     for (int j = 0; j < ZSEG; ++j) {
       const int k = k0 + j;
-      if (k < nz) {
+      if (FULL || k < nz) {
         cplx a, b, c;
         double m2;
-        zrow<REALZ>(T, k, s, a, b, c, m2);
-        const double n2 = elim<REALZ>(a, b, c, ring.get(sg, j), cp, dp);
+        zrow<RT>(T, k, s, a, b, c, m2);
+        const double n2 = elim<RT>(a, b, c, ring.get(sg, j), cp, dp);
         minpiv = fminf(minpiv, __fdividef((float)n2, (float)fma(b.x, b.x, fma(b.y, b.y, m2))));
       }
     }
@@ -286,26 +299,42 @@ __global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks
     for (int j = 0; j < ZSEG; ++j) {
       const int k = k0 + j;
       rb[j] = mk(0, 0);
-      if (k < nz) {
+      if (FULL || k < nz) {
         cplx a, b, c;
         double m2;
-        zrow<REALZ>(T, k, s, a, b, c, m2);
-        elim<REALZ>(a, b, c, ring.get(sg, j), cc, dd);
+        zrow<RT>(T, k, s, a, b, c, m2);
+        elim<RT>(a, b, c, ring.get(sg, j), cc, dd);
         rb[j] = dd;
       }
       cs[j] = cc;
     }
+    double2* lp = line + (int64_t)k0 * nxy;
 #pragma unroll
     for (int j = ZSEG - 1; j >= 0; --j) {
-      const int k = k0 + j;
-      if (k < nz) {
-        x = rb[j] - cs[j] * x;
-        line[(int64_t)k * nxy] = make_double2(x.x, x.y);
+      if (FULL || k0 + j < nz) {
+        x = backsub<RT>(rb[j], cs[j], x);
+        lp[j * nxy] = make_double2(x.x, x.y);
       }
     }
   }
   cp_wait<0>();
   commit_minpiv(minpiv, minpiv_out);
+}
+
+template <bool REALZ, int TL, bool FULL>
+__global__ void __launch_bounds__(ZT, 2) k_zs1(const ZBlock* __restrict__ blocks, int nz, ZTab tab, Bufs bufs,
+                                               double* minpiv_out) {
+  extern __shared__ __align__(16) double2 zsm[];
+  const ZBlock B = blocks[blockIdx.y];
+  Tile t;
+  if (!make_tile<TL>(B, t)) return;  // whole CTA, before any barrier
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
+  __syncthreads();
+  double2* ring = zsm + ztab_slots(nz, REALZ);
+  if (!REALZ) zs1_body<0, FULL, TL>(B, t, nz, T, TAB, bufs, ring, minpiv_out);
+  else if (B.pad_) zs1_body<2, FULL, TL>(B, t, nz, T, TAB, bufs, ring, minpiv_out);  // real shift
+  else zs1_body<1, FULL, TL>(B, t, nz, T, TAB, bufs, ring, minpiv_out);
 }
 
 // ===================================================================== step 6
@@ -321,24 +350,17 @@ struct FaceStage {
   static constexpr int SLOTS = GR + ZSEG * TM;  // double2 per stage
 };
 
-template <bool REALZ, int TL>
-__global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks, int nz, ZTab tab, int64_t sig_off,
-                                               Bufs bufs, double* minpiv_out) {
+template <int RT, bool FULL, int TL>
+__device__ __forceinline__ void zs2_body(const ZBlock& B, const Tile& t, int nz, const ZTabS& T, const double2* TAB,
+                                         Bufs& bufs, double2* fsm) {
   constexpr int ZSEG = 8, NSTAGE = 2, TM = ZT / TL;
   using FS = FaceStage<TL, ZSEG>;
-  extern __shared__ __align__(16) double2 zsm[];
-  const ZBlock B = blocks[blockIdx.y];
-  Tile t;
-  if (!make_tile<TL>(B, t)) return;
   const int r = blockIdx.z;
-  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
-  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
-  double2* fsm = zsm + ztab_slots(nz, REALZ);  // [2][FS::SLOTS]
   const int64_t nxy = (int64_t)B.nx * B.ny;
   double2* line = reinterpret_cast<double2*>(bufs.p[B_MS]) + B.ms_off + (int64_t)r * nz * nxy +
                   (int64_t)(t.active ? t.m : 0) * B.nx + (t.active ? t.l : 0);
-  const Ring<ZSEG, NSTAGE> ring{fsm + 2 * FS::SLOTS, line, nxy, nz, t.active};
+  const Ring<ZSEG, NSTAGE, FULL> ring{fsm + 2 * FS::SLOTS, line, nxy, nz, t.active};
   const int nseg = (nz + ZSEG - 1) / ZSEG;
   const int64_t nslot = (int64_t)gridDim.x * gridDim.y * gridDim.z * ZT;
   double2* ck = ck_base(bufs);
@@ -357,11 +379,11 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
         const double2* src = nullptr;
         if (c < FS::GL) {  // GB / GT rows, TL entries each
           const int f = c / (ZSEG * TL), j = (c / TL) % ZSEG, li = c % TL, k = k0 + j;
-          if (k < nz && t.l0 + li < B.nx && (f ? hT : hB)) src = IF + (f ? B.gT : B.gB) + ro + k * fs + t.l0 + li;
+          if ((FULL || k < nz) && t.l0 + li < B.nx && (f ? hT : hB)) src = IF + (f ? B.gT : B.gB) + ro + k * fs + t.l0 + li;
         } else {  // GL / GR rows, TM entries each
           const int c2 = c - FS::GL;
           const int f = c2 / (ZSEG * TM), j = (c2 / TM) % ZSEG, mi = c2 % TM, k = k0 + j;
-          if (k < nz && t.m0 + mi < B.ny && (f ? hR : hL)) src = IF + (f ? B.gR : B.gL) + ro + k * fs + t.m0 + mi;
+          if ((FULL || k < nz) && t.m0 + mi < B.ny && (f ? hR : hL)) src = IF + (f ? B.gR : B.gL) + ro + k * fs + t.m0 + mi;
         }
         if (src) cp16(d + c, src);
       }
@@ -384,7 +406,6 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
     if (hT) acc = cfma(cT, mk(d[FS::GT + j * TL + tx]), acc);
     return acc;
   };
-  __syncthreads();  // z tables
   const cplx s = t.active ? ld(TAB + B.lamx + t.l) + ld(TAB + B.lamy + t.m) : mk(0, 0);
   // ---- forward sweep
   cplx cp = mk(0, 0), dp = mk(0, 0);
@@ -400,11 +421,11 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
 #pragma unroll
       for (int j = 0; j < ZSEG; ++j) {
         const int k = k0 + j;
-        if (k < nz) {
+        if (FULL || k < nz) {
           cplx a, b, c;
           double m2;
-          zrow<REALZ>(T, k, s, a, b, c, m2);
-          elim<REALZ>(a, b, c, lift(sg, j), cp, dp);  // same T_lm as step 2: pivots monitored there
+          zrow<RT>(T, k, s, a, b, c, m2);
+          elim<RT>(a, b, c, lift(sg, j), cp, dp);  // same T_lm as step 2: pivots monitored there
         }
       }
     }
@@ -433,28 +454,44 @@ __global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks
       for (int j = 0; j < ZSEG; ++j) {
         const int k = k0 + j;
         rb[j] = mk(0, 0);
-        if (k < nz) {
+        if (FULL || k < nz) {
           cplx a, b, c;
           double m2;
-          zrow<REALZ>(T, k, s, a, b, c, m2);
-          elim<REALZ>(a, b, c, lift(sg, j), cc, dd);
+          zrow<RT>(T, k, s, a, b, c, m2);
+          elim<RT>(a, b, c, lift(sg, j), cc, dd);
           rb[j] = dd;
         }
         cs[j] = cc;
       }
+      double2* lp = line + (int64_t)k0 * nxy;
 #pragma unroll
       for (int j = ZSEG - 1; j >= 0; --j) {
-        const int k = k0 + j;
-        if (k < nz) {
-          x = rb[j] - cs[j] * x;
+        if (FULL || k0 + j < nz) {
+          x = backsub<RT>(rb[j], cs[j], x);
           const cplx o = ring.get(sg, j);
-          line[(int64_t)k * nxy] = make_double2(o.x + x.x, o.y + x.y);
+          lp[j * nxy] = make_double2(o.x + x.x, o.y + x.y);
         }
       }
     }
     __syncthreads();
   }
   cp_wait<0>();
+}
+
+
+template <bool REALZ, int TL, bool FULL>
+__global__ void __launch_bounds__(ZT, 2) k_zs2(const ZBlock* __restrict__ blocks, int nz, ZTab tab, Bufs bufs) {
+  extern __shared__ __align__(16) double2 zsm[];
+  const ZBlock B = blocks[blockIdx.y];
+  Tile t;
+  if (!make_tile<TL>(B, t)) return;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
+  __syncthreads();
+  double2* fsm = zsm + ztab_slots(nz, REALZ);  // [2][FaceStage::SLOTS], then the ring
+  if (!REALZ) zs2_body<0, FULL, TL>(B, t, nz, T, TAB, bufs, fsm);
+  else if (B.pad_) zs2_body<2, FULL, TL>(B, t, nz, T, TAB, bufs, fsm);
+  else zs2_body<1, FULL, TL>(B, t, nz, T, TAB, bufs, fsm);
 }
 
 // ===================================================================== step 5
@@ -474,13 +511,12 @@ struct RankStage {
   static constexpr int SLOTS = FWD > BWD ? FWD : BWD;
 };
 
-template <bool REALZ, int TL, int NIF>
-__global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks, int nz, ZTab tab, GSweep G,
-                                               Bufs bufs, double* minpiv_out) {
+template <int RT, bool FULL, int TL, int NIF>
+__device__ __forceinline__ void zs3_body(const ZBlock& B, int nz, const ZTabS& T, const GSweep& G, Bufs& bufs,
+                                         double2* wsm, double* minpiv_out) {
   using RS = RankStage<TL, NIF>;
   constexpr int ZSEG = RS::ZSEG, TM = RS::TM, KA = RS::KA, NSTAGE = 3;
-  extern __shared__ __align__(16) double2 zsm[];
-  const ZBlock B = blocks[blockIdx.y];
+  constexpr int CKG = 2;  // c' checkpoints every CKG segments (8 rows): c' needs no right side
   Tile t;
   {  // tiles cover this rank's global x-modes [l_begin, l_end) (all of them on one GPU)
     const int tiles_l = (G.l_end - G.l_begin + TL - 1) / TL;
@@ -495,8 +531,7 @@ __global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks
   const int r = blockIdx.z;
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
-  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
-  double2* wsm = zsm + ztab_slots(nz, REALZ);  // union: forward staging / backward ring
+  // wsm: union of the forward staging and the backward ring
   double2* R1s = wsm;                           // [2][ZSEG][KA][TM]
   double2* R2s = wsm + 2 * RS::R1S;             // [2][ZSEG][KA][TL]
   double2* RH = wsm + 2 * RS::STAGE;            // [ZSEG][TM][TL+1] (padded: conflict-free)
@@ -532,12 +567,12 @@ __global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks
       for (int c = threadIdx.x; c < RS::STAGE; c += ZT) {
         if (c < RS::R1S) {  // R1[a][r*nz + k][m]
           const int j = c / (KA * TM), a = (c / TM) % KA, mm = t.m0 + c % TM, k = k0 + j;
-          if (a < G.nifx && mm < G.ny && k < nz)
+          if (a < G.nifx && mm < G.ny && (FULL || k < nz))
             cp16(d1 + c, IF + G.r1 + ((int64_t)a * RZ + (int64_t)r * nz + k) * G.ny + mm);
         } else {  // R2[b][r*nz + k][l]
           const int c2 = c - RS::R1S;
           const int j = c2 / (KA * TL), b = (c2 / TL) % KA, ll = t.l0 + c2 % TL, k = k0 + j;
-          if (b < G.nify && ll < G.nx && k < nz)
+          if (b < G.nify && ll < G.nx && (FULL || k < nz))
             cp16(d2 + c2, IF + G.r2 + ((int64_t)b * RZ + (int64_t)r * nz + k) * G.nx + ll);
         }
       }
@@ -589,15 +624,15 @@ __global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks
     rhs_tile(sg);
     __syncthreads();  // RHS tile complete; staging slot sg&1 free for segment sg+2
     if (t.active) {
-      ck[(int64_t)sg * nslot] = make_double2(cp.x, cp.y);
+      if (sg % CKG == 0) ck[(int64_t)(sg / CKG) * nslot] = make_double2(cp.x, cp.y);
 #pragma unroll
       for (int j = 0; j < ZSEG; ++j) {
         const int k = k0 + j;
-        if (k < nz) {
+        if (FULL || k < nz) {
           cplx a, b, c;
           double m2;
-          zrow<REALZ>(T, k, s, a, b, c, m2);
-          const double n2 = elim<REALZ>(a, b, c, mk(RH[(j * TM + ty) * (TL + 1) + tx]), cp, dp);
+          zrow<RT>(T, k, s, a, b, c, m2);
+          const double n2 = elim<RT>(a, b, c, mk(RH[(j * TM + ty) * (TL + 1) + tx]), cp, dp);
           minpiv = fminf(minpiv, __fdividef((float)n2, (float)fma(b.x, b.x, fma(b.y, b.y, m2))));
           line[(int64_t)k * nxy] = make_double2(dp.x, dp.y);  // d'
         }
@@ -608,41 +643,64 @@ __global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks
   cp_wait<0>();
   __threadfence_block();  // own d' stores precede the cp.async re-reads
   __syncthreads();        // the forward staging area becomes the backward ring
-  const Ring<ZSEG, NSTAGE> ring{wsm, line, nxy, nz, t.active};
+  const Ring<ZSEG, NSTAGE, FULL> ring{wsm, line, nxy, nz, t.active};
 #pragma unroll
   for (int qq = 0; qq < NSTAGE - 1; ++qq) ring.issue(nseg - 1 - qq);
   cplx x = mk(0, 0);
-  double2 nc = ck[(int64_t)(nseg - 1) * nslot];
-  for (int sg = nseg - 1; sg >= 0; --sg) {
-    const int k0 = sg * ZSEG;
-    ring.issue(sg - (NSTAGE - 1));
-    cp_wait<NSTAGE - 1>();
-    if (!t.active) continue;
-    cplx cs[ZSEG];
+  const int ngrp = (nseg + CKG - 1) / CKG;
+  double2 nc = ck[(int64_t)(ngrp - 1) * nslot];
+  for (int gi = ngrp - 1; gi >= 0; --gi) {
+    // c' of the group's rows recomputed from its checkpoint (no right side needed)
+    cplx cs[CKG * ZSEG];
     cplx cc = mk(nc);
-    if (sg > 0) nc = ck[(int64_t)(sg - 1) * nslot];
+    if (gi > 0) nc = ck[(int64_t)(gi - 1) * nslot];
+    if (t.active) {
 #pragma unroll
-    for (int j = 0; j < ZSEG; ++j) {
-      const int k = k0 + j;
-      if (k < nz) {
-        cplx a, b, c;
-        double m2;
-        zrow<REALZ>(T, k, s, a, b, c, m2);
-        elim_c<REALZ>(a, b, c, cc);
+      for (int j = 0; j < CKG * ZSEG; ++j) {
+        const int k = gi * CKG * ZSEG + j;
+        if (FULL || k < nz) {
+          cplx a, b, c;
+          double m2;
+          zrow<RT>(T, k, s, a, b, c, m2);
+          elim_c<RT>(a, b, c, cc);
+        }
+        cs[j] = cc;
       }
-      cs[j] = cc;
     }
 #pragma unroll
-    for (int j = ZSEG - 1; j >= 0; --j) {
-      const int k = k0 + j;
-      if (k < nz) {
-        x = ring.get(sg, j) - cs[j] * x;
-        line[(int64_t)k * nxy] = make_double2(x.x, x.y);
+    for (int q = CKG - 1; q >= 0; --q) {
+      const int sg = gi * CKG + q;
+      if (sg >= nseg) continue;  // uniform: the last group may be short
+      const int k0 = sg * ZSEG;
+      ring.issue(sg - (NSTAGE - 1));
+      cp_wait<NSTAGE - 1>();
+      if (!t.active) continue;
+      double2* lp = line + (int64_t)k0 * nxy;
+#pragma unroll
+      for (int j = ZSEG - 1; j >= 0; --j) {
+        if (FULL || k0 + j < nz) {
+          x = backsub<RT>(ring.get(sg, j), cs[q * ZSEG + j], x);
+          lp[j * nxy] = make_double2(x.x, x.y);
+        }
       }
     }
   }
   cp_wait<0>();
   commit_minpiv(minpiv, minpiv_out);
+}
+
+
+template <bool REALZ, int TL, int NIF, bool FULL>
+__global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks, int nz, ZTab tab, GSweep G,
+                                               Bufs bufs, double* minpiv_out) {
+  extern __shared__ __align__(16) double2 zsm[];
+  const ZBlock B = blocks[blockIdx.y];
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);  // barrier inside the body
+  double2* wsm = zsm + ztab_slots(nz, REALZ);
+  if (!REALZ) zs3_body<0, FULL, TL, NIF>(B, nz, T, G, bufs, wsm, minpiv_out);
+  else if (B.pad_) zs3_body<2, FULL, TL, NIF>(B, nz, T, G, bufs, wsm, minpiv_out);
+  else zs3_body<1, FULL, TL, NIF>(B, nz, T, G, bufs, wsm, minpiv_out);
 }
 
 // ===================================================================== launch
@@ -662,26 +720,26 @@ cudaError_t prep(K kern, size_t sm) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
 }
 
-template <bool REALZ, int TL>
-cudaError_t launch_tl(int mode, dim3 grid, cudaStream_t st, const ZBlock* b, int nz, ZTab tab, int64_t sig,
-                      const GSweep& g, const Bufs& bufs, double* mp) {
+template <bool REALZ, int TL, bool FULL>
+cudaError_t launch_tl(int mode, dim3 grid, cudaStream_t st, const ZBlock* b, int nz, ZTab tab, const GSweep& g,
+                      const Bufs& bufs, double* mp) {
   const size_t zt = (size_t)ztab_slots(nz, REALZ) * sizeof(double2);
   cudaError_t e;
   if (mode == 1) {
     const size_t sm = zt + (size_t)3 * 8 * ZT * sizeof(double2);
-    if ((e = prep(k_zs1<REALZ, TL>, sm)) != cudaSuccess) return e;
-    k_zs1<REALZ, TL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs, mp);
+    if ((e = prep(k_zs1<REALZ, TL, FULL>, sm)) != cudaSuccess) return e;
+    k_zs1<REALZ, TL, FULL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs, mp);
   } else if (mode == 2) {
     const size_t sm = zt + (size_t)(2 * FaceStage<TL, 8>::SLOTS + 2 * 8 * ZT) * sizeof(double2);
-    if ((e = prep(k_zs2<REALZ, TL>, sm)) != cudaSuccess) return e;
-    k_zs2<REALZ, TL><<<grid, ZT, sm, st>>>(b, nz, tab, sig, bufs, mp);
+    if ((e = prep(k_zs2<REALZ, TL, FULL>, sm)) != cudaSuccess) return e;
+    k_zs2<REALZ, TL, FULL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs);
   } else {
     const int nif = g.nifx > g.nify ? g.nifx : g.nify;
-#define Z3(N)                                                                 \
-  {                                                                           \
-    const size_t sm = zt + (size_t)RankStage<TL, N>::SLOTS * sizeof(double2); \
-    if ((e = prep(k_zs3<REALZ, TL, N>, sm)) != cudaSuccess) return e;         \
-    k_zs3<REALZ, TL, N><<<grid, ZT, sm, st>>>(b, nz, tab, g, bufs, mp);       \
+#define Z3(N)                                                                     \
+  {                                                                               \
+    const size_t sm = zt + (size_t)RankStage<TL, N>::SLOTS * sizeof(double2);     \
+    if ((e = prep(k_zs3<REALZ, TL, N, FULL>, sm)) != cudaSuccess) return e;       \
+    k_zs3<REALZ, TL, N, FULL><<<grid, ZT, sm, st>>>(b, nz, tab, g, bufs, mp);     \
   }
     if (nif <= 4) Z3(4)
     else if (nif <= 8) Z3(8)
@@ -690,6 +748,15 @@ cudaError_t launch_tl(int mode, dim3 grid, cudaStream_t st, const ZBlock* b, int
 #undef Z3
   }
   return cudaGetLastError();
+}
+
+template <bool REALZ, int TL>
+cudaError_t launch_full(int mode, dim3 grid, cudaStream_t st, const ZBlock* b, int nz, ZTab tab, const GSweep& g,
+                        const Bufs& bufs, double* mp) {
+  // no ragged tail: 8-row segments (steps 2, 6) and 8-row checkpoint groups (step 5)
+  const bool full = nz % 8 == 0;
+  return full ? launch_tl<REALZ, TL, true>(mode, grid, st, b, nz, tab, g, bufs, mp)
+              : launch_tl<REALZ, TL, false>(mode, grid, st, b, nz, tab, g, bufs, mp);
 }
 
 }  // namespace
@@ -714,10 +781,11 @@ cudaError_t launch_zsolve(int mode, const ZBlock* d_blocks, int nblocks, int max
   const int tl = tile_l(mode, max_nx, G.nifx > G.nify ? G.nifx : G.nify);
   const dim3 grid = zs_grid(nblocks, mode == 3 ? G.l_end - G.l_begin : max_nx, max_ny, R, tl);
   if (grid.x == 0) return cudaSuccess;
-  if (realz) return tl == 32 ? launch_tl<true, 32>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv)
-                             : launch_tl<true, 16>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv);
-  return tl == 32 ? launch_tl<false, 32>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv)
-                  : launch_tl<false, 16>(mode, grid, st, d_blocks, nz, tab, sig_off, G, bufs, d_minpiv);
+  (void)sig_off;
+  if (realz) return tl == 32 ? launch_full<true, 32>(mode, grid, st, d_blocks, nz, tab, G, bufs, d_minpiv)
+                             : launch_full<true, 16>(mode, grid, st, d_blocks, nz, tab, G, bufs, d_minpiv);
+  return tl == 32 ? launch_full<false, 32>(mode, grid, st, d_blocks, nz, tab, G, bufs, d_minpiv)
+                  : launch_full<false, 16>(mode, grid, st, d_blocks, nz, tab, G, bufs, d_minpiv);
 }
 
 }  // namespace lfds

@@ -62,6 +62,7 @@ _lib.lfds_workspace_bytes_host.argtypes = [_P, ctypes.c_int]
 _lib.lfds_workspace_bytes_host.restype = ctypes.c_size_t
 _lib.lfds_solve.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
 _lib.lfds_solve_host.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
+_lib.lfds_solve_host_async.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
 _lib.lfds_residual.argtypes = [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P]
 _lib.lfds_get_report.argtypes = [_P, ctypes.POINTER(Report)]
 _lib.lfds_get_info.argtypes = [_P, ctypes.POINTER(Info)]
@@ -80,7 +81,7 @@ _lib.lfds_last_error.restype = ctypes.c_char_p
 _lib.lfds_version.restype = ctypes.c_char_p
 
 EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
-            "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_residual", "lfds_get_report",
+            "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_get_report",
             "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version",
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
             "lfds_exchange_layout", "lfds_solve_phase"]
@@ -175,9 +176,10 @@ class Plan:
         import torch
         return torch
 
-    def workspace(self, nrhs: int, host: bool = False):
+    def workspace(self, nrhs: int, host: bool = False, slot: int = 0):
+        """Cached device workspace (slot: independent workspaces for concurrent solves)."""
         torch = self._torch()
-        key = (nrhs, host)
+        key = (nrhs, host, slot)
         nb = self.workspace_bytes_host(nrhs) if host else self.workspace_bytes(nrhs)
         if nb == 0:
             raise LfdsError(5, _lib.lfds_last_error().decode() or "workspace query failed")
@@ -208,8 +210,9 @@ class Plan:
                                ws.numel(), _P(st)))
         return U[0] if single else U
 
-    def solve_host(self, f_host, out=None, stream=None):
-        """End-to-end: host f (pinned CPU tensor) -> device -> solve -> host u."""
+    def solve_host(self, f_host, out=None, stream=None, sync: bool = True, slot: int = 0):
+        """End-to-end: host f (pinned CPU tensor) -> device -> solve -> host u.  sync=False
+        only enqueues (lfds_solve_host_async); concurrent solves need distinct `slot`s."""
         torch = self._torch()
         single = f_host.dim() == 3
         F = f_host.unsqueeze(0) if single else f_host
@@ -217,10 +220,10 @@ class Plan:
             raise ValueError("f_host must be a contiguous CPU tensor of the plan dtype")
         nrhs = F.shape[0]
         U = torch.empty_like(F, pin_memory=F.is_pinned()) if out is None else (out.unsqueeze(0) if single else out)
-        ws = self.workspace(nrhs, host=True)
+        ws = self.workspace(nrhs, host=True, slot=slot)
         st = (stream or torch.cuda.current_stream()).cuda_stream
-        _check(_lib.lfds_solve_host(self._h, _P(F.data_ptr()), _P(U.data_ptr()), nrhs, _P(ws.data_ptr()),
-                                    ws.numel(), _P(st)))
+        fn = _lib.lfds_solve_host if sync else _lib.lfds_solve_host_async
+        _check(fn(self._h, _P(F.data_ptr()), _P(U.data_ptr()), nrhs, _P(ws.data_ptr()), ws.numel(), _P(st)))
         return U[0] if single else U
 
     # ------------------------------------------------------------------ block sharding
