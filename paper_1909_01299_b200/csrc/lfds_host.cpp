@@ -102,7 +102,7 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   int nzb = 0;               // owned blocks (entries of d_zb before the global one)
   int* d_own = nullptr;      // per-block ownership flags (step-4 partial residual)
   int n_pd3 = 0;
-  StageDescs s1x, s1y, s3x, s3y, s5r1, s5r2, s5wx, s5wy, s6f, s7y, s7x;
+  StageDescs s1x, s1y, s3x, s3y, s5r1, s5wx, s6f, s7y, s7x;  // s5r1: R1 and R2; s5wx: WX and WY
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
   std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
   bool use_xform = false;
@@ -297,16 +297,15 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     }
   stage(pp.s3y, std::move(v)); v.clear();
   // step 5: R1[a][rk][m] = sum_q W_y[q][m] RX[a][rk][q];  R2[b][rk][l] = sum_p W_x[p][l] RY[b][rk][p]  (b-units)
+  // (both in one launch: the two contractions are independent)
   if (nifx) v.push_back(gd(Y.Wg, 1, Ny, Ny, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
-  stage(pp.s5r1, std::move(v)); v.clear();
   if (nify) v.push_back(gd(X.Wg, 1, Nx, Nx, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2, 1, Nx, 0, (int)(nify * RZ), 1, 0));
-  stage(pp.s5r2, std::move(v)); v.clear();
+  stage(pp.s5r1, std::move(v)); v.clear();
   // P1, P2 (projections of w^ onto the planes): k_projm, see run_pass
   // w on the planes: WX[a][rk][q] = sum_m W_y[q][m] P1[a][rk][m];  WY[b][rk][p] = sum_l W_x[p][l] P2[b][rk][l]
   if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, 1, Ny, 0, B_IF, pp.wx, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
-  stage(pp.s5wx, std::move(v)); v.clear();
   if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, 1, Nx, 0, B_IF, pp.wy, 1, Nx, 0, (int)(nify * RZ), 1, 0));
-  stage(pp.s5wy, std::move(v)); v.clear();
+  stage(pp.s5wx, std::move(v)); v.clear();
   // step 6: face transforms GF[b][face][rk][mode] (faces L, R, B, T), e.g. GL = F_y w_L
   std::vector<ZBlock> zb;  // owned blocks (k_zs1, k_zs2), then the global 'block' (k_zs3)
   for (int j = 0; j < nby; ++j)
@@ -565,8 +564,17 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     CUDA_TRY(launch_proj(pp.d_pd, pp.n_pd3, P->lpad, 2, R * Nz, st, bufs));
     P->launches++;
     end(); begin(ST_EDGE);
-    if ((rc = gemm(pp.s3x))) return rc;
-    if ((rc = gemm(pp.s3y))) return rc;
+    // node values next to the faces: VX = W_y G, VY = W_x H (DMMA, complex path)
+    if (pp.use_xform) {
+      for (const StageDescs* s3 : {&pp.s3x, &pp.s3y})
+        if (s3->n) {
+          CUDA_TRY(launch_xform(pp.d_descs + s3->off, s3->n, s3->maxM, s3->maxN, false, true, bufs, st));
+          P->launches += (s3->n + 65534) / 65535;
+        }
+    } else {
+      if ((rc = gemm(pp.s3x))) return rc;
+      if ((rc = gemm(pp.s3y))) return rc;
+    }
     end(); begin(ST_IFRES);
     // step 4
     IfaceRes ir{};
@@ -585,7 +593,6 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   if ((phases & PH_2) && has_if) {
     // step 5
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
-    if ((rc = xform(pp.s5r2, StageDescs{}, pp.s5r2, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     begin(ST_GSWEEP);
     GSweep g{};
     g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
@@ -620,10 +627,14 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   if (phases & PH_3) {
   if (has_if) {
     if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
-    if ((rc = xform(pp.s5wy, StageDescs{}, pp.s5wy, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
     begin(ST_FACE);
-    // step 6
-    if ((rc = gemm(pp.s6f))) return rc;
+    // step 6: face transforms (DMMA, complex path)
+    if (pp.use_xform && pp.s6f.n) {
+      CUDA_TRY(launch_xform(pp.d_descs + pp.s6f.off, pp.s6f.n, pp.s6f.maxM, pp.s6f.maxN, false, true, bufs, st));
+      P->launches += (pp.s6f.n + 65534) / 65535;
+    } else if ((rc = gemm(pp.s6f))) {
+      return rc;
+    }
     end(); begin(ST_Z2);
     if (pp.nzb) {
       CUDA_TRY(launch_zsolve(2, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_lift, P->t_sig, nullptr, bufs, minpiv,

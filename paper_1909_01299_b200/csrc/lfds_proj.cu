@@ -152,6 +152,92 @@ __global__ void __launch_bounds__(512) k_proj(const PDesc* __restrict__ descs, B
         if (e < E2) IF[D.h_off + (int64_t)e * D.h_es + (int64_t)p * D.h_ps + lj[j]] = h[j][e];
 }
 
+// Row-per-warp variant for narrow planes (block planes, nx <= 32*LPW): warp w streams rows
+// m = w, w + NW, ... and each lane holds LPW columns, so a row sum of G is complete inside
+// the warp (reduce-scatter) and the CTA needs no barrier in its row loop; H (column sums)
+// accumulates per warp and is combined once per plane through shared memory, in warp order.
+template <int E, int LPW>
+__global__ void __launch_bounds__(128) k_proj_rows(const PDesc* __restrict__ descs, Bufs bufs) {
+  constexpr int N = 2 * E, NW = 4;
+  __shared__ double2 hs[NW][E][32 * LPW];
+  const PDesc& D = descs[blockIdx.y];
+  const int p = blockIdx.x;
+  if (p >= D.nplanes) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nx = D.nx, ny = D.ny, E1 = D.E1, E2 = D.E2;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const double2* X = reinterpret_cast<const double2*>(bufs.p[D.x_buf]) + D.x_off + (int64_t)p * D.ps;
+  double2* IF = reinterpret_cast<double2*>(bufs.p[B_IF]);
+  double2 wr[LPW][E], h[LPW][E];
+#pragma unroll
+  for (int j = 0; j < LPW; ++j) {
+    const int l = lane + 32 * j;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      wr[j][e] = (l < nx && e < E1) ? __ldg(TAB + D.wr + (int64_t)e * D.wr_es + l) : make_double2(0, 0);
+      h[j][e] = make_double2(0, 0);
+    }
+  }
+  double2 xc[LPW], xn[LPW];
+  auto load = [&](double2 (&xb)[LPW], int m) {
+#pragma unroll
+    for (int j = 0; j < LPW; ++j) {
+      const int l = lane + 32 * j;
+      xb[j] = (m < ny && l < nx) ? __ldg(X + (int64_t)m * nx + l) : make_double2(0, 0);
+    }
+  };
+  load(xn, warp);
+  for (int m = warp; m < ny; m += NW) {
+#pragma unroll
+    for (int j = 0; j < LPW; ++j) xc[j] = xn[j];
+    load(xn, m + NW);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e < E2) {
+        const double2 w = __ldg(TAB + D.wc + (int64_t)e * D.wc_es + m);
+#pragma unroll
+        for (int j = 0; j < LPW; ++j) {
+          h[j][e].x = fma(w.x, xc[j].x, fma(-w.y, xc[j].y, h[j][e].x));
+          h[j][e].y = fma(w.x, xc[j].y, fma(w.y, xc[j].x, h[j][e].y));
+        }
+      }
+    }
+    double g[N];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      double gx = 0, gy = 0;
+#pragma unroll
+      for (int j = 0; j < LPW; ++j) {
+        gx = fma(wr[j][e].x, xc[j].x, fma(-wr[j][e].y, xc[j].y, gx));
+        gy = fma(wr[j][e].x, xc[j].y, fma(wr[j][e].y, xc[j].x, gy));
+      }
+      g[2 * e] = gx;
+      g[2 * e + 1] = gy;
+    }
+    int idx;
+    const double s = reduce_scatter<N>(g, idx);
+    if (((lane & (32 / N - 1)) == 0 || N >= 32) && (idx >> 1) < E1)
+      reinterpret_cast<double*>(IF + D.g_off + (int64_t)(idx >> 1) * D.g_es + (int64_t)p * D.g_ps + m)[idx & 1] = s;
+  }
+#pragma unroll
+  for (int j = 0; j < LPW; ++j)
+#pragma unroll
+    for (int e = 0; e < E; ++e) hs[warp][e][lane + 32 * j] = h[j][e];
+  __syncthreads();
+  for (int t = threadIdx.x; t < E * 32 * LPW; t += blockDim.x) {
+    const int e = t / (32 * LPW), l = t % (32 * LPW);
+    if (e < E2 && l < nx) {
+      double2 acc = hs[0][e][l];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) {
+        acc.x += hs[w][e][l].x;
+        acc.y += hs[w][e][l].y;
+      }
+      IF[D.h_off + (int64_t)e * D.h_es + (int64_t)p * D.h_ps + l] = acc;
+    }
+  }
+}
+
 template <int E, int LPT>
 cudaError_t launch_e(const PDesc* d, int ndesc, int maxplanes, int threads, cudaStream_t st, const Bufs& bufs) {
   const size_t sm = (size_t)2 * RB * (threads / 32) * 2 * E * sizeof(double);
@@ -175,6 +261,17 @@ cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, i
                         const Bufs& bufs) {
   if (ndesc <= 0 || maxplanes <= 0) return cudaSuccess;
   if (ndesc > 65535 || max_nx > 1024) return cudaErrorInvalidValue;
+  if (maxE <= 2 && max_nx > 32 && max_nx <= 128) {  // wide block planes: row-per-warp variant
+    const dim3 grid((unsigned)maxplanes, (unsigned)ndesc);
+#define PR(LPW)                                                   \
+  {                                                               \
+    k_proj_rows<2, LPW><<<grid, 128, 0, st>>>(d_descs, bufs);     \
+    return cudaGetLastError();                                    \
+  }
+    if (max_nx <= 64) PR(2)
+    PR(4)
+#undef PR
+  }
   int threads = ((max_nx + 31) / 32) * 32;
   if (threads <= 512) return launch_l<1>(maxE, d_descs, ndesc, maxplanes, threads, st, bufs);
   threads = ((max_nx + 63) / 64) * 32;
