@@ -129,6 +129,7 @@ struct lfds_plan {
   size_t tab_elems = 0;
   ZTab zt_scaled{}, zt_plain{}, zt_lift{};  // zt_lift: zt_scaled rows divided by -sigma_k (step 6)
   std::map<int, int64_t> t_tw;  // FFT twiddle tables per length L
+  int64_t t_dd[3] = {0, 0, 0};  // double-double stencil tables (x, y, z) for the residual
   int64_t t_hz = 0, t_hhz = 0, t_sig = 0, t_sige = 0, t_ifx = 0, t_ify = 0, t_bx = 0, t_by = 0, t_xlo = 0, t_ylo = 0;
   std::map<std::tuple<int, int, int>, PassPlan> passes;
   lfds_report report{};
@@ -867,6 +868,27 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
     }
     P->t_tw[L] = T.put(tw);
   }
+  {  // double-double stencil coefficients 1/h^x_t, 1/h^y_t, sigma_{t+1/2}/h^z_t (long double, split)
+    auto split_put = [&](const std::vector<std::complex<long double>>& v) {
+      std::vector<zc> w(2 * v.size());
+      for (size_t t = 0; t < v.size(); ++t) {
+        const long double re = v[t].real(), im = v[t].imag();
+        const double rh = (double)re, ih = (double)im;
+        w[2 * t] = zc(rh, (double)(re - rh));
+        w[2 * t + 1] = zc(ih, (double)(im - ih));
+      }
+      return T.put(w);
+    };
+    for (int a = 0; a < 2; ++a) {
+      std::vector<std::complex<long double>> r(P->ax[a].N + 1);
+      for (int t = 0; t <= P->ax[a].N; ++t) r[t] = 1.0L / std::complex<long double>(P->ax[a].h[t]);
+      P->t_dd[a] = split_put(r);
+    }
+    std::vector<std::complex<long double>> r(nz + 1);
+    for (int t = 0; t <= nz; ++t)
+      r[t] = std::complex<long double>(P->sig_edge[t]) / std::complex<long double>(P->hz[t]);
+    P->t_dd[2] = split_put(r);
+  }
   P->t_hz = T.put(P->hz);
   P->t_hhz = T.put(P->hhz);
   P->t_sig = T.put(P->sig_node);
@@ -965,7 +987,7 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         if (P->opt.profile) { ra = P->prof.get(); cudaEventRecord(ra, st); }
         CUDA_TRY(launch_residual(X.N, Y.N, P->nz, Rc, dt, P->opt.residual_dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff,
                                  Y.hhoff, P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()),
-                                 b.p[B_U], b.p[B_F], res, 1, norms, b, st));
+                                 P->t_dd, b.p[B_U], b.p[B_F], res, 1, norms, b, st));
         P->launches++;
         if (P->opt.profile) { cudaEvent_t rb2 = P->prof.get(); cudaEventRecord(rb2, st); P->prof.recs.push_back({ST_RESID, 1, ra, rb2}); }
         std::vector<double> hn(2 * Rc);
@@ -1141,7 +1163,8 @@ int lfds_residual(lfds_plan* P, const void* u_dev, const void* f_dev, lfds_z* r_
   const Axis& X = P->ax[0];
   const Axis& Y = P->ax[1];
   CUDA_TRY(launch_residual(X.N, Y.N, P->nz, nrhs, dt, dd, f_dev != nullptr, X.hoff, Y.hoff, P->t_hz, X.hhoff, Y.hhoff,
-                           P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()), u_dev, f_dev,
+                           P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()), P->t_dd, u_dev,
+                           f_dev,
                            reinterpret_cast<double2*>(r_dev), 0, d_norms, b, st));
   if (norms) {
     CUDA_TRY(cudaMemcpyAsync(norms, d_norms, sizeof(double) * 2 * nrhs, cudaMemcpyDeviceToHost, st));

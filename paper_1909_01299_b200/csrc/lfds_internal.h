@@ -126,8 +126,9 @@ cudaError_t launch_write_iface_u(int nx, int ny, int nz, int R, int dtype, int n
                                  const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, int has_f,
                             int64_t hx, int64_t hy, int64_t hz, int64_t hhx, int64_t hhy, int64_t hhz,
-                            int64_t sig, int64_t sige, double2 lam, const void* u, const void* f,
-                            double2* r, int to_f_units, double* d_norms, const Bufs& bufs, cudaStream_t st);
+                            int64_t sig, int64_t sige, double2 lam, const int64_t* ddtabs, const void* u,
+                            const void* f, double2* r, int to_f_units, double* d_norms, const Bufs& bufs,
+                            cudaStream_t st);
 cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st);
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
 size_t zsolve_checkpoint_bytes(int nblocks, int max_nx, int max_ny, int R, int nz);

@@ -336,20 +336,11 @@ __device__ __forceinline__ zdd zmul(zdd a, zdd b) {
   return zdd{dd_add(dd_mul(a.x, b.x), dd_neg(dd_mul(a.y, b.y))), dd_add(dd_mul(a.x, b.y), dd_mul(a.y, b.x))};
 }
 __device__ __forceinline__ zdd zfrom(cplx a) { return zdd{dd{a.x, 0}, dd{a.y, 0}}; }
-// 1/h in double-double (Newton step on the fp64 reciprocal)
-__device__ __forceinline__ zdd zinv_dd(cplx h) {
-  zdd H = zfrom(h);
-  cplx r0 = cinv(h);
-  zdd R0 = zfrom(r0);
-  // r1 = r0 + r0 (1 - h r0)
-  zdd e = zsub(zdd{dd{1.0, 0}, dd{0, 0}}, zmul(H, R0));
-  return zadd(R0, zmul(R0, e));
-}
-
 struct ResParams {
   int nx, ny, nz, R, dtype, dd, has_f, to_f;
   int64_t hx, hy, hz, hhx, hhy, hhz, sig, sige;
   double2 lam;
+  int64_t rxd, ryd, szd;  // double-double tables: 1/h^x_t, 1/h^y_t, sigma_{t+1/2}/h^z_t (2 slots each)
 };
 
 __device__ __forceinline__ cplx load_u(const void* u, int dtype, int64_t off) {
@@ -416,10 +407,14 @@ __global__ void k_residual(ResParams P, const void* __restrict__ u, const void* 
     } else {
       // every product and sum in double-double, rounded once at the end
       const zdd Uc = zfrom(uc);
-      zdd tx = zsub(zmul(zsub(zfrom(ur), Uc), zinv_dd(hx1)), zmul(zsub(Uc, zfrom(ul)), zinv_dd(hx0)));
-      zdd ty = zsub(zmul(zsub(zfrom(un), Uc), zinv_dd(hy1)), zmul(zsub(Uc, zfrom(us)), zinv_dd(hy0)));
-      zdd tz = zsub(zmul(zmul(zfrom(se1), zsub(zfrom(ut), Uc)), zinv_dd(hz1)),
-                    zmul(zmul(zfrom(se0), zsub(Uc, zfrom(ub))), zinv_dd(hz0)));
+      // stencil coefficients from the plan's double-double tables (no reciprocals per point)
+      auto tdd = [&](int64_t off, int t) {
+        const double2 a = __ldg(TAB + off + 2 * t), b = __ldg(TAB + off + 2 * t + 1);
+        return zdd{dd{a.x, a.y}, dd{b.x, b.y}};
+      };
+      zdd tx = zsub(zmul(zsub(zfrom(ur), Uc), tdd(P.rxd, i + 1)), zmul(zsub(Uc, zfrom(ul)), tdd(P.rxd, i)));
+      zdd ty = zsub(zmul(zsub(zfrom(un), Uc), tdd(P.ryd, j + 1)), zmul(zsub(Uc, zfrom(us)), tdd(P.ryd, j)));
+      zdd tz = zsub(zmul(zsub(zfrom(ut), Uc), tdd(P.szd, k + 1)), zmul(zsub(Uc, zfrom(ub)), tdd(P.szd, k)));
       // control volumes (h_{i-1}+h_i)/2 exactly in dd
       zdd Cx = zmul(zadd(zfrom(hx0), zfrom(hx1)), zdd{dd{0.5, 0}, dd{0, 0}});
       zdd Cy = zmul(zadd(zfrom(hy0), zfrom(hy1)), zdd{dd{0.5, 0}, dd{0, 0}});
@@ -449,9 +444,10 @@ __global__ void k_residual(ResParams P, const void* __restrict__ u, const void* 
 
 cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int ddm, int has_f, int64_t hx, int64_t hy,
                             int64_t hz, int64_t hhx, int64_t hhy, int64_t hhz, int64_t sig, int64_t sige, double2 lam,
-                            const void* u, const void* f, double2* r, int to_f_units, double* d_norms, const Bufs& bufs,
-                            cudaStream_t st) {
-  ResParams P{nx, ny, nz, R, dtype, ddm, has_f, to_f_units, hx, hy, hz, hhx, hhy, hhz, sig, sige, lam};
+                            const int64_t* ddtabs, const void* u, const void* f, double2* r, int to_f_units,
+                            double* d_norms, const Bufs& bufs, cudaStream_t st) {
+  ResParams P{nx, ny, nz, R, dtype, ddm, has_f, to_f_units, hx, hy, hz, hhx, hhy, hhz, sig, sige, lam,
+              ddtabs[0], ddtabs[1], ddtabs[2]};
   int64_t total = (int64_t)nx * ny * nz * R;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;

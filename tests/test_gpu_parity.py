@@ -209,6 +209,42 @@ def test_full_size_configs_vs_oracle(name):
     assert rel(U[0], ref) < TOL, rel(U[0], ref)
 
 
+@pytest.mark.slow
+def test_full_size_c4_vs_oracle():
+    """C4 at its full BASELINE.json size (1024 x 1024 x 256, 8 x 8 blocks), the launch bench.py
+    times (one right-hand side, no refinement): element by element against oracle (ii)'s global
+    separable solve, plus the double-double residual bar of north_star."""
+    p = make_problem("c4")
+    F = p.rhs_all()
+    plan, U = gpu_solve(p, F)
+    ut = torch.from_numpy(U).cuda()
+    _, norms = plan.residual(ut, torch.from_numpy(F).cuda(), dd=True)
+    assert norms[0, 0] / norms[0, 1] < 1e-10
+    ref = oracle.solve_separable(p, oracle.mass_rhs(p, F[0]))
+    assert rel(U[0], ref) < TOL, rel(U[0], ref)
+
+
+@pytest.mark.slow
+def test_full_size_c5_chunked_vs_oracle():
+    """C5 grid at full size (512 x 512 x 200, 16 x 16 blocks) with the bench's RHS chunking
+    (here 3 right-hand sides in chunks of 2).  C5's lambda > 0 is near-resonant (reading R13:
+    min |lambda_l + mu_m + theta_t| ~ 1e-7), so one fp64 pass is only kappa*eps accurate; with
+    double-double refinement the GPU solution agrees with the oracle's 80-bit-refined one."""
+    import dataclasses
+    p = dataclasses.replace(make_problem("c5"), nrhs=3)
+    F = p.rhs_all()
+    plan, U = gpu_solve(p, F, rhs_chunk=2, refine=-1, refine_tol=1e-14)
+    _, U1 = gpu_solve(p, F, refine=-1, refine_tol=1e-14)
+    assert rel(U, U1) < 1e-12
+    ut = torch.from_numpy(U).cuda()
+    _, norms = plan.residual(ut, torch.from_numpy(F).cuda(), dd=True)
+    assert (norms[:, 0] / norms[:, 1]).max() < 1e-12
+    _, U0 = gpu_solve(p, F[1:2])                     # single pass, as timed without refinement
+    ref = oracle.solve(p, F[1])                      # oracle (ii) + 80-bit refinement
+    print("c5 single-pass error", rel(U0[0], ref), "refined", rel(U[1], ref))
+    assert rel(U[1], ref) < TOL, rel(U[1], ref)
+
+
 @pytest.mark.parametrize("name,world", [("c2", 2), ("c5", 3), ("c4", 4)])
 def test_block_sharded_solve_matches_single_device(name, world):
     """Block sharding (north_star: blocks over ranks, one interface exchange): `world` ranks
