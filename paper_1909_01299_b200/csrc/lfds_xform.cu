@@ -234,7 +234,7 @@ cudaError_t launch_one(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, con
 //   T1 = Sr Br, T2 = Si Bi, T3 = (Sr + Si)(Br + Bi);   Cr = T1 - T2,  Ci = T3 - T1 - T2
 // 3 DMMA per complex 8x8x4 step instead of 4 (25% fewer tensor-pipe cycles; the sums are
 // one DADD per fragment element).  CTA 64 x 64, 8 warps of 32 rows x 16 complex columns.
-constexpr int X3_THREADS = 256, X3_STAGES = 3;
+constexpr int X3_THREADS = 256;
 
 template <bool KCONTIG>
 __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __restrict__ descs, Bufs bufs) {
@@ -304,19 +304,15 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
     for (int b = 0; b < 2; ++b)
 #pragma unroll
       for (int h = 0; h < 2; ++h) t1[a][b][h] = t2[a][b][h] = t3[a][b][h] = 0.0;
-  // 3-stage cp.async pipeline, one barrier per K chunk: chunk c+2 is issued after the barrier
-  // of chunk c, into the slot chunk c-1 used (every thread is past its reads by then)
   const int nchunks = (K + XT_K - 1) / XT_K;
   load_chunk(0, 0);
   cp_commit();
-  if (1 < nchunks) load_chunk(1, XT_K);
-  cp_commit();
   for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) load_chunk((c + 1) & 1, (c + 1) * XT_K);
+    cp_commit();
     cp_wait<1>();
     __syncthreads();
-    if (c + 2 < nchunks) load_chunk((c + 2) % X3_STAGES, (c + 2) * XT_K);
-    cp_commit();
-    const double2* As = reinterpret_cast<const double2*>(xsm + (c % X3_STAGES) * STAGE);
+    const double2* As = reinterpret_cast<const double2*>(xsm + (c & 1) * STAGE);
     const double2* Bs = As + XT_K * LDA_C;
 #pragma unroll
     for (int kk = 0; kk < XT_K; kk += 4) {
@@ -341,6 +337,7 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
           dmma(t3[i][j][0], t3[i][j][1], sa[i], sb[j]);
         }
     }
+    __syncthreads();
   }
   cp_wait<0>();
   double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
@@ -365,7 +362,7 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
 
 template <bool KCONTIG>
 cudaError_t launch_3m(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
-  const size_t sm = (size_t)X3_STAGES * XSmem<false>::STAGE * sizeof(double);
+  const size_t sm = XSmem<false>::BYTES;
   cudaError_t e = cudaFuncSetAttribute(k_xform3m<KCONTIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   for (int z0 = 0; z0 < ndesc; z0 += 65535) {
