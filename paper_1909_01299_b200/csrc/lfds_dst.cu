@@ -12,6 +12,8 @@
 // threads run R2-point FFTs.  Only the outputs k = 1..N-1 are kept.  FP64 CUDA-core
 // arithmetic: ~5 L log2 L flops per column instead of the 4 n^2 of the dense real matrix.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -190,6 +192,104 @@ cudaError_t dst_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& b
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- warp-autonomous variant
+// A warp transforms CPW = 32/R2 columns at a time, R2 lanes per column, with no CTA barrier:
+// lane t of a column loads its R1 inputs y[R2 n1 + t] of the odd extension straight from
+// global memory into registers (for contiguous columns one load instruction covers R2
+// consecutive elements; for adjacent strided columns the CPW columns of a warp are adjacent
+// in memory, so every 32-byte sector is used), runs the first R1-point FFTs, exchanges
+// through a per-warp shared-memory transpose (__syncwarp only), runs the R2-point FFTs and
+// stores its outputs directly.  Many independent warps keep many loads in flight; each warp
+// walks its columns in a grid-stride loop.  Used for contiguous columns (x direction): for
+// strided columns two adjacent columns per warp use only 32-byte pieces of each row, and the
+// CTA-tiled k_dst (8 adjacent columns per row) is faster there.
+constexpr int DSTW_WARPS = 4;
+
+template <int R1, int R2>
+__global__ void __launch_bounds__(DSTW_WARPS * 32) k_dstw(const GemmDesc* __restrict__ descs, int ndesc, int64_t maxN,
+                                                          Bufs bufs) {
+  constexpr int L = R1 * R2, N = L / 2, CPW = 32 / R2, LDE = R2 + 1;
+  __shared__ double2 twl[L];
+  __shared__ double2 tws[R1 * R2];                       // W_L^{t k1} at [k1][t]
+  __shared__ double2 exs[DSTW_WARPS][CPW * R1 * LDE];    // per-warp exchange
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cw = lane / R2, t = lane % R2;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const double2* TW = TAB + descs[0].a_off;              // one length per launch
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    twl[j] = __ldg(TW + j);
+    tws[j] = __ldg(TW + ((j % R2) * (j / R2)) % L);
+  }
+  __syncthreads();
+  double2* ex = exs[warp];
+  const int64_t groups_per_desc = (maxN + CPW - 1) / CPW;
+  const int64_t total = groups_per_desc * ndesc;
+  for (int64_t gi = (int64_t)blockIdx.x * DSTW_WARPS + warp; gi < total; gi += (int64_t)gridDim.x * DSTW_WARPS) {
+    const GemmDesc& D = descs[gi / groups_per_desc];
+    const int64_t col = (gi % groups_per_desc) * CPW + cw, NC = (int64_t)D.N1 * D.N2;
+    const bool ok = col < NC;
+    const int64_t n1c = ok ? col / D.N2 : 0, n2c = ok ? col - n1c * D.N2 : 0;
+    const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off + n1c * D.sB1 + n2c * D.sB2;
+    double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off + n1c * D.sC1 + n2c * D.sC2;
+    const int64_t sb = D.sBj, sc = D.sCi;
+    // ---- loads: y[q], q = R2 n1 + t (x_{q-1} for 0 < q < N, -x_{L-q-1} for q > N, 0 at 0, N)
+    zc2 a[R1];
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) {
+      const int q = R2 * n1 + t;
+      zc2 v{0, 0};
+      if (ok && q > 0 && q < N) {
+        const double2 w = __ldg(B + (int64_t)(q - 1) * sb);
+        v = zc2{w.x, w.y};
+      } else if (ok && q > N) {
+        const double2 w = __ldg(B + (int64_t)(L - q - 1) * sb);
+        v = zc2{-w.x, -w.y};
+      }
+      a[n1] = v;
+    }
+    fft_reg<R1, L>(a, twl);
+#pragma unroll
+    for (int k1 = 1; k1 < R1; ++k1) {
+      const double2 w = tws[k1 * R2 + t];
+      a[k1] = zmul(a[k1], zc2{w.x, w.y});
+    }
+    __syncwarp();  // previous column group's exchange reads are done
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) ex[(cw * R1 + k1) * LDE + t] = make_double2(a[k1].x, a[k1].y);
+    __syncwarp();
+    // ---- R2-point FFTs: lane t < R1 of the column takes row k1 = t; outputs k = k1 + R1 k2
+    if (t < R1) {
+      zc2 b[R2];
+#pragma unroll
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const double2 w = ex[(cw * R1 + t) * LDE + n2];
+        b[n2] = zc2{w.x, w.y};
+      }
+      fft_reg<R2, L>(b, twl);
+      const double half = 0.5 * D.scale;
+#pragma unroll
+      for (int k2 = 0; k2 < R2 / 2; ++k2) {
+        const int k = t + R1 * k2;
+        if (ok && k >= 1 && k < N) C[(int64_t)(k - 1) * sc] = make_double2(-half * b[k2].y, half * b[k2].x);  // (i/2) Y
+      }
+    }
+  }
+}
+
+template <int R1, int R2>
+cudaError_t dstw_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dstw<R1, R2>, DSTW_WARPS * 32, 0);
+  if (e != cudaSuccess) return e;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  constexpr int CPW = 32 / R2;
+  const int64_t warps = ((maxN + CPW - 1) / CPW) * ndesc;
+  const int64_t grid = std::min<int64_t>((warps + DSTW_WARPS - 1) / DSTW_WARPS, (int64_t)sms * std::max(1, per_sm));
+  k_dstw<R1, R2><<<(unsigned)grid, DSTW_WARPS * 32, 0, st>>>(d, ndesc, maxN, bufs);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool dst_supported(int n) {
@@ -208,7 +308,9 @@ cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, 
     case 32: DL(4, 8);
     case 64: DL(8, 8);
     case 128: DL(8, 16);
-    case 256: DL(16, 16);
+    case 256:  // contiguous columns: warp-autonomous kernel; strided columns: CTA tiles (coalescing)
+      if (kcontig) return dstw_launch<16, 16>(d_descs, ndesc, maxN, bufs, st);
+      return dst_launch<16, 16, false>(d_descs, ndesc, maxN, bufs, st);
     case 512: DL(16, 32);
     default: return cudaErrorInvalidValue;
   }
