@@ -63,6 +63,73 @@ __device__ __forceinline__ void fft_reg(zc2 (&v)[R], const double2* __restrict__
   }
 }
 
+// Mixed-radix in-register DFT of length R = 2^a 3^b 5^c (compile-time Cooley-Tukey, decimation
+// in time: R = P Q with P the smallest prime factor; X[k1 + P k2] = sum_n2 W_Q^{n2 k2}
+// W_R^{n2 k1} sum_n1 W_P^{n1 k1} x[Q n1 + n2]); twiddles from the W_L table (R divides L).
+template <int P>
+__device__ __forceinline__ void dft_small(zc2 (&x)[P]) {
+  if constexpr (P == 2) {
+    const zc2 a = x[0], b = x[1];
+    x[0] = zadd(a, b);
+    x[1] = zsub(a, b);
+  } else if constexpr (P == 3) {  // W = e^{-2 pi i/3}
+    constexpr double h = 0.86602540378443864676;  // sqrt(3)/2
+    const zc2 a = x[0], t1 = zadd(x[1], x[2]), d = zsub(x[1], x[2]);
+    const zc2 t2{a.x - 0.5 * t1.x, a.y - 0.5 * t1.y};
+    x[0] = zadd(a, t1);
+    x[1] = zc2{t2.x + h * d.y, t2.y - h * d.x};  // t2 - i h d
+    x[2] = zc2{t2.x - h * d.y, t2.y + h * d.x};  // t2 + i h d
+  } else {  // P == 5, W = e^{-2 pi i/5}
+    constexpr double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+    constexpr double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;
+    const zc2 a = x[0];
+    const zc2 t1 = zadd(x[1], x[4]), t2 = zadd(x[2], x[3]), t3 = zsub(x[1], x[4]), t4 = zsub(x[2], x[3]);
+    const zc2 r1{a.x + c1 * t1.x + c2 * t2.x, a.y + c1 * t1.y + c2 * t2.y};
+    const zc2 r2{a.x + c2 * t1.x + c1 * t2.x, a.y + c2 * t1.y + c1 * t2.y};
+    const zc2 i1{s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y};
+    const zc2 i2{s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y};
+    x[0] = zc2{a.x + t1.x + t2.x, a.y + t1.y + t2.y};
+    x[1] = zc2{r1.x + i1.y, r1.y - i1.x};  // r1 - i i1
+    x[4] = zc2{r1.x - i1.y, r1.y + i1.x};
+    x[2] = zc2{r2.x + i2.y, r2.y - i2.x};
+    x[3] = zc2{r2.x - i2.y, r2.y + i2.x};
+  }
+}
+
+template <int R, int L>
+__device__ __forceinline__ void dft_reg(zc2 (&v)[R], const double2* __restrict__ twl) {
+  if constexpr ((R & (R - 1)) == 0) {
+    fft_reg<R, L>(v, twl);
+  } else if constexpr (R == 3 || R == 5) {
+    dft_small<R>(v);
+  } else {
+    constexpr int P = R % 2 == 0 ? 2 : R % 3 == 0 ? 3 : 5, Q = R / P;
+    zc2 A[P][Q];
+#pragma unroll
+    for (int n2 = 0; n2 < Q; ++n2) {
+      zc2 x[P];
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1) x[n1] = v[Q * n1 + n2];
+      dft_small<P>(x);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) {
+        if (n2 * k1 == 0) {
+          A[k1][n2] = x[k1];
+        } else {
+          const double2 w = twl[(n2 * k1 * (L / R)) % L];
+          A[k1][n2] = zmul(x[k1], zc2{w.x, w.y});
+        }
+      }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+      dft_reg<Q, L>(A[k1], twl);
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) v[k1 + P * k2] = A[k1][k2];
+    }
+  }
+}
+
 constexpr int DST_THREADS = 128;  // 8 columns per CTA at L = 256: small CTAs, many resident per SM
 
 __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool valid) {
@@ -131,7 +198,7 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
     }
     a[n1] = v;
   }
-  fft_reg<R1, L>(a, twl);
+  dft_reg<R1, L>(a, twl);
 #pragma unroll
   for (int k1 = 1; k1 < R1; ++k1) {
     const double2 w = twl[(t * k1) % L];
@@ -141,23 +208,33 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
 #pragma unroll
   for (int k1 = 0; k1 < R1; ++k1) ex[(col * R1 + k1) * LDE + t] = make_double2(a[k1].x, a[k1].y);
   __syncthreads();
-  // ---- step 3: thread k1 = t < R1: R2-point FFT over n2 -> Y[k1 + R1 k2], keep k < N
-  zc2 b[R2];
-  if (t < R1) {
+  // ---- step 3: rows k1 = t, t + R2, ...: R2-point FFT over n2 -> Y[k1 + R1 k2], keep k < N.
+  // The exchange is read completely before the output tile (aliased) is written.
+  constexpr int RPT = (R1 + R2 - 1) / R2;  // rows per thread
+  zc2 b[RPT][R2];
 #pragma unroll
-    for (int n2 = 0; n2 < R2; ++n2) {
-      const double2 w = ex[(col * R1 + t) * LDE + n2];
-      b[n2] = zc2{w.x, w.y};
+  for (int rr = 0; rr < RPT; ++rr) {
+    const int k1 = t + rr * R2;
+    if (k1 < R1) {
+#pragma unroll
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const double2 w = ex[(col * R1 + k1) * LDE + n2];
+        b[rr][n2] = zc2{w.x, w.y};
+      }
+      fft_reg<R2, L>(b[rr], twl);
     }
-    fft_reg<R2, L>(b, twl);
   }
   __syncthreads();  // exchange consumed; reuse as output tile[c][col]
   const double half = 0.5 * D.scale;
-  if (t < R1) {
 #pragma unroll
-    for (int k2 = 0; k2 < R2 / 2; ++k2) {
-      const int k = t + R1 * k2;
-      if (k >= 1 && k < N) tile[(k - 1) * LDT + col] = make_double2(-half * b[k2].y, half * b[k2].x);  // (i/2) Y
+  for (int rr = 0; rr < RPT; ++rr) {
+    const int k1 = t + rr * R2;
+    if (k1 < R1) {
+#pragma unroll
+      for (int k2 = 0; k2 < R2 / 2; ++k2) {
+        const int k = k1 + R1 * k2;
+        if (k >= 1 && k < N) tile[(k - 1) * LDT + col] = make_double2(-half * b[rr][k2].y, half * b[rr][k2].x);
+      }
     }
   }
   __syncthreads();
@@ -203,12 +280,15 @@ cudaError_t dst_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& b
 // walks its columns in a grid-stride loop.  Used for contiguous columns (x direction): for
 // strided columns two adjacent columns per warp use only 32-byte pieces of each row, and the
 // CTA-tiled k_dst (8 adjacent columns per row) is faster there.
-constexpr int DSTW_WARPS = 4;
+template <int R1>
+struct DstwWarps {  // warps per CTA (static shared memory: per-warp exchange + two twiddle tables)
+  static constexpr int value = R1 > 16 ? 2 : 4;
+};
 
 template <int R1, int R2>
-__global__ void __launch_bounds__(DSTW_WARPS * 32) k_dstw(const GemmDesc* __restrict__ descs, int ndesc, int64_t maxN,
+__global__ void __launch_bounds__(DstwWarps<R1>::value * 32) k_dstw(const GemmDesc* __restrict__ descs, int ndesc, int64_t maxN,
                                                           Bufs bufs) {
-  constexpr int L = R1 * R2, N = L / 2, CPW = 32 / R2, LDE = R2 + 1;
+  constexpr int L = R1 * R2, N = L / 2, CPW = 32 / R2, LDE = R2 + 1, DSTW_WARPS = DstwWarps<R1>::value;
   __shared__ double2 twl[L];
   __shared__ double2 tws[R1 * R2];                       // W_L^{t k1} at [k1][t]
   __shared__ double2 exs[DSTW_WARPS][CPW * R1 * LDE];    // per-warp exchange
@@ -247,7 +327,7 @@ __global__ void __launch_bounds__(DSTW_WARPS * 32) k_dstw(const GemmDesc* __rest
       }
       a[n1] = v;
     }
-    fft_reg<R1, L>(a, twl);
+    dft_reg<R1, L>(a, twl);
 #pragma unroll
     for (int k1 = 1; k1 < R1; ++k1) {
       const double2 w = tws[k1 * R2 + t];
@@ -257,20 +337,24 @@ __global__ void __launch_bounds__(DSTW_WARPS * 32) k_dstw(const GemmDesc* __rest
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) ex[(cw * R1 + k1) * LDE + t] = make_double2(a[k1].x, a[k1].y);
     __syncwarp();
-    // ---- R2-point FFTs: lane t < R1 of the column takes row k1 = t; outputs k = k1 + R1 k2
-    if (t < R1) {
-      zc2 b[R2];
+    // ---- R2-point FFTs: lane t of the column takes rows k1 = t, t + R2, ...; outputs k = k1 + R1 k2
 #pragma unroll
-      for (int n2 = 0; n2 < R2; ++n2) {
-        const double2 w = ex[(cw * R1 + t) * LDE + n2];
-        b[n2] = zc2{w.x, w.y};
-      }
-      fft_reg<R2, L>(b, twl);
-      const double half = 0.5 * D.scale;
+    for (int rr = 0; rr < (R1 + R2 - 1) / R2; ++rr) {
+      const int k1 = t + rr * R2;
+      if (k1 < R1) {
+        zc2 b[R2];
 #pragma unroll
-      for (int k2 = 0; k2 < R2 / 2; ++k2) {
-        const int k = t + R1 * k2;
-        if (ok && k >= 1 && k < N) C[(int64_t)(k - 1) * sc] = make_double2(-half * b[k2].y, half * b[k2].x);  // (i/2) Y
+        for (int n2 = 0; n2 < R2; ++n2) {
+          const double2 w = ex[(cw * R1 + k1) * LDE + n2];
+          b[n2] = zc2{w.x, w.y};
+        }
+        fft_reg<R2, L>(b, twl);
+        const double half = 0.5 * D.scale;
+#pragma unroll
+        for (int k2 = 0; k2 < R2 / 2; ++k2) {
+          const int k = k1 + R1 * k2;
+          if (ok && k >= 1 && k < N) C[(int64_t)(k - 1) * sc] = make_double2(-half * b[k2].y, half * b[k2].x);
+        }
       }
     }
   }
@@ -278,6 +362,7 @@ __global__ void __launch_bounds__(DSTW_WARPS * 32) k_dstw(const GemmDesc* __rest
 
 template <int R1, int R2>
 cudaError_t dstw_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
+  constexpr int DSTW_WARPS = DstwWarps<R1>::value;
   int per_sm = 0, dev = 0, sms = 148;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dstw<R1, R2>, DSTW_WARPS * 32, 0);
   if (e != cudaSuccess) return e;
@@ -294,7 +379,10 @@ cudaError_t dstw_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& 
 
 bool dst_supported(int n) {
   const int L = 2 * (n + 1);
-  return L == 16 || L == 32 || L == 64 || L == 128 || L == 256 || L == 512;
+  if (L == 16 || L == 32 || L == 64 || L == 128 || L == 256 || L == 512) return true;
+  // mixed radix: L = R1 * 16 with R1 in {3, 5, 6, 10, 12, 20} (e.g. n = 159: L = 320)
+  const int r1 = L / 16;
+  return L % 16 == 0 && (r1 == 3 || r1 == 5 || r1 == 6 || r1 == 10 || r1 == 12 || r1 == 20);
 }
 
 cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, bool kcontig, const Bufs& bufs,
@@ -312,6 +400,12 @@ cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, 
       if (kcontig) return dstw_launch<16, 16>(d_descs, ndesc, maxN, bufs, st);
       return dst_launch<16, 16, false>(d_descs, ndesc, maxN, bufs, st);
     case 512: DL(16, 32);
+#define DM(R1)                                                                        \
+  case 16 * R1:                                                                       \
+    if (kcontig) return dstw_launch<R1, 16>(d_descs, ndesc, maxN, bufs, st);          \
+    return dst_launch<R1, 16, false>(d_descs, ndesc, maxN, bufs, st);
+    DM(3) DM(5) DM(6) DM(10) DM(12) DM(20)
+#undef DM
     default: return cudaErrorInvalidValue;
   }
 #undef DL

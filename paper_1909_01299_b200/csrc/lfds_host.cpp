@@ -860,11 +860,14 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
     }
     P->zt_lift = ZTab{T.put(la), T.put(lg), T.put(lc), T.put(le)};
   }
-  for (int L = 16; L <= 512; L *= 2) {  // FFT twiddles W_L^j = exp(-2 pi i j/L) for the sine transforms
+  for (auto& a : P->ax)  // FFT twiddles W_L^j = exp(-2 pi i j/L) for the sine transforms in use
+    for (auto& b : a.blocks) {
+    const int L = 2 * (b.n + 1);
+    if (!b.dst || P->t_tw.count(L)) continue;
     std::vector<zc> tw(L);
     for (int j = 0; j < L; ++j) {
-      const long double a = -2.0L * 3.141592653589793238462643383279502884L * j / L;
-      tw[j] = zc((double)std::cos(a), (double)std::sin(a));
+      const long double ang = -2.0L * 3.141592653589793238462643383279502884L * j / L;
+      tw[j] = zc((double)std::cos(ang), (double)std::sin(ang));
     }
     P->t_tw[L] = T.put(tw);
   }

@@ -41,7 +41,7 @@ def gpu_solve(p, F, **kw):
     return plan, u.cpu().numpy()
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "c4j"])
 def test_shrunken_configs_single_pass(name):
     """Two-level GPU solve vs oracle (i) sparse LU, no refinement."""
     p = shrunken(name)
@@ -163,9 +163,10 @@ def test_uniform_blocks_with_pml_blocks():
     assert rel(U[0], ref) < TOL
 
 
-@pytest.mark.parametrize("n", [7, 31, 63, 127, 255])
+@pytest.mark.parametrize("n", [7, 31, 63, 127, 255, 23, 39, 47, 79, 95, 159])
 def test_sine_transform_lengths(n):
-    """Every FFT length of the sine-transform kernel (L = 2(n+1) = 16 .. 512) against the oracle,
+    """Every FFT length of the sine-transform kernel (L = 2(n+1) = 16 .. 512, and the mixed-radix
+    lengths 16*{3, 5, 6, 10, 12, 20}) against the oracle,
     with the sine direction along x (contiguous columns) and along y (strided columns)."""
     N = 2 * n + 1
     hx = np.ones(N + 1)

@@ -33,7 +33,7 @@ from typing import Callable, List, Optional
 
 import numpy as np
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c4j")
 
 
 def _rng(cfg: int, stream: int) -> np.random.Generator:
@@ -211,6 +211,13 @@ def make_problem(name: str) -> Problem:
         return _build(5, "c5", C=448, G=24, q=1.2, P=8, pml="quad", nz=200, layers=30, lrange=(-1, 1),
                       lam=_lam(10), B=16, nrhs=64, rhs_kind="cn", core_jitter=True,
                       description="multi-RHS 512x512x200 x 64 RHS, 16x16 blocks")
+    if name == "c4j":
+        # C4 with the paper's partition strategy for grids with a uniform survey core (PAPER.md:75,
+        # "three subgrids": thin non-uniform / PML tails, uniform core computed by FFT), kept at
+        # BASELINE.json's 8 x 8 block count: interfaces at the last left-PML node and the last core
+        # node, six uniform core blocks of 159 nodes (sine transforms of length 320) between
+        j = [32, 192, 352, 512, 672, 832, 992]
+        return make_problem("c4").with_partition(j, j, name="c4j")
     raise KeyError(name)
 
 
@@ -227,6 +234,10 @@ def shrunken(name: str, nrhs: Optional[int] = None) -> Problem:
     if name == "c4":
         return _build(104, "c4s", C=30, G=0, q=1.0, P=8, pml="const", nz=12, layers=5, lrange=(-1, 1),
                       lam=_lam(10), B=4, nrhs=nrhs or 1, rhs_kind="points16")
+    if name == "c4j":  # tails 7 / 8 PML nodes, two uniform core blocks of 15 (L = 32)
+        j = [8, 24, 40]
+        return _build(106, "c4js", C=32, G=0, q=1.0, P=8, pml="const", nz=12, layers=5, lrange=(-1, 1),
+                      lam=_lam(10), B=4, nrhs=nrhs or 1, rhs_kind="points16").with_partition(j, j, name="c4js")
     if name == "c5":
         return _build(105, "c5s", C=20, G=6, q=1.2, P=4, pml="quad", nz=9, layers=5, lrange=(-1, 1),
                       lam=_lam(10), B=5, nrhs=nrhs or 3, rhs_kind="cn", core_jitter=True)
