@@ -181,8 +181,9 @@ def stage_algorithmic(p, R: int, plan=None):
     ky = [plan.basis(1, j)[2] if plan else 2 for j in range(len(by))]
     nz = p.nz
 
-    def is_sine(kind, n):
-        return kind == 0 and (2 * (n + 1)) in (16, 32, 64, 128, 256, 512)
+    def is_sine(kind, n):  # mirrors dst_supported() in lfds_dst.cu
+        L = 2 * (n + 1)
+        return kind == 0 and (L in (16, 32, 64, 128, 256, 512) or (L % 16 == 0 and L // 16 in (3, 5, 6, 10, 12, 20)))
 
     def dense(kinds, sz, axis):
         fl, el = 0.0, 0.0

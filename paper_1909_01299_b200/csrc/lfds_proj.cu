@@ -261,7 +261,7 @@ cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, i
                         const Bufs& bufs) {
   if (ndesc <= 0 || maxplanes <= 0) return cudaSuccess;
   if (ndesc > 65535 || max_nx > 1024) return cudaErrorInvalidValue;
-  if (maxE <= 2 && max_nx > 32 && max_nx <= 128) {  // wide block planes: row-per-warp variant
+  if (maxE <= 2 && max_nx > 32 && max_nx <= 160) {  // wide block planes: row-per-warp variant
     const dim3 grid((unsigned)maxplanes, (unsigned)ndesc);
 #define PR(LPW)                                                   \
   {                                                               \
@@ -269,7 +269,8 @@ cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, i
     return cudaGetLastError();                                    \
   }
     if (max_nx <= 64) PR(2)
-    PR(4)
+    if (max_nx <= 128) PR(4)
+    PR(5)
 #undef PR
   }
   int threads = ((max_nx + 31) / 32) * 32;

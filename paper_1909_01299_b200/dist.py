@@ -24,7 +24,8 @@ def block_costs(nx_blocks: Sequence[int], ny_blocks: Sequence[int], kinds_x: Seq
     """Modelled cost of each block (row-major [j][i]): elements x per-direction transform cost
     (+ the z-solves and edge work, ~60 units per element)."""
     def dcost(kind, n):
-        if kind == 0 and (2 * (n + 1)) in (16, 32, 64, 128, 256, 512):
+        L = 2 * (n + 1)
+        if kind == 0 and (L in (16, 32, 64, 128, 256, 512) or (L % 16 == 0 and L // 16 in (3, 5, 6, 10, 12, 20))):
             return 40.0                                   # sine transform, HBM-bound
         return (8.0 if kind == 2 else 4.0) * n             # dense DMMA contraction
     c = np.zeros((len(ny_blocks), len(nx_blocks)))
