@@ -583,32 +583,40 @@ __device__ __forceinline__ void zs3_body(const ZBlock& B, int nz, const ZTabS& T
   const int tx = threadIdx.x % TL, ty = threadIdx.x / TL;
   // warp -> row j = warp % ZSEG of the segment and (m-tile, l-tile) pairs warp / ZSEG + WPR*i
   constexpr int NT = TL / 8, MT = TM / 8, NPAIR = NT * MT, WPR = 8 / ZSEG, PPW = NPAIR / WPR;
+  // 3-multiplication complex form, all pairs of the warp interleaved: 3*PPW independent
+  // accumulator chains of KA/2 DMMAs each (short dependency chains, A fragments shared)
   auto rhs_tile = [&](int sg) {
     const int j = warp % ZSEG;
     const double2* a1 = R1s + (sg & 1) * RS::R1S + j * KA * TM;  // [a][m]
     const double2* b2 = R2s + (sg & 1) * RS::R2S + j * KA * TL;  // [b][l]
+    double t1[PPW][2], t2[PPW][2], t3[PPW][2];
+#pragma unroll
+    for (int pi = 0; pi < PPW; ++pi) t1[pi][0] = t1[pi][1] = t2[pi][0] = t2[pi][1] = t3[pi][0] = t3[pi][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KA / 4; ++ks) {
+      const int kk = 4 * ks + q;
+#pragma unroll
+      for (int pi = 0; pi < PPW; ++pi) {
+        const int pr = warp / ZSEG + WPR * pi, mt = pr / NT, nt = pr % NT;
+        const double2 A = a1[kk * TM + mt * 8 + g], Bv = WXs[kk * TL + nt * 8 + g];
+        const double2 A2 = WYs[kk * TM + mt * 8 + g], B2 = b2[kk * TL + nt * 8 + g];
+        dmma(t1[pi][0], t1[pi][1], A.x, Bv.x);
+        dmma(t2[pi][0], t2[pi][1], A.y, Bv.y);
+        dmma(t3[pi][0], t3[pi][1], A.x + A.y, Bv.x + Bv.y);
+        dmma(t1[pi][0], t1[pi][1], A2.x, B2.x);
+        dmma(t2[pi][0], t2[pi][1], A2.y, B2.y);
+        dmma(t3[pi][0], t3[pi][1], A2.x + A2.y, B2.x + B2.y);
+      }
+    }
 #pragma unroll
     for (int pi = 0; pi < PPW; ++pi) {
       const int pr = warp / ZSEG + WPR * pi, mt = pr / NT, nt = pr % NT;
-      double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
-#pragma unroll
-      for (int ks = 0; ks < KA / 4; ++ks) {
-        const int kk = 4 * ks + q;
-        const double2 A = a1[kk * TM + mt * 8 + g], Bv = WXs[kk * TL + nt * 8 + g];
-        dmma(cr0, cr1, A.x, Bv.x);
-        dmma(cr0, cr1, -A.y, Bv.y);
-        dmma(ci0, ci1, A.x, Bv.y);
-        dmma(ci0, ci1, A.y, Bv.x);
-        const double2 A2 = WYs[kk * TM + mt * 8 + g], B2 = b2[kk * TL + nt * 8 + g];
-        dmma(cr0, cr1, A2.x, B2.x);
-        dmma(cr0, cr1, -A2.y, B2.y);
-        dmma(ci0, ci1, A2.x, B2.y);
-        dmma(ci0, ci1, A2.y, B2.x);
-      }
       // C[m = mt*8 + g][l = nt*8 + 2q (+1)] -> the slot of thread (tx = l, ty = m)
       const int mm = mt * 8 + g, ll = nt * 8 + 2 * q;
-      RH[(j * TM + mm) * (TL + 1) + ll] = make_double2(cr0, ci0);
-      RH[(j * TM + mm) * (TL + 1) + ll + 1] = make_double2(cr1, ci1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        RH[(j * TM + mm) * (TL + 1) + ll + h] =
+            make_double2(t1[pi][h] - t2[pi][h], t3[pi][h] - t1[pi][h] - t2[pi][h]);
     }
   };
   float minpiv = 1.0f;
