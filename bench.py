@@ -333,8 +333,9 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         ne = min(nrhs, args.e2e_rhs) if not blocks else nrhs
         fh = f[:ne].cpu().pin_memory()
-        uhs = [torch.empty_like(fh).pin_memory() for _ in range(2)]
-        streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+        NSL = 3  # solves in flight: H2D of one, compute of another, D2H of a third
+        uhs = [torch.empty_like(fh).pin_memory() for _ in range(NSL)]
+        streams = [torch.cuda.Stream(device=dev) for _ in range(NSL)]
 
         def step_host(i):
             if blocks:  # H2D of f, sharded solve, D2H of u (this rank's part)
@@ -343,15 +344,15 @@ def run_ours(args, rank, world, local_rank):
                 uhs[0].copy_(u, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             else:
-                # consecutive solves alternate between two streams and workspaces: the
-                # host-to-device copy of one overlaps the compute / device-to-host copy of the other
-                plan.solve_host(fh, out=uhs[i % 2], stream=streams[i % 2], sync=False, slot=i % 2)
-        step_host(0)
-        step_host(1)
+                # consecutive solves rotate over NSL streams and workspaces, so the host-to-device
+                # copy, the compute and the device-to-host copy of different solves overlap
+                plan.solve_host(fh, out=uhs[i % NSL], stream=streams[i % NSL], sync=False, slot=i % NSL)
+        for i in range(NSL):
+            step_host(i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        k2 = max(4, args.steps)
+        k2 = max(6, args.steps)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for s_ in streams:
