@@ -443,7 +443,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shard", choices=["blocks", "rhs"], default=None,
                     help="N > 1: block sharding with two NCCL exchanges (default) or RHS sharding")
-    ap.add_argument("--e2e-rhs", type=int, default=8, dest="e2e_rhs", help="RHS per e2e step (host memory)")
+    ap.add_argument("--e2e-rhs", type=int, default=4, dest="e2e_rhs", help="RHS per e2e step (memory bound)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
