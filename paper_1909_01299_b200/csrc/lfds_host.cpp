@@ -871,8 +871,10 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
     }
     P->t_tw[L] = T.put(tw);
   }
-  {  // double-double stencil coefficients 1/h^x_t, 1/h^y_t, sigma_{t+1/2}/h^z_t (long double, split)
-    auto split_put = [&](const std::vector<std::complex<long double>>& v) {
+  {  // double-double stencil coefficients per node (long double, split into hi + lo):
+     // x, y: cl_i = 1/(h_{i-1} hh_i), cr_i = 1/(h_i hh_i); z: sigma_{k-1/2}/(h_{k-1} hh_k), sigma_{k+1/2}/(h_k hh_k)
+    using lc = std::complex<long double>;
+    auto split_put = [&](const std::vector<lc>& v) {
       std::vector<zc> w(2 * v.size());
       for (size_t t = 0; t < v.size(); ++t) {
         const long double re = v[t].real(), im = v[t].imag();
@@ -882,15 +884,20 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
       }
       return T.put(w);
     };
-    for (int a = 0; a < 2; ++a) {
-      std::vector<std::complex<long double>> r(P->ax[a].N + 1);
-      for (int t = 0; t <= P->ax[a].N; ++t) r[t] = 1.0L / std::complex<long double>(P->ax[a].h[t]);
-      P->t_dd[a] = split_put(r);
-    }
-    std::vector<std::complex<long double>> r(nz + 1);
-    for (int t = 0; t <= nz; ++t)
-      r[t] = std::complex<long double>(P->sig_edge[t]) / std::complex<long double>(P->hz[t]);
-    P->t_dd[2] = split_put(r);
+    auto node_tab = [&](const std::vector<zc>& h, const std::vector<zc>* se) {
+      const int n = (int)h.size() - 1;
+      std::vector<lc> v(2 * n);
+      for (int i = 0; i < n; ++i) {
+        const lc h0(h[i]), h1(h[i + 1]), hh = (h0 + h1) / 2.0L;
+        const lc s0 = se ? lc((*se)[i]) : lc(1), s1 = se ? lc((*se)[i + 1]) : lc(1);
+        v[2 * i] = s0 / (h0 * hh);
+        v[2 * i + 1] = s1 / (h1 * hh);
+      }
+      return split_put(v);
+    };
+    P->t_dd[0] = node_tab(P->ax[0].h, nullptr);
+    P->t_dd[1] = node_tab(P->ax[1].h, nullptr);
+    P->t_dd[2] = node_tab(P->hz, &P->sig_edge);
   }
   P->t_hz = T.put(P->hz);
   P->t_hhz = T.put(P->hhz);

@@ -340,7 +340,7 @@ struct ResParams {
   int nx, ny, nz, R, dtype, dd, has_f, to_f;
   int64_t hx, hy, hz, hhx, hhy, hhz, sig, sige;
   double2 lam;
-  int64_t rxd, ryd, szd;  // double-double tables: 1/h^x_t, 1/h^y_t, sigma_{t+1/2}/h^z_t (2 slots each)
+  int64_t rxd, ryd, szd;  // double-double node tables [n][cl, cr] (see k_residual), 2 slots per value
 };
 
 __device__ __forceinline__ cplx load_u(const void* u, int dtype, int64_t off) {
@@ -349,37 +349,32 @@ __device__ __forceinline__ cplx load_u(const void* u, int dtype, int64_t off) {
   return mk(v.x, v.y);
 }
 
-__global__ void k_residual(ResParams P, const void* __restrict__ u, const void* __restrict__ f, double2* __restrict__ rout,
-                           double* norms, Bufs bufs) {
+__device__ __forceinline__ zdd zmul_zd(zdd a, cplx b) {  // dd x double complex
+  auto m = [](dd x, double y) {
+    const double p = x.hi * y;
+    const double e = fma(x.hi, y, -p) + x.lo * y;
+    const double hi = p + e;
+    return dd{hi, e - (hi - p)};
+  };
+  return zdd{dd_add(m(a.x, b.x), dd_neg(m(a.y, b.y))), dd_add(m(a.x, b.y), m(a.y, b.x))};
+}
+
+// One thread per node: grid (x-tiles of 128, y, r*nz + k).  The double-double path evaluates
+// the residual in f-units, r_f = f - (A u)/V with V = hx^ hy^ hz^:
+//   (A u)/V = sigma_k [cxr (u_{i+1} - u_i) - cxl (u_i - u_{i-1}) + cyr (..) - cyl (..)]
+//           + czr (u_{k+1} - u_k) - czl (u_k - u_{k-1}) + lambda u_i,
+// cxl_i = 1/(h_{i-1} hx^_i), cxr_i = 1/(h_i hx^_i), czl_k = sigma_{k-1/2}/(h_{k-1} hz^_k), ...
+// from the plan's long-double tables (Eq. (fd) divided by the control volume, term by term).
+__global__ void __launch_bounds__(128) k_residual(ResParams P, const void* __restrict__ u, const void* __restrict__ f,
+                                                  double2* __restrict__ rout, double* norms, Bufs bufs) {
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const int nx = P.nx, ny = P.ny, nz = P.nz;
-  const int64_t plane = (int64_t)nx * ny, vol = plane * nz, total = vol * P.R;
-  // per-rhs partial norms: registers -> block reduction in shared memory -> one atomic per
-  // block and rhs (a per-thread atomic on two addresses serialises the whole kernel)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  const int r = blockIdx.z / nz, k = blockIdx.z - r * nz;
+  const int64_t plane = (int64_t)nx * ny;
   double acc_r = 0, acc_b = 0;
-  int rcur = -1;
-  auto flush = [&](int rr) {
-    if (!norms) return;
-    double a = acc_r, b2 = acc_b;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b2 += __shfl_xor_sync(0xffffffffu, b2, o);
-    }
-    if (rr >= 0 && (threadIdx.x & 31) == 0) {
-      atomicAdd(norms + 2 * rr, a);
-      atomicAdd(norms + 2 * rr + 1, b2);
-    }
-    acc_r = acc_b = 0;
-  };
-  (void)total;
-  for (int r = 0; r < P.R; ++r) {
-  rcur = r;
-  for (int64_t tl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; tl < vol; tl += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = (int64_t)r * vol + tl;
-    const int i = (int)(tl % nx);
-    const int j = (int)((tl / nx) % ny);
-    const int k = (int)(tl / plane);
+  if (i < nx) {
+    const int64_t t = ((int64_t)r * nz + k) * plane + (int64_t)j * nx + i;
     const cplx uc = load_u(u, P.dtype, t);
     const cplx ul = i > 0 ? load_u(u, P.dtype, t - 1) : mk(0, 0);
     const cplx ur = i < nx - 1 ? load_u(u, P.dtype, t + 1) : mk(0, 0);
@@ -387,58 +382,56 @@ __global__ void k_residual(ResParams P, const void* __restrict__ u, const void* 
     const cplx un = j < ny - 1 ? load_u(u, P.dtype, t + nx) : mk(0, 0);
     const cplx ub = k > 0 ? load_u(u, P.dtype, t - plane) : mk(0, 0);
     const cplx ut = k < nz - 1 ? load_u(u, P.dtype, t + plane) : mk(0, 0);
-    const cplx hx0 = ld(TAB + P.hx + i), hx1 = ld(TAB + P.hx + i + 1);
-    const cplx hy0 = ld(TAB + P.hy + j), hy1 = ld(TAB + P.hy + j + 1);
-    const cplx hz0 = ld(TAB + P.hz + k), hz1 = ld(TAB + P.hz + k + 1);
     const cplx cx = ld(TAB + P.hhx + i), cy = ld(TAB + P.hhy + j), cz = ld(TAB + P.hhz + k);
-    const cplx sg = ld(TAB + P.sig + k), se0 = ld(TAB + P.sige + k), se1 = ld(TAB + P.sige + k + 1);
+    const cplx sg = ld(TAB + P.sig + k);
     const cplx lam = mk(P.lam.x, P.lam.y);
-    cplx fv = P.has_f ? load_f(f, P.dtype, t) : mk(0, 0);
+    const cplx fv = P.has_f ? load_f(f, P.dtype, t) : mk(0, 0);
+    const cplx V = cx * cy * cz;
     cplx res, bnorm;
     if (!P.dd) {
+      const cplx hx0 = ld(TAB + P.hx + i), hx1 = ld(TAB + P.hx + i + 1);
+      const cplx hy0 = ld(TAB + P.hy + j), hy1 = ld(TAB + P.hy + j + 1);
+      const cplx hz0 = ld(TAB + P.hz + k), hz1 = ld(TAB + P.hz + k + 1);
+      const cplx se0 = ld(TAB + P.sige + k), se1 = ld(TAB + P.sige + k + 1);
       cplx tx = (ur - uc) * cinv(hx1) - (uc - ul) * cinv(hx0);
       cplx ty = (un - uc) * cinv(hy1) - (uc - us) * cinv(hy0);
       cplx tz = se1 * (ut - uc) * cinv(hz1) - se0 * (uc - ub) * cinv(hz0);
-      cplx Au = sg * tx * cy * cz + sg * ty * cx * cz + tz * cx * cy + lam * uc * cx * cy * cz;
-      cplx b = fv * cx * cy * cz;
+      cplx Au = sg * tx * cy * cz + sg * ty * cx * cz + tz * cx * cy + lam * uc * V;
+      cplx b = fv * V;
       res = b - Au;
       bnorm = b;
-      if (P.to_f) res = res * cinv(cx * cy * cz);
+      if (P.to_f) res = res * cinv(V);
     } else {
-      // every product and sum in double-double, rounded once at the end
-      const zdd Uc = zfrom(uc);
-      // stencil coefficients from the plan's double-double tables (no reciprocals per point)
-      auto tdd = [&](int64_t off, int t) {
-        const double2 a = __ldg(TAB + off + 2 * t), b = __ldg(TAB + off + 2 * t + 1);
+      auto tdd = [&](int64_t off, int n, int e) {  // node table: [n][cl, cr], 2 slots each
+        const double2 a = __ldg(TAB + off + 4 * n + 2 * e), b = __ldg(TAB + off + 4 * n + 2 * e + 1);
         return zdd{dd{a.x, a.y}, dd{b.x, b.y}};
       };
-      zdd tx = zsub(zmul(zsub(zfrom(ur), Uc), tdd(P.rxd, i + 1)), zmul(zsub(Uc, zfrom(ul)), tdd(P.rxd, i)));
-      zdd ty = zsub(zmul(zsub(zfrom(un), Uc), tdd(P.ryd, j + 1)), zmul(zsub(Uc, zfrom(us)), tdd(P.ryd, j)));
-      zdd tz = zsub(zmul(zsub(zfrom(ut), Uc), tdd(P.szd, k + 1)), zmul(zsub(Uc, zfrom(ub)), tdd(P.szd, k)));
-      // control volumes (h_{i-1}+h_i)/2 exactly in dd
-      zdd Cx = zmul(zadd(zfrom(hx0), zfrom(hx1)), zdd{dd{0.5, 0}, dd{0, 0}});
-      zdd Cy = zmul(zadd(zfrom(hy0), zfrom(hy1)), zdd{dd{0.5, 0}, dd{0, 0}});
-      zdd Cz = zmul(zadd(zfrom(hz0), zfrom(hz1)), zdd{dd{0.5, 0}, dd{0, 0}});
-      zdd S = zfrom(sg);
-      zdd Au = zmul(zmul(S, tx), zmul(Cy, Cz));
-      Au = zadd(Au, zmul(zmul(S, ty), zmul(Cx, Cz)));
-      Au = zadd(Au, zmul(tz, zmul(Cx, Cy)));
-      zdd V = zmul(Cx, zmul(Cy, Cz));
-      Au = zadd(Au, zmul(zmul(zfrom(lam), Uc), V));
-      zdd b = zmul(zfrom(fv), V);
-      zdd rr = zsub(b, Au);
-      res = mk(rr.x.hi + rr.x.lo, rr.y.hi + rr.y.lo);
-      bnorm = mk(b.x.hi, b.y.hi);
-      if (P.to_f) res = res * cinv(cx * cy * cz);
+      const zdd Uc = zfrom(uc);
+      zdd h = zsub(zmul(zsub(zfrom(ur), Uc), tdd(P.rxd, i, 1)), zmul(zsub(Uc, zfrom(ul)), tdd(P.rxd, i, 0)));
+      h = zadd(h, zsub(zmul(zsub(zfrom(un), Uc), tdd(P.ryd, j, 1)), zmul(zsub(Uc, zfrom(us)), tdd(P.ryd, j, 0))));
+      zdd Lu = zmul_zd(h, sg);
+      Lu = zadd(Lu, zsub(zmul(zsub(zfrom(ut), Uc), tdd(P.szd, k, 1)), zmul(zsub(Uc, zfrom(ub)), tdd(P.szd, k, 0))));
+      Lu = zadd(Lu, zmul_zd(zfrom(uc), lam));
+      const zdd rf = zsub(zfrom(fv), Lu);
+      const cplx rfc = mk(rf.x.hi + rf.x.lo, rf.y.hi + rf.y.lo);
+      res = P.to_f ? rfc : rfc * V;
+      bnorm = fv * V;
     }
     if (rout) rout[t] = make_double2(res.x, res.y);
-    if (norms) {
-      cplx rb = P.to_f ? res * (cx * cy * cz) : res;
-      acc_r += rb.x * rb.x + rb.y * rb.y;
-      acc_b += bnorm.x * bnorm.x + bnorm.y * bnorm.y;
-    }
+    const cplx rb = P.to_f ? res * V : res;
+    acc_r = rb.x * rb.x + rb.y * rb.y;
+    acc_b = bnorm.x * bnorm.x + bnorm.y * bnorm.y;
   }
-  flush(rcur);
+  if (norms) {  // warp sums, one atomic pair per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc_r += __shfl_xor_sync(0xffffffffu, acc_r, o);
+      acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(norms + 2 * r, acc_r);
+      atomicAdd(norms + 2 * r + 1, acc_b);
+    }
   }
 }
 
@@ -448,10 +441,9 @@ cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int ddm, i
                             double* d_norms, const Bufs& bufs, cudaStream_t st) {
   ResParams P{nx, ny, nz, R, dtype, ddm, has_f, to_f_units, hx, hy, hz, hhx, hhy, hhz, sig, sige, lam,
               ddtabs[0], ddtabs[1], ddtabs[2]};
-  int64_t total = (int64_t)nx * ny * nz * R;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  k_residual<<<(unsigned)blocks, 256, 0, st>>>(P, u, f, r, d_norms, bufs);
+  if ((int64_t)nz * R > 65535 || ny > 65535) return cudaErrorInvalidValue;
+  k_residual<<<dim3((unsigned)((nx + 127) / 128), (unsigned)ny, (unsigned)(nz * R)), 128, 0, st>>>(P, u, f, r, d_norms,
+                                                                                                    bufs);
   return cudaGetLastError();
 }
 
