@@ -95,8 +95,9 @@ size_t lfds_workspace_bytes(const lfds_plan* plan, int nrhs);
  * Solve A u = M f for nrhs right-hand sides on `cuda_stream` (a cudaStream_t; NULL =
  * legacy default stream).  f_dev, u_dev: device pointers, [nrhs][nz][ny][nx], 16-byte
  * aligned; u may alias f.  ws_dev: caller-owned device workspace of >= lfds_workspace_bytes.
- * Stream-ordered: the call returns after enqueueing, except when refinement is on (it
- * reads the residual norm back, which synchronises the stream).  The caller owns f, u, ws.
+ * Stream-ordered: the call returns after enqueueing, except in automatic refinement
+ * (refine = -1), which reads residual norms back and so synchronises the stream.  The caller
+ * owns f, u, ws.
  */
 int lfds_solve(lfds_plan* plan, const void* f_dev, void* u_dev, int nrhs,
                void* ws_dev, size_t ws_bytes, void* cuda_stream);
@@ -151,7 +152,8 @@ int lfds_solve_phase(lfds_plan* plan, int phase, const void* f_dev, void* u_dev,
 
 typedef struct {
   int passes;                  /* solve passes in the last lfds_solve (1 + refinements)     */
-  double rel_residual[9];      /* ||Au-Mf||/||Mf|| after each pass (max over rhs), if known */
+  double rel_residual[9];      /* refine = -1 (auto): ||Au-Mf||/||Mf|| before each refinement    */
+                               /* pass and after the last (max over rhs); -1 = not read back     */
   double min_pivot_ratio;      /* min |pivot| / row-norm over all z-sweeps of the last call  */
   int n_kernel_launches;       /* kernels enqueued by the last lfds_solve                   */
 } lfds_report;

@@ -992,19 +992,28 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
       double prev = 1e300;
       const int maxref = P->opt.refine < 0 ? 8 : P->opt.refine;
       for (int it = 0; it <= maxref; ++it) {
-        CUDA_TRY(cudaMemsetAsync(norms, 0, sizeof(double) * 2 * Rc, st));
+        // a fixed pass count needs no residual after the last correction (auto mode does: it
+        // decides whether to continue from it)
+        if (it == maxref && P->opt.refine > 0) break;
+        // auto mode reads the residual norms back (it decides on them, which synchronises the
+        // stream); a fixed pass count stays asynchronous
+        const bool auto_mode = P->opt.refine < 0;
+        if (auto_mode) CUDA_TRY(cudaMemsetAsync(norms, 0, sizeof(double) * 2 * Rc, st));
         cudaEvent_t ra = nullptr;
         if (P->opt.profile) { ra = P->prof.get(); cudaEventRecord(ra, st); }
         CUDA_TRY(launch_residual(X.N, Y.N, P->nz, Rc, dt, P->opt.residual_dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff,
                                  Y.hhoff, P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()),
-                                 P->t_dd, b.p[B_U], b.p[B_F], res, 1, norms, b, st));
+                                 P->t_dd, b.p[B_U], b.p[B_F], res, 1, auto_mode ? norms : nullptr, b, st));
         P->launches++;
         if (P->opt.profile) { cudaEvent_t rb2 = P->prof.get(); cudaEventRecord(rb2, st); P->prof.recs.push_back({ST_RESID, 1, ra, rb2}); }
-        std::vector<double> hn(2 * Rc);
-        CUDA_TRY(cudaMemcpyAsync(hn.data(), norms, sizeof(double) * 2 * Rc, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        double worst = 0;
-        for (int r = 0; r < Rc; ++r) worst = std::max(worst, hn[2 * r + 1] > 0 ? std::sqrt(hn[2 * r] / hn[2 * r + 1]) : 0.0);
+        double worst = -1.0;
+        if (auto_mode) {
+          std::vector<double> hn(2 * Rc);
+          CUDA_TRY(cudaMemcpyAsync(hn.data(), norms, sizeof(double) * 2 * Rc, cudaMemcpyDeviceToHost, st));
+          CUDA_TRY(cudaStreamSynchronize(st));
+          worst = 0;
+          for (int r = 0; r < Rc; ++r) worst = std::max(worst, hn[2 * r + 1] > 0 ? std::sqrt(hn[2 * r] / hn[2 * r + 1]) : 0.0);
+        }
         if (it < 9) maxres[it] = std::max(maxres[it], worst);
         if (it == maxref) break;
         if (P->opt.refine < 0 && (worst <= P->opt.refine_tol || worst > 0.5 * prev)) break;
@@ -1022,7 +1031,7 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
       }
     }
     passes_done = std::max(passes_done, passes);
-    if (P->opt.refine != 0) {  // the stream is already synchronised by the refinement loop
+    if (P->opt.refine < 0) {  // the stream is already synchronised by the refinement loop
       double mp = 1.0;
       CUDA_TRY(cudaMemcpyAsync(&mp, red, sizeof(double), cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
