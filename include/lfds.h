@@ -59,9 +59,12 @@ typedef struct {
   int device;       /* CUDA device ordinal; <0 = host-only plan (setup/basis queries only) */
   int rhs_chunk;    /* max right-hand sides processed per pipeline pass (0 = all)          */
   int profile;      /* 1: record CUDA events around every stage on the solve stream        */
+  int s5_modal;     /* 1: step 5 with the z direction diagonalised too, when the z tables  */
+                    /* are real (interface-only computation, no z sweeps);  */
+                    /* 0: per-mode tridiagonal z-sweeps (the paper's form)   */
 } lfds_options;
 
-/* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0. */
+/* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1. */
 void lfds_default_options(lfds_options* opt);
 
 /*
@@ -76,7 +79,8 @@ void lfds_default_options(lfds_options* opt);
  *  sigma_edge[nz+1]              host, sigma_{k+1/2} for k = 0..nz (Re > 0).
  *  lambda                        the shift of Eq. (wave2) (complex accepted, reading R11).
  *  if_x[n_if_x], if_y[n_if_y]    host, sorted 1-based interface nodes (width-1 planes,
- *                                reading R9); 2 <= node <= N-1, consecutive nodes >= 2 apart.
+ *                                reading R9); 2 <= node <= N-1, consecutive nodes >= 2 apart,
+ *                                at most 16 per axis (17 blocks).
  *                                n_if = 0 gives a single block (the global separable solve).
  *  opt                           may be NULL (defaults).
  *  *out                          receives the plan; release with lfds_destroy.
@@ -168,6 +172,9 @@ typedef struct {
   double eig_max_residual;     /* max over all bases of ||AW-MWL||/(||A|| ||W||)              */
   double eig_max_biorth;       /* max over all bases of ||W^T M W - I||_max                   */
   size_t device_table_bytes;
+  int s5_modal;                /* 1 if step 5 runs in the z-modal form (options.s5_modal, real z) */
+  double z_eig_residual;       /* z modal basis: max|A'z - theta E z| / (||A'|| max|Z|)       */
+  double z_eig_orth;           /* z modal basis: max|Z^T E Z - I|                             */
 } lfds_info;
 int lfds_get_info(const lfds_plan* plan, lfds_info* info);
 

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "liblfds.so")
-SOURCES = ["lfds_kernels.cu", "lfds_zsolve.cu", "lfds_proj.cu", "lfds_xform.cu", "lfds_dst.cu", "lfds_host.cpp", "lfds_eig.cpp"]
+SOURCES = ["lfds_kernels.cu", "lfds_zsolve.cu", "lfds_proj.cu", "lfds_xform.cu", "lfds_dst.cu", "lfds_modal.cu", "lfds_host.cpp", "lfds_eig.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-cudart", "static", "--expt-relaxed-constexpr"]
@@ -29,14 +29,16 @@ def build(force=False, verbose=False):
     if not force and not needs_build():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    objs = []
-    for s in SOURCES:
-        o = os.path.join(HERE, "_lib", s + ".o")
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(SRC, s), "-o", o]
-        if verbose:
+    objs = [os.path.join(HERE, "_lib", s + ".o") for s in SOURCES]
+    cmds = [[NVCC] + FLAGS + ["-c", os.path.join(SRC, s), "-o", o] for s, o in zip(SOURCES, objs)]
+    if verbose:
+        for cmd in cmds:
             print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
-        objs.append(o)
+    # translation units compile in parallel (one nvcc process each)
+    procs = [subprocess.Popen(cmd) for cmd in cmds]
+    codes = [p.wait() for p in procs]
+    if any(codes):
+        raise subprocess.CalledProcessError(next(c for c in codes if c), "nvcc")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-o", OUT] + objs
     if verbose:

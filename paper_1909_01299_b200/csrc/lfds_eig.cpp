@@ -409,4 +409,119 @@ bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err) {
   return true;
 }
 
+
+// ---------------------------------------------------------------------------------------
+// z-direction modal basis for step 5 (build design): the global z-systems of
+// PAPER.md:56 are T(s) = A' + s E with A' = tridiag(a, g, c) real symmetric (a_k = c_{k-1})
+// and E = diag(e) > 0 (e_k = sigma_k hz^_k, reading R1).  With A' Z = E Z Theta and
+// Z^T E Z = I, T(s)^{-1} = Z (Theta + s)^{-1} Z^T.  S = E^{-1/2} A' E^{-1/2} is real symmetric
+// tridiagonal; its eigenpairs come from the implicit QL iteration with Wilkinson shifts and
+// accumulated plane rotations (orthogonal to working precision), in long double.
+static bool ql_real_vectors(std::vector<long double>& d, std::vector<long double> e, std::vector<long double>& V) {
+  const int n = (int)d.size();
+  e.resize(n, 0.0L);  // e[i] couples i and i+1; e[n-1] = 0
+  V.assign((size_t)n * n, 0.0L);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0L;  // V[row * n + col]
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const long double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= LDBL_EPSILON * dd) break;
+      }
+      if (m == l) break;
+      if (++iter > 80) return false;
+      // shift from the leading 2x2 block (eigenvalue closer to d[l])
+      long double g = (d[l + 1] - d[l]) / (2.0L * e[l]);
+      long double r = std::hypot(g, 1.0L);
+      g = d[m] - d[l] + e[l] / (g + (g >= 0 ? r : -r));
+      long double s = 1.0L, c = 1.0L, p = 0.0L;
+      int i;
+      bool deflated = false;
+      for (i = m - 1; i >= l; --i) {
+        long double f = s * e[i];
+        const long double b = c * e[i];
+        r = std::hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0L) {  // underflow: split the matrix here
+          d[i + 1] -= p;
+          e[m] = 0.0L;
+          deflated = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * s + 2.0L * c * b;
+        p = s * r;
+        d[i + 1] = g + p;
+        g = c * r - b;
+        for (int k = 0; k < n; ++k) {  // accumulate the rotation on columns i, i+1
+          f = V[(size_t)k * n + i + 1];
+          V[(size_t)k * n + i + 1] = s * V[(size_t)k * n + i] + c * f;
+          V[(size_t)k * n + i] = c * V[(size_t)k * n + i] - s * f;
+        }
+      }
+      if (deflated) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[m] = 0.0L;
+    } while (m != l);
+  }
+  return true;
+}
+
+bool z_modal_basis(const std::vector<double>& a, const std::vector<double>& g, const std::vector<double>& c,
+                   const std::vector<double>& e, std::vector<double>& theta, std::vector<double>& Z,
+                   double& residual, double& orth, std::string& err) {
+  const int n = (int)g.size();
+  if (n < 1) { err = "empty z pencil"; return false; }
+  std::vector<long double> sq(n), d(n), off(n > 1 ? n - 1 : 0), V;
+  for (int k = 0; k < n; ++k) {
+    if (!(e[k] > 0)) { err = "z mass not positive"; return false; }
+    sq[k] = std::sqrt((long double)e[k]);
+    d[k] = (long double)g[k] / (long double)e[k];
+  }
+  for (int k = 0; k + 1 < n; ++k) {
+    if (c[k] != a[k + 1]) { err = "z operator not symmetric"; return false; }
+    off[k] = (long double)c[k] / (sq[k] * sq[k + 1]);
+  }
+  if (!ql_real_vectors(d, off, V)) { err = "QL iteration did not converge (z pencil)"; return false; }
+  std::vector<int> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int p, int q) { return d[p] < d[q]; });
+  theta.assign(n, 0.0);
+  Z.assign((size_t)n * n, 0.0);  // Z[k * n + t]
+  std::vector<long double> ZL((size_t)n * n);
+  for (int t = 0; t < n; ++t) {
+    theta[t] = (double)d[idx[t]];
+    for (int k = 0; k < n; ++k) {
+      ZL[(size_t)k * n + t] = V[(size_t)k * n + idx[t]] / sq[k];
+      Z[(size_t)k * n + t] = (double)ZL[(size_t)k * n + t];
+    }
+  }
+  // diagnostics on the rounded (double) basis: pencil residual and E-orthonormality
+  long double anorm = 0, res = 0, orr = 0, zmax = 0;
+  for (int k = 0; k < n; ++k)
+    anorm = std::max(anorm, std::fabs((long double)a[k]) + std::fabs((long double)g[k]) + std::fabs((long double)c[k]));
+  for (auto v : Z) zmax = std::max(zmax, std::fabs((long double)v));
+  for (int t = 0; t < n; ++t)
+    for (int k = 0; k < n; ++k) {
+      long double az = (long double)g[k] * Z[(size_t)k * n + t];
+      if (k > 0) az += (long double)a[k] * Z[(size_t)(k - 1) * n + t];
+      if (k + 1 < n) az += (long double)c[k] * Z[(size_t)(k + 1) * n + t];
+      res = std::max(res, std::fabs(az - (long double)theta[t] * e[k] * Z[(size_t)k * n + t]));
+    }
+  for (int t1 = 0; t1 < n; ++t1)
+    for (int t2 = t1; t2 < n; ++t2) {
+      long double acc = 0;
+      for (int k = 0; k < n; ++k) acc += (long double)Z[(size_t)k * n + t1] * e[k] * Z[(size_t)k * n + t2];
+      if (t1 == t2) acc -= 1;
+      orr = std::max(orr, std::fabs(acc));
+    }
+  residual = (double)(res / (anorm * (zmax > 0 ? zmax : 1)));
+  orth = (double)orr;
+  return true;
+}
+
 }  // namespace lfds

@@ -20,4 +20,12 @@ struct Basis {
 // Eigenbasis of the Dirichlet pencil of the N+1 steps h (N interior nodes).
 bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err);
 
+// z modal basis for step 5 (real z tables only): A' Z = E Z diag(theta), Z^T E Z = I, with
+// A' = tridiag(a, g, c) (a[k] couples k-1, c[k] couples k+1; a[k+1] == c[k]) and E = diag(e).
+// Z is row-major Z[k * n + t]; theta ascending.  residual = max |A'z - theta E z| /
+// (||A'||_inf max|Z|), orth = max |Z^T E Z - I|.
+bool z_modal_basis(const std::vector<double>& a, const std::vector<double>& g, const std::vector<double>& c,
+                   const std::vector<double>& e, std::vector<double>& theta, std::vector<double>& Z,
+                   double& residual, double& orth, std::string& err);
+
 }  // namespace lfds

@@ -103,6 +103,9 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   int* d_own = nullptr;      // per-block ownership flags (step-4 partial residual)
   int n_pd3 = 0;
   StageDescs s1x, s1y, s3x, s3y, s5r1, s5wx, s6f, s7y, s7x;  // s5r1: R1 and R2; s5wx: WX and WY
+  StageDescs s5zf, s5zi;     // z-modal step 5: R~ = Z^T R (R1, R2) and P = Z P~ (P1, P2), real S
+  bool s5m = false;          // step 5 in z-modal form (lfds_modal.cu)
+  int64_t r1t = 0, r2t = 0, p1t = 0, p2t = 0, p2p = 0;
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
   std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
   bool use_xform = false;
@@ -129,6 +132,10 @@ struct lfds_plan {
   size_t tab_elems = 0;
   ZTab zt_scaled{}, zt_plain{}, zt_lift{};  // zt_lift: zt_scaled rows divided by -sigma_k (step 6)
   std::map<int, int64_t> t_tw;  // FFT twiddle tables per length L
+  // step-5 z-modal form (real z tables): Z^T (t x k) and Z (k x t) as real tables (offsets in
+  // doubles), theta_t (complex slots)
+  bool s5m = false;
+  int64_t t_zt = 0, t_zf = 0, t_theta = 0;
   int64_t t_dd[3] = {0, 0, 0};  // double-double stencil tables (x, y, z) for the residual
   int64_t t_hz = 0, t_hhz = 0, t_sig = 0, t_sige = 0, t_ifx = 0, t_ify = 0, t_bx = 0, t_by = 0, t_xlo = 0, t_ylo = 0;
   std::map<std::tuple<int, int, int>, PassPlan> passes;
@@ -225,6 +232,14 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   pp.wx = o; o += align4((int64_t)nifx * R * Nz * Ny);
   pp.wy = o; o += align4((int64_t)nify * R * Nz * Nx);
   pp.gf = o; o += align4((int64_t)nblk * 4 * R * P->fpad * Nz);
+  pp.s5m = P->s5m && !in_real && !out_real && s5m_ka(nifx, nify) > 0;
+  if (pp.s5m) {
+    pp.r1t = o; o += align4((int64_t)nifx * R * Nz * Ny);
+    pp.r2t = o; o += align4((int64_t)nify * R * Nz * Nx);
+    pp.p1t = o; o += align4((int64_t)nifx * R * Nz * Ny);
+    pp.p2t = o; o += align4((int64_t)nify * R * Nz * Nx);
+    pp.p2p = o; o += align4((int64_t)nify * R * Nz * s5m_mtiles(Ny) * Nx);
+  }
   const int64_t if_elems = o;
   size_t off = 0;
   pp.off_ms = off; off = al256(off + ms_elems * 16);
@@ -307,6 +322,18 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, 1, Ny, 0, B_IF, pp.wx, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
   if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, 1, Nx, 0, B_IF, pp.wy, 1, Nx, 0, (int)(nify * RZ), 1, 0));
   stage(pp.s5wx, std::move(v)); v.clear();
+  if (pp.s5m) {  // z-modal step 5: R~[a][r][t][m] = sum_k Z[k][t] R[a][r][k][m]; P = Z P~ (real Z)
+    if (nifx) v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r1, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.r1t, Ny,
+                             (int64_t)Nz * Ny, 1, nifx * R, Ny, 0));
+    if (nify) v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r2, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.r2t, Nx,
+                             (int64_t)Nz * Nx, 1, nify * R, Nx, 0));
+    stage(pp.s5zf, std::move(v)); v.clear();
+    if (nifx) v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p1t, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.p1, Ny,
+                             (int64_t)Nz * Ny, 1, nifx * R, Ny, 0));
+    if (nify) v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p2t, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.p2, Nx,
+                             (int64_t)Nz * Nx, 1, nify * R, Nx, 0));
+    stage(pp.s5zi, std::move(v)); v.clear();
+  }
   // step 6: face transforms GF[b][face][rk][mode] (faces L, R, B, T), e.g. GL = F_y w_L
   std::vector<ZBlock> zb;  // owned blocks (k_zs1, k_zs2), then the global 'block' (k_zs3)
   for (int j = 0; j < nby; ++j)
@@ -591,7 +618,26 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     end();
   }
   }
-  if ((phases & PH_2) && has_if) {
+  if ((phases & PH_2) && has_if && pp.s5m) {
+    // step 5, z-modal form: plane transforms (W_y^T, W_x^T), z-modes (Z^T), the modal solve
+    // projected onto the planes, back to z (Z) -> exchange 2 = [P1, P2]
+    if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
+    begin(ST_GFWD);
+    CUDA_TRY(launch_xform(pp.d_descs + pp.s5zf.off, pp.s5zf.n, pp.s5zf.maxM, pp.s5zf.maxN, true, false, bufs, st));
+    P->launches += 1;
+    end(); begin(ST_GSWEEP);
+    S5M S{};
+    S.nx = Nx; S.ny = Ny; S.nz = Nz; S.R = R; S.nifx = nifx; S.nify = nify;
+    S.l_begin = l_begin; S.l_end = l_end; S.nmt = s5m_mtiles(Ny);
+    S.lamx = X.lamg; S.lamy = Y.lamg; S.theta = P->t_theta; S.wxi = X.WI; S.wyi = Y.WI;
+    S.r1t = pp.r1t; S.r2t = pp.r2t; S.p1t = pp.p1t; S.p2p = pp.p2p; S.p2t = pp.p2t;
+    CUDA_TRY(launch_s5m(S, bufs, st));
+    P->launches += nify ? 2 : 1;
+    end(); begin(ST_GPROJ);
+    CUDA_TRY(launch_xform(pp.d_descs + pp.s5zi.off, pp.s5zi.n, pp.s5zi.maxM, pp.s5zi.maxN, true, false, bufs, st));
+    P->launches += 1;
+    end();
+  } else if ((phases & PH_2) && has_if) {
     // step 5
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     begin(ST_GSWEEP);
@@ -670,6 +716,7 @@ void lfds_default_options(lfds_options* o) {
   o->device = 0;
   o->rhs_chunk = 0;
   o->profile = 0;
+  o->s5_modal = 1;
 }
 
 int lfds_stage_count(void) { return ST_COUNT; }
@@ -709,6 +756,8 @@ static int setup_axis(Axis& A, int N, const lfds_z* h, int nif, const int* iface
   A.hh.resize(N);
   for (int i = 0; i < N; ++i) A.hh[i] = 0.5 * (A.h[i] + A.h[i + 1]);
   A.iface.assign(iface, iface + nif);
+  // step 5 contracts over the interface planes on the tensor pipe with |I| padded to 8 or 16
+  if (nif > 16) return fail(LFDS_EINVAL, "%s: at most 16 interfaces (17 blocks) per axis, got %d", name, nif);
   for (int a = 0; a < nif; ++a) {
     int v = A.iface[a];
     if (v < 2 || v > N - 1) return fail(LFDS_EINVAL, "%s: interface node %d outside 2..N-1", name, v);
@@ -851,6 +900,30 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
       if (z->imag() != 0) P->real_z = false;
   }
   P->zt_plain = ZTab{T.put(za), T.put(zg), T.put(zcv), T.put(ze)};
+  if (P->opt.s5_modal && P->real_z && (!X.iface.empty() || !Y.iface.empty())) {
+    // z modal basis of the step-5 systems T(s) = A' + s E (A' = tridiag(za, zg, zcv), E = diag(ze))
+    std::vector<double> a(nz), g(nz), c(nz), e(nz), theta, Z;
+    for (int k = 0; k < nz; ++k) { a[k] = za[k].real(); g[k] = zg[k].real(); c[k] = zcv[k].real(); e[k] = ze[k].real(); }
+    double zres = 0, zorth = 0;
+    std::string zerr;
+    if (!z_modal_basis(a, g, c, e, theta, Z, zres, zorth, zerr))
+      return fail(LFDS_EEIG, "z modal basis: %s", zerr.c_str());
+    if (!(zres < 1e-12) || !(zorth < 1e-12))
+      return fail(LFDS_EEIG, "z modal basis: residual %.3g, orthonormality %.3g", zres, zorth);
+    std::vector<zc> zt((size_t)nz * nz), zf((size_t)nz * nz), th(nz);
+    for (int k = 0; k < nz; ++k)
+      for (int t = 0; t < nz; ++t) {
+        zf[(size_t)k * nz + t] = Z[(size_t)k * nz + t];
+        zt[(size_t)t * nz + k] = Z[(size_t)k * nz + t];
+      }
+    for (int t = 0; t < nz; ++t) th[t] = theta[t];
+    P->t_zt = T.put_real(zt);
+    P->t_zf = T.put_real(zf);
+    P->t_theta = T.put(th);
+    P->s5m = true;
+    P->info.z_eig_residual = zres;
+    P->info.z_eig_orth = zorth;
+  }
   P->zt_scaled = ZTab{T.put(sa), T.put(sg), T.put(scv), T.put(se)};
   {  // step-6 lifting RHS is -sigma_k (sum of face terms): fold -sigma_k into the rows
     std::vector<zc> la(nz), lg(nz), lc(nz), le(nz);
@@ -926,6 +999,7 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
   I.eig_max_residual = mres;
   I.eig_max_biorth = mbio;
   I.device_table_bytes = T.v.size() * sizeof(double2);
+  I.s5_modal = P->s5m ? 1 : 0;
   *out = P.release();
   return LFDS_OK;
 }

@@ -105,6 +105,20 @@ struct ProjM {
   int64_t h_off, h_es, h_ps;
 };
 int projm_chunks(int nx);
+
+// Step 5 in z-modal form (lfds_modal.cu): P1~, P2~ from R1~, R2~ for every z-mode t.
+struct S5M {
+  int nx, ny, nz, R, nifx, nify;
+  int l_begin, l_end;          // this rank's global x-modes
+  int nmt;                     // m-tiles (P2 partials)
+  int64_t lamx, lamy, theta;   // TAB: lambda_l (nx), mu_m (ny), theta_t (nz), complex
+  int64_t wxi, wyi;            // TAB: W_x[I_a][l] (nifx x nx), W_y[I_b][m] (nify x ny)
+  int64_t r1t, r2t;            // IF: R1~[a][r][t][m], R2~[b][r][t][l]
+  int64_t p1t, p2p, p2t;       // IF: P1~[a][r][t][m], P2 partials [b][r][t][mt][l], P2~[b][r][t][l]
+};
+int s5m_ka(int nifx, int nify);   // padded |I| (8 or 16), 0 = unsupported
+int s5m_mtiles(int ny);
+cudaError_t launch_s5m(const S5M& S, const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_projm(const ProjM& P, const Bufs& bufs, cudaStream_t st);
 
 // launchers (lfds_kernels.cu); return cudaGetLastError()

@@ -289,3 +289,35 @@ def test_block_sharded_solve_matches_single_device(name, world):
     # every block is computed by exactly one rank
     owners = dist.shard(Plan.from_problem(p), 0, world)["owner"]
     assert set(np.unique(owners)) <= set(range(world))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "c4j"])
+def test_step5_modal_matches_sweeps(name):
+    """Step 5 in z-modal form (z diagonalised as well; interface-only) against the
+    per-mode tridiagonal z-sweeps of PAPER.md:56 and the oracle: the same u."""
+    p = shrunken(name, nrhs=1)
+    F = p.rhs_all()
+    pm, Um = gpu_solve(p, F)
+    ps, Us = gpu_solve(p, F, s5_modal=False)
+    assert pm.info()["s5_modal"] == 1 and ps.info()["s5_modal"] == 0
+    assert rel(Um, Us) < 1e-11, rel(Um, Us)
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
+    assert rel(Um[0], ref) < TOL
+
+
+@pytest.mark.parametrize("nifx,nify", [(12, 9), (16, 3), (0, 11), (3, 16)])
+def test_step5_modal_interface_counts(nifx, nify):
+    """|I| padded to 8 and 16 on the tensor pipe, one axis without interfaces; ragged m- and
+    l-tiles (N = 70, 90)."""
+    nx, ny, nz = 70, 90, 11
+    rng = np.random.default_rng(nifx * 100 + nify)
+    hx = np.ones(nx + 1) + 0.4j * (np.arange(nx + 1) < 6)
+    hy = rng.uniform(0.8, 1.2, ny + 1)
+    ix = [int(round((b + 1) * (nx + 1) / (nifx + 1))) for b in range(nifx)]
+    iy = [int(round((b + 1) * (ny + 1) / (nify + 1))) for b in range(nify)]
+    p = _steps_problem(hx, hy, nz, ix, iy, lam=0.35)
+    F = (rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape))
+    plan, U = gpu_solve(p, F)
+    assert plan.info()["s5_modal"] == 1
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
+    assert rel(U[0], ref) < TOL, rel(U[0], ref)

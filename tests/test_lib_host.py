@@ -3,6 +3,7 @@ validates its inputs, and its host eigensolver (setup) meet
 closed forms and the pencil invariants — compared with the oracle's independent LAPACK route.
 No compute call is made (host-only plans, options.device = -1)."""
 import ctypes
+import dataclasses
 import os
 import re
 
@@ -58,6 +59,7 @@ def test_host_only_plan_refuses_compute(lfds):
 
 
 @pytest.mark.parametrize("bad", [dict(iface_x=[5, 6]), dict(iface_x=[1]), dict(iface_x=[44]),
+                                 dict(iface_x=list(range(2, 38, 2))),  # 18 interfaces: more than 16
                                  dict(iface_x=[9, 4])])
 def test_setup_rejects_bad_partitions(lfds, bad):
     p = shrunken("c3")
@@ -151,3 +153,21 @@ def test_single_block_global_basis_equals_block_basis():
     lam_g, W_g, _, _ = plan.basis(0, -1)
     lam_b, W_b, _, _ = plan.basis(0, 0)
     assert np.array_equal(lam_g, lam_b) and np.array_equal(W_g, W_b)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_z_modal_basis_of_the_step5_pencil(name):
+    """Setup diagonalises the real step-5 z pencil T(s) = A' + s E (reading R1): A' Z = E Z Theta,
+    Z^T E Z = I (long-double implicit QL with accumulated rotations), checked on the rounded basis."""
+    info = host_plan(make_problem(name)).info()
+    assert info["real_z"] == 1 and info["s5_modal"] == 1
+    assert info["z_eig_residual"] < 1e-15 and info["z_eig_orth"] < 1e-14
+
+
+def test_z_modal_form_needs_real_z_tables():
+    """Complex sigma (or lambda) makes the z pencil complex symmetric: step 5 keeps the sweeps."""
+    p = shrunken("c2")
+    pc = dataclasses.replace(p, sigma_node=p.sigma_node * (1 + 0.1j), sigma_edge=p.sigma_edge * (1 + 0.1j))
+    assert host_plan(pc).info()["s5_modal"] == 0
+    assert host_plan(dataclasses.replace(p, lam=p.lam + 0.01j)).info()["s5_modal"] == 0
+    assert host_plan(p, s5_modal=False).info()["s5_modal"] == 0
