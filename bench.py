@@ -172,7 +172,8 @@ def stage_algorithmic(p, R: int, plan=None):
     MAC, a real one (R blocks) 4 (real matrix x complex data); each element moves 32 B.
     Sine stages (uniform blocks, FFT-based DST): HBM-bound, 32 B per element.
     z-solves: 32 B per unknown (read + write).  Step 5: the rank-|I| contraction costs
-    8 (|I_x| + |I_y|) flops per global unknown (RHS build and projection each)."""
+    8 (|I_x| + |I_y|) flops per global unknown (RHS build and projection each; both in k_s5m
+    in the z-modal form)."""
     def sizes(n, iface):
         cuts = [0] + list(iface) + [n + 1]
         return [cuts[i + 1] - cuts[i] - 1 for i in range(len(cuts) - 1)]
@@ -210,14 +211,19 @@ def stage_algorithmic(p, R: int, plan=None):
     nif = nifx + nify
     plane = 8.0 * (nifx * p.ny * p.ny + nify * p.nx * p.nx) * nz * R
     xd, yd = dense(kx, bx, 0), dense(ky, by, 1)
+    modal = bool(plan.info().get("s5_modal", 0)) if plan else False
+    # z-modal step 5: plane data to and from z-modes, real Z x complex data
+    # (4 nz flops per plane element); k_s5m: r^ (8 |I| flops) plus both projections (8 |I|)
+    # per global unknown
+    zpl = 4.0 * nz * (nifx * p.ny + nify * p.nx) * nz * R
     xs, ys = sine(kx, 0), sine(ky, 1)
     return {
         "step1_x_sine": xs, "step1_x_dense": xd, "step1_y_sine": ys, "step1_y_dense": yd,
         "step2_zsolve": (None, 32.0 * el_blk),
         "step3_edge_projection": (None, 16.0 * el_blk),
-        "step5_plane_forward": (plane, None),
-        "step5_global_zsolve": (8.0 * nif * el_all, 16.0 * el_all),
-        "step5_projection": (8.0 * nif * el_all, 16.0 * el_all),
+        "step5_plane_forward": ((plane + zpl) if modal else plane, None),
+        "step5_global_zsolve": (16.0 * nif * el_all, None) if modal else (8.0 * nif * el_all, 16.0 * el_all),
+        "step5_projection": (zpl, None) if modal else (8.0 * nif * el_all, 16.0 * el_all),
         "step5_plane_inverse": (plane, None),
         "step6_zsolve_lift": (None, 32.0 * el_blk),
         "step7_y_sine": ys, "step7_y_dense": yd, "step7_x_sine": xs, "step7_x_dense": xd,

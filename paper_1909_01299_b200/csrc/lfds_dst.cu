@@ -142,9 +142,8 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
   constexpr int L = R1 * R2, N = L / 2;
   constexpr int CPB = DST_THREADS / R2;      // columns per CTA
   constexpr int LDT = CPB + 1;               // tile row stride (complex)
-  constexpr int LDE = R2 + 1;                // exchange row stride
   extern __shared__ __align__(16) double2 dsm[];
-  // buffer: tile [N-1][LDT] (load, later output staging) aliased with exchange [CPB][R1][LDE]
+  // buffer: tile [N-1][LDT] (load, later output staging) aliased with exchange [R1][R2][CPB]
   double2* tile = dsm;
   double2* ex = dsm;
   __shared__ double2 twl[L];                 // W_L^j, j < L
@@ -182,7 +181,10 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
   }
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
-  const int col = tid / R2, t = tid % R2;
+  // thread -> (column, FFT lane t): the CPB columns of a warp are adjacent, so a warp's
+  // accesses at fixed t cover whole 128-byte rows, and its twiddles W_L^{t k1} are shared by
+  // the CPB lanes of each t (shared-memory broadcast)
+  const int col = tid % CPB, t = tid / CPB;
   // ---- step 1: thread n2 = t: R1-point FFT over n1 of y[R2 n1 + n2], twiddle W_L^{n2 k1}
   zc2 a[R1];
 #pragma unroll
@@ -205,11 +207,11 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
     a[k1] = zmul(a[k1], zc2{w.x, w.y});
   }
   __syncthreads();  // tile fully consumed
+  // exchange [k1][n2][col]: conflict-free writes (fixed k1) and reads (fixed n2)
 #pragma unroll
-  for (int k1 = 0; k1 < R1; ++k1) ex[(col * R1 + k1) * LDE + t] = make_double2(a[k1].x, a[k1].y);
+  for (int k1 = 0; k1 < R1; ++k1) ex[(k1 * R2 + t) * CPB + col] = make_double2(a[k1].x, a[k1].y);
   __syncthreads();
   // ---- step 3: rows k1 = t, t + R2, ...: R2-point FFT over n2 -> Y[k1 + R1 k2], keep k < N.
-  // The exchange is read completely before the output tile (aliased) is written.
   constexpr int RPT = (R1 + R2 - 1) / R2;  // rows per thread
   zc2 b[RPT][R2];
 #pragma unroll
@@ -218,14 +220,29 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
     if (k1 < R1) {
 #pragma unroll
       for (int n2 = 0; n2 < R2; ++n2) {
-        const double2 w = ex[(col * R1 + k1) * LDE + n2];
+        const double2 w = ex[(k1 * R2 + n2) * CPB + col];
         b[rr][n2] = zc2{w.x, w.y};
       }
       fft_reg<R2, L>(b[rr], twl);
     }
   }
-  __syncthreads();  // exchange consumed; reuse as output tile[c][col]
   const double half = 0.5 * D.scale;
+  if (D.sCi != 1) {  // strided output rows: store straight from registers (a warp writes whole rows)
+    const int64_t o = colC[col];
+#pragma unroll
+    for (int rr = 0; rr < RPT; ++rr) {
+      const int k1 = t + rr * R2;
+      if (k1 < R1 && o >= 0) {
+#pragma unroll
+        for (int k2 = 0; k2 < R2 / 2; ++k2) {
+          const int k = k1 + R1 * k2;
+          if (k >= 1 && k < N) C[o + (int64_t)(k - 1) * D.sCi] = make_double2(-half * b[rr][k2].y, half * b[rr][k2].x);
+        }
+      }
+    }
+    return;
+  }
+  __syncthreads();  // exchange consumed; reuse as output tile[c][col]
 #pragma unroll
   for (int rr = 0; rr < RPT; ++rr) {
     const int k1 = t + rr * R2;
@@ -238,18 +255,10 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict_
     }
   }
   __syncthreads();
-  if (D.sCi == 1) {  // output column contiguous
-    for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
-      const int cc = idx / n, c = idx - cc * n;
-      const int64_t o = colC[cc];
-      if (o >= 0) C[o + c] = tile[c * LDT + cc];
-    }
-  } else {
-    for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {
-      const int c = idx / CPB, cc = idx - c * CPB;
-      const int64_t o = colC[cc];
-      if (o >= 0) C[o + (int64_t)c * D.sCi] = tile[c * LDT + cc];
-    }
+  for (int idx = tid; idx < n * CPB; idx += DST_THREADS) {  // output column contiguous
+    const int cc = idx / n, c = idx - cc * n;
+    const int64_t o = colC[cc];
+    if (o >= 0) C[o + c] = tile[c * LDT + cc];
   }
 }
 
@@ -257,7 +266,7 @@ template <int R1, int R2, bool KC>
 cudaError_t dst_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
   constexpr int L = R1 * R2, N = L / 2, CPB = DST_THREADS / R2;
   const size_t tile = (size_t)(N - 1) * (CPB + 1) * sizeof(double2);
-  const size_t ex = (size_t)CPB * R1 * (R2 + 1) * sizeof(double2);
+  const size_t ex = (size_t)CPB * R1 * R2 * sizeof(double2);
   const size_t sm = tile > ex ? tile : ex;
   cudaError_t e = cudaFuncSetAttribute(k_dst<R1, R2, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

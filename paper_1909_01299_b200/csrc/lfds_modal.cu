@@ -49,6 +49,21 @@ __device__ __forceinline__ void cmma3(double (&t)[3][2], double2 a, double2 b) {
   dmma(t[1][0], t[1][1], a.y, b.y);
   dmma(t[2][0], t[2][1], a.x + a.y, b.x + b.y);
 }
+// 3M step with the A operand's (re, im, re + im) precomputed
+__device__ __forceinline__ void cmma3s(double (&t)[3][2], double3 a, double2 b) {
+  dmma(t[0][0], t[0][1], a.x, b.x);
+  dmma(t[1][0], t[1][1], a.y, b.y);
+  dmma(t[2][0], t[2][1], a.z, b.x + b.y);
+}
+// reciprocal from the MUFU.RCP64H seed and two Newton steps (full fp64 accuracy)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
 __device__ __forceinline__ double2 cres(const double (&t)[3][2], int h) {  // (re, im) of element h
   return make_double2(t[0][h] - t[1][h], t[2][h] - t[0][h] - t[1][h]);
 }
@@ -122,11 +137,12 @@ __global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
   cp_wait<1>();  // fixed operands
   __syncthreads();
   // A fragments of phase A for this warp's 8 rows m = 8 warp + g (fixed over the l loop)
-  double2 fa1[KA / 4], fa2[KA / 4];
+  double3 fa1[KA / 4], fa2[KA / 4];
 #pragma unroll
   for (int ks = 0; ks < KA / 4; ++ks) {
-    fa1[ks] = A1[(4 * ks + q) * LA + 8 * warp + g];
-    fa2[ks] = A2[(4 * ks + q) * LA + 8 * warp + g];
+    const double2 v1 = A1[(4 * ks + q) * LA + 8 * warp + g], v2 = A2[(4 * ks + q) * LA + 8 * warp + g];
+    fa1[ks] = make_double3(v1.x, v1.y, v1.x + v1.y);
+    fa2[ks] = make_double3(v2.x, v2.y, v2.x + v2.y);
   }
   const int mrow = 8 * warp + g, mglob = m0 + mrow;
   const bool mok = mglob < S.ny;
@@ -158,8 +174,8 @@ __global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
       for (int ks = 0; ks < KA / 4; ++ks)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
-          cmma3(c[nt], fa1[ks], bx[(4 * ks + q) * LW + 8 * nt + g]);
-          cmma3(c[nt], fa2[ks], b2[(4 * ks + q) * LW + 8 * nt + g]);
+          cmma3s(c[nt], fa1[ks], bx[(4 * ks + q) * LW + 8 * nt + g]);
+          cmma3s(c[nt], fa2[ks], b2[(4 * ks + q) * LW + 8 * nt + g]);
         }
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
@@ -168,7 +184,7 @@ __global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
           const int j = 8 * nt + 2 * q + h;
           const double2 cv = cres(c[nt], h), la = lm[j];
           const double dr = mu.x + la.x, di = mu.y + la.y;
-          const double inv = 1.0 / fma(dr, dr, di * di);
+          const double inv = fast_rcp(fma(dr, dr, di * di));
           double2 w = make_double2(fma(cv.x, dr, cv.y * di) * inv, fma(cv.y, dr, -cv.x * di) * inv);
           if (!mok || l0 + j >= l_end) w = make_double2(0, 0);
           Wt[mrow * LW + j] = w;
