@@ -190,27 +190,32 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
   }
   cp_wait<0>();
 
-  // ---- epilogue: thread holds C rows (wm + 8i + g), columns 2q, 2q+1 of each 8-wide tile
+  // ---- epilogue: thread holds C rows (wm + 8i + g), columns 2q, 2q+1 of each 8-wide tile.
+  // Columns outer, rows inner: a column's offset is stepped from the previous one (one 64-bit
+  // division per thread, not one per stored element).
   double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
-  auto store = [&](int i, int64_t n, double re, double im) {
-    if (i >= M || n >= N) return;
-    const int64_t n1 = n / N2, n2 = n - n1 * N2;
-    C[(int64_t)i * D.sCi + n1 * D.sC1 + n2 * D.sC2] = make_double2(re, im);
-  };
+  {
+    // columns in store order: real S -> wn + 4j + q (j < 8); complex S -> wn + 8j' + 2q + h
+    int64_t n = n0 + wn + (REAL_S ? q : 2 * q);
+    int64_t n1 = n / N2, n2 = n - n1 * N2;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = i0 + wm + 8 * i + g;
-    if (REAL_S) {
-      // real column 2*wn + 8j + 2q (+1) == complex column wn + 4j + q, (re, im)
+    for (int e = 0; e < 8; ++e) {
+      if (n < N) {
+        const int64_t off = n1 * D.sC1 + n2 * D.sC2;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) store(row, n0 + wn + 4 * j + q, acc[i][j][0], acc[i][j][1]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t col = n0 + wn + 8 * j + 2 * q;
-        store(row, col, acc[i][2 * j][0], acc[i][2 * j + 1][0]);
-        store(row, col + 1, acc[i][2 * j][1], acc[i][2 * j + 1][1]);
+        for (int i = 0; i < 4; ++i) {
+          const int row = i0 + wm + 8 * i + g;
+          if (row >= M) continue;
+          // real S: acc[i][e] = (re, im) of column e; complex S: re in acc[i][2j], im in acc[i][2j+1]
+          const double2 v = REAL_S ? make_double2(acc[i][e][0], acc[i][e][1])
+                                   : make_double2(acc[i][2 * (e >> 1)][e & 1], acc[i][2 * (e >> 1) + 1][e & 1]);
+          C[(int64_t)row * D.sCi + off] = v;
+        }
       }
+      const int step = REAL_S ? 4 : ((e & 1) ? 7 : 1);
+      n += step;
+      n2 += step;
+      while (n2 >= N2) { n2 -= N2; ++n1; }
     }
   }
 }
@@ -341,22 +346,29 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
   }
   cp_wait<0>();
   double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
+  // columns outer (wn + 8j + 2q + h, j < 2, h < 2; offsets stepped), rows inner
+  {
+    int64_t n = n0 + wn + 2 * q;
+    int64_t n1 = n / N2, n2 = n - n1 * N2;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = i0 + wm + 8 * i + g;
-    if (row >= M) continue;
+    for (int e = 0; e < 4; ++e) {
+      const int j = e >> 1, h = e & 1;
+      if (n < N) {
+        const int64_t off = n1 * D.sC1 + n2 * D.sC2;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t n = n0 + wn + 8 * j + 2 * q + h;
-        if (n < N) {
-          const int64_t n1 = n / N2, n2 = n - n1 * N2;
+        for (int i = 0; i < 4; ++i) {
+          const int row = i0 + wm + 8 * i + g;
+          if (row >= M) continue;
           const double re = t1[i][j][h] - t2[i][j][h];
           const double im = t3[i][j][h] - t1[i][j][h] - t2[i][j][h];
-          C[(int64_t)row * D.sCi + n1 * D.sC1 + n2 * D.sC2] = make_double2(re, im);
+          C[(int64_t)row * D.sCi + off] = make_double2(re, im);
         }
       }
+      const int step = h ? 7 : 1;
+      n += step;
+      n2 += step;
+      while (n2 >= N2) { n2 -= N2; ++n1; }
+    }
   }
 }
 
