@@ -56,23 +56,30 @@ struct XSmem {
   static constexpr size_t BYTES = (size_t)2 * STAGE * sizeof(double);
 };
 
-template <bool REAL_S, bool KCONTIG>
+// SMALLM (real S, M <= 32: blocks of at most 32 nodes): a 32-row tile, every warp 32 rows x
+// 16 complex columns, so no warp works on the all-zero rows 32..63 of the 64-row tile.
+template <bool REAL_S, bool KCONTIG, bool SMALLM = false>
 __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict__ descs, Bufs bufs) {
+  static_assert(REAL_S || !SMALLM, "SMALLM: real S only");
+  constexpr int TM = SMALLM ? 32 : XT_M;
+  constexpr int NJ = SMALLM ? 4 : 8;  // real-view 8-column tiles per warp
   extern __shared__ __align__(16) double xsm[];
   const GemmDesc& D = descs[blockIdx.z];
   const int M = D.M, K = D.K;
   const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
-  const int i0 = blockIdx.y * XT_M;
+  const int i0 = blockIdx.y * TM;
   const int64_t n0 = (int64_t)blockIdx.x * XT_N;
   if (i0 >= M || n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp tile origin (complex columns)
+  // warp tile origin (row, complex column)
+  const int wm = SMALLM ? 0 : (warp >> 1) * 32, wn = SMALLM ? warp * 16 : (warp & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
 
   const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off;
   // ---- per-thread load assignments (fixed across K chunks)
-  // A (S): 64 x 16 elements, thread -> row ai = tid/2, 8 consecutive j
-  const int ai = tid >> 1, aj0 = (tid & 1) * 8;
+  // A (S): TM x 16 elements, thread -> row ai = tid/2, 8 consecutive j (SMALLM: tid/4, 4 j)
+  constexpr int AJ = SMALLM ? 4 : 8;
+  const int ai = SMALLM ? tid >> 2 : tid >> 1, aj0 = SMALLM ? (tid & 3) * 4 : (tid & 1) * 8;
   const bool arow_ok = (i0 + ai) < M;
   // B (data): 16 x 64 complex.  Coalesced mappings: K-contiguous data -> 16 threads cover
   // one 256-byte column segment (8 columns per instruction); otherwise 64 consecutive
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
     if (REAL_S) {
       const double* A = reinterpret_cast<const double*>(bufs.p[B_TAB]) + D.a_off;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < AJ; ++e) {
         const int j = j0 + aj0 + e;
         const bool ok = arow_ok && j < K;
         cp_async8(As + (aj0 + e) * LDA_R + ai, ok ? A + (int64_t)(i0 + ai) * D.sAi + (int64_t)j * D.sAj : A, ok);
@@ -136,11 +143,11 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
 
   // accumulators: complex S -> [4 row tiles][4 col tiles][re/im][2]; real S -> [4][8][2] over
   // the real view (8 real column tiles of 8 = 32 complex columns)
-  double acc[4][8][2];
+  double acc[4][NJ][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NJ; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   const int nchunks = (K + XT_K - 1) / XT_K;
   load_chunk(0, 0);
@@ -155,19 +162,20 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
 #pragma unroll
     for (int kk = 0; kk < XT_K; kk += 4) {
       if (REAL_S) {
-        double a[4], b[8];
+        double a[4], b[NJ];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = As[(kk + q) * LDA_R + wm + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) b[j] = Bs[(kk + q) * (2 * LDB_C) + 2 * wn + 8 * j + g];
+        for (int j = 0; j < NJ; ++j) b[j] = Bs[(kk + q) * (2 * LDB_C) + 2 * wn + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+          for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
       } else {
         const double2* As2 = reinterpret_cast<const double2*>(As);
         const double2* Bs2 = reinterpret_cast<const double2*>(Bs);
         double2 a[4], b[4];
+        static_assert(NJ == 8 || REAL_S, "complex S uses the 64 x 64 tile");
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = As2[(kk + q) * LDA_C + wm + 8 * i + g];
 #pragma unroll
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
     int64_t n = n0 + wn + (REAL_S ? q : 2 * q);
     int64_t n1 = n / N2, n2 = n - n1 * N2;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < NJ; ++e) {
       if (n < N) {
         const int64_t off = n1 * D.sC1 + n2 * D.sC2;
 #pragma unroll
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
           if (row >= M) continue;
           // real S: acc[i][e] = (re, im) of column e; complex S: re in acc[i][2j], im in acc[i][2j+1]
           const double2 v = REAL_S ? make_double2(acc[i][e][0], acc[i][e][1])
-                                   : make_double2(acc[i][2 * (e >> 1)][e & 1], acc[i][2 * (e >> 1) + 1][e & 1]);
+                                   : make_double2(acc[i][(2 * (e >> 1)) % NJ][e & 1], acc[i][(2 * (e >> 1) + 1) % NJ][e & 1]);
           C[(int64_t)row * D.sCi + off] = v;
         }
       }
@@ -220,17 +228,23 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
   }
 }
 
-template <bool REAL_S, bool KCONTIG>
-cudaError_t launch_one(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
+template <bool REAL_S, bool KCONTIG, bool SMALLM>
+cudaError_t launch_one_t(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
   const size_t sm = XSmem<REAL_S>::BYTES;
-  cudaError_t e = cudaFuncSetAttribute(k_xform<REAL_S, KCONTIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  constexpr int TM = SMALLM ? 32 : XT_M;
+  cudaError_t e = cudaFuncSetAttribute(k_xform<REAL_S, KCONTIG, SMALLM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   for (int z0 = 0; z0 < ndesc; z0 += 65535) {
     const int nzz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
-    dim3 grid((unsigned)((maxN + XT_N - 1) / XT_N), (unsigned)((maxM + XT_M - 1) / XT_M), (unsigned)nzz);
-    k_xform<REAL_S, KCONTIG><<<grid, XT_THREADS, sm, st>>>(d + z0, bufs);
+    dim3 grid((unsigned)((maxN + XT_N - 1) / XT_N), (unsigned)((maxM + TM - 1) / TM), (unsigned)nzz);
+    k_xform<REAL_S, KCONTIG, SMALLM><<<grid, XT_THREADS, sm, st>>>(d + z0, bufs);
   }
   return cudaGetLastError();
+}
+template <bool REAL_S, bool KCONTIG>
+cudaError_t launch_one(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
+  if (REAL_S && maxM <= 32) return launch_one_t<true, KCONTIG, true>(d, ndesc, maxM, maxN, bufs, st);
+  return launch_one_t<REAL_S, KCONTIG, false>(d, ndesc, maxM, maxN, bufs, st);
 }
 
 
