@@ -59,7 +59,7 @@ struct XSmem {
 // SMALLM (real S, M <= 32: blocks of at most 32 nodes): a 32-row tile, every warp 32 rows x
 // 16 complex columns, so no warp works on the all-zero rows 32..63 of the 64-row tile.
 template <bool REAL_S, bool KCONTIG, bool SMALLM = false>
-__global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict__ descs, Bufs bufs) {
+__global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict__ descs, int gm, Bufs bufs) {
   static_assert(REAL_S || !SMALLM, "SMALLM: real S only");
   constexpr int TM = SMALLM ? 32 : XT_M;
   constexpr int NJ = SMALLM ? 4 : 8;  // real-view 8-column tiles per warp
@@ -67,8 +67,9 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
   const GemmDesc& D = descs[blockIdx.z];
   const int M = D.M, K = D.K;
   const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
-  const int i0 = blockIdx.y * TM;
-  const int64_t n0 = (int64_t)blockIdx.x * XT_N;
+  // row tiles fastest: the CTAs of one column tile run together and share its B tile in L2
+  const int i0 = (int)(blockIdx.x % gm) * TM;
+  const int64_t n0 = (int64_t)(blockIdx.x / gm) * XT_N;
   if (i0 >= M || n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // warp tile origin (row, complex column)
@@ -236,8 +237,9 @@ cudaError_t launch_one_t(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, c
   if (e != cudaSuccess) return e;
   for (int z0 = 0; z0 < ndesc; z0 += 65535) {
     const int nzz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
-    dim3 grid((unsigned)((maxN + XT_N - 1) / XT_N), (unsigned)((maxM + TM - 1) / TM), (unsigned)nzz);
-    k_xform<REAL_S, KCONTIG, SMALLM><<<grid, XT_THREADS, sm, st>>>(d + z0, bufs);
+    const int gm = (maxM + TM - 1) / TM;
+    dim3 grid((unsigned)(((maxN + XT_N - 1) / XT_N) * gm), 1, (unsigned)nzz);
+    k_xform<REAL_S, KCONTIG, SMALLM><<<grid, XT_THREADS, sm, st>>>(d + z0, gm, bufs);
   }
   return cudaGetLastError();
 }
@@ -256,13 +258,13 @@ cudaError_t launch_one(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, con
 constexpr int X3_THREADS = 256;
 
 template <bool KCONTIG>
-__global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __restrict__ descs, Bufs bufs) {
+__global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __restrict__ descs, int gm, Bufs bufs) {
   extern __shared__ __align__(16) double xsm[];
   const GemmDesc& D = descs[blockIdx.z];
   const int M = D.M, K = D.K;
   const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
-  const int i0 = blockIdx.y * XT_M;
-  const int64_t n0 = (int64_t)blockIdx.x * XT_N;
+  const int i0 = (int)(blockIdx.x % gm) * XT_M;  // row tiles fastest (B tile reuse in L2)
+  const int64_t n0 = (int64_t)(blockIdx.x / gm) * XT_N;
   if (i0 >= M || n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
@@ -393,8 +395,9 @@ cudaError_t launch_3m(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, cons
   if (e != cudaSuccess) return e;
   for (int z0 = 0; z0 < ndesc; z0 += 65535) {
     const int nzz = ndesc - z0 < 65535 ? ndesc - z0 : 65535;
-    dim3 grid((unsigned)((maxN + XT_N - 1) / XT_N), (unsigned)((maxM + XT_M - 1) / XT_M), (unsigned)nzz);
-    k_xform3m<KCONTIG><<<grid, X3_THREADS, sm, st>>>(d + z0, bufs);
+    const int gm = (maxM + XT_M - 1) / XT_M;
+    dim3 grid((unsigned)(((maxN + XT_N - 1) / XT_N) * gm), 1, (unsigned)nzz);
+    k_xform3m<KCONTIG><<<grid, X3_THREADS, sm, st>>>(d + z0, gm, bufs);
   }
   return cudaGetLastError();
 }
