@@ -23,7 +23,7 @@ for rx in "k_zs2" "k_s5m" "k_zs1" "k_dstw" "k_dst<" "k_xform3m" "k_proj_rows" "k
   i=$((i+1))
   c=$cmd1; [ "$rx" = "k_residual" ] && c="python bench.py --config c2 --steps 1 --warmup 0 --no-e2e --no-cpu"
   out=/tmp/${tag}_k$i
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$rx" -c 1 -o $out $c > gpurun_out/${tag}_prof_k${i}.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$rx" -c 1 -o $out $c > gpurun_out/${tag}_prof_k${i}.log 2>&1
   ncu -i $out.ncu-rep --page raw --csv > gpurun_out/${tag}_prof_k${i}_raw.csv 2>/dev/null
   ncu -i $out.ncu-rep --page source --csv > /tmp/src.csv 2>/dev/null && gzip -c /tmp/src.csv > gpurun_out/${tag}_prof_k${i}_source.csv.gz
 done
