@@ -396,10 +396,20 @@ __device__ __forceinline__ void zs2_body(const ZBlock& B, const Tile& t, int nz,
   const cplx cT = hT && t.active ? mk(B.cT) * ld(TAB + B.wy1 + t.m) : mk(0, 0);
   const int tx = threadIdx.x % TL, ty = threadIdx.x / TL;
   // l~(k) = -sigma_k (cL_l GL[k][m] + cR_l GR[k][m] + cB_m GB[k][l] + cT_m GT[k][l]); the
-  // -sigma_k is in the (row-scaled) z table, so the right side is the bracket
+  // -sigma_k is in the (row-scaled) z table, so the right side is the bracket.  Real-basis
+  // blocks (RT 2: real steps, so real W rows and real face couplings) take real coefficients:
+  // 2 FMAs per face term instead of 4.
   auto lift = [&](int sg, int j) {
     const double2* d = fsm + (sg & 1) * FS::SLOTS;
     cplx acc = mk(0, 0);
+    if (RT == 2) {
+      auto rfma = [](double c, double2 v, cplx a) { return mk(fma(c, v.x, a.x), fma(c, v.y, a.y)); };
+      if (hL) acc = rfma(cL.x, d[FS::GL + j * TM + ty], acc);
+      if (hR) acc = rfma(cR.x, d[FS::GR + j * TM + ty], acc);
+      if (hB) acc = rfma(cB.x, d[FS::GB + j * TL + tx], acc);
+      if (hT) acc = rfma(cT.x, d[FS::GT + j * TL + tx], acc);
+      return acc;
+    }
     if (hL) acc = cfma(cL, mk(d[FS::GL + j * TM + ty]), acc);
     if (hR) acc = cfma(cR, mk(d[FS::GR + j * TM + ty]), acc);
     if (hB) acc = cfma(cB, mk(d[FS::GB + j * TL + tx]), acc);
