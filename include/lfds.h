@@ -122,6 +122,35 @@ int lfds_solve_host_async(lfds_plan* plan, const void* f_host, void* u_host, int
                           void* ws_dev, size_t ws_bytes, void* cuda_stream);
 
 /*
+ * Horizontally heterogeneous media — the paper's motivating use (large 3D
+ * problems need iterative solvers, "the choice of preconditioner is crucial", preconditioning
+ * "via discrete Green's function in layered medium").  Solves A_het u = M f where lambda varies
+ * per node, lambda_ijk = lambda + dlam_ijk (Eq. (fd), with a node-wise lambda):
+ *     A_het = A + diag(dlam) M.
+ * Right-preconditioned restarted GMRES(restart) in the Lippmann-Schwinger (FDIE)
+ * form  (I + diag(dlam) S) y = f,  u = S y,  with S = this plan's fast direct solve
+ * (u = A^{-1} M f, lfds_solve), which equals M^{-1} A_het S exactly: one fast solve per
+ * iteration, no stencil matvec.  Classical Gram-Schmidt with reorthogonalisation (CGS2).
+ *   dlam_dev, f_dev, u_dev   device complex128 [nz][ny][nx], 16-B aligned; u_dev must not
+ *                            alias f_dev or dlam_dev (nrhs = 1; complex128 plans only).
+ *   tol                      stop when ||f - (I + dlam S) y||_2 <= tol ||f||_2 (> 0).
+ *   maxit                    total iterations (>= 1); restart in 1..64.
+ *   ws_dev                   >= lfds_gmres_workspace_bytes(plan, restart) (restart + 4 field
+ *                            vectors, the solve workspace and reduction scratch).
+ * Synchronises the stream (each Hessenberg column is read back).  The inner products are
+ * per-CTA partial sums added on the host in a fixed order (deterministic).  Returns
+ * LFDS_ENOTCONVERGED if maxit iterations do not reach tol (u then holds the last iterate).
+ */
+typedef struct {
+  int iterations;          /* Arnoldi steps (= fast solves inside the iteration)            */
+  int cycles;              /* restart cycles                                                 */
+  double rel_residual;     /* ||f - (I + dlam S) y|| / ||f|| at exit (Arnoldi estimate)      */
+} lfds_krylov_report;
+size_t lfds_gmres_workspace_bytes(const lfds_plan* plan, int restart);
+int lfds_gmres(lfds_plan* plan, const void* dlam_dev, const void* f_dev, void* u_dev, double tol, int maxit,
+               int restart, void* ws_dev, size_t ws_bytes, void* cuda_stream, lfds_krylov_report* report);
+
+/*
  * Residual r = M f - A u (b-units, PAPER.md Eq. (fdmtr)) on the device; f_dev may be NULL
  * (then r = -A u).  dd = 1 evaluates in double-double and rounds once.  r_dev is
  * complex128 [nrhs][nz][ny][nx] even for LFDS_F64 plans.  If norms != NULL it receives

@@ -19,3 +19,4 @@ from .operator import (control_volumes, axis_pencil, z_pencil, assemble, assembl
 from .eig import gen_eig, sine_basis  # noqa: F401
 from .solve import (solve_direct, solve_separable, solve, block_solutions,  # noqa: F401
                     residual_ext, interface_mask, GlobalBases)
+from .hetero import assemble_hetero, solve_hetero_direct, rel_residual_hetero  # noqa: F401

@@ -1120,6 +1120,150 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
   return LFDS_OK;
 }
 
+// ------------------------------------------------------------------ heterogeneous media (GMRES)
+size_t lfds_gmres_workspace_bytes(const lfds_plan* P, int restart) {
+  if (!P || P->opt.device < 0 || restart < 1 || restart > 64) return 0;
+  const size_t n = (size_t)P->ax[0].N * P->ax[1].N * P->nz;
+  const size_t vec = al256(n * sizeof(double2));
+  return vec * (size_t)(restart + 4) + al256((size_t)KRYLOV_DOT_BLOCKS * 80 * sizeof(double2)) +
+         al256(80 * sizeof(double2)) + lfds_workspace_bytes(P, 1);
+}
+
+int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double tol, int maxit, int restart, void* ws,
+               size_t ws_bytes, void* stream, lfds_krylov_report* rep) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (P->opt.device < 0) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  if (P->opt.dtype != LFDS_C128) return fail(LFDS_EINVAL, "lfds_gmres: complex128 plans only");
+  if (restart < 1 || restart > 64 || maxit < 1 || !(tol > 0))
+    return fail(LFDS_EINVAL, "lfds_gmres: need 1 <= restart <= 64, maxit >= 1, tol > 0");
+  if (!dlam || !f || !u || !ws) return fail(LFDS_EINVAL, "lfds_gmres: NULL pointer");
+  for (const void* q : {dlam, f, (const void*)u, (const void*)ws})
+    if (reinterpret_cast<uintptr_t>(q) % 16) return fail(LFDS_EINVAL, "lfds_gmres: pointers must be 16-byte aligned");
+  if (u == f || u == dlam) return fail(LFDS_EINVAL, "lfds_gmres: u must not alias f or dlam");
+  const size_t need = lfds_gmres_workspace_bytes(P, restart);
+  if (ws_bytes < need) return fail(LFDS_EINVAL, "lfds_gmres: workspace too small: %zu < %zu", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int m = restart;
+  const int64_t n = (int64_t)P->ax[0].N * P->ax[1].N * P->nz;
+  const size_t vec = al256((size_t)n * sizeof(double2));
+  const int64_t vs = (int64_t)(vec / sizeof(double2));
+  char* w0 = static_cast<char*>(ws);
+  double2* V = reinterpret_cast<double2*>(w0);                        // m + 1 basis vectors
+  double2* W = reinterpret_cast<double2*>(w0 + vec * (m + 1));
+  double2* S = W + vs;
+  double2* Y = S + vs;
+  double2* part = reinterpret_cast<double2*>(w0 + vec * (m + 4));
+  double2* coef = reinterpret_cast<double2*>(reinterpret_cast<char*>(part) +
+                                             al256((size_t)KRYLOV_DOT_BLOCKS * 80 * sizeof(double2)));
+  void* sws = reinterpret_cast<char*>(coef) + al256(80 * sizeof(double2));
+  const size_t sws_bytes = lfds_workspace_bytes(P, 1);
+  const double2* F = static_cast<const double2*>(f);
+  const double2* DL = static_cast<const double2*>(dlam);
+  std::vector<double2> hp((size_t)KRYLOV_DOT_BLOCKS * 80);
+  auto dots = [&](int cnt, const double2* Vb, const double2* x, std::vector<zc>& out) -> int {
+    CUDA_TRY(launch_dots(n, cnt, Vb, vs, x, part, st));
+    CUDA_TRY(cudaMemcpyAsync(hp.data(), part, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    out.assign(cnt, zc(0));
+    for (int b = 0; b < KRYLOV_DOT_BLOCKS; ++b)  // fixed order: deterministic
+      for (int i = 0; i < cnt; ++i) out[i] += zc(hp[(size_t)b * 80 + i].x, hp[(size_t)b * 80 + i].y);
+    return LFDS_OK;
+  };
+  auto axpy = [&](int cnt, const std::vector<zc>& c, double2* target) -> int {
+    std::vector<double2> hc(cnt);
+    for (int i = 0; i < cnt; ++i) hc[i] = make_double2(c[i].real(), c[i].imag());
+    CUDA_TRY(cudaMemcpyAsync(coef, hc.data(), sizeof(double2) * cnt, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(launch_maxpy(n, cnt, V, vs, coef, target, st));
+    CUDA_TRY(cudaStreamSynchronize(st));  // hc must outlive the copy
+    return LFDS_OK;
+  };
+  int rc;
+  std::vector<zc> d;
+  if ((rc = dots(1, F, F, d))) return rc;
+  const double beta0 = std::sqrt(std::max(0.0, d[0].real()));
+  if (rep) *rep = lfds_krylov_report{0, 0, 0.0};
+  if (beta0 == 0) {
+    CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(double2) * (size_t)n, st));
+    return LFDS_OK;
+  }
+  CUDA_TRY(cudaMemsetAsync(Y, 0, sizeof(double2) * (size_t)n, st));
+  CUDA_TRY(launch_scale(n, make_double2(1.0 / beta0, 0), F, V, st));
+  double beta = beta0, res = 1.0;
+  int it = 0, cycles = 0;
+  bool conv = false, have_sy = false;
+  std::vector<zc> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), h, h2;
+  while (true) {
+    std::fill(H.begin(), H.end(), zc(0));
+    std::fill(g.begin(), g.end(), zc(0));
+    g[0] = beta;
+    int jend = 0;
+    for (int j = 0; j < m; ++j) {
+      double2* Vj = V + (int64_t)j * vs;
+      if ((rc = solve_impl(P, Vj, S, 1, sws, sws_bytes, st))) return rc;   // S V_j
+      CUDA_TRY(launch_fdie(n, Vj, DL, S, W, st));                           // W = V_j + dlam S V_j
+      h.assign(j + 1, zc(0));
+      for (int pass = 0; pass < 2; ++pass) {  // CGS2
+        if ((rc = dots(j + 1, V, W, h2))) return rc;
+        std::vector<zc> c(j + 1);
+        for (int i = 0; i <= j; ++i) { c[i] = -h2[i]; h[i] += h2[i]; }
+        if ((rc = axpy(j + 1, c, W))) return rc;
+      }
+      if ((rc = dots(1, W, W, d))) return rc;
+      const double hn = std::sqrt(std::max(0.0, d[0].real()));
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = h[i];
+      for (int i = 0; i < j; ++i) {  // previous Givens rotations
+        const zc a = H[(size_t)i * m + j], b = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a + sn[i] * b;
+        H[(size_t)(i + 1) * m + j] = -std::conj(sn[i]) * a + cs[i] * b;
+      }
+      const zc a = H[(size_t)j * m + j];
+      if (std::abs(a) == 0) {
+        cs[j] = 0;
+        sn[j] = 1;
+        H[(size_t)j * m + j] = hn;
+      } else {
+        const double t = std::hypot(std::abs(a), hn);
+        const zc al = a / std::abs(a);
+        cs[j] = std::abs(a) / t;
+        sn[j] = al * hn / t;
+        H[(size_t)j * m + j] = al * t;
+      }
+      g[j + 1] = -std::conj(sn[j]) * g[j];
+      g[j] = cs[j] * g[j];
+      ++it;
+      jend = j + 1;
+      res = std::abs(g[j + 1]) / beta0;
+      const bool stop = res <= tol || it >= maxit || hn == 0;
+      if (!stop && j + 1 < m) CUDA_TRY(launch_scale(n, make_double2(1.0 / hn, 0), W, V + (int64_t)(j + 1) * vs, st));
+      if (stop) break;
+    }
+    std::vector<zc> c(jend);  // R c = g, y += V c
+    for (int i = jend - 1; i >= 0; --i) {
+      zc sacc = g[i];
+      for (int k = i + 1; k < jend; ++k) sacc -= H[(size_t)i * m + k] * c[k];
+      c[i] = sacc / H[(size_t)i * m + i];
+    }
+    if ((rc = axpy(jend, c, Y))) return rc;
+    ++cycles;
+    if (res <= tol) { conv = true; break; }
+    if (it >= maxit) break;
+    // restart from the true preconditioned residual r = f - (y + dlam S y)
+    if ((rc = solve_impl(P, Y, S, 1, sws, sws_bytes, st))) return rc;
+    CUDA_TRY(launch_fdie_res(n, F, Y, DL, S, W, st));
+    if ((rc = dots(1, W, W, d))) return rc;
+    beta = std::sqrt(std::max(0.0, d[0].real()));
+    res = beta / beta0;
+    if (res <= tol) { conv = true; have_sy = true; break; }
+    CUDA_TRY(launch_scale(n, make_double2(1.0 / beta, 0), W, V, st));
+  }
+  if (have_sy) CUDA_TRY(cudaMemcpyAsync(u, S, sizeof(double2) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  else if ((rc = solve_impl(P, Y, u, 1, sws, sws_bytes, st))) return rc;    // u = S y
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (rep) *rep = lfds_krylov_report{it, cycles, res};
+  if (!conv) return fail(LFDS_ENOTCONVERGED, "lfds_gmres: %d iterations, relative residual %.3g > %.3g", it, res, tol);
+  return LFDS_OK;
+}
+
 int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_end, int rank0) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
   const int nblk = P->nbx * P->nby, Nx = P->ax[0].N;

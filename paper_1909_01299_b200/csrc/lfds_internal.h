@@ -116,6 +116,19 @@ struct S5M {
   int64_t r1t, r2t;            // IF: R1~[a][r][t][m], R2~[b][r][t][l]
   int64_t p1t, p2p, p2t;       // IF: P1~[a][r][t][m], P2 partials [b][r][t][mt][l], P2~[b][r][t][l]
 };
+// Krylov vector kernels (lfds_krylov.cu) for lfds_gmres; dots write partial[blk * 80 + i]
+// for blk < KRYLOV_DOT_BLOCKS, i < cnt <= 80
+constexpr int KRYLOV_DOT_BLOCKS = 592;
+cudaError_t launch_fdie(int64_t n, const double2* v, const double2* dlam, const double2* s, double2* out,
+                        cudaStream_t st);
+cudaError_t launch_fdie_res(int64_t n, const double2* f, const double2* y, const double2* dlam, const double2* s,
+                            double2* out, cudaStream_t st);
+cudaError_t launch_dots(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* w, double2* partial,
+                        cudaStream_t st);
+cudaError_t launch_maxpy(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* coef, double2* w,
+                         cudaStream_t st);
+cudaError_t launch_scale(int64_t n, double2 alpha, const double2* w, double2* out, cudaStream_t st);
+
 int s5m_ka(int nifx, int nify);   // padded |I| (8 or 16), 0 = unsupported
 int s5m_mtiles(int ny);
 cudaError_t launch_s5m(const S5M& S, const Bufs& bufs, cudaStream_t st);

@@ -45,6 +45,10 @@ class Report(ctypes.Structure):
                 ("min_pivot_ratio", ctypes.c_double), ("n_kernel_launches", ctypes.c_int)]
 
 
+class KrylovReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("cycles", ctypes.c_int), ("rel_residual", ctypes.c_double)]
+
+
 class Info(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("nbx", ctypes.c_int),
                 ("nby", ctypes.c_int), ("n_if_x", ctypes.c_int), ("n_if_y", ctypes.c_int), ("real_z", ctypes.c_int),
@@ -73,6 +77,10 @@ _lib.lfds_set_partition.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c
 _lib.lfds_exchange_layout.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
                                       ctypes.POINTER(ctypes.c_size_t)]
 _lib.lfds_solve_phase.argtypes = [_P, ctypes.c_int, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
+_lib.lfds_gmres_workspace_bytes.argtypes = [_P, ctypes.c_int]
+_lib.lfds_gmres_workspace_bytes.restype = ctypes.c_size_t
+_lib.lfds_gmres.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, _P,
+                            ctypes.POINTER(KrylovReport)]
 _lib.lfds_destroy.argtypes = [_P]
 _lib.lfds_stage_count.restype = ctypes.c_int
 _lib.lfds_stage_name.argtypes = [ctypes.c_int]
@@ -211,6 +219,26 @@ class Plan:
         _check(_lib.lfds_solve(self._h, _P(F.data_ptr()), _P(U.data_ptr()), nrhs, _P(ws.data_ptr()),
                                ws.numel(), _P(st)))
         return U[0] if single else U
+
+    def solve_hetero(self, f, dlam, tol: float = 1e-10, maxit: int = 200, restart: int = 20, out=None,
+                     stream=None):
+        """Heterogeneous medium lambda_ijk = lambda + dlam_ijk (lfds_gmres): right-preconditioned
+        GMRES with this plan's fast solve.  f, dlam: contiguous CUDA complex128 (nz, ny, nx).
+        Returns (u, report dict)."""
+        torch = self._torch()
+        for name, t in (("f", f), ("dlam", dlam)):
+            if not (t.is_cuda and t.is_contiguous() and t.dtype == torch.complex128 and tuple(t.shape) == self.shape):
+                raise ValueError(f"{name} must be a contiguous CUDA complex128 tensor of shape {self.shape}")
+        U = torch.empty_like(f) if out is None else out
+        nb = int(_lib.lfds_gmres_workspace_bytes(self._h, int(restart)))
+        if nb == 0:
+            raise ValueError("lfds_gmres: restart must be in 1..64 on a device plan")
+        ws = torch.empty(nb, dtype=torch.uint8, device=f.device)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        rep = KrylovReport()
+        _check(_lib.lfds_gmres(self._h, _P(dlam.data_ptr()), _P(f.data_ptr()), _P(U.data_ptr()), float(tol),
+                               int(maxit), int(restart), _P(ws.data_ptr()), nb, _P(st), ctypes.byref(rep)))
+        return U, {"iterations": rep.iterations, "cycles": rep.cycles, "rel_residual": rep.rel_residual}
 
     def solve_host(self, f_host, out=None, stream=None, sync: bool = True, slot: int = 0):
         """End-to-end: host f (pinned CPU tensor) -> device -> solve -> host u.  sync=False

@@ -7,4 +7,4 @@ BASELINE.json's configs describe, following SURVEY.md §8(d)'s recipe.
 Both the oracle (``oracle/``) and the CUDA path (``paper_1909_01299_b200``)
 consume its output; neither is imported here.
 """
-from .configs import Problem, make_problem, CONFIG_NAMES, shrunken  # noqa: F401
+from .configs import Problem, make_problem, CONFIG_NAMES, shrunken, anomaly  # noqa: F401

@@ -242,3 +242,14 @@ def shrunken(name: str, nrhs: Optional[int] = None) -> Problem:
         return _build(105, "c5s", C=20, G=6, q=1.2, P=4, pml="quad", nz=9, layers=5, lrange=(-1, 1),
                       lam=_lam(10), B=5, nrhs=nrhs or 3, rhs_kind="cn", core_jitter=True)
     raise KeyError(name)
+
+
+def anomaly(p: Problem, eps: float = -0.1, box=((0.375, 0.625), (0.375, 0.625), (0.375, 0.625))) -> np.ndarray:
+    """Node-wise shift perturbation dlam of an embedded inhomogeneity: a box of
+    velocity c_bg (1 + eps) in the layered background, so lambda = omega^2 / c^2 becomes
+    lambda (1 + eps)^-2 inside.  ``box`` holds (lo, hi) fractions of the unknown nodes along
+    (z, y, x).  Returns dlam with the field layout (N_z, N_y, N_x), complex128."""
+    dl = np.zeros(p.shape, dtype=np.complex128)
+    sl = tuple(slice(int(lo * n), max(int(lo * n) + 1, int(hi * n))) for (lo, hi), n in zip(box, p.shape))
+    dl[sl] = complex(p.lam) * ((1.0 + eps) ** -2 - 1.0)
+    return dl
