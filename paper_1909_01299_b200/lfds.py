@@ -93,7 +93,7 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_get_report",
             "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version",
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
-            "lfds_exchange_layout", "lfds_solve_phase"]
+            "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres"]
 
 
 def _check(rc):
