@@ -235,8 +235,77 @@ def stage_algorithmic(p, R: int, plan=None):
     }
 
 
+def roofline_summary(p, nrhs, plan, stages, steps, config, ms_max):
+    """Roofline of the dominant stage and of the whole solve.  Stage work is per
+    solve pass; a step runs `passes` of them (1 + refinement passes, or the fast solves inside
+    a GMRES solve), counted from the step-2 z-solve launches (one per pass)."""
+    passes = max(1.0, stages.get("step2_zsolve", (0.0, steps))[1] / max(1, steps))
+    # roofline of the dominant stage (the kernel kind with the largest device time per step);
+    # governing bound = whichever of flops/peak and bytes/peak is the larger time
+    alg = stage_algorithmic(p, nrhs, plan)
+    hbm_peak, hbm_src = _peaks()
+    # (stages with a stated algorithmic work; plane-sized glue stages have none)
+    cand = {k: v for k, v in stages.items() if any(x for x in alg.get(k, (None, None)))} or stages
+    dom = max(cand.items(), key=lambda kv: kv[1][0])
+    name, (st_ms, st_launch) = dom
+    per_step_ms = st_ms / max(1, steps)
+    flops, nbytes = alg.get(name, (None, None))
+    # a solve stage runs once per pass; the refinement stages once per refinement
+    mult = st_launch / max(1, steps) if name.startswith("refine_") else passes
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
+            ent = json.load(fh_).get(config, {}).get(name)
+            traffic = ent["dram_bytes_per_launch"] if ent else None  # ncu dram read+write, one launch
+    except Exception:
+        pass
+    t_tensor = (flops or 0) / (FP64_PEAK_TFLOPS * 1e12)
+    t_hbm = (nbytes or 0) / (hbm_peak * 1e9)
+    if t_tensor >= t_hbm and flops:
+        achieved = flops * mult / (per_step_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "kernel": name,
+                "peak_source": "FP64 tensor (DMMA) = 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5); "
+                               "measured DMMA 37.1 TF/s (profiles/r01_fp64_peaks.log)"}
+    else:
+        achieved = (nbytes or 0) * mult / (per_step_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "kernel": name,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
+    # whole-solve roofline (SURVEY.md §8(d)): T_roof = max(64 B/unknown / HBM, F_alg / FP64)
+    f_alg = sum(v[0] or 0 for k, v in alg.items() if "dense" in k or k.startswith("step5_"))
+    b_alg = (64.0 if not p.real else 32.0) * p.unknowns * nrhs
+    t_roof = passes * max(b_alg / (hbm_peak * 1e9), f_alg / (FP64_PEAK_TFLOPS * 1e12)) * 1e3
+    roof["solve"] = {"t_roof_ms": t_roof, "frac": t_roof / ms_max, "alg_bytes": b_alg, "alg_flops": f_alg}
+    roof["stage_ms_per_step"] = {k: v[0] / max(1, steps) for k, v in stages.items() if v[1]}
+    roof["passes_per_step"] = passes
+    return roof
+
+
 def run_reference(args, rank, world):
     if rank != 0:
+        return
+    if args.config in HETERO:  # oracle: sparse LU of A_het on the shrunken analog, per step
+        import oracle
+        from workloads import anomaly, shrunken
+        base, eps = HETERO[args.config]
+        ps = shrunken(base, nrhs=1)
+        dls, fs = anomaly(ps, eps=eps), ps.rhs(0)
+        ts = []
+        for _ in range(args.warmup + args.steps):
+            t1 = time.perf_counter()
+            oracle.solve_hetero_direct(ps, dls, fs)
+            ts.append(time.perf_counter() - t1)
+        t = statistics.mean(ts[args.warmup:])
+        val = ps.unknowns / t
+        smp = f"{ps.name} analog {ps.shape} with the same anomaly recipe, sparse LU of A_het"
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC.replace("direct solve", "heterogeneous solve, GMRES + fast-solver preconditioner"),
+            "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic", "config": {"workload": args.config, "sample": smp},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": smp},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
         return
     p = make_problem(args.config)
     nz_s = args.cpu_nz
@@ -379,42 +448,7 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": p.unknowns * ne * (1 if blocks else world) / (float(t.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item()),
                "nrhs_per_gpu": ne}
-    # roofline of the dominant stage (the kernel kind with the largest device time per step);
-    # governing bound = whichever of flops/peak and bytes/peak is the larger time
-    alg = stage_algorithmic(p, nrhs, plan)
-    hbm_peak, hbm_src = _peaks()
-    # (stages with a stated algorithmic work; plane-sized glue stages have none)
-    cand = {k: v for k, v in stages.items() if any(x for x in alg.get(k, (None, None)))} or stages
-    dom = max(cand.items(), key=lambda kv: kv[1][0])
-    name, (st_ms, st_launch) = dom
-    per_step_ms = st_ms / max(1, args.steps)
-    flops, nbytes = alg.get(name, (None, None))
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
-            ent = json.load(fh_).get(args.config, {}).get(name)
-            traffic = ent["dram_bytes_per_launch"] if ent else None  # ncu dram read+write, one launch
-    except Exception:
-        pass
-    t_tensor = (flops or 0) / (FP64_PEAK_TFLOPS * 1e12)
-    t_hbm = (nbytes or 0) / (hbm_peak * 1e9)
-    if t_tensor >= t_hbm and flops:
-        achieved = flops / (per_step_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "kernel": name,
-                "peak_source": "FP64 tensor (DMMA) = 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5); "
-                               "measured DMMA 37.1 TF/s (profiles/r01_fp64_peaks.log)"}
-    else:
-        achieved = (nbytes or 0) / (per_step_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic, "kernel": name,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
-    # whole-solve roofline: T_roof = max(64 B/unknown / HBM, F_alg / FP64)
-    f_alg = sum(v[0] or 0 for k, v in alg.items() if "dense" in k or k.startswith("step5_"))
-    b_alg = (64.0 if not p.real else 32.0) * p.unknowns * nrhs
-    t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (FP64_PEAK_TFLOPS * 1e12)) * 1e3
-    roof["solve"] = {"t_roof_ms": t_roof, "frac": t_roof / ms_max, "alg_bytes": b_alg, "alg_flops": f_alg}
-    roof["stage_ms_per_step"] = {k: v[0] / max(1, args.steps) for k, v in stages.items() if v[1]}
+    roof = roofline_summary(p, nrhs, plan, stages, args.steps, args.config, ms_max)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         ps, ts, threads = cpu_oracle_sample(p, args.cpu_nz, 1)
@@ -441,12 +475,113 @@ def run_ours(args, rank, world, local_rank):
     plan.close()
 
 
+# heterogeneous workload: the C4 grid and background with an
+# embedded velocity anomaly (workloads.anomaly: a box over the middle quarter of every axis at
+# c_bg (1 + eps)); solved by lfds_gmres (right-preconditioned GMRES, the fast solve as the
+# preconditioner) to HETERO_TOL
+HETERO = {"c4h": ("c4", -0.1)}
+HETERO_TOL, HETERO_RESTART = 1e-10, 16
+
+
+def run_hetero(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1909_01299_b200 import Plan
+    from workloads import anomaly, shrunken
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    base, eps = HETERO[args.config]
+    p = make_problem(base)
+    dl = anomaly(p, eps=eps)
+    t0 = time.perf_counter()
+    plan = Plan.from_problem(p, device=local_rank, profile=True)
+    setup_s = time.perf_counter() - t0
+    f = torch.from_numpy(p.rhs(0)).to(dev)
+    dlam = torch.from_numpy(dl).to(dev)
+    u = torch.empty_like(f)
+    reps = []
+
+    def step():
+        _, r = plan.solve_hetero(f, dlam, tol=HETERO_TOL, restart=HETERO_RESTART, maxit=400, out=u)
+        reps.append(r)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    plan.stage_times()  # reset
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    stages = plan.stage_times()
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    value = p.unknowns * world / (ms_max * 1e-3)  # replicas: every rank solves its own copy
+    roof = roofline_summary(p, 1, plan, stages, args.steps, args.config, ms_max)
+    e2e = None
+    if not args.no_e2e:  # pinned host f -> device, solve, u -> host, every step
+        fh = f.cpu().pin_memory()
+        uh = torch.empty_like(fh).pin_memory()
+        fd = torch.empty_like(f)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k2 = max(2, min(args.steps, 3))
+        a.record(stream)
+        for _ in range(k2):
+            fd.copy_(fh, non_blocking=True)
+            plan.solve_hetero(fd, dlam, tol=HETERO_TOL, restart=HETERO_RESTART, maxit=400, out=u)
+            uh.copy_(u, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t_e2e = a.elapsed_time(b) / k2
+        nb = fh.numel() * fh.element_size()
+        e2e = {"value": p.unknowns * world / (t_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "ms_per_step": t_e2e, "nrhs_per_gpu": 1}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:  # oracle: sparse LU of A_het on the shrunken analog
+        import oracle
+        ps = shrunken(base, nrhs=1)
+        dls = anomaly(ps, eps=eps)
+        t1 = time.perf_counter()
+        oracle.solve_hetero_direct(ps, dls, ps.rhs(0))
+        tc = time.perf_counter() - t1
+        cpu = {"value": ps.unknowns / tc, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"{ps.name} analog {ps.shape} with the same anomaly recipe, sparse LU of A_het "
+                         f"({ps.unknowns} unknowns, {tc:.2f} s)"}
+    last = reps[-1]
+    if rank == 0:
+        line = {
+            "metric": METRIC.replace("direct solve", "heterogeneous solve, GMRES + fast-solver preconditioner"),
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic",
+            "config": {"workload": args.config, "nx": p.nx, "ny": p.ny, "nz": p.nz,
+                       "blocks": [len(p.iface_x) + 1, len(p.iface_y) + 1], "anomaly_eps": eps,
+                       "tol": HETERO_TOL, "restart": HETERO_RESTART, "krylov_iterations": last["iterations"],
+                       "krylov_cycles": last["cycles"], "rel_residual_preconditioned": last["rel_residual"],
+                       "parallelism": "1 gpu" if world == 1 else f"replicas x{world}",
+                       "l2": "inputs larger than L2 (no flush)", "setup_s": setup_s},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": plan.report()["n_kernel_launches"] * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "c4j"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "c4j", "c4h"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nrhs", type=int, default=0, help="RHS per GPU (0 = the config's)")
     ap.add_argument("--refine", type=int, default=None)
@@ -469,7 +604,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.config in HETERO:
+            run_hetero(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

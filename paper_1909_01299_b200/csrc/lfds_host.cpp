@@ -1160,8 +1160,10 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
   const double2* F = static_cast<const double2*>(f);
   const double2* DL = static_cast<const double2*>(dlam);
   std::vector<double2> hp((size_t)KRYLOV_DOT_BLOCKS * 80);
+  int kl = 0;  // kernels launched (all fast solves and vector kernels)
   auto dots = [&](int cnt, const double2* Vb, const double2* x, std::vector<zc>& out) -> int {
     CUDA_TRY(launch_dots(n, cnt, Vb, vs, x, part, st));
+    ++kl;
     CUDA_TRY(cudaMemcpyAsync(hp.data(), part, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     out.assign(cnt, zc(0));
@@ -1174,10 +1176,16 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
     for (int i = 0; i < cnt; ++i) hc[i] = make_double2(c[i].real(), c[i].imag());
     CUDA_TRY(cudaMemcpyAsync(coef, hc.data(), sizeof(double2) * cnt, cudaMemcpyHostToDevice, st));
     CUDA_TRY(launch_maxpy(n, cnt, V, vs, coef, target, st));
+    ++kl;
     CUDA_TRY(cudaStreamSynchronize(st));  // hc must outlive the copy
     return LFDS_OK;
   };
   int rc;
+  auto solve = [&](const void* src, void* dst) -> int {
+    const int r = solve_impl(P, src, dst, 1, sws, sws_bytes, st);
+    kl += P->launches;
+    return r;
+  };
   std::vector<zc> d;
   if ((rc = dots(1, F, F, d))) return rc;
   const double beta0 = std::sqrt(std::max(0.0, d[0].real()));
@@ -1199,8 +1207,9 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
     int jend = 0;
     for (int j = 0; j < m; ++j) {
       double2* Vj = V + (int64_t)j * vs;
-      if ((rc = solve_impl(P, Vj, S, 1, sws, sws_bytes, st))) return rc;   // S V_j
+      if ((rc = solve(Vj, S))) return rc;   // S V_j
       CUDA_TRY(launch_fdie(n, Vj, DL, S, W, st));                           // W = V_j + dlam S V_j
+      ++kl;
       h.assign(j + 1, zc(0));
       for (int pass = 0; pass < 2; ++pass) {  // CGS2
         if ((rc = dots(j + 1, V, W, h2))) return rc;
@@ -1248,7 +1257,7 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
     if (res <= tol) { conv = true; break; }
     if (it >= maxit) break;
     // restart from the true preconditioned residual r = f - (y + dlam S y)
-    if ((rc = solve_impl(P, Y, S, 1, sws, sws_bytes, st))) return rc;
+    if ((rc = solve(Y, S))) return rc;
     CUDA_TRY(launch_fdie_res(n, F, Y, DL, S, W, st));
     if ((rc = dots(1, W, W, d))) return rc;
     beta = std::sqrt(std::max(0.0, d[0].real()));
@@ -1257,9 +1266,10 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
     CUDA_TRY(launch_scale(n, make_double2(1.0 / beta, 0), W, V, st));
   }
   if (have_sy) CUDA_TRY(cudaMemcpyAsync(u, S, sizeof(double2) * (size_t)n, cudaMemcpyDeviceToDevice, st));
-  else if ((rc = solve_impl(P, Y, u, 1, sws, sws_bytes, st))) return rc;    // u = S y
+  else if ((rc = solve(Y, u))) return rc;    // u = S y
   CUDA_TRY(cudaStreamSynchronize(st));
   if (rep) *rep = lfds_krylov_report{it, cycles, res};
+  P->report.n_kernel_launches = kl;
   if (!conv) return fail(LFDS_ENOTCONVERGED, "lfds_gmres: %d iterations, relative residual %.3g > %.3g", it, res, tol);
   return LFDS_OK;
 }
