@@ -479,7 +479,7 @@ def run_ours(args, rank, world, local_rank):
 # embedded velocity anomaly (workloads.anomaly: a box over the middle quarter of every axis at
 # c_bg (1 + eps)); solved by lfds_gmres (right-preconditioned GMRES, the fast solve as the
 # preconditioner) to HETERO_TOL
-HETERO = {"c4h": ("c4", -0.1)}
+HETERO = {"c4h": ("c4", -0.01)}
 HETERO_TOL, HETERO_RESTART = 1e-10, 16
 
 

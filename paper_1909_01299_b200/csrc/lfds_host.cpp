@@ -1161,14 +1161,16 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
   const double2* DL = static_cast<const double2*>(dlam);
   std::vector<double2> hp((size_t)KRYLOV_DOT_BLOCKS * 80);
   int kl = 0;  // kernels launched (all fast solves and vector kernels)
-  auto dots = [&](int cnt, const double2* Vb, const double2* x, std::vector<zc>& out) -> int {
-    CUDA_TRY(launch_dots(n, cnt, Vb, vs, x, part, st));
+  // out[i] = <V_i, x> for i < cnt (and out[cnt] = <x, x> if with_self)
+  auto dots = [&](int cnt, const double2* Vb, const double2* x, std::vector<zc>& out, int with_self = 0) -> int {
+    CUDA_TRY(launch_dots(n, cnt, Vb, vs, x, part, st, with_self));
     ++kl;
     CUDA_TRY(cudaMemcpyAsync(hp.data(), part, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    out.assign(cnt, zc(0));
+    const int tot = cnt + (with_self ? 1 : 0);
+    out.assign(tot, zc(0));
     for (int b = 0; b < KRYLOV_DOT_BLOCKS; ++b)  // fixed order: deterministic
-      for (int i = 0; i < cnt; ++i) out[i] += zc(hp[(size_t)b * 80 + i].x, hp[(size_t)b * 80 + i].y);
+      for (int i = 0; i < tot; ++i) out[i] += zc(hp[(size_t)b * 80 + i].x, hp[(size_t)b * 80 + i].y);
     return LFDS_OK;
   };
   auto axpy = [&](int cnt, const std::vector<zc>& c, double2* target) -> int {
@@ -1211,11 +1213,14 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
       CUDA_TRY(launch_fdie(n, Vj, DL, S, W, st));                           // W = V_j + dlam S V_j
       ++kl;
       h.assign(j + 1, zc(0));
-      for (int pass = 0; pass < 2; ++pass) {  // CGS2
-        if ((rc = dots(j + 1, V, W, h2))) return rc;
+      for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, repeated when needed
+        if ((rc = dots(j + 1, V, W, h2, pass == 0))) return rc;
         std::vector<zc> c(j + 1);
-        for (int i = 0; i <= j; ++i) { c[i] = -h2[i]; h[i] += h2[i]; }
+        double hh = 0;
+        for (int i = 0; i <= j; ++i) { c[i] = -h2[i]; h[i] += h2[i]; hh += std::norm(h2[i]); }
         if ((rc = axpy(j + 1, c, W))) return rc;
+        // Kahan-Parlett: a second pass only if the projection removed most of w (cancellation)
+        if (pass == 0 && hh < 0.51 * h2[j + 1].real()) break;
       }
       if ((rc = dots(1, W, W, d))) return rc;
       const double hn = std::sqrt(std::max(0.0, d[0].real()));

@@ -124,7 +124,7 @@ cudaError_t launch_fdie(int64_t n, const double2* v, const double2* dlam, const 
 cudaError_t launch_fdie_res(int64_t n, const double2* f, const double2* y, const double2* dlam, const double2* s,
                             double2* out, cudaStream_t st);
 cudaError_t launch_dots(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* w, double2* partial,
-                        cudaStream_t st);
+                        cudaStream_t st, int with_self = 0);
 cudaError_t launch_maxpy(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* coef, double2* w,
                          cudaStream_t st);
 cudaError_t launch_scale(int64_t n, double2 alpha, const double2* w, double2* out, cudaStream_t st);

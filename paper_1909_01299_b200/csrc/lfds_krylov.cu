@@ -40,19 +40,21 @@ __global__ void k_fdie_res(int64_t n, const double2* __restrict__ f, const doubl
   }
 }
 
-// partial[blk][i] = sum over this CTA's elements of conj(V_i) w, i < cnt (4 vectors per sweep)
+// partial[blk][i] = sum over this CTA's elements of conj(V_i) w, i < cnt (4 vectors per sweep);
+// with_self: also conj(w) w in slot cnt (the norm before orthogonalisation, same sweep)
 __global__ void k_dots(int64_t n, int cnt, const double2* __restrict__ V, int64_t vstride,
-                       const double2* __restrict__ w, double2* partial) {
+                       const double2* __restrict__ w, double2* partial, int with_self) {
   __shared__ double2 red[KT / 32][4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i0 = 0; i0 < cnt; i0 += 4) {
+  const int tot = cnt + (with_self ? 1 : 0);
+  for (int i0 = 0; i0 < tot; i0 += 4) {
     double2 acc[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
     for (int64_t e = (int64_t)blockIdx.x * KT + threadIdx.x; e < n; e += (int64_t)gridDim.x * KT) {
       const double2 b = w[e];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (i0 + q < cnt) {
-          const double2 a = V[(int64_t)(i0 + q) * vstride + e];
+        if (i0 + q < tot) {
+          const double2 a = i0 + q < cnt ? V[(int64_t)(i0 + q) * vstride + e] : b;
           acc[q].x = fma(a.x, b.x, fma(a.y, b.y, acc[q].x));   // conj(a) b
           acc[q].y = fma(a.x, b.y, fma(-a.y, b.x, acc[q].y));
         }
@@ -69,7 +71,7 @@ __global__ void k_dots(int64_t n, int cnt, const double2* __restrict__ V, int64_
 #pragma unroll
       for (int q = 0; q < 4; ++q) red[warp][q] = acc[q];
     __syncthreads();
-    if (threadIdx.x < 4 && i0 + (int)threadIdx.x < cnt) {
+    if (threadIdx.x < 4 && i0 + (int)threadIdx.x < tot) {
       double2 s = red[0][threadIdx.x];
       for (int wi = 1; wi < KT / 32; ++wi) {
         s.x += red[wi][threadIdx.x].x;
@@ -127,9 +129,9 @@ cudaError_t launch_fdie_res(int64_t n, const double2* f, const double2* y, const
   return cudaGetLastError();
 }
 cudaError_t launch_dots(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* w, double2* partial,
-                        cudaStream_t st) {
-  if (cnt < 1 || cnt > 80) return cudaErrorInvalidValue;
-  k_dots<<<KRYLOV_DOT_BLOCKS, KT, 0, st>>>(n, cnt, V, vstride, w, partial);
+                        cudaStream_t st, int with_self) {
+  if (cnt < 1 || cnt + (with_self ? 1 : 0) > 80) return cudaErrorInvalidValue;
+  k_dots<<<KRYLOV_DOT_BLOCKS, KT, 0, st>>>(n, cnt, V, vstride, w, partial, with_self);
   return cudaGetLastError();
 }
 cudaError_t launch_maxpy(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* coef, double2* w,
