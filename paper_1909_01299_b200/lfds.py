@@ -233,7 +233,11 @@ class Plan:
         nb = int(_lib.lfds_gmres_workspace_bytes(self._h, int(restart)))
         if nb == 0:
             raise ValueError("lfds_gmres: restart must be in 1..64 on a device plan")
-        ws = torch.empty(nb, dtype=torch.uint8, device=f.device)
+        key = ("gmres", int(restart))
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nb or ws.device != f.device:  # cached like the solve workspace
+            self._ws.pop(key, None)
+            ws = self._ws[key] = torch.empty(nb, dtype=torch.uint8, device=f.device)
         st = (stream or torch.cuda.current_stream()).cuda_stream
         rep = KrylovReport()
         _check(_lib.lfds_gmres(self._h, _P(dlam.data_ptr()), _P(f.data_ptr()), _P(U.data_ptr()), float(tol),
