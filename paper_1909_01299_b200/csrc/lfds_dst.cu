@@ -31,8 +31,49 @@ __device__ __forceinline__ zc2 zmul(zc2 a, zc2 b) {
   return zc2{fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
 }
 
-// in-register radix-2 DIT FFT (forward, e^{-2 pi i k n / R}); all indices compile-time;
-// twiddles W_len^j = W_L^{j L/len} are warp-uniform broadcast reads of the W_L table
+// in-register radix-2 DIT FFT (forward, e^{-2 pi i k n / R}); all indices compile-time.
+// Twiddles W_len^j = W_L^{j L/len}: the trivial ones are applied without a general complex
+// multiply (W^0 = 1, W^{len/4} = -i, W^{len/8} = (1-i)/sqrt2, W^{3len/8} = -(1+i)/sqrt2 — in a
+// 16-point FFT only 4 of the 32 butterflies need one); the others are warp-uniform broadcast
+// reads of the W_L table.
+template <int LEN, int J, int L>
+__device__ __forceinline__ zc2 twiddle_mul(zc2 b, const double2* __restrict__ twl) {
+  constexpr double SH = 0.70710678118654752440;  // sqrt(1/2)
+  if constexpr (J == 0) {
+    return b;
+  } else if constexpr (4 * J == LEN) {
+    return zc2{b.y, -b.x};
+  } else if constexpr (8 * J == LEN) {
+    return zc2{SH * (b.x + b.y), SH * (b.y - b.x)};
+  } else if constexpr (8 * J == 3 * LEN) {
+    return zc2{SH * (b.y - b.x), -SH * (b.x + b.y)};
+  } else {
+    const double2 w2 = twl[J * (L / LEN)];
+    return zmul(zc2{w2.x, w2.y}, b);
+  }
+}
+
+template <int R, int L, int LEN, int J>
+__device__ __forceinline__ void fft_butterflies(zc2 (&v)[R], const double2* __restrict__ twl) {
+  if constexpr (J < LEN / 2) {
+#pragma unroll
+    for (int i = 0; i < R; i += LEN) {
+      const zc2 u = v[i + J], t = twiddle_mul<LEN, J, L>(v[i + J + LEN / 2], twl);
+      v[i + J] = zadd(u, t);
+      v[i + J + LEN / 2] = zsub(u, t);
+    }
+    fft_butterflies<R, L, LEN, J + 1>(v, twl);
+  }
+}
+
+template <int R, int L, int LEN>
+__device__ __forceinline__ void fft_stages(zc2 (&v)[R], const double2* __restrict__ twl) {
+  if constexpr (LEN <= R) {
+    fft_butterflies<R, L, LEN, 0>(v, twl);
+    fft_stages<R, L, 2 * LEN>(v, twl);
+  }
+}
+
 template <int R, int L>
 __device__ __forceinline__ void fft_reg(zc2 (&v)[R], const double2* __restrict__ twl) {
   // bit reversal
@@ -47,20 +88,7 @@ __device__ __forceinline__ void fft_reg(zc2 (&v)[R], const double2* __restrict__
       v[j] = t2;
     }
   }
-#pragma unroll
-  for (int len = 2; len <= R; len <<= 1) {
-#pragma unroll
-    for (int i = 0; i < R; i += len) {
-#pragma unroll
-      for (int j = 0; j < len / 2; ++j) {
-        const double2 w2 = twl[j * (L / len)];
-        const zc2 w{w2.x, w2.y};
-        const zc2 u = v[i + j], t = zmul(w, v[i + j + len / 2]);
-        v[i + j] = zadd(u, t);
-        v[i + j + len / 2] = zsub(u, t);
-      }
-    }
-  }
+  fft_stages<R, L, 2>(v, twl);
 }
 
 // Mixed-radix in-register DFT of length R = 2^a 3^b 5^c (compile-time Cooley-Tukey, decimation
@@ -138,7 +166,7 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool val
 }
 
 template <int R1, int R2, bool KCONTIG>
-__global__ void __launch_bounds__(DST_THREADS) k_dst(const GemmDesc* __restrict__ descs, Bufs bufs) {
+__global__ void __launch_bounds__(DST_THREADS, (R1 <= 16 && R2 <= 16) ? 5 : 1) k_dst(const GemmDesc* __restrict__ descs, Bufs bufs) {
   constexpr int L = R1 * R2, N = L / 2;
   constexpr int CPB = DST_THREADS / R2;      // columns per CTA
   constexpr int LDT = CPB + 1;               // tile row stride (complex)
