@@ -235,11 +235,10 @@ def stage_algorithmic(p, R: int, plan=None):
     }
 
 
-def roofline_summary(p, nrhs, plan, stages, steps, config, ms_max):
+def roofline_summary(p, nrhs, plan, stages, steps, config, ms_max, passes=1):
     """Roofline of the dominant stage and of the whole solve.  Stage work is per
-    solve pass; a step runs `passes` of them (1 + refinement passes, or the fast solves inside
-    a GMRES solve), counted from the step-2 z-solve launches (one per pass)."""
-    passes = max(1.0, stages.get("step2_zsolve", (0.0, steps))[1] / max(1, steps))
+    solve pass over all nrhs right-hand sides; a step runs `passes` of them (1 + refinement
+    passes, or the fast solves inside a GMRES solve)."""
     # roofline of the dominant stage (the kernel kind with the largest device time per step);
     # governing bound = whichever of flops/peak and bytes/peak is the larger time
     alg = stage_algorithmic(p, nrhs, plan)
@@ -251,7 +250,7 @@ def roofline_summary(p, nrhs, plan, stages, steps, config, ms_max):
     per_step_ms = st_ms / max(1, steps)
     flops, nbytes = alg.get(name, (None, None))
     # a solve stage runs once per pass; the refinement stages once per refinement
-    mult = st_launch / max(1, steps) if name.startswith("refine_") else passes
+    mult = max(1, passes - 1) if name.startswith("refine_") else passes
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
@@ -448,7 +447,7 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": p.unknowns * ne * (1 if blocks else world) / (float(t.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item()),
                "nrhs_per_gpu": ne}
-    roof = roofline_summary(p, nrhs, plan, stages, args.steps, args.config, ms_max)
+    roof = roofline_summary(p, nrhs, plan, stages, args.steps, args.config, ms_max, passes=1 + refine)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         ps, ts, threads = cpu_oracle_sample(p, args.cpu_nz, 1)
@@ -526,7 +525,8 @@ def run_hetero(args, rank, world, local_rank):
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
     value = p.unknowns * world / (ms_max * 1e-3)  # replicas: every rank solves its own copy
-    roof = roofline_summary(p, 1, plan, stages, args.steps, args.config, ms_max)
+    solves = stages.get("step2_zsolve", (0.0, args.steps))[1] / max(1, args.steps)  # one k_zs1 per solve
+    roof = roofline_summary(p, 1, plan, stages, args.steps, args.config, ms_max, passes=max(1.0, solves))
     e2e = None
     if not args.no_e2e:  # pinned host f -> device, solve, u -> host, every step
         fh = f.cpu().pin_memory()

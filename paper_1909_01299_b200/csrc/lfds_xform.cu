@@ -48,6 +48,19 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// (n1, n2) of column n + step from those of column n (n = n1 * N2 + n2), with the step's own
+// decomposition step = d1 * N2 + d2 precomputed once per thread (no division per column)
+struct ColStep {
+  int d1, d2;  // step <= 16, so both fit 32 bits
+  __device__ __forceinline__ ColStep(int step, int64_t N2)
+      : d1((int)(step / N2)), d2((int)(step - (step / N2) * N2)) {}
+  __device__ __forceinline__ void advance(int64_t& n1, int64_t& n2, int64_t N2) const {
+    n1 += d1;
+    n2 += d2;
+    if (n2 >= N2) { n2 -= N2; ++n1; }
+  }
+};
+
 template <bool REAL_S>
 struct XSmem {
   static constexpr int A_ELEMS = REAL_S ? XT_K * LDA_R : XT_K * LDA_C * 2;  // in doubles
@@ -207,6 +220,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
     // columns in store order: real S -> wn + 4j + q (j < 8); complex S -> wn + 8j' + 2q + h
     int64_t n = n0 + wn + (REAL_S ? q : 2 * q);
     int64_t n1 = n / N2, n2 = n - n1 * N2;
+    const ColStep c1(1, N2), c4(4, N2), c7(7, N2);
 #pragma unroll
     for (int e = 0; e < NJ; ++e) {
       if (n < N) {
@@ -221,10 +235,9 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
           C[(int64_t)row * D.sCi + off] = v;
         }
       }
-      const int step = REAL_S ? 4 : ((e & 1) ? 7 : 1);
-      n += step;
-      n2 += step;
-      while (n2 >= N2) { n2 -= N2; ++n1; }
+      if (REAL_S) { n += 4; c4.advance(n1, n2, N2); }
+      else if (e & 1) { n += 7; c7.advance(n1, n2, N2); }
+      else { n += 1; c1.advance(n1, n2, N2); }
     }
   }
 }
@@ -275,23 +288,23 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
   // A: 64 x 16 -> thread row tid/4, 4 consecutive j
   const int ai = tid >> 2, aj0 = (tid & 3) * 4;
   const bool arow_ok = (i0 + ai) < M;
-  int64_t bcol[4];
+  // KCONTIG: thread -> j = tid % 16, columns tid/16 + 16e (e < 4), offsets stepped from the
+  // first column in every chunk (no per-column registers to keep: this kernel is at the
+  // 128-register cap of two CTAs per SM); otherwise thread -> column tid % 64, rows tid/64 + 4e
   int bj, bn0;
-  if (KCONTIG) {  // thread -> j = tid % 16, columns tid/16 + 16e
+  int64_t bcol0, bn1_0, bn2_0;
+  if (KCONTIG) {
     bj = tid & 15;
     bn0 = tid >> 4;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t n = n0 + bn0 + 16 * e;
-      const int64_t n1 = n / N2, n2 = n - n1 * N2;
-      bcol[e] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
-    }
-  } else {        // thread -> column tid % 64, rows tid/64 + 4e
+  } else {
     bj = tid >> 6;
     bn0 = tid & 63;
+  }
+  {
     const int64_t n = n0 + bn0;
-    const int64_t n1 = n / N2, n2 = n - n1 * N2;
-    bcol[0] = (n < N) ? n1 * D.sB1 + n2 * D.sB2 : -1;
+    bn1_0 = n / N2;
+    bn2_0 = n - bn1_0 * N2;
+    bcol0 = (n < N) ? bn1_0 * D.sB1 + bn2_0 * D.sB2 : -1;
   }
   auto load_chunk = [&](int stage, int j0) {
     double2* As = reinterpret_cast<double2*>(xsm + stage * STAGE);
@@ -304,17 +317,25 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
     }
     if (KCONTIG) {
       const int j = j0 + bj;
+      int64_t n = n0 + bn0, n1 = bn1_0, n2 = bn2_0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const bool ok = bcol[e] >= 0 && j < K;
-        cp_async16(Bs + bj * LDB_C + bn0 + 16 * e, ok ? B + bcol[e] + j : B, ok);
+        const bool ok = n < N && j < K;
+        cp_async16(Bs + bj * LDB_C + bn0 + 16 * e, ok ? B + n1 * D.sB1 + n2 * D.sB2 + j : B, ok);
+        n += 16;
+        if (N2 == 1) {  // plane transforms: one column per n1
+          n1 += 16;
+        } else {        // block transforms (N2 = block height >= 16: one wrap at most)
+          n2 += 16;
+          while (n2 >= N2) { n2 -= N2; ++n1; }
+        }
       }
     } else {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int j = j0 + bj + 4 * e;
-        const bool ok = bcol[0] >= 0 && j < K;
-        cp_async16(Bs + (bj + 4 * e) * LDB_C + bn0, ok ? B + bcol[0] + (int64_t)j * D.sBj : B, ok);
+        const bool ok = bcol0 >= 0 && j < K;
+        cp_async16(Bs + (bj + 4 * e) * LDB_C + bn0, ok ? B + bcol0 + (int64_t)j * D.sBj : B, ok);
       }
     }
   };
@@ -366,6 +387,7 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
   {
     int64_t n = n0 + wn + 2 * q;
     int64_t n1 = n / N2, n2 = n - n1 * N2;
+    const ColStep c1(1, N2), c7(7, N2);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int j = e >> 1, h = e & 1;
@@ -380,10 +402,8 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
           C[(int64_t)row * D.sCi + off] = make_double2(re, im);
         }
       }
-      const int step = h ? 7 : 1;
-      n += step;
-      n2 += step;
-      while (n2 >= N2) { n2 -= N2; ++n1; }
+      if (h) { n += 7; c7.advance(n1, n2, N2); }
+      else { n += 1; c1.advance(n1, n2, N2); }
     }
   }
 }
