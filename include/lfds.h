@@ -80,7 +80,8 @@ void lfds_default_options(lfds_options* opt);
  *  lambda                        the shift of Eq. (wave2) (complex accepted, reading R11).
  *  if_x[n_if_x], if_y[n_if_y]    host, sorted 1-based interface nodes (width-1 planes,
  *                                reading R9); 2 <= node <= N-1, consecutive nodes >= 2 apart,
- *                                at most 16 per axis (17 blocks).
+ *                                at most 32 per axis (33 blocks; more than 16 only with the
+ *                                z-modal step 5, i.e. real z tables and options.s5_modal = 1).
  *                                n_if = 0 gives a single block (the global separable solve).
  *  opt                           may be NULL (defaults).
  *  *out                          receives the plan; release with lfds_destroy.

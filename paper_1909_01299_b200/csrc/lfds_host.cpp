@@ -756,8 +756,9 @@ static int setup_axis(Axis& A, int N, const lfds_z* h, int nif, const int* iface
   A.hh.resize(N);
   for (int i = 0; i < N; ++i) A.hh[i] = 0.5 * (A.h[i] + A.h[i + 1]);
   A.iface.assign(iface, iface + nif);
-  // step 5 contracts over the interface planes on the tensor pipe with |I| padded to 8 or 16
-  if (nif > 16) return fail(LFDS_EINVAL, "%s: at most 16 interfaces (17 blocks) per axis, got %d", name, nif);
+  // step 5 contracts over the interface planes on the tensor pipe with |I| padded to 8, 16 or 32
+  // (32: z-modal form only, checked once the z tables are known)
+  if (nif > 32) return fail(LFDS_EINVAL, "%s: at most 32 interfaces (33 blocks) per axis, got %d", name, nif);
   for (int a = 0; a < nif; ++a) {
     int v = A.iface[a];
     if (v < 2 || v > N - 1) return fail(LFDS_EINVAL, "%s: interface node %d outside 2..N-1", name, v);
@@ -925,6 +926,9 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
     P->info.z_eig_orth = zorth;
   }
   P->zt_scaled = ZTab{T.put(sa), T.put(sg), T.put(scv), T.put(se)};
+  if (!P->s5m && std::max(X.iface.size(), Y.iface.size()) > 16)
+    return fail(LFDS_EINVAL, "more than 16 interfaces per axis need the z-modal step 5 (real z tables, "
+                             "options.s5_modal = 1)");
   {  // step-6 lifting RHS is -sigma_k (sum of face terms): fold -sigma_k into the rows
     std::vector<zc> la(nz), lg(nz), lc(nz), le(nz);
     for (int k = 0; k < nz; ++k) {

@@ -86,8 +86,8 @@ struct S5Smem {
 };
 
 template <int KA>
-__global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
-  static_assert(KA % 8 == 0 && KA <= 16, "KA: |I| padded to 8 or 16");
+__global__ void __launch_bounds__(S5_THREADS, KA <= 16 ? 2 : 1) k_s5m(S5M S, Bufs bufs) {
+  static_assert(KA % 8 == 0 && KA <= 32, "KA: |I| padded to 8, 16 or 32");
   using SM = S5Smem<KA>;
   extern __shared__ __align__(16) double2 s5[];
   double2* Wt = s5;
@@ -137,12 +137,20 @@ __global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
   cp_wait<1>();  // fixed operands
   __syncthreads();
   // A fragments of phase A for this warp's 8 rows m = 8 warp + g (fixed over the l loop)
-  double3 fa1[KA / 4], fa2[KA / 4];
+  // (KA = 32: read from shared memory at each use instead, to stay within the register file)
+  constexpr bool AREG = KA <= 16;
+  constexpr int NFA = AREG ? KA / 4 : 1;
+  double3 fa1[NFA], fa2[NFA];
+  auto afrag = [&](const double2* Asm, int ks) {
+    const double2 v = Asm[(4 * ks + q) * LA + 8 * warp + g];
+    return make_double3(v.x, v.y, v.x + v.y);
+  };
+  if constexpr (AREG) {
 #pragma unroll
-  for (int ks = 0; ks < KA / 4; ++ks) {
-    const double2 v1 = A1[(4 * ks + q) * LA + 8 * warp + g], v2 = A2[(4 * ks + q) * LA + 8 * warp + g];
-    fa1[ks] = make_double3(v1.x, v1.y, v1.x + v1.y);
-    fa2[ks] = make_double3(v2.x, v2.y, v2.x + v2.y);
+    for (int ks = 0; ks < KA / 4; ++ks) {
+      fa1[ks] = afrag(A1, ks);
+      fa2[ks] = afrag(A2, ks);
+    }
   }
   const int mrow = 8 * warp + g, mglob = m0 + mrow;
   const bool mok = mglob < S.ny;
@@ -156,8 +164,8 @@ __global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
   for (int as = 0; as < KA / 8; ++as) zero3(p1[as]);
   // phase-C assignment: (b-tile, l-tile) pairs over the warps, K = m split in halves if needed
   constexpr int NPAIR = (KA / 8) * 4, HALVES = NPAIR >= 8 ? 1 : 8 / NPAIR, KSC = TM / 4 / HALVES;
-  const int pair = warp % NPAIR, half = warp / NPAIR;
-  const int cbs = pair / 4, cls = pair % 4;
+  constexpr int PSTEP = HALVES == 1 ? 8 : NPAIR;  // pairs of a warp: warp, warp + 8, ... (or one)
+  const int pair0 = warp % NPAIR, half = HALVES == 1 ? 0 : warp / NPAIR;
   for (int lt = 0; lt < nlt; ++lt) {
     const int bf = lt & 1, l0 = l_beg + lt * TL;
     cp_wait<0>();
@@ -171,12 +179,21 @@ __global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) zero3(c[nt]);
 #pragma unroll
-      for (int ks = 0; ks < KA / 4; ++ks)
+      for (int ks = 0; ks < KA / 4; ++ks) {
+        double3 x1, x2;
+        if constexpr (AREG) {
+          x1 = fa1[ks];
+          x2 = fa2[ks];
+        } else {
+          x1 = afrag(A1, ks);
+          x2 = afrag(A2, ks);
+        }
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
-          cmma3s(c[nt], fa1[ks], bx[(4 * ks + q) * LW + 8 * nt + g]);
-          cmma3s(c[nt], fa2[ks], b2[(4 * ks + q) * LW + 8 * nt + g]);
+          cmma3s(c[nt], x1, bx[(4 * ks + q) * LW + 8 * nt + g]);
+          cmma3s(c[nt], x2, b2[(4 * ks + q) * LW + 8 * nt + g]);
         }
+      }
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -199,7 +216,9 @@ __global__ void __launch_bounds__(S5_THREADS, 2) k_s5m(S5M S, Bufs bufs) {
       for (int as = 0; as < KA / 8; ++as) cmma3(p1[as], aw, bx[(8 * as + g) * LW + 4 * ks + q]);
     }
     // ---- phase C: P2 partial[b][l] = sum_{m in tile} W_y[I_b][m] W^[m][l]
-    {
+#pragma unroll
+    for (int pair = pair0; pair < NPAIR; pair += PSTEP) {
+      const int cbs = pair / 4, cls = pair % 4;
       double p2[3][2];
       zero3(p2);
 #pragma unroll
@@ -268,7 +287,7 @@ __global__ void k_p2sum(S5M S, Bufs bufs) {
 
 int s5m_ka(int nifx, int nify) {
   const int n = nifx > nify ? nifx : nify;
-  return n <= 8 ? 8 : n <= 16 ? 16 : 0;
+  return n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 0;
 }
 int s5m_mtiles(int ny) { return (ny + TM - 1) / TM; }
 
@@ -282,10 +301,14 @@ cudaError_t launch_s5m(const S5M& S, const Bufs& bufs, cudaStream_t st) {
       const size_t sm = S5Smem<8>::TOTAL * sizeof(double2);
       if ((e = cudaFuncSetAttribute(k_s5m<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
       k_s5m<8><<<grid, S5_THREADS, sm, st>>>(S, bufs);
-    } else {
+    } else if (ka == 16) {
       const size_t sm = S5Smem<16>::TOTAL * sizeof(double2);
       if ((e = cudaFuncSetAttribute(k_s5m<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
       k_s5m<16><<<grid, S5_THREADS, sm, st>>>(S, bufs);
+    } else {
+      const size_t sm = S5Smem<32>::TOTAL * sizeof(double2);
+      if ((e = cudaFuncSetAttribute(k_s5m<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
+      k_s5m<32><<<grid, S5_THREADS, sm, st>>>(S, bufs);
     }
     if ((e = cudaGetLastError())) return e;
   }

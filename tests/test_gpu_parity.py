@@ -305,10 +305,10 @@ def test_step5_modal_matches_sweeps(name):
     assert rel(Um[0], ref) < TOL
 
 
-@pytest.mark.parametrize("nifx,nify", [(12, 9), (16, 3), (0, 11), (3, 16)])
+@pytest.mark.parametrize("nifx,nify", [(12, 9), (16, 3), (0, 11), (3, 16), (31, 20), (17, 32)])
 def test_step5_modal_interface_counts(nifx, nify):
-    """|I| padded to 8 and 16 on the tensor pipe, one axis without interfaces; ragged m- and
-    l-tiles (N = 70, 90)."""
+    """|I| padded to 8, 16 and 32 on the tensor pipe (32: the sqrt(N)-block regime of SPEC
+    S:68-85), one axis without interfaces; ragged m- and l-tiles (N = 70, 90)."""
     nx, ny, nz = 70, 90, 11
     rng = np.random.default_rng(nifx * 100 + nify)
     hx = np.ones(nx + 1) + 0.4j * (np.arange(nx + 1) < 6)

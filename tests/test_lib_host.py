@@ -59,7 +59,6 @@ def test_host_only_plan_refuses_compute(lfds):
 
 
 @pytest.mark.parametrize("bad", [dict(iface_x=[5, 6]), dict(iface_x=[1]), dict(iface_x=[44]),
-                                 dict(iface_x=list(range(2, 38, 2))),  # 18 interfaces: more than 16
                                  dict(iface_x=[9, 4])])
 def test_setup_rejects_bad_partitions(lfds, bad):
     p = shrunken("c3")
@@ -171,3 +170,19 @@ def test_z_modal_form_needs_real_z_tables():
     assert host_plan(pc).info()["s5_modal"] == 0
     assert host_plan(dataclasses.replace(p, lam=p.lam + 0.01j)).info()["s5_modal"] == 0
     assert host_plan(p, s5_modal=False).info()["s5_modal"] == 0
+
+
+def test_interface_count_limits():
+    """Up to 32 interfaces per axis with the z-modal step 5 (KA = 32 on the tensor pipe); more
+    than 16 with complex z tables (per-mode sweeps) or s5_modal = 0 is rejected at setup."""
+    from paper_1909_01299_b200.lfds import LfdsError
+    p = shrunken("c3").with_partition(list(range(2, 38, 2)), [])  # 18 interfaces
+    assert host_plan(p).info()["s5_modal"] == 1
+    for bad in (dict(s5_modal=False),):
+        with pytest.raises(LfdsError) as e:
+            host_plan(p, **bad)
+        assert e.value.code == 1
+    pc = dataclasses.replace(p, sigma_node=p.sigma_node * (1 + 0.1j), sigma_edge=p.sigma_edge * (1 + 0.1j))
+    with pytest.raises(LfdsError) as e:
+        host_plan(pc)
+    assert e.value.code == 1

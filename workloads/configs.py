@@ -33,7 +33,7 @@ from typing import Callable, List, Optional
 
 import numpy as np
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c4j")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c4j", "c4q")
 
 
 def _rng(cfg: int, stream: int) -> np.random.Generator:
@@ -218,6 +218,11 @@ def make_problem(name: str) -> Problem:
         # node, six uniform core blocks of 159 nodes (sine transforms of length 320) between
         j = [32, 192, 352, 512, 672, 832, 992]
         return make_problem("c4").with_partition(j, j, name="c4j")
+    if name == "c4q":
+        # C4 with the sqrt(N)-block partition (SPEC S:68-85's second cost regime): 32 x 32 blocks of
+        # 31 nodes, interfaces at multiples of 32 (the first and last blocks are the PML tails)
+        j = [32 * b for b in range(1, 32)]
+        return make_problem("c4").with_partition(j, j, name="c4q")
     raise KeyError(name)
 
 
