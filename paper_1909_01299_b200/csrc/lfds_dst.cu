@@ -428,12 +428,18 @@ cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, 
   const int L = 2 * (n + 1);
 #define DL(A, B) return kcontig ? dst_launch<A, B, true>(d_descs, ndesc, maxN, bufs, st) \
                                 : dst_launch<A, B, false>(d_descs, ndesc, maxN, bufs, st)
-  switch (L) {
+  switch (L) {  // contiguous columns: warp-autonomous kernel; strided columns: CTA tiles (coalescing)
     case 16: DL(4, 4);
-    case 32: DL(4, 8);
-    case 64: DL(8, 8);
-    case 128: DL(8, 16);
-    case 256:  // contiguous columns: warp-autonomous kernel; strided columns: CTA tiles (coalescing)
+    case 32:
+      if (kcontig) return dstw_launch<4, 8>(d_descs, ndesc, maxN, bufs, st);
+      return dst_launch<4, 8, false>(d_descs, ndesc, maxN, bufs, st);
+    case 64:
+      if (kcontig) return dstw_launch<8, 8>(d_descs, ndesc, maxN, bufs, st);
+      return dst_launch<8, 8, false>(d_descs, ndesc, maxN, bufs, st);
+    case 128:
+      if (kcontig) return dstw_launch<8, 16>(d_descs, ndesc, maxN, bufs, st);
+      return dst_launch<8, 16, false>(d_descs, ndesc, maxN, bufs, st);
+    case 256:
       if (kcontig) return dstw_launch<16, 16>(d_descs, ndesc, maxN, bufs, st);
       return dst_launch<16, 16, false>(d_descs, ndesc, maxN, bufs, st);
     case 512: DL(16, 32);

@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/${tag}_pytest_gpu.log 2>&1
 echo "pytest gpu exit $?" >> gpurun_out/${tag}_pytest_gpu.log; tail -2 gpurun_out/${tag}_pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1; echo "smoke exit $?"; tail -1 gpurun_out/${tag}_smoke.log
-for c in c4 c1 c2 c3 c5 c4j c4h; do
+for c in c4 c1 c2 c3 c5 c4j c4q c4h; do
   timeout 1200 python bench.py --config $c > gpurun_out/${tag}_bench_$c.json 2> gpurun_out/${tag}_bench_$c.err
   python -c "import json; d=json.load(open('gpurun_out/${tag}_bench_$c.json')); print('$c', round(d['ms_per_step'],3), 'ms', '%.3e'%d['value'], 'e2e', d['e2e'] and '%.3e'%d['e2e']['value'], 'cpu', d['cpu_baseline'] and '%.3e'%d['cpu_baseline']['value'], d['roofline']['kernel'], round(d['roofline']['frac'],3), 'solve', round(d['roofline']['solve']['frac'],3))" || tail -3 gpurun_out/${tag}_bench_$c.err
 done
