@@ -345,7 +345,9 @@ def run_ours(args, rank, world, local_rank):
     if blocks and refine:
         raise SystemExit("block-sharded solves do not refine; use --shard rhs for " + args.config)
     t0 = time.perf_counter()
-    plan = Plan.from_problem(p, device=local_rank, refine=refine, profile=True,
+    # the timed solve replays a CUDA graph of its launches (options.graph; stage events are graph
+    # nodes); the sharded path runs phase by phase with the exchanges in between
+    plan = Plan.from_problem(p, device=local_rank, refine=refine, profile=True, graph=not blocks,
                              rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0))
     setup_s = time.perf_counter() - t0
     part = lfds_dist.shard(plan, rank, world) if blocks else None

@@ -62,9 +62,12 @@ typedef struct {
   int s5_modal;     /* 1: step 5 with the z direction diagonalised too, when the z tables  */
                     /* are real (interface-only computation, no z sweeps);  */
                     /* 0: per-mode tridiagonal z-sweeps (the paper's form)   */
+  int graph;        /* 1: lfds_solve captures its launches into a CUDA graph and replays  */
+                    /* it while (f, u, nrhs, workspace) repeat (refine >= 0 only); 0: off */
 } lfds_options;
 
-/* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1. */
+/* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1,
+ * graph 0. */
 void lfds_default_options(lfds_options* opt);
 
 /*

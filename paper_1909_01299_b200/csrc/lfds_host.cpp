@@ -78,7 +78,7 @@ const char* kStageNames[ST_COUNT] = {
     "step7_x_sine", "step7_x_dense", "step7_write_iface", "refine_residual", "refine_axpy"};
 
 struct Profiler {
-  struct Rec { int stage, launches; cudaEvent_t a, b; };
+  struct Rec { int stage, launches; cudaEvent_t a, b; bool graph = false; };  // graph: events owned by a graph
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
   double ms[ST_COUNT] = {0};
@@ -88,6 +88,15 @@ struct Profiler {
     cudaEvent_t e = pool.back(); pool.pop_back(); return e;
   }
 };
+
+// Stage-timing event record: inside a stream capture it must be an external event node
+// (cudaEventRecordExternal), so that every graph replay re-records it for cudaEventElapsedTime.
+static inline void prof_record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else cudaEventRecord(e, st);
+}
 
 struct StageDescs {
   int64_t off = 0;  // index of the first desc in the device desc array
@@ -143,6 +152,17 @@ struct lfds_plan {
   lfds_info info{};
   int launches = 0;
   Profiler prof;
+  // CUDA graph of the last lfds_solve (options.graph): replayed while the key repeats
+  cudaGraphExec_t gexec = nullptr;
+  const void* gkey_f = nullptr;
+  void* gkey_u = nullptr;
+  void* gkey_ws = nullptr;
+  size_t gkey_wsb = 0;
+  int gkey_nrhs = 0;
+  std::vector<Profiler::Rec> grecs;  // stage events captured in the graph (re-recorded per replay)
+  lfds_report grep{};
+  cudaStream_t cap_stream = nullptr;  // capture happens on a private stream (the legacy default
+                                      // stream cannot be captured); the graph runs on the caller's
   // block sharding (lfds_set_partition): owned blocks, the global x-mode range of step 5,
   // and whether this rank adds the b-terms of the interface residual and writes u on the planes
   std::vector<char> own;
@@ -527,12 +547,12 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   auto begin = [&](int stg) {
     cur_stage = stg;
     cur_launch0 = P->launches;
-    if (prof) { ev_a = P->prof.get(); cudaEventRecord(ev_a, st); }
+    if (prof) { ev_a = P->prof.get(); prof_record(ev_a, st); }
   };
   auto end = [&]() {
     if (prof && cur_stage >= 0) {
       cudaEvent_t b = P->prof.get();
-      cudaEventRecord(b, st);
+      prof_record(b, st);
       P->prof.recs.push_back({cur_stage, P->launches - cur_launch0, ev_a, b});
     }
     cur_stage = -1;
@@ -717,6 +737,7 @@ void lfds_default_options(lfds_options* o) {
   o->rhs_chunk = 0;
   o->profile = 0;
   o->s5_modal = 1;
+  o->graph = 0;
 }
 
 int lfds_stage_count(void) { return ST_COUNT; }
@@ -730,8 +751,10 @@ int lfds_stage_times(lfds_plan* P, double* ms, int* launches) {
     CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
     P->prof.ms[r.stage] += t;
     P->prof.launches[r.stage] += r.launches;
-    P->prof.pool.push_back(r.a);
-    P->prof.pool.push_back(r.b);
+    if (!r.graph) {
+      P->prof.pool.push_back(r.a);
+      P->prof.pool.push_back(r.b);
+    }
   }
   P->prof.recs.clear();
   for (int i = 0; i < ST_COUNT; ++i) {
@@ -1078,12 +1101,12 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         const bool auto_mode = P->opt.refine < 0;
         if (auto_mode) CUDA_TRY(cudaMemsetAsync(norms, 0, sizeof(double) * 2 * Rc, st));
         cudaEvent_t ra = nullptr;
-        if (P->opt.profile) { ra = P->prof.get(); cudaEventRecord(ra, st); }
+        if (P->opt.profile) { ra = P->prof.get(); prof_record(ra, st); }
         CUDA_TRY(launch_residual(X.N, Y.N, P->nz, Rc, dt, P->opt.residual_dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff,
                                  Y.hhoff, P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()),
                                  P->t_dd, b.p[B_U], b.p[B_F], res, 1, auto_mode ? norms : nullptr, b, st));
         P->launches++;
-        if (P->opt.profile) { cudaEvent_t rb2 = P->prof.get(); cudaEventRecord(rb2, st); P->prof.recs.push_back({ST_RESID, 1, ra, rb2}); }
+        if (P->opt.profile) { cudaEvent_t rb2 = P->prof.get(); prof_record(rb2, st); P->prof.recs.push_back({ST_RESID, 1, ra, rb2}); }
         double worst = -1.0;
         if (auto_mode) {
           std::vector<double> hn(2 * Rc);
@@ -1101,10 +1124,10 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         rb.p[B_U] = res;
         if ((rc = run_pass(P, *pp_ref, rb, Rc, 0, 0, st))) return rc;
         cudaEvent_t xa = nullptr;
-        if (P->opt.profile) { xa = P->prof.get(); cudaEventRecord(xa, st); }
+        if (P->opt.profile) { xa = P->prof.get(); prof_record(xa, st); }
         CUDA_TRY(launch_axpy_u(vol * Rc, dt, res, b.p[B_U], st));
         P->launches++;
-        if (P->opt.profile) { cudaEvent_t xb = P->prof.get(); cudaEventRecord(xb, st); P->prof.recs.push_back({ST_AXPY, 1, xa, xb}); }
+        if (P->opt.profile) { cudaEvent_t xb = P->prof.get(); prof_record(xb, st); P->prof.recs.push_back({ST_AXPY, 1, xa, xb}); }
         passes++;
       }
     }
@@ -1367,7 +1390,49 @@ int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws,
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
   if (nrhs < 1 || !f_dev || !u_dev || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
   if (((uintptr_t)f_dev | (uintptr_t)u_dev | (uintptr_t)ws) & 15) return fail(LFDS_EINVAL, "pointers must be 16-byte aligned");
-  return solve_impl(P, f_dev, u_dev, nrhs, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!P->opt.graph || P->opt.refine < 0) return solve_impl(P, f_dev, u_dev, nrhs, ws, ws_bytes, st);
+  // CUDA graph: captured once per (f, u, nrhs, workspace) and replayed; the stage events of a
+  // profiled plan are graph nodes, re-recorded by every replay
+  const bool hit = P->gexec && P->gkey_f == f_dev && P->gkey_u == u_dev && P->gkey_ws == ws &&
+                   P->gkey_wsb == ws_bytes && P->gkey_nrhs == nrhs;
+  if (!hit) {
+    if (P->gexec) {
+      cudaGraphExecDestroy(P->gexec);
+      P->gexec = nullptr;
+      for (auto& r : P->grecs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+      P->grecs.clear();
+    }
+    // pass plans allocate device descriptors on first use: build them before capturing
+    const int R = chunk_of(P, nrhs), dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
+    for (int r0 = 0; r0 < nrhs; r0 += R) {
+      PassPlan* pp;
+      int rc;
+      if ((rc = get_pass(P, std::min(R, nrhs - r0), dt, dt, &pp))) return rc;
+      if (P->opt.refine != 0 && (rc = get_pass(P, std::min(R, nrhs - r0), 0, 0, &pp))) return rc;
+    }
+    // events already pending in the profile belong to earlier solves: keep them out of the graph
+    const size_t nrec0 = P->prof.recs.size();
+    if (!P->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->cap_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeRelaxed));
+    const int rc = solve_impl(P, f_dev, u_dev, nrhs, ws, ws_bytes, P->cap_stream);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(P->cap_stream, &g);
+    if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+    CUDA_TRY(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&P->gexec, g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(ie);
+    P->grecs.assign(P->prof.recs.begin() + nrec0, P->prof.recs.end());
+    P->prof.recs.resize(nrec0);
+    for (auto& r : P->grecs) r.graph = true;
+    P->gkey_f = f_dev; P->gkey_u = u_dev; P->gkey_ws = ws; P->gkey_wsb = ws_bytes; P->gkey_nrhs = nrhs;
+    P->grep = P->report;
+  }
+  CUDA_TRY(cudaGraphLaunch(P->gexec, st));
+  P->report = P->grep;
+  for (const auto& r : P->grecs) P->prof.recs.push_back(r);  // this replay's stage events
+  return LFDS_OK;
 }
 
 static int solve_host_impl(lfds_plan* P, const void* f_host, void* u_host, int nrhs, void* ws, size_t ws_bytes,
@@ -1477,7 +1542,12 @@ void lfds_destroy(lfds_plan* P) {
     cudaFree(kv.second.d_own);
   }
   if (P->d_tab) cudaFree(P->d_tab);
-  for (auto& r : P->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  if (P->gexec) cudaGraphExecDestroy(P->gexec);
+  if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
+  for (auto& r : P->grecs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto& r : P->prof.recs)
+    if (r.graph) continue;
+    else { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : P->prof.pool) cudaEventDestroy(e);
   delete P;
 }

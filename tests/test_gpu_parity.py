@@ -321,3 +321,26 @@ def test_step5_modal_interface_counts(nifx, nify):
     assert plan.info()["s5_modal"] == 1
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
     assert rel(U[0], ref) < TOL, rel(U[0], ref)
+
+
+@pytest.mark.parametrize("name,refine", [("c2", 1), ("c3", 0), ("c4", 0)])
+def test_graph_replay_matches_stream_solve(name, refine):
+    """options.graph: the captured CUDA graph replays bit-identically to the stream-ordered solve;
+    new buffers trigger a recapture; a profiled plan still reports its stage times."""
+    from paper_1909_01299_b200 import Plan
+    p = shrunken(name, nrhs=2)
+    F = torch.from_numpy(p.rhs_all()).cuda()
+    ua = Plan.from_problem(p, refine=refine).solve(F)
+    b = Plan.from_problem(p, refine=refine, graph=True, profile=True)
+    U = torch.empty_like(F)
+    b.solve(F, out=U)          # capture + first replay
+    first = U.clone()
+    b.solve(F, out=U)          # replay
+    torch.cuda.synchronize()
+    assert torch.equal(first, ua) and torch.equal(U, ua)
+    st = b.stage_times()
+    assert st["step2_zsolve"][0] > 0 and st["step2_zsolve"][1] >= 2
+    U2 = torch.empty_like(F)
+    b.solve(F, out=U2)         # new output buffer: recaptured
+    torch.cuda.synchronize()
+    assert torch.equal(U2, ua)
