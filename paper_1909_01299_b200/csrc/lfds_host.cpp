@@ -1209,6 +1209,19 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
     CUDA_TRY(cudaStreamSynchronize(st));  // hc must outlive the copy
     return LFDS_OK;
   };
+  // W += V c and ||W||^2 of the result in the same sweep (the Gram-Schmidt update)
+  auto axpy_norm = [&](int cnt, const std::vector<zc>& c, double& nrm2) -> int {
+    std::vector<double2> hc(cnt);
+    for (int i = 0; i < cnt; ++i) hc[i] = make_double2(c[i].real(), c[i].imag());
+    CUDA_TRY(cudaMemcpyAsync(coef, hc.data(), sizeof(double2) * cnt, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(launch_maxpy_norm(n, cnt, V, vs, coef, W, part, st));
+    ++kl;
+    CUDA_TRY(cudaMemcpyAsync(hp.data(), part, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    nrm2 = 0;
+    for (int b = 0; b < KRYLOV_DOT_BLOCKS; ++b) nrm2 += hp[(size_t)b * 80].x;  // fixed order
+    return LFDS_OK;
+  };
   int rc;
   auto solve = [&](const void* src, void* dst) -> int {
     const int r = solve_impl(P, src, dst, 1, sws, sws_bytes, st);
@@ -1237,20 +1250,24 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
     for (int j = 0; j < m; ++j) {
       double2* Vj = V + (int64_t)j * vs;
       if ((rc = solve(Vj, S))) return rc;   // S V_j
-      CUDA_TRY(launch_fdie(n, Vj, DL, S, W, st));                           // W = V_j + dlam S V_j
+      // (I + dlam S) V_j = V_j + z with z = dlam S V_j: orthogonalise z only (its V_j part is
+      // exact: H[j][j] gets + 1), so no cancellation against the identity part of the operator
+      CUDA_TRY(launch_fdie(n, nullptr, DL, S, W, st));                      // W = z = dlam S V_j
       ++kl;
       h.assign(j + 1, zc(0));
+      double wn2 = 0, wn2_new = 0;
       for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, repeated when needed
         if ((rc = dots(j + 1, V, W, h2, pass == 0))) return rc;
+        if (pass == 0) wn2 = h2[j + 1].real();
         std::vector<zc> c(j + 1);
-        double hh = 0;
-        for (int i = 0; i <= j; ++i) { c[i] = -h2[i]; h[i] += h2[i]; hh += std::norm(h2[i]); }
-        if ((rc = axpy(j + 1, c, W))) return rc;
-        // Kahan-Parlett: a second pass only if the projection removed most of w (cancellation)
-        if (pass == 0 && hh < 0.51 * h2[j + 1].real()) break;
+        for (int i = 0; i <= j; ++i) { c[i] = -h2[i]; h[i] += h2[i]; }
+        if ((rc = axpy_norm(j + 1, c, wn2_new))) return rc;
+        // Kahan-Parlett: a second pass only if the projection removed most of w (||w'|| < ||w|| / sqrt2)
+        if (wn2_new >= 0.5 * wn2) break;
+        wn2 = wn2_new;
       }
-      if ((rc = dots(1, W, W, d))) return rc;
-      const double hn = std::sqrt(std::max(0.0, d[0].real()));
+      const double hn = std::sqrt(std::max(0.0, wn2_new));
+      h[j] += 1.0;  // the identity part of (I + dlam S) V_j
       for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = h[i];
       for (int i = 0; i < j; ++i) {  // previous Givens rotations
         const zc a = H[(size_t)i * m + j], b = H[(size_t)(i + 1) * m + j];

@@ -127,6 +127,8 @@ cudaError_t launch_dots(int64_t n, int cnt, const double2* V, int64_t vstride, c
                         cudaStream_t st, int with_self = 0);
 cudaError_t launch_maxpy(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* coef, double2* w,
                          cudaStream_t st);
+cudaError_t launch_maxpy_norm(int64_t n, int cnt, const double2* V, int64_t vstride, const double2* coef, double2* w,
+                              double2* partial, cudaStream_t st);  // w += V c; partial[blk*80] = ||w||^2 part
 cudaError_t launch_scale(int64_t n, double2 alpha, const double2* w, double2* out, cudaStream_t st);
 
 int s5m_ka(int nifx, int nify);   // padded |I| (8 or 16), 0 = unsupported
