@@ -334,8 +334,13 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   stage(pp.s3y, std::move(v)); v.clear();
   // step 5: R1[a][rk][m] = sum_q W_y[q][m] RX[a][rk][q];  R2[b][rk][l] = sum_p W_x[p][l] RY[b][rk][p]  (b-units)
   // (both in one launch: the two contractions are independent)
+  // (block sharding: step 5 of this rank reads R2[b][rk][l] only for its x-modes l in
+  // [l_begin, l_end), so only those rows of W_x^T RY are formed)
+  const int l0s = P->sharded ? P->l_begin : 0, l1s = P->sharded ? P->l_end : Nx;
   if (nifx) v.push_back(gd(Y.Wg, 1, Ny, Ny, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
-  if (nify) v.push_back(gd(X.Wg, 1, Nx, Nx, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2, 1, Nx, 0, (int)(nify * RZ), 1, 0));
+  if (nify && l1s > l0s)
+    v.push_back(gd(X.Wg + l0s, 1, Nx, l1s - l0s, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2 + l0s, 1, Nx, 0,
+                   (int)(nify * RZ), 1, 0));
   stage(pp.s5r1, std::move(v)); v.clear();
   // P1, P2 (projections of w^ onto the planes): k_projm, see run_pass
   // w on the planes: WX[a][rk][q] = sum_m W_y[q][m] P1[a][rk][m];  WY[b][rk][p] = sum_l W_x[p][l] P2[b][rk][l]
@@ -345,8 +350,9 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   if (pp.s5m) {  // z-modal step 5: R~[a][r][t][m] = sum_k Z[k][t] R[a][r][k][m]; P = Z P~ (real Z)
     if (nifx) v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r1, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.r1t, Ny,
                              (int64_t)Nz * Ny, 1, nifx * R, Ny, 0));
-    if (nify) v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r2, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.r2t, Nx,
-                             (int64_t)Nz * Nx, 1, nify * R, Nx, 0));
+    if (nify && l1s > l0s)
+      v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r2 + l0s, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.r2t + l0s, Nx,
+                     (int64_t)Nz * Nx, 1, nify * R, l1s - l0s, 0));
     stage(pp.s5zf, std::move(v)); v.clear();
     if (nifx) v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p1t, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.p1, Ny,
                              (int64_t)Nz * Ny, 1, nifx * R, Ny, 0));
