@@ -1,0 +1,38 @@
+"""CPU checks of bench.py's accounting (no GPU): the algorithmic work per stage and the roofline
+arithmetic that the JSON line reports."""
+import bench
+from workloads import make_problem
+
+
+def test_stage_algorithmic_c4_matches_the_survey_totals():
+    """C4 grid: dense-transform flops (8 per complex MAC) and z-solve bytes (32 per unknown) per
+    stage, from the block sizes."""
+    p = make_problem("c4")
+    alg = bench.stage_algorithmic(p, 1, None)  # plan=None: every block counted as complex dense
+    # with plan=None all 64 blocks are dense in both directions (block sizes 7 x 127 and 128):
+    # per direction sum_ij n_i n_j nz x 8 n_dir flops
+    b = [127] * 7 + [128]
+    per_dir = sum(bi * bj * 256 * 8 * bi for bi in b for bj in b)
+    dense = sum(alg[k][0] for k in ("step1_x_dense", "step1_y_dense", "step7_y_dense", "step7_x_dense"))
+    assert abs(dense - 4 * per_dir) < 1e-9 * dense
+    assert alg["step2_zsolve"] == (None, 32.0 * sum(bi * bj for bi in b for bj in b) * 256)
+
+
+def test_roofline_counts_passes_per_step():
+    p = make_problem("c2")
+    stages = {"step2_zsolve": (2.0, 2), "step6_zsolve_lift": (4.0, 2), "refine_residual": (1.0, 1)}
+    r1 = bench.roofline_summary(p, 1, None, stages, 1, "c2", 10.0, passes=1)
+    r2 = bench.roofline_summary(p, 1, None, stages, 1, "c2", 10.0, passes=2)
+    assert r1["kernel"] == r2["kernel"] == "step6_zsolve_lift"
+    assert abs(r2["achieved"] - 2 * r1["achieved"]) < 1e-9 * r1["achieved"]
+    assert abs(r2["solve"]["t_roof_ms"] - 2 * r1["solve"]["t_roof_ms"]) < 1e-12
+    assert r1["unit"] == "GB/s" and r1["bound"] == "hbm" and 0 < r1["frac"] == r1["achieved"] / r1["peak"]
+
+
+def test_refinement_stage_counted_once_per_refinement():
+    p = make_problem("c2")
+    stages = {"refine_residual": (5.0, 1), "step2_zsolve": (1.0, 2)}
+    r = bench.roofline_summary(p, 1, None, stages, 1, "c2", 10.0, passes=2)
+    alg = bench.stage_algorithmic(p, 1, None)
+    assert r["kernel"] == "refine_residual"
+    assert abs(r["achieved"] - alg["refine_residual"][1] / 5e-3 / 1e9) < 1e-6 * r["achieved"]
