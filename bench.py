@@ -44,6 +44,10 @@ UNIT = "unknowns/s"
 # the refined solution, tests/test_gpu_parity.py::test_full_size_c5_chunked_vs_oracle) -> one
 # double-double refinement pass each; C1, C3, C4 need none.
 REFINE = {"c1": 0, "c2": 1, "c3": 0, "c4": 0, "c5": 1}
+# the refinement residual in fp64 already meets the 1e-9 bar on both (tools/single_pass_error.py:
+# C5 2.5e-10, C2 1.9e-16 against the oracle's 80-bit-refined solution; double-double reaches
+# 4.4e-14 / 3.6e-18 at ~6x the residual cost), so the timed step uses the fp64 residual
+RESIDUAL_DD = {"c2": False, "c5": False}
 # right-hand sides per pipeline pass (workspace scales with it): C5's 64 RHS x 0.84 GB per
 # array do not fit next to f and u in one pass; 16 per pass keeps the workspace at ~35 GB
 RHS_CHUNK = {"c5": 16}
@@ -347,8 +351,9 @@ def run_ours(args, rank, world, local_rank):
     t0 = time.perf_counter()
     # the timed solve replays a CUDA graph of its launches (options.graph; stage events are graph
     # nodes); the sharded path runs phase by phase with the exchanges in between
-    plan = Plan.from_problem(p, device=local_rank, refine=refine, profile=True, graph=not blocks,
-                             rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0))
+    res_dd = RESIDUAL_DD.get(args.config, True)
+    plan = Plan.from_problem(p, device=local_rank, refine=refine, residual_dd=res_dd, profile=True,
+                             graph=not blocks, rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0))
     setup_s = time.perf_counter() - t0
     part = lfds_dist.shard(plan, rank, world) if blocks else None
     dt = torch.float64 if p.real else torch.complex128
@@ -465,6 +470,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": args.config, "nx": p.nx, "ny": p.ny, "nz": p.nz,
                        "blocks": [len(p.iface_x) + 1, len(p.iface_y) + 1], "nrhs_per_gpu": nrhs,
                        "refine_passes": refine,
+                       "refine_residual": ("double-double" if res_dd else "fp64") if refine else None,
                        "parallelism": (f"block-sharded x{world} (LPT blocks, step-5 modes, 2 NCCL all-reduces)"
                                        if blocks else f"rhs-sharded x{world}" if world > 1 else "1 gpu"),
                        "l2": "inputs larger than L2 (no flush)" if p.unknowns * 16 > 126e6 else "L2-resident",

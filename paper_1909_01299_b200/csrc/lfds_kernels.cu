@@ -389,18 +389,19 @@ __global__ void __launch_bounds__(128) k_residual(ResParams P, const void* __res
     const cplx V = cx * cy * cz;
     cplx res, bnorm;
     if (!P.dd) {
-      const cplx hx0 = ld(TAB + P.hx + i), hx1 = ld(TAB + P.hx + i + 1);
-      const cplx hy0 = ld(TAB + P.hy + j), hy1 = ld(TAB + P.hy + j + 1);
-      const cplx hz0 = ld(TAB + P.hz + k), hz1 = ld(TAB + P.hz + k + 1);
-      const cplx se0 = ld(TAB + P.sige + k), se1 = ld(TAB + P.sige + k + 1);
-      cplx tx = (ur - uc) * cinv(hx1) - (uc - ul) * cinv(hx0);
-      cplx ty = (un - uc) * cinv(hy1) - (uc - us) * cinv(hy0);
-      cplx tz = se1 * (ut - uc) * cinv(hz1) - se0 * (uc - ub) * cinv(hz0);
-      cplx Au = sg * tx * cy * cz + sg * ty * cx * cz + tz * cx * cy + lam * uc * V;
-      cplx b = fv * V;
-      res = b - Au;
-      bnorm = b;
-      if (P.to_f) res = res * cinv(V);
+      // fp64: the same f-units evaluation from the per-node stencil tables (their leading
+      // doubles), no per-point reciprocals
+      auto t64 = [&](int64_t off, int n, int e) {
+        const double2 a = __ldg(TAB + off + 4 * n + 2 * e), b = __ldg(TAB + off + 4 * n + 2 * e + 1);
+        return mk(a.x, b.x);
+      };
+      const cplx hx = (ur - uc) * t64(P.rxd, i, 1) - (uc - ul) * t64(P.rxd, i, 0);
+      const cplx hy = (un - uc) * t64(P.ryd, j, 1) - (uc - us) * t64(P.ryd, j, 0);
+      const cplx hz = (ut - uc) * t64(P.szd, k, 1) - (uc - ub) * t64(P.szd, k, 0);
+      const cplx Lu = sg * (hx + hy) + hz + lam * uc;
+      const cplx rf = fv - Lu;
+      res = P.to_f ? rf : rf * V;
+      bnorm = fv * V;
     } else {
       auto tdd = [&](int64_t off, int n, int e) {  // node table: [n][cl, cr], 2 slots each
         const double2 a = __ldg(TAB + off + 4 * n + 2 * e), b = __ldg(TAB + off + 4 * n + 2 * e + 1);

@@ -24,12 +24,12 @@ t0 = time.time()
 ref = oracle.solve(p, F[0])
 print(f"{name} oracle (ii) + 80-bit refinement: {time.time() - t0:.1f} s")
 f = torch.from_numpy(F).cuda()
-for modal in (True, False):
-    for refine in (0, 1):
-        plan = Plan.from_problem(p, s5_modal=modal, refine=refine)
-        u = plan.solve(f).cpu().numpy()[0]
-        err = float(np.linalg.norm(u - ref) / np.linalg.norm(ref))
-        _, norms = plan.residual(torch.from_numpy(u[None]).cuda(), f, dd=True)
-        print(f"{name} s5_modal={int(modal)} refine={refine}: rel error {err:.3e}, "
-              f"rel residual {float(norms[0, 0] / norms[0, 1]):.3e}")
-        plan.close()
+cases = [(True, 0, True), (True, 1, True), (True, 1, False), (False, 0, True), (False, 1, True)]
+for modal, refine, dd in cases:
+    plan = Plan.from_problem(p, s5_modal=modal, refine=refine, residual_dd=dd)
+    u = plan.solve(f).cpu().numpy()[0]
+    err = float(np.linalg.norm(u - ref) / np.linalg.norm(ref))
+    _, norms = plan.residual(torch.from_numpy(u[None]).cuda(), f, dd=True)
+    print(f"{name} s5_modal={int(modal)} refine={refine} residual_dd={int(dd)}: rel error {err:.3e}, "
+          f"rel residual {float(norms[0, 0] / norms[0, 1]):.3e}")
+    plan.close()
