@@ -110,6 +110,7 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   PDesc* d_pd = nullptr;     // step-3 two-sided edge projections, one per block
   int nzb = 0;               // owned blocks (entries of d_zb before the global one)
   int* d_own = nullptr;      // per-block ownership flags (step-4 partial residual)
+  int* d_wmask = nullptr;    // block sharding: interface-plane segments this rank writes (k_write_iface)
   int n_pd3 = 0;
   StageDescs s1x, s1y, s3x, s3y, s5r1, s5wx, s6f, s7y, s7x;  // s5r1: R1 and R2; s5wx: WX and WY
   StageDescs s5zf, s5zi;     // z-modal step 5: R~ = Z^T R (R1, R2) and P = Z P~ (P1, P2), real S
@@ -344,8 +345,43 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   stage(pp.s5r1, std::move(v)); v.clear();
   // P1, P2 (projections of w^ onto the planes): k_projm, see run_pass
   // w on the planes: WX[a][rk][q] = sum_m W_y[q][m] P1[a][rk][m];  WY[b][rk][p] = sum_l W_x[p][l] P2[b][rk][l]
-  if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, 1, Ny, 0, B_IF, pp.wx, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
-  if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, 1, Nx, 0, B_IF, pp.wy, 1, Nx, 0, (int)(nify * RZ), 1, 0));
+  std::vector<int> wmask;  // sharded: [x-plane a][block row j], then [y-plane b][block column i]
+  if (!P->sharded) {
+    if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, 1, Ny, 0, B_IF, pp.wx, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
+    if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, 1, Nx, 0, B_IF, pp.wy, 1, Nx, 0, (int)(nify * RZ), 1, 0));
+  } else {
+    // Block sharding: a rank needs w on the interface planes only where its own blocks' faces
+    // read it (step 6) and where it writes u on the planes (step 7): the segment of x-plane a in
+    // block row j belongs to the owner of the block on its left (i = a), the segment of y-plane
+    // b in block column i to the owner of the block below (j = b); the plane intersections to
+    // rank0.  Only those rows of W_y P1 / W_x P2 are formed.
+    auto own_blk = [&](int i, int j) { return owned(j * nbx + i); };
+    for (int a = 0; a < nifx; ++a)
+      for (int j = 0; j < nby; ++j) {
+        const bool writes = own_blk(a, j);
+        wmask.push_back(writes ? 1 : 0);
+        if (!(writes || own_blk(a + 1, j))) continue;
+        const AxisBlock& by = Y.blocks[j];
+        v.push_back(gd(Y.Wg + (int64_t)(by.lo - 1) * Ny, Ny, 1, by.n, Ny, B_IF, pp.p1 + (int64_t)a * RZ * Ny, 1, Ny, 0,
+                       B_IF, pp.wx + (int64_t)a * RZ * Ny + (by.lo - 1), 1, Ny, 0, (int)RZ, 1, 0));
+      }
+    for (int b = 0; b < nify; ++b)
+      for (int i = 0; i < nbx; ++i) {
+        const bool writes = own_blk(i, b);
+        wmask.push_back(writes ? 1 : 0);
+        if (!(writes || own_blk(i, b + 1))) continue;
+        const AxisBlock& bx = X.blocks[i];
+        v.push_back(gd(X.Wg + (int64_t)(bx.lo - 1) * Nx, Nx, 1, bx.n, Nx, B_IF, pp.p2 + (int64_t)b * RZ * Nx, 1, Nx, 0,
+                       B_IF, pp.wy + (int64_t)b * RZ * Nx + (bx.lo - 1), 1, Nx, 0, (int)RZ, 1, 0));
+      }
+    if (P->rank0)  // intersections of x-plane a with y-plane b: written from WX[a][rk][q_b]
+      for (int a = 0; a < nifx; ++a)
+        for (int b = 0; b < nify; ++b) {
+          const int q = Y.iface[b] - 1;
+          v.push_back(gd(Y.Wg + (int64_t)q * Ny, Ny, 1, 1, Ny, B_IF, pp.p1 + (int64_t)a * RZ * Ny, 1, Ny, 0, B_IF,
+                         pp.wx + (int64_t)a * RZ * Ny + q, 1, Ny, 0, (int)RZ, 1, 0));
+        }
+  }
   stage(pp.s5wx, std::move(v)); v.clear();
   if (pp.s5m) {  // z-modal step 5: R~[a][r][t][m] = sum_k Z[k][t] R[a][r][k][m]; P = Z P~ (real Z)
     if (nifx) v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r1, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.r1t, Ny,
@@ -514,6 +550,10 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     for (int b = 0; b < nblk; ++b) own[b] = owned(b) ? 1 : 0;
     CUDA_TRY(cudaMalloc(&pp.d_own, sizeof(int) * nblk));
     CUDA_TRY(cudaMemcpy(pp.d_own, own.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice));
+    if (!wmask.empty()) {
+      CUDA_TRY(cudaMalloc(&pp.d_wmask, sizeof(int) * wmask.size()));
+      CUDA_TRY(cudaMemcpy(pp.d_wmask, wmask.data(), sizeof(int) * wmask.size(), cudaMemcpyHostToDevice));
+    }
   }
   CUDA_TRY(cudaMalloc(&pp.d_zb, sizeof(ZBlock) * zb.size()));
   CUDA_TRY(cudaMemcpy(pp.d_zb, zb.data(), sizeof(ZBlock) * zb.size(), cudaMemcpyHostToDevice));
@@ -719,9 +759,10 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   // step 7
   if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false, &pp.y7s, ST_Y7S, ST_Y7D))) return rc;
   if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s, ST_X7S, ST_X7D))) return rc;
-  if (has_if && (!P->sharded || P->rank0)) {
+  if (has_if) {  // (sharded: every rank writes its own segments of the planes, pp.d_wmask)
     begin(ST_WRITE);
-    CUDA_TRY(launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st));
+    CUDA_TRY(launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st,
+                                  pp.d_wmask, P->t_bx, P->t_by, P->nbx, P->nby, P->sharded ? P->rank0 : 1));
     P->launches++;
     end();
   }
@@ -1351,6 +1392,7 @@ int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_
     cudaFree(kv.second.d_zb);
     cudaFree(kv.second.d_pd);
     cudaFree(kv.second.d_own);
+    cudaFree(kv.second.d_wmask);
   }
   P->passes.clear();
   return LFDS_OK;
@@ -1563,6 +1605,7 @@ void lfds_destroy(lfds_plan* P) {
     cudaFree(kv.second.d_zb);
     cudaFree(kv.second.d_pd);
     cudaFree(kv.second.d_own);
+    cudaFree(kv.second.d_wmask);
   }
   if (P->d_tab) cudaFree(P->d_tab);
   if (P->gexec) cudaGraphExecDestroy(P->gexec);

@@ -150,9 +150,12 @@ cudaError_t launch_zsolve(int mode, const ZBlock* d_blocks, int nblocks, int max
                           ZTab tab, int64_t sig_off, const GSweep* g, const Bufs& bufs, double* d_minpiv,
                           cudaStream_t st, bool realz);
 cudaError_t launch_iface_residual(const IfaceRes& p, const Bufs& bufs, cudaStream_t st);
+// wmask (block sharding, else NULL = write all): [a][block row j] then [b][block column i]
+// flags of the plane segments this rank writes; intersections only if rank0
 cudaError_t launch_write_iface_u(int nx, int ny, int nz, int R, int dtype, int nifx, int nify,
                                  int64_t ifx, int64_t ify, int64_t wx, int64_t wy,
-                                 const Bufs& bufs, cudaStream_t st);
+                                 const Bufs& bufs, cudaStream_t st, const int* wmask = nullptr,
+                                 int64_t bxo = 0, int64_t byo = 0, int nbx = 1, int nby = 1, int rank0 = 1);
 cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, int has_f,
                             int64_t hx, int64_t hy, int64_t hz, int64_t hhx, int64_t hhy, int64_t hhz,
                             int64_t sig, int64_t sige, double2 lam, const int64_t* ddtabs, const void* u,

@@ -256,11 +256,14 @@ cudaError_t launch_iface_residual(const IfaceRes& p, const Bufs& bufs, cudaStrea
 
 // ---------------------------------------------------------------- u = w on the interface planes
 __global__ void k_write_iface(int nx, int ny, int nz, int R, int dtype, int nifx, int nify, int64_t ifxo,
-                              int64_t ifyo, int64_t wx, int64_t wy, Bufs bufs) {
+                              int64_t ifyo, int64_t wx, int64_t wy, Bufs bufs, const int* __restrict__ wmask,
+                              int64_t bxo, int64_t byo, int nbx, int nby, int rank0) {
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
   const int* ifx = reinterpret_cast<const int*>(TAB + ifxo);
   const int* ify = reinterpret_cast<const int*>(TAB + ifyo);
+  const int* bx_of = reinterpret_cast<const int*>(TAB + bxo);  // block column of node p (-1: interface)
+  const int* by_of = reinterpret_cast<const int*>(TAB + byo);
   void* u = bufs.p[B_U];
   const int64_t nxp = (int64_t)nifx * R * nz * ny;
   const int64_t total = nxp + (int64_t)nify * R * nz * nx;
@@ -273,6 +276,10 @@ __global__ void k_write_iface(int nx, int ny, int nz, int R, int dtype, int nifx
       const int k = (int)(rest % nz); rest /= nz;
       const int r = (int)(rest % R);
       const int a = (int)(rest / R);
+      if (wmask) {
+        const int j = by_of[q];
+        if (j < 0 ? !rank0 : !wmask[a * nby + j]) continue;
+      }
       uo = (((int64_t)r * nz + k) * ny + q) * nx + (ifx[a] - 1);
       v = IF[wx + t];
     } else {
@@ -286,6 +293,7 @@ __global__ void k_write_iface(int nx, int ny, int nz, int R, int dtype, int nifx
       bool on_x = false;
       for (int a = 0; a < nifx; ++a) on_x |= (ifx[a] - 1 == p);
       if (on_x) continue;
+      if (wmask && !wmask[nifx * nby + b * nbx + bx_of[p]]) continue;
       uo = (((int64_t)r * nz + k) * ny + (ify[b] - 1)) * nx + p;
       v = IF[wy + s];
     }
@@ -295,12 +303,13 @@ __global__ void k_write_iface(int nx, int ny, int nz, int R, int dtype, int nifx
 }
 
 cudaError_t launch_write_iface_u(int nx, int ny, int nz, int R, int dtype, int nifx, int nify, int64_t ifx,
-                                 int64_t ify, int64_t wx, int64_t wy, const Bufs& bufs, cudaStream_t st) {
+                                 int64_t ify, int64_t wx, int64_t wy, const Bufs& bufs, cudaStream_t st,
+                                 const int* wmask, int64_t bxo, int64_t byo, int nbx, int nby, int rank0) {
   int64_t total = (int64_t)nifx * R * nz * ny + (int64_t)nify * R * nz * nx;
   if (total == 0) return cudaSuccess;
   int64_t blocks = (total + 255) / 256;
-  k_write_iface<<<(unsigned)(blocks > 1048576 ? 1048576 : blocks), 256, 0, st>>>(nx, ny, nz, R, dtype, nifx, nify,
-                                                                                  ifx, ify, wx, wy, bufs);
+  k_write_iface<<<(unsigned)(blocks > 1048576 ? 1048576 : blocks), 256, 0, st>>>(
+      nx, ny, nz, R, dtype, nifx, nify, ifx, ify, wx, wy, bufs, wmask, bxo, byo, nbx, nby, rank0);
   return cudaGetLastError();
 }
 
