@@ -178,11 +178,21 @@ int lfds_residual(lfds_plan* plan, const void* u_dev, const void* f_dev, lfds_z*
  *   lfds_solve_phase(3)
  * lfds_exchange_layout gives each exchange's byte offset inside the workspace and its length
  * in doubles (exchange 1 = the interface residual on the planes, exchange 2 = the step-5
- * correction projected onto the planes).  Afterwards u_dev holds u on this rank's blocks (and,
- * for the rank0 rank, on the interface planes); other entries are not written.  Phased solves
- * take all nrhs right-hand sides in one pass and do not refine (LFDS_EINVAL otherwise).
+ * correction projected onto the planes).  Afterwards u_dev holds u on this rank's blocks and
+ * on its segments of the interface planes (the segment of an x-plane in a block row belongs to
+ * the owner of the block on its left, of a y-plane in a block column to the owner of the block
+ * below, the plane intersections to the rank0 rank); other entries are not written.  Phased
+ * solves take all nrhs right-hand sides in one pass and do not refine (LFDS_EINVAL otherwise).
  */
 int lfds_set_partition(lfds_plan* plan, const int* block_owned, int l_begin, int l_end, int rank0);
+/*
+ * Optional second split of the z-modal step 5 (options.s5_modal, real z tables): this rank
+ * forms the global y-modes m in [m_begin, m_end) (multiples of 64, the k_s5m tile, or ny) of
+ * its x-modes, so R1 = W_y^T RX is formed only for those m; exchange 2 sums the (m, l) parts.
+ * Call after lfds_set_partition (which resets it to all m).  LFDS_EINVAL for a bad or unaligned
+ * range or when step 5 runs as per-mode z-sweeps.
+ */
+int lfds_set_mode_rows(lfds_plan* plan, int m_begin, int m_end);
 int lfds_exchange_layout(const lfds_plan* plan, int nrhs, int which, size_t* byte_offset, size_t* n_doubles);
 int lfds_solve_phase(lfds_plan* plan, int phase, const void* f_dev, void* u_dev, int nrhs, void* ws,
                      size_t ws_bytes, void* cuda_stream);

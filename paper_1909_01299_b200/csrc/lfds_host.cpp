@@ -168,6 +168,7 @@ struct lfds_plan {
   // and whether this rank adds the b-terms of the interface residual and writes u on the planes
   std::vector<char> own;
   int l_begin = 0, l_end = -1, rank0 = 1;
+  int m_begin = 0, m_end = -1;  // z-modal step 5: this rank's global y-modes (-1: all)
   bool sharded = false;
 };
 
@@ -338,7 +339,12 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   // (block sharding: step 5 of this rank reads R2[b][rk][l] only for its x-modes l in
   // [l_begin, l_end), so only those rows of W_x^T RY are formed)
   const int l0s = P->sharded ? P->l_begin : 0, l1s = P->sharded ? P->l_end : Nx;
-  if (nifx) v.push_back(gd(Y.Wg, 1, Ny, Ny, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
+  // (and with a y-mode split of the z-modal step 5, R1 only for the rank's y-modes m)
+  const bool msplit = P->sharded && P->m_end >= 0 && P->s5m && !in_real && !out_real;
+  const int m0s = msplit ? P->m_begin : 0, m1s = msplit ? P->m_end : Ny;
+  if (nifx && m1s > m0s)
+    v.push_back(gd(Y.Wg + m0s, 1, Ny, m1s - m0s, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1 + m0s, 1, Ny, 0,
+                   (int)(nifx * RZ), 1, 0));
   if (nify && l1s > l0s)
     v.push_back(gd(X.Wg + l0s, 1, Nx, l1s - l0s, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2 + l0s, 1, Nx, 0,
                    (int)(nify * RZ), 1, 0));
@@ -384,14 +390,16 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   }
   stage(pp.s5wx, std::move(v)); v.clear();
   if (pp.s5m) {  // z-modal step 5: R~[a][r][t][m] = sum_k Z[k][t] R[a][r][k][m]; P = Z P~ (real Z)
-    if (nifx) v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r1, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.r1t, Ny,
-                             (int64_t)Nz * Ny, 1, nifx * R, Ny, 0));
+    if (nifx && m1s > m0s)
+      v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r1 + m0s, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.r1t + m0s, Ny,
+                     (int64_t)Nz * Ny, 1, nifx * R, m1s - m0s, 0));
     if (nify && l1s > l0s)
       v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r2 + l0s, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.r2t + l0s, Nx,
                      (int64_t)Nz * Nx, 1, nify * R, l1s - l0s, 0));
     stage(pp.s5zf, std::move(v)); v.clear();
-    if (nifx) v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p1t, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.p1, Ny,
-                             (int64_t)Nz * Ny, 1, nifx * R, Ny, 0));
+    if (nifx && m1s > m0s)  // (y-mode split: P1 rows outside [m0s, m1s) are zeroed in run_pass)
+      v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p1t + m0s, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.p1 + m0s, Ny,
+                     (int64_t)Nz * Ny, 1, nifx * R, m1s - m0s, 0));
     if (nify) v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p2t, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.p2, Nx,
                              (int64_t)Nz * Nx, 1, nify * R, Nx, 0));
     stage(pp.s5zi, std::move(v)); v.clear();
@@ -695,13 +703,21 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     S5M S{};
     S.nx = Nx; S.ny = Ny; S.nz = Nz; S.R = R; S.nifx = nifx; S.nify = nify;
     S.l_begin = l_begin; S.l_end = l_end; S.nmt = s5m_mtiles(Ny);
+    const bool msplit = P->sharded && P->m_end >= 0;
+    S.mt_begin = msplit ? (P->m_begin + 63) / 64 : 0;  // (an empty range at the end: [ny, ny))
+    S.mt_end = msplit ? (P->m_end + 63) / 64 : S.nmt;
     S.lamx = X.lamg; S.lamy = Y.lamg; S.theta = P->t_theta; S.wxi = X.WI; S.wyi = Y.WI;
     S.r1t = pp.r1t; S.r2t = pp.r2t; S.p1t = pp.p1t; S.p2p = pp.p2p; S.p2t = pp.p2t;
     CUDA_TRY(launch_s5m(S, bufs, st));
     P->launches += nify ? 2 : 1;
     end(); begin(ST_GPROJ);
-    CUDA_TRY(launch_xform(pp.d_descs + pp.s5zi.off, pp.s5zi.n, pp.s5zi.maxM, pp.s5zi.maxN, true, false, bufs, st));
-    P->launches += 1;
+    if (msplit && nifx)  // P1 rows of other y-modes: zero (exchange 2 sums the ranks' parts)
+      CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.p1, 0,
+                               sizeof(double2) * (size_t)nifx * R * Nz * Ny, st));
+    if (pp.s5zi.n) {
+      CUDA_TRY(launch_xform(pp.d_descs + pp.s5zi.off, pp.s5zi.n, pp.s5zi.maxM, pp.s5zi.maxN, true, false, bufs, st));
+      P->launches += 1;
+    }
     end();
   } else if ((phases & PH_2) && has_if) {
     // step 5
@@ -1379,6 +1395,8 @@ int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_
     P->l_begin = 0;
     P->l_end = -1;
     P->rank0 = 1;
+    P->m_begin = 0;
+    P->m_end = -1;
   } else {
     if (l_begin < 0 || l_end < l_begin || l_end > Nx) return fail(LFDS_EINVAL, "bad x-mode range [%d, %d) of %d", l_begin, l_end, Nx);
     P->own.assign(block_owned, block_owned + nblk);
@@ -1386,8 +1404,30 @@ int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_
     P->l_begin = l_begin;
     P->l_end = l_end;
     P->rank0 = rank0 ? 1 : 0;
+    P->m_begin = 0;
+    P->m_end = -1;
   }
   for (auto& kv : P->passes) {  // descriptors depend on the owned blocks: rebuild lazily
+    cudaFree(kv.second.d_descs);
+    cudaFree(kv.second.d_zb);
+    cudaFree(kv.second.d_pd);
+    cudaFree(kv.second.d_own);
+    cudaFree(kv.second.d_wmask);
+  }
+  P->passes.clear();
+  return LFDS_OK;
+}
+
+int lfds_set_mode_rows(lfds_plan* P, int m_begin, int m_end) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  const int Ny = P->ax[1].N;
+  if (!P->sharded) return fail(LFDS_EINVAL, "lfds_set_mode_rows: call lfds_set_partition first");
+  if (!P->s5m) return fail(LFDS_EINVAL, "lfds_set_mode_rows: step 5 runs as z-sweeps (complex z or s5_modal = 0)");
+  if (m_begin < 0 || m_end < m_begin || m_end > Ny || (m_begin % 64 && m_begin != Ny) || (m_end % 64 && m_end != Ny))
+    return fail(LFDS_EINVAL, "bad y-mode range [%d, %d) of %d (multiples of 64)", m_begin, m_end, Ny);
+  P->m_begin = m_begin;
+  P->m_end = m_end;
+  for (auto& kv : P->passes) {  // descriptors depend on the range: rebuild lazily
     cudaFree(kv.second.d_descs);
     cudaFree(kv.second.d_zb);
     cudaFree(kv.second.d_pd);

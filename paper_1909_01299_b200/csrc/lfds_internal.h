@@ -111,6 +111,7 @@ struct S5M {
   int nx, ny, nz, R, nifx, nify;
   int l_begin, l_end;          // this rank's global x-modes
   int nmt;                     // m-tiles (P2 partials)
+  int mt_begin, mt_end;        // this rank's m-tiles (y-mode split; all: 0, nmt)
   int64_t lamx, lamy, theta;   // TAB: lambda_l (nx), mu_m (ny), theta_t (nz), complex
   int64_t wxi, wyi;            // TAB: W_x[I_a][l] (nifx x nx), W_y[I_b][m] (nify x ny)
   int64_t r1t, r2t;            // IF: R1~[a][r][t][m], R2~[b][r][t][l]

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(S5_THREADS, KA <= 16 ? 2 : 1) k_s5m(S5M S, Buf
   double2* A1 = LM + 2 * SM::LM;
   double2* A2 = A1 + SM::A1;
   double2* CB = A2 + SM::A2;
-  const int mt = blockIdx.x, t = blockIdx.y, r = blockIdx.z;
+  const int mt = S.mt_begin + (int)blockIdx.x, t = blockIdx.y, r = blockIdx.z;
   const int m0 = mt * TM;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
@@ -273,7 +273,7 @@ __global__ void k_p2sum(S5M S, Bufs bufs) {
     double2 acc = make_double2(0, 0);
     if (l >= S.l_begin && l < S.l_end) {
       const double2* p = IF + S.p2p + row * S.nmt * S.nx + l;
-      for (int k = 0; k < S.nmt; ++k) {
+      for (int k = S.mt_begin; k < S.mt_end; ++k) {
         const double2 v = p[(int64_t)k * S.nx];
         acc.x += v.x;
         acc.y += v.y;
@@ -294,9 +294,9 @@ int s5m_mtiles(int ny) { return (ny + TM - 1) / TM; }
 cudaError_t launch_s5m(const S5M& S, const Bufs& bufs, cudaStream_t st) {
   const int ka = s5m_ka(S.nifx, S.nify);
   if (!ka || S.R > 65535 || S.nz > 65535) return cudaErrorInvalidValue;
-  const dim3 grid((unsigned)S.nmt, (unsigned)S.nz, (unsigned)S.R);
+  const dim3 grid((unsigned)(S.mt_end - S.mt_begin), (unsigned)S.nz, (unsigned)S.R);
   cudaError_t e;
-  {  // (a rank without x-modes still writes P1~ = 0)
+  if (S.mt_end > S.mt_begin) {  // (a rank without x-modes still writes P1~ = 0 on its m rows)
     if (ka == 8) {
       const size_t sm = S5Smem<8>::TOTAL * sizeof(double2);
       if ((e = cudaFuncSetAttribute(k_s5m<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;

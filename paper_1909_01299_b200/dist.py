@@ -8,7 +8,8 @@ i,j"), so each rank computes a subset, chosen by longest-processing-time-first o
 sine-transform directions ~O(log n)).  The interface step is one exchange: every rank adds the
 contributions of its own blocks to the residual on the interface planes and the
 residuals are summed over the ranks (exchange 1).  Step 5 is split by global
-x-modes l: each rank sweeps its l-range and the plane projections are summed (exchange 2).
+x-modes l (and, in the z-modal form, by global y-modes m): each rank handles its (m, l) range and
+the plane projections are summed (exchange 2).
 Both sums are `torch.distributed.all_reduce` on views of the library workspace (NCCL on GPUs);
 `allreduce` can be replaced (tests use an in-process emulation and gloo).
 """
@@ -61,8 +62,18 @@ def mode_ranges(nx: int, world: int, align: int = 32) -> List[tuple]:
     return out
 
 
+def mode_grid(world: int, modal: bool) -> tuple:
+    """(W_m, W_l): ranks along the step-5 y-modes and x-modes.  The z-modal step 5 splits both
+    (W_m = the largest divisor of world not above sqrt(world)), so that R1 = W_y^T RX is also
+    formed per rank; the per-mode z-sweeps split x-modes only."""
+    if not modal:
+        return 1, world
+    wm = max(d for d in range(1, int(world ** 0.5) + 1) if world % d == 0)
+    return wm, world // wm
+
+
 def shard(plan, rank: int, world: int) -> dict:
-    """Configure `plan` for `rank` of `world` (LPT block ownership, step-5 x-mode range)."""
+    """Configure `plan` for `rank` of `world` (LPT block ownership, step-5 mode ranges)."""
     info = plan.info()
     nbx, nby = info["nbx"], info["nby"]
     bx = [plan.basis(0, i) for i in range(nbx)]
@@ -70,9 +81,15 @@ def shard(plan, rank: int, world: int) -> dict:
     costs = block_costs([b[1].shape[0] for b in bx], [b[1].shape[0] for b in by], [b[2] for b in bx],
                         [b[2] for b in by])
     owner = lpt_partition(costs, world)
-    l0, l1 = mode_ranges(info["nx"], world)[rank]
+    wm, wl = mode_grid(world, bool(info.get("s5_modal", 0)))
+    rm, rl = rank // wl, rank % wl
+    l0, l1 = mode_ranges(info["nx"], wl)[rl]
     plan.set_partition(owner == rank, l0, l1, rank == 0)
-    return {"owner": owner, "l_range": (l0, l1), "costs": costs}
+    m0, m1 = 0, info["ny"]
+    if wm > 1:
+        m0, m1 = mode_ranges(info["ny"], wm, align=64)[rm]
+        plan.set_mode_rows(m0, m1)
+    return {"owner": owner, "l_range": (l0, l1), "m_range": (m0, m1), "costs": costs}
 
 
 def solve_sharded(plan, f, u, ws, allreduce: Optional[Callable] = None, stream=None):

@@ -77,6 +77,7 @@ _lib.lfds_set_partition.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c
 _lib.lfds_exchange_layout.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
                                       ctypes.POINTER(ctypes.c_size_t)]
 _lib.lfds_solve_phase.argtypes = [_P, ctypes.c_int, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
+_lib.lfds_set_mode_rows.argtypes = [_P, ctypes.c_int, ctypes.c_int]
 _lib.lfds_gmres_workspace_bytes.argtypes = [_P, ctypes.c_int]
 _lib.lfds_gmres_workspace_bytes.restype = ctypes.c_size_t
 _lib.lfds_gmres.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, _P,
@@ -93,7 +94,8 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_get_report",
             "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version",
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
-            "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres"]
+            "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
+            "lfds_set_mode_rows"]
 
 
 def _check(rc):
@@ -270,6 +272,11 @@ class Plan:
         else:
             own = np.ascontiguousarray(np.asarray(block_owned, dtype=np.int32).ravel())
             _check(_lib.lfds_set_partition(self._h, own.ctypes.data_as(_P), int(l_begin), int(l_end), int(rank0)))
+        self._ws = {}
+
+    def set_mode_rows(self, m_begin: int, m_end: int):
+        """Second split of the z-modal step 5: this rank's global y-modes [m_begin, m_end)."""
+        _check(_lib.lfds_set_mode_rows(self._h, int(m_begin), int(m_end)))
         self._ws = {}
 
     def exchange_view(self, ws, nrhs: int, which: int):
