@@ -203,14 +203,24 @@ def stage_algorithmic(p, R: int, plan=None):
                     el += e
         return fl, 2 * esz * el
 
+    plane_dst = bool(getattr(plan, "plane_dst", True)) if plan else True
+
+    def fused(i, j):  # mirrors fused2() in lfds_host.cpp / dst2_supported() in lfds_dst.cu
+        return (plane_dst and not p.real and is_sine(kx[i], bx[i]) and is_sine(ky[j], by[j])
+                and bx[i] == by[j] and 2 * (bx[i] + 1) in (32, 64, 128))
+
     def sine(kinds, axis):
         el = 0.0
         for i in range(len(bx)):
             for j in range(len(by)):
                 k, n = (kinds[i], bx[i]) if axis == 0 else (kinds[j], by[j])
-                if is_sine(k, n) and not p.real:
+                if is_sine(k, n) and not p.real and not fused(i, j):
                     el += bx[i] * by[j] * nz * R
         return None, 32.0 * el
+
+    # plane sine transform (both axes in one pass): 32 B per element of the fused blocks
+    psine = (None, 32.0 * sum(bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by))
+                              if fused(i, j)))
     el_blk = sum(nx * ny * nz * R for nx in bx for ny in by)
     el_all = p.nx * p.ny * nz * R
     nifx, nify = len(p.iface_x), len(p.iface_y)
@@ -234,6 +244,7 @@ def stage_algorithmic(p, R: int, plan=None):
         "step5_plane_inverse": (plane, None),
         "step6_zsolve_lift": (None, 2 * esz * el_blk),
         "step7_y_sine": ys, "step7_y_dense": yd, "step7_x_sine": xs, "step7_x_dense": xd,
+        "step1_plane_sine": psine, "step7_plane_sine": psine,
         # refinement: r = Mf - Au reads u and f and writes r; u += r reads both, writes u
         "refine_residual": (None, 48.0 * el_all), "refine_axpy": (None, 48.0 * el_all),
     }
@@ -353,7 +364,8 @@ def run_ours(args, rank, world, local_rank):
     # nodes); the sharded path runs phase by phase with the exchanges in between
     res_dd = RESIDUAL_DD.get(args.config, True)
     plan = Plan.from_problem(p, device=local_rank, refine=refine, residual_dd=res_dd, profile=True,
-                             graph=not blocks, rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0))
+                             graph=not blocks, rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0),
+                             plane_dst=bool(args.plane_dst))
     setup_s = time.perf_counter() - t0
     part = lfds_dist.shard(plan, rank, world) if blocks else None
     dt = torch.float64 if p.real else torch.complex128
@@ -501,7 +513,7 @@ def run_hetero(args, rank, world, local_rank):
     p = make_problem(base)
     dl = anomaly(p, eps=eps)
     t0 = time.perf_counter()
-    plan = Plan.from_problem(p, device=local_rank, profile=True)
+    plan = Plan.from_problem(p, device=local_rank, profile=True, plane_dst=bool(args.plane_dst))
     setup_s = time.perf_counter() - t0
     f = torch.from_numpy(p.rhs(0)).to(dev)
     dlam = torch.from_numpy(dl).to(dev)
@@ -599,6 +611,8 @@ def main():
                     help="N > 1: block sharding with two NCCL exchanges (default) or RHS sharding")
     ap.add_argument("--e2e-rhs", type=int, default=4, dest="e2e_rhs", help="RHS per e2e step (memory bound)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--plane-dst", type=int, default=1, choices=[0, 1], dest="plane_dst",
+                    help="1: plane sine transforms on uniform x uniform blocks (options.plane_dst)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

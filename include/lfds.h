@@ -64,10 +64,13 @@ typedef struct {
                     /* 0: per-mode tridiagonal z-sweeps (the paper's form)   */
   int graph;        /* 1: lfds_solve captures its launches into a CUDA graph and replays  */
                     /* it while (f, u, nrhs, workspace) repeat (refine >= 0 only); 0: off */
+  int plane_dst;    /* 1: steps 1 and 7 of a block that is uniform on both axes with the    */
+                    /* same length run as ONE plane sine transform (both     */
+                    /* axes, one pass over the block); 0: an x pass and a y pass           */
 } lfds_options;
 
 /* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1,
- * graph 0. */
+ * graph 0, plane_dst 1. */
 void lfds_default_options(lfds_options* opt);
 
 /*

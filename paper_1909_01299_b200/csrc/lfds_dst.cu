@@ -11,6 +11,7 @@
 // R1-point FFT in registers, multiply by W_L^{n2 k1}, exchange through shared memory, then R1
 // threads run R2-point FFTs.  Only the outputs k = 1..N-1 are kept.  FP64 CUDA-core
 // arithmetic: ~5 L log2 L flops per column instead of the 4 n^2 of the dense real matrix.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,6 +22,8 @@
 
 namespace lfds {
 namespace {
+
+namespace cg = cooperative_groups;
 
 struct zc2 {
   double x, y;
@@ -412,7 +415,223 @@ cudaError_t dstw_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& 
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- plane (2-D) transform
+// A uniform x uniform block with n nodes on both axes: the tensor-product transform
+// C = a_y a_x S_y B S_x^T of every (r, k) plane in ONE pass over the block (the separate x and
+// y passes read and write the volume twice).  The plane lives in shared memory between the two
+// 1-D transforms: one CTA holds it for n <= 31 (15 KB), a cluster of CL = ceil(n/32) CTAs for
+// larger n (n = 63: 2 CTAs of 33 KB), CTA q owning the x-modes [q RPC, (q+1) RPC) of all rows:
+//   x phase: CTA q transforms the rows [q RPC, (q+1) RPC) exactly like k_dstw (loads straight
+//            from global memory into registers, per-warp exchange) and stores every output
+//            (row, x-mode l) into the shared memory of the CTA owning l (DSMEM stores);
+//   cluster barrier (release / acquire);
+//   y phase: CTA q transforms its RPC columns from local shared memory and stores them (two
+//            adjacent columns per warp instruction: whole 32-byte sectors).
+// Clusters stride over the (block, plane) items; a second cluster barrier ends each item.  Used
+// for L = 2(n+1) in {32, 64, 128}; see dst2_supported() for why not beyond.
+template <int R1, int R2>
+struct Dst2Cfg {
+  static constexpr int L = R1 * R2, N = L / 2, n = N - 1;
+  static constexpr int CL = (n + 31) / 32;                  // CTAs per cluster (<= 8)
+  static constexpr int RPC = (n + CL - 1) / CL;              // x-modes / rows per CTA
+  static constexpr int LDT = RPC % 2 ? RPC : RPC + 1;        // odd: conflict-free column reads
+  static constexpr int WARPS = R1 > 16 ? 2 : 4, CPW = 32 / R2, LDE = R2 + 1;
+  static constexpr size_t smem = (size_t)n * LDT * sizeof(double2);
+};
+
+template <int R1, int R2>
+__device__ __forceinline__ void dst2_fft(zc2 (&a)[R1], const double2* twl, const double2* tws, double2* ex, int cw,
+                                         int t, zc2 (&b)[(R1 + R2 - 1) / R2][R2]) {
+  constexpr int L = R1 * R2, LDE = R2 + 1;
+  dft_reg<R1, L>(a, twl);
+#pragma unroll
+  for (int k1 = 1; k1 < R1; ++k1) {
+    const double2 w = tws[k1 * R2 + t];
+    a[k1] = zmul(a[k1], zc2{w.x, w.y});
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) ex[(cw * R1 + k1) * LDE + t] = make_double2(a[k1].x, a[k1].y);
+  __syncwarp();
+#pragma unroll
+  for (int rr = 0; rr < (R1 + R2 - 1) / R2; ++rr) {
+    const int k1 = t + rr * R2;
+    if (k1 < R1) {
+#pragma unroll
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const double2 w = ex[(cw * R1 + k1) * LDE + n2];
+        b[rr][n2] = zc2{w.x, w.y};
+      }
+      fft_reg<R2, L>(b[rr], twl);
+    }
+  }
+}
+
+template <int R1, int R2>
+__global__ void __launch_bounds__(Dst2Cfg<R1, R2>::WARPS * 32) k_dst2(const Dst2Desc* __restrict__ descs, int ndesc,
+                                                                      int nplanes, Bufs bufs) {
+  using C = Dst2Cfg<R1, R2>;
+  constexpr int L = C::L, N = C::N, n = C::n, RPC = C::RPC, LDT = C::LDT, CPW = C::CPW, RPT = (R1 + R2 - 1) / R2;
+  extern __shared__ __align__(16) double2 Tsm[];   // [row q < n][x-mode l - q0 < RPC], row stride LDT
+  __shared__ double2 twl[L];
+  __shared__ double2 tws[R1 * R2];                  // W_L^{t k1} at [k1][t]
+  __shared__ double2 exs[C::WARPS][CPW * R1 * C::LDE];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = (int)cluster.block_rank();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, cw = lane / R2, t = lane % R2;
+  {  // one length per launch: every descriptor has the same twiddle table
+    const double2* TW = reinterpret_cast<const double2*>(bufs.p[B_TAB]) + descs[0].tw_off;
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+      twl[j] = __ldg(TW + j);
+      tws[j] = __ldg(TW + ((j % R2) * (j / R2)) % L);
+    }
+  }
+  __syncthreads();
+  double2* ex = exs[warp];
+  const int r0 = q * RPC, nr = min(RPC, n - r0);
+  // persistent clusters: work item w = (descriptor, plane), clusters stride over the items
+  const int64_t total = (int64_t)ndesc * nplanes, ncl = gridDim.x / C::CL;
+  auto load_row = [&](const double2* B, int64_t sBr, int g, zc2 (&a)[R1]) {
+    const int rl = g * CPW + cw;
+    const bool ok = rl < nr;
+    const double2* Br = B + (int64_t)(ok ? r0 + rl : 0) * sBr;
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) {
+      const int qq = R2 * n1 + t;
+      zc2 v{0, 0};
+      if (ok && qq > 0 && qq < N) {
+        const double2 w = __ldg(Br + (qq - 1));
+        v = zc2{w.x, w.y};
+      } else if (ok && qq > N) {
+        const double2 w = __ldg(Br + (L - qq - 1));
+        v = zc2{-w.x, -w.y};
+      }
+      a[n1] = v;
+    }
+  };
+  for (int64_t w = blockIdx.x / C::CL; w < total; w += ncl) {
+    const Dst2Desc& D = descs[w / nplanes];
+    const int64_t plane = w % nplanes;
+    const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off + plane * D.sB1;
+    double2* Cg = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off + plane * D.sC1;
+    // ---- x phase: rows r0 .. r0+nr-1, CPW rows per warp step, outputs to the owner's Tsm
+    const double hx = 0.5 * D.ax;
+    for (int g = warp; g * CPW < nr; g += C::WARPS) {
+      const int rl = g * CPW + cw, r = r0 + rl;
+      const bool ok = rl < nr;
+      zc2 a[R1];
+      load_row(B, D.sBr, g, a);
+      zc2 b[RPT][R2];
+      dst2_fft<R1, R2>(a, twl, tws, ex, cw, t, b);
+#pragma unroll
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int k1 = t + rr * R2;
+        if (k1 < R1 && ok) {
+#pragma unroll
+          for (int k2 = 0; k2 < R2 / 2; ++k2) {
+            const int k = k1 + R1 * k2;
+            if (k >= 1 && k < N) {
+              const int l = k - 1, o = l / RPC;
+              double2* dst = cluster.map_shared_rank(Tsm, o);
+              dst[r * LDT + (l - o * RPC)] = make_double2(-hx * b[rr][k2].y, hx * b[rr][k2].x);
+            }
+          }
+        }
+      }
+    }
+    cluster.sync();  // the plane's x-transformed rows are complete in the cluster
+    // ---- y phase: columns (x-modes) r0 .. r0+nr-1 of all n rows, CPW columns per warp step
+    const double hy = 0.5 * D.ay;
+    for (int g = warp; g * CPW < nr; g += C::WARPS) {
+      const int cl = g * CPW + cw;
+      const bool ok = cl < nr;
+      const int cc = ok ? cl : 0;
+      zc2 a[R1];
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) {
+        const int qq = R2 * n1 + t;
+        zc2 v{0, 0};
+        if (qq > 0 && qq < N) {
+          const double2 x = Tsm[(qq - 1) * LDT + cc];
+          v = zc2{x.x, x.y};
+        } else if (qq > N) {
+          const double2 x = Tsm[(L - qq - 1) * LDT + cc];
+          v = zc2{-x.x, -x.y};
+        }
+        a[n1] = v;
+      }
+      zc2 b[RPT][R2];
+      dst2_fft<R1, R2>(a, twl, tws, ex, cw, t, b);
+      double2* Cc = Cg + r0 + cl;
+#pragma unroll
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int k1 = t + rr * R2;
+        if (k1 < R1 && ok) {
+#pragma unroll
+          for (int k2 = 0; k2 < R2 / 2; ++k2) {
+            const int k = k1 + R1 * k2;
+            if (k >= 1 && k < N) Cc[(int64_t)(k - 1) * D.sCr] = make_double2(-hy * b[rr][k2].y, hy * b[rr][k2].x);
+          }
+        }
+      }
+    }
+    cluster.sync();  // every CTA has read its Tsm before the next x phase writes into it
+  }
+}
+
+template <int R1, int R2>
+cudaError_t dst2_launch(const Dst2Desc* d, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st) {
+  using C = Dst2Cfg<R1, R2>;
+  auto kern = k_dst2<R1, R2>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(C::WARPS * 32, 1, 1);
+  cfg.dynamicSmemBytes = C::smem;
+  cfg.stream = st;
+  // clusters stride over the (descriptor, plane) items: 4 x the co-resident clusters (measured
+  // better than exactly one wave: a cluster that finishes early is replaced at once; loading
+  // the next item's rows ahead into registers measured slower at L = 64 / 128)
+  cfg.gridDim = dim3(C::CL, 1, 1);
+  int ncl = 0;
+  e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+  if (e != cudaSuccess) return e;
+  const int64_t items = (int64_t)ndesc * nplanes;
+  ncl = (int)std::min<int64_t>(std::max(1, ncl) * 4LL, items);
+  cfg.gridDim = dim3((unsigned)(ncl * C::CL), 1, 1);
+  e = cudaLaunchKernelEx(&cfg, kern, d, ndesc, nplanes, bufs);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+bool dst2_supported(int n) {
+  // lengths where the plane transform beats the x pass + y pass (tools/plane_dst_ab.py on the
+  // C4 grid: L = 64 7.97 -> 6.98 ms, L = 128 8.04 -> 7.52 ms per step of sine stages).  At
+  // L = 256 (4-CTA clusters) and 320 (5) a plane needs 2 or 1 CTAs per SM (shared memory
+  // 110 / 138 KB, ~220 registers per thread): too few warps to hide the load latency
+  // (L = 256: 5.99 -> 6.64 ms, L = 320: 6.41 -> 14.7 ms), so those stay on the 1-D passes.
+  const int L = 2 * (n + 1);
+  return L == 32 || L == 64 || L == 128;
+}
+
+cudaError_t launch_dst2(const Dst2Desc* d_descs, int ndesc, int n, int nplanes, const Bufs& bufs, cudaStream_t st) {
+  if (ndesc <= 0 || nplanes <= 0) return cudaSuccess;
+  switch (2 * (n + 1)) {
+    case 32: return dst2_launch<4, 8>(d_descs, ndesc, nplanes, bufs, st);
+    case 64: return dst2_launch<8, 8>(d_descs, ndesc, nplanes, bufs, st);
+    case 128: return dst2_launch<8, 16>(d_descs, ndesc, nplanes, bufs, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 bool dst_supported(int n) {
   const int L = 2 * (n + 1);

@@ -70,12 +70,13 @@ struct Axis {
 
 // one stage per kernel kind (sine = FFT-based DST on uniform blocks, dense = DMMA contraction)
 enum Stage { ST_X1S, ST_X1D, ST_Y1S, ST_Y1D, ST_Z1, ST_EPROJ, ST_EDGE, ST_IFRES, ST_GFWD, ST_GSWEEP, ST_GPROJ,
-             ST_GPLANE, ST_FACE, ST_Z2, ST_Y7S, ST_Y7D, ST_X7S, ST_X7D, ST_WRITE, ST_RESID, ST_AXPY, ST_COUNT };
+             ST_GPLANE, ST_FACE, ST_Z2, ST_Y7S, ST_Y7D, ST_X7S, ST_X7D, ST_WRITE, ST_RESID, ST_AXPY, ST_P1S, ST_P7S, ST_COUNT };
 const char* kStageNames[ST_COUNT] = {
     "step1_x_sine", "step1_x_dense", "step1_y_sine", "step1_y_dense", "step2_zsolve", "step3_edge_projection",
     "step3_edge_values", "step4_iface_residual", "step5_plane_forward", "step5_global_zsolve", "step5_projection",
     "step5_plane_inverse", "step6_face_transform", "step6_zsolve_lift", "step7_y_sine", "step7_y_dense",
-    "step7_x_sine", "step7_x_dense", "step7_write_iface", "refine_residual", "refine_axpy"};
+    "step7_x_sine", "step7_x_dense", "step7_write_iface", "refine_residual", "refine_axpy", "step1_plane_sine",
+    "step7_plane_sine"};
 
 struct Profiler {
   struct Rec { int stage, launches; cudaEvent_t a, b; bool graph = false; };  // graph: events owned by a graph
@@ -118,6 +119,11 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   int64_t r1t = 0, r2t = 0, p1t = 0, p2t = 0, p2p = 0;
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
   std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
+  // plane sine transforms of uniform x uniform blocks (k_dst2), per length n: forward (step 1)
+  // and inverse (step 7) descriptors in d_dst2 [off, off + count)
+  struct Dst2Group { int n; int64_t off; int count; };
+  std::vector<Dst2Group> p1s, p7s;
+  Dst2Desc* d_dst2 = nullptr;
   bool use_xform = false;
   int max_systems = 0, max_systems_global = 0;
   // workspace layout (bytes)
@@ -126,6 +132,15 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   int64_t g_off = 0, h_off = 0, vx_off = 0, vy_off = 0, rx = 0, ry = 0, r1 = 0, r2 = 0, p1 = 0, p2 = 0, wx = 0,
           wy = 0, gf = 0;
 };
+
+void free_pass(PassPlan& pp) {
+  cudaFree(pp.d_descs);
+  cudaFree(pp.d_zb);
+  cudaFree(pp.d_pd);
+  cudaFree(pp.d_own);
+  cudaFree(pp.d_wmask);
+  cudaFree(pp.d_dst2);
+}
 
 }  // namespace
 
@@ -474,6 +489,40 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
 
   // DMMA transform passes: the same contractions, split by real / complex eigenvector matrix
   pp.use_xform = !in_real && !out_real;
+  // blocks uniform on both axes with one length: steps 1 and 7 as plane transforms (k_dst2)
+  auto fused2 = [&](int b) {
+    const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
+    return P->opt.plane_dst && bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
+  };
+  if (pp.use_xform) {
+    std::map<int, std::vector<Dst2Desc>> f2, i2;  // per length n
+    for (int b : blk_ids) {
+      if (!fused2(b)) continue;
+      const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
+      const int64_t pl = (int64_t)bx.n * by.n, g0 = (int64_t)(by.lo - 1) * Nx + (bx.lo - 1);
+      Dst2Desc d{};
+      d.tw_off = P->t_tw.at(2 * (bx.n + 1));
+      d.nplanes = (int)RZ;
+      d.b_buf = B_F; d.b_off = g0; d.sB1 = (int64_t)Nx * Ny; d.sBr = Nx;       // f[rk][y0+q][x0+p]
+      d.c_buf = B_MS; d.c_off = ms[b]; d.sC1 = pl; d.sCr = bx.n;                // MS[rk][m][l]
+      d.ax = bx.dst_fwd; d.ay = by.dst_fwd;
+      f2[bx.n].push_back(d);
+      d.b_buf = B_MS; d.b_off = ms[b]; d.sB1 = pl; d.sBr = bx.n;                // MS[rk][m][l]
+      d.c_buf = B_U; d.c_off = g0; d.sC1 = (int64_t)Nx * Ny; d.sCr = Nx;        // u[rk][y0+q][x0+p]
+      d.ax = bx.dst_inv; d.ay = by.dst_inv;
+      i2[bx.n].push_back(d);
+    }
+    std::vector<Dst2Desc> all;
+    for (auto* m : {&f2, &i2})
+      for (auto& kv : *m) {
+        (m == &f2 ? pp.p1s : pp.p7s).push_back({kv.first, (int64_t)all.size(), (int)kv.second.size()});
+        all.insert(all.end(), kv.second.begin(), kv.second.end());
+      }
+    if (!all.empty()) {
+      CUDA_TRY(cudaMalloc(&pp.d_dst2, sizeof(Dst2Desc) * all.size()));
+      CUDA_TRY(cudaMemcpy(pp.d_dst2, all.data(), sizeof(Dst2Desc) * all.size(), cudaMemcpyHostToDevice));
+    }
+  }
   if (pp.use_xform) {
     std::vector<GemmDesc> vc, vr;
     auto split = [&](StageDescs& sc, StageDescs& sr, std::vector<std::pair<int, StageDescs>>& sd,
@@ -485,6 +534,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
         const int b = blk_ids[q];
         const AxisBlock& ab = xaxis ? X.blocks[b % nbx] : Y.blocks[b / nbx];
         const int64_t roff = fwd ? ab.Fr : ab.Wr;
+        if (fused2(b)) continue;  // k_dst2 (both axes at once)
         if (ab.dst) {
           d.scale = fwd ? ab.dst_fwd : ab.dst_inv;
           d.a_off = P->t_tw.at(2 * (ab.n + 1));  // twiddles W_L^j of the odd-extension FFT
@@ -646,12 +696,24 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     end();
     return LFDS_OK;
   };
+  // plane sine transforms (uniform x uniform blocks), one launch per block length
+  auto plane2 = [&](const std::vector<PassPlan::Dst2Group>& gs, int stg) -> int {
+    if (gs.empty()) return LFDS_OK;
+    begin(stg);
+    for (auto& g : gs) {
+      CUDA_TRY(launch_dst2(pp.d_dst2 + g.off, g.count, g.n, (int)((int64_t)R * Nz), bufs, st));
+      P->launches += (g.count + 65534) / 65535;
+    }
+    end();
+    return LFDS_OK;
+  };
   int rc;
   const bool has_if = nifx + nify > 0;
   const int l_begin = P->sharded ? P->l_begin : 0, l_end = P->sharded ? P->l_end : Nx;
   (void)nblk;
   // pass 1
   if (phases & PH_1) {
+  if ((rc = plane2(pp.p1s, ST_P1S))) return rc;
   if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s, ST_X1S, ST_X1D))) return rc;
   if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s, ST_Y1S, ST_Y1D))) return rc;
   begin(ST_Z1);
@@ -773,6 +835,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     end();
   }
   // step 7
+  if ((rc = plane2(pp.p7s, ST_P7S))) return rc;
   if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false, &pp.y7s, ST_Y7S, ST_Y7D))) return rc;
   if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s, ST_X7S, ST_X7D))) return rc;
   if (has_if) {  // (sharded: every rank writes its own segments of the planes, pp.d_wmask)
@@ -801,13 +864,14 @@ void lfds_default_options(lfds_options* o) {
   o->profile = 0;
   o->s5_modal = 1;
   o->graph = 0;
+  o->plane_dst = 1;
 }
 
 int lfds_stage_count(void) { return ST_COUNT; }
 const char* lfds_stage_name(int i) { return (i >= 0 && i < ST_COUNT) ? kStageNames[i] : ""; }
 
-int lfds_stage_times(lfds_plan* P, double* ms, int* launches) {
-  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+// accumulate the pending stage records (waits for their events)
+static int prof_drain(lfds_plan* P) {
   for (auto& r : P->prof.recs) {
     CUDA_TRY(cudaEventSynchronize(r.b));
     float t = 0;
@@ -820,6 +884,13 @@ int lfds_stage_times(lfds_plan* P, double* ms, int* launches) {
     }
   }
   P->prof.recs.clear();
+  return LFDS_OK;
+}
+
+int lfds_stage_times(lfds_plan* P, double* ms, int* launches) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  int rc;
+  if ((rc = prof_drain(P))) return rc;
   for (int i = 0; i < ST_COUNT; ++i) {
     if (ms) ms[i] = P->prof.ms[i];
     if (launches) launches[i] = P->prof.launches[i];
@@ -1408,11 +1479,7 @@ int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_
     P->m_end = -1;
   }
   for (auto& kv : P->passes) {  // descriptors depend on the owned blocks: rebuild lazily
-    cudaFree(kv.second.d_descs);
-    cudaFree(kv.second.d_zb);
-    cudaFree(kv.second.d_pd);
-    cudaFree(kv.second.d_own);
-    cudaFree(kv.second.d_wmask);
+    free_pass(kv.second);
   }
   P->passes.clear();
   return LFDS_OK;
@@ -1428,11 +1495,7 @@ int lfds_set_mode_rows(lfds_plan* P, int m_begin, int m_end) {
   P->m_begin = m_begin;
   P->m_end = m_end;
   for (auto& kv : P->passes) {  // descriptors depend on the range: rebuild lazily
-    cudaFree(kv.second.d_descs);
-    cudaFree(kv.second.d_zb);
-    cudaFree(kv.second.d_pd);
-    cudaFree(kv.second.d_own);
-    cudaFree(kv.second.d_wmask);
+    free_pass(kv.second);
   }
   P->passes.clear();
   return LFDS_OK;
@@ -1503,6 +1566,10 @@ int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws,
                    P->gkey_wsb == ws_bytes && P->gkey_nrhs == nrhs;
   if (!hit) {
     if (P->gexec) {
+      // pending stage records of earlier replays refer to the old graph's events: take their
+      // times now, before those events are destroyed
+      int rc;
+      if ((rc = prof_drain(P))) return rc;
       cudaGraphExecDestroy(P->gexec);
       P->gexec = nullptr;
       for (auto& r : P->grecs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -1641,11 +1708,7 @@ int lfds_get_basis(const lfds_plan* P, int axis, int block, int* n, int* kind, i
 void lfds_destroy(lfds_plan* P) {
   if (!P) return;
   for (auto& kv : P->passes) {
-    cudaFree(kv.second.d_descs);
-    cudaFree(kv.second.d_zb);
-    cudaFree(kv.second.d_pd);
-    cudaFree(kv.second.d_own);
-    cudaFree(kv.second.d_wmask);
+    free_pass(kv.second);
   }
   if (P->d_tab) cudaFree(P->d_tab);
   if (P->gexec) cudaGraphExecDestroy(P->gexec);

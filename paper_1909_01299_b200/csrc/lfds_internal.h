@@ -145,6 +145,18 @@ cudaError_t launch_xform(const GemmDesc* d_descs, int ndesc, int maxM, int64_t m
 bool dst_supported(int n);
 cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, bool kcontig, const Bufs& bufs,
                        cudaStream_t st);
+// Plane (2-D) sine transform of a uniform x uniform block, both axes of length n: per plane
+// r < nplanes, C[r][m][l] = ay ax sum_{q,p} S_mq S_lp B[r][q][p] (S = DST-I; rows q/m strided
+// by sBr/sCr, p/l contiguous).  One pass over the block instead of an x pass and a y pass.
+struct Dst2Desc {
+  int64_t b_off, sB1, sBr;
+  int64_t c_off, sC1, sCr;
+  int64_t tw_off;            // W_L^j table in B_TAB
+  int nplanes, b_buf, c_buf, pad;
+  double ax, ay;             // DST-I scales of the two axes (dst_fwd or dst_inv)
+};
+bool dst2_supported(int n);
+cudaError_t launch_dst2(const Dst2Desc* d_descs, int ndesc, int n, int nplanes, const Bufs& bufs, cudaStream_t st);
 // z-solves (lfds_zsolve.cu): mode 1 = in place (step 2), 2 = Dirichlet lifting added to v~
 // (step 6), 3 = step-5 global modes with the rank-|I| RHS built from R1/R2 (g != NULL)
 cudaError_t launch_zsolve(int mode, const ZBlock* d_blocks, int nblocks, int max_nx, int max_ny, int R, int nz,

@@ -37,7 +37,8 @@ class _Z(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("refine", ctypes.c_int), ("refine_tol", ctypes.c_double),
                 ("residual_dd", ctypes.c_int), ("device", ctypes.c_int), ("rhs_chunk", ctypes.c_int),
-                ("profile", ctypes.c_int), ("s5_modal", ctypes.c_int), ("graph", ctypes.c_int)]
+                ("profile", ctypes.c_int), ("s5_modal", ctypes.c_int), ("graph", ctypes.c_int),
+                ("plane_dst", ctypes.c_int)]
 
 
 class Report(ctypes.Structure):
@@ -118,7 +119,8 @@ class Plan:
     def __init__(self, hx, hy, hz, sigma_node, sigma_edge, lam, iface_x: Sequence[int] = (),
                  iface_y: Sequence[int] = (), *, dtype: str = "c128", refine: int = 0,
                  refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0,
-                 profile: bool = False, s5_modal: bool = True, graph: bool = False):
+                 profile: bool = False, s5_modal: bool = True, graph: bool = False,
+                 plane_dst: bool = True):
         opt = Options()
         _lib.lfds_default_options(ctypes.byref(opt))
         opt.dtype = LFDS_F64 if dtype in ("f64", "float64") else LFDS_C128
@@ -126,6 +128,8 @@ class Plan:
         opt.device, opt.rhs_chunk, opt.profile = int(device), int(rhs_chunk), int(bool(profile))
         opt.s5_modal = int(bool(s5_modal))
         opt.graph = int(bool(graph))
+        opt.plane_dst = int(bool(plane_dst))
+        self.plane_dst = bool(plane_dst)
         self.dtype = opt.dtype
         hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
         sn_, psn = _zarr(sigma_node); se_, pse = _zarr(sigma_edge)

@@ -184,6 +184,29 @@ def test_sine_transform_lengths(n):
     assert rel(Ut[0], reft) < TOL
 
 
+@pytest.mark.parametrize("n", [15, 31, 63])
+def test_plane_sine_lengths(n):
+    """Plane (2-D) sine transform k_dst2 of uniform x uniform blocks at every length it is used for
+    (L = 32, 64: one CTA per plane; 128: a 2-CTA cluster), next to thin complex
+    (non-uniform) blocks that stay on the 1-D passes; element-wise against the oracle, and the
+    plane stages must have run.  Non-square RHS pattern: a transposed operand would show."""
+    from workloads.configs import axis_steps
+    h = axis_steps(2 * n + 3, 0, 1.0, 3, "const")   # 3 PML + core (nodes 4 .. 2n+6) + 3 PML
+    ifc = [4, n + 5, 2 * n + 6]                        # blocks: 3 (PML), n, n (uniform), 3 (PML)
+    p = _steps_problem(h, 0.8 * h, 3, ifc, ifc)        # different step per axis: a_x != a_y
+    rng = np.random.default_rng(1000 + n)
+    F = rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape)
+    F[0, :, : p.shape[1] // 3, :] *= 3.0
+    plan, U = gpu_solve(p, F, profile=True)
+    st = plan.stage_times()
+    assert st["step1_plane_sine"][1] >= 1 and st["step7_plane_sine"][1] >= 1, st
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
+    assert rel(U[0], ref) < TOL, rel(U[0], ref)
+    _, U1 = gpu_solve(p, F, plane_dst=False)           # the x pass + y pass form, same operator
+    assert rel(U1[0], ref) < TOL
+    assert rel(U[0], U1[0]) < 1e-12
+
+
 def test_zero_rhs_gives_zero():
     p = shrunken("c3")
     _, U = gpu_solve(p, np.zeros((1,) + p.shape, complex))
@@ -340,10 +363,13 @@ def test_graph_replay_matches_stream_solve(name, refine):
     assert torch.equal(first, ua) and torch.equal(U, ua)
     st = b.stage_times()
     assert st["step2_zsolve"][0] > 0 and st["step2_zsolve"][1] >= 2
+    b.solve(F, out=U)          # replay; its stage records stay pending ...
     U2 = torch.empty_like(F)
-    b.solve(F, out=U2)         # new output buffer: recaptured
+    b.solve(F, out=U2)         # ... across a recapture (new output buffer), which drops the old graph
     torch.cuda.synchronize()
     assert torch.equal(U2, ua)
+    st = b.stage_times()       # the pending records were taken before their events were freed
+    assert st["step2_zsolve"][1] >= 2 and st["step2_zsolve"][0] > 0
 
 
 @pytest.mark.parametrize("world", [4, 8])

@@ -19,7 +19,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 echo "launch list exit $?"
 cmd1="python bench.py --config c4 --steps 1 --warmup 0 --no-e2e --no-cpu"
 i=0
-for rx in "k_zs2" "k_s5m" "k_zs1" "k_dstw" "k_dst<" "k_xform3m" "k_proj_rows" "k_residual"; do
+for rx in "k_zs2" "k_s5m" "k_zs1" "k_dstw" "k_dst<" "k_xform3m" "k_proj_rows" "k_residual" "k_dst2"; do
   i=$((i+1))
   c=$cmd1; [ "$rx" = "k_residual" ] && c="python bench.py --config c2 --steps 1 --warmup 0 --no-e2e --no-cpu"
   out=/tmp/${tag}_k$i

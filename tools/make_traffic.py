@@ -12,6 +12,7 @@ STAGES = [  # (regex on the demangled kernel name, bench stages it stands for)
     (r"k_s5m<", ["step5_global_zsolve"]),
     (r"k_zs3", ["step5_global_zsolve"]),
     (r"k_dstw<", ["step1_x_sine", "step7_x_sine"]),
+    (r"k_dst2<", ["step1_plane_sine", "step7_plane_sine"]),
     (r"k_zs2", ["step6_zsolve_lift"]),
     (r"k_zs1", ["step2_zsolve"]),
     (r"k_dst<.*, (1|true)>", ["step1_x_sine", "step7_x_sine"]),
