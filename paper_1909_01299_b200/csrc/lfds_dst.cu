@@ -169,7 +169,7 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool val
 }
 
 template <int R1, int R2, bool KCONTIG>
-__global__ void __launch_bounds__(DST_THREADS, (R1 <= 16 && R2 <= 16) ? 5 : 1) k_dst(const GemmDesc* __restrict__ descs, Bufs bufs) {
+__global__ void __launch_bounds__(DST_THREADS, (R1 <= 16 && R2 <= 16) ? 5 : R1 == 20 ? 4 : 1) k_dst(const GemmDesc* __restrict__ descs, Bufs bufs) {
   constexpr int L = R1 * R2, N = L / 2;
   constexpr int CPB = DST_THREADS / R2;      // columns per CTA
   constexpr int LDT = CPB + 1;               // tile row stride (complex)

@@ -1,7 +1,8 @@
 #!/bin/bash
 # Round evidence on one GPU: bench lines of every config (with e2e and the CPU oracle
 # baseline), the --impl reference line, the ncu launch list of the default bench command, and
-# ncu --set full captures (one launch each) of the main kernels of the default config.
+# ncu --set full captures (one launch each) of the main kernels of the default config (the
+# residual kernel on C2, the plane sine transform on C4q).
 tag=${1:-r01ev}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/${tag}_pytest_gpu.log 2>&1
@@ -22,6 +23,7 @@ i=0
 for rx in "k_zs2" "k_s5m" "k_zs1" "k_dstw" "k_dst<" "k_xform3m" "k_proj_rows" "k_residual" "k_dst2"; do
   i=$((i+1))
   c=$cmd1; [ "$rx" = "k_residual" ] && c="python bench.py --config c2 --steps 1 --warmup 0 --no-e2e --no-cpu"
+  [ "$rx" = "k_dst2" ] && c="python bench.py --config c4q --steps 1 --warmup 0 --no-e2e --no-cpu"
   out=/tmp/${tag}_k$i
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$rx" -c 1 -o $out $c > gpurun_out/${tag}_prof_k${i}.log 2>&1
   ncu -i $out.ncu-rep --page raw --csv > gpurun_out/${tag}_prof_k${i}_raw.csv 2>/dev/null
