@@ -25,6 +25,14 @@ namespace {
 
 namespace cg = cooperative_groups;
 
+// cluster barrier without release semantics: orders only execution (used where the CTAs just
+// need each other's reads of their own shared memory done — a release would also wait for all
+// of this thread's outstanding global stores)
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+}
+
 struct zc2 {
   double x, y;
 };
@@ -532,14 +540,15 @@ __global__ void __launch_bounds__(Dst2Cfg<R1, R2>::WARPS * 32) k_dst2(const Dst2
             const int k = k1 + R1 * k2;
             if (k >= 1 && k < N) {
               const int l = k - 1, o = l / RPC;
-              double2* dst = cluster.map_shared_rank(Tsm, o);
+              double2* dst = C::CL == 1 ? Tsm : cluster.map_shared_rank(Tsm, o);
               dst[r * LDT + (l - o * RPC)] = make_double2(-hx * b[rr][k2].y, hx * b[rr][k2].x);
             }
           }
         }
       }
     }
-    cluster.sync();  // the plane's x-transformed rows are complete in the cluster
+    // the plane's x-transformed rows are complete in the cluster (one CTA: a block barrier)
+    if constexpr (C::CL == 1) __syncthreads(); else cluster.sync();
     // ---- y phase: columns (x-modes) r0 .. r0+nr-1 of all n rows, CPW columns per warp step
     const double hy = 0.5 * D.ay;
     for (int g = warp; g * CPW < nr; g += C::WARPS) {
@@ -575,7 +584,8 @@ __global__ void __launch_bounds__(Dst2Cfg<R1, R2>::WARPS * 32) k_dst2(const Dst2
         }
       }
     }
-    cluster.sync();  // every CTA has read its Tsm before the next x phase writes into it
+    // every CTA has read its Tsm before the next x phase writes into it
+    if constexpr (C::CL == 1) __syncthreads(); else cluster_sync_relaxed();
   }
 }
 
