@@ -36,3 +36,36 @@ def test_refinement_stage_counted_once_per_refinement():
     alg = bench.stage_algorithmic(p, 1, None)
     assert r["kernel"] == "refine_residual"
     assert abs(r["achieved"] - alg["refine_residual"][1] / 5e-3 / 1e9) < 1e-6 * r["achieved"]
+
+
+class _KindsPlan:
+    """Stand-in for a Plan: every block uniform (kind 0) except the first and last (PML, kind 2)."""
+
+    def __init__(self, nblocks, plane_dst):
+        self.nb, self.plane_dst = nblocks, plane_dst
+
+    def basis(self, axis, b):
+        return None, None, 2 if b in (0, self.nb - 1) else 0
+
+    def info(self):
+        return {"s5_modal": 1}
+
+
+def test_plane_sine_bytes_replace_the_two_passes():
+    """C4q (31-node blocks, L = 64): with plane_dst the uniform x uniform blocks move 32 B per
+    element once (step1_plane_sine) instead of in the x pass and again in the y pass; the sine
+    passes keep only the blocks uniform along one axis.  Total sine bytes drop by exactly the
+    fused volume."""
+    p = make_problem("c4q")
+    nb = len(p.iface_x) + 1
+    on = bench.stage_algorithmic(p, 1, _KindsPlan(nb, True))
+    off = bench.stage_algorithmic(p, 1, _KindsPlan(nb, False))
+    cuts = [0] + list(p.iface_x) + [p.nx + 1]
+    n = [cuts[i + 1] - cuts[i] - 1 for i in range(nb)]
+    fused = sum(n[i] * n[j] * p.nz for i in range(1, nb - 1) for j in range(1, nb - 1))
+    assert on["step1_plane_sine"][1] == on["step7_plane_sine"][1] == 32.0 * fused
+    assert off["step1_plane_sine"][1] == 0
+    for st in ("step1_x_sine", "step1_y_sine", "step7_x_sine", "step7_y_sine"):
+        assert off[st][1] - on[st][1] == 32.0 * fused
+    # dense passes are untouched
+    assert on["step1_x_dense"] == off["step1_x_dense"]
