@@ -221,6 +221,9 @@ def stage_algorithmic(p, R: int, plan=None):
     # plane sine transform (both axes in one pass): 32 B per element of the fused blocks
     psine = (None, 32.0 * sum(bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by))
                               if fused(i, j)))
+    nf = plan.info().get("n_plane_dst") if plan else None
+    if nf is not None and nf != sum(fused(i, j) for i in range(len(bx)) for j in range(len(by))):
+        raise RuntimeError(f"plane-transform block count {nf} (library) != bench accounting")
     el_blk = sum(nx * ny * nz * R for nx in bx for ny in by)
     el_all = p.nx * p.ny * nz * R
     nifx, nify = len(p.iface_x), len(p.iface_y)

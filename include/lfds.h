@@ -221,6 +221,9 @@ typedef struct {
   int s5_modal;                /* 1 if step 5 runs in the z-modal form (options.s5_modal, real z) */
   double z_eig_residual;       /* z modal basis: max|A'z - theta E z| / (||A'|| max|Z|)       */
   double z_eig_orth;           /* z modal basis: max|Z^T E Z - I|                             */
+  int n_plane_dst;             /* blocks whose steps 1 and 7 run as one plane sine transform  */
+                               /* (options.plane_dst; uniform on both axes, one length L <= 128,
+                                  complex data)                                              */
 } lfds_info;
 int lfds_get_info(const lfds_plan* plan, lfds_info* info);
 

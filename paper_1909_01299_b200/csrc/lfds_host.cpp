@@ -1161,6 +1161,10 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
   I.eig_max_biorth = mbio;
   I.device_table_bytes = T.v.size() * sizeof(double2);
   I.s5_modal = P->s5m ? 1 : 0;
+  I.n_plane_dst = 0;  // the fused2() rule of build_pass (complex data only)
+  if (P->opt.plane_dst && P->opt.dtype != LFDS_F64)
+    for (auto& by : Y.blocks)
+      for (auto& bx : X.blocks) I.n_plane_dst += bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
   *out = P.release();
   return LFDS_OK;
 }

@@ -55,7 +55,8 @@ class Info(ctypes.Structure):
                 ("nby", ctypes.c_int), ("n_if_x", ctypes.c_int), ("n_if_y", ctypes.c_int), ("real_z", ctypes.c_int),
                 ("setup_seconds", ctypes.c_double), ("eig_max_residual", ctypes.c_double),
                 ("eig_max_biorth", ctypes.c_double), ("device_table_bytes", ctypes.c_size_t),
-                ("s5_modal", ctypes.c_int), ("z_eig_residual", ctypes.c_double), ("z_eig_orth", ctypes.c_double)]
+                ("s5_modal", ctypes.c_int), ("z_eig_residual", ctypes.c_double), ("z_eig_orth", ctypes.c_double),
+                ("n_plane_dst", ctypes.c_int)]
 
 
 _P = ctypes.c_void_p

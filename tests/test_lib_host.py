@@ -186,3 +186,21 @@ def test_interface_count_limits():
     with pytest.raises(LfdsError) as e:
         host_plan(pc)
     assert e.value.code == 1
+
+
+def test_plane_transform_block_count(lfds):
+    """lfds_info.n_plane_dst: the blocks whose steps 1 and 7 run as one plane sine transform —
+    uniform on both axes with one length L = 2(n+1) <= 128 (C4q: the 30 x 30 core blocks of 31
+    nodes; C4: its 127-node core blocks stay on the two 1-D passes; off with plane_dst=False,
+    and for the real f64 path, which has no sine kernels)."""
+    import bench
+    from workloads import make_problem
+    q = make_problem("c4q")
+    pq = host_plan(q)
+    assert pq.info()["n_plane_dst"] == 30 * 30
+    assert host_plan(q, plane_dst=False).info()["n_plane_dst"] == 0
+    assert host_plan(make_problem("c4")).info()["n_plane_dst"] == 0
+    assert host_plan(shrunken("c1")).info()["n_plane_dst"] == 0
+    # bench.py's byte accounting agrees with the library's rule (it raises otherwise)
+    alg = bench.stage_algorithmic(q, 1, pq)
+    assert alg["step1_plane_sine"][1] == 32.0 * 900 * 31 * 31 * q.nz
