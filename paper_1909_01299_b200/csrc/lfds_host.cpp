@@ -396,11 +396,17 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
                        B_IF, pp.wy + (int64_t)b * RZ * Nx + (bx.lo - 1), 1, Nx, 0, (int)RZ, 1, 0));
       }
     if (P->rank0)  // intersections of x-plane a with y-plane b: written from WX[a][rk][q_b]
+      // (rows q_b of W_y P1; equally spaced interface rows form one strided descriptor per run,
+      // instead of one single-row contraction per intersection)
       for (int a = 0; a < nifx; ++a)
-        for (int b = 0; b < nify; ++b) {
-          const int q = Y.iface[b] - 1;
-          v.push_back(gd(Y.Wg + (int64_t)q * Ny, Ny, 1, 1, Ny, B_IF, pp.p1 + (int64_t)a * RZ * Ny, 1, Ny, 0, B_IF,
-                         pp.wx + (int64_t)a * RZ * Ny + q, 1, Ny, 0, (int)RZ, 1, 0));
+        for (int b0 = 0; b0 < nify;) {
+          int cnt = 1;
+          const int d = b0 + 1 < nify ? Y.iface[b0 + 1] - Y.iface[b0] : 1;
+          while (b0 + cnt < nify && Y.iface[b0 + cnt] - Y.iface[b0 + cnt - 1] == d) ++cnt;
+          const int q = Y.iface[b0] - 1;
+          v.push_back(gd(Y.Wg + (int64_t)q * Ny, (int64_t)d * Ny, 1, cnt, Ny, B_IF, pp.p1 + (int64_t)a * RZ * Ny, 1, Ny,
+                         0, B_IF, pp.wx + (int64_t)a * RZ * Ny + q, d, Ny, 0, (int)RZ, 1, 0));
+          b0 += cnt;
         }
   }
   stage(pp.s5wx, std::move(v)); v.clear();
