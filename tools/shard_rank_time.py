@@ -59,3 +59,19 @@ for world in worlds:
           f"comm est {comm:.2f} ms -> {est:.2f} ms, speed-up {t1 / est:.2f}x (1 GPU {t1:.2f} ms)", flush=True)
 plan.set_partition(None)
 print(json.dumps(out))
+if os.environ.get("SHARD_STAGES"):  # stage breakdown of rank 0 of the largest world
+    pp = Plan.from_problem(p, profile=True)
+    W = max(worlds)
+    dist.shard(pp, 0, W)
+    ws = pp.workspace(1)
+    for ph in (1, 2, 3):
+        pp.solve_phase(ph, f, u, ws)
+    torch.cuda.synchronize()
+    pp.stage_times()
+    for _ in range(3):
+        for ph in (1, 2, 3):
+            pp.solve_phase(ph, f, u, ws)
+    torch.cuda.synchronize()
+    st = {k: v[0] / 3 for k, v in pp.stage_times().items() if v[1]}
+    print(f"{cfg} world {W} rank 0 stages (ms):", " ".join(f"{k}={v:.3f}" for k, v in st.items()),
+          f"sum={sum(st.values()):.3f}", flush=True)
