@@ -207,6 +207,31 @@ def test_plane_sine_lengths(n):
     assert rel(U[0], U1[0]) < 1e-12
 
 
+def test_plane_sine_under_graph_capture_and_rhs_chunks():
+    """The plane transform (cluster launch) replays bit-identically from a captured CUDA graph
+    and gives the same result with RHS chunking (planes = chunk x N_z per launch)."""
+    from workloads.configs import axis_steps
+    from paper_1909_01299_b200 import Plan
+    n = 63
+    h = axis_steps(2 * n + 3, 0, 1.0, 3, "const")
+    ifc = [4, n + 5, 2 * n + 6]
+    p = _steps_problem(h, h, 5, ifc, ifc)
+    rng = np.random.default_rng(77)
+    F = torch.from_numpy(rng.standard_normal((3,) + p.shape) + 1j * rng.standard_normal((3,) + p.shape)).cuda()
+    ua = Plan.from_problem(p).solve(F)
+    g = Plan.from_problem(p, graph=True)
+    assert g.info()["n_plane_dst"] == 4
+    U = torch.empty_like(F)
+    g.solve(F, out=U)
+    g.solve(F, out=U)
+    uc = Plan.from_problem(p, rhs_chunk=2).solve(F)
+    torch.cuda.synchronize()
+    assert torch.equal(U, ua)
+    assert torch.equal(uc, ua)
+    ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[1].cpu().numpy()))
+    assert rel(ua[1].cpu().numpy(), ref) < TOL
+
+
 def test_zero_rhs_gives_zero():
     p = shrunken("c3")
     _, U = gpu_solve(p, np.zeros((1,) + p.shape, complex))
