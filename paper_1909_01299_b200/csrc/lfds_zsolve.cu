@@ -353,37 +353,39 @@ struct FaceStage {
 template <int RT, bool FULL, int TL>
 __device__ __forceinline__ void zs2_body(const ZBlock& B, const Tile& t, int nz, const ZTabS& T, const double2* TAB,
                                          Bufs& bufs, double2* fsm) {
-  constexpr int ZSEG = 8, NSTAGE = 2, TM = ZT / TL;
-  using FS = FaceStage<TL, ZSEG>;
+  // 8-row solve segments; the face rows are staged 16 rows (two segments) at a time, so the
+  // CTA meets at a barrier twice per 16 rows instead of twice per 8
+  constexpr int ZSEG = 8, FSEG = 2 * ZSEG, NSTAGE = 2, TM = ZT / TL;
+  using FS = FaceStage<TL, FSEG>;
   const int r = blockIdx.z;
   const double2* IF = reinterpret_cast<const double2*>(bufs.p[B_IF]);
   const int64_t nxy = (int64_t)B.nx * B.ny;
   double2* line = reinterpret_cast<double2*>(bufs.p[B_MS]) + B.ms_off + (int64_t)r * nz * nxy +
                   (int64_t)(t.active ? t.m : 0) * B.nx + (t.active ? t.l : 0);
   const Ring<ZSEG, NSTAGE, FULL> ring{fsm + 2 * FS::SLOTS, line, nxy, nz, t.active};
-  const int nseg = (nz + ZSEG - 1) / ZSEG;
+  const int nseg = (nz + ZSEG - 1) / ZSEG, nfs = (nz + FSEG - 1) / FSEG;
   const int64_t nslot = (int64_t)gridDim.x * gridDim.y * gridDim.z * ZT;
   double2* ck = ck_base(bufs);
   // face f row k at IF[base_f + (r*nz + k)*fs + index]
   const int64_t fs = B.fstride, ro = (int64_t)r * nz * fs;
   const bool hL = B.gL >= 0, hR = B.gR >= 0, hB = B.gB >= 0, hT = B.gT >= 0;
-  // cooperative copy of segment sg into slot sg&1: copy c -> (face, row j, index)
-  auto stage = [&](int sg) {
-    if (sg >= 0 && sg < nseg) {
-      double2* d = fsm + (sg & 1) * FS::SLOTS;
-      const int k0 = sg * ZSEG;
+  // cooperative copy of face segment q (rows 16q .. 16q+15) into slot q&1
+  auto stage = [&](int q) {
+    if (q >= 0 && q < nfs) {
+      double2* d = fsm + (q & 1) * FS::SLOTS;
+      const int k0 = q * FSEG;
 #pragma unroll
       for (int i = 0; i < (FS::SLOTS + ZT - 1) / ZT; ++i) {
         const int c = threadIdx.x + i * ZT;
         if (c >= FS::SLOTS) break;
         const double2* src = nullptr;
         if (c < FS::GL) {  // GB / GT rows, TL entries each
-          const int f = c / (ZSEG * TL), j = (c / TL) % ZSEG, li = c % TL, k = k0 + j;
-          if ((FULL || k < nz) && t.l0 + li < B.nx && (f ? hT : hB)) src = IF + (f ? B.gT : B.gB) + ro + k * fs + t.l0 + li;
+          const int f = c / (FSEG * TL), j = (c / TL) % FSEG, li = c % TL, k = k0 + j;
+          if (k < nz && t.l0 + li < B.nx && (f ? hT : hB)) src = IF + (f ? B.gT : B.gB) + ro + k * fs + t.l0 + li;
         } else {  // GL / GR rows, TM entries each
           const int c2 = c - FS::GL;
-          const int f = c2 / (ZSEG * TM), j = (c2 / TM) % ZSEG, mi = c2 % TM, k = k0 + j;
-          if ((FULL || k < nz) && t.m0 + mi < B.ny && (f ? hR : hL)) src = IF + (f ? B.gR : B.gL) + ro + k * fs + t.m0 + mi;
+          const int f = c2 / (FSEG * TM), j = (c2 / TM) % FSEG, mi = c2 % TM, k = k0 + j;
+          if (k < nz && t.m0 + mi < B.ny && (f ? hR : hL)) src = IF + (f ? B.gR : B.gL) + ro + k * fs + t.m0 + mi;
         }
         if (src) cp16(d + c, src);
       }
@@ -400,20 +402,21 @@ __device__ __forceinline__ void zs2_body(const ZBlock& B, const Tile& t, int nz,
   // blocks (RT 2: real steps, so real W rows and real face couplings) take real coefficients:
   // 2 FMAs per face term instead of 4.
   auto lift = [&](int sg, int j) {
-    const double2* d = fsm + (sg & 1) * FS::SLOTS;
+    const double2* d = fsm + ((sg >> 1) & 1) * FS::SLOTS;
+    const int jj = (sg & 1) * ZSEG + j;
     cplx acc = mk(0, 0);
     if (RT == 2) {
       auto rfma = [](double c, double2 v, cplx a) { return mk(fma(c, v.x, a.x), fma(c, v.y, a.y)); };
-      if (hL) acc = rfma(cL.x, d[FS::GL + j * TM + ty], acc);
-      if (hR) acc = rfma(cR.x, d[FS::GR + j * TM + ty], acc);
-      if (hB) acc = rfma(cB.x, d[FS::GB + j * TL + tx], acc);
-      if (hT) acc = rfma(cT.x, d[FS::GT + j * TL + tx], acc);
+      if (hL) acc = rfma(cL.x, d[FS::GL + jj * TM + ty], acc);
+      if (hR) acc = rfma(cR.x, d[FS::GR + jj * TM + ty], acc);
+      if (hB) acc = rfma(cB.x, d[FS::GB + jj * TL + tx], acc);
+      if (hT) acc = rfma(cT.x, d[FS::GT + jj * TL + tx], acc);
       return acc;
     }
-    if (hL) acc = cfma(cL, mk(d[FS::GL + j * TM + ty]), acc);
-    if (hR) acc = cfma(cR, mk(d[FS::GR + j * TM + ty]), acc);
-    if (hB) acc = cfma(cB, mk(d[FS::GB + j * TL + tx]), acc);
-    if (hT) acc = cfma(cT, mk(d[FS::GT + j * TL + tx]), acc);
+    if (hL) acc = cfma(cL, mk(d[FS::GL + jj * TM + ty]), acc);
+    if (hR) acc = cfma(cR, mk(d[FS::GR + jj * TM + ty]), acc);
+    if (hB) acc = cfma(cB, mk(d[FS::GB + jj * TL + tx]), acc);
+    if (hT) acc = cfma(cT, mk(d[FS::GT + jj * TL + tx]), acc);
     return acc;
   };
   const cplx s = t.active ? ld(TAB + B.lamx + t.l) + ld(TAB + B.lamy + t.m) : mk(0, 0);
@@ -422,9 +425,11 @@ __device__ __forceinline__ void zs2_body(const ZBlock& B, const Tile& t, int nz,
   stage(0);
   for (int sg = 0; sg < nseg; ++sg) {
     const int k0 = sg * ZSEG;
-    stage(sg + 1);
-    cp_wait<1>();
-    __syncthreads();  // segment sg staged by every thread
+    if ((sg & 1) == 0) {  // first segment of face segment sg/2
+      stage((sg >> 1) + 1);
+      cp_wait<1>();
+      __syncthreads();  // face segment staged by every thread
+    }
     if (t.active) {
       ck[(int64_t)(2 * sg) * nslot] = make_double2(cp.x, cp.y);
       ck[(int64_t)(2 * sg + 1) * nslot] = make_double2(dp.x, dp.y);
@@ -439,20 +444,22 @@ __device__ __forceinline__ void zs2_body(const ZBlock& B, const Tile& t, int nz,
         }
       }
     }
-    __syncthreads();  // slot sg&1 consumed before it is refilled with segment sg+2
+    if ((sg & 1) == 1 || sg == nseg - 1) __syncthreads();  // slot consumed before it is refilled
   }
   // ---- backward sweep: faces staged again in reverse order, v~ through the ring
   cp_wait<0>();
-  stage(nseg - 1);
+  stage((nseg - 1) >> 1);
   ring.issue(nseg - 1);
   cplx x = mk(0, 0);
   double2 nc = ck[(int64_t)(2 * (nseg - 1)) * nslot], nd = ck[(int64_t)(2 * (nseg - 1) + 1) * nslot];
   for (int sg = nseg - 1; sg >= 0; --sg) {
     const int k0 = sg * ZSEG;
-    stage(sg - 1);
+    const bool first = (sg & 1) == 1 || sg == nseg - 1;  // first visited segment of its face segment
+    if (first) stage((sg >> 1) - 1);
+    else cp_commit();
     ring.issue(sg - 1);
-    cp_wait<2>();  // this segment's faces and ring rows, issued one iteration earlier
-    __syncthreads();
+    cp_wait<2>();  // this face segment and this segment's ring rows, issued earlier
+    if (first) __syncthreads();
     if (t.active) {
       cplx rb[ZSEG], cs[ZSEG];
       cplx cc = mk(nc), dd = mk(nd);
@@ -483,7 +490,7 @@ __device__ __forceinline__ void zs2_body(const ZBlock& B, const Tile& t, int nz,
         }
       }
     }
-    __syncthreads();
+    if ((sg & 1) == 0) __syncthreads();  // face slot consumed before it is refilled
   }
   cp_wait<0>();
 }
@@ -749,7 +756,7 @@ cudaError_t launch_tl(int mode, dim3 grid, cudaStream_t st, const ZBlock* b, int
     if ((e = prep(k_zs1<REALZ, TL, FULL>, sm)) != cudaSuccess) return e;
     k_zs1<REALZ, TL, FULL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs, mp);
   } else if (mode == 2) {
-    const size_t sm = zt + (size_t)(2 * FaceStage<TL, 8>::SLOTS + 2 * 8 * ZT) * sizeof(double2);
+    const size_t sm = zt + (size_t)(2 * FaceStage<TL, 16>::SLOTS + 2 * 8 * ZT) * sizeof(double2);
     if ((e = prep(k_zs2<REALZ, TL, FULL>, sm)) != cudaSuccess) return e;
     k_zs2<REALZ, TL, FULL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs);
   } else {
