@@ -65,8 +65,10 @@ typedef struct {
   int graph;        /* 1: lfds_solve captures its launches into a CUDA graph and replays  */
                     /* it while (f, u, nrhs, workspace) repeat (refine >= 0 only); 0: off */
   int plane_dst;    /* 1: steps 1 and 7 of a block that is uniform on both axes with the    */
-                    /* same length run as ONE plane sine transform (both     */
-                    /* axes, one pass over the block); 0: an x pass and a y pass           */
+                    /* same length n, 2(n+1) <= 128, run as ONE plane sine   */
+                    /* transform (both axes, one pass over the block; longer blocks keep   */
+                    /* the two passes); 0: always an x pass and a y pass;   */
+                    /* lfds_info.n_plane_dst counts the blocks it applies to               */
 } lfds_options;
 
 /* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1,
