@@ -421,8 +421,11 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     if (nifx && m1s > m0s)  // (y-mode split: P1 rows outside [m0s, m1s) are zeroed in run_pass)
       v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p1t + m0s, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.p1 + m0s, Ny,
                      (int64_t)Nz * Ny, 1, nifx * R, m1s - m0s, 0));
-    if (nify) v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p2t, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.p2, Nx,
-                             (int64_t)Nz * Nx, 1, nify * R, Nx, 0));
+    // (block sharding: P2~ is zero outside the rank's x-modes, so only those columns of P2 are
+    // formed; run_pass zeroes the rest for the exchange)
+    if (nify && l1s > l0s)
+      v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p2t + l0s, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.p2 + l0s, Nx,
+                     (int64_t)Nz * Nx, 1, nify * R, l1s - l0s, 0));
     stage(pp.s5zi, std::move(v)); v.clear();
   }
   // step 6: face transforms GF[b][face][rk][mode] (faces L, R, B, T), e.g. GL = F_y w_L
@@ -782,6 +785,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     if (msplit && nifx)  // P1 rows of other y-modes: zero (exchange 2 sums the ranks' parts)
       CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.p1, 0,
                                sizeof(double2) * (size_t)nifx * R * Nz * Ny, st));
+    if (P->sharded && nify && (l_begin > 0 || l_end < Nx))  // P2 columns of other x-modes: zero
+      CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.p2, 0,
+                               sizeof(double2) * (size_t)nify * R * Nz * Nx, st));
     if (pp.s5zi.n) {
       CUDA_TRY(launch_xform(pp.d_descs + pp.s5zi.off, pp.s5zi.n, pp.s5zi.maxM, pp.s5zi.maxN, true, false, bufs, st));
       P->launches += 1;
