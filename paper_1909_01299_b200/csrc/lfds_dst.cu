@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(Dst2Cfg<R1, R2>::WARPS * 32) k_dst2(const Dst2
     if constexpr (C::CL == 1) __syncthreads(); else cluster.sync();
     // ---- y phase: columns (x-modes) r0 .. r0+nr-1 of all n rows, CPW columns per warp step
     const double hy = 0.5 * D.ay;
+    const bool rows_out = D.sCr != n;  // (uniform over the cluster: one descriptor per item)
     for (int g = warp; g * CPW < nr; g += C::WARPS) {
       const int cl = g * CPW + cw;
       const bool ok = cl < nr;
@@ -571,7 +572,9 @@ __global__ void __launch_bounds__(Dst2Cfg<R1, R2>::WARPS * 32) k_dst2(const Dst2
       }
       zc2 b[RPT][R2];
       dst2_fft<R1, R2>(a, twl, tws, ex, cw, t, b);
-      double2* Cc = Cg + r0 + cl;
+      // output rows strided in a larger array (step 7: u rows of the global grid): back into the
+      // column in place (this warp read all of it above) and stored as whole rows below; a
+      // contiguous output plane (step 1: the block's mode space) takes the direct stores
 #pragma unroll
       for (int rr = 0; rr < RPT; ++rr) {
         const int k1 = t + rr * R2;
@@ -579,9 +582,20 @@ __global__ void __launch_bounds__(Dst2Cfg<R1, R2>::WARPS * 32) k_dst2(const Dst2
 #pragma unroll
           for (int k2 = 0; k2 < R2 / 2; ++k2) {
             const int k = k1 + R1 * k2;
-            if (k >= 1 && k < N) Cc[(int64_t)(k - 1) * D.sCr] = make_double2(-hy * b[rr][k2].y, hy * b[rr][k2].x);
+            if (k >= 1 && k < N) {
+              const double2 v = make_double2(-hy * b[rr][k2].y, hy * b[rr][k2].x);
+              if (rows_out) Tsm[(k - 1) * LDT + cl] = v;
+              else Cg[(int64_t)(k - 1) * D.sCr + r0 + cl] = v;
+            }
           }
         }
+      }
+    }
+    if (rows_out) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < n * nr; idx += blockDim.x) {  // row m: x-modes r0 .. r0+nr-1
+        const int m = idx / nr, c = idx - m * nr;
+        Cg[(int64_t)m * D.sCr + r0 + c] = Tsm[m * LDT + c];
       }
     }
     // every CTA has read its Tsm before the next x phase writes into it
