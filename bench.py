@@ -253,7 +253,114 @@ def stage_algorithmic(p, R: int, plan=None):
     }
 
 
-def roofline_summary(p, nrhs, plan, stages, steps, config, ms_max, passes=1):
+def kernel_algorithmic(p, R: int, plan=None):
+    """Algorithmic (flops, bytes) per solve pass of each kernel kind (DESIGN.md §5 table), the
+    same accounting as stage_algorithmic regrouped by the kernel that does the work:
+
+    k_xform3m (complex eigenvector matrix, DMMA 3M): the dense passes of C blocks (8 n flops per
+    element and direction), the step-5 plane transforms W^T R / W P (8 N flops per plane element),
+    step 3's edge values (W_y G, W_x H: 8 n^2 per edge column) and step 6's face transforms
+    (F w-face: 8 n^2 per face column); 32 B per element of the dense passes and planes.
+    k_xform (real matrix): dense passes of R blocks (4 n) and the step-5 z-transforms (4 N_z per
+    plane element, both directions).  Sine kernels, z-solves, edge projection, refinement: bytes."""
+    alg = stage_algorithmic(p, R, plan)
+
+    def sizes(n, iface):
+        cuts = [0] + list(iface) + [n + 1]
+        return [cuts[i + 1] - cuts[i] - 1 for i in range(len(cuts) - 1)]
+    bx, by = sizes(p.nx, p.iface_x), sizes(p.ny, p.iface_y)
+    kx = [plan.basis(0, i)[2] if plan else 2 for i in range(len(bx))]
+    ky = [plan.basis(1, j)[2] if plan else 2 for j in range(len(by))]
+    nz = p.nz
+    esz = 8.0 if p.real else 16.0
+
+    def is_sine(kind, n):
+        L = 2 * (n + 1)
+        return kind == 0 and (L in (16, 32, 64, 128, 256, 512) or (L % 16 == 0 and L // 16 in (3, 5, 6, 10, 12, 20)))
+
+    fc = bc = fr = br = 0.0  # complex-S / real-S dense passes (4 per block: x, y forward + inverse)
+    for i in range(len(bx)):
+        for j in range(len(by)):
+            e = bx[i] * by[j] * nz * R
+            for k, n in ((kx[i], bx[i]), (ky[j], by[j])):
+                if p.real or is_sine(k, n):
+                    continue
+                if k == 2:
+                    fc += 2 * 8.0 * n * e
+                    bc += 2 * 2 * esz * e
+                else:
+                    fr += 2 * 4.0 * n * e
+                    br += 2 * 2 * esz * e
+    nifx, nify = len(p.iface_x), len(p.iface_y)
+    plane_el = (nifx * p.ny + nify * p.nx) * nz * R
+    if nifx + nify and not p.real:
+        fc += 2 * 8.0 * (nifx * p.ny * p.ny + nify * p.nx * p.nx) * nz * R  # forward + inverse plane transforms
+        bc += 2 * 2 * esz * plane_el
+        # step 3 edge values (two edge rows per block side) and step 6 face transforms (one per interior face)
+        for i in range(len(bx)):
+            for j in range(len(by)):
+                fc += 8.0 * (by[j] ** 2 + bx[i] ** 2) * 2 * nz * R
+                nfx = (i > 0) + (i < len(bx) - 1)
+                nfy = (j > 0) + (j < len(by) - 1)
+                fc += 8.0 * (nfx * by[j] ** 2 + nfy * bx[i] ** 2) * nz * R
+    modal = bool(plan.info().get("s5_modal", 0)) if plan else False
+    if modal:
+        fr += 2 * 4.0 * nz * plane_el
+        br += 2 * 2 * esz * plane_el
+    out = {
+        "k_xform3m": (fc or None, bc or None), "k_xform": (fr or None, br or None),
+        "k_dstw": (None, (alg["step1_x_sine"][1] or 0) + (alg["step7_x_sine"][1] or 0) or None),
+        "k_dst": (None, (alg["step1_y_sine"][1] or 0) + (alg["step7_y_sine"][1] or 0) or None),
+        "k_dst2": (None, (alg["step1_plane_sine"][1] or 0) + (alg["step7_plane_sine"][1] or 0) or None),
+        "k_zs1": alg["step2_zsolve"], "k_zs2": alg["step6_zsolve_lift"], "k_proj_rows": alg["step3_edge_projection"],
+        "k_s5m": (alg["step5_global_zsolve"][0], None) if modal else (None, None),
+        "k_zs3": (None, None) if modal else alg["step5_global_zsolve"],
+        "k_projm": (None, None) if modal else alg["step5_projection"],
+        "k_residual": alg["refine_residual"], "k_axpy": alg["refine_axpy"],
+    }
+    return out
+
+
+def kernel_roofline(p, nrhs, plan, kernels, steps, config, passes=1, fp64_peak=None):
+    """Per-kernel-kind roofline table: device ms per step (CUDA events around every launch of the
+    kind, inside the timed region), share of the summed kernel time, algorithmic work ÷ time
+    against the bound that governs it (FP64 tensor for the DMMA contractions, HBM otherwise), and
+    ncu DRAM bytes per launch ÷ algorithmic bytes where a capture exists."""
+    alg = kernel_algorithmic(p, nrhs, plan)
+    hbm_peak, hbm_src = _peaks()
+    fpk = fp64_peak or FP64_PEAK_TFLOPS
+    try:  # per kernel kind: ncu dram read + write bytes summed over one pass's launches
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
+            ncu = json.load(fh_).get(config, {}).get("kernels", {})
+    except Exception:
+        ncu = {}
+    tot = sum(v[0] for v in kernels.values()) or 1.0
+    table = {}
+    for name, (ms, nl) in kernels.items():
+        if not nl:
+            continue
+        mult = max(1, passes - 1) if name in ("k_residual", "k_axpy") else passes
+        per_step_ms = ms / max(1, steps)
+        flops, nbytes = alg.get(name, (None, None))
+        t_tensor = (flops or 0) / (fpk * 1e12)
+        t_hbm = (nbytes or 0) / (hbm_peak * 1e9)
+        ent = {"ms_per_step": per_step_ms, "share": ms / tot, "launches_per_step": nl / max(1, steps)}
+        if flops and t_tensor >= t_hbm:
+            a = flops * mult / (per_step_ms * 1e-3) / 1e12
+            ent.update(bound="tensor", achieved=a, peak=fpk, unit="TFLOP/s", frac=a / fpk, alg_flops=flops * mult)
+        elif nbytes:
+            a = nbytes * mult / (per_step_ms * 1e-3) / 1e9
+            ent.update(bound="hbm", achieved=a, peak=hbm_peak, unit="GB/s", frac=a / hbm_peak, alg_bytes=nbytes * mult)
+        tr = ncu.get(name)
+        if tr:
+            ent["ncu_dram_bytes_per_launch"] = tr["dram_bytes_per_pass"] / max(1, tr["launches_per_pass"])
+            if nbytes:  # dram traffic of one pass vs its algorithmic bytes (> 1: re-reads)
+                ent["ncu_traffic_ratio"] = tr["dram_bytes_per_pass"] / nbytes
+        table[name] = ent
+    return table
+
+
+def roofline_summary(p, nrhs, plan, stages, steps, config, ms_max, passes=1, kernels=None, fp64_peak=None):
     """Roofline of the dominant stage and of the whole solve.  Stage work is per
     solve pass over all nrhs right-hand sides; a step runs `passes` of them (1 + refinement
     passes, or the fast solves inside a GMRES solve)."""
@@ -296,6 +403,20 @@ def roofline_summary(p, nrhs, plan, stages, steps, config, ms_max, passes=1):
     roof["solve"] = {"t_roof_ms": t_roof, "frac": t_roof / ms_max, "alg_bytes": b_alg, "alg_flops": f_alg}
     roof["stage_ms_per_step"] = {k: v[0] / max(1, steps) for k, v in stages.items() if v[1]}
     roof["passes_per_step"] = passes
+    if kernels:
+        # the dominant KERNEL (largest device time per step over all its launches) is the one the
+        # top-level fields report; the stage view above stays for reference
+        table = kernel_roofline(p, nrhs, plan, kernels, steps, config, passes, fp64_peak)
+        roof["kernels"] = table
+        cand = {k: v for k, v in table.items() if "frac" in v}
+        if cand:
+            name, ent = max(cand.items(), key=lambda kv: kv[1]["ms_per_step"])
+            tr = ent.get("ncu_dram_bytes_per_launch")  # average over the kind's launches
+            roof.update(bound=ent["bound"], achieved=ent["achieved"], peak=ent["peak"], unit=ent["unit"],
+                        frac=ent["frac"], traffic=tr, kernel=name, share=ent["share"],
+                        peak_source=("in-run DMMA loop (lfds_fp64_peak)" if ent["bound"] == "tensor" and fp64_peak
+                                     else roof["peak_source"] if ent["bound"] == roof["bound"]
+                                     else f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"))
     return roof
 
 
@@ -389,6 +510,7 @@ def run_ours(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     plan.stage_times()  # reset
+    plan.kernel_times()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -403,6 +525,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     stages = plan.stage_times()
+    kernels = plan.kernel_times()
     launches_per_step = plan.report()["n_kernel_launches"]
     tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -469,7 +592,15 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": p.unknowns * ne * (1 if blocks else world) / (float(t.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": float(t.item()),
                "nrhs_per_gpu": ne}
-    roof = roofline_summary(p, nrhs, plan, stages, args.steps, args.config, ms_max, passes=1 + refine)
+    fp64_peak = None
+    try:  # in-run FP64 tensor peak (the DMMA kernels' denominator), after the timed region
+        from paper_1909_01299_b200.lfds import fp64_peak as _fp64_peak
+        fp64_peak = _fp64_peak()
+    except Exception:
+        pass
+    roof = roofline_summary(p, nrhs, plan, stages, args.steps, args.config, ms_max, passes=1 + refine,
+                            kernels=kernels, fp64_peak=fp64_peak)
+    roof["fp64_peak_tflops_in_run"] = fp64_peak
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         ps, ts, threads = cpu_oracle_sample(p, args.cpu_nz, 1)
@@ -531,6 +662,7 @@ def run_hetero(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     plan.stage_times()  # reset
+    plan.kernel_times()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -543,13 +675,15 @@ def run_hetero(args, rank, world, local_rank):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     stages = plan.stage_times()
+    kernels = plan.kernel_times()
     tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
     value = p.unknowns * world / (ms_max * 1e-3)  # replicas: every rank solves its own copy
     solves = stages.get("step2_zsolve", (0.0, args.steps))[1] / max(1, args.steps)  # one k_zs1 per solve
-    roof = roofline_summary(p, 1, plan, stages, args.steps, args.config, ms_max, passes=max(1.0, solves))
+    roof = roofline_summary(p, 1, plan, stages, args.steps, args.config, ms_max, passes=max(1.0, solves),
+                            kernels=kernels)
     e2e = None
     if not args.no_e2e:  # pinned host f -> device, solve, u -> host, every step
         fh = f.cpu().pin_memory()

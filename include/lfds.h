@@ -247,6 +247,22 @@ int lfds_stage_count(void);
 const char* lfds_stage_name(int stage);
 int lfds_stage_times(lfds_plan* plan, double* ms, int* launches);
 
+/*
+ * Kernel timing (options.profile = 1): the same CUDA-event accounting per kernel KIND
+ * (k_xform3m, k_zs1, ...; names from lfds_kernel_name), events recorded around every launch
+ * of that kind on the solve stream; accumulated since the previous call, which resets them.
+ */
+int lfds_kernel_count(void);
+const char* lfds_kernel_name(int kernel);
+int lfds_kernel_times(lfds_plan* plan, double* ms, int* launches);
+
+/*
+ * In-run FP64 peak of the current device (roofline denominator of the DMMA-bound kernels):
+ * a back-to-back mma.sync.m8n8k4.f64 (DMMA) loop on every SM, timed with CUDA events on
+ * `cuda_stream` (synchronises it).  *tflops = 2 x FMA / s.  Returns LFDS_ECUDA on failure.
+ */
+int lfds_fp64_peak(void* cuda_stream, double* tflops);
+
 void lfds_destroy(lfds_plan* plan);
 const char* lfds_last_error(void);
 const char* lfds_version(void);

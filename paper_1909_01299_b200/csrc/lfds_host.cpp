@@ -78,12 +78,20 @@ const char* kStageNames[ST_COUNT] = {
     "step7_x_sine", "step7_x_dense", "step7_write_iface", "refine_residual", "refine_axpy", "step1_plane_sine",
     "step7_plane_sine"};
 
+// kernel kinds (per-kernel device time: the roofline of the dominant kernel, bench.py)
+enum Kern { K_XFORM3M, K_XFORM, K_DSTW, K_DST, K_DST2, K_ZS1, K_ZS2, K_ZS3, K_PROJ, K_PROJM, K_S5M, K_IFRES,
+            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_COUNT };
+const char* kKernNames[K_COUNT] = {
+    "k_xform3m", "k_xform", "k_dstw", "k_dst", "k_dst2", "k_zs1", "k_zs2", "k_zs3", "k_proj_rows", "k_projm",
+    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm"};
+
 struct Profiler {
+  // stage < ST_COUNT: a stage record; stage = ST_COUNT + k: a record of kernel kind k
   struct Rec { int stage, launches; cudaEvent_t a, b; bool graph = false; };  // graph: events owned by a graph
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
-  double ms[ST_COUNT] = {0};
-  int launches[ST_COUNT] = {0};
+  double ms[ST_COUNT + K_COUNT] = {0};
+  int launches[ST_COUNT + K_COUNT] = {0};
   cudaEvent_t get() {
     if (pool.empty()) { cudaEvent_t e; cudaEventCreate(&e); return e; }
     cudaEvent_t e = pool.back(); pool.pop_back(); return e;
@@ -670,10 +678,24 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     }
     cur_stage = -1;
   };
+  // kernel-kind events (inside the stage events): device time per kernel kind, `n` launches
+  auto kern = [&](int k, int n, auto&& launch) -> cudaError_t {
+    cudaEvent_t a = nullptr;
+    if (prof) { a = P->prof.get(); prof_record(a, st); }
+    const cudaError_t e = launch();
+    P->launches += n;
+    if (prof) {
+      cudaEvent_t b = P->prof.get();
+      prof_record(b, st);
+      P->prof.recs.push_back({ST_COUNT + k, n, a, b});
+    }
+    return e;
+  };
+  auto nl = [](int ndesc) { return (ndesc + 65534) / 65535; };
   auto gemm = [&](const StageDescs& s) -> int {
     if (!s.n) return LFDS_OK;
-    CUDA_TRY(launch_gemm(pp.d_descs + s.off, s.n, s.maxM, (int)std::min<int64_t>(s.maxN, INT32_MAX), 0, bufs, st));
-    P->launches += (s.n + 65534) / 65535;
+    CUDA_TRY(kern(K_GEMM, nl(s.n), [&] {
+      return launch_gemm(pp.d_descs + s.off, s.n, s.maxM, (int)std::min<int64_t>(s.maxN, INT32_MAX), 0, bufs, st); }));
     return LFDS_OK;
   };
   // transform pass: sine-transform launches timed as stage st_s, dense ones as st_d
@@ -687,21 +709,18 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     }
     if (sd && !sd->empty()) {
       begin(st_s);
-      for (auto& kv : *sd) {
-        CUDA_TRY(launch_dst(pp.d_descs + kv.second.off, kv.second.n, kv.first, kv.second.maxN, kcontig, bufs, st));
-        P->launches += (kv.second.n + 65534) / 65535;
-      }
+      for (auto& kv : *sd)
+        CUDA_TRY(kern(kcontig ? K_DSTW : K_DST, nl(kv.second.n), [&] {
+          return launch_dst(pp.d_descs + kv.second.off, kv.second.n, kv.first, kv.second.maxN, kcontig, bufs, st); }));
       end();
     }
     begin(st_d);
-    if (sc.n) {
-      CUDA_TRY(launch_xform(pp.d_descs + sc.off, sc.n, sc.maxM, sc.maxN, false, kcontig, bufs, st));
-      P->launches += (sc.n + 65534) / 65535;
-    }
-    if (sr.n) {
-      CUDA_TRY(launch_xform(pp.d_descs + sr.off, sr.n, sr.maxM, sr.maxN, true, kcontig, bufs, st));
-      P->launches += (sr.n + 65534) / 65535;
-    }
+    if (sc.n)
+      CUDA_TRY(kern(K_XFORM3M, nl(sc.n), [&] {
+        return launch_xform(pp.d_descs + sc.off, sc.n, sc.maxM, sc.maxN, false, kcontig, bufs, st); }));
+    if (sr.n)
+      CUDA_TRY(kern(K_XFORM, nl(sr.n), [&] {
+        return launch_xform(pp.d_descs + sr.off, sr.n, sr.maxM, sr.maxN, true, kcontig, bufs, st); }));
     end();
     return LFDS_OK;
   };
@@ -709,10 +728,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   auto plane2 = [&](const std::vector<PassPlan::Dst2Group>& gs, int stg) -> int {
     if (gs.empty()) return LFDS_OK;
     begin(stg);
-    for (auto& g : gs) {
-      CUDA_TRY(launch_dst2(pp.d_dst2 + g.off, g.count, g.n, (int)((int64_t)R * Nz), bufs, st));
-      P->launches += (g.count + 65534) / 65535;
-    }
+    for (auto& g : gs)
+      CUDA_TRY(kern(K_DST2, nl(g.count), [&] {
+        return launch_dst2(pp.d_dst2 + g.off, g.count, g.n, (int)((int64_t)R * Nz), bufs, st); }));
     end();
     return LFDS_OK;
   };
@@ -726,24 +744,21 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s, ST_X1S, ST_X1D))) return rc;
   if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s, ST_Y1S, ST_Y1D))) return rc;
   begin(ST_Z1);
-  if (pp.nzb) {
-    CUDA_TRY(launch_zsolve(1, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv,
-                           st, P->real_z));
-    P->launches++;
-  }
+  if (pp.nzb)
+    CUDA_TRY(kern(K_ZS1, 1, [&] {
+      return launch_zsolve(1, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv,
+                           st, P->real_z); }));
   end();
   if (has_if) {
     begin(ST_EPROJ);
-    CUDA_TRY(launch_proj(pp.d_pd, pp.n_pd3, P->lpad, 2, R * Nz, st, bufs));
-    P->launches++;
+    CUDA_TRY(kern(K_PROJ, 1, [&] { return launch_proj(pp.d_pd, pp.n_pd3, P->lpad, 2, R * Nz, st, bufs); }));
     end(); begin(ST_EDGE);
     // node values next to the faces: VX = W_y G, VY = W_x H (DMMA, complex path)
     if (pp.use_xform) {
       for (const StageDescs* s3 : {&pp.s3x, &pp.s3y})
-        if (s3->n) {
-          CUDA_TRY(launch_xform(pp.d_descs + s3->off, s3->n, s3->maxM, s3->maxN, false, true, bufs, st));
-          P->launches += (s3->n + 65534) / 65535;
-        }
+        if (s3->n)
+          CUDA_TRY(kern(K_XFORM3M, nl(s3->n), [&] {
+            return launch_xform(pp.d_descs + s3->off, s3->n, s3->maxM, s3->maxN, false, true, bufs, st); }));
     } else {
       if ((rc = gemm(pp.s3x))) return rc;
       if ((rc = gemm(pp.s3y))) return rc;
@@ -758,8 +773,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     ir.blk_of_x = P->t_bx; ir.blk_of_y = P->t_by; ir.xlo = P->t_xlo; ir.ylo = P->t_ylo;
     ir.nbx = P->nbx; ir.nby = P->nby; ir.qpad = P->mpad; ir.ppad = P->lpad;
     ir.own = pp.d_own; ir.with_b = P->sharded ? P->rank0 : 1;
-    CUDA_TRY(launch_iface_residual(ir, bufs, st));
-    P->launches++;
+    CUDA_TRY(kern(K_IFRES, 1, [&] { return launch_iface_residual(ir, bufs, st); }));
     end();
   }
   }
@@ -768,8 +782,8 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     // projected onto the planes, back to z (Z) -> exchange 2 = [P1, P2]
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     begin(ST_GFWD);
-    CUDA_TRY(launch_xform(pp.d_descs + pp.s5zf.off, pp.s5zf.n, pp.s5zf.maxM, pp.s5zf.maxN, true, false, bufs, st));
-    P->launches += 1;
+    CUDA_TRY(kern(K_XFORM, 1, [&] {
+      return launch_xform(pp.d_descs + pp.s5zf.off, pp.s5zf.n, pp.s5zf.maxM, pp.s5zf.maxN, true, false, bufs, st); }));
     end(); begin(ST_GSWEEP);
     S5M S{};
     S.nx = Nx; S.ny = Ny; S.nz = Nz; S.R = R; S.nifx = nifx; S.nify = nify;
@@ -779,8 +793,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     S.mt_end = msplit ? (P->m_end + 63) / 64 : S.nmt;
     S.lamx = X.lamg; S.lamy = Y.lamg; S.theta = P->t_theta; S.wxi = X.WI; S.wyi = Y.WI;
     S.r1t = pp.r1t; S.r2t = pp.r2t; S.p1t = pp.p1t; S.p2p = pp.p2p; S.p2t = pp.p2t;
-    CUDA_TRY(launch_s5m(S, bufs, st));
-    P->launches += nify ? 2 : 1;
+    CUDA_TRY(kern(K_S5M, nify ? 2 : 1, [&] { return launch_s5m(S, bufs, st); }));
     end(); begin(ST_GPROJ);
     if (msplit && nifx)  // P1 rows of other y-modes: zero (exchange 2 sums the ranks' parts)
       CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.p1, 0,
@@ -788,10 +801,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     if (P->sharded && nify && (l_begin > 0 || l_end < Nx))  // P2 columns of other x-modes: zero
       CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.p2, 0,
                                sizeof(double2) * (size_t)nify * R * Nz * Nx, st));
-    if (pp.s5zi.n) {
-      CUDA_TRY(launch_xform(pp.d_descs + pp.s5zi.off, pp.s5zi.n, pp.s5zi.maxM, pp.s5zi.maxN, true, false, bufs, st));
-      P->launches += 1;
-    }
+    if (pp.s5zi.n)
+      CUDA_TRY(kern(K_XFORM, 1, [&] {
+        return launch_xform(pp.d_descs + pp.s5zi.off, pp.s5zi.n, pp.s5zi.maxM, pp.s5zi.maxN, true, false, bufs, st); }));
     end();
   } else if ((phases & PH_2) && has_if) {
     // step 5
@@ -801,9 +813,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     g.nx = Nx; g.ny = Ny; g.nifx = nifx; g.nify = nify; g.nz = Nz; g.R = R;
     g.lamx = X.lamg; g.lamy = Y.lamg; g.wxi = X.WI; g.wyi = Y.WI; g.r1 = pp.r1; g.r2 = pp.r2; g.what = 0;
     g.l_begin = l_begin; g.l_end = l_end;
-    CUDA_TRY(launch_zsolve(3, pp.d_zb + pp.nzb, 1, Nx, Ny, R, Nz, P->zt_plain, P->t_sig, &g, bufs, minpiv, st,
-                           P->real_z));
-    P->launches += 1;
+    CUDA_TRY(kern(K_ZS3, 1, [&] {
+      return launch_zsolve(3, pp.d_zb + pp.nzb, 1, Nx, Ny, R, Nz, P->zt_plain, P->t_sig, &g, bufs, minpiv, st,
+                           P->real_z); }));
     end(); begin(ST_GPROJ);
     {
       const int64_t RZ = (int64_t)R * Nz;
@@ -822,8 +834,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
       if (pm.nlc > 1) { pm.g_off = pp.gp; pm.g_lcs = (int64_t)nifx * RZ * Ny; }
       else { pm.g_off = pp.p1; pm.g_lcs = 0; }
       pm.h_off = pp.p2; pm.h_es = RZ * Nx; pm.h_ps = Nx;
-      CUDA_TRY(launch_projm(pm, bufs, st));
-      P->launches += pm.nlc > 1 ? 2 : 1;
+      CUDA_TRY(kern(K_PROJM, pm.nlc > 1 ? 2 : 1, [&] { return launch_projm(pm, bufs, st); }));
     }
     end();
   }
@@ -833,17 +844,16 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     begin(ST_FACE);
     // step 6: face transforms (DMMA, complex path)
     if (pp.use_xform && pp.s6f.n) {
-      CUDA_TRY(launch_xform(pp.d_descs + pp.s6f.off, pp.s6f.n, pp.s6f.maxM, pp.s6f.maxN, false, true, bufs, st));
-      P->launches += (pp.s6f.n + 65534) / 65535;
+      CUDA_TRY(kern(K_XFORM3M, nl(pp.s6f.n), [&] {
+        return launch_xform(pp.d_descs + pp.s6f.off, pp.s6f.n, pp.s6f.maxM, pp.s6f.maxN, false, true, bufs, st); }));
     } else if ((rc = gemm(pp.s6f))) {
       return rc;
     }
     end(); begin(ST_Z2);
-    if (pp.nzb) {
-      CUDA_TRY(launch_zsolve(2, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_lift, P->t_sig, nullptr, bufs, minpiv,
-                             st, P->real_z));
-      P->launches++;
-    }
+    if (pp.nzb)
+      CUDA_TRY(kern(K_ZS2, 1, [&] {
+        return launch_zsolve(2, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_lift, P->t_sig, nullptr, bufs, minpiv,
+                             st, P->real_z); }));
     end();
   }
   // step 7
@@ -852,9 +862,9 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s, ST_X7S, ST_X7D))) return rc;
   if (has_if) {  // (sharded: every rank writes its own segments of the planes, pp.d_wmask)
     begin(ST_WRITE);
-    CUDA_TRY(launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st,
-                                  pp.d_wmask, P->t_bx, P->t_by, P->nbx, P->nby, P->sharded ? P->rank0 : 1));
-    P->launches++;
+    CUDA_TRY(kern(K_WRITE, 1, [&] {
+      return launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st,
+                                  pp.d_wmask, P->t_bx, P->t_by, P->nbx, P->nby, P->sharded ? P->rank0 : 1); }));
     end();
   }
   }
@@ -908,6 +918,22 @@ int lfds_stage_times(lfds_plan* P, double* ms, int* launches) {
     if (launches) launches[i] = P->prof.launches[i];
     P->prof.ms[i] = 0;
     P->prof.launches[i] = 0;
+  }
+  return LFDS_OK;
+}
+
+int lfds_kernel_count(void) { return K_COUNT; }
+const char* lfds_kernel_name(int i) { return (i >= 0 && i < K_COUNT) ? kKernNames[i] : ""; }
+
+int lfds_kernel_times(lfds_plan* P, double* ms, int* launches) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  int rc;
+  if ((rc = prof_drain(P))) return rc;
+  for (int i = 0; i < K_COUNT; ++i) {
+    if (ms) ms[i] = P->prof.ms[ST_COUNT + i];
+    if (launches) launches[i] = P->prof.launches[ST_COUNT + i];
+    P->prof.ms[ST_COUNT + i] = 0;
+    P->prof.launches[ST_COUNT + i] = 0;
   }
   return LFDS_OK;
 }
@@ -1250,13 +1276,20 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         // stream); a fixed pass count stays asynchronous
         const bool auto_mode = P->opt.refine < 0;
         if (auto_mode) CUDA_TRY(cudaMemsetAsync(norms, 0, sizeof(double) * 2 * Rc, st));
-        cudaEvent_t ra = nullptr;
-        if (P->opt.profile) { ra = P->prof.get(); prof_record(ra, st); }
+        cudaEvent_t ra = nullptr, ra2 = nullptr, rb2k = nullptr;  // stage and kernel-kind events
+        if (P->opt.profile) { ra = P->prof.get(); prof_record(ra, st); ra2 = P->prof.get(); prof_record(ra2, st); }
         CUDA_TRY(launch_residual(X.N, Y.N, P->nz, Rc, dt, P->opt.residual_dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff,
                                  Y.hhoff, P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()),
                                  P->t_dd, b.p[B_U], b.p[B_F], res, 1, auto_mode ? norms : nullptr, b, st));
         P->launches++;
-        if (P->opt.profile) { cudaEvent_t rb2 = P->prof.get(); prof_record(rb2, st); P->prof.recs.push_back({ST_RESID, 1, ra, rb2}); }
+        if (P->opt.profile) {
+          rb2k = P->prof.get();
+          prof_record(rb2k, st);
+          cudaEvent_t rb2 = P->prof.get();
+          prof_record(rb2, st);
+          P->prof.recs.push_back({ST_RESID, 1, ra, rb2});
+          P->prof.recs.push_back({ST_COUNT + K_RESID, 1, ra2, rb2k});
+        }
         double worst = -1.0;
         if (auto_mode) {
           std::vector<double> hn(2 * Rc);
@@ -1273,11 +1306,18 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         rb.p[B_F] = res;
         rb.p[B_U] = res;
         if ((rc = run_pass(P, *pp_ref, rb, Rc, 0, 0, st))) return rc;
-        cudaEvent_t xa = nullptr;
-        if (P->opt.profile) { xa = P->prof.get(); prof_record(xa, st); }
+        cudaEvent_t xa = nullptr, xa2 = nullptr, xb2 = nullptr;
+        if (P->opt.profile) { xa = P->prof.get(); prof_record(xa, st); xa2 = P->prof.get(); prof_record(xa2, st); }
         CUDA_TRY(launch_axpy_u(vol * Rc, dt, res, b.p[B_U], st));
         P->launches++;
-        if (P->opt.profile) { cudaEvent_t xb = P->prof.get(); prof_record(xb, st); P->prof.recs.push_back({ST_AXPY, 1, xa, xb}); }
+        if (P->opt.profile) {
+          xb2 = P->prof.get();
+          prof_record(xb2, st);
+          cudaEvent_t xb = P->prof.get();
+          prof_record(xb, st);
+          P->prof.recs.push_back({ST_AXPY, 1, xa, xb});
+          P->prof.recs.push_back({ST_COUNT + K_AXPY, 1, xa2, xb2});
+        }
         passes++;
       }
     }

@@ -89,6 +89,11 @@ _lib.lfds_stage_count.restype = ctypes.c_int
 _lib.lfds_stage_name.argtypes = [ctypes.c_int]
 _lib.lfds_stage_name.restype = ctypes.c_char_p
 _lib.lfds_stage_times.argtypes = [_P, _P, _P]
+_lib.lfds_kernel_count.restype = ctypes.c_int
+_lib.lfds_kernel_name.argtypes = [ctypes.c_int]
+_lib.lfds_kernel_name.restype = ctypes.c_char_p
+_lib.lfds_kernel_times.argtypes = [_P, _P, _P]
+_lib.lfds_fp64_peak.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
 _lib.lfds_last_error.restype = ctypes.c_char_p
 _lib.lfds_version.restype = ctypes.c_char_p
 
@@ -97,7 +102,8 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version",
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
             "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
-            "lfds_set_mode_rows"]
+            "lfds_set_mode_rows", "lfds_kernel_count", "lfds_kernel_name", "lfds_kernel_times",
+            "lfds_fp64_peak"]
 
 
 def _check(rc):
@@ -188,6 +194,14 @@ class Plan:
         la = np.zeros(n, np.int32)
         _check(_lib.lfds_stage_times(self._h, ms.ctypes.data_as(_P), la.ctypes.data_as(_P)))
         return {_lib.lfds_stage_name(i).decode(): (float(ms[i]), int(la[i])) for i in range(n)}
+
+    def kernel_times(self) -> dict:
+        """{kernel kind: (device ms, launches)} accumulated since the last call (profile=True)."""
+        n = _lib.lfds_kernel_count()
+        ms = np.zeros(n, np.float64)
+        la = np.zeros(n, np.int32)
+        _check(_lib.lfds_kernel_times(self._h, ms.ctypes.data_as(_P), la.ctypes.data_as(_P)))
+        return {_lib.lfds_kernel_name(i).decode(): (float(ms[i]), int(la[i])) for i in range(n)}
 
     # ------------------------------------------------------------------ compute
     def _torch(self):
@@ -322,6 +336,15 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def fp64_peak(stream=None) -> float:
+    """In-run FP64 tensor-pipe (DMMA) peak of the current device in TFLOP/s (lfds_fp64_peak)."""
+    import torch
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    tf = ctypes.c_double()
+    _check(_lib.lfds_fp64_peak(_P(st), ctypes.byref(tf)))
+    return tf.value
 
 
 def setup_grid(hx, hy, hz, sigma_node, sigma_edge, lam, iface_x=(), iface_y=(), **kw) -> Plan:

@@ -69,3 +69,39 @@ def test_plane_sine_bytes_replace_the_two_passes():
         assert off[st][1] - on[st][1] == 32.0 * fused
     # dense passes are untouched
     assert on["step1_x_dense"] == off["step1_x_dense"]
+
+
+def test_kernel_roofline_names_the_kernel_with_the_largest_time():
+    """The top-level roofline reports the kernel KIND with the largest summed device time (all
+    its launches across stages), not the largest stage; its share and frac come from the table."""
+    p = make_problem("c4")
+    plan = _KindsPlan(len(p.iface_x) + 1, True)
+    stages = {"step6_zsolve_lift": (2.5, 1), "step1_x_dense": (2.0, 1), "step7_x_dense": (2.0, 1)}
+    kernels = {"k_zs2": (2.5, 1), "k_xform3m": (10.5, 20), "k_zs1": (2.3, 1)}
+    r = bench.roofline_summary(p, 1, plan, stages, 1, "c4", 25.0, passes=1, kernels=kernels, fp64_peak=37.0)
+    assert r["kernel"] == "k_xform3m" and r["bound"] == "tensor" and r["unit"] == "TFLOP/s"
+    alg = bench.kernel_algorithmic(p, 1, plan)
+    assert abs(r["achieved"] - alg["k_xform3m"][0] / 10.5e-3 / 1e12) < 1e-9 * r["achieved"]
+    assert abs(r["share"] - 10.5 / 15.3) < 1e-12
+    assert r["kernels"]["k_zs2"]["bound"] == "hbm"
+
+
+def test_kernel_algorithmic_dense_flops_c4():
+    """C4 with its PML blocks first and last on each axis (kind 2) and uniform (sine) blocks in
+    between: the complex dense passes are exactly the blocks whose x or y block is a PML block,
+    8 n flops per element and direction, forward and inverse."""
+    p = make_problem("c4")
+    nb = len(p.iface_x) + 1
+    alg = bench.kernel_algorithmic(p, 1, _KindsPlan(nb, True))
+    cuts = [0] + list(p.iface_x) + [p.nx + 1]
+    n = [cuts[i + 1] - cuts[i] - 1 for i in range(nb)]
+    pml = {0, nb - 1}
+    dense = sum(2 * 8.0 * n[i] * n[i] * n[j] * p.nz + 2 * 8.0 * n[j] * n[i] * n[j] * p.nz * 0
+                for i in pml for j in range(nb))  # x passes of blocks in a PML column
+    dense += sum(2 * 8.0 * n[j] * n[i] * n[j] * p.nz for i in range(nb) for j in pml)  # y passes
+    nif = len(p.iface_x)
+    plane = 2 * 8.0 * 2 * nif * p.nx * p.nx * p.nz
+    edges = sum(8.0 * (n[i] ** 2 + n[j] ** 2) * 2 * p.nz for i in range(nb) for j in range(nb))
+    faces = sum(8.0 * (((i > 0) + (i < nb - 1)) * n[j] ** 2 + ((j > 0) + (j < nb - 1)) * n[i] ** 2) * p.nz
+                for i in range(nb) for j in range(nb))
+    assert abs(alg["k_xform3m"][0] - (dense + plane + edges + faces)) < 1e-9 * alg["k_xform3m"][0]
