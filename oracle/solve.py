@@ -16,7 +16,9 @@ literal stencil (reading R13): u <- u + S(b - A u) until ||r||/||b|| stops decre
 
 ``block_solutions`` gives the pass-1 quantity v of PAPER.md:43-44 by definition
 (sparse LU of each block's restricted matrix, v = 0 on the interfaces), used to pin
-the interface-support invariant and the CUDA path's intermediate steps.
+the interface-support invariant and, through r_b = b - A v on the planes,
+the CUDA path's steps 1-4 (tests/test_gpu_parity.py::
+test_pass1_interface_residual_matches_oracle_block_solutions).
 
 Pins: tests/test_oracle_solve.py ((i) == (ii) on shrunken analogs of every config,
 random manufactured discrete solutions, exact discrete eigenfunction, reciprocity,

@@ -598,8 +598,12 @@ __global__ void __launch_bounds__(Dst2Cfg<R1, R2>::WARPS * 32) k_dst2(const Dst2
         Cg[(int64_t)m * D.sCr + r0 + c] = Tsm[m * LDT + c];
       }
     }
-    // every CTA has read its Tsm before the next x phase writes into it
-    if constexpr (C::CL == 1) __syncthreads(); else cluster_sync_relaxed();
+    // every CTA has read its Tsm before the next x phase writes into it; with rows_out the CTA
+    // also WROTE its Tsm above, and the peer's next remote stores must be ordered after those
+    // local writes: a release/acquire cluster barrier (a relaxed arrive only orders the reads)
+    if constexpr (C::CL == 1) __syncthreads();
+    else if (rows_out) cluster.sync();
+    else cluster_sync_relaxed();
   }
 }
 

@@ -1,16 +1,23 @@
 // Host orchestration and C ABI (include/lfds.h) of the blocked separable solve
 // (arXiv 1909.01299).  Setup builds every table once (timed separately);
-// lfds_solve enqueues the seven steps as stream-ordered kernels:
+// lfds_solve enqueues the seven steps as stream-ordered kernels (kernel kinds as reported by
+// lfds_kernel_times):
 //
-//   pass 1 (per block S^ij)   step 1  f~ = (F_x (x) F_y (x) I) f,  F = W^T M      (k_gemm x2)
-//                             step 2  T_lm v~_lm = f~_lm (z-solves)               (k_zs<1>)
-//                             step 3  v at the rows next to every block face      (k_gemm x4)
-//   interface                 step 4  r_b = b - A v on the interface planes       (k_iface_res)
-//                             step 5  w on the planes via the global bases        (k_xform, k_zs<3>, k_xform_m8)
-//   pass 2 (per block)        step 6  w~ from the Dirichlet lifting of w          (k_gemm, k_zs<2>)
-//                             step 7  u = (W_x (x) W_y (x) I)(v~ + w~), u = w on planes (k_gemm x2, k_write_iface)
+//   pass 1 (per block S^ij)   step 1  f~ = (F_x (x) F_y (x) I) f,  F = W^T M
+//                                     k_dst2 (uniform x uniform blocks, both axes), k_dstw / k_dst
+//                                     (sine x / y passes), k_xform3m / k_xform (dense, complex / real W)
+//                             step 2  T_lm v~_lm = f~_lm (z-solves)               k_zs1
+//                             step 3  v at the rows next to every block face      k_proj_rows + k_xform3m
+//   interface                 step 4  r_b = b - A v on the interface planes       k_iface_res
+//                             step 5  w on the planes via the global bases        k_xform3m (plane transforms),
+//                                     k_xform (z-modes), k_s5m (modal solve + projections); complex z
+//                                     tables: k_zs3 + k_projm
+//   pass 2 (per block)        step 6  w~ from the Dirichlet lifting of w          k_xform3m (faces), k_zs2
+//                             step 7  u = (W_x (x) W_y (x) I)(v~ + w~), u = w on the planes
+//                                     (the step-1 kernels, inverse), k_write_iface
 //
-// optional refinement: r = M f - A u in double-double (k_residual), u += solve(r).
+// optional refinement: r = M f - A u (k_residual, fp64 or double-double), u += solve(r) (k_axpy).
+// k_gemm (plain FP64 tiles) runs only the f64 (real, C1) plans' transforms.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -287,10 +294,12 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   }
   const int64_t if_elems = o;
   size_t off = 0;
+  // RED (pivot monitor, residual norms) first: the same offset in every pass plan of one R, so
+  // the real main pass and the complex refinement pass of an f64 plan share it
+  pp.off_red = off; off = al256(off + (size_t)(2 * R + 8) * 8);
   pp.off_ms = off; off = al256(off + ms_elems * 16);
   pp.off_t1 = off; off = al256(off + t1_elems * 16);
   pp.off_if = off; off = al256(off + if_elems * 16);
-  pp.off_red = off; off = al256(off + (size_t)(2 * R + 8) * 8);
   pp.off_ck = off;
   off = al256(off + std::max(zsolve_checkpoint_bytes(nblk, P->lpad, P->mpad, R, Nz), zsolve_checkpoint_bytes(1, Nx, Ny, R, Nz)));
   pp.off_res = off;
@@ -893,6 +902,19 @@ int lfds_stage_count(void) { return ST_COUNT; }
 const char* lfds_stage_name(int i) { return (i >= 0 && i < ST_COUNT) ? kStageNames[i] : ""; }
 
 // accumulate the pending stage records (waits for their events)
+static int prof_drain(lfds_plan* P);
+// the captured graph replays launches that read the pass plans' device descriptors and the
+// workspace layout they were built for: drop it whenever the pass plans are freed
+static void drop_graph(lfds_plan* P) {
+  if (!P->gexec) return;
+  prof_drain(P);  // pending replay records refer to the graph's events
+  cudaGraphExecDestroy(P->gexec);
+  P->gexec = nullptr;
+  for (auto& r : P->grecs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  P->grecs.clear();
+  P->gkey_f = nullptr; P->gkey_u = nullptr; P->gkey_ws = nullptr; P->gkey_wsb = 0; P->gkey_nrhs = 0;
+}
+
 static int prof_drain(lfds_plan* P) {
   for (auto& r : P->prof.recs) {
     CUDA_TRY(cudaEventSynchronize(r.b));
@@ -1219,7 +1241,14 @@ size_t lfds_workspace_bytes(const lfds_plan* cp, int nrhs) {
   int in_real = P->opt.dtype == LFDS_F64;
   PassPlan* pp;
   if (get_pass(P, R, in_real, in_real, &pp)) return 0;
-  return pp->total;
+  size_t total = pp->total;
+  // refinement passes run the complex pass plan (its own layout in the same workspace; for a
+  // complex plan it is the main one); a last chunk smaller than R has a smaller layout
+  if (P->opt.refine != 0) {
+    if (get_pass(P, R, 0, 0, &pp)) return 0;
+    total = std::max(total, pp->total);
+  }
+  return total;
 }
 
 size_t lfds_workspace_bytes_host(const lfds_plan* P, int nrhs) {
@@ -1231,6 +1260,8 @@ size_t lfds_workspace_bytes_host(const lfds_plan* P, int nrhs) {
 }
 
 static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes, cudaStream_t st) {
+  // a partitioned plan computes only its own blocks: whole solves must go through the phases
+  if (P->sharded) return fail(LFDS_EINVAL, "partitioned plan: use lfds_solve_phase with the two exchanges");
   const int R = chunk_of(P, nrhs);
   const int dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
   const size_t el = dt ? 8 : 16;
@@ -1246,7 +1277,8 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
     int rc;
     if ((rc = get_pass(P, Rc, dt, dt, &pp_main))) return rc;
     if (P->opt.refine != 0 && (rc = get_pass(P, Rc, 0, 0, &pp_ref))) return rc;
-    if (ws_bytes < pp_main->total) return fail(LFDS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, pp_main->total);
+    const size_t need = std::max(pp_main->total, pp_ref ? pp_ref->total : size_t(0));
+    if (ws_bytes < need) return fail(LFDS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
     char* w = reinterpret_cast<char*>(ws);
     Bufs b{};
     b.p[B_TAB] = P->d_tab;
@@ -1262,7 +1294,9 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
     if ((rc = run_pass(P, *pp_main, b, Rc, dt, dt, st))) return rc;
     int passes = 1;
     if (P->opt.refine != 0) {
-      double2* res = reinterpret_cast<double2*>(w + pp_main->off_res);
+      // the refinement pass runs pp_ref on pp_ref's own layout of the workspace (an f64 plan's
+      // real main pass has another); the residual lives past all of pp_ref's buffers
+      double2* res = reinterpret_cast<double2*>(w + pp_ref->off_res);
       double* norms = red + 8;
       const Axis& X = P->ax[0];
       const Axis& Y = P->ax[1];
@@ -1305,6 +1339,11 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         Bufs rb = b;
         rb.p[B_F] = res;
         rb.p[B_U] = res;
+        rb.p[B_MS] = w + pp_ref->off_ms;
+        rb.p[B_T1] = w + pp_ref->off_t1;
+        rb.p[B_IF] = w + pp_ref->off_if;
+        rb.p[B_RED] = w + pp_ref->off_red;  // == pp_main->off_red (RED first in every layout)
+        rb.p[B_CK] = w + pp_ref->off_ck;
         if ((rc = run_pass(P, *pp_ref, rb, Rc, 0, 0, st))) return rc;
         cudaEvent_t xa = nullptr, xa2 = nullptr, xb2 = nullptr;
         if (P->opt.profile) { xa = P->prof.get(); prof_record(xa, st); xa2 = P->prof.get(); prof_record(xa2, st); }
@@ -1534,6 +1573,7 @@ int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_
     P->m_begin = 0;
     P->m_end = -1;
   }
+  drop_graph(P);
   for (auto& kv : P->passes) {  // descriptors depend on the owned blocks: rebuild lazily
     free_pass(kv.second);
   }
@@ -1550,6 +1590,7 @@ int lfds_set_mode_rows(lfds_plan* P, int m_begin, int m_end) {
     return fail(LFDS_EINVAL, "bad y-mode range [%d, %d) of %d (multiples of 64)", m_begin, m_end, Ny);
   P->m_begin = m_begin;
   P->m_end = m_end;
+  drop_graph(P);
   for (auto& kv : P->passes) {  // descriptors depend on the range: rebuild lazily
     free_pass(kv.second);
   }
@@ -1621,16 +1662,9 @@ int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws,
   const bool hit = P->gexec && P->gkey_f == f_dev && P->gkey_u == u_dev && P->gkey_ws == ws &&
                    P->gkey_wsb == ws_bytes && P->gkey_nrhs == nrhs;
   if (!hit) {
-    if (P->gexec) {
-      // pending stage records of earlier replays refer to the old graph's events: take their
-      // times now, before those events are destroyed
-      int rc;
-      if ((rc = prof_drain(P))) return rc;
-      cudaGraphExecDestroy(P->gexec);
-      P->gexec = nullptr;
-      for (auto& r : P->grecs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
-      P->grecs.clear();
-    }
+    // pending stage records of earlier replays refer to the old graph's events: drop_graph
+    // takes their times before those events are destroyed
+    drop_graph(P);
     // pass plans allocate device descriptors on first use: build them before capturing
     const int R = chunk_of(P, nrhs), dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
     for (int r0 = 0; r0 < nrhs; r0 += R) {

@@ -1,8 +1,8 @@
 // sm_100a kernels of the blocked separable Helmholtz solve (arXiv 1909.01299).
 //
-//  k_gemm          strided batched complex contraction: block forward/inverse transforms
-//                  (steps 1 and 7), interface-adjacent evaluation (step 3), sparse global
-//                  transforms (step 5), face transforms for the Dirichlet lifting (step 6).
+//  k_gemm          strided batched complex contraction on FP64 ALUs: every transform of the
+//                  f64 (real, LFDS_F64) plans; complex plans run their transforms on the tensor
+//                  pipe (lfds_xform.cu) and the sine kernels (lfds_dst.cu).
 //  (z-solves of steps 2, 5 and 6: lfds_zsolve.cu)
 //  k_iface_res     step 4: residual b - A v on the interface planes.
 //  k_write_iface   u = w on the interface planes (last sentence).

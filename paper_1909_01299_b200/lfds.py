@@ -137,6 +137,7 @@ class Plan:
         opt.graph = int(bool(graph))
         opt.plane_dst = int(bool(plane_dst))
         self.plane_dst = bool(plane_dst)
+        self.device = int(device)
         self.dtype = opt.dtype
         hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
         sn_, psn = _zarr(sigma_node); se_, pse = _zarr(sigma_edge)
@@ -217,9 +218,23 @@ class Plan:
             raise LfdsError(5, _lib.lfds_last_error().decode() or "workspace query failed")
         ws = self._ws.get(key)
         if ws is None or ws.numel() < nb:
-            ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            ws = torch.empty(nb, dtype=torch.uint8, device=torch.device("cuda", max(self.device, 0)))
             self._ws[key] = ws
         return ws
+
+    def _check_out(self, out, like, single, host=False):
+        """The library writes nrhs*nz*ny*nx elements through out's raw pointer: same shape and
+        dtype as f, contiguous, and on f's device (pinned CPU memory for host solves)."""
+        if out is None:
+            return
+        O = out.unsqueeze(0) if single else out
+        if tuple(O.shape) != tuple(like.shape) or O.dtype != like.dtype or not O.is_contiguous():
+            raise ValueError(f"out must be a contiguous {like.dtype} tensor of shape {tuple(like.shape)}")
+        if host:
+            if O.is_cuda:
+                raise ValueError("out must be a CPU tensor for solve_host")
+        elif O.device != like.device:
+            raise ValueError(f"out is on {O.device}, f on {like.device}")
 
     def _fdtype(self):
         torch = self._torch()
@@ -235,6 +250,7 @@ class Plan:
         if tuple(F.shape[1:]) != self.shape:
             raise ValueError(f"f shape {tuple(F.shape)} does not match grid {self.shape}")
         nrhs = F.shape[0]
+        self._check_out(out, F, single)
         U = torch.empty_like(F) if out is None else (out.unsqueeze(0) if single else out)
         ws = self.workspace(nrhs)
         st = (stream or torch.cuda.current_stream()).cuda_stream
@@ -251,6 +267,7 @@ class Plan:
         for name, t in (("f", f), ("dlam", dlam)):
             if not (t.is_cuda and t.is_contiguous() and t.dtype == torch.complex128 and tuple(t.shape) == self.shape):
                 raise ValueError(f"{name} must be a contiguous CUDA complex128 tensor of shape {self.shape}")
+        self._check_out(out, f, False)
         U = torch.empty_like(f) if out is None else out
         nb = int(_lib.lfds_gmres_workspace_bytes(self._h, int(restart)))
         if nb == 0:
@@ -275,6 +292,7 @@ class Plan:
         if F.is_cuda or not F.is_contiguous() or F.dtype != self._fdtype():
             raise ValueError("f_host must be a contiguous CPU tensor of the plan dtype")
         nrhs = F.shape[0]
+        self._check_out(out, F, single, host=True)
         U = torch.empty_like(F, pin_memory=F.is_pinned()) if out is None else (out.unsqueeze(0) if single else out)
         ws = self.workspace(nrhs, host=True, slot=slot)
         st = (stream or torch.cuda.current_stream()).cuda_stream

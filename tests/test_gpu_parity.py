@@ -31,6 +31,38 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
+def parity_norms(p, U, ref):
+    """(2-norm relative error, worst per-block max-norm error, worst per-interface-plane max-norm
+    error), the max-norm errors relative to each block's / plane's own max |u_ref| (PAPER.md:52:
+    the interface step lives on the union of the block boundaries, so a localized error in one
+    block or one plane segment must show up here even when the 2-norm hides it)."""
+    U = np.asarray(U).reshape(p.shape)
+    ref = np.asarray(ref).reshape(p.shape)
+    err = np.abs(U - ref)
+    blk = 0.0
+    for (x0, x1) in oracle.block_ranges(p.nx, p.iface_x):
+        for (y0, y1) in oracle.block_ranges(p.ny, p.iface_y):
+            sl = (slice(None), slice(y0 - 1, y1), slice(x0 - 1, x1))
+            blk = max(blk, float(err[sl].max() / np.abs(ref[sl]).max()))
+    pl = 0.0
+    for a in p.iface_x:
+        pl = max(pl, float(err[:, :, a - 1].max() / np.abs(ref[:, :, a - 1]).max()))
+    for b in p.iface_y:
+        pl = max(pl, float(err[:, b - 1, :].max() / np.abs(ref[:, b - 1, :]).max()))
+    return rel(U, ref), blk, pl
+
+
+def assert_parity(p, U, ref, tol=TOL, local_tol=None):
+    """North_star's 2-norm bar plus the per-block and per-plane max-norm bars (local_tol,
+    default 10 x tol: a block far from the sources holds values orders below the global max,
+    so the same absolute rounding is a larger fraction of its own max)."""
+    e2, eb, ep = parity_norms(p, U, ref)
+    lt = 10 * tol if local_tol is None else local_tol
+    print(f"{p.name}: rel2 {e2:.2e}  block max-norm {eb:.2e}  plane max-norm {ep:.2e}")
+    assert e2 < tol, (p.name, e2)
+    assert eb < lt and ep < lt, (p.name, e2, eb, ep)
+
+
 def gpu_solve(p, F, **kw):
     Plan = _lib()
     plan = Plan.from_problem(p, **kw)
@@ -49,7 +81,7 @@ def test_shrunken_configs_single_pass(name):
     plan, U = gpu_solve(p, F)
     for r in range(p.nrhs):
         ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[r]))
-        assert rel(U[r], ref) < TOL, (name, r, rel(U[r], ref))
+        assert_parity(p, U[r], ref)
         assert oracle.rel_residual(p, U[r], F[r], np.clongdouble) < 1e-10
 
 
@@ -62,8 +94,95 @@ def test_shrunken_refined(name):
     assert rep["passes"] >= 1
     for r in range(p.nrhs):
         ref = oracle.solve(p, F[r])
-        assert rel(U[r], ref) < 1e-12
+        assert_parity(p, U[r], ref, tol=1e-12)
         assert oracle.rel_residual(p, U[r], F[r], np.clongdouble) < 1e-14
+
+
+@pytest.mark.parametrize("refine", [-1, 2])
+def test_f64_plan_refined(refine):
+    """C1 (an LFDS_F64 plan: real main pass) with refinement, whose passes run the complex pass
+    plan on its own workspace layout: the refined solution matches the oracle to 1e-13."""
+    p = make_problem("c1")
+    F = p.rhs_all()
+    plan, U = gpu_solve(p, F, refine=refine, refine_tol=1e-18)  # (auto: until the residual stagnates)
+    assert plan.report()["passes"] >= 2
+    ref = oracle.solve(p, F[0])
+    assert_parity(p, U[0], ref, tol=1e-13)
+
+
+def test_pass1_interface_residual_matches_oracle_block_solutions():
+    """Steps 1-4 pinned on their own: the interface residual r_b = b - A v on the planes after
+    pass 1 (exchange 1 of lfds_solve_phase, RX then RY with RY = 0 at the intersections) against
+    the oracle's v by definition (sparse LU of every block, v = 0 on the interfaces, PAPER.md:43-44,
+    :52)."""
+    from paper_1909_01299_b200 import Plan
+    for name in ("c2", "c3", "c4", "c5"):
+        p = shrunken(name, nrhs=1)
+        F = p.rhs_all()
+        plan = Plan.from_problem(p)
+        nbx, nby = len(p.iface_x) + 1, len(p.iface_y) + 1
+        plan.set_partition(np.ones((nby, nbx), np.int32), 0, p.nx, True)
+        ws = plan.workspace(1)
+        f = torch.from_numpy(F).cuda()
+        u = torch.zeros_like(f)
+        plan.solve_phase(1, f, u, ws)
+        torch.cuda.synchronize()
+        X = plan.exchange_view(ws, 1, 1).cpu().numpy().view(np.complex128)
+        b = oracle.mass_rhs(p, F[0])
+        v = oracle.block_solutions(p, b)
+        r = b - oracle.apply_stencil(p, v)
+        nifx = len(p.iface_x)
+        nrx = nifx * p.nz * p.ny
+        RX = X[:nrx].reshape(nifx, p.nz, p.ny)
+        ry0 = (nrx + 3) // 4 * 4  # align4 between the arrays (lfds_host.cpp build_pass)
+        RY = X[ry0:ry0 + len(p.iface_y) * p.nz * p.nx].reshape(len(p.iface_y), p.nz, p.nx)
+        rx_ref = np.stack([r[:, :, a - 1] for a in p.iface_x])
+        ry_ref = np.stack([r[:, bb - 1, :] for bb in p.iface_y])
+        ry_ref[:, :, [a - 1 for a in p.iface_x]] = 0  # intersections counted once (in RX)
+        scale = np.abs(r).max()
+        assert np.abs(RX - rx_ref).max() < 1e-12 * scale, (name, np.abs(RX - rx_ref).max() / scale)
+        assert np.abs(RY - ry_ref).max() < 1e-12 * scale, (name, np.abs(RY - ry_ref).max() / scale)
+        plan.close()
+
+
+def test_partition_then_graph_replay_uses_rebuilt_descriptors():
+    """A graph-capturing plan that solved, was partitioned and un-partitioned again must not
+    replay the old graph (its descriptors were freed): the next solve equals the reference."""
+    from paper_1909_01299_b200 import Plan
+    p = shrunken("c4", nrhs=1)
+    F = torch.from_numpy(p.rhs_all()).cuda()
+    ref = Plan.from_problem(p).solve(F)
+    pl = Plan.from_problem(p, graph=True)
+    U = torch.empty_like(F)
+    pl.solve(F, out=U)
+    nbx, nby = len(p.iface_x) + 1, len(p.iface_y) + 1
+    own = np.zeros((nby, nbx), np.int32)
+    own[0, 0] = 1
+    pl.set_partition(own, 0, 32, True)
+    pl.set_partition(None)
+    U.zero_()
+    pl.solve(F, out=U)
+    torch.cuda.synchronize()
+    assert torch.equal(U, ref)
+
+
+def test_partitioned_plan_rejects_whole_solves_and_bad_out():
+    from paper_1909_01299_b200 import LfdsError, Plan
+    p = shrunken("c2", nrhs=1)
+    F = torch.from_numpy(p.rhs_all()).cuda()
+    pl = Plan.from_problem(p)
+    with pytest.raises(ValueError):
+        pl.solve(F, out=torch.empty((1, 2, 3), dtype=F.dtype, device="cuda"))
+    with pytest.raises(ValueError):
+        pl.solve(F, out=torch.empty_like(F, dtype=torch.complex64))
+    with pytest.raises(ValueError):
+        pl.solve_host(F.cpu(), out=torch.empty(F.shape, dtype=F.dtype, device="cuda"))
+    nbx, nby = len(p.iface_x) + 1, len(p.iface_y) + 1
+    pl.set_partition(np.ones((nby, nbx), np.int32), 0, p.nx, True)
+    with pytest.raises(LfdsError):
+        pl.solve_host(F.cpu().pin_memory())
+    with pytest.raises(LfdsError):
+        pl.solve(F)
 
 
 def test_single_block_is_global_separable_solve():
@@ -71,7 +190,7 @@ def test_single_block_is_global_separable_solve():
     F = p.rhs_all()
     _, U = gpu_solve(p, F)
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(U[0], ref) < TOL
+    assert_parity(p, U[0], ref)
 
 
 def test_partition_independence_and_one_axis_split():
@@ -138,7 +257,7 @@ def test_edge_sizes(nz):
     F = (rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape))
     _, U = gpu_solve(p, F)
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(U[0], ref) < TOL
+    assert_parity(p, U[0], ref)
 
 
 def _steps_problem(hx, hy, nz, ix, iy, lam=0.3, seed=0, layers=(0.5, 2.0, 1.0)):
@@ -160,7 +279,7 @@ def test_uniform_blocks_with_pml_blocks():
     kinds = [plan.basis(0, b)[2] for b in range(4)]
     assert kinds == [2, 0, 0, 2], kinds
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(U[0], ref) < TOL
+    assert_parity(p, U[0], ref)
 
 
 @pytest.mark.parametrize("n", [7, 31, 63, 127, 255, 23, 39, 47, 79, 95, 159])
@@ -176,7 +295,7 @@ def test_sine_transform_lengths(n):
     F = rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape)
     _, U = gpu_solve(p, F)
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(U[0], ref) < TOL
+    assert_parity(p, U[0], ref)
     pt = _steps_problem(hy, hx, 3, [4], [n + 1])
     Ft = np.ascontiguousarray(np.swapaxes(F, 2, 3))
     _, Ut = gpu_solve(pt, Ft)
@@ -201,7 +320,7 @@ def test_plane_sine_lengths(n):
     st = plan.stage_times()
     assert st["step1_plane_sine"][1] >= 1 and st["step7_plane_sine"][1] >= 1, st
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(U[0], ref) < TOL, rel(U[0], ref)
+    assert_parity(p, U[0], ref)
     _, U1 = gpu_solve(p, F, plane_dst=False)           # the x pass + y pass form, same operator
     assert rel(U1[0], ref) < TOL
     assert rel(U[0], U1[0]) < 1e-12
@@ -255,22 +374,28 @@ def test_full_size_configs_vs_oracle(name):
     F = p.rhs_all()
     plan, U = gpu_solve(p, F, refine=(-1 if name == "c2" else 0))
     ref = oracle.solve(p, F[0])
-    assert rel(U[0], ref) < TOL, rel(U[0], ref)
+    assert_parity(p, U[0], ref)
 
 
 @pytest.mark.slow
 def test_full_size_c4_vs_oracle():
     """C4 at its full BASELINE.json size (1024 x 1024 x 256, 8 x 8 blocks), the launch bench.py
     times (one right-hand side, no refinement): element by element against oracle (ii)'s global
-    separable solve, plus the double-double residual bar of north_star."""
+    separable solve (2-norm, per-block and per-plane max norms), plus the double-double residual
+    bar of north_star; the same for the C4j and C4q partitions of the same problem."""
     p = make_problem("c4")
     F = p.rhs_all()
-    plan, U = gpu_solve(p, F)
-    ut = torch.from_numpy(U).cuda()
-    _, norms = plan.residual(ut, torch.from_numpy(F).cuda(), dd=True)
-    assert norms[0, 0] / norms[0, 1] < 1e-10
     ref = oracle.solve_separable(p, oracle.mass_rhs(p, F[0]))
-    assert rel(U[0], ref) < TOL, rel(U[0], ref)
+    # the default 8 x 8 partition and the two partition variants (NEXT #1: the paper's three
+    # subgrids, and 32 x 32 blocks) of the same grid and right-hand side: one oracle solution
+    for pv in (p, make_problem("c4j"), make_problem("c4q")):
+        plan, U = gpu_solve(pv, F)
+        ut = torch.from_numpy(U).cuda()
+        _, norms = plan.residual(ut, torch.from_numpy(F).cuda(), dd=True)
+        assert norms[0, 0] / norms[0, 1] < 1e-10
+        assert_parity(pv, U[0], ref)
+        plan.close()
+        del U, ut
 
 
 @pytest.mark.slow
@@ -291,7 +416,7 @@ def test_full_size_c5_chunked_vs_oracle():
     _, U0 = gpu_solve(p, F[1:2])                     # single pass, as timed without refinement
     ref = oracle.solve(p, F[1])                      # oracle (ii) + 80-bit refinement
     print("c5 single-pass error", rel(U0[0], ref), "refined", rel(U[1], ref))
-    assert rel(U[1], ref) < TOL, rel(U[1], ref)
+    assert_parity(p, U[1], ref)
 
 
 @pytest.mark.parametrize("name,world", [("c2", 2), ("c5", 3), ("c4", 4)])
@@ -333,7 +458,7 @@ def test_block_sharded_solve_matches_single_device(name, world):
     torch.cuda.synchronize()
     assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) < 1e-12
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(u.cpu().numpy()[0], ref) < TOL
+    assert_parity(p, u.cpu().numpy()[0], ref)
     # every block is computed by exactly one rank
     owners = dist.shard(Plan.from_problem(p), 0, world)["owner"]
     assert set(np.unique(owners)) <= set(range(world))
@@ -350,7 +475,7 @@ def test_step5_modal_matches_sweeps(name):
     assert pm.info()["s5_modal"] == 1 and ps.info()["s5_modal"] == 0
     assert rel(Um, Us) < 1e-11, rel(Um, Us)
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(Um[0], ref) < TOL
+    assert_parity(p, Um[0], ref)
 
 
 @pytest.mark.parametrize("nifx,nify", [(12, 9), (16, 3), (0, 11), (3, 16), (31, 20), (17, 32)])
@@ -368,7 +493,7 @@ def test_step5_modal_interface_counts(nifx, nify):
     plan, U = gpu_solve(p, F)
     assert plan.info()["s5_modal"] == 1
     ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[0]))
-    assert rel(U[0], ref) < TOL, rel(U[0], ref)
+    assert_parity(p, U[0], ref)
 
 
 @pytest.mark.parametrize("name,refine", [("c2", 1), ("c3", 0), ("c4", 0)])
@@ -436,3 +561,6 @@ def test_block_sharded_2d_mode_split_matches_single_device(world):
     # the (m, l) partial sums change the rounding order of the step-5 projections: agreement
     # to rounding amplified by the conditioning (measured 1.5e-12), far inside the 1e-9 bar
     assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) < 1e-10
+    # and against the oracle's global separable solve (not only the unsharded GPU solve)
+    ref = oracle.solve_separable(p, oracle.mass_rhs(p, F[0]))
+    assert_parity(p, u.cpu().numpy()[0], ref)
