@@ -69,10 +69,15 @@ typedef struct {
                     /* transform (both axes, one pass over the block; longer blocks keep   */
                     /* the two passes); 0: always an x pass and a y pass;   */
                     /* lfds_info.n_plane_dst counts the blocks it applies to               */
+  double resonance_tol; /* setup fails with LFDS_ERESONANCE when a block or the global family  */
+                    /* of z-systems T_lm = A' + (lambda_l + mu_m) E has a relative margin   */
+                    /* min|lambda_l + mu_m + theta_t| / (max|lambda_l| + max|mu_m| +        */
+                    /* max|theta_t|) below this (reading R13; default 1e-13; <= 0: report   */
+                    /* the margins in lfds_info without failing)                           */
 } lfds_options;
 
 /* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1,
- * graph 0, plane_dst 1. */
+ * graph 0, plane_dst 1, resonance_tol 1e-13. */
 void lfds_default_options(lfds_options* opt);
 
 /*
@@ -94,7 +99,10 @@ void lfds_default_options(lfds_options* opt);
  *  opt                           may be NULL (defaults).
  *  *out                          receives the plan; release with lfds_destroy.
  * Returns LFDS_EINVAL on bad input, LFDS_EEIG if an eigenbasis fails its checks,
- * LFDS_ECUDA / LFDS_ENOMEM on device errors.  All host arrays are only read.
+ * LFDS_ERESONANCE if a block's or the global z-systems are singular to within
+ * opt->resonance_tol (the message names "global" or the block (i, j), the harmonic (l, m) and
+ * the z-mode t; lfds_last_error), LFDS_ECUDA / LFDS_ENOMEM on device errors.  All host arrays
+ * are only read.  (The margins are computed on the device: host-only plans report -1.)
  */
 int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, const lfds_z* hz,
                     const lfds_z* sigma_node, const lfds_z* sigma_edge, lfds_z lambda,
@@ -207,8 +215,13 @@ typedef struct {
   double rel_residual[9];      /* refine = -1 (auto): ||Au-Mf||/||Mf|| before each refinement    */
                                /* pass and after the last (max over rhs); -1 = not read back     */
   double min_pivot_ratio;      /* min |pivot| / row-norm over all z-sweeps of the last call  */
+                               /* (copied stream-ordered into pinned host memory at the end of */
+                               /* the solve; lfds_get_report waits for that copy)              */
   int n_kernel_launches;       /* kernels enqueued by the last lfds_solve                   */
 } lfds_report;
+/* Synchronises the last solve's stream (for min_pivot_ratio).  Returns LFDS_ERESONANCE (and still
+ * fills *rep) when min_pivot_ratio < 1e-14: an unpivoted z-sweep met a near-zero pivot and the
+ * last solve must not be trusted (reported, never perturbed). */
 int lfds_get_report(const lfds_plan* plan, lfds_report* rep);
 
 typedef struct {
@@ -226,6 +239,15 @@ typedef struct {
   int n_plane_dst;             /* blocks whose steps 1 and 7 run as one plane sine transform  */
                                /* (options.plane_dst; uniform on both axes, one length L <= 128,
                                   complex data)                                              */
+  /* resonance margins (reading R13): min over (l, m, t) of |lambda_l + mu_m + theta_t|, theta_t
+     the eigenvalues of the z pencil A' z = theta E z (ascending Re, then Im), lambda_l / mu_m in
+     each basis' order (lfds_get_basis); 0-based indices; _rel divides by max|lambda_l| +
+     max|mu_m| + max|theta_t| of the family; -1 if not computed (host-only plan)             */
+  double margin_global, margin_global_rel;  /* step-5 global z-systems (single block: = block) */
+  int margin_global_lmt[3];
+  double margin_block, margin_block_rel;    /* the worst block's z-systems (steps 2 and 6)     */
+  int margin_block_ij[2];                   /* that block (x index, y index)                   */
+  int margin_block_lmt[3];
 } lfds_info;
 int lfds_get_info(const lfds_plan* plan, lfds_info* info);
 

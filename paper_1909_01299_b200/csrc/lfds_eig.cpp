@@ -524,4 +524,28 @@ bool z_modal_basis(const std::vector<double>& a, const std::vector<double>& g, c
   return true;
 }
 
+// Eigenvalues theta_t of the z pencil A' z = theta E z (complex tables allowed: complex sigma or
+// lambda, reading R11): the complex-symmetric tridiagonal S = E^{-1/2} A' E^{-1/2} (principal
+// square roots) by implicit QL in long double.  Used for the resonance margins
+// min |lambda_l + mu_m + theta_t| of the block and global z-systems T_lm = A' + (lambda_l + mu_m) E.
+bool z_pencil_values(const std::vector<zc>& a, const std::vector<zc>& g, const std::vector<zc>& c,
+                     const std::vector<zc>& e, std::vector<zc>& theta, std::string& err) {
+  const int n = (int)g.size();
+  if (n < 1) { err = "empty z pencil"; return false; }
+  std::vector<lc> sq(n), d(n), off(n > 1 ? n - 1 : 0);
+  for (int k = 0; k < n; ++k) {
+    if (e[k] == zc(0)) { err = "z mass has a zero entry"; return false; }
+    sq[k] = std::sqrt(lc(e[k]));
+    d[k] = lc(g[k]) / lc(e[k]);
+  }
+  for (int k = 0; k + 1 < n; ++k) {
+    if (c[k] != a[k + 1]) { err = "z operator not symmetric"; return false; }
+    off[k] = lc(c[k]) / (sq[k] * sq[k + 1]);
+  }
+  if (!ql_values(d, off)) { err = "QL iteration did not converge (z pencil values)"; return false; }
+  theta.resize(n);
+  for (int t = 0; t < n; ++t) theta[t] = zc((double)d[t].real(), (double)d[t].imag());
+  return true;
+}
+
 }  // namespace lfds

@@ -28,4 +28,8 @@ bool z_modal_basis(const std::vector<double>& a, const std::vector<double>& g, c
                    const std::vector<double>& e, std::vector<double>& theta, std::vector<double>& Z,
                    double& residual, double& orth, std::string& err);
 
+// Eigenvalues of the (possibly complex) z pencil A' z = theta E z, same table convention.
+bool z_pencil_values(const std::vector<zc>& a, const std::vector<zc>& g, const std::vector<zc>& c,
+                     const std::vector<zc>& e, std::vector<zc>& theta, std::string& err);
+
 }  // namespace lfds

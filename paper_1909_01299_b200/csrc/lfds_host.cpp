@@ -200,6 +200,10 @@ struct lfds_plan {
   int l_begin = 0, l_end = -1, rank0 = 1;
   int m_begin = 0, m_end = -1;  // z-modal step 5: this rank's global y-modes (-1: all)
   bool sharded = false;
+  // pivot monitor of the last solve: copied stream-ordered into pinned host memory at its end
+  double* h_piv = nullptr;
+  cudaStream_t piv_stream = nullptr;
+  bool piv_pending = false;
 };
 
 namespace {
@@ -896,6 +900,7 @@ void lfds_default_options(lfds_options* o) {
   o->s5_modal = 1;
   o->graph = 0;
   o->plane_dst = 1;
+  o->resonance_tol = 1e-13;
 }
 
 int lfds_stage_count(void) { return ST_COUNT; }
@@ -962,6 +967,88 @@ int lfds_kernel_times(lfds_plan* P, double* ms, int* launches) {
 
 const char* lfds_last_error(void) { return g_err.c_str(); }
 const char* lfds_version(void) { return "lfds 0.1 (sm_100a)"; }
+
+// min over (l, m, t) of |lambda_l + mu_m + theta_t| for every block (steps 2, 6) and the global
+// family (step 5) on the device (lfds_margin.cu); LFDS_ERESONANCE below opt.resonance_tol
+static int resonance_margins(lfds_plan* P, const std::vector<zc>& za, const std::vector<zc>& zg,
+                             const std::vector<zc>& zcv, const std::vector<zc>& ze) {
+  std::vector<zc> theta;
+  std::string err;
+  if (!z_pencil_values(za, zg, zcv, ze, theta, err)) return fail(LFDS_EEIG, "z pencil: %s", err.c_str());
+  std::stable_sort(theta.begin(), theta.end(), [](const zc& a, const zc& b) {
+    return a.real() < b.real() || (a.real() == b.real() && a.imag() < b.imag());
+  });
+  const Axis& X = P->ax[0];
+  const Axis& Y = P->ax[1];
+  std::vector<zc> ev;
+  std::vector<MarginSet> sets;
+  auto put = [&](const std::vector<zc>& v) { int64_t o = (int64_t)ev.size(); ev.insert(ev.end(), v.begin(), v.end()); return o; };
+  std::vector<int64_t> bxo, byo;
+  for (auto& b : X.blocks) bxo.push_back(put(b.B.lam));
+  for (auto& b : Y.blocks) byo.push_back(put(b.B.lam));
+  for (int j = 0; j < P->nby; ++j)
+    for (int i = 0; i < P->nbx; ++i) sets.push_back({bxo[i], byo[j], X.blocks[i].n, Y.blocks[j].n});
+  const bool glob = X.G.n > 0 && Y.G.n > 0;
+  if (glob) sets.push_back({put(X.G.lam), put(Y.G.lam), X.G.n, Y.G.n});
+  const int nz = P->nz, ns = (int)sets.size();
+  double2 *d_ev = nullptr, *d_th = nullptr;
+  MarginSet* d_sets = nullptr;
+  unsigned long long* d_out = nullptr;
+  std::vector<double2> hev(ev.size()), hth(nz);
+  for (size_t q = 0; q < ev.size(); ++q) hev[q] = make_double2(ev[q].real(), ev[q].imag());
+  for (int t = 0; t < nz; ++t) hth[t] = make_double2(theta[t].real(), theta[t].imag());
+  std::vector<unsigned long long> keys(ns);
+  cudaError_t e = cudaMalloc(&d_ev, hev.size() * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&d_th, hth.size() * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&d_sets, ns * sizeof(MarginSet));
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, ns * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemcpy(d_ev, hev.data(), hev.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_th, hth.data(), hth.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_sets, sets.data(), ns * sizeof(MarginSet), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_margins(d_ev, d_sets, ns, d_th, nz, d_out, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(keys.data(), d_out, ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(d_ev); cudaFree(d_th); cudaFree(d_sets); cudaFree(d_out);
+  CUDA_TRY(e);
+  double tmax = 0;
+  for (auto& t : theta) tmax = std::max(tmax, std::abs(t));
+  auto amax = [](const std::vector<zc>& v, int64_t o, int n) {
+    double m = 0;
+    for (int q = 0; q < n; ++q) m = std::max(m, std::abs(v[o + q]));
+    return m;
+  };
+  lfds_info& I = P->info;
+  for (int s = 0; s < ns; ++s) {
+    const MarginSet& S = sets[s];
+    const uint32_t idx = (uint32_t)(keys[s] & 0xffffffffull);
+    const int l = (int)(idx % (uint32_t)S.nx), m = (int)((idx / (uint32_t)S.nx) % (uint32_t)S.ny),
+              t = (int)(idx / ((uint32_t)S.nx * (uint32_t)S.ny));
+    const double mg = std::abs(ev[S.lx + l] + ev[S.ly + m] + theta[t]);  // exact value at the argmin
+    const double rel = mg / (amax(ev, S.lx, S.nx) + amax(ev, S.ly, S.ny) + tmax);
+    if (glob && s == ns - 1) {
+      I.margin_global = mg; I.margin_global_rel = rel;
+      I.margin_global_lmt[0] = l; I.margin_global_lmt[1] = m; I.margin_global_lmt[2] = t;
+    } else if (I.margin_block_rel < 0 || rel < I.margin_block_rel) {
+      I.margin_block = mg; I.margin_block_rel = rel;
+      I.margin_block_ij[0] = s % P->nbx; I.margin_block_ij[1] = s / P->nbx;
+      I.margin_block_lmt[0] = l; I.margin_block_lmt[1] = m; I.margin_block_lmt[2] = t;
+    }
+  }
+  if (!glob) {  // a single block is the global problem
+    I.margin_global = I.margin_block; I.margin_global_rel = I.margin_block_rel;
+    for (int q = 0; q < 3; ++q) I.margin_global_lmt[q] = I.margin_block_lmt[q];
+  }
+  const double tol = P->opt.resonance_tol;
+  if (tol > 0 && glob && I.margin_global_rel < tol)
+    return fail(LFDS_ERESONANCE, "resonance: global z-systems singular to %.3g (relative margin %.3g < %.3g) at "
+                "harmonic (l, m) = (%d, %d), z-mode t = %d", I.margin_global, I.margin_global_rel, tol,
+                I.margin_global_lmt[0], I.margin_global_lmt[1], I.margin_global_lmt[2]);
+  if (tol > 0 && I.margin_block_rel < tol)
+    return fail(LFDS_ERESONANCE, "resonance: block (%d, %d) z-systems singular to %.3g (relative margin %.3g < %.3g) "
+                "at harmonic (l, m) = (%d, %d), z-mode t = %d", I.margin_block_ij[0], I.margin_block_ij[1],
+                I.margin_block, I.margin_block_rel, tol, I.margin_block_lmt[0], I.margin_block_lmt[1],
+                I.margin_block_lmt[2]);
+  return LFDS_OK;
+}
 
 static int setup_axis(Axis& A, int N, const lfds_z* h, int nif, const int* iface, bool need_global, const char* name) {
   A.N = N;
@@ -1211,6 +1298,23 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
     CUDA_TRY(cudaSetDevice(P->opt.device));
     CUDA_TRY(cudaMalloc(&P->d_tab, T.v.size() * sizeof(double2)));
     CUDA_TRY(cudaMemcpy(P->d_tab, T.v.data(), T.v.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMallocHost(&P->h_piv, sizeof(double)));
+    *P->h_piv = -1.0;
+  }
+  // ---- resonance margins of the block and global z-systems (reading R13; never regularised)
+  {
+    lfds_info& I = P->info;
+    I.margin_global = I.margin_global_rel = I.margin_block = I.margin_block_rel = -1.0;
+    for (int q = 0; q < 3; ++q) I.margin_global_lmt[q] = I.margin_block_lmt[q] = -1;
+    I.margin_block_ij[0] = I.margin_block_ij[1] = -1;
+    if (P->opt.device >= 0 && (int64_t)nx * ny * nz < (int64_t)UINT32_MAX) {
+      if ((rc = resonance_margins(P.get(), za, zg, zcv, ze))) {
+        const std::string msg = g_err;
+        lfds_destroy(P.release());  // device tables already allocated
+        g_err = msg;
+        return rc;
+      }
+    }
   }
   auto t1 = std::chrono::steady_clock::now();
   lfds_info& I = P->info;
@@ -1269,6 +1373,10 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
   P->launches = 0;
   P->report = lfds_report{};
   P->report.min_pivot_ratio = 1.0;
+  // the pivot monitor lives at offset 0 of the workspace in every pass plan (RED first): one
+  // fill per solve, every chunk and refinement pass takes its min into the same word
+  double* red0 = reinterpret_cast<double*>(ws);
+  CUDA_TRY(launch_fill_minpiv(red0, st));
   double maxres[9] = {0};
   int passes_done = 0;
   for (int r0 = 0; r0 < nrhs; r0 += R) {
@@ -1290,7 +1398,6 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
     b.p[B_RED] = w + pp_main->off_red;
     b.p[B_CK] = w + pp_main->off_ck;
     double* red = reinterpret_cast<double*>(b.p[B_RED]);
-    CUDA_TRY(launch_fill_minpiv(red, st));
     if ((rc = run_pass(P, *pp_main, b, Rc, dt, dt, st))) return rc;
     int passes = 1;
     if (P->opt.refine != 0) {
@@ -1361,15 +1468,12 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
       }
     }
     passes_done = std::max(passes_done, passes);
-    if (P->opt.refine < 0) {  // the stream is already synchronised by the refinement loop
-      double mp = 1.0;
-      CUDA_TRY(cudaMemcpyAsync(&mp, red, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      P->report.min_pivot_ratio = std::min(P->report.min_pivot_ratio, mp);
-    } else {
-      P->report.min_pivot_ratio = -1.0;  // not read back (would synchronise the stream)
-    }
   }
+  // stream-ordered copy of the monitor into pinned host memory (a graph node when captured):
+  // lfds_get_report waits for it, the solve itself never synchronises for it
+  CUDA_TRY(cudaMemcpyAsync(P->h_piv, red0, sizeof(double), cudaMemcpyDeviceToHost, st));
+  P->piv_stream = st;
+  P->piv_pending = true;
   P->report.passes = passes_done;
   for (int i = 0; i < 9; ++i) P->report.rel_residual[i] = maxres[i];
   P->report.n_kernel_launches = P->launches;
@@ -1645,7 +1749,11 @@ int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, in
   if ((rc = run_pass(P, *pp, b, R, dt, dt, st, phase == 1 ? PH_1 : phase == 2 ? PH_2 : PH_3))) return rc;
   P->report.passes = 1;
   P->report.n_kernel_launches = P->launches;
-  P->report.min_pivot_ratio = -1.0;
+  if (phase == 3) {
+    CUDA_TRY(cudaMemcpyAsync(P->h_piv, b.p[B_RED], sizeof(double), cudaMemcpyDeviceToHost, st));
+    P->piv_stream = st;
+    P->piv_pending = true;
+  }
   return LFDS_OK;
 }
 
@@ -1693,6 +1801,8 @@ int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws,
   }
   CUDA_TRY(cudaGraphLaunch(P->gexec, st));
   P->report = P->grep;
+  P->piv_stream = st;  // the graph ends with the monitor's copy into P->h_piv
+  P->piv_pending = true;
   for (const auto& r : P->grecs) P->prof.recs.push_back(r);  // this replay's stage events
   return LFDS_OK;
 }
@@ -1758,9 +1868,19 @@ int lfds_residual(lfds_plan* P, const void* u_dev, const void* f_dev, lfds_z* r_
   return LFDS_OK;
 }
 
-int lfds_get_report(const lfds_plan* P, lfds_report* rep) {
-  if (!P || !rep) return fail(LFDS_EINVAL, "NULL argument");
+int lfds_get_report(const lfds_plan* cP, lfds_report* rep) {
+  if (!cP || !rep) return fail(LFDS_EINVAL, "NULL argument");
+  lfds_plan* P = const_cast<lfds_plan*>(cP);
+  if (P->piv_pending) {
+    CUDA_TRY(cudaStreamSynchronize(P->piv_stream));
+    P->report.min_pivot_ratio = *P->h_piv;
+    if (P->gexec) P->grep.min_pivot_ratio = *P->h_piv;
+    P->piv_pending = false;
+  }
   *rep = P->report;
+  if (rep->min_pivot_ratio >= 0 && rep->min_pivot_ratio < 1e-14)
+    return fail(LFDS_ERESONANCE, "z-sweep pivot ratio %.3g < 1e-14 in the last solve (near-singular T_lm)",
+                rep->min_pivot_ratio);
   return LFDS_OK;
 }
 
@@ -1801,6 +1921,7 @@ void lfds_destroy(lfds_plan* P) {
     free_pass(kv.second);
   }
   if (P->d_tab) cudaFree(P->d_tab);
+  if (P->h_piv) cudaFreeHost(P->h_piv);
   if (P->gexec) cudaGraphExecDestroy(P->gexec);
   if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
   for (auto& r : P->grecs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

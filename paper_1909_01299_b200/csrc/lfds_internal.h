@@ -177,5 +177,13 @@ cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, in
 cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st);
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
 size_t zsolve_checkpoint_bytes(int nblocks, int max_nx, int max_ny, int R, int nz);
+// resonance margins (lfds_margin.cu): per set, min over (l, m, t) of |ev[lx + l] + ev[ly + m] +
+// theta[t]| as a 64-bit key (float bits << 32 | flat index (t * ny + m) * nx + l) in out[set]
+struct MarginSet {
+  int64_t lx, ly;
+  int nx, ny;
+};
+cudaError_t launch_margins(const double2* d_ev, const MarginSet* d_sets, int nsets, const double2* d_theta, int nz,
+                           unsigned long long* d_out, cudaStream_t st);
 
 }  // namespace lfds

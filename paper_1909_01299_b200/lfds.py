@@ -38,7 +38,7 @@ class Options(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("refine", ctypes.c_int), ("refine_tol", ctypes.c_double),
                 ("residual_dd", ctypes.c_int), ("device", ctypes.c_int), ("rhs_chunk", ctypes.c_int),
                 ("profile", ctypes.c_int), ("s5_modal", ctypes.c_int), ("graph", ctypes.c_int),
-                ("plane_dst", ctypes.c_int)]
+                ("plane_dst", ctypes.c_int), ("resonance_tol", ctypes.c_double)]
 
 
 class Report(ctypes.Structure):
@@ -56,7 +56,11 @@ class Info(ctypes.Structure):
                 ("setup_seconds", ctypes.c_double), ("eig_max_residual", ctypes.c_double),
                 ("eig_max_biorth", ctypes.c_double), ("device_table_bytes", ctypes.c_size_t),
                 ("s5_modal", ctypes.c_int), ("z_eig_residual", ctypes.c_double), ("z_eig_orth", ctypes.c_double),
-                ("n_plane_dst", ctypes.c_int)]
+                ("n_plane_dst", ctypes.c_int),
+                ("margin_global", ctypes.c_double), ("margin_global_rel", ctypes.c_double),
+                ("margin_global_lmt", ctypes.c_int * 3),
+                ("margin_block", ctypes.c_double), ("margin_block_rel", ctypes.c_double),
+                ("margin_block_ij", ctypes.c_int * 2), ("margin_block_lmt", ctypes.c_int * 3)]
 
 
 _P = ctypes.c_void_p
@@ -127,7 +131,7 @@ class Plan:
                  iface_y: Sequence[int] = (), *, dtype: str = "c128", refine: int = 0,
                  refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0,
                  profile: bool = False, s5_modal: bool = True, graph: bool = False,
-                 plane_dst: bool = True):
+                 plane_dst: bool = True, resonance_tol: float = 1e-13):
         opt = Options()
         _lib.lfds_default_options(ctypes.byref(opt))
         opt.dtype = LFDS_F64 if dtype in ("f64", "float64") else LFDS_C128
@@ -136,6 +140,7 @@ class Plan:
         opt.s5_modal = int(bool(s5_modal))
         opt.graph = int(bool(graph))
         opt.plane_dst = int(bool(plane_dst))
+        opt.resonance_tol = float(resonance_tol)
         self.plane_dst = bool(plane_dst)
         self.device = int(device)
         self.dtype = opt.dtype
@@ -169,11 +174,19 @@ class Plan:
     def info(self) -> dict:
         i = Info()
         _check(_lib.lfds_get_info(self._h, ctypes.byref(i)))
-        return {k: getattr(i, k) for k, _ in Info._fields_}
+        out = {}
+        for k, _ in Info._fields_:
+            v = getattr(i, k)
+            out[k] = list(v) if isinstance(v, ctypes.Array) else v
+        return out
 
-    def report(self) -> dict:
+    def report(self, check: bool = False) -> dict:
+        """Last solve's report (waits for its pivot-monitor copy).  check=True raises LfdsError
+        (ERESONANCE) when the monitor saw a pivot below 1e-14 of its row norm."""
         r = Report()
-        _check(_lib.lfds_get_report(self._h, ctypes.byref(r)))
+        rc = _lib.lfds_get_report(self._h, ctypes.byref(r))
+        if rc != 3 or check:
+            _check(rc)
         return {"passes": r.passes, "rel_residual": list(r.rel_residual)[:max(r.passes, 1)],
                 "min_pivot_ratio": r.min_pivot_ratio, "n_kernel_launches": r.n_kernel_launches}
 

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
+from oracle.solve import block_ranges
 from workloads import make_problem, shrunken
 from workloads.configs import Problem
 
@@ -40,8 +41,8 @@ def parity_norms(p, U, ref):
     ref = np.asarray(ref).reshape(p.shape)
     err = np.abs(U - ref)
     blk = 0.0
-    for (x0, x1) in oracle.block_ranges(p.nx, p.iface_x):
-        for (y0, y1) in oracle.block_ranges(p.ny, p.iface_y):
+    for (x0, x1) in block_ranges(p.nx, p.iface_x):
+        for (y0, y1) in block_ranges(p.ny, p.iface_y):
             sl = (slice(None), slice(y0 - 1, y1), slice(x0 - 1, x1))
             blk = max(blk, float(err[sl].max() / np.abs(ref[sl]).max()))
     pl = 0.0
