@@ -491,6 +491,7 @@ def run_ours(args, rank, world, local_rank):
                              graph=not blocks, rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0),
                              plane_dst=bool(args.plane_dst))
     setup_s = time.perf_counter() - t0
+    info0 = plan.info()
     part = lfds_dist.shard(plan, rank, world) if blocks else None
     dt = torch.float64 if p.real else torch.complex128
     # right-hand sides generated one at a time straight into device memory (C5: 64 x 0.84 GB)
@@ -526,7 +527,9 @@ def run_ours(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1) / args.steps
     stages = plan.stage_times()
     kernels = plan.kernel_times()
-    launches_per_step = plan.report()["n_kernel_launches"]
+    rep0 = plan.report()
+    launches_per_step = rep0["n_kernel_launches"]
+    piv = rep0["min_pivot_ratio"]
     tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -620,7 +623,12 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": (f"block-sharded x{world} (LPT blocks, step-5 modes, 2 NCCL all-reduces)"
                                        if blocks else f"rhs-sharded x{world}" if world > 1 else "1 gpu"),
                        "l2": "inputs larger than L2 (no flush)" if p.unknowns * 16 > 126e6 else "L2-resident",
-                       "setup_s": setup_s, "rel_residual_dd": rel_res},
+                       "setup_s": setup_s, "rel_residual_dd": rel_res,
+                       # reading R13: min |lambda_l + mu_m + theta_t| of the global and block
+                       # z-systems (relative to the family's spectral scale), from lfds_info
+                       "resonance_margin": {k: info0[k] for k in ("margin_global", "margin_global_rel",
+                                                                  "margin_block", "margin_block_rel")},
+                       "min_pivot_ratio": piv},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
         }
