@@ -493,6 +493,8 @@ def run_ours(args, rank, world, local_rank):
     setup_s = time.perf_counter() - t0
     info0 = plan.info()
     part = lfds_dist.shard(plan, rank, world) if blocks else None
+    if blocks and world > 1 and args.exchange == "library":
+        lfds_dist.attach_nccl(plan, rank, world)  # both exchanges as ncclAllReduce on the solve stream
     dt = torch.float64 if p.real else torch.complex128
     # right-hand sides generated one at a time straight into device memory (C5: 64 x 0.84 GB)
     f = torch.empty((nrhs,) + p.shape, dtype=dt, device=dev)
@@ -620,7 +622,8 @@ def run_ours(args, rank, world, local_rank):
                        "blocks": [len(p.iface_x) + 1, len(p.iface_y) + 1], "nrhs_per_gpu": nrhs,
                        "refine_passes": refine,
                        "refine_residual": ("double-double" if res_dd else "fp64") if refine else None,
-                       "parallelism": (f"block-sharded x{world} (LPT blocks, step-5 modes, 2 NCCL all-reduces)"
+                       "parallelism": (f"block-sharded x{world} (LPT blocks, step-5 modes, 2 NCCL all-reduces, "
+                                       f"{'in-library' if args.exchange == 'library' else 'torch.distributed'})"
                                        if blocks else f"rhs-sharded x{world}" if world > 1 else "1 gpu"),
                        "l2": "inputs larger than L2 (no flush)" if p.unknowns * 16 > 126e6 else "L2-resident",
                        "setup_s": setup_s, "rel_residual_dd": rel_res,
@@ -755,6 +758,8 @@ def main():
     ap.add_argument("--shard", choices=["blocks", "rhs"], default=None,
                     help="N > 1: block sharding with two NCCL exchanges (default) or RHS sharding")
     ap.add_argument("--e2e-rhs", type=int, default=4, dest="e2e_rhs", help="RHS per e2e step (memory bound)")
+    ap.add_argument("--exchange", choices=["library", "torch"], default="library",
+                    help="block sharding: exchanges inside lfds_solve (NCCL, lfds_set_comm) or torch.distributed")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--plane-dst", type=int, default=1, choices=[0, 1], dest="plane_dst",
                     help="1: plane sine transforms on uniform x uniform blocks (options.plane_dst)")

@@ -207,6 +207,19 @@ int lfds_set_partition(lfds_plan* plan, const int* block_owned, int l_begin, int
  */
 int lfds_set_mode_rows(lfds_plan* plan, int m_begin, int m_end);
 int lfds_exchange_layout(const lfds_plan* plan, int nrhs, int which, size_t* byte_offset, size_t* n_doubles);
+/*
+ * In-library exchanges (BASELINE.json north_star: "NCCL over NVLink only for the interface
+ * exchange"; PAPER.md:69-70 is that exchange).  NCCL is loaded at run time (dlopen of the
+ * libnccl.so.2 already in the process, else the system one; LFDS_NCCL_LIB overrides): the
+ * library links none.  One rank calls lfds_nccl_unique_id and the caller broadcasts the 128
+ * bytes; then every rank of the group calls lfds_set_comm (collective, like ncclCommInitRank)
+ * on its partitioned plan.  From then on lfds_solve on that plan runs the three phases with the
+ * two exchanges summed by ncclAllReduce (float64, in place in the workspace) on the solve stream:
+ * no host round trip between the phases.  id = NULL releases the communicator (back to
+ * lfds_solve_phase + caller-driven sums).  LFDS_ENCCL if NCCL is missing or fails.
+ */
+int lfds_nccl_unique_id(unsigned char* id);  /* id: 128 bytes */
+int lfds_set_comm(lfds_plan* plan, const unsigned char* id, int rank, int world);
 int lfds_solve_phase(lfds_plan* plan, int phase, const void* f_dev, void* u_dev, int nrhs, void* ws,
                      size_t ws_bytes, void* cuda_stream);
 

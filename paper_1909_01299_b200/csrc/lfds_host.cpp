@@ -19,6 +19,7 @@
 // optional refinement: r = M f - A u (k_residual, fp64 or double-double), u += solve(r) (k_axpy).
 // k_gemm (plain FP64 tiles) runs only the f64 (real, C1) plans' transforms.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -55,6 +56,44 @@ static int fail(int code, const char* fmt, ...) {
   } while (0)
 
 namespace {
+
+// ---- NCCL, loaded at run time (dlopen): the library links no NCCL; the process's own copy
+// (the one torch loaded) is preferred.  Only the handful of entry points the exchanges use.
+struct NcclId { char internal[128]; };           // == ncclUniqueId
+typedef struct ncclComm* NcclComm;                // == ncclComm_t
+struct NcclApi {
+  bool ok = false;
+  int (*get_unique_id)(NcclId*) = nullptr;
+  int (*comm_init_rank)(NcclComm*, int, NcclId, int) = nullptr;
+  int (*comm_destroy)(NcclComm) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+};
+enum { NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = nullptr;
+  const char* env = getenv("LFDS_NCCL_LIB");
+  const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+  for (const char* n : names) {
+    if (!n) continue;
+    h = dlopen(n, RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);  // already in the process (torch)?
+    if (!h) h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (h) break;
+  }
+  if (!h) return api;
+  api.get_unique_id = reinterpret_cast<int (*)(NcclId*)>(dlsym(h, "ncclGetUniqueId"));
+  api.comm_init_rank = reinterpret_cast<int (*)(NcclComm*, int, NcclId, int)>(dlsym(h, "ncclCommInitRank"));
+  api.comm_destroy = reinterpret_cast<int (*)(NcclComm)>(dlsym(h, "ncclCommDestroy"));
+  api.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t)>(
+      dlsym(h, "ncclAllReduce"));
+  api.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+  api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_reduce && api.error_string;
+  return api;
+}
 
 struct AxisBlock {
   int lo, n;         // first node (1-based), interior size
@@ -200,6 +239,9 @@ struct lfds_plan {
   int l_begin = 0, l_end = -1, rank0 = 1;
   int m_begin = 0, m_end = -1;  // z-modal step 5: this rank's global y-modes (-1: all)
   bool sharded = false;
+  // in-library exchanges (lfds_set_comm): the NCCL communicator of this rank's group
+  NcclComm comm = nullptr;
+  int comm_rank = 0, comm_world = 1;
   // pivot monitor of the last solve: copied stream-ordered into pinned host memory at its end
   double* h_piv = nullptr;
   cudaStream_t piv_stream = nullptr;
@@ -1656,6 +1698,58 @@ int lfds_gmres(lfds_plan* P, const void* dlam, const void* f, void* u, double to
   return LFDS_OK;
 }
 
+int lfds_nccl_unique_id(unsigned char* id) {
+  if (!id) return fail(LFDS_EINVAL, "id is NULL");
+  NcclApi& A = nccl();
+  if (!A.ok) return fail(LFDS_ENCCL, "NCCL not found (dlopen libnccl.so.2; LFDS_NCCL_LIB overrides)");
+  NcclId u{};
+  const int r = A.get_unique_id(&u);
+  if (r) return fail(LFDS_ENCCL, "ncclGetUniqueId: %s", A.error_string(r));
+  std::memcpy(id, u.internal, sizeof u.internal);
+  return LFDS_OK;
+}
+
+int lfds_set_comm(lfds_plan* P, const unsigned char* id, int rank, int world) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  NcclApi& A = nccl();
+  if (P->comm) {
+    if (A.ok) A.comm_destroy(P->comm);
+    P->comm = nullptr;
+  }
+  drop_graph(P);  // a captured sharded graph holds the old communicator's collectives
+  if (!id) return LFDS_OK;  // back to caller-driven exchanges
+  if (world < 1 || rank < 0 || rank >= world) return fail(LFDS_EINVAL, "bad rank %d of %d", rank, world);
+  if (!A.ok) return fail(LFDS_ENCCL, "NCCL not found (dlopen libnccl.so.2; LFDS_NCCL_LIB overrides)");
+  CUDA_TRY(cudaSetDevice(P->opt.device));
+  NcclId u{};
+  std::memcpy(u.internal, id, sizeof u.internal);
+  const int r = A.comm_init_rank(&P->comm, world, u, rank);
+  if (r) { P->comm = nullptr; return fail(LFDS_ENCCL, "ncclCommInitRank: %s", A.error_string(r)); }
+  P->comm_rank = rank;
+  P->comm_world = world;
+  return LFDS_OK;
+}
+
+// the three phases with both exchanges summed over the communicator on the solve stream
+// (stream-ordered: no host round trip between the phases, and the whole sharded solve can be
+// captured in a CUDA graph); nrhs in one pass, no refinement (as lfds_solve_phase)
+static int solve_sharded_nccl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes,
+                              cudaStream_t st) {
+  NcclApi& A = nccl();
+  int rc;
+  for (int ph = 1; ph <= 3; ++ph) {
+    if ((rc = lfds_solve_phase(P, ph, f_dev, u_dev, nrhs, ws, ws_bytes, st))) return rc;
+    if (ph == 3) break;
+    size_t off = 0, n = 0;
+    if ((rc = lfds_exchange_layout(P, nrhs, ph, &off, &n))) return rc;
+    double* x = reinterpret_cast<double*>(static_cast<char*>(ws) + off);
+    const int r = A.all_reduce(x, x, n, NCCL_FLOAT64, NCCL_SUM, P->comm, st);
+    if (r) return fail(LFDS_ENCCL, "ncclAllReduce (exchange %d): %s", ph, A.error_string(r));
+  }
+  return LFDS_OK;
+}
+
 int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_end, int rank0) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
   const int nblk = P->nbx * P->nby, Nx = P->ax[0].N;
@@ -1757,9 +1851,15 @@ int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, in
   return LFDS_OK;
 }
 
+static int solve_sharded_nccl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes,
+                              cudaStream_t st);
+
 int lfds_solve(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes, void* stream) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
-  if (P->sharded) return fail(LFDS_EINVAL, "partitioned plan: use lfds_solve_phase with the two exchanges");
+  if (P->sharded && P->comm)  // block-sharded solve with the exchanges inside the library
+    return solve_sharded_nccl(P, f_dev, u_dev, nrhs, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+  if (P->sharded) return fail(LFDS_EINVAL, "partitioned plan: use lfds_solve_phase with the two exchanges, or "
+                                           "lfds_set_comm for in-library exchanges");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
   if (nrhs < 1 || !f_dev || !u_dev || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
   if (((uintptr_t)f_dev | (uintptr_t)u_dev | (uintptr_t)ws) & 15) return fail(LFDS_EINVAL, "pointers must be 16-byte aligned");
@@ -1917,6 +2017,7 @@ int lfds_get_basis(const lfds_plan* P, int axis, int block, int* n, int* kind, i
 
 void lfds_destroy(lfds_plan* P) {
   if (!P) return;
+  if (P->comm && nccl().ok) nccl().comm_destroy(P->comm);
   for (auto& kv : P->passes) {
     free_pass(kv.second);
   }

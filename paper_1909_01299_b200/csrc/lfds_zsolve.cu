@@ -32,6 +32,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "lfds_internal.h"
 
@@ -746,17 +747,31 @@ cudaError_t prep(K kern, size_t sm) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
 }
 
+// experiment knob (tools/zs_occupancy.sh): extra dynamic shared memory per CTA of the step-2 /
+// step-6 solvers, to force fewer CTAs per SM (fewer lines in flight: the backward-sweep re-read
+// of k_zs1 then hits L2).  0 unless LFDS_ZS_PAD1 / LFDS_ZS_PAD2 is set.
+size_t zs_pad(int mode) {
+  static long p1 = -1, p2 = -1;
+  if (p1 < 0) {
+    const char* a = getenv("LFDS_ZS_PAD1");
+    const char* b = getenv("LFDS_ZS_PAD2");
+    p1 = a ? atol(a) : 0;
+    p2 = b ? atol(b) : 0;
+  }
+  return (size_t)(mode == 1 ? p1 : mode == 2 ? p2 : 0);
+}
+
 template <bool REALZ, int TL, bool FULL>
 cudaError_t launch_tl(int mode, dim3 grid, cudaStream_t st, const ZBlock* b, int nz, ZTab tab, const GSweep& g,
                       const Bufs& bufs, double* mp) {
   const size_t zt = (size_t)ztab_slots(nz, REALZ) * sizeof(double2);
   cudaError_t e;
   if (mode == 1) {
-    const size_t sm = zt + (size_t)3 * 8 * ZT * sizeof(double2);
+    const size_t sm = zt + (size_t)3 * 8 * ZT * sizeof(double2) + zs_pad(1);
     if ((e = prep(k_zs1<REALZ, TL, FULL>, sm)) != cudaSuccess) return e;
     k_zs1<REALZ, TL, FULL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs, mp);
   } else if (mode == 2) {
-    const size_t sm = zt + (size_t)(2 * FaceStage<TL, 16>::SLOTS + 2 * 8 * ZT) * sizeof(double2);
+    const size_t sm = zt + (size_t)(2 * FaceStage<TL, 16>::SLOTS + 2 * 8 * ZT) * sizeof(double2) + zs_pad(2);
     if ((e = prep(k_zs2<REALZ, TL, FULL>, sm)) != cudaSuccess) return e;
     k_zs2<REALZ, TL, FULL><<<grid, ZT, sm, st>>>(b, nz, tab, bufs);
   } else {

@@ -10,8 +10,9 @@ contributions of its own blocks to the residual on the interface planes (PAPER.m
 residuals are summed over the ranks (exchange 1).  Step 5 is split by global
 x-modes l (and, in the z-modal form, by global y-modes m): each rank handles its (m, l) range and
 the plane projections are summed (exchange 2).
-Both sums are `torch.distributed.all_reduce` on views of the library workspace (NCCL on GPUs);
-`allreduce` can be replaced (tests use an in-process emulation and gloo).
+Both sums run either inside the library (attach_nccl: ncclAllReduce on the solve stream, no
+host round trip) or as `torch.distributed.all_reduce` on views of the library workspace
+(`allreduce` can be replaced: tests use an in-process emulation and gloo).
 """
 from __future__ import annotations
 
@@ -92,9 +93,33 @@ def shard(plan, rank: int, world: int) -> dict:
     return {"owner": owner, "l_range": (l0, l1), "m_range": (m0, m1), "costs": costs}
 
 
+def attach_nccl(plan, rank: int, world: int, broadcast: Optional[Callable] = None) -> bytes:
+    """In-library exchanges for a sharded plan: rank 0 makes the NCCL group id, `broadcast`
+    (default: torch.distributed.broadcast of a uint8 tensor from rank 0) shares it, and every
+    rank joins (lfds_set_comm).  lfds_solve then runs the phases and both all-reduces on the
+    solve stream."""
+    from .lfds import nccl_unique_id
+    uid = nccl_unique_id() if rank == 0 else bytes(128)
+    if world > 1:
+        if broadcast is None:
+            import torch
+            import torch.distributed as tdist
+            dev = torch.device("cuda", torch.cuda.current_device()) if tdist.get_backend() == "nccl" else "cpu"
+            t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+            tdist.broadcast(t, 0)
+            uid = bytes(t.cpu().tolist())
+        else:
+            uid = broadcast(uid)
+    plan.set_comm(uid, rank, world)
+    return uid
+
+
 def solve_sharded(plan, f, u, ws, allreduce: Optional[Callable] = None, stream=None):
     """One block-sharded solve: phase 1, sum of exchange 1, phase 2, sum of exchange 2, phase 3.
-    `allreduce(tensor)` sums in place over the ranks (default: torch.distributed.all_reduce)."""
+    `allreduce(tensor)` sums in place over the ranks (default: torch.distributed.all_reduce).
+    A plan with an in-library communicator (attach_nccl) does all of it in one lfds_solve."""
+    if getattr(plan, "has_comm", False) and allreduce is None:
+        return plan.solve(f, out=u, stream=stream)
     if allreduce is None:
         import torch.distributed as dist
 

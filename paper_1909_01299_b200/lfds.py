@@ -98,6 +98,8 @@ _lib.lfds_kernel_name.argtypes = [ctypes.c_int]
 _lib.lfds_kernel_name.restype = ctypes.c_char_p
 _lib.lfds_kernel_times.argtypes = [_P, _P, _P]
 _lib.lfds_fp64_peak.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
+_lib.lfds_nccl_unique_id.argtypes = [_P]
+_lib.lfds_set_comm.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int]
 _lib.lfds_last_error.restype = ctypes.c_char_p
 _lib.lfds_version.restype = ctypes.c_char_p
 
@@ -107,7 +109,7 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
             "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
             "lfds_set_mode_rows", "lfds_kernel_count", "lfds_kernel_name", "lfds_kernel_times",
-            "lfds_fp64_peak"]
+            "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm"]
 
 
 def _check(rc):
@@ -143,6 +145,7 @@ class Plan:
         opt.resonance_tol = float(resonance_tol)
         self.plane_dst = bool(plane_dst)
         self.device = int(device)
+        self.has_comm = False
         self.dtype = opt.dtype
         hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
         sn_, psn = _zarr(sigma_node); se_, pse = _zarr(sigma_edge)
@@ -329,6 +332,17 @@ class Plan:
         _check(_lib.lfds_set_mode_rows(self._h, int(m_begin), int(m_end)))
         self._ws = {}
 
+    def set_comm(self, uid: Optional[bytes], rank: int = 0, world: int = 1):
+        """In-library exchanges: join the NCCL group `uid` (128 bytes from nccl_unique_id(),
+        the same on every rank; collective).  None releases it."""
+        if uid is None:
+            _check(_lib.lfds_set_comm(self._h, None, 0, 1))
+            self.has_comm = False
+            return
+        buf = (ctypes.c_ubyte * 128).from_buffer_copy(bytes(uid))
+        _check(_lib.lfds_set_comm(self._h, ctypes.cast(buf, _P), int(rank), int(world)))
+        self.has_comm = True
+
     def exchange_view(self, ws, nrhs: int, which: int):
         """float64 view of exchange `which` (1: interface residual, 2: plane projections) in ws."""
         torch = self._torch()
@@ -376,6 +390,13 @@ def fp64_peak(stream=None) -> float:
     tf = ctypes.c_double()
     _check(_lib.lfds_fp64_peak(_P(st), ctypes.byref(tf)))
     return tf.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL group id (lfds_nccl_unique_id) for Plan.set_comm."""
+    buf = (ctypes.c_ubyte * 128)()
+    _check(_lib.lfds_nccl_unique_id(ctypes.cast(buf, _P)))
+    return bytes(buf)
 
 
 def setup_grid(hx, hy, hz, sigma_node, sigma_edge, lam, iface_x=(), iface_y=(), **kw) -> Plan:

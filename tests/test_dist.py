@@ -81,3 +81,69 @@ def test_solve_sharded_protocol_gloo_world2():
         assert calls == [1, ("x", 1), 2, ("x", 2), 3]
         assert seen1 == [3.0] * 6                     # 1 + 2: exchange 1 summed before phase 2
         assert ex2 == [0.0, 3.0, 6.0, 9.0]            # (1 + 2) * arange: exchange 2 summed
+
+
+class _OraclePlan:
+    """Stand-in whose phase 1 is the interface residual of PAPER.md:52/:69 computed by the ORACLE
+    for this rank's own blocks only: -A v_b restricted to the planes for every owned block b
+    (v_b = the oracle's block solution, zero elsewhere), plus b = M f on the planes on rank 0.
+    Summed over the ranks (exchange 1) it must equal r_b = b - A v on the planes for the whole
+    partition, whatever the LPT ownership."""
+
+    def __init__(self, p, rank, world, owner):
+        import oracle
+        from oracle.solve import block_ranges
+        b = oracle.mass_rhs(p, p.rhs(0))
+        v = oracle.block_solutions(p, b)
+        own = np.zeros(p.shape, bool)
+        bxr, byr = block_ranges(p.nx, p.iface_x), block_ranges(p.ny, p.iface_y)
+        for j, (y0, y1) in enumerate(byr):
+            for i, (x0, x1) in enumerate(bxr):
+                if owner[j, i] == rank:
+                    own[:, y0 - 1:y1, x0 - 1:x1] = True
+        part = -oracle.apply_stencil(p, np.where(own, v, 0))
+        if rank == 0:
+            part = part + b
+        self.p, self.full = p, b - oracle.apply_stencil(p, v)
+        self.ex1 = torch.from_numpy(self._planes(part).view(np.float64).copy())
+        self.ex2 = torch.zeros(2, dtype=torch.float64)
+
+    def _planes(self, r):
+        return np.concatenate([r[:, :, a - 1].ravel() for a in self.p.iface_x] +
+                              [r[:, bb - 1, :].ravel() for bb in self.p.iface_y])
+
+    def solve_phase(self, phase, f, u, ws, stream=None):
+        if phase == 2:
+            self.seen1 = self.ex1.numpy().view(np.complex128).copy()
+
+    def exchange_view(self, ws, nrhs, which):
+        return self.ex1 if which == 1 else self.ex2
+
+
+def _oracle_worker(rank, world, port, out):
+    from workloads import shrunken
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist_mod.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = shrunken("c3", nrhs=1)
+        nb = [len(p.iface_x) + 1, len(p.iface_y) + 1]
+        # ownership as dist.shard assigns it (LPT on the modelled costs, here all blocks real)
+        owner = dist.lpt_partition(dist.block_costs([1] * nb[0], [1] * nb[1], [1] * nb[0], [1] * nb[1]) +
+                                   np.arange(nb[0] * nb[1]).reshape(nb[1], nb[0]), world)
+        fp = _OraclePlan(p, rank, world, owner)
+        dist.solve_sharded(fp, torch.zeros(1, 1, 1, 1), None, None)
+        out[rank] = float(np.abs(fp.seen1 - fp._planes(fp.full)).max() / np.abs(fp.full).max())
+    finally:
+        dist_mod.destroy_process_group()
+
+
+def test_exchange1_sums_the_ranks_partial_interface_residuals_gloo_world2():
+    """Two gloo ranks, each owning the LPT half of the blocks of the shrunken C3 analog: the
+    summed exchange 1 equals the oracle's interface residual of the whole partition."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_oracle_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] < 1e-13 and out[1] < 1e-13, dict(out)

@@ -565,3 +565,28 @@ def test_block_sharded_2d_mode_split_matches_single_device(world):
     # and against the oracle's global separable solve (not only the unsharded GPU solve)
     ref = oracle.solve_separable(p, oracle.mass_rhs(p, F[0]))
     assert_parity(p, u.cpu().numpy()[0], ref)
+
+
+def test_in_library_nccl_exchange_size1_communicator():
+    """The in-library exchange path (lfds_set_comm: ncclAllReduce of both exchanges on the solve
+    stream inside lfds_solve) through a size-1 NCCL communicator equals the unsharded solve and
+    the oracle; releasing the communicator restores caller-driven phases."""
+    from paper_1909_01299_b200 import LfdsError, Plan, dist
+    p = shrunken("c4", nrhs=1)
+    F = p.rhs_all()
+    f = torch.from_numpy(F).cuda()
+    u_ref = Plan.from_problem(p).solve(f)
+    pl = Plan.from_problem(p)
+    dist.shard(pl, 0, 1)
+    dist.attach_nccl(pl, 0, 1)
+    u = torch.zeros_like(f)
+    ws = pl.workspace(1)
+    dist.solve_sharded(pl, f, u, ws)
+    torch.cuda.synchronize()
+    assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) < 1e-12
+    assert_parity(p, u.cpu().numpy()[0], oracle.solve_direct(p, oracle.mass_rhs(p, F[0])))
+    assert 0 < pl.report()["min_pivot_ratio"] <= 1
+    pl.set_comm(None)
+    with pytest.raises(LfdsError):
+        pl.solve(f)
+    pl.close()
