@@ -312,7 +312,8 @@ def kernel_algorithmic(p, R: int, plan=None):
         "k_dstw": (None, (alg["step1_x_sine"][1] or 0) + (alg["step7_x_sine"][1] or 0) or None),
         "k_dst": (None, (alg["step1_y_sine"][1] or 0) + (alg["step7_y_sine"][1] or 0) or None),
         "k_dst2": (None, (alg["step1_plane_sine"][1] or 0) + (alg["step7_plane_sine"][1] or 0) or None),
-        "k_zs1": alg["step2_zsolve"], "k_zs2": alg["step6_zsolve_lift"], "k_proj_rows": alg["step3_edge_projection"],
+        "k_zs1": alg["step2_zsolve"], "k_zsw": alg["step2_zsolve"], "k_zs2": alg["step6_zsolve_lift"],
+        "k_proj_rows": alg["step3_edge_projection"],
         "k_s5m": (alg["step5_global_zsolve"][0], None) if modal else (None, None),
         "k_zs3": (None, None) if modal else alg["step5_global_zsolve"],
         "k_projm": (None, None) if modal else alg["step5_projection"],

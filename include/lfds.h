@@ -74,10 +74,14 @@ typedef struct {
                     /* min|lambda_l + mu_m + theta_t| / (max|lambda_l| + max|mu_m| +        */
                     /* max|theta_t|) below this (reading R13; default 1e-13; <= 0: report   */
                     /* the margins in lfds_info without failing)                           */
+  int zs_warp;      /* 1: step 2 with a warp per z-line (Thomas on 32 row chunks + parallel  */
+                    /* cyclic reduction of the chunk separators across the lanes, tiles    */
+                    /* staged in shared memory: one read and one write of v~    */
+                    /* §6b); 0 (default): a thread per line (k_zs1, measured faster)        */
 } lfds_options;
 
 /* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1,
- * graph 0, plane_dst 1, resonance_tol 1e-13. */
+ * graph 0, plane_dst 1, resonance_tol 1e-13, zs_warp 0. */
 void lfds_default_options(lfds_options* opt);
 
 /*

@@ -126,10 +126,10 @@ const char* kStageNames[ST_COUNT] = {
 
 // kernel kinds (per-kernel device time: the roofline of the dominant kernel, bench.py)
 enum Kern { K_XFORM3M, K_XFORM, K_DSTW, K_DST, K_DST2, K_ZS1, K_ZS2, K_ZS3, K_PROJ, K_PROJM, K_S5M, K_IFRES,
-            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_COUNT };
+            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_ZSW, K_COUNT };
 const char* kKernNames[K_COUNT] = {
     "k_xform3m", "k_xform", "k_dstw", "k_dst", "k_dst2", "k_zs1", "k_zs2", "k_zs3", "k_proj_rows", "k_projm",
-    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm"};
+    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm", "k_zsw"};
 
 struct Profiler {
   // stage < ST_COUNT: a stage record; stage = ST_COUNT + k: a record of kernel kind k
@@ -165,6 +165,8 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   PDesc* d_pd = nullptr;     // step-3 two-sided edge projections, one per block
   int nzb = 0;               // owned blocks (entries of d_zb before the global one)
   int* d_own = nullptr;      // per-block ownership flags (step-4 partial residual)
+  int* d_zwo = nullptr;      // step 2 (k_zsw): owned-block indices grouped by system class
+  int zw_cnt[3] = {0, 0, 0}; // blocks per class: complex tables, complex shift, real shift
   int* d_wmask = nullptr;    // block sharding: interface-plane segments this rank writes (k_write_iface)
   int n_pd3 = 0;
   StageDescs s1x, s1y, s3x, s3y, s5r1, s5wx, s6f, s7y, s7x;  // s5r1: R1 and R2; s5wx: WX and WY
@@ -194,6 +196,7 @@ void free_pass(PassPlan& pp) {
   cudaFree(pp.d_own);
   cudaFree(pp.d_wmask);
   cudaFree(pp.d_dst2);
+  cudaFree(pp.d_zwo);
 }
 
 }  // namespace
@@ -538,6 +541,18 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
       zb.push_back(z);
     }
   pp.nzb = (int)zb.size();
+  {  // step 2 with a warp per line: blocks grouped by class (each class one launch, own registers)
+    std::vector<int> ord;
+    for (int cls = 0; cls < 3; ++cls) {
+      pp.zw_cnt[cls] = 0;
+      for (int q = 0; q < pp.nzb; ++q)
+        if ((P->real_z ? (zb[q].pad_ ? 2 : 1) : 0) == cls) { ord.push_back(q); ++pp.zw_cnt[cls]; }
+    }
+    if (!ord.empty()) {
+      CUDA_TRY(cudaMalloc(&pp.d_zwo, sizeof(int) * ord.size()));
+      CUDA_TRY(cudaMemcpy(pp.d_zwo, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice));
+    }
+  }
   stage(pp.s6f, std::move(v)); v.clear();
   // step 7: y-inverse T1[rk][q][l] = sum_m W_y[q][m] MS[rk][m][l];  x-inverse u[rk][y0+q][x0+p] = sum_l W_x[p][l] T1
   for (int j = 0; j < nby; ++j)
@@ -799,7 +814,10 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s, ST_X1S, ST_X1D))) return rc;
   if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s, ST_Y1S, ST_Y1D))) return rc;
   begin(ST_Z1);
-  if (pp.nzb)
+  if (pp.nzb && P->opt.zs_warp && zsw_supported(Nz))  // a warp per z-line, one read and one write of v~
+    CUDA_TRY(kern(K_ZSW, (pp.zw_cnt[0] > 0) + (pp.zw_cnt[1] > 0) + (pp.zw_cnt[2] > 0), [&] {
+      return launch_zsw(pp.d_zb, pp.d_zwo, pp.zw_cnt, P->lpad, P->mpad, R, Nz, P->zt_scaled, bufs, minpiv, st); }));
+  else if (pp.nzb)
     CUDA_TRY(kern(K_ZS1, 1, [&] {
       return launch_zsolve(1, pp.d_zb, pp.nzb, P->lpad, P->mpad, R, Nz, P->zt_scaled, P->t_sig, nullptr, bufs, minpiv,
                            st, P->real_z); }));
@@ -943,6 +961,7 @@ void lfds_default_options(lfds_options* o) {
   o->graph = 0;
   o->plane_dst = 1;
   o->resonance_tol = 1e-13;
+  o->zs_warp = 0;
 }
 
 int lfds_stage_count(void) { return ST_COUNT; }

@@ -177,6 +177,11 @@ cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, in
 cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st);
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
 size_t zsolve_checkpoint_bytes(int nblocks, int max_nx, int max_ny, int R, int nz);
+// step 2 with a warp per z-line (lfds_zsolve.cu k_zsw): d_order = owned-block indices grouped by
+// class (complex z tables, real tables + complex shift, real tables + real shift), counts[3]
+bool zsw_supported(int nz);
+cudaError_t launch_zsw(const ZBlock* d_blocks, const int* d_order, const int counts[3], int max_nx, int max_ny, int R,
+                       int nz, ZTab tab, const Bufs& bufs, double* d_minpiv, cudaStream_t st);
 // resonance margins (lfds_margin.cu): per set, min over (l, m, t) of |ev[lx + l] + ev[ly + m] +
 // theta[t]| as a 64-bit key (float bits << 32 | flat index (t * ny + m) * nx + l) in out[set]
 struct MarginSet {

@@ -32,6 +32,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "lfds_internal.h"
@@ -729,6 +730,279 @@ __global__ void __launch_bounds__(ZT, 3) k_zs3(const ZBlock* __restrict__ blocks
   else zs3_body<1, FULL, TL, NIF>(B, nz, T, G, bufs, wsm, minpiv_out);
 }
 
+// ===================================================================== step 2, warp per line
+// k_zsw: the step-2 systems T_lm v~_lm = f~_lm with ONE read and ONE write of every mode-space
+// value (k_zs1 reads the right side twice: its per-thread lines do not fit on chip, so the
+// backward sweep re-reads them).  A warp solves one z-line held in its registers, Q = 32-row
+// chunks per lane ("partition" form of Thomas, the warp-shuffle PCR/Thomas hybrid of the
+// north_star):
+//   1. each lane eliminates the interior rows of its chunk (Thomas, unpivoted like k_zs1,
+//      reading R15): interior x = y - L X_{t-1} - R X_t, with X_t the lane's last row (the
+//      separator) and y, L, R the chunk solves for the right side and the two coupling spikes;
+//   2. the separators obey a 32-row tridiagonal system (lane t: row X_t, coupled to X_{t-1}
+//      and X_{t+1} through the neighbours' spikes), solved by parallel cyclic reduction over the
+//      lanes with shuffles (5 steps);
+//   3. every lane forms its interior values from X_{t-1} and X_t.
+// Mode tiles (8 consecutive l at one m, all N_z rows: 128-B rows) are staged by coalesced 16-B
+// cp.async copies, NBUF-buffered in a persistent loop (the next tiles land while the current one
+// is solved), and stored back by coalesced rows.  Rows are padded to 9 units and Q is odd, so
+// the 8 lanes of a shared-memory phase (rows tQ + j, t = 0..7) hit 8 different bank groups.
+// (A first version staged each 128-B row with a cp.async.bulk copy on an mbarrier: correct and
+// single-read, but ~10x slower: 512 tiny bulk operations per tile serialise on the copy engine.)
+constexpr int ZW_WARPS = 8, ZW_TL = 8;  // lines (l) per tile = warps per CTA
+
+template <int Q>
+struct ZwTile {  // 16-B units of one tile buffer: rows of 8 complex + 1 pad unit (odd stride)
+  static constexpr int W = ZW_TL + 1;
+  static constexpr int UNITS = W * 32 * Q;
+  __device__ static __forceinline__ int row(int k) { return W * k; }
+};
+
+__device__ __forceinline__ cplx shfl_c(cplx v, int src) {
+  return mk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ double shfl_c(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+// coefficient arithmetic: TC = double for real systems (RT 2: real table and real shift: the
+// pivots, c' and both spikes are real), cplx otherwise; data (right side, y, X) always cplx
+__device__ __forceinline__ cplx cm(double a, cplx b) { return mk(a * b.x, a * b.y); }
+__device__ __forceinline__ cplx cm(cplx a, cplx b) { return a * b; }
+__device__ __forceinline__ double cm(double a, double b) { return a * b; }
+__device__ __forceinline__ double tc_n2(double a) { return a * a; }
+__device__ __forceinline__ double tc_n2(cplx a) { return fma(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ double tc_abs1(double a) { return fabs(a); }
+__device__ __forceinline__ double tc_abs1(cplx a) { return cabs1(a); }
+__device__ __forceinline__ double tc_inv(double r) { return fast_rcp(r); }
+__device__ __forceinline__ cplx tc_inv(cplx r) {
+  const double in = fast_rcp(fma(r.x, r.x, r.y * r.y));
+  return mk(r.x * in, -r.y * in);
+}
+__device__ __forceinline__ double tc_neg(double a) { return -a; }
+__device__ __forceinline__ cplx tc_neg(cplx a) { return mk(-a.x, -a.y); }
+__device__ __forceinline__ double tc_zero(double) { return 0.0; }
+__device__ __forceinline__ cplx tc_zero(cplx) { return mk(0, 0); }
+__device__ __forceinline__ double tc_one(double) { return 1.0; }
+__device__ __forceinline__ cplx tc_one(cplx) { return mk(1, 0); }
+
+// the row coefficients of T_lm (zrow) in the coefficient type
+template <int RT, class TC>
+__device__ __forceinline__ void zrow_tc(const ZTabS& T, int k, int nz, cplx s, TC& a, TC& b, TC& c, double& m2) {
+  if (k >= nz) {  // padding rows: identity, decoupled (row nz-1 has c = 0)
+    a = tc_zero(a); b = tc_one(b); c = tc_zero(c); m2 = 0;
+    return;
+  }
+  cplx ac, bc, cc;
+  zrow<RT>(T, k, s, ac, bc, cc, m2);
+  if constexpr (RT == 2) { a = ac.x; b = bc.x; c = cc.x; }
+  else { a = ac; b = bc; c = cc; }
+}
+
+// one line: lane t owns rows tQ .. tQ+Q-1 (values in x[], from and back into the tile)
+template <int RT, int Q>
+__device__ __forceinline__ float zsw_line(const ZTabS& T, int nz, cplx s, cplx (&x)[Q]) {
+  using TC = typename std::conditional<RT == 2, double, cplx>::type;
+  const int t = threadIdx.x & 31;
+  const int k0 = t * Q;
+  const int J = t < 31 ? Q - 1 : Q;  // interior rows (the last lane has no separator)
+  float minpiv = 1.0f;
+  // ---- 1. interior chunk: Thomas forward elimination (pivot r, c' = c / r) with three right
+  // sides: the data (y, kept in x[]), the spike of X_{t-1} (a_0 e_0: L) and of X_t
+  // (c_{J-1} e_{J-1}: R, whose forward value is just c'_{J-1})
+  TC cp[Q], Lv[Q], Rv[Q];
+  {
+    TC cprev = tc_zero(TC{}), lprev = tc_zero(TC{});
+    cplx dprev = mk(0, 0);
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      if (j < J) {
+        TC a, b, c;
+        double m2;
+        zrow_tc<RT>(T, k0 + j, nz, s, a, b, c, m2);
+        const TC r = j == 0 ? b : b - cm(a, cprev);
+        const TC inv = tc_inv(r);
+        const double bn = tc_abs1(b);
+        minpiv = fminf(minpiv, __fdividef((float)tc_n2(r), (float)fma(bn, bn, m2) + 1e-30f));
+        cp[j] = cm(c, inv);
+        x[j] = cm(inv, j == 0 ? x[j] : x[j] - cm(a, dprev));
+        Lv[j] = j == 0 ? cm(a, inv) : tc_neg(cm(cm(a, lprev), inv));
+        Rv[j] = tc_zero(TC{});
+        cprev = cp[j]; dprev = x[j]; lprev = Lv[j];
+      }
+    }
+    if (J > 0) Rv[J - 1] = cp[J - 1];
+    // back substitution of the three right sides
+#pragma unroll
+    for (int j = Q - 2; j >= 0; --j) {
+      if (j < J - 1) {
+        x[j] = x[j] - cm(cp[j], x[j + 1]);
+        Lv[j] = Lv[j] - cm(cp[j], Lv[j + 1]);
+        Rv[j] = tc_neg(cm(cp[j], Rv[j + 1]));
+      }
+    }
+  }
+  // ---- 2. separator system (lane t < 31: unknown X_t = row tQ + Q - 1), PCR over the lanes
+  const int up = (t + 1) & 31;
+  const cplx yf = shfl_c(x[0], up);
+  const TC Lf = shfl_c(Lv[0], up), Rf = shfl_c(Rv[0], up);
+  TC A = tc_zero(TC{}), Bc = tc_one(TC{}), C = tc_zero(TC{});
+  cplx D = mk(0, 0);
+  if (t < 31) {
+    TC a, b, c;
+    double m2;
+    zrow_tc<RT>(T, k0 + Q - 1, nz, s, a, b, c, m2);
+    // x_{k-1} = y_{Q-2} - L_{Q-2} X_{t-1} - R_{Q-2} X_t ;  x_{k+1} = yf - Lf X_t - Rf X_{t+1}
+    A = tc_neg(cm(a, Lv[Q - 2]));
+    Bc = b - cm(a, Rv[Q - 2]) - cm(c, Lf);
+    C = tc_neg(cm(c, Rf));
+    D = x[Q - 1] - cm(a, x[Q - 2]) - cm(c, yf);
+  }
+  const double bnorm = tc_abs1(A) + tc_abs1(Bc) + tc_abs1(C);
+#pragma unroll
+  for (int dl = 1; dl < 32; dl <<= 1) {
+    const int lo = t - dl, hi = t + dl;
+    const TC Al = shfl_c(A, lo & 31), Bl = shfl_c(Bc, lo & 31), Cl = shfl_c(C, lo & 31);
+    const TC Ah = shfl_c(A, hi & 31), Bh = shfl_c(Bc, hi & 31), Ch = shfl_c(C, hi & 31);
+    const cplx Dl = shfl_c(D, lo & 31), Dh = shfl_c(D, hi & 31);
+    const TC al = lo >= 0 ? tc_neg(cm(A, tc_inv(Bl))) : tc_zero(TC{});
+    const TC ga = hi < 32 ? tc_neg(cm(C, tc_inv(Bh))) : tc_zero(TC{});
+    const TC An = cm(al, Al), Cn = cm(ga, Ch);
+    Bc = Bc + cm(al, Cl) + cm(ga, Ah);
+    D = D + cm(al, Dl) + cm(ga, Dh);
+    A = An;
+    C = Cn;
+  }
+  const cplx X = t < 31 ? cm(tc_inv(Bc), D) : mk(0, 0);
+  if (t < 31 && bnorm > 0) {
+    const float q = (float)(tc_abs1(Bc) / bnorm);
+    minpiv = fminf(minpiv, q * q);
+  }
+  const cplx Xs = shfl_c(X, (t - 1) & 31);
+  const cplx Xl = t > 0 ? Xs : mk(0, 0);
+  // ---- 3. interior values
+#pragma unroll
+  for (int j = 0; j < Q; ++j)
+    if (j < J) x[j] = x[j] - cm(Lv[j], Xl) - cm(Rv[j], X);
+  if (t < 31) x[Q - 1] = X;
+  return minpiv;
+}
+
+// NBUF tile buffers: NBUF - 1 tiles in flight (cp.async) while one is solved.  Persistent grid
+// over the flattened (block, rhs, tile) items of one system class: every SM busy to the end.
+template <int RT, int Q, int NBUF>
+__global__ void __launch_bounds__(ZW_WARPS * 32, RT == 2 ? 2 : 1) k_zsw(const ZBlock* __restrict__ blocks,
+                                                                      const int* __restrict__ order, int nblocks,
+                                                                      int R, int tiles_per, int nz, ZTab tab,
+                                                                      Bufs bufs, double* minpiv_out) {
+  constexpr bool REALZ = RT >= 1;
+  static_assert(Q % 2 == 1, "odd rows per lane: conflict-free chunk reads with the 9-unit row stride");
+  extern __shared__ __align__(16) double2 zsm[];
+  using TT = ZwTile<Q>;
+  const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
+  const ZTabS T = stage_ztab<REALZ>(tab, TAB, nz, zsm);
+  double2* tiles = zsm + ((ztab_slots(nz, REALZ) + 7) & ~7);  // tile buffers after the z table
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t items = (int64_t)nblocks * R * tiles_per;
+  // item -> block, rhs, tile (m-major, 8-wide l tiles); false for the padding items of blocks
+  // smaller than the largest one
+  struct Item { const ZBlock* B; double2* src; int nv, l, m; };
+  auto locate = [&](int64_t it, Item& I) -> bool {
+    const int tile = (int)(it % tiles_per);
+    const int64_t br = it / tiles_per;
+    const int r = (int)(br % R), b = (int)(br / R);
+    const ZBlock& Bk = blocks[order[b]];
+    const int tiles_l = (Bk.nx + ZW_TL - 1) / ZW_TL;
+    const int m = tile / tiles_l, l0 = (tile - m * tiles_l) * ZW_TL;
+    if (m >= Bk.ny) return false;
+    const int64_t nxy = (int64_t)Bk.nx * Bk.ny;
+    I.B = &Bk;
+    I.nv = min(ZW_TL, Bk.nx - l0);
+    I.l = l0;
+    I.m = m;
+    I.src = reinterpret_cast<double2*>(bufs.p[Bk.buf]) + Bk.ms_off + (int64_t)r * nz * nxy + (int64_t)m * Bk.nx + l0;
+    return true;
+  };
+  // coalesced 16-B cp.async loads of an item into buffer `bf`: a warp covers four 128-B rows
+  auto issue = [&](int64_t it, int bf) {
+    Item I;
+    if (it < items && locate(it, I)) {
+      const int64_t nxy = (int64_t)I.B->nx * I.B->ny;
+      double2* dst = tiles + bf * TT::UNITS;
+      for (int idx = threadIdx.x; idx < nz * ZW_TL; idx += ZW_WARPS * 32) {
+        const int k = idx >> 3, w = idx & 7;
+        if (w < I.nv) cp16(dst + TT::row(k) + w, I.src + (int64_t)k * nxy + w);
+      }
+    }
+    cp_commit();
+  };
+  float minpiv = 1.0f;
+  const int64_t it0 = blockIdx.x, G = gridDim.x;
+#pragma unroll
+  for (int q = 0; q < NBUF - 1; ++q) issue(it0 + q * G, q);
+  int n = 0;
+  for (int64_t it = it0; it < items; it += G, ++n) {
+    const int bf = n % NBUF;
+    __syncthreads();  // buffer (n - 1) % NBUF fully stored by the previous iteration
+    issue(it + (NBUF - 1) * G, (n + NBUF - 1) % NBUF);
+    cp_wait<NBUF - 1>();
+    __syncthreads();  // item n visible to every warp
+    Item I;
+    if (!locate(it, I)) continue;
+    const int64_t nxy = (int64_t)I.B->nx * I.B->ny;
+    double2* tb = tiles + bf * TT::UNITS;
+    if (warp < I.nv) {
+      const cplx s = ld(TAB + I.B->lamx + I.l + warp) + ld(TAB + I.B->lamy + I.m);
+      cplx x[Q];
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const int k = lane * Q + j;
+        x[j] = k < nz ? mk(tb[TT::row(k) + warp]) : mk(0, 0);
+      }
+      minpiv = fminf(minpiv, zsw_line<RT, Q>(T, nz, s, x));
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const int k = lane * Q + j;
+        if (k < nz) tb[TT::row(k) + warp] = make_double2(x[j].x, x[j].y);
+      }
+    }
+    __syncthreads();  // the solved tile back in shared memory
+    for (int idx = threadIdx.x; idx < nz * ZW_TL; idx += ZW_WARPS * 32) {
+      const int k = idx >> 3, w = idx & 7;
+      if (w < I.nv) I.src[(int64_t)k * nxy + w] = tb[TT::row(k) + w];
+    }
+  }
+  cp_wait<0>();
+  commit_minpiv(minpiv, minpiv_out);
+}
+
+template <int RT, int Q>
+cudaError_t zsw_launch(const ZBlock* b, const int* order, int nblocks, int max_nx, int max_ny, int R, int nz, ZTab tab,
+                       const Bufs& bufs, double* mp, cudaStream_t st) {
+  constexpr bool REALZ = RT >= 1;
+  constexpr int NBUF = RT == 2 ? 2 : 3;  // 2 CTAs/SM (real: 128 registers) or 1 with 2 tiles in flight
+  const size_t sm = (size_t)(((ztab_slots(nz, REALZ) + 7) & ~7) + NBUF * ZwTile<Q>::UNITS) * sizeof(double2);
+  auto kern = k_zsw<RT, Q, NBUF>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, ZW_WARPS * 32, sm)) != cudaSuccess) return e;
+  const int tiles_per = ((max_nx + ZW_TL - 1) / ZW_TL) * max_ny;
+  const int64_t items = (int64_t)nblocks * R * tiles_per;
+  const int64_t grid = std::min<int64_t>(items, (int64_t)std::max(1, per) * sms);
+  kern<<<(unsigned)grid, ZW_WARPS * 32, sm, st>>>(b, order, nblocks, R, tiles_per, nz, tab, bufs, mp);
+  return cudaGetLastError();
+}
+
+template <int RT>
+cudaError_t zsw_dispatch(const ZBlock* b, const int* order, int nblocks, int max_nx, int max_ny, int R, int nz,
+                         ZTab tab, const Bufs& bufs, double* mp, cudaStream_t st) {
+  if (nblocks <= 0) return cudaSuccess;
+  if (nz <= 96) return zsw_launch<RT, 3>(b, order, nblocks, max_nx, max_ny, R, nz, tab, bufs, mp, st);
+  if (nz <= 160) return zsw_launch<RT, 5>(b, order, nblocks, max_nx, max_ny, R, nz, tab, bufs, mp, st);
+  if (nz <= 288) return zsw_launch<RT, 9>(b, order, nblocks, max_nx, max_ny, R, nz, tab, bufs, mp, st);
+  return zsw_launch<RT, 17>(b, order, nblocks, max_nx, max_ny, R, nz, tab, bufs, mp, st);
+}
+
 // ===================================================================== launch
 int tile_l(int mode, int max_nx, int nif) {
   if (mode == 3 && nif > 8) return 16;  // keeps the 16-row staging of k_zs3 within 2 CTAs/SM
@@ -827,6 +1101,21 @@ cudaError_t launch_zsolve(int mode, const ZBlock* d_blocks, int nblocks, int max
                              : launch_full<true, 16>(mode, grid, st, d_blocks, nz, tab, G, bufs, d_minpiv);
   return tl == 32 ? launch_full<false, 32>(mode, grid, st, d_blocks, nz, tab, G, bufs, d_minpiv)
                   : launch_full<false, 16>(mode, grid, st, d_blocks, nz, tab, G, bufs, d_minpiv);
+}
+
+bool zsw_supported(int nz) { return nz >= 2 && nz <= 544; }
+
+cudaError_t launch_zsw(const ZBlock* d_blocks, const int* d_order, const int counts[3], int max_nx, int max_ny, int R,
+                       int nz, ZTab tab, const Bufs& bufs, double* d_minpiv, cudaStream_t st) {
+  if (R > 65535) return cudaErrorInvalidValue;
+  cudaError_t e;
+  // d_order lists the blocks by class: complex tables (RT 0), real tables with a complex shift
+  // (RT 1), real tables and shift (RT 2)
+  if ((e = zsw_dispatch<0>(d_blocks, d_order, counts[0], max_nx, max_ny, R, nz, tab, bufs, d_minpiv, st))) return e;
+  if ((e = zsw_dispatch<1>(d_blocks, d_order + counts[0], counts[1], max_nx, max_ny, R, nz, tab, bufs, d_minpiv, st)))
+    return e;
+  return zsw_dispatch<2>(d_blocks, d_order + counts[0] + counts[1], counts[2], max_nx, max_ny, R, nz, tab, bufs,
+                         d_minpiv, st);
 }
 
 }  // namespace lfds

@@ -38,7 +38,8 @@ class Options(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("refine", ctypes.c_int), ("refine_tol", ctypes.c_double),
                 ("residual_dd", ctypes.c_int), ("device", ctypes.c_int), ("rhs_chunk", ctypes.c_int),
                 ("profile", ctypes.c_int), ("s5_modal", ctypes.c_int), ("graph", ctypes.c_int),
-                ("plane_dst", ctypes.c_int), ("resonance_tol", ctypes.c_double)]
+                ("plane_dst", ctypes.c_int), ("resonance_tol", ctypes.c_double),
+                ("zs_warp", ctypes.c_int)]
 
 
 class Report(ctypes.Structure):
@@ -133,7 +134,7 @@ class Plan:
                  iface_y: Sequence[int] = (), *, dtype: str = "c128", refine: int = 0,
                  refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0,
                  profile: bool = False, s5_modal: bool = True, graph: bool = False,
-                 plane_dst: bool = True, resonance_tol: float = 1e-13):
+                 plane_dst: bool = True, resonance_tol: float = 1e-13, zs_warp: bool = False):
         opt = Options()
         _lib.lfds_default_options(ctypes.byref(opt))
         opt.dtype = LFDS_F64 if dtype in ("f64", "float64") else LFDS_C128
@@ -143,6 +144,7 @@ class Plan:
         opt.graph = int(bool(graph))
         opt.plane_dst = int(bool(plane_dst))
         opt.resonance_tol = float(resonance_tol)
+        opt.zs_warp = int(bool(zs_warp))
         self.plane_dst = bool(plane_dst)
         self.device = int(device)
         self.has_comm = False

@@ -590,3 +590,31 @@ def test_in_library_nccl_exchange_size1_communicator():
     with pytest.raises(LfdsError):
         pl.solve(f)
     pl.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_warp_per_line_step2_matches_oracle(name):
+    """options.zs_warp: step 2 with a warp per z-line (Thomas on 32 row chunks per line, the
+    chunk separators by parallel cyclic reduction across the lanes, the north_star's
+    warp-shuffle PCR/Thomas hybrid) against the oracle and the thread-per-line solver."""
+    p = shrunken(name)
+    F = p.rhs_all()
+    pw, Uw = gpu_solve(p, F, zs_warp=True)
+    _, Ut = gpu_solve(p, F)
+    assert rel(Uw, Ut) < 1e-11, rel(Uw, Ut)
+    for r in range(p.nrhs):
+        assert_parity(p, Uw[r], oracle.solve_direct(p, oracle.mass_rhs(p, F[r])))
+    assert 0 < pw.report()["min_pivot_ratio"] <= 1
+
+
+@pytest.mark.parametrize("nz", [2, 33, 70, 130, 200, 300])
+def test_warp_per_line_z_lengths(nz):
+    """Every rows-per-lane variant of the warp solver (Q = 3, 5, 9, 17) and ragged tails."""
+    rng = np.random.default_rng(100 + nz)
+    nx, ny = 19, 11
+    hx = rng.uniform(0.5, 2, nx + 1) + 0.3j * rng.uniform(0, 1, nx + 1)
+    hy = rng.uniform(0.5, 2, ny + 1)
+    p = _steps_problem(hx, hy, nz, [9], [5])
+    F = rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape)
+    _, U = gpu_solve(p, F, zs_warp=True)
+    assert_parity(p, U[0], oracle.solve_direct(p, oracle.mass_rhs(p, F[0])))
