@@ -311,6 +311,7 @@ def kernel_algorithmic(p, R: int, plan=None):
         "k_xform3m": (fc or None, bc or None), "k_xform": (fr or None, br or None),
         "k_dstw": (None, (alg["step1_x_sine"][1] or 0) + (alg["step7_x_sine"][1] or 0) or None),
         "k_dst": (None, (alg["step1_y_sine"][1] or 0) + (alg["step7_y_sine"][1] or 0) or None),
+        "k_dstt": (None, (alg["step1_y_sine"][1] or 0) + (alg["step7_y_sine"][1] or 0) or None),
         "k_dst2": (None, (alg["step1_plane_sine"][1] or 0) + (alg["step7_plane_sine"][1] or 0) or None),
         "k_zs1": alg["step2_zsolve"], "k_zsw": alg["step2_zsolve"], "k_zs2": alg["step6_zsolve_lift"],
         "k_proj_rows": alg["step3_edge_projection"],
@@ -490,7 +491,7 @@ def run_ours(args, rank, world, local_rank):
     res_dd = RESIDUAL_DD.get(args.config, True)
     plan = Plan.from_problem(p, device=local_rank, refine=refine, residual_dd=res_dd, profile=True,
                              graph=not blocks, rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0),
-                             plane_dst=bool(args.plane_dst))
+                             plane_dst=bool(args.plane_dst), dst_tma=bool(args.dst_tma))
     setup_s = time.perf_counter() - t0
     info0 = plan.info()
     part = lfds_dist.shard(plan, rank, world) if blocks else None
@@ -762,6 +763,8 @@ def main():
     ap.add_argument("--exchange", choices=["library", "torch"], default="library",
                     help="block sharding: exchanges inside lfds_solve (NCCL, lfds_set_comm) or torch.distributed")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dst-tma", type=int, default=1, choices=[0, 1], dest="dst_tma",
+                    help="1: TMA-fed strided sine passes (options.dst_tma)")
     ap.add_argument("--plane-dst", type=int, default=1, choices=[0, 1], dest="plane_dst",
                     help="1: plane sine transforms on uniform x uniform blocks (options.plane_dst)")
     args = ap.parse_args()

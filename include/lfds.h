@@ -78,10 +78,12 @@ typedef struct {
                     /* cyclic reduction of the chunk separators across the lanes, tiles    */
                     /* staged in shared memory: one read and one write of v~    */
                     /* §6b); 0 (default): a thread per line (k_zs1, measured faster)        */
+  int dst_tma;      /* 1 (default): the strided (y) sine passes load their tiles with TMA   */
+                    /* tensor copies (k_dstt, one tensor map per block); 0: cp.async tiles */
 } lfds_options;
 
 /* Defaults: C128, refine 0, refine_tol 1e-13, residual_dd 1, device 0, rhs_chunk 0, s5_modal 1,
- * graph 0, plane_dst 1, resonance_tol 1e-13, zs_warp 0. */
+ * graph 0, plane_dst 1, resonance_tol 1e-13, zs_warp 0, dst_tma 1. */
 void lfds_default_options(lfds_options* opt);
 
 /*

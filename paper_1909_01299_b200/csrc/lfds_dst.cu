@@ -12,6 +12,7 @@
 // threads run R2-point FFTs.  Only the outputs k = 1..N-1 are kept.  FP64 CUDA-core
 // arithmetic: ~5 L log2 L flops per column instead of the 4 n^2 of the dense real matrix.
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -314,6 +315,175 @@ cudaError_t dst_launch(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& b
     dim3 grid((unsigned)((maxN + CPB - 1) / CPB), 1, (unsigned)nzz);
     k_dst<R1, R2, KC><<<grid, DST_THREADS, sm, st>>>(d + z0, bufs);
   }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- TMA-fed strided variant
+// k_dst for strided columns (y direction) with its tiles moved by the tensor memory
+// accelerator: per descriptor a 3-D tensor map (2 N2 doubles x K rows x N1 planes, the box one
+// 8-column tile of all K rows of one plane), one cp.async.bulk.tensor per tile completing on an
+// mbarrier, NBUF tiles in flight per CTA in a persistent loop over the (descriptor, plane,
+// column-tile) items.  k_dst issues 8 cp.async per thread per tile and its five CTAs per SM
+// meet at their wait_all; here one thread issues one instruction per tile and the FFTs of a
+// tile overlap the copies of the next ones.  Same arithmetic and output order as k_dst.
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int R1, int R2, int NBUF>
+__global__ void __launch_bounds__(DST_THREADS, (R1 <= 16 && R2 <= 16) ? 3 : 1) k_dstt(
+    const GemmDesc* __restrict__ descs, const CUtensorMap* __restrict__ maps, int ndesc, int col_tiles,
+    int tiles_per_desc, Bufs bufs) {
+  constexpr int L = R1 * R2, N = L / 2, n = N - 1;
+  constexpr int CPB = DST_THREADS / R2;
+  constexpr int TILE = n * CPB;                  // dense box [p][col] (a multiple of 128 B)
+  extern __shared__ __align__(16) double2 dsmt[];
+  // tensor-copy destinations must be 128-B aligned: the launch adds 128 B of slack
+  double2* tiles = reinterpret_cast<double2*>(((uintptr_t)dsmt + 127) & ~(uintptr_t)127);  // [NBUF][TILE]
+  double2* ex = tiles + NBUF * TILE;             // [R1][R2][CPB]
+  __shared__ double2 twl[L];
+  __shared__ __align__(8) uint64_t full[NBUF];
+  const int tid = threadIdx.x;
+  const int64_t items = (int64_t)ndesc * tiles_per_desc;
+  if ((int64_t)blockIdx.x >= items) return;
+  {
+    const GemmDesc& D0 = descs[0];
+    for (int j = tid; j < L; j += DST_THREADS) twl[j] = __ldg(reinterpret_cast<const double2*>(bufs.p[B_TAB]) + D0.a_off + j);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < NBUF; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(dsmem_addr(&full[q])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t it, int bf) {
+    if (tid != 0 || it >= items) return;
+    const int d = (int)(it / tiles_per_desc), t = (int)(it % tiles_per_desc);
+    const int plane = t / col_tiles, c0 = (t % col_tiles) * CPB;
+    const CUtensorMap* m = maps + d;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(dsmem_addr(&full[bf])),
+                 "r"((uint32_t)(TILE * 16))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            dsmem_addr(tiles + bf * TILE)),
+        "l"(m), "r"(2 * c0), "r"(0), "r"(plane), "r"(dsmem_addr(&full[bf]))
+        : "memory");
+  };
+  const int64_t G = gridDim.x;
+#pragma unroll
+  for (int q = 0; q < NBUF - 1; ++q) issue(blockIdx.x + q * G, q);
+  const int col = tid % CPB, t = tid / CPB;
+  int k = 0;
+  for (int64_t it = blockIdx.x; it < items; it += G, ++k) {
+    const int bf = k % NBUF;
+    __syncthreads();  // buffer (k - 1) % NBUF and the exchange of tile k - 1 fully consumed
+    issue(it + (NBUF - 1) * G, (k + NBUF - 1) % NBUF);
+    {
+      const uint32_t bar = dsmem_addr(&full[bf]), par = (uint32_t)((k / NBUF) & 1);
+      asm volatile(
+          "{\n\t.reg .pred p;\n"
+          "WAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+          "r"(par)
+          : "memory");
+    }
+    const int d = (int)(it / tiles_per_desc), ti = (int)(it % tiles_per_desc);
+    const GemmDesc& D = descs[d];
+    const int plane = ti / col_tiles, c0 = (ti % col_tiles) * CPB;
+    const double2* tile = tiles + bf * TILE;
+    zc2 a[R1];
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) {
+      const int q = R2 * n1 + t;
+      zc2 v{0, 0};
+      if (q > 0 && q < N) {
+        const double2 w = tile[(q - 1) * CPB + col];
+        v = zc2{w.x, w.y};
+      } else if (q > N) {
+        const double2 w = tile[(L - q - 1) * CPB + col];
+        v = zc2{-w.x, -w.y};
+      }
+      a[n1] = v;
+    }
+    dft_reg<R1, L>(a, twl);
+#pragma unroll
+    for (int k1 = 1; k1 < R1; ++k1) {
+      const double2 w = twl[(t * k1) % L];
+      a[k1] = zmul(a[k1], zc2{w.x, w.y});
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) ex[(k1 * R2 + t) * CPB + col] = make_double2(a[k1].x, a[k1].y);
+    __syncthreads();
+    constexpr int RPT = (R1 + R2 - 1) / R2;
+    zc2 b[RPT][R2];
+#pragma unroll
+    for (int rr = 0; rr < RPT; ++rr) {
+      const int k1 = t + rr * R2;
+      if (k1 < R1) {
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+          const double2 w = ex[(k1 * R2 + n2) * CPB + col];
+          b[rr][n2] = zc2{w.x, w.y};
+        }
+        fft_reg<R2, L>(b[rr], twl);
+      }
+    }
+    const double half = 0.5 * D.scale;
+    double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]);
+    const int64_t n2c = c0 + col;
+    if (n2c < D.N2) {  // strided output rows, straight from registers (a warp writes whole rows)
+      const int64_t o = D.c_off + (int64_t)plane * D.sC1 + n2c * D.sC2;
+#pragma unroll
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int k1 = t + rr * R2;
+        if (k1 < R1) {
+#pragma unroll
+          for (int k2 = 0; k2 < R2 / 2; ++k2) {
+            const int kk = k1 + R1 * k2;
+            if (kk >= 1 && kk < N) C[o + (int64_t)(kk - 1) * D.sCi] = make_double2(-half * b[rr][k2].y, half * b[rr][k2].x);
+          }
+        }
+      }
+    }
+  }
+}
+
+// driver entry point of cuTensorMapEncodeTiled (the runtime links no libcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+template <int R1, int R2>
+cudaError_t dstt_launch(const GemmDesc* d, const void* maps, int ndesc, int maxN2, int maxN1, const Bufs& bufs,
+                        cudaStream_t st) {
+  constexpr int L = R1 * R2, N = L / 2, n = N - 1, CPB = DST_THREADS / R2, NBUF = 2;
+  const size_t sm = (size_t)(NBUF * n * CPB + CPB * R1 * R2) * sizeof(double2) + 128;
+  auto kern = k_dstt<R1, R2, NBUF>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, DST_THREADS, sm)) != cudaSuccess) return e;
+  const int col_tiles = (maxN2 + CPB - 1) / CPB;
+  const int tiles_per_desc = col_tiles * maxN1;
+  const int64_t items = (int64_t)ndesc * tiles_per_desc;
+  const int64_t grid = std::min<int64_t>(items, (int64_t)std::max(1, per) * sms);
+  kern<<<(unsigned)grid, DST_THREADS, sm, st>>>(d, reinterpret_cast<const CUtensorMap*>(maps), ndesc, col_tiles,
+                                                tiles_per_desc, bufs);
   return cudaGetLastError();
 }
 
@@ -699,6 +869,50 @@ cudaError_t launch_dst(const GemmDesc* d_descs, int ndesc, int n, int64_t maxN, 
     default: return cudaErrorInvalidValue;
   }
 #undef DL
+}
+
+// Tensor map of descriptor D's input (strided columns of the y sine passes): 2 N2 doubles x K
+// rows x N1 planes, box = one CPB-column tile of all rows of one plane.  false when the layout
+// is not that one (columns contiguous within a plane, output rows strided) or encoding fails.
+bool dst_tma_encode(const GemmDesc& D, int n, const Bufs& bufs, void* map_out) {
+  EncodeTiledFn enc = encode_tiled();
+  const int L = 2 * (n + 1);
+  const int R2 = L == 16 ? 4 : L == 32 || L == 64 ? 8 : L == 512 ? 32 : 16;
+  const int CPB = DST_THREADS / R2;
+  if (!enc || D.sB2 != 1 || D.sCi == 1 || D.K != n || D.N1 < 1) return false;
+  if ((D.sBj * 16) % 16 || (D.sB1 * 16) % 16) return false;
+  void* base = reinterpret_cast<char*>(bufs.p[D.b_buf]) + D.b_off * 16;
+  if (reinterpret_cast<uintptr_t>(base) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)2 * D.N2, (cuuint64_t)n, (cuuint64_t)D.N1};
+  cuuint64_t strides[2] = {(cuuint64_t)D.sBj * 16, (cuuint64_t)D.sB1 * 16};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * CPB), (cuuint32_t)n, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (D.N1 > 1 && D.sB1 < D.sBj * (int64_t)n) return false;  // planes must not overlap the rows
+  return enc(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool dst_tma_supported(int n) {
+  // measured (profiles/r02/experiments/dstt_*): L = 256 (C4's 127-node blocks) 3.35 -> 3.14 ms
+  // per step; L = 320 (C4j) and L = 32 (C3) slightly slower than the cp.async tiles of k_dst
+  const int L = 2 * (n + 1);
+  return encode_tiled() != nullptr && L == 256;
+}
+
+cudaError_t launch_dst_tma(const GemmDesc* d_descs, const void* d_maps, int ndesc, int n, int maxN2, int maxN1,
+                           const Bufs& bufs, cudaStream_t st) {
+  if (ndesc <= 0) return cudaSuccess;
+  switch (2 * (n + 1)) {
+    case 32: return dstt_launch<4, 8>(d_descs, d_maps, ndesc, maxN2, maxN1, bufs, st);
+    case 64: return dstt_launch<8, 8>(d_descs, d_maps, ndesc, maxN2, maxN1, bufs, st);
+    case 128: return dstt_launch<8, 16>(d_descs, d_maps, ndesc, maxN2, maxN1, bufs, st);
+    case 256: return dstt_launch<16, 16>(d_descs, d_maps, ndesc, maxN2, maxN1, bufs, st);
+#define DT(R1) case 16 * R1: return dstt_launch<R1, 16>(d_descs, d_maps, ndesc, maxN2, maxN1, bufs, st);
+    DT(3) DT(5) DT(6) DT(10) DT(12) DT(20)
+#undef DT
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace lfds

@@ -126,10 +126,10 @@ const char* kStageNames[ST_COUNT] = {
 
 // kernel kinds (per-kernel device time: the roofline of the dominant kernel, bench.py)
 enum Kern { K_XFORM3M, K_XFORM, K_DSTW, K_DST, K_DST2, K_ZS1, K_ZS2, K_ZS3, K_PROJ, K_PROJM, K_S5M, K_IFRES,
-            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_ZSW, K_COUNT };
+            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_ZSW, K_DSTT, K_COUNT };
 const char* kKernNames[K_COUNT] = {
     "k_xform3m", "k_xform", "k_dstw", "k_dst", "k_dst2", "k_zs1", "k_zs2", "k_zs3", "k_proj_rows", "k_projm",
-    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm", "k_zsw"};
+    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm", "k_zsw", "k_dstt"};
 
 struct Profiler {
   // stage < ST_COUNT: a stage record; stage = ST_COUNT + k: a record of kernel kind k
@@ -159,6 +159,16 @@ struct StageDescs {
   int64_t maxN = 0;
 };
 
+// TMA tensor maps of one strided (y) sine group: one 128-B map per descriptor, encoded on the
+// host for the group's current input buffer (a map embeds the address) and copied to the device
+// stream-ordered (from pinned memory: a graph captures the copy)
+struct TmaMaps {
+  void* h = nullptr;         // pinned host maps
+  void* d = nullptr;         // device maps (64-B aligned)
+  const void* key = nullptr; // input buffer the maps were built for
+  bool ok = false;
+};
+
 struct PassPlan {  // descriptors for one (R, in_real, out_real)
   GemmDesc* d_descs = nullptr;
   ZBlock* d_zb = nullptr;
@@ -175,6 +185,8 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   int64_t r1t = 0, r2t = 0, p1t = 0, p2t = 0, p2p = 0;
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
   std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
+  std::vector<GemmDesc> h_descs;                                // host copy of d_descs
+  std::map<int64_t, TmaMaps> tma;                               // y sine groups (by first descriptor)
   // plane sine transforms of uniform x uniform blocks (k_dst2), per length n: forward (step 1)
   // and inverse (step 7) descriptors in d_dst2 [off, off + count)
   struct Dst2Group { int n; int64_t off; int count; };
@@ -190,6 +202,11 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
 };
 
 void free_pass(PassPlan& pp) {
+  for (auto& kv : pp.tma) {
+    cudaFreeHost(kv.second.h);
+    cudaFree(kv.second.d);
+  }
+  pp.tma.clear();
   cudaFree(pp.d_descs);
   cudaFree(pp.d_zb);
   cudaFree(pp.d_pd);
@@ -644,6 +661,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     split(pp.x7c, pp.x7r, pp.x7s, pp.s7x, true, false);
   }
 
+  pp.h_descs = D;
   CUDA_TRY(cudaMalloc(&pp.d_descs, sizeof(GemmDesc) * std::max<size_t>(1, D.size())));
   CUDA_TRY(cudaMemcpy(pp.d_descs, D.data(), sizeof(GemmDesc) * D.size(), cudaMemcpyHostToDevice));
   {  // the step-5 global z-solve as one more 'block': all Nx x Ny global modes, in place in T1
@@ -779,9 +797,39 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     }
     if (sd && !sd->empty()) {
       begin(st_s);
-      for (auto& kv : *sd)
+      for (auto& kv : *sd) {
+        // strided (y) passes: TMA-fed tiles when the maps can be built for this input buffer
+        if (!kcontig && P->opt.dst_tma && dst_tma_supported(kv.first)) {
+          TmaMaps& tm = pp.tma[kv.second.off];
+          const GemmDesc* hd = pp.h_descs.data() + kv.second.off;
+          const void* key = bufs.p[hd[0].b_buf];
+          if (tm.key != key) {
+            const size_t nb = (size_t)kv.second.n * 128;
+            if (!tm.h) {
+              CUDA_TRY(cudaMallocHost(&tm.h, nb));
+              CUDA_TRY(cudaMalloc(&tm.d, nb));
+            }
+            tm.ok = true;
+            int maxN1 = 0, maxN2 = 0;
+            for (int q = 0; q < kv.second.n && tm.ok; ++q) {
+              tm.ok = dst_tma_encode(hd[q], kv.first, bufs, static_cast<char*>(tm.h) + (size_t)q * 128);
+              maxN1 = std::max(maxN1, hd[q].N1);
+              maxN2 = std::max(maxN2, hd[q].N2);
+            }
+            if (tm.ok) CUDA_TRY(cudaMemcpyAsync(tm.d, tm.h, nb, cudaMemcpyHostToDevice, st));
+            tm.key = key;
+          }
+          if (tm.ok) {
+            int maxN1 = 0, maxN2 = 0;
+            for (int q = 0; q < kv.second.n; ++q) { maxN1 = std::max(maxN1, hd[q].N1); maxN2 = std::max(maxN2, hd[q].N2); }
+            CUDA_TRY(kern(K_DSTT, 1, [&] {
+              return launch_dst_tma(pp.d_descs + kv.second.off, tm.d, kv.second.n, kv.first, maxN2, maxN1, bufs, st); }));
+            continue;
+          }
+        }
         CUDA_TRY(kern(kcontig ? K_DSTW : K_DST, nl(kv.second.n), [&] {
           return launch_dst(pp.d_descs + kv.second.off, kv.second.n, kv.first, kv.second.maxN, kcontig, bufs, st); }));
+      }
       end();
     }
     begin(st_d);
@@ -962,6 +1010,7 @@ void lfds_default_options(lfds_options* o) {
   o->plane_dst = 1;
   o->resonance_tol = 1e-13;
   o->zs_warp = 0;
+  o->dst_tma = 1;
 }
 
 int lfds_stage_count(void) { return ST_COUNT; }

@@ -156,6 +156,12 @@ struct Dst2Desc {
   double ax, ay;             // DST-I scales of the two axes (dst_fwd or dst_inv)
 };
 bool dst2_supported(int n);
+// y (strided) sine passes fed by TMA (k_dstt): one 128-byte tensor map per descriptor, built on
+// the host for the descriptor's current input buffer (the map embeds its address)
+bool dst_tma_supported(int n);
+bool dst_tma_encode(const GemmDesc& D, int n, const Bufs& bufs, void* map_out);
+cudaError_t launch_dst_tma(const GemmDesc* d_descs, const void* d_maps, int ndesc, int n, int maxN2, int maxN1,
+                           const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_dst2(const Dst2Desc* d_descs, int ndesc, int n, int nplanes, const Bufs& bufs, cudaStream_t st);
 // z-solves (lfds_zsolve.cu): mode 1 = in place (step 2), 2 = Dirichlet lifting added to v~
 // (step 6), 3 = step-5 global modes with the rank-|I| RHS built from R1/R2 (g != NULL)

@@ -39,7 +39,7 @@ class Options(ctypes.Structure):
                 ("residual_dd", ctypes.c_int), ("device", ctypes.c_int), ("rhs_chunk", ctypes.c_int),
                 ("profile", ctypes.c_int), ("s5_modal", ctypes.c_int), ("graph", ctypes.c_int),
                 ("plane_dst", ctypes.c_int), ("resonance_tol", ctypes.c_double),
-                ("zs_warp", ctypes.c_int)]
+                ("zs_warp", ctypes.c_int), ("dst_tma", ctypes.c_int)]
 
 
 class Report(ctypes.Structure):
@@ -134,7 +134,8 @@ class Plan:
                  iface_y: Sequence[int] = (), *, dtype: str = "c128", refine: int = 0,
                  refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0,
                  profile: bool = False, s5_modal: bool = True, graph: bool = False,
-                 plane_dst: bool = True, resonance_tol: float = 1e-13, zs_warp: bool = False):
+                 plane_dst: bool = True, resonance_tol: float = 1e-13, zs_warp: bool = False,
+                 dst_tma: bool = True):
         opt = Options()
         _lib.lfds_default_options(ctypes.byref(opt))
         opt.dtype = LFDS_F64 if dtype in ("f64", "float64") else LFDS_C128
@@ -145,6 +146,7 @@ class Plan:
         opt.plane_dst = int(bool(plane_dst))
         opt.resonance_tol = float(resonance_tol)
         opt.zs_warp = int(bool(zs_warp))
+        opt.dst_tma = int(bool(dst_tma))
         self.plane_dst = bool(plane_dst)
         self.device = int(device)
         self.has_comm = False
