@@ -495,8 +495,14 @@ def run_ours(args, rank, world, local_rank):
     setup_s = time.perf_counter() - t0
     info0 = plan.info()
     part = lfds_dist.shard(plan, rank, world) if blocks else None
-    if blocks and world > 1 and args.exchange == "library":
-        lfds_dist.attach_nccl(plan, rank, world)  # both exchanges as ncclAllReduce on the solve stream
+    exchange = args.exchange if blocks and world > 1 else None
+    if exchange == "library":
+        try:  # both exchanges as ncclAllReduce on the solve stream, inside lfds_solve
+            lfds_dist.attach_nccl(plan, rank, world)
+        except Exception as exc:  # no usable NCCL in the process: the torch.distributed exchanges
+            print(f"rank {rank}: in-library exchanges unavailable ({exc}); using torch.distributed", file=sys.stderr)
+            exchange = "torch"
+            plan.set_comm(None)
     dt = torch.float64 if p.real else torch.complex128
     # right-hand sides generated one at a time straight into device memory (C5: 64 x 0.84 GB)
     f = torch.empty((nrhs,) + p.shape, dtype=dt, device=dev)
@@ -625,7 +631,7 @@ def run_ours(args, rank, world, local_rank):
                        "refine_passes": refine,
                        "refine_residual": ("double-double" if res_dd else "fp64") if refine else None,
                        "parallelism": (f"block-sharded x{world} (LPT blocks, step-5 modes, 2 NCCL all-reduces, "
-                                       f"{'in-library' if args.exchange == 'library' else 'torch.distributed'})"
+                                       f"{'in-library' if exchange == 'library' else 'torch.distributed'})"
                                        if blocks else f"rhs-sharded x{world}" if world > 1 else "1 gpu"),
                        "l2": "inputs larger than L2 (no flush)" if p.unknowns * 16 > 126e6 else "L2-resident",
                        "setup_s": setup_s, "rel_residual_dd": rel_res,

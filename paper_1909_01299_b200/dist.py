@@ -99,7 +99,12 @@ def attach_nccl(plan, rank: int, world: int, broadcast: Optional[Callable] = Non
     rank joins (lfds_set_comm).  lfds_solve then runs the phases and both all-reduces on the
     solve stream."""
     from .lfds import nccl_unique_id
-    uid = nccl_unique_id() if rank == 0 else bytes(128)
+    uid = bytes(128)
+    if rank == 0:
+        try:
+            uid = nccl_unique_id()
+        except Exception:  # broadcast the empty id anyway: every rank then fails the same way
+            uid = bytes(128)
     if world > 1:
         if broadcast is None:
             import torch
@@ -110,6 +115,8 @@ def attach_nccl(plan, rank: int, world: int, broadcast: Optional[Callable] = Non
             uid = bytes(t.cpu().tolist())
         else:
             uid = broadcast(uid)
+    if uid == bytes(128):
+        raise RuntimeError("no NCCL group id (lfds_nccl_unique_id failed on rank 0)")
     plan.set_comm(uid, rank, world)
     return uid
 
