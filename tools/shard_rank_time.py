@@ -17,7 +17,7 @@ from workloads import make_problem  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
 worlds = [int(a) for a in sys.argv[2:]] or [2, 4, 8]
-BUS_GBS = 400.0  # assumed NCCL all-reduce bus bandwidth on NVLink 5 (nccl-tests class figure)
+BUS_GBS = float(os.environ.get("BUS_GBS", "725"))  # 8-rank NCCL all-reduce bus bandwidth measured on this pool (B200_PROFILING.md)
 p = make_problem(cfg)
 f = torch.from_numpy(p.rhs(0)[None]).cuda()
 u = torch.zeros_like(f)
