@@ -197,7 +197,7 @@ int lfds_residual(lfds_plan* plan, const void* u_dev, const void* f_dev, lfds_z*
  *   lfds_solve_phase(3)
  * lfds_exchange_layout gives each exchange's byte offset inside the workspace and its length
  * in doubles (exchange 1 = the interface residual on the planes, exchange 2 = the step-5
- * correction projected onto the planes).  Afterwards u_dev holds u on this rank's blocks and
+ * correction projected onto the planes; exchange 3 = [R1~, R2~], see lfds_set_formation_rows).  Afterwards u_dev holds u on this rank's blocks and
  * on its segments of the interface planes (the segment of an x-plane in a block row belongs to
  * the owner of the block on its left, of a y-plane in a block column to the owner of the block
  * below, the plane intersections to the rank0 rank); other entries are not written.  Phased
@@ -212,6 +212,16 @@ int lfds_set_partition(lfds_plan* plan, const int* block_owned, int l_begin, int
  * range or when step 5 runs as per-mode z-sweeps.
  */
 int lfds_set_mode_rows(lfds_plan* plan, int m_begin, int m_end);
+/*
+ * Formation split of the z-modal step 5 (after lfds_set_mode_rows): this rank FORMS only the
+ * rows m in [m_begin, m_end) of R1~ = Z^T W_y^T RX and l in [l_begin, l_end) of R2~ (its share of
+ * the plane transforms of the ranks that read the same rows), the other rows are zero, and a
+ * third exchange sums [R1~, R2~] over the ranks (lfds_exchange_layout(3)).  The solve then runs
+ * phase 1, exchange 1, phase 4 (step 5 up to R~), exchange 3, phase 5 (the modal solve and the
+ * projections), exchange 2, phase 3; lfds_solve_phase(2) still runs 4 and 5 together.
+ * m_begin < 0 switches it off.  LFDS_EINVAL without a partition or the z-modal step 5.
+ */
+int lfds_set_formation_rows(lfds_plan* plan, int m_begin, int m_end, int l_begin, int l_end);
 int lfds_exchange_layout(const lfds_plan* plan, int nrhs, int which, size_t* byte_offset, size_t* n_doubles);
 /*
  * In-library exchanges (BASELINE.json north_star: "NCCL over NVLink only for the interface

@@ -182,6 +182,7 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   StageDescs s1x, s1y, s3x, s3y, s5r1, s5wx, s6f, s7y, s7x;  // s5r1: R1 and R2; s5wx: WX and WY
   StageDescs s5zf, s5zi;     // z-modal step 5: R~ = Z^T R (R1, R2) and P = Z P~ (P1, P2), real S
   bool s5m = false;          // step 5 in z-modal form (lfds_modal.cu)
+  bool fsplit = false;       // formation split of R1~ / R2~ (exchange 3 between phases 2a and 2b)
   int64_t r1t = 0, r2t = 0, p1t = 0, p2t = 0, p2p = 0;
   StageDescs x1c, x1r, y1c, y1r, y7c, y7r, x7c, x7r;  // DMMA transform passes (complex / real S)
   std::vector<std::pair<int, StageDescs>> x1s, y1s, y7s, x7s;  // fast sine transforms, per length n
@@ -258,6 +259,10 @@ struct lfds_plan {
   std::vector<char> own;
   int l_begin = 0, l_end = -1, rank0 = 1;
   int m_begin = 0, m_end = -1;  // z-modal step 5: this rank's global y-modes (-1: all)
+  // z-modal step 5, formation split (lfds_set_formation_rows): the rows of R1~ (y-modes) and
+  // R2~ (x-modes) this rank FORMS (plane transform + z-transform); exchange 3 sums them over the
+  // group that shares them, so every rank's k_s5m still reads its whole (m, l) range (-1: off)
+  int fm0 = -1, fm1 = -1, fl0 = -1, fl1 = -1;
   bool sharded = false;
   // in-library exchanges (lfds_set_comm): the NCCL communicator of this rank's group
   NcclComm comm = nullptr;
@@ -440,11 +445,16 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   // (and with a y-mode split of the z-modal step 5, R1 only for the rank's y-modes m)
   const bool msplit = P->sharded && P->m_end >= 0 && P->s5m && !in_real && !out_real;
   const int m0s = msplit ? P->m_begin : 0, m1s = msplit ? P->m_end : Ny;
-  if (nifx && m1s > m0s)
-    v.push_back(gd(Y.Wg + m0s, 1, Ny, m1s - m0s, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1 + m0s, 1, Ny, 0,
+  // (formation split: this rank forms only its share of those rows, exchange 3 completes them)
+  const bool fsplit = P->sharded && P->fm0 >= 0 && P->s5m && !in_real && !out_real;
+  const int mf0 = fsplit ? P->fm0 : m0s, mf1 = fsplit ? P->fm1 : m1s;
+  const int lf0 = fsplit ? P->fl0 : l0s, lf1 = fsplit ? P->fl1 : l1s;
+  pp.fsplit = fsplit;
+  if (nifx && mf1 > mf0)
+    v.push_back(gd(Y.Wg + mf0, 1, Ny, mf1 - mf0, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1 + mf0, 1, Ny, 0,
                    (int)(nifx * RZ), 1, 0));
-  if (nify && l1s > l0s)
-    v.push_back(gd(X.Wg + l0s, 1, Nx, l1s - l0s, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2 + l0s, 1, Nx, 0,
+  if (nify && lf1 > lf0)
+    v.push_back(gd(X.Wg + lf0, 1, Nx, lf1 - lf0, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2 + lf0, 1, Nx, 0,
                    (int)(nify * RZ), 1, 0));
   stage(pp.s5r1, std::move(v)); v.clear();
   // P1, P2 (projections of w^ onto the planes): k_projm, see run_pass
@@ -494,12 +504,12 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   }
   stage(pp.s5wx, std::move(v)); v.clear();
   if (pp.s5m) {  // z-modal step 5: R~[a][r][t][m] = sum_k Z[k][t] R[a][r][k][m]; P = Z P~ (real Z)
-    if (nifx && m1s > m0s)
-      v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r1 + m0s, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.r1t + m0s, Ny,
-                     (int64_t)Nz * Ny, 1, nifx * R, m1s - m0s, 0));
-    if (nify && l1s > l0s)
-      v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r2 + l0s, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.r2t + l0s, Nx,
-                     (int64_t)Nz * Nx, 1, nify * R, l1s - l0s, 0));
+    if (nifx && mf1 > mf0)
+      v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r1 + mf0, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.r1t + mf0, Ny,
+                     (int64_t)Nz * Ny, 1, nifx * R, mf1 - mf0, 0));
+    if (nify && lf1 > lf0)
+      v.push_back(gd(P->t_zt, Nz, 1, Nz, Nz, B_IF, pp.r2 + lf0, Nx, (int64_t)Nz * Nx, 1, B_IF, pp.r2t + lf0, Nx,
+                     (int64_t)Nz * Nx, 1, nify * R, lf1 - lf0, 0));
     stage(pp.s5zf, std::move(v)); v.clear();
     if (nifx && m1s > m0s)  // (y-mode split: P1 rows outside [m0s, m1s) are zeroed in run_pass)
       v.push_back(gd(P->t_zf, Nz, 1, Nz, Nz, B_IF, pp.p1t + m0s, Ny, (int64_t)Nz * Ny, 1, B_IF, pp.p1 + m0s, Ny,
@@ -741,7 +751,7 @@ static int get_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan** o
 // 2 = step 5 on this rank's global x-modes; 4 = plane inverse, pass 2 (steps 6-7).  With block
 // sharding the caller sums exchange 1 ([RX, RY]) over the ranks between phases 1 and 2 and
 // exchange 2 ([P1, P2]) between phases 2 and 4 (lfds_exchange_layout).
-enum { PH_1 = 1, PH_2 = 2, PH_3 = 4, PH_ALL = 7 };
+enum { PH_1 = 1, PH_2A = 2, PH_3 = 4, PH_2B = 8, PH_2 = PH_2A | PH_2B, PH_ALL = 15 };
 static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, int out_dtype, cudaStream_t st,
                     int phases = PH_ALL) {
   const Axis& X = P->ax[0];
@@ -898,14 +908,21 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     end();
   }
   }
-  if ((phases & PH_2) && has_if && pp.s5m) {
+  if ((phases & PH_2A) && has_if && pp.s5m) {
     // step 5, z-modal form: plane transforms (W_y^T, W_x^T), z-modes (Z^T), the modal solve
     // projected onto the planes, back to z (Z) -> exchange 2 = [P1, P2]
+    if (pp.fsplit)  // formation split: rows this rank does not form are zero in exchange 3
+      CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.r1t, 0,
+                               sizeof(double2) * (size_t)(pp.p1t - pp.r1t), st));
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     begin(ST_GFWD);
-    CUDA_TRY(kern(K_XFORM, 1, [&] {
-      return launch_xform(pp.d_descs + pp.s5zf.off, pp.s5zf.n, pp.s5zf.maxM, pp.s5zf.maxN, true, false, bufs, st); }));
-    end(); begin(ST_GSWEEP);
+    if (pp.s5zf.n)
+      CUDA_TRY(kern(K_XFORM, 1, [&] {
+        return launch_xform(pp.d_descs + pp.s5zf.off, pp.s5zf.n, pp.s5zf.maxM, pp.s5zf.maxN, true, false, bufs, st); }));
+    end();
+  }
+  if ((phases & PH_2B) && has_if && pp.s5m) {
+    begin(ST_GSWEEP);
     S5M S{};
     S.nx = Nx; S.ny = Ny; S.nz = Nz; S.R = R; S.nifx = nifx; S.nify = nify;
     S.l_begin = l_begin; S.l_end = l_end; S.nmt = s5m_mtiles(Ny);
@@ -926,7 +943,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
       CUDA_TRY(kern(K_XFORM, 1, [&] {
         return launch_xform(pp.d_descs + pp.s5zi.off, pp.s5zi.n, pp.s5zi.maxM, pp.s5zi.maxN, true, false, bufs, st); }));
     end();
-  } else if ((phases & PH_2) && has_if) {
+  } else if ((phases & PH_2A) && has_if && !pp.s5m) {
     // step 5
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     begin(ST_GSWEEP);
@@ -1806,14 +1823,24 @@ static int solve_sharded_nccl(lfds_plan* P, const void* f_dev, void* u_dev, int 
                               cudaStream_t st) {
   NcclApi& A = nccl();
   int rc;
-  for (int ph = 1; ph <= 3; ++ph) {
-    if ((rc = lfds_solve_phase(P, ph, f_dev, u_dev, nrhs, ws, ws_bytes, st))) return rc;
-    if (ph == 3) break;
+  auto exchange = [&](int which) -> int {
     size_t off = 0, n = 0;
-    if ((rc = lfds_exchange_layout(P, nrhs, ph, &off, &n))) return rc;
+    int e;
+    if ((e = lfds_exchange_layout(P, nrhs, which, &off, &n))) return e;
+    if (!n) return LFDS_OK;
     double* x = reinterpret_cast<double*>(static_cast<char*>(ws) + off);
     const int r = A.all_reduce(x, x, n, NCCL_FLOAT64, NCCL_SUM, P->comm, st);
-    if (r) return fail(LFDS_ENCCL, "ncclAllReduce (exchange %d): %s", ph, A.error_string(r));
+    if (r) return fail(LFDS_ENCCL, "ncclAllReduce (exchange %d): %s", which, A.error_string(r));
+    return LFDS_OK;
+  };
+  // phases 1, 2 (= 2a + 2b), 3 with exchanges 1 and 2; with the formation split 2a, exchange 3
+  // (the ranks' R1~ / R2~ rows), 2b
+  // (phase, exchange after it): 1 -> 1, 2 -> 2, 3;  split: 1 -> 1, 4 -> 3, 5 -> 2, 3
+  const bool split = P->fm0 >= 0;
+  const int phases[4][2] = {{1, 1}, {split ? 4 : 2, split ? 3 : 2}, {split ? 5 : 3, split ? 2 : 0}, {3, 0}};
+  for (int q = 0; q < (split ? 4 : 3); ++q) {
+    if ((rc = lfds_solve_phase(P, phases[q][0], f_dev, u_dev, nrhs, ws, ws_bytes, st))) return rc;
+    if (phases[q][1] && (rc = exchange(phases[q][1]))) return rc;
   }
   return LFDS_OK;
 }
@@ -1829,8 +1856,10 @@ int lfds_set_partition(lfds_plan* P, const int* block_owned, int l_begin, int l_
     P->rank0 = 1;
     P->m_begin = 0;
     P->m_end = -1;
+    P->fm0 = P->fm1 = P->fl0 = P->fl1 = -1;
   } else {
     if (l_begin < 0 || l_end < l_begin || l_end > Nx) return fail(LFDS_EINVAL, "bad x-mode range [%d, %d) of %d", l_begin, l_end, Nx);
+    P->fm0 = P->fm1 = P->fl0 = P->fl1 = -1;
     P->own.assign(block_owned, block_owned + nblk);
     P->sharded = true;
     P->l_begin = l_begin;
@@ -1864,16 +1893,36 @@ int lfds_set_mode_rows(lfds_plan* P, int m_begin, int m_end) {
   return LFDS_OK;
 }
 
+int lfds_set_formation_rows(lfds_plan* P, int m_begin, int m_end, int l_begin, int l_end) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (m_begin < 0) {  // off
+    P->fm0 = P->fm1 = P->fl0 = P->fl1 = -1;
+  } else {
+    if (!P->sharded || !P->s5m)
+      return fail(LFDS_EINVAL, "lfds_set_formation_rows: needs a partitioned plan with the z-modal step 5");
+    if (m_end < m_begin || m_end > P->ax[1].N || l_begin < 0 || l_end < l_begin || l_end > P->ax[0].N)
+      return fail(LFDS_EINVAL, "bad formation rows [%d, %d) x [%d, %d)", m_begin, m_end, l_begin, l_end);
+    P->fm0 = m_begin; P->fm1 = m_end; P->fl0 = l_begin; P->fl1 = l_end;
+  }
+  drop_graph(P);
+  for (auto& kv : P->passes) free_pass(kv.second);
+  P->passes.clear();
+  return LFDS_OK;
+}
+
 int lfds_exchange_layout(const lfds_plan* cp, int nrhs, int which, size_t* byte_offset, size_t* n_doubles) {
   lfds_plan* P = const_cast<lfds_plan*>(cp);
-  if (!P || (which != 1 && which != 2) || !byte_offset || !n_doubles) return fail(LFDS_EINVAL, "bad arguments");
+  if (!P || which < 1 || which > 3 || !byte_offset || !n_doubles) return fail(LFDS_EINVAL, "bad arguments");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
   const int R = chunk_of(P, nrhs);
   if (R != nrhs) return fail(LFDS_EINVAL, "sharded solves take all right-hand sides in one pass (rhs_chunk)");
   PassPlan* pp;
   int rc = get_pass(P, R, P->opt.dtype == LFDS_F64, P->opt.dtype == LFDS_F64, &pp);
   if (rc) return rc;
-  const int64_t lo = which == 1 ? pp->rx : pp->p1, hi = which == 1 ? pp->r1 : pp->gp;  // [RX, RY] / [P1, P2]
+  if (which == 3 && !pp->s5m) { *byte_offset = pp->off_if; *n_doubles = 0; return LFDS_OK; }
+  // [RX, RY] / [P1, P2] / [R1~, R2~]
+  const int64_t lo = which == 1 ? pp->rx : which == 2 ? pp->p1 : pp->r1t;
+  const int64_t hi = which == 1 ? pp->r1 : which == 2 ? pp->gp : pp->p1t;
   *byte_offset = pp->off_if + (size_t)lo * 16;
   *n_doubles = (size_t)(hi - lo) * 2;
   return LFDS_OK;
@@ -1883,7 +1932,7 @@ int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, in
                      void* stream) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
-  if (phase < 1 || phase > 3) return fail(LFDS_EINVAL, "phase must be 1, 2 or 3");
+  if (phase < 1 || phase > 5) return fail(LFDS_EINVAL, "phase must be 1..5");
   if (nrhs < 1 || !f_dev || !u_dev || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
   if (P->opt.refine != 0) return fail(LFDS_EINVAL, "phased (sharded) solves do not refine");
   const int R = chunk_of(P, nrhs);
@@ -1908,7 +1957,8 @@ int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, in
     P->launches = 0;
     CUDA_TRY(launch_fill_minpiv(reinterpret_cast<double*>(b.p[B_RED]), st));
   }
-  if ((rc = run_pass(P, *pp, b, R, dt, dt, st, phase == 1 ? PH_1 : phase == 2 ? PH_2 : PH_3))) return rc;
+  const int ph = phase == 1 ? PH_1 : phase == 2 ? PH_2 : phase == 3 ? PH_3 : phase == 4 ? PH_2A : PH_2B;
+  if ((rc = run_pass(P, *pp, b, R, dt, dt, st, ph))) return rc;
   P->report.passes = 1;
   P->report.n_kernel_launches = P->launches;
   if (phase == 3) {

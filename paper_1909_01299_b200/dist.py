@@ -9,7 +9,8 @@ sine-transform directions ~O(log n)).  The interface step is one exchange: every
 contributions of its own blocks to the residual on the interface planes and the
 residuals are summed over the ranks (exchange 1).  Step 5 is split by global
 x-modes l (and, in the z-modal form, by global y-modes m): each rank handles its (m, l) range and
-the plane projections are summed (exchange 2).
+the plane projections are summed (exchange 2); the plane data R1~ / R2~ that a group of ranks
+reads in common is formed in parts and summed (exchange 3).
 Both sums run either inside the library (attach_nccl: ncclAllReduce on the solve stream, no
 host round trip) or as `torch.distributed.all_reduce` on views of the library workspace
 (`allreduce` can be replaced: tests use an in-process emulation and gloo).
@@ -73,8 +74,11 @@ def mode_grid(world: int, modal: bool) -> tuple:
     return wm, world // wm
 
 
-def shard(plan, rank: int, world: int) -> dict:
-    """Configure `plan` for `rank` of `world` (LPT block ownership, step-5 mode ranges)."""
+def shard(plan, rank: int, world: int, formation: bool = True) -> dict:
+    """Configure `plan` for `rank` of `world` (LPT block ownership, step-5 mode ranges).
+    formation: split the FORMING of R1~ (W_y^T RX and its z-transform) among the ranks that read
+    the same y-modes, and of R2~ among those that read the same x-modes (a third exchange sums
+    the parts); without it every rank of a group forms the same rows (the z-modal step 5 only)."""
     info = plan.info()
     nbx, nby = info["nbx"], info["nby"]
     bx = [plan.basis(0, i) for i in range(nbx)]
@@ -90,7 +94,14 @@ def shard(plan, rank: int, world: int) -> dict:
     if wm > 1:
         m0, m1 = mode_ranges(info["ny"], wm, align=64)[rm]
         plan.set_mode_rows(m0, m1)
-    return {"owner": owner, "l_range": (l0, l1), "m_range": (m0, m1), "costs": costs}
+    fm, fl = (m0, m1), (l0, l1)
+    if formation and world > 1 and info.get("s5_modal", 0):
+        # the W_l ranks of this y-mode group share [m0, m1): rank rl forms part rl; the W_m ranks
+        # of this x-mode group share [l0, l1): rank rm forms part rm
+        fm = tuple(m0 + x for x in mode_ranges(m1 - m0, wl, align=8)[rl])
+        fl = tuple(l0 + x for x in mode_ranges(l1 - l0, wm, align=8)[rm])
+        plan.set_formation_rows(fm[0], fm[1], fl[0], fl[1])
+    return {"owner": owner, "l_range": (l0, l1), "m_range": (m0, m1), "form_m": fm, "form_l": fl, "costs": costs}
 
 
 def attach_nccl(plan, rank: int, world: int, broadcast: Optional[Callable] = None) -> bytes:
@@ -135,7 +146,12 @@ def solve_sharded(plan, f, u, ws, allreduce: Optional[Callable] = None, stream=N
     nrhs = f.shape[0]
     plan.solve_phase(1, f, u, ws, stream)
     allreduce(plan.exchange_view(ws, nrhs, 1))
-    plan.solve_phase(2, f, u, ws, stream)
+    if getattr(plan, "formation", False):  # step 5 in two halves around exchange 3 ([R1~, R2~])
+        plan.solve_phase(4, f, u, ws, stream)
+        allreduce(plan.exchange_view(ws, nrhs, 3))
+        plan.solve_phase(5, f, u, ws, stream)
+    else:
+        plan.solve_phase(2, f, u, ws, stream)
     allreduce(plan.exchange_view(ws, nrhs, 2))
     plan.solve_phase(3, f, u, ws, stream)
     return u

@@ -85,6 +85,7 @@ _lib.lfds_exchange_layout.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POI
                                       ctypes.POINTER(ctypes.c_size_t)]
 _lib.lfds_solve_phase.argtypes = [_P, ctypes.c_int, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
 _lib.lfds_set_mode_rows.argtypes = [_P, ctypes.c_int, ctypes.c_int]
+_lib.lfds_set_formation_rows.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
 _lib.lfds_gmres_workspace_bytes.argtypes = [_P, ctypes.c_int]
 _lib.lfds_gmres_workspace_bytes.restype = ctypes.c_size_t
 _lib.lfds_gmres.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, _P,
@@ -110,7 +111,7 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
             "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
             "lfds_set_mode_rows", "lfds_kernel_count", "lfds_kernel_name", "lfds_kernel_times",
-            "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm"]
+            "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm", "lfds_set_formation_rows"]
 
 
 def _check(rc):
@@ -150,6 +151,7 @@ class Plan:
         self.plane_dst = bool(plane_dst)
         self.device = int(device)
         self.has_comm = False
+        self.formation = False
         self.dtype = opt.dtype
         hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
         sn_, psn = _zarr(sigma_node); se_, pse = _zarr(sigma_edge)
@@ -330,6 +332,7 @@ class Plan:
             own = np.ascontiguousarray(np.asarray(block_owned, dtype=np.int32).ravel())
             _check(_lib.lfds_set_partition(self._h, own.ctypes.data_as(_P), int(l_begin), int(l_end), int(rank0)))
         self._ws = {}
+        self.formation = False
 
     def set_mode_rows(self, m_begin: int, m_end: int):
         """Second split of the z-modal step 5: this rank's global y-modes [m_begin, m_end)."""
@@ -347,6 +350,12 @@ class Plan:
         _check(_lib.lfds_set_comm(self._h, ctypes.cast(buf, _P), int(rank), int(world)))
         self.has_comm = True
 
+    def set_formation_rows(self, m_begin: int, m_end: int, l_begin: int, l_end: int):
+        """Formation split of the z-modal step 5 (exchange 3); m_begin < 0 switches it off."""
+        _check(_lib.lfds_set_formation_rows(self._h, int(m_begin), int(m_end), int(l_begin), int(l_end)))
+        self._ws = {}
+        self.formation = m_begin >= 0
+
     def exchange_view(self, ws, nrhs: int, which: int):
         """float64 view of exchange `which` (1: interface residual, 2: plane projections) in ws."""
         torch = self._torch()
@@ -355,7 +364,8 @@ class Plan:
         return ws[off.value:off.value + 8 * n.value].view(torch.float64)
 
     def solve_phase(self, phase: int, f, u, ws, stream=None):
-        """One phase (1, 2, 3) of a sharded solve; f, u: (nrhs, nz, ny, nx) device tensors."""
+        """One phase of a sharded solve (1, 2, 3; with the formation split 2 = 4 + 5);
+        f, u: (nrhs, nz, ny, nx) device tensors."""
         torch = self._torch()
         st = (stream or torch.cuda.current_stream()).cuda_stream
         _check(_lib.lfds_solve_phase(self._h, int(phase), _P(f.data_ptr()), _P(u.data_ptr()), f.shape[0],

@@ -450,8 +450,15 @@ def test_block_sharded_solve_matches_single_device(name, world):
     for pl, w, u in zip(plans, ws, us):
         pl.solve_phase(1, f, u, w)
     exchange(1)
-    for pl, w, u in zip(plans, ws, us):
-        pl.solve_phase(2, f, u, w)
+    if plans[0].formation:  # z-modal step 5 with its formation split: 4, exchange 3, 5
+        for pl, w, u in zip(plans, ws, us):
+            pl.solve_phase(4, f, u, w)
+        exchange(3)
+        for pl, w, u in zip(plans, ws, us):
+            pl.solve_phase(5, f, u, w)
+    else:
+        for pl, w, u in zip(plans, ws, us):
+            pl.solve_phase(2, f, u, w)
     exchange(2)
     for pl, w, u in zip(plans, ws, us):
         pl.solve_phase(3, f, u, w)
@@ -552,11 +559,13 @@ def test_block_sharded_2d_mode_split_matches_single_device(world):
         for v in views:
             v.copy_(total)
 
-    for phase in (1, 2, 3):
+    # phases 1, 4, 5, 3 with exchanges 1, 3, 2 (formation split of R1~ / R2~)
+    assert all(pl.formation for pl in plans)
+    for phase, which in ((1, 1), (4, 3), (5, 2), (3, 0)):
         for pl, w, u in zip(plans, ws, us):
             pl.solve_phase(phase, f, u, w)
-        if phase < 3:
-            exchange(phase)
+        if which:
+            exchange(which)
     u = sum(us)
     torch.cuda.synchronize()
     # the (m, l) partial sums change the rounding order of the step-5 projections: agreement

@@ -46,8 +46,11 @@ for world in worlds:
         ws = plan.workspace(1)
         xbytes = sum(plan.exchange_view(ws, 1, w).numel() * 8 for w in (1, 2))
 
+        phases = (1, 4, 5, 3) if plan.formation else (1, 2, 3)
+        xbytes = sum(plan.exchange_view(ws, 1, w).numel() * 8 for w in ((1, 2, 3) if plan.formation else (1, 2)))
+
         def run():
-            for ph in (1, 2, 3):
+            for ph in phases:
                 plan.solve_phase(ph, f, u, ws)
         ranks.append(timed(run))
     comm = 2 * (world - 1) / world * xbytes / (BUS_GBS * 1e9) * 1e3  # ring all-reduce volume per rank
@@ -64,12 +67,13 @@ if os.environ.get("SHARD_STAGES"):  # stage breakdown of rank 0 of the largest w
     W = max(worlds)
     dist.shard(pp, 0, W)
     ws = pp.workspace(1)
-    for ph in (1, 2, 3):
+    phs = (1, 4, 5, 3) if pp.formation else (1, 2, 3)
+    for ph in phs:
         pp.solve_phase(ph, f, u, ws)
     torch.cuda.synchronize()
     pp.stage_times()
     for _ in range(3):
-        for ph in (1, 2, 3):
+        for ph in phs:
             pp.solve_phase(ph, f, u, ws)
     torch.cuda.synchronize()
     st = {k: v[0] / 3 for k, v in pp.stage_times().items() if v[1]}
