@@ -294,7 +294,11 @@ def kernel_algorithmic(p, R: int, plan=None):
     nifx, nify = len(p.iface_x), len(p.iface_y)
     plane_el = (nifx * p.ny + nify * p.nx) * nz * R
     if nifx + nify and not p.real:
-        fc += 2 * 8.0 * (nifx * p.ny * p.ny + nify * p.nx * p.nx) * nz * R  # forward + inverse plane transforms
+        # forward + inverse plane transforms; a palindromic global axis contracts folded data at
+        # half length (lfds_info.global_fold: bit 0 x, bit 1 y)
+        gf = plan.info().get("global_fold", 0) if plan else 0
+        fy, fxx = (0.5 if gf & 2 else 1.0), (0.5 if gf & 1 else 1.0)
+        fc += 2 * 8.0 * (nifx * p.ny * p.ny * fy + nify * p.nx * p.nx * fxx) * nz * R
         bc += 2 * 2 * esz * plane_el
         # step 3 edge values (two edge rows per block side) and step 6 face transforms (one per interior face)
         for i in range(len(bx)):

@@ -277,6 +277,9 @@ typedef struct {
   double margin_block, margin_block_rel;    /* the worst block's z-systems (steps 2 and 6)     */
   int margin_block_ij[2];                   /* that block (x index, y index)                   */
   int margin_block_lmt[3];
+  int global_fold;             /* bit 0 / bit 1: the global x / y steps are palindromic, so the  */
+                               /* step-5 plane transforms along that axis run on folded data at  */
+                               /* half length (even / odd modes)                  */
 } lfds_info;
 int lfds_get_info(const lfds_plan* plan, lfds_info* info);
 

@@ -29,6 +29,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <numeric>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -112,6 +113,11 @@ struct Axis {
   std::vector<int> blk_of;  // per node (0-based): block index or -1 (interface)
   Basis G;                  // global basis
   int64_t Wg = 0, lamg = 0, WI = 0, hoff = 0, hhoff = 0;
+  // palindromic steps: every global mode is even or odd under p -> N-1-p (exactly, by the parity
+  // split of the eigensolver); the device tables hold the even modes first (ne of them), so the
+  // step-5 plane transforms fold the data (x_p +- x_{N-1-p}) and contract half-length (§6a)
+  bool gpal = false;
+  int ne = 0;
 };
 
 // one stage per kernel kind (sine = FFT-based DST on uniform blocks, dense = DMMA contraction)
@@ -126,10 +132,10 @@ const char* kStageNames[ST_COUNT] = {
 
 // kernel kinds (per-kernel device time: the roofline of the dominant kernel, bench.py)
 enum Kern { K_XFORM3M, K_XFORM, K_DSTW, K_DST, K_DST2, K_ZS1, K_ZS2, K_ZS3, K_PROJ, K_PROJM, K_S5M, K_IFRES,
-            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_ZSW, K_DSTT, K_COUNT };
+            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_ZSW, K_DSTT, K_FOLD, K_COUNT };
 const char* kKernNames[K_COUNT] = {
     "k_xform3m", "k_xform", "k_dstw", "k_dst", "k_dst2", "k_zs1", "k_zs2", "k_zs3", "k_proj_rows", "k_projm",
-    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm", "k_zsw", "k_dstt"};
+    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm", "k_zsw", "k_dstt", "k_fold"};
 
 struct Profiler {
   // stage < ST_COUNT: a stage record; stage = ST_COUNT + k: a record of kernel kind k
@@ -199,7 +205,9 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   size_t off_ms = 0, off_t1 = 0, off_if = 0, off_red = 0, off_ck = 0, off_res = 0, total = 0;
   int64_t gp = 0;  // step-5 P1 partials per l-chunk
   int64_t g_off = 0, h_off = 0, vx_off = 0, vy_off = 0, rx = 0, ry = 0, r1 = 0, r2 = 0, p1 = 0, p2 = 0, wx = 0,
-          wy = 0, gf = 0;
+          wy = 0, gf = 0, fx = 0, fy = 0;
+  bool foldf[2] = {false, false};  // step-5 forward plane transform folded along y (R1) / x (R2)
+  bool foldi[2] = {false, false};  // plane inverse folded (unsharded only): WX / WY
 };
 
 void free_pass(PassPlan& pp) {
@@ -355,6 +363,9 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   pp.wx = o; o += align4((int64_t)nifx * R * Nz * Ny);
   pp.wy = o; o += align4((int64_t)nify * R * Nz * Nx);
   pp.gf = o; o += align4((int64_t)nblk * 4 * R * P->fpad * Nz);
+  // step-5 fold scratch (palindromic global axes): [sym | anti] halves of the plane data
+  pp.fx = o; o += align4((int64_t)nifx * R * Nz * Ny + nifx * R * Nz);
+  pp.fy = o; o += align4((int64_t)nify * R * Nz * Nx + nify * R * Nz);
   pp.s5m = P->s5m && !in_real && !out_real && s5m_ka(nifx, nify) > 0;
   if (pp.s5m) {
     pp.r1t = o; o += align4((int64_t)nifx * R * Nz * Ny);
@@ -450,19 +461,49 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   const int mf0 = fsplit ? P->fm0 : m0s, mf1 = fsplit ? P->fm1 : m1s;
   const int lf0 = fsplit ? P->fl0 : l0s, lf1 = fsplit ? P->fl1 : l1s;
   pp.fsplit = fsplit;
-  if (nifx && mf1 > mf0)
-    v.push_back(gd(Y.Wg + mf0, 1, Ny, mf1 - mf0, Ny, B_IF, pp.rx, 1, Ny, 0, B_IF, pp.r1 + mf0, 1, Ny, 0,
-                   (int)(nifx * RZ), 1, 0));
-  if (nify && lf1 > lf0)
-    v.push_back(gd(X.Wg + lf0, 1, Nx, lf1 - lf0, Nx, B_IF, pp.ry, 1, Nx, 0, B_IF, pp.r2 + lf0, 1, Nx, 0,
-                   (int)(nify * RZ), 1, 0));
+  // palindromic axis: even modes [0, ne) contract the folded sums x_q + x_{N-1-q} over the first
+  // ceil(N/2) rows, odd modes [ne, N) the differences over the first floor(N/2) rows
+  auto fwd = [&](const Axis& A, int N, int nif, int64_t src, int64_t fold, int64_t dst, int c0, int c1, bool& folded) {
+    if (!nif || c1 <= c0) return;
+    const int64_t rows = (int64_t)nif * RZ;
+    folded = A.gpal && !in_real && !out_real;
+    if (!folded) {
+      v.push_back(gd(A.Wg + c0, 1, N, c1 - c0, N, B_IF, src, 1, N, 0, B_IF, dst + c0, 1, N, 0, (int)rows, 1, 0));
+      return;
+    }
+    const int nh = N / 2, ks = N - nh;
+    const int e0 = c0, e1 = std::min(c1, A.ne), o0 = std::max(c0, A.ne), o1 = c1;
+    if (e1 > e0)
+      v.push_back(gd(A.Wg + e0, 1, N, e1 - e0, ks, B_IF, fold, 1, ks, 0, B_IF, dst + e0, 1, N, 0, (int)rows, 1, 0));
+    if (o1 > o0 && nh > 0)
+      v.push_back(gd(A.Wg + o0, 1, N, o1 - o0, nh, B_IF, fold + rows * ks, 1, nh, 0, B_IF, dst + o0, 1, N, 0, (int)rows,
+                     1, 0));
+  };
+  fwd(Y, Ny, nifx, pp.rx, pp.fx, pp.r1, mf0, mf1, pp.foldf[0]);
+  fwd(X, Nx, nify, pp.ry, pp.fy, pp.r2, lf0, lf1, pp.foldf[1]);
   stage(pp.s5r1, std::move(v)); v.clear();
   // P1, P2 (projections of w^ onto the planes): k_projm, see run_pass
   // w on the planes: WX[a][rk][q] = sum_m W_y[q][m] P1[a][rk][m];  WY[b][rk][p] = sum_l W_x[p][l] P2[b][rk][l]
   std::vector<int> wmask;  // sharded: [x-plane a][block row j], then [y-plane b][block column i]
   if (!P->sharded) {
-    if (nifx) v.push_back(gd(Y.Wg, Ny, 1, Ny, Ny, B_IF, pp.p1, 1, Ny, 0, B_IF, pp.wx, 1, Ny, 0, (int)(nifx * RZ), 1, 0));
-    if (nify) v.push_back(gd(X.Wg, Nx, 1, Nx, Nx, B_IF, pp.p2, 1, Nx, 0, B_IF, pp.wy, 1, Nx, 0, (int)(nify * RZ), 1, 0));
+    // palindromic axis: E = W_even P (first ceil(N/2) rows), O = W_odd P (first floor(N/2)
+    // rows), then w_q = E_q + O_q and w_{N-1-q} = E_q - O_q (k_unfold)
+    auto inv = [&](const Axis& A, int N, int nif, int64_t src, int64_t fold, int64_t dst, bool& folded) {
+      if (!nif) return;
+      const int64_t rows = (int64_t)nif * RZ;
+      folded = A.gpal && !in_real && !out_real;
+      if (!folded) {
+        v.push_back(gd(A.Wg, N, 1, N, N, B_IF, src, 1, N, 0, B_IF, dst, 1, N, 0, (int)rows, 1, 0));
+        return;
+      }
+      const int nh = N / 2, ks = N - nh;
+      v.push_back(gd(A.Wg, N, 1, ks, A.ne, B_IF, src, 1, N, 0, B_IF, fold, 1, ks, 0, (int)rows, 1, 0));
+      if (nh > 0 && N - A.ne > 0)
+        v.push_back(gd(A.Wg + A.ne, N, 1, nh, N - A.ne, B_IF, src + A.ne, 1, N, 0, B_IF, fold + rows * ks, 1, nh, 0,
+                       (int)rows, 1, 0));
+    };
+    inv(Y, Ny, nifx, pp.p1, pp.fx, pp.wx, pp.foldi[0]);
+    inv(X, Nx, nify, pp.p2, pp.fy, pp.wy, pp.foldi[1]);
   } else {
     // Block sharding: a rank needs w on the interface planes only where its own blocks' faces
     // read it (step 6) and where it writes u on the planes (step 7): the segment of x-plane a in
@@ -862,6 +903,24 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     end();
     return LFDS_OK;
   };
+  // step-5 plane data folded for the half-length contractions of palindromic global axes:
+  // forward (before the plane transform) x -> [x_q + x_{N-1-q} | x_q - x_{N-1-q}]; inverse (after)
+  // [E | O] -> w_q = E_q + O_q, w_{N-1-q} = E_q - O_q
+  auto fold_planes = [&](bool forward) -> int {
+    const bool* fl = forward ? pp.foldf : pp.foldi;
+    if (!fl[0] && !fl[1]) return LFDS_OK;
+    if (prof) begin(forward ? ST_GFWD : ST_GPLANE);
+    for (int ax = 0; ax < 2; ++ax) {
+      if (!fl[ax]) continue;
+      const int N = ax == 0 ? Ny : Nx;
+      const int64_t rows = (int64_t)(ax == 0 ? nifx : nify) * R * Nz;
+      const int64_t plane = ax == 0 ? (forward ? pp.rx : pp.wx) : (forward ? pp.ry : pp.wy);
+      const int64_t fold = ax == 0 ? pp.fx : pp.fy;
+      CUDA_TRY(kern(K_FOLD, 1, [&] { return launch_fold(forward, rows, N, plane, fold, bufs, st); }));
+    }
+    if (prof) end();
+    return LFDS_OK;
+  };
   int rc;
   const bool has_if = nifx + nify > 0;
   const int l_begin = P->sharded ? P->l_begin : 0, l_end = P->sharded ? P->l_end : Nx;
@@ -914,6 +973,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     if (pp.fsplit)  // formation split: rows this rank does not form are zero in exchange 3
       CUDA_TRY(cudaMemsetAsync(reinterpret_cast<double2*>(bufs.p[B_IF]) + pp.r1t, 0,
                                sizeof(double2) * (size_t)(pp.p1t - pp.r1t), st));
+    if ((rc = fold_planes(true))) return rc;
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     begin(ST_GFWD);
     if (pp.s5zf.n)
@@ -945,6 +1005,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     end();
   } else if ((phases & PH_2A) && has_if && !pp.s5m) {
     // step 5
+    if ((rc = fold_planes(true))) return rc;
     if ((rc = xform(pp.s5r1, StageDescs{}, pp.s5r1, true, nullptr, ST_GFWD, ST_GFWD))) return rc;
     begin(ST_GSWEEP);
     GSweep g{};
@@ -979,6 +1040,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   if (phases & PH_3) {
   if (has_if) {
     if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
+    if ((rc = fold_planes(false))) return rc;
     begin(ST_FACE);
     // step 6: face transforms (DMMA, complex path)
     if (pp.use_xform && pp.s6f.n) {
@@ -1306,11 +1368,42 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
       }
     }
     if (a.G.n) {
-      a.Wg = T.put(a.G.W);
-      a.lamg = T.put(a.G.lam);
-      std::vector<zc> WI((size_t)a.iface.size() * a.N);
+      const int N = a.N;
+      std::vector<int> perm(N);
+      std::iota(perm.begin(), perm.end(), 0);
+      bool palin = N >= 2;
+      for (int t = 0; t <= N && palin; ++t) palin = a.h[t] == a.h[N - t];
+      a.gpal = false;
+      a.ne = 0;
+      if (palin) {  // classify every column by its exact mirror symmetry
+        std::vector<int> ev, od;
+        bool ok = true;
+        for (int c = 0; c < N && ok; ++c) {
+          int pm = 0;
+          for (int p = 1; p < N / 2; ++p)
+            if (std::abs(a.G.W[(size_t)p * N + c]) > std::abs(a.G.W[(size_t)pm * N + c])) pm = p;
+          const zc w = a.G.W[(size_t)pm * N + c], wm = a.G.W[(size_t)(N - 1 - pm) * N + c];
+          if (w == zc(0)) ok = false;
+          else if (wm == w) ev.push_back(c);
+          else if (wm == -w) od.push_back(c);
+          else ok = false;
+        }
+        if (ok && (int)ev.size() == (N + 1) / 2) {
+          for (int c = 0; c < (int)ev.size(); ++c) perm[c] = ev[c];
+          for (int c = 0; c < (int)od.size(); ++c) perm[ev.size() + c] = od[c];
+          a.gpal = true;
+          a.ne = (int)ev.size();
+        }
+      }
+      std::vector<zc> Wp((size_t)N * N), lp(N);
+      for (int p = 0; p < N; ++p)
+        for (int c = 0; c < N; ++c) Wp[(size_t)p * N + c] = a.G.W[(size_t)p * N + perm[c]];
+      for (int c = 0; c < N; ++c) lp[c] = a.G.lam[perm[c]];
+      a.Wg = T.put(Wp);
+      a.lamg = T.put(lp);
+      std::vector<zc> WI((size_t)a.iface.size() * N);
       for (size_t q = 0; q < a.iface.size(); ++q)
-        for (int l = 0; l < a.N; ++l) WI[q * a.N + l] = a.G.W[(size_t)(a.iface[q] - 1) * a.N + l];
+        for (int l = 0; l < N; ++l) WI[q * N + l] = Wp[(size_t)(a.iface[q] - 1) * N + l];
       a.WI = T.put(WI);
     }
     a.hoff = T.put(a.h);
@@ -1452,6 +1545,7 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
   I.eig_max_biorth = mbio;
   I.device_table_bytes = T.v.size() * sizeof(double2);
   I.s5_modal = P->s5m ? 1 : 0;
+  I.global_fold = (X.gpal ? 1 : 0) | (Y.gpal ? 2 : 0);
   I.n_plane_dst = 0;  // the fused2() rule of build_pass (complex data only)
   if (P->opt.plane_dst && P->opt.dtype != LFDS_F64)
     for (auto& by : Y.blocks)

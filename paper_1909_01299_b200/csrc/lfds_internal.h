@@ -181,6 +181,11 @@ cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int dd, in
                             const void* f, double2* r, int to_f_units, double* d_norms, const Bufs& bufs,
                             cudaStream_t st);
 cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, cudaStream_t st);
+// step-5 folds (palindromic global axes), IF offsets, rows x N plane data:
+//   forward: plane [rows][N] -> fold [rows][ceil(N/2)] sums, then [rows][floor(N/2)] differences
+//   inverse: fold [E | O] -> plane, w_q = E_q + O_q, w_{N-1-q} = E_q - O_q
+cudaError_t launch_fold(bool forward, int64_t rows, int N, int64_t plane, int64_t fold, const Bufs& bufs,
+                        cudaStream_t st);
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
 size_t zsolve_checkpoint_bytes(int nblocks, int max_nx, int max_ny, int R, int nz);
 // step 2 with a warp per z-line (lfds_zsolve.cu k_zsw): d_order = owned-block indices grouped by

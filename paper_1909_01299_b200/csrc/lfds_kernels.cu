@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 namespace lfds {
 
 // ---------------------------------------------------------------- complex helpers
@@ -480,6 +482,57 @@ cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, c
 __global__ void k_fill_one(double* p) { *p = 1.0; }
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st) {
   k_fill_one<<<1, 1, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- step-5 folds
+// A palindromic axis (h_t = h_{N-t}) has only even and odd global modes, W[N-1-q][l] = +-W[q][l]
+// exactly, so sum_q W[q][l] x_q = sum_{q < ceil(N/2)} W[q][l] (x_q + x_{N-1-q}) for even l (the
+// middle row once) and sum_{q < floor(N/2)} W[q][l] (x_q - x_{N-1-q}) for odd l: half-length
+// contractions of the folded data.  k_fold forms the folds, k_unfold recombines the two halves.
+__global__ void k_fold(int64_t rows, int N, const double2* __restrict__ x, double2* __restrict__ s) {
+  const int nh = N / 2, ks = N - nh;
+  double2* a = s + rows * ks;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    const double2* xr = x + i * N;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < ks; q += gridDim.x * blockDim.x) {
+      const double2 u = xr[q];
+      if (q < nh) {
+        const double2 v = xr[N - 1 - q];
+        s[i * ks + q] = make_double2(u.x + v.x, u.y + v.y);
+        a[i * nh + q] = make_double2(u.x - v.x, u.y - v.y);
+      } else {
+        s[i * ks + q] = u;  // middle row of an odd N
+      }
+    }
+  }
+}
+__global__ void k_unfold(int64_t rows, int N, const double2* __restrict__ s, double2* __restrict__ w) {
+  const int nh = N / 2, ks = N - nh;
+  const double2* o = s + rows * ks;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    double2* wr = w + i * N;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < ks; q += gridDim.x * blockDim.x) {
+      const double2 e = s[i * ks + q];
+      if (q < nh) {
+        const double2 d = o[i * nh + q];
+        wr[q] = make_double2(e.x + d.x, e.y + d.y);
+        wr[N - 1 - q] = make_double2(e.x - d.x, e.y - d.y);
+      } else {
+        wr[q] = e;
+      }
+    }
+  }
+}
+
+cudaError_t launch_fold(bool forward, int64_t rows, int N, int64_t plane, int64_t fold, const Bufs& bufs,
+                        cudaStream_t st) {
+  if (rows <= 0 || N < 1) return cudaSuccess;
+  double2* IF = reinterpret_cast<double2*>(bufs.p[B_IF]);
+  const int ks = N - N / 2;
+  const dim3 grid((unsigned)((ks + 127) / 128), (unsigned)std::min<int64_t>(rows, 65535));
+  if (forward) k_fold<<<grid, 128, 0, st>>>(rows, N, IF + plane, IF + fold);
+  else k_unfold<<<grid, 128, 0, st>>>(rows, N, IF + fold, IF + plane);
   return cudaGetLastError();
 }
 

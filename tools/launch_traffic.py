@@ -15,7 +15,7 @@ KINDS = [(r"k_xform3m<", "k_xform3m"), (r"k_xform<", "k_xform"), (r"k_dstw<", "k
          (r"k_dst<", "k_dst"), (r"k_zs1<", "k_zs1"), (r"k_zs2<", "k_zs2"), (r"k_zs3<", "k_zs3"),
          (r"k_proj_rows<|k_proj<", "k_proj_rows"), (r"k_projm", "k_projm"), (r"k_s5m<|k_p2sum", "k_s5m"),
          (r"k_iface_res", "k_iface_res"), (r"k_write_iface", "k_write_iface"), (r"k_gemm", "k_gemm"),
-         (r"k_oz", "k_oz"), (r"k_zsw", "k_zsw")]
+         (r"k_zsw", "k_zsw"), (r"k_fold|k_unfold", "k_fold")]
 
 
 def kind_of(name):
