@@ -1180,6 +1180,7 @@ static int resonance_margins(lfds_plan* P, const std::vector<zc>& za, const std:
   const bool glob = X.G.n > 0 && Y.G.n > 0;
   if (glob) sets.push_back({put(X.G.lam), put(Y.G.lam), X.G.n, Y.G.n});
   const int nz = P->nz, ns = (int)sets.size();
+  (void)cudaGetLastError();  // (stale non-sticky errors of the caller)
   double2 *d_ev = nullptr, *d_th = nullptr;
   MarginSet* d_sets = nullptr;
   unsigned long long* d_out = nullptr;
@@ -1585,6 +1586,7 @@ size_t lfds_workspace_bytes_host(const lfds_plan* P, int nrhs) {
 }
 
 static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, void* ws, size_t ws_bytes, cudaStream_t st) {
+  (void)cudaGetLastError();  // a stale non-sticky error of the caller is not ours to report
   // a partitioned plan computes only its own blocks: whole solves must go through the phases
   if (P->sharded) return fail(LFDS_EINVAL, "partitioned plan: use lfds_solve_phase with the two exchanges");
   const int R = chunk_of(P, nrhs);
@@ -2047,6 +2049,7 @@ int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, in
   b.p[B_IF] = w + pp->off_if;
   b.p[B_RED] = w + pp->off_red;
   b.p[B_CK] = w + pp->off_ck;
+  (void)cudaGetLastError();  // (stale non-sticky errors of the caller)
   if (phase == 1) {
     P->launches = 0;
     CUDA_TRY(launch_fill_minpiv(reinterpret_cast<double*>(b.p[B_RED]), st));

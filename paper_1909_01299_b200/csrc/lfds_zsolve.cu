@@ -977,7 +977,9 @@ template <int RT, int Q>
 cudaError_t zsw_launch(const ZBlock* b, const int* order, int nblocks, int max_nx, int max_ny, int R, int nz, ZTab tab,
                        const Bufs& bufs, double* mp, cudaStream_t st) {
   constexpr bool REALZ = RT >= 1;
-  constexpr int NBUF = RT == 2 ? 2 : 3;  // 2 CTAs/SM (real: 128 registers) or 1 with 2 tiles in flight
+  // 2 CTAs/SM (real: 128 registers) or 1 with 2 tiles in flight; 2 buffers for the longest lines
+  // (Q = 17: 78 KB per tile)
+  constexpr int NBUF = (RT == 2 || Q > 9) ? 2 : 3;
   const size_t sm = (size_t)(((ztab_slots(nz, REALZ) + 7) & ~7) + NBUF * ZwTile<Q>::UNITS) * sizeof(double2);
   auto kern = k_zsw<RT, Q, NBUF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
