@@ -236,6 +236,10 @@ int lfds_exchange_layout(const lfds_plan* plan, int nrhs, int which, size_t* byt
  */
 int lfds_nccl_unique_id(unsigned char* id);  /* id: 128 bytes */
 int lfds_set_comm(lfds_plan* plan, const unsigned char* id, int rank, int world);
+/* Exchange-3 groups (collective over the communicator, ncclCommSplit): ranks with the same
+ * color_m share their y-mode range (R1~ rows), the same color_l their x-mode range (R2~ rows);
+ * exchange 3 then sums each half over its group only.  Without it, over all ranks. */
+int lfds_set_comm_groups(lfds_plan* plan, int color_m, int color_l);
 int lfds_solve_phase(lfds_plan* plan, int phase, const void* f_dev, void* u_dev, int nrhs, void* ws,
                      size_t ws_bytes, void* cuda_stream);
 

@@ -68,6 +68,7 @@ struct NcclApi {
   int (*comm_init_rank)(NcclComm*, int, NcclId, int) = nullptr;
   int (*comm_destroy)(NcclComm) = nullptr;
   int (*all_reduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*comm_split)(NcclComm, int, int, NcclComm*, void*) = nullptr;  // optional (NCCL >= 2.18)
   const char* (*error_string)(int) = nullptr;
 };
 enum { NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
@@ -92,6 +93,7 @@ NcclApi& nccl() {
   api.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t)>(
       dlsym(h, "ncclAllReduce"));
   api.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+  api.comm_split = reinterpret_cast<int (*)(NcclComm, int, int, NcclComm*, void*)>(dlsym(h, "ncclCommSplit"));
   api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_reduce && api.error_string;
   return api;
 }
@@ -275,6 +277,7 @@ struct lfds_plan {
   // in-library exchanges (lfds_set_comm): the NCCL communicator of this rank's group
   NcclComm comm = nullptr;
   int comm_rank = 0, comm_world = 1;
+  NcclComm comm_m = nullptr, comm_l = nullptr;  // exchange-3 groups (same y-mode / x-mode range)
   // pivot monitor of the last solve: copied stream-ordered into pinned host memory at its end
   double* h_piv = nullptr;
   cudaStream_t piv_stream = nullptr;
@@ -1894,10 +1897,11 @@ int lfds_set_comm(lfds_plan* P, const unsigned char* id, int rank, int world) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
   NcclApi& A = nccl();
-  if (P->comm) {
-    if (A.ok) A.comm_destroy(P->comm);
-    P->comm = nullptr;
-  }
+  for (NcclComm* c : {&P->comm_m, &P->comm_l, &P->comm})
+    if (*c) {
+      if (A.ok) A.comm_destroy(*c);
+      *c = nullptr;
+    }
   drop_graph(P);  // a captured sharded graph holds the old communicator's collectives
   if (!id) return LFDS_OK;  // back to caller-driven exchanges
   if (world < 1 || rank < 0 || rank >= world) return fail(LFDS_EINVAL, "bad rank %d of %d", rank, world);
@@ -1909,6 +1913,19 @@ int lfds_set_comm(lfds_plan* P, const unsigned char* id, int rank, int world) {
   if (r) { P->comm = nullptr; return fail(LFDS_ENCCL, "ncclCommInitRank: %s", A.error_string(r)); }
   P->comm_rank = rank;
   P->comm_world = world;
+  return LFDS_OK;
+}
+
+int lfds_set_comm_groups(lfds_plan* P, int color_m, int color_l) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  NcclApi& A = nccl();
+  if (!P->comm) return fail(LFDS_EINVAL, "lfds_set_comm_groups: call lfds_set_comm first");
+  if (!A.comm_split) return fail(LFDS_ENCCL, "ncclCommSplit not available in the loaded NCCL");
+  for (NcclComm* c : {&P->comm_m, &P->comm_l})
+    if (*c) { A.comm_destroy(*c); *c = nullptr; }
+  int r = A.comm_split(P->comm, color_m, P->comm_rank, &P->comm_m, nullptr);
+  if (!r) r = A.comm_split(P->comm, color_l, P->comm_rank, &P->comm_l, nullptr);
+  if (r) return fail(LFDS_ENCCL, "ncclCommSplit: %s", A.error_string(r));
   return LFDS_OK;
 }
 
@@ -1925,6 +1942,17 @@ static int solve_sharded_nccl(lfds_plan* P, const void* f_dev, void* u_dev, int 
     if ((e = lfds_exchange_layout(P, nrhs, which, &off, &n))) return e;
     if (!n) return LFDS_OK;
     double* x = reinterpret_cast<double*>(static_cast<char*>(ws) + off);
+    if (which == 3 && P->comm_m && P->comm_l) {
+      // R1~ rows are shared by the ranks of a y-mode group, R2~ rows by an x-mode group: each
+      // half summed over its own group only (the rows outside a group's range are zero there)
+      PassPlan* pp;
+      if ((e = get_pass(P, nrhs, 0, 0, &pp))) return e;
+      const size_t n1 = (size_t)(pp->r2t - pp->r1t) * 2;
+      int r = A.all_reduce(x, x, n1, NCCL_FLOAT64, NCCL_SUM, P->comm_m, st);
+      if (!r) r = A.all_reduce(x + n1, x + n1, n - n1, NCCL_FLOAT64, NCCL_SUM, P->comm_l, st);
+      if (r) return fail(LFDS_ENCCL, "ncclAllReduce (exchange 3): %s", A.error_string(r));
+      return LFDS_OK;
+    }
     const int r = A.all_reduce(x, x, n, NCCL_FLOAT64, NCCL_SUM, P->comm, st);
     if (r) return fail(LFDS_ENCCL, "ncclAllReduce (exchange %d): %s", which, A.error_string(r));
     return LFDS_OK;
@@ -2232,7 +2260,9 @@ int lfds_get_basis(const lfds_plan* P, int axis, int block, int* n, int* kind, i
 
 void lfds_destroy(lfds_plan* P) {
   if (!P) return;
-  if (P->comm && nccl().ok) nccl().comm_destroy(P->comm);
+  if (nccl().ok)
+    for (NcclComm c : {P->comm_m, P->comm_l, P->comm})
+      if (c) nccl().comm_destroy(c);
   for (auto& kv : P->passes) {
     free_pass(kv.second);
   }

@@ -101,7 +101,8 @@ def shard(plan, rank: int, world: int, formation: bool = True) -> dict:
         fm = tuple(m0 + x for x in mode_ranges(m1 - m0, wl, align=8)[rl])
         fl = tuple(l0 + x for x in mode_ranges(l1 - l0, wm, align=8)[rm])
         plan.set_formation_rows(fm[0], fm[1], fl[0], fl[1])
-    return {"owner": owner, "l_range": (l0, l1), "m_range": (m0, m1), "form_m": fm, "form_l": fl, "costs": costs}
+    return {"owner": owner, "l_range": (l0, l1), "m_range": (m0, m1), "form_m": fm, "form_l": fl, "costs": costs,
+            "grid": (rm, rl)}
 
 
 def attach_nccl(plan, rank: int, world: int, broadcast: Optional[Callable] = None) -> bytes:
@@ -129,6 +130,11 @@ def attach_nccl(plan, rank: int, world: int, broadcast: Optional[Callable] = Non
     if uid == bytes(128):
         raise RuntimeError("no NCCL group id (lfds_nccl_unique_id failed on rank 0)")
     plan.set_comm(uid, rank, world)
+    if getattr(plan, "formation", False) and world > 1:
+        # exchange 3 within the groups that share R1~ rows (same y-mode range) / R2~ rows
+        info = plan.info()
+        wm, wl = mode_grid(world, bool(info.get("s5_modal", 0)))
+        plan.set_comm_groups(rank // wl, rank % wl)
     return uid
 
 

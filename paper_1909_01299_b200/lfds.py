@@ -103,6 +103,7 @@ _lib.lfds_kernel_times.argtypes = [_P, _P, _P]
 _lib.lfds_fp64_peak.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
 _lib.lfds_nccl_unique_id.argtypes = [_P]
 _lib.lfds_set_comm.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int]
+_lib.lfds_set_comm_groups.argtypes = [_P, ctypes.c_int, ctypes.c_int]
 _lib.lfds_last_error.restype = ctypes.c_char_p
 _lib.lfds_version.restype = ctypes.c_char_p
 
@@ -112,7 +113,8 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
             "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
             "lfds_set_mode_rows", "lfds_kernel_count", "lfds_kernel_name", "lfds_kernel_times",
-            "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm", "lfds_set_formation_rows"]
+            "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm", "lfds_set_formation_rows",
+            "lfds_set_comm_groups"]
 
 
 def _check(rc):
@@ -356,6 +358,10 @@ class Plan:
         _check(_lib.lfds_set_formation_rows(self._h, int(m_begin), int(m_end), int(l_begin), int(l_end)))
         self._ws = {}
         self.formation = m_begin >= 0
+
+    def set_comm_groups(self, color_m: int, color_l: int):
+        """Exchange-3 groups of the in-library communicator (collective; lfds_set_comm_groups)."""
+        _check(_lib.lfds_set_comm_groups(self._h, int(color_m), int(color_l)))
 
     def exchange_view(self, ws, nrhs: int, which: int):
         """float64 view of exchange `which` (1: interface residual, 2: plane projections) in ws."""

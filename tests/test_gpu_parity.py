@@ -599,6 +599,15 @@ def test_in_library_nccl_exchange_size1_communicator():
     assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) < 1e-12
     assert_parity(p, u.cpu().numpy()[0], oracle.solve_direct(p, oracle.mass_rhs(p, F[0])))
     assert 0 < pl.report()["min_pivot_ratio"] <= 1
+    # the formation split (phases 4 / 5 around exchange 3) through split sub-communicators
+    nb = pl.info()
+    pl.set_formation_rows(0, nb["ny"], 0, nb["nx"])
+    dist.attach_nccl(pl, 0, 1)
+    pl.set_comm_groups(0, 0)
+    u2 = torch.zeros_like(f)
+    dist.solve_sharded(pl, f, u2, pl.workspace(1))
+    torch.cuda.synchronize()
+    assert rel(u2.cpu().numpy(), u_ref.cpu().numpy()) < 1e-12
     pl.set_comm(None)
     with pytest.raises(LfdsError):
         pl.solve(f)

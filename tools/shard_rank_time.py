@@ -53,7 +53,17 @@ for world in worlds:
             for ph in phases:
                 plan.solve_phase(ph, f, u, ws)
         ranks.append(timed(run))
-    comm = 2 * (world - 1) / world * xbytes / (BUS_GBS * 1e9) * 1e3  # ring all-reduce volume per rank
+    # ring all-reduce volume per rank: exchanges 1 and 2 over all ranks; exchange 3 (formation
+    # split) within its groups (R1~ over the W_l ranks of a y-mode group, R2~ over the W_m of an
+    # x-mode group: lfds_set_comm_groups)
+    x12 = sum(plan.exchange_view(ws, 1, w).numel() * 8 for w in (1, 2))
+    comm = 2 * (world - 1) / world * x12 / (BUS_GBS * 1e9) * 1e3
+    if plan.formation:
+        wm, wl = dist.mode_grid(world, True)
+        inf = plan.info()
+        x3m = inf["n_if_x"] * inf["nz"] * inf["ny"] * 16  # R1~ bytes (one right-hand side)
+        x3l = inf["n_if_y"] * inf["nz"] * inf["nx"] * 16  # R2~ bytes
+        comm += (2 * (wl - 1) / wl * x3m + 2 * (wm - 1) / wm * x3l) / (BUS_GBS * 1e9) * 1e3
     est = max(ranks) + comm
     out["worlds"][world] = {"rank_ms": [round(x, 3) for x in ranks], "max_rank_ms": max(ranks),
                             "exchange_bytes": xbytes, "comm_ms_est": comm, "step_ms_est": est,
