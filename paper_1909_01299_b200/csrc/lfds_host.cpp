@@ -167,14 +167,18 @@ struct StageDescs {
   int64_t maxN = 0;
 };
 
-// TMA tensor maps of one strided (y) sine group: one 128-B map per descriptor, encoded on the
-// host for the group's current input buffer (a map embeds the address) and copied to the device
-// stream-ordered (from pinned memory: a graph captures the copy)
+// TMA tensor maps of one strided (y) sine group: one 128-B map per descriptor.  A map embeds the
+// address of its input buffer, so every input buffer (i.e. every workspace the plan has solved
+// with) gets its own pinned host copy and device copy, encoded once and uploaded stream-ordered
+// once; nothing is overwritten afterwards (concurrent solves on other workspaces and captured
+// graphs keep reading their own maps)
 struct TmaMaps {
-  void* h = nullptr;         // pinned host maps
-  void* d = nullptr;         // device maps (64-B aligned)
-  const void* key = nullptr; // input buffer the maps were built for
-  bool ok = false;
+  struct Ent {
+    void* h = nullptr;       // pinned host maps
+    void* d = nullptr;       // device maps
+    bool ok = false;
+  };
+  std::map<const void*, Ent> by_key;  // input buffer -> its maps
 };
 
 struct PassPlan {  // descriptors for one (R, in_real, out_real)
@@ -213,10 +217,11 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
 };
 
 void free_pass(PassPlan& pp) {
-  for (auto& kv : pp.tma) {
-    cudaFreeHost(kv.second.h);
-    cudaFree(kv.second.d);
-  }
+  for (auto& kv : pp.tma)
+    for (auto& e : kv.second.by_key) {
+      cudaFreeHost(e.second.h);
+      cudaFree(e.second.d);
+    }
   pp.tma.clear();
   cudaFree(pp.d_descs);
   cudaFree(pp.d_zb);
@@ -854,25 +859,21 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
       for (auto& kv : *sd) {
         // strided (y) passes: TMA-fed tiles when the maps can be built for this input buffer
         if (!kcontig && P->opt.dst_tma && dst_tma_supported(kv.first)) {
-          TmaMaps& tm = pp.tma[kv.second.off];
           const GemmDesc* hd = pp.h_descs.data() + kv.second.off;
           const void* key = bufs.p[hd[0].b_buf];
-          if (tm.key != key) {
+          auto found = pp.tma[kv.second.off].by_key.find(key);
+          if (found == pp.tma[kv.second.off].by_key.end()) {
+            TmaMaps::Ent e;
             const size_t nb = (size_t)kv.second.n * 128;
-            if (!tm.h) {
-              CUDA_TRY(cudaMallocHost(&tm.h, nb));
-              CUDA_TRY(cudaMalloc(&tm.d, nb));
-            }
-            tm.ok = true;
-            int maxN1 = 0, maxN2 = 0;
-            for (int q = 0; q < kv.second.n && tm.ok; ++q) {
-              tm.ok = dst_tma_encode(hd[q], kv.first, bufs, static_cast<char*>(tm.h) + (size_t)q * 128);
-              maxN1 = std::max(maxN1, hd[q].N1);
-              maxN2 = std::max(maxN2, hd[q].N2);
-            }
-            if (tm.ok) CUDA_TRY(cudaMemcpyAsync(tm.d, tm.h, nb, cudaMemcpyHostToDevice, st));
-            tm.key = key;
+            CUDA_TRY(cudaMallocHost(&e.h, nb));
+            CUDA_TRY(cudaMalloc(&e.d, nb));
+            e.ok = true;
+            for (int q = 0; q < kv.second.n && e.ok; ++q)
+              e.ok = dst_tma_encode(hd[q], kv.first, bufs, static_cast<char*>(e.h) + (size_t)q * 128);
+            if (e.ok) CUDA_TRY(cudaMemcpyAsync(e.d, e.h, nb, cudaMemcpyHostToDevice, st));
+            found = pp.tma[kv.second.off].by_key.emplace(key, e).first;
           }
+          const TmaMaps::Ent& tm = found->second;
           if (tm.ok) {
             int maxN1 = 0, maxN2 = 0;
             for (int q = 0; q < kv.second.n; ++q) { maxN1 = std::max(maxN1, hd[q].N1); maxN2 = std::max(maxN2, hd[q].N2); }

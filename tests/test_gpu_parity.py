@@ -640,3 +640,31 @@ def test_warp_per_line_z_lengths(nz):
     F = rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape)
     _, U = gpu_solve(p, F, zs_warp=True)
     assert_parity(p, U[0], oracle.solve_direct(p, oracle.mass_rhs(p, F[0])))
+
+
+def test_tma_sine_maps_per_workspace_concurrent_host_solves():
+    """The TMA-fed y sine passes (L = 256: 127-node uniform blocks) embed their input buffer's
+    address in per-workspace tensor maps: solves on three workspaces in flight on three streams
+    (lfds_solve_host_async, as the e2e measurement runs them) each equal the device solve, and a
+    graph replay after them still uses its own maps."""
+    from paper_1909_01299_b200 import Plan
+    from workloads.configs import axis_steps
+    h = axis_steps(223, 0, 1.0, 16, "const")  # 16 PML + 223 core + 16 PML = 255 nodes
+    p = _steps_problem(h, h, 6, [127], [127])
+    rng = np.random.default_rng(7)
+    F = [rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape) for _ in range(3)]
+    plan = Plan.from_problem(p, graph=True)
+    assert plan.basis(0, 1)[2] == 0  # the second block along x is uniform: a sine block of 127
+    refs = [plan.solve(torch.from_numpy(Fi).cuda()).cpu() for Fi in F]
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    fh = [torch.from_numpy(Fi).pin_memory() for Fi in F]
+    uh = [torch.empty_like(x).pin_memory() for x in fh]
+    for rep in range(2):
+        for i in range(3):
+            plan.solve_host(fh[i], out=uh[i], stream=streams[i], sync=False, slot=i)
+        torch.cuda.synchronize()
+        for i in range(3):
+            assert torch.equal(uh[i], refs[i]), (rep, i)
+    again = plan.solve(torch.from_numpy(F[0]).cuda()).cpu()
+    assert torch.equal(again, refs[0])
+    assert_parity(p, refs[0].numpy()[0], oracle.solve_direct(p, oracle.mass_rhs(p, F[0][0])))
