@@ -649,8 +649,8 @@ def test_tma_sine_maps_per_workspace_concurrent_host_solves():
     graph replay after them still uses its own maps."""
     from paper_1909_01299_b200 import Plan
     from workloads.configs import axis_steps
-    h = axis_steps(223, 0, 1.0, 16, "const")  # 16 PML + 223 core + 16 PML = 255 nodes
-    p = _steps_problem(h, h, 6, [127], [127])
+    h = axis_steps(143, 0, 1.0, 8, "const")  # 8 PML + 143 core + 8 PML = 159 nodes
+    p = _steps_problem(h, h, 6, [16, 144], [16, 144])  # the middle block: 127 core nodes
     rng = np.random.default_rng(7)
     F = [rng.standard_normal((1,) + p.shape) + 1j * rng.standard_normal((1,) + p.shape) for _ in range(3)]
     plan = Plan.from_problem(p, graph=True)
