@@ -58,7 +58,8 @@ typedef struct {
   int residual_dd;  /* 1: refinement residual in double-double (reading R13), 0: fp64      */
   int device;       /* CUDA device ordinal; <0 = host-only plan (setup/basis queries only) */
   int rhs_chunk;    /* max right-hand sides processed per pipeline pass (0 = all)          */
-  int profile;      /* 1: record CUDA events around every stage on the solve stream        */
+  int profile;      /* 1: record CUDA events around every stage on the solve stream;       */
+                    /* 2: also around every launch, per kernel kind (lfds_kernel_times)    */
   int s5_modal;     /* 1: step 5 with the z direction diagonalised too, when the z tables  */
                     /* are real (interface-only computation, no z sweeps);  */
                     /* 0: per-mode tridiagonal z-sweeps (the paper's form)   */
@@ -306,10 +307,11 @@ const char* lfds_stage_name(int stage);
 int lfds_stage_times(lfds_plan* plan, double* ms, int* launches);
 
 /*
- * Kernel timing (options.profile = 1): the same CUDA-event accounting per kernel KIND
+ * Kernel timing (options.profile = 2): the same CUDA-event accounting per kernel KIND
  * (k_xform3m, k_zs1, ...; names from lfds_kernel_name), events recorded around every launch
  * of that kind on the solve stream; accumulated since the previous call, which resets them.
  */
+int lfds_set_profile(lfds_plan* plan, int level);  /* 0, 1 or 2 (options.profile) for later solves */
 int lfds_kernel_count(void);
 const char* lfds_kernel_name(int kernel);
 int lfds_kernel_times(lfds_plan* plan, double* ms, int* launches);

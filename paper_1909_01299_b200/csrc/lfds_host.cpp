@@ -810,6 +810,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   const int nblk = P->nbx * P->nby;
   double* minpiv = reinterpret_cast<double*>(bufs.p[B_RED]);
   const bool prof = P->opt.profile != 0;
+  const bool kprof = P->opt.profile >= 2;  // per-kernel-kind events too
   int cur_stage = -1, cur_launch0 = 0;
   cudaEvent_t ev_a = nullptr;
   auto begin = [&](int stg) {
@@ -828,10 +829,10 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   // kernel-kind events (inside the stage events): device time per kernel kind, `n` launches
   auto kern = [&](int k, int n, auto&& launch) -> cudaError_t {
     cudaEvent_t a = nullptr;
-    if (prof) { a = P->prof.get(); prof_record(a, st); }
+    if (kprof) { a = P->prof.get(); prof_record(a, st); }
     const cudaError_t e = launch();
     P->launches += n;
-    if (prof) {
+    if (kprof) {
       cudaEvent_t b = P->prof.get();
       prof_record(b, st);
       P->prof.recs.push_back({ST_COUNT + k, n, a, b});
@@ -1139,6 +1140,14 @@ int lfds_stage_times(lfds_plan* P, double* ms, int* launches) {
     P->prof.ms[i] = 0;
     P->prof.launches[i] = 0;
   }
+  return LFDS_OK;
+}
+
+int lfds_set_profile(lfds_plan* P, int level) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (level < 0 || level > 2) return fail(LFDS_EINVAL, "profile level must be 0, 1 or 2");
+  if (level != P->opt.profile) drop_graph(P);  // the captured graph holds the old event nodes
+  P->opt.profile = level;
   return LFDS_OK;
 }
 
@@ -1645,18 +1654,21 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         const bool auto_mode = P->opt.refine < 0;
         if (auto_mode) CUDA_TRY(cudaMemsetAsync(norms, 0, sizeof(double) * 2 * Rc, st));
         cudaEvent_t ra = nullptr, ra2 = nullptr, rb2k = nullptr;  // stage and kernel-kind events
-        if (P->opt.profile) { ra = P->prof.get(); prof_record(ra, st); ra2 = P->prof.get(); prof_record(ra2, st); }
+        if (P->opt.profile) { ra = P->prof.get(); prof_record(ra, st); }
+        if (P->opt.profile >= 2) { ra2 = P->prof.get(); prof_record(ra2, st); }
         CUDA_TRY(launch_residual(X.N, Y.N, P->nz, Rc, dt, P->opt.residual_dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff,
                                  Y.hhoff, P->t_hhz, P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()),
                                  P->t_dd, b.p[B_U], b.p[B_F], res, 1, auto_mode ? norms : nullptr, b, st));
         P->launches++;
-        if (P->opt.profile) {
+        if (P->opt.profile >= 2) {
           rb2k = P->prof.get();
           prof_record(rb2k, st);
+          P->prof.recs.push_back({ST_COUNT + K_RESID, 1, ra2, rb2k});
+        }
+        if (P->opt.profile) {
           cudaEvent_t rb2 = P->prof.get();
           prof_record(rb2, st);
           P->prof.recs.push_back({ST_RESID, 1, ra, rb2});
-          P->prof.recs.push_back({ST_COUNT + K_RESID, 1, ra2, rb2k});
         }
         double worst = -1.0;
         if (auto_mode) {
@@ -1680,16 +1692,19 @@ static int solve_impl(lfds_plan* P, const void* f_dev, void* u_dev, int nrhs, vo
         rb.p[B_CK] = w + pp_ref->off_ck;
         if ((rc = run_pass(P, *pp_ref, rb, Rc, 0, 0, st))) return rc;
         cudaEvent_t xa = nullptr, xa2 = nullptr, xb2 = nullptr;
-        if (P->opt.profile) { xa = P->prof.get(); prof_record(xa, st); xa2 = P->prof.get(); prof_record(xa2, st); }
+        if (P->opt.profile) { xa = P->prof.get(); prof_record(xa, st); }
+        if (P->opt.profile >= 2) { xa2 = P->prof.get(); prof_record(xa2, st); }
         CUDA_TRY(launch_axpy_u(vol * Rc, dt, res, b.p[B_U], st));
         P->launches++;
-        if (P->opt.profile) {
+        if (P->opt.profile >= 2) {
           xb2 = P->prof.get();
           prof_record(xb2, st);
+          P->prof.recs.push_back({ST_COUNT + K_AXPY, 1, xa2, xb2});
+        }
+        if (P->opt.profile) {
           cudaEvent_t xb = P->prof.get();
           prof_record(xb, st);
           P->prof.recs.push_back({ST_AXPY, 1, xa, xb});
-          P->prof.recs.push_back({ST_COUNT + K_AXPY, 1, xa2, xb2});
         }
         passes++;
       }

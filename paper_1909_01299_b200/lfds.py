@@ -100,6 +100,7 @@ _lib.lfds_kernel_count.restype = ctypes.c_int
 _lib.lfds_kernel_name.argtypes = [ctypes.c_int]
 _lib.lfds_kernel_name.restype = ctypes.c_char_p
 _lib.lfds_kernel_times.argtypes = [_P, _P, _P]
+_lib.lfds_set_profile.argtypes = [_P, ctypes.c_int]
 _lib.lfds_fp64_peak.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
 _lib.lfds_nccl_unique_id.argtypes = [_P]
 _lib.lfds_set_comm.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int]
@@ -114,7 +115,7 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
             "lfds_set_mode_rows", "lfds_kernel_count", "lfds_kernel_name", "lfds_kernel_times",
             "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm", "lfds_set_formation_rows",
-            "lfds_set_comm_groups"]
+            "lfds_set_comm_groups", "lfds_set_profile"]
 
 
 def _check(rc):
@@ -137,14 +138,14 @@ class Plan:
     def __init__(self, hx, hy, hz, sigma_node, sigma_edge, lam, iface_x: Sequence[int] = (),
                  iface_y: Sequence[int] = (), *, dtype: str = "c128", refine: int = 0,
                  refine_tol: float = 1e-13, residual_dd: bool = True, device: int = 0, rhs_chunk: int = 0,
-                 profile: bool = False, s5_modal: bool = True, graph: bool = False,
+                 profile: int = 0, s5_modal: bool = True, graph: bool = False,
                  plane_dst: bool = True, resonance_tol: float = 1e-13, zs_warp: bool = False,
                  dst_tma: bool = True):
         opt = Options()
         _lib.lfds_default_options(ctypes.byref(opt))
         opt.dtype = LFDS_F64 if dtype in ("f64", "float64") else LFDS_C128
         opt.refine, opt.refine_tol, opt.residual_dd = int(refine), float(refine_tol), int(bool(residual_dd))
-        opt.device, opt.rhs_chunk, opt.profile = int(device), int(rhs_chunk), int(bool(profile))
+        opt.device, opt.rhs_chunk, opt.profile = int(device), int(rhs_chunk), int(profile)
         opt.s5_modal = int(bool(s5_modal))
         opt.graph = int(bool(graph))
         opt.plane_dst = int(bool(plane_dst))
@@ -220,6 +221,10 @@ class Plan:
         la = np.zeros(n, np.int32)
         _check(_lib.lfds_stage_times(self._h, ms.ctypes.data_as(_P), la.ctypes.data_as(_P)))
         return {_lib.lfds_stage_name(i).decode(): (float(ms[i]), int(la[i])) for i in range(n)}
+
+    def set_profile(self, level: int):
+        """0 none, 1 stage events, 2 stage + per-kernel-kind events (for later solves)."""
+        _check(_lib.lfds_set_profile(self._h, int(level)))
 
     def kernel_times(self) -> dict:
         """{kernel kind: (device ms, launches)} accumulated since the last call (profile=True)."""
