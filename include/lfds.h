@@ -327,6 +327,36 @@ void lfds_destroy(lfds_plan* plan);
 const char* lfds_last_error(void);
 const char* lfds_version(void);
 
+/*
+ * Multi-level (nested) partition — PAPER.md:77-79 (remark: "multiple mutually embedded
+ * partitions of S" trade the global interface step for solves on each level of embedding).
+ * Three levels: coarse blocks C between the coarse interfaces (c_x, c_y) and, inside every C,
+ * fine blocks between the fine interfaces (f_x, f_y, a superset of c_x, c_y).  Every coarse-block
+ * Dirichlet problem (PAPER.md:66-67 and :71-72 on the coarse partition) is solved by the
+ * two-level method of its own fine partition, whose interface step uses C's eigenbases; only the
+ * coarse planes take the global step 5.  A solve is
+ *   v_C = A_C^{-1} M f_C;  r_b = M f - A v on the coarse planes;  w = step 5 (global bases);
+ *   u_C = A_C^{-1} (M f_C - A_{C,dC} w);  u = w on the coarse planes,
+ * exact up to rounding like the two-level method (u = A^{-1} M f).  Arguments as
+ * lfds_setup_grid; c_x / c_y follow its interface rules, every one must be in f_x / f_y.
+ * Complex128 device plans only, no refinement (LFDS_EINVAL otherwise).
+ *  lfds_ml_solve: f_dev, u_dev device complex128 [nz][ny][nx] (one right-hand side), 16-byte
+ *  aligned; ws_dev of at least lfds_ml_workspace_bytes; everything stream-ordered on
+ *  cuda_stream.  The coarse-block plans replay as CUDA graphs (constant buffers).
+ * Errors: the codes of lfds_setup_grid / lfds_solve, message in lfds_ml_last_error().
+ */
+typedef struct lfds_ml lfds_ml;
+int lfds_ml_setup(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, const lfds_z* hz,
+                  const lfds_z* sigma_node, const lfds_z* sigma_edge, lfds_z lambda,
+                  int n_cx, const int* c_x, int n_cy, const int* c_y,
+                  int n_fx, const int* f_x, int n_fy, const int* f_y,
+                  const lfds_options* opt, lfds_ml** out);
+size_t lfds_ml_workspace_bytes(const lfds_ml* ml);
+int lfds_ml_solve(lfds_ml* ml, const void* f_dev, void* u_dev, void* ws_dev, size_t ws_bytes, void* cuda_stream);
+int lfds_ml_get_plans(const lfds_ml* ml, int* n_coarse_blocks);
+void lfds_ml_destroy(lfds_ml* ml);
+const char* lfds_ml_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -800,7 +800,7 @@ static int get_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan** o
 // 2 = step 5 on this rank's global x-modes; 4 = plane inverse, pass 2 (steps 6-7).  With block
 // sharding the caller sums exchange 1 ([RX, RY]) over the ranks between phases 1 and 2 and
 // exchange 2 ([P1, P2]) between phases 2 and 4 (lfds_exchange_layout).
-enum { PH_1 = 1, PH_2A = 2, PH_3 = 4, PH_2B = 8, PH_2 = PH_2A | PH_2B, PH_ALL = 15 };
+enum { PH_1 = 1, PH_2A = 2, PH_3 = 4, PH_2B = 8, PH_2 = PH_2A | PH_2B, PH_ALL = 15, PH_INV = 16 };
 static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, int out_dtype, cudaStream_t st,
                     int phases = PH_ALL) {
   const Axis& X = P->ax[0];
@@ -1040,6 +1040,17 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
       pm.h_off = pp.p2; pm.h_es = RZ * Nx; pm.h_ps = Nx;
       CUDA_TRY(kern(K_PROJM, pm.nlc > 1 ? 2 : 1, [&] { return launch_projm(pm, bufs, st); }));
     }
+    end();
+  }
+  if ((phases & PH_INV) && has_if) {
+    // w on the interface planes only (the multi-level solve's coarse level): plane inverse and
+    // u = w on the planes, no block pass
+    if ((rc = xform(pp.s5wx, StageDescs{}, pp.s5wx, true, nullptr, ST_GPLANE, ST_GPLANE))) return rc;
+    if ((rc = fold_planes(false))) return rc;
+    begin(ST_WRITE);
+    CUDA_TRY(kern(K_WRITE, 1, [&] {
+      return launch_write_iface_u(Nx, Ny, Nz, R, out_dtype, nifx, nify, P->t_ifx, P->t_ify, pp.wx, pp.wy, bufs, st,
+                                  pp.d_wmask, P->t_bx, P->t_by, P->nbx, P->nby, P->sharded ? P->rank0 : 1); }));
     end();
   }
   if (phases & PH_3) {
@@ -2033,6 +2044,22 @@ int lfds_set_mode_rows(lfds_plan* P, int m_begin, int m_end) {
   return LFDS_OK;
 }
 
+}  // extern "C"
+
+int lfds::plane_layout(lfds_plan* P, PlaneLayout* out) {
+  PassPlan* pp;
+  int rc;
+  if ((rc = get_pass(P, 1, 0, 0, &pp))) return rc;
+  out->rx = pp->rx;
+  out->ry = pp->ry;
+  out->wx = pp->wx;
+  out->wy = pp->wy;
+  out->off_if = pp->off_if;
+  return LFDS_OK;
+}
+
+extern "C" {
+
 int lfds_set_formation_rows(lfds_plan* P, int m_begin, int m_end, int l_begin, int l_end) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
   if (m_begin < 0) {  // off
@@ -2052,7 +2079,7 @@ int lfds_set_formation_rows(lfds_plan* P, int m_begin, int m_end, int l_begin, i
 
 int lfds_exchange_layout(const lfds_plan* cp, int nrhs, int which, size_t* byte_offset, size_t* n_doubles) {
   lfds_plan* P = const_cast<lfds_plan*>(cp);
-  if (!P || which < 1 || which > 3 || !byte_offset || !n_doubles) return fail(LFDS_EINVAL, "bad arguments");
+  if (!P || which < 1 || which > 4 || !byte_offset || !n_doubles) return fail(LFDS_EINVAL, "bad arguments");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
   const int R = chunk_of(P, nrhs);
   if (R != nrhs) return fail(LFDS_EINVAL, "sharded solves take all right-hand sides in one pass (rhs_chunk)");
@@ -2060,9 +2087,9 @@ int lfds_exchange_layout(const lfds_plan* cp, int nrhs, int which, size_t* byte_
   int rc = get_pass(P, R, P->opt.dtype == LFDS_F64, P->opt.dtype == LFDS_F64, &pp);
   if (rc) return rc;
   if (which == 3 && !pp->s5m) { *byte_offset = pp->off_if; *n_doubles = 0; return LFDS_OK; }
-  // [RX, RY] / [P1, P2] / [R1~, R2~]
-  const int64_t lo = which == 1 ? pp->rx : which == 2 ? pp->p1 : pp->r1t;
-  const int64_t hi = which == 1 ? pp->r1 : which == 2 ? pp->gp : pp->p1t;
+  // [RX, RY] / [P1, P2] / [R1~, R2~] / [WX, WY] (w on the planes)
+  const int64_t lo = which == 1 ? pp->rx : which == 2 ? pp->p1 : which == 3 ? pp->r1t : pp->wx;
+  const int64_t hi = which == 1 ? pp->r1 : which == 2 ? pp->gp : which == 3 ? pp->p1t : pp->gf;
   *byte_offset = pp->off_if + (size_t)lo * 16;
   *n_doubles = (size_t)(hi - lo) * 2;
   return LFDS_OK;
@@ -2072,7 +2099,7 @@ int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, in
                      void* stream) {
   if (!P) return fail(LFDS_EINVAL, "plan is NULL");
   if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
-  if (phase < 1 || phase > 5) return fail(LFDS_EINVAL, "phase must be 1..5");
+  if (phase < 1 || phase > 6) return fail(LFDS_EINVAL, "phase must be 1..6");
   if (nrhs < 1 || !f_dev || !u_dev || !ws) return fail(LFDS_EINVAL, "bad solve arguments");
   if (P->opt.refine != 0) return fail(LFDS_EINVAL, "phased (sharded) solves do not refine");
   const int R = chunk_of(P, nrhs);
@@ -2098,7 +2125,8 @@ int lfds_solve_phase(lfds_plan* P, int phase, const void* f_dev, void* u_dev, in
     P->launches = 0;
     CUDA_TRY(launch_fill_minpiv(reinterpret_cast<double*>(b.p[B_RED]), st));
   }
-  const int ph = phase == 1 ? PH_1 : phase == 2 ? PH_2 : phase == 3 ? PH_3 : phase == 4 ? PH_2A : PH_2B;
+  const int ph = phase == 1 ? PH_1 : phase == 2 ? PH_2 : phase == 3 ? PH_3 : phase == 4 ? PH_2A : phase == 5 ? PH_2B
+                                                                                                   : PH_INV;
   if ((rc = run_pass(P, *pp, b, R, dt, dt, st, ph))) return rc;
   P->report.passes = 1;
   P->report.n_kernel_launches = P->launches;

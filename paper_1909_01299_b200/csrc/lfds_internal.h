@@ -186,6 +186,30 @@ cudaError_t launch_axpy_u(int64_t n, int dtype, const double2* delta, void* u, c
 //   inverse: fold [E | O] -> plane, w_q = E_q + O_q, w_{N-1-q} = E_q - O_q
 cudaError_t launch_fold(bool forward, int64_t rows, int N, int64_t plane, int64_t fold, const Bufs& bufs,
                         cudaStream_t st);
+// multi-level solve (lfds_ml.cpp) glue:
+//   gather: RX[a][k][q] = r[k][q][ifx[a]-1] (all q), RY[b][k][p] = r[k][ify[b]-1][p], 0 at x-interface p
+//   lift:   f2[k][y][x] = f[k][y][x] - sigma_k (cL wL[k*ldw+y] [x=0] + cR wR[..] [x=nxc-1]
+//                                              + cB wB[k*ldw2+x] [y=0] + cT wT[..] [y=nyc-1])
+cudaError_t launch_ml_gather(const double2* r, int nx, int ny, int nz, const int* d_ifx, int nifx, const int* d_ify,
+                             int nify, double2* rx, double2* ry, cudaStream_t st);
+struct MlLift {
+  int nxc, nyc, nz;
+  double2 cL, cR, cB, cT;            // face couplings (0 when the face is the outer boundary)
+  const double2 *wL, *wR, *wB, *wT;  // w rows on the faces (k-major), or null
+  int64_t ldx, ldy;                  // k strides of the x-plane rows (Ny) and y-plane rows (Nx)
+  int64_t ox, oy;                    // offsets of the block's first row (y0) / column (x0) in them
+};
+cudaError_t launch_ml_lift(const MlLift& L, const double2* sig, const double2* f, double2* f2, cudaStream_t st);
+// (host) element offsets of RX, RY, WX, WY in a plan's interface buffer and that buffer's byte
+// offset in the workspace, for nrhs = 1
+struct PlaneLayout {
+  int64_t rx, ry, wx, wy;
+  size_t off_if;
+};
+}  // namespace lfds
+struct lfds_plan;
+namespace lfds {
+int plane_layout(lfds_plan* plan, PlaneLayout* out);  // (lfds_host.cpp)
 cudaError_t launch_fill_minpiv(double* p, cudaStream_t st);
 size_t zsolve_checkpoint_bytes(int nblocks, int max_nx, int max_ny, int R, int nz);
 // step 2 with a warp per z-line (lfds_zsolve.cu k_zsw): d_order = owned-block indices grouped by

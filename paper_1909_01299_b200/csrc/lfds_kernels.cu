@@ -536,4 +536,59 @@ cudaError_t launch_fold(bool forward, int64_t rows, int N, int64_t plane, int64_
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- multi-level glue (lfds_ml.cpp)
+__global__ void k_ml_gather(const double2* __restrict__ r, int nx, int ny, int nz, const int* __restrict__ ifx,
+                            int nifx, const int* __restrict__ ify, int nify, double2* __restrict__ rx,
+                            double2* __restrict__ ry) {
+  const int64_t nX = (int64_t)nifx * nz * ny, total = nX + (int64_t)nify * nz * nx;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < nX) {
+      const int q = (int)(t % ny);
+      const int64_t rest = t / ny;
+      const int k = (int)(rest % nz), a = (int)(rest / nz);
+      rx[t] = r[((int64_t)k * ny + q) * nx + ifx[a] - 1];
+    } else {
+      const int64_t u = t - nX;
+      const int p = (int)(u % nx);
+      const int64_t rest = u / nx;
+      const int k = (int)(rest % nz), b = (int)(rest / nz);
+      bool on_x = false;
+      for (int a = 0; a < nifx; ++a) on_x |= (ifx[a] - 1 == p);
+      ry[u] = on_x ? make_double2(0, 0) : r[((int64_t)k * ny + ify[b] - 1) * nx + p];
+    }
+  }
+}
+
+__global__ void k_ml_lift(MlLift L, const double2* __restrict__ sig, const double2* __restrict__ f,
+                          double2* __restrict__ f2) {
+  const int64_t total = (int64_t)L.nz * L.nyc * L.nxc;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(t % L.nxc);
+    const int64_t rest = t / L.nxc;
+    const int y = (int)(rest % L.nyc), k = (int)(rest / L.nyc);
+    cplx acc = mk(0, 0);
+    if (x == 0 && L.wL) acc = acc + mk(L.cL.x, L.cL.y) * ld(L.wL + k * L.ldx + L.ox + y);
+    if (x == L.nxc - 1 && L.wR) acc = acc + mk(L.cR.x, L.cR.y) * ld(L.wR + k * L.ldx + L.ox + y);
+    if (y == 0 && L.wB) acc = acc + mk(L.cB.x, L.cB.y) * ld(L.wB + k * L.ldy + L.oy + x);
+    if (y == L.nyc - 1 && L.wT) acc = acc + mk(L.cT.x, L.cT.y) * ld(L.wT + k * L.ldy + L.oy + x);
+    const cplx v = ld(f + t) - ld(sig + k) * acc;
+    f2[t] = make_double2(v.x, v.y);
+  }
+}
+
+cudaError_t launch_ml_gather(const double2* r, int nx, int ny, int nz, const int* d_ifx, int nifx, const int* d_ify,
+                             int nify, double2* rx, double2* ry, cudaStream_t st) {
+  const int64_t total = (int64_t)nifx * nz * ny + (int64_t)nify * nz * nx;
+  if (!total) return cudaSuccess;
+  k_ml_gather<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(r, nx, ny, nz, d_ifx, nifx,
+                                                                                            d_ify, nify, rx, ry);
+  return cudaGetLastError();
+}
+cudaError_t launch_ml_lift(const MlLift& L, const double2* sig, const double2* f, double2* f2, cudaStream_t st) {
+  const int64_t total = (int64_t)L.nz * L.nyc * L.nxc;
+  if (!total) return cudaSuccess;
+  k_ml_lift<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(L, sig, f, f2);
+  return cudaGetLastError();
+}
+
 }  // namespace lfds

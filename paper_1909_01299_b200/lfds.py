@@ -107,6 +107,14 @@ _lib.lfds_set_comm.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int]
 _lib.lfds_set_comm_groups.argtypes = [_P, ctypes.c_int, ctypes.c_int]
 _lib.lfds_last_error.restype = ctypes.c_char_p
 _lib.lfds_version.restype = ctypes.c_char_p
+_lib.lfds_ml_setup.argtypes = [ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P, _P, _Z,
+                               ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P, _P]
+_lib.lfds_ml_workspace_bytes.argtypes = [_P]
+_lib.lfds_ml_workspace_bytes.restype = ctypes.c_size_t
+_lib.lfds_ml_solve.argtypes = [_P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.lfds_ml_get_plans.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
+_lib.lfds_ml_destroy.argtypes = [_P]
+_lib.lfds_ml_last_error.restype = ctypes.c_char_p
 
 EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
             "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_get_report",
@@ -115,7 +123,8 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
             "lfds_set_mode_rows", "lfds_kernel_count", "lfds_kernel_name", "lfds_kernel_times",
             "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm", "lfds_set_formation_rows",
-            "lfds_set_comm_groups", "lfds_set_profile"]
+            "lfds_set_comm_groups", "lfds_set_profile", "lfds_ml_setup", "lfds_ml_workspace_bytes",
+            "lfds_ml_solve", "lfds_ml_get_plans", "lfds_ml_destroy", "lfds_ml_last_error"]
 
 
 def _check(rc):
@@ -423,6 +432,77 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_ubyte * 128)()
     _check(_lib.lfds_nccl_unique_id(ctypes.cast(buf, _P)))
     return bytes(buf)
+
+
+def _ml_check(rc):
+    if rc != 0:
+        raise LfdsError(rc, _lib.lfds_ml_last_error().decode())
+
+
+class MLPlan:
+    """Multi-level (nested) partition, lfds_ml_setup: coarse interfaces
+    (coarse_x, coarse_y) take the global step 5, every coarse block is solved by the two-level
+    method of its own fine partition (fine_x, fine_y, a superset of the coarse ones)."""
+
+    def __init__(self, hx, hy, hz, sigma_node, sigma_edge, lam, coarse_x=(), coarse_y=(), fine_x=(), fine_y=(), *,
+                 device: int = 0, s5_modal: bool = True, plane_dst: bool = True, resonance_tol: float = 1e-13,
+                 dst_tma: bool = True):
+        opt = Options()
+        _lib.lfds_default_options(ctypes.byref(opt))
+        opt.dtype = LFDS_C128
+        opt.device = int(device)
+        opt.s5_modal, opt.plane_dst = int(bool(s5_modal)), int(bool(plane_dst))
+        opt.resonance_tol, opt.dst_tma = float(resonance_tol), int(bool(dst_tma))
+        self.device = int(device)
+        hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
+        sn_, psn = _zarr(sigma_node); se_, pse = _zarr(sigma_edge)
+        ints = [np.ascontiguousarray(np.asarray(list(v), dtype=np.int32)) for v in (coarse_x, coarse_y, fine_x, fine_y)]
+        lam = complex(lam)
+        h = _P()
+        _ml_check(_lib.lfds_ml_setup(len(hx_) - 1, px, len(hy_) - 1, py, len(hz_) - 1, pz, psn, pse,
+                                     _Z(lam.real, lam.imag), *[a for v in ints for a in (len(v), v.ctypes.data_as(_P))],
+                                     ctypes.byref(opt), ctypes.byref(h)))
+        self._h = h
+        self.shape = (len(hz_) - 1, len(hy_) - 1, len(hx_) - 1)
+        self._ws = None
+
+    def n_coarse_blocks(self) -> int:
+        n = ctypes.c_int()
+        _ml_check(_lib.lfds_ml_get_plans(self._h, ctypes.byref(n)))
+        return n.value
+
+    def workspace(self):
+        import torch
+        nb = int(_lib.lfds_ml_workspace_bytes(self._h))
+        if self._ws is None or self._ws.numel() < nb:
+            self._ws = torch.empty(nb, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        return self._ws
+
+    def solve(self, f, out=None, stream=None):
+        """u = A^{-1} M f for one contiguous CUDA complex128 right-hand side (nz, ny, nx)."""
+        import torch
+        if not (f.is_cuda and f.is_contiguous() and f.dtype == torch.complex128) or tuple(f.shape) != self.shape:
+            raise ValueError(f"f must be a contiguous CUDA complex128 tensor of shape {self.shape}")
+        if out is not None and (tuple(out.shape) != self.shape or out.dtype != f.dtype or not out.is_contiguous()
+                                or out.device != f.device):
+            raise ValueError("out must match f")
+        U = torch.empty_like(f) if out is None else out
+        ws = self.workspace()
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _ml_check(_lib.lfds_ml_solve(self._h, _P(f.data_ptr()), _P(U.data_ptr()), _P(ws.data_ptr()), ws.numel(),
+                                     _P(st)))
+        return U
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lfds_ml_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def setup_grid(hx, hy, hz, sigma_node, sigma_edge, lam, iface_x=(), iface_y=(), **kw) -> Plan:
