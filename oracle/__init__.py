@@ -11,6 +11,9 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 CUDA path (``paper_1909_01299_b200``) and never imports it; its only shared input
 is the seeded generator package ``workloads``.
 
+``oracle.maxwell`` is the same for the Lebedev-grid Maxwell system of PAPER.md §3 (the curl-curl
+operator of Eq. (abstr) assembled from Eq. (fin), solved by sparse LU).
+
 Parity status per function is stated in each module header (all pinned; see
 DESIGN.md §4 for the pin list).
 """
