@@ -357,6 +357,46 @@ int lfds_ml_get_plans(const lfds_ml* ml, int* n_coarse_blocks);
 void lfds_ml_destroy(lfds_ml* ml);
 const char* lfds_ml_last_error(void);
 
+/*
+ * Lebedev-grid Maxwell solve in a horizontally layered medium — PAPER.md §3 (lines 81-372).
+ * Solves A_h H = f with A_h H = curl_h(rho curl_h H) - i omega mu H (Eq. (abstr), the curls
+ * built from Eq. (fin)), rho = diag(c1, c2, c3)(z) (diagonal),
+ * H on the Lebedev P-grid, boundary conditions H x n = 0 on dOmega ∩ P, E x n = 0 on dOmega ∩ R
+ * (PAPER.md:238-241), by the paper's separable route: x/y transforms of the four families pp, dd
+ * (even levels), pd, dp (odd levels) in the primary (Dirichlet) / dual (Neumann) eigenbases
+ * (PAPER.md:248-268), per harmonic four decoupled systems with H_z eliminated, i.e. 2x2
+ * block-tridiagonal z-systems, inverse transforms.  Exact up to rounding.
+ *  nx, ny, nz   node counts N of the grid M (odd, >= 5; nodes 0..N-1, both ends on dOmega and
+ *               primary, reading M1); hx[nx-1] ... steps x_{t+1} - x_t (complex
+ *               steps = coordinate stretching, e.g. a PML).
+ *  c1, c2, c3   rho = diag(c1, c2, c3) per z node (nz values each; used on the R nodes).
+ *  mu, omega    permeability (complex allowed) and angular frequency (> 0).
+ *  device       CUDA device; profile = 1 records CUDA events around the seven launch groups of
+ *               every solve (lfds_mw_kernel_times; synchronises the stream after each solve).
+ * Field layout (f, H, r): device complex128 [3][nz][ny][nx] (component x, y, z; x fastest),
+ * 16-byte aligned; values are taken / written on the interior P nodes (i + j + k even, 0-based),
+ * H and r are 0 elsewhere, f is ignored elsewhere.  Stream-ordered on cuda_stream.
+ * Errors: LFDS_EINVAL (bad sizes / NULL / even N), LFDS_EEIG (an axis basis failed its checks),
+ * LFDS_ERESONANCE (c2 lambda_l^2 + c1 nu_m^2 - i omega mu within 1e-13 of 0: the H_z
+ * elimination is singular; the message names (l, m) and the level), LFDS_ECUDA / LFDS_ENOMEM.
+ * Message in lfds_mw_last_error().
+ */
+typedef struct lfds_mw lfds_mw;
+int lfds_mw_setup(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, const lfds_z* hz,
+                  const lfds_z* c1, const lfds_z* c2, const lfds_z* c3, lfds_z mu, double omega,
+                  int device, int profile, lfds_mw** out);
+size_t lfds_mw_workspace_bytes(const lfds_mw* plan);
+int lfds_mw_solve(lfds_mw* plan, const void* f_dev, void* h_dev, void* ws_dev, size_t ws_bytes, void* cuda_stream);
+/* r = f - A_h H on the interior P nodes (0 elsewhere), evaluated directly on the grid (the same
+ * workspace; its first 3 nz ny nx complex128 hold E = rho curl_h H afterwards). */
+int lfds_mw_residual(lfds_mw* plan, const void* h_dev, const void* f_dev, void* r_dev, void* ws_dev,
+                     size_t ws_bytes, void* cuda_stream);
+int lfds_mw_kernel_count(void);
+const char* lfds_mw_kernel_name(int kernel);
+int lfds_mw_kernel_times(lfds_mw* plan, double* ms, int* launches);  /* accumulated; resets */
+void lfds_mw_destroy(lfds_mw* plan);
+const char* lfds_mw_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

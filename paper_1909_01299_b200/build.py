@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "liblfds.so")
-SOURCES = ["lfds_kernels.cu", "lfds_peak.cu", "lfds_margin.cu", "lfds_zsolve.cu", "lfds_proj.cu", "lfds_xform.cu", "lfds_dst.cu", "lfds_modal.cu", "lfds_krylov.cu", "lfds_host.cpp", "lfds_eig.cpp", "lfds_ml.cpp"]
+SOURCES = ["lfds_kernels.cu", "lfds_peak.cu", "lfds_margin.cu", "lfds_zsolve.cu", "lfds_proj.cu", "lfds_xform.cu", "lfds_dst.cu", "lfds_modal.cu", "lfds_krylov.cu", "lfds_host.cpp", "lfds_eig.cpp", "lfds_ml.cpp", "lfds_mw.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-cudart", "static", "--expt-relaxed-constexpr"]

@@ -256,8 +256,16 @@ static bool tridiag_eig(const std::vector<lc>& d, const std::vector<lc>& e, std:
   return true;
 }
 
-bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err) {
+bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err, const std::vector<zc>* mass) {
   const int n = (int)h.size() - 1;
+  if (mass && (int)mass->size() != n) {
+    err = "mass size";
+    return false;
+  }
+  auto hhat = [&](int i) -> lc {
+    if (mass) return lc((*mass)[i].real(), (*mass)[i].imag());
+    return 0.5L * (lc(h[i].real(), h[i].imag()) + lc(h[i + 1].real(), h[i + 1].imag()));
+  };
   B.n = n;
   B.lam.assign(n, zc(0));
   B.W.assign((size_t)n * n, zc(0));
@@ -270,6 +278,11 @@ bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err) {
     if (h[t].imag() != 0) real = false;
     if (h[t] != h[0]) uniform = false;
   }
+  if (mass)
+    for (int t = 0; t < n; ++t) {
+      if ((*mass)[t].imag() != 0) real = false;
+      if ((*mass)[t] != h[0]) uniform = false;
+    }
   std::vector<long double> ord_re(n), ord_im(n);
   std::vector<lc> lamL(n), WL((size_t)n * n);  // WL row-major W[p*n + l]
   if (real && uniform) {
@@ -291,7 +304,7 @@ bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err) {
     std::vector<lc> hh(n), s(n), d(n), e(n > 1 ? n - 1 : 0);
     for (int i = 0; i < n; ++i) {
       lc h0(h[i].real(), h[i].imag()), h1(h[i + 1].real(), h[i + 1].imag());
-      hh[i] = 0.5L * (h0 + h1);
+      hh[i] = hhat(i);
       s[i] = lc(1) / std::sqrt(hh[i]);
       d[i] = -(lc(1) / h0 + lc(1) / h1) * s[i] * s[i];
     }
@@ -301,6 +314,7 @@ bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err) {
     }
     bool palin = n >= 2;
     for (int t = 0; t <= n && palin; ++t) palin = (h[t] == h[n - t]);
+    for (int t = 0; mass && t < n && palin; ++t) palin = ((*mass)[t] == (*mass)[n - 1 - t]);
     std::vector<lc> lamv;
     std::vector<lc> V;  // column-major n x n
     if (!palin) {
@@ -374,7 +388,7 @@ bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err) {
     std::vector<lc> hh(n), a_sub(n), a_dia(n), a_sup(n);
     for (int i = 0; i < n; ++i) {
       lc h0(h[i].real(), h[i].imag()), h1(h[i + 1].real(), h[i + 1].imag());
-      hh[i] = 0.5L * (h0 + h1);
+      hh[i] = hhat(i);
       a_sub[i] = i > 0 ? lc(1) / h0 : lc(0);
       a_sup[i] = i + 1 < n ? lc(1) / h1 : lc(0);
       a_dia[i] = -(lc(1) / h0 + lc(1) / h1);

@@ -17,8 +17,10 @@ struct Basis {
   double biorth = 0;         // max |W^T M W - I| over sampled columns
 };
 
-// Eigenbasis of the Dirichlet pencil of the N+1 steps h (N interior nodes).
-bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err);
+// Eigenbasis of the Dirichlet pencil of the N+1 steps h (N interior nodes).  mass (N values)
+// replaces the control volumes (h_{i-1} + h_i)/2 as the diagonal of M when given (the
+// Lebedev-grid primary pencil of the Maxwell solve, lfds_mw.cpp).
+bool pencil_basis(const std::vector<zc>& h, Basis& B, std::string& err, const std::vector<zc>* mass = nullptr);
 
 // z modal basis for step 5 (real z tables only): A' Z = E Z diag(theta), Z^T E Z = I, with
 // A' = tridiag(a, g, c) (a[k] couples k-1, c[k] couples k+1; a[k+1] == c[k]) and E = diag(e).

@@ -115,6 +115,17 @@ _lib.lfds_ml_solve.argtypes = [_P, _P, _P, _P, ctypes.c_size_t, _P]
 _lib.lfds_ml_get_plans.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
 _lib.lfds_ml_destroy.argtypes = [_P]
 _lib.lfds_ml_last_error.restype = ctypes.c_char_p
+_lib.lfds_mw_setup.argtypes = [ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P, _P, _P, _Z, ctypes.c_double,
+                               ctypes.c_int, ctypes.c_int, _P]
+_lib.lfds_mw_workspace_bytes.argtypes = [_P]
+_lib.lfds_mw_workspace_bytes.restype = ctypes.c_size_t
+_lib.lfds_mw_solve.argtypes = [_P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.lfds_mw_residual.argtypes = [_P, _P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.lfds_mw_kernel_name.argtypes = [ctypes.c_int]
+_lib.lfds_mw_kernel_name.restype = ctypes.c_char_p
+_lib.lfds_mw_kernel_times.argtypes = [_P, _P, _P]
+_lib.lfds_mw_destroy.argtypes = [_P]
+_lib.lfds_mw_last_error.restype = ctypes.c_char_p
 
 EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
             "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_get_report",
@@ -124,7 +135,10 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_set_mode_rows", "lfds_kernel_count", "lfds_kernel_name", "lfds_kernel_times",
             "lfds_fp64_peak", "lfds_nccl_unique_id", "lfds_set_comm", "lfds_set_formation_rows",
             "lfds_set_comm_groups", "lfds_set_profile", "lfds_ml_setup", "lfds_ml_workspace_bytes",
-            "lfds_ml_solve", "lfds_ml_get_plans", "lfds_ml_destroy", "lfds_ml_last_error"]
+            "lfds_ml_solve", "lfds_ml_get_plans", "lfds_ml_destroy", "lfds_ml_last_error",
+            "lfds_mw_setup", "lfds_mw_workspace_bytes", "lfds_mw_solve", "lfds_mw_residual",
+            "lfds_mw_kernel_count", "lfds_mw_kernel_name", "lfds_mw_kernel_times", "lfds_mw_destroy",
+            "lfds_mw_last_error"]
 
 
 def _check(rc):
@@ -496,6 +510,86 @@ class MLPlan:
     def close(self):
         if getattr(self, "_h", None):
             _lib.lfds_ml_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _mw_check(rc):
+    if rc != 0:
+        raise LfdsError(rc, _lib.lfds_mw_last_error().decode())
+
+
+class MWPlan:
+    """Lebedev-grid Maxwell solve in a layered medium (lfds_mw_setup, §3): H = A_h^{-1} f
+    with A_h = curl rho curl - i omega mu.  Fields are CUDA complex128 (3, N_z, N_y, N_x)."""
+
+    def __init__(self, hx, hy, hz, c1, c2, c3, mu, omega: float, *, device: int = 0, profile: bool = False):
+        hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
+        a1, p1 = _zarr(c1); a2, p2 = _zarr(c2); a3, p3 = _zarr(c3)
+        mu = complex(mu)
+        h = _P()
+        _mw_check(_lib.lfds_mw_setup(len(hx_) + 1, px, len(hy_) + 1, py, len(hz_) + 1, pz, p1, p2, p3,
+                                     _Z(mu.real, mu.imag), float(omega), int(device), int(bool(profile)),
+                                     ctypes.byref(h)))
+        self._h = h
+        self.device = int(device)
+        self.shape = (3, len(hz_) + 1, len(hy_) + 1, len(hx_) + 1)
+        self._ws = None
+
+    @classmethod
+    def from_problem(cls, p, **kw):
+        return cls(p.hx, p.hy, p.hz, p.c1, p.c2, p.c3, p.mu, p.omega, **kw)
+
+    def workspace(self):
+        import torch
+        nb = int(_lib.lfds_mw_workspace_bytes(self._h))
+        if self._ws is None or self._ws.numel() < nb:
+            self._ws = torch.empty(nb, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        return self._ws
+
+    def _chk(self, t, name):
+        import torch
+        if not (t.is_cuda and t.is_contiguous() and t.dtype == torch.complex128) or tuple(t.shape) != self.shape:
+            raise ValueError(f"{name} must be a contiguous CUDA complex128 tensor of shape {self.shape}")
+
+    def solve(self, f, out=None, stream=None):
+        import torch
+        self._chk(f, "f")
+        H = torch.empty_like(f) if out is None else out
+        self._chk(H, "out")
+        ws = self.workspace()
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _mw_check(_lib.lfds_mw_solve(self._h, _P(f.data_ptr()), _P(H.data_ptr()), _P(ws.data_ptr()), ws.numel(),
+                                     _P(st)))
+        return H
+
+    def residual(self, H, f, out=None, stream=None):
+        """r = f - A_h H on the interior P nodes (lfds_mw_residual)."""
+        import torch
+        self._chk(H, "H")
+        self._chk(f, "f")
+        r = torch.empty_like(f) if out is None else out
+        ws = self.workspace()
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _mw_check(_lib.lfds_mw_residual(self._h, _P(H.data_ptr()), _P(f.data_ptr()), _P(r.data_ptr()),
+                                        _P(ws.data_ptr()), ws.numel(), _P(st)))
+        return r
+
+    def kernel_times(self) -> dict:
+        n = _lib.lfds_mw_kernel_count()
+        ms = np.zeros(n, np.float64)
+        la = np.zeros(n, np.int32)
+        _mw_check(_lib.lfds_mw_kernel_times(self._h, ms.ctypes.data_as(_P), la.ctypes.data_as(_P)))
+        return {_lib.lfds_mw_kernel_name(i).decode(): (float(ms[i]), int(la[i])) for i in range(n)}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lfds_mw_destroy(self._h)
             self._h = None
 
     def __del__(self):
