@@ -397,6 +397,27 @@ int lfds_mw_kernel_times(lfds_mw* plan, double* ms, int* launches);  /* accumula
 void lfds_mw_destroy(lfds_mw* plan);
 const char* lfds_mw_last_error(void);
 
+/*
+ * Two-level (blocked) Maxwell solve, H = H^1 + H^2: blocks S^ij between the
+ * x-interfaces ix[] and y-interfaces iy[] (node indices, even, >= 4 apart and >= 4 from the
+ * ends, so every block is a Lebedev sub-grid with primary boundary nodes).  H^1 = block solves
+ * with H x n = 0 on dS ∩ P, E x n = 0 on dS ∩ R (each block its own layered plan); the residual
+ * f - A_h H^1 lives on the three node layers around each plane; step 5 evaluates A_h^{-1} of it on
+ * those layers only (layer-restricted global transforms + all harmonics' 2x2 block z-systems);
+ * the interface data H_tan (plane P nodes) and E_tan (plane R nodes) are lifted into the block
+ * right sides and the blocks are solved again ("the boundary conditions are imposed on both
+ * these grids").  Exact up to rounding.  Arguments and field layout as
+ * lfds_mw_setup / lfds_mw_solve; errors in lfds_mw_last_error().
+ */
+typedef struct lfds_mw2 lfds_mw2;
+int lfds_mw2_setup(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, const lfds_z* hz,
+                   const lfds_z* c1, const lfds_z* c2, const lfds_z* c3, lfds_z mu, double omega,
+                   int n_ix, const int* ix, int n_iy, const int* iy, int device, lfds_mw2** out);
+size_t lfds_mw2_workspace_bytes(const lfds_mw2* plan);
+int lfds_mw2_solve(lfds_mw2* plan, const void* f_dev, void* h_dev, void* ws_dev, size_t ws_bytes, void* cuda_stream);
+int lfds_mw2_blocks(const lfds_mw2* plan, int* n_blocks);
+void lfds_mw2_destroy(lfds_mw2* plan);
+
 #ifdef __cplusplus
 }
 #endif

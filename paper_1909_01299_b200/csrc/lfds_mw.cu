@@ -185,7 +185,10 @@ __device__ __forceinline__ Lev level_terms(const MwDev& D, int k, cx sx, cx sy) 
   return L;
 }
 
-__global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict__ fam, double2* __restrict__ cp) {
+// fam2 (optional, the two-level step 5): a second right-hand-side array in the same layout,
+// added to fam's on reading (the x-plane and y-plane parts of the transformed residual).
+__global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict__ fam, double2* __restrict__ cp,
+                                                   const double2* __restrict__ fam2) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)4 * D.plane) return;
   const int l = (int)(t % D.nx), m = (int)((t / D.nx) % D.ny), s = (int)(t / D.plane);
@@ -204,7 +207,9 @@ __global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict_
   double2* CP = cp + (int64_t)s * (D.nz) * 4 * D.plane + hoff;
   const cx zero = mk(0, 0);
   const cx iwm = mk(D.iwm.x, D.iwm.y);
-  auto rdz = [&](int k) -> cx { return az ? zero : ldw(FZ + (int64_t)lev_of(fz, k) * D.plane); };
+  const int64_t d2 = fam2 ? (int64_t)(fam2 - fam) : 0;  // element offset of the second array
+  auto rd = [&](const double2* p) -> cx { return fam2 ? ldw(p) + ldw(p + d2) : ldw(p); };
+  auto rdz = [&](int k) -> cx { return az ? zero : rd(FZ + (int64_t)lev_of(fz, k) * D.plane); };
   auto interior = [&](int k) { return k >= 1 && k <= D.Nz - 2; };
   // forward sweep
   Lev Lm{};
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict_
     m2 Dg{c3 * sy * sy - iwm, -(c3 * sx * sy), -(c3 * sx * sy), c3 * sx * sx - iwm};
     Dg = msub(msub(Dg, Ap), Am);
     const int lx = lev_of(fx, k), ly = lev_of(fy, k);
-    v2 rhs{ax ? zero : ldw(FX + (int64_t)lx * D.plane), ay ? zero : ldw(FY + (int64_t)ly * D.plane)};
+    v2 rhs{ax ? zero : rd(FX + (int64_t)lx * D.plane), ay ? zero : rd(FY + (int64_t)ly * D.plane)};
     if (gp) rhs = vsub(rhs, v2{Lp.sqx * fzp * idz, Lp.sqy * fzp * idz});
     if (gm) rhs = v2{rhs.x + Lm.sqx * fzm * idz, rhs.y + Lm.sqy * fzm * idz};
     if (r > 0) {
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict_
     st(FY + (int64_t)lev_of(fy, k) * D.plane, ay ? zero : Xn.y);
     if (interior(k + 1)) hz_at(k + 1, Xn, v2{zero, zero});
   }
+  CP -= 4 * D.plane;  // (row nX - 1's C' multiplies nothing)
   for (int r = nX - 2; r >= 0; --r) {
     const int k = k0 + 2 * r;
     CP -= 4 * D.plane;
@@ -622,7 +628,7 @@ int lfds_mw_solve(lfds_mw* P, const void* f_dev, void* h_dev, void* ws, size_t w
   mark(3);
   if (!e) {
     const int64_t nt = 4 * P->D.plane;
-    k_mw_zsolve<<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(P->D, fam, cp);
+    k_mw_zsolve<<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(P->D, fam, cp, nullptr);
     e = cudaGetLastError();
   }
   mark(4);
@@ -676,6 +682,544 @@ int lfds_mw_residual(lfds_mw* P, const void* h_dev, const void* f_dev, void* r_d
                                   static_cast<double2*>(r_dev));
   const cudaError_t e = cudaGetLastError();
   if (e) return mwfail(LFDS_ECUDA, "maxwell residual: %s", cudaGetErrorString(e));
+  return LFDS_OK;
+}
+
+}  // extern "C"
+
+// =====================================================================================
+// Two-level (blocked) Maxwell solve: H = H^1 + H^2.
+//
+// The blocks S^ij lie between x-interfaces I_a and y-interfaces J_b (even nodes: every block is a
+// Lebedev sub-grid whose boundary nodes are primary, reading M6).  With A_S the block operator
+// (H x n = 0 on dS ∩ P, E x n = 0 on dS ∩ R — exactly the layered problem on the sub-grid):
+//   1-3. v = H^1: A_S v_S = f_S on every block, v = 0 on the interface planes   (block plans)
+//   4.   r = f - A_h v; it lives on the layers {I-1, I, I+1} x all y and all x x {J-1, J, J+1}
+//        (the block equations next to a plane assumed E_tan = 0 on it; reading M6)
+//   5.   w = A_h^{-1} r on those layers only ("computed on the fifth step"):
+//        the global separable solve with its x- and y-transforms restricted to the layer
+//        columns / rows — forward: y-transform of the K_x layer columns then the sparse x-sum,
+//        x-transform of the K_y layer rows then the sparse y-sum; all harmonics' z-systems
+//        (k_mw_zsolve with the two parts summed); inverse evaluated on the layers only;
+//        H = v + w there, so H^2's boundary data are H_tan on the plane P nodes and
+//        E_tan = (rho curl_h H)_tan on the plane R nodes ("imposed on both these grids")
+//   6-7. A_S H_S = f_S - [curl_h E_b + curl_h (rho curl_h H_b)] next to dS (the interface data
+//        lifted into the right side), block plans again; H = w on the plane P nodes.
+// Exact like the scalar method: H = A_h^{-1} f up to rounding.
+namespace {
+
+__global__ void k_mw2_gather_r(MwDev D, const double2* __restrict__ r, double2* __restrict__ out,
+                               const int64_t* __restrict__ cxo, const int64_t* __restrict__ cyo,
+                               const int* __restrict__ lx, const int* __restrict__ ly, int Kx0, int Kx1, int Ky0,
+                               int Ky1, const unsigned char* __restrict__ isx, int64_t total) {
+  // compact layer arrays: x-part [f][c*lev][y-node][kx], y-part [f][c*lev][ky][x-node] (zero at
+  // the x-layer columns, which the x-part carries)
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t u = t;
+    int part = 0, f = 0;
+    int64_t sz = 0;
+    for (part = 0; part < 2; ++part) {
+      for (f = 0; f < 4; ++f) {
+        const int K = part == 0 ? (fam_xk(f) ? Kx1 : Kx0) : (fam_yk(f) ? Ky1 : Ky0);
+        sz = (int64_t)3 * D.nlev[f] * K * (part == 0 ? D.ny : D.nx);
+        if (u < sz) break;
+        u -= sz;
+      }
+      if (f < 4) break;
+    }
+    const int xk = fam_xk(f), yk = fam_yk(f);
+    const int nxf = xk ? D.nx : D.nx - 1, nyf = yk ? D.ny : D.ny - 1;
+    int i, j, cl;
+    double2 v = make_double2(0, 0);
+    bool ok;
+    if (part == 0) {
+      const int K = xk ? Kx1 : Kx0;
+      const int kx = (int)(u % K);
+      const int yy = (int)((u / K) % D.ny);
+      cl = (int)(u / ((int64_t)K * D.ny));
+      i = lx[xk * (Kx0 + 0) + kx];  // node of layer column kx (lists: primary then dual)
+      j = yk ? 2 * yy + 1 : 2 * yy + 2;
+      ok = yy < nyf;
+    } else {
+      const int K = yk ? Ky1 : Ky0;
+      const int xx = (int)(u % D.nx);
+      const int ky = (int)((u / D.nx) % K);
+      cl = (int)(u / ((int64_t)K * D.nx));
+      j = ly[yk * (Ky0 + 0) + ky];
+      i = xk ? 2 * xx + 1 : 2 * xx + 2;
+      ok = xx < nxf && !isx[i];
+    }
+    if (ok) {
+      const int c = cl / D.nlev[f], lev = cl % D.nlev[f];
+      const int k = f < 2 ? 2 * lev + 2 : 2 * lev + 1;
+      v = r[(((int64_t)c * D.Nz + k) * D.Ny + j) * D.Nx + i];
+    }
+    out[(part == 0 ? cxo[f] : cyo[f]) + u] = v;
+  }
+}
+
+__global__ void k_mw2_add_w(MwDev D, const double2* __restrict__ w, double2* __restrict__ H,
+                            const int64_t* __restrict__ cxo, const int64_t* __restrict__ cyo,
+                            const int* __restrict__ lx, const int* __restrict__ ly, int Kx0, int Kx1, int Ky0, int Ky1,
+                            const unsigned char* __restrict__ isx, int64_t total) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t u = t;
+    int part = 0, f = 0;
+    for (part = 0; part < 2; ++part) {
+      for (f = 0; f < 4; ++f) {
+        const int K = part == 0 ? (fam_xk(f) ? Kx1 : Kx0) : (fam_yk(f) ? Ky1 : Ky0);
+        const int64_t sz = (int64_t)3 * D.nlev[f] * K * (part == 0 ? D.ny : D.nx);
+        if (u < sz) break;
+        u -= sz;
+      }
+      if (f < 4) break;
+    }
+    const int xk = fam_xk(f), yk = fam_yk(f);
+    const int nxf = xk ? D.nx : D.nx - 1, nyf = yk ? D.ny : D.ny - 1;
+    int i, j, cl;
+    bool ok;
+    if (part == 0) {
+      const int K = xk ? Kx1 : Kx0;
+      const int kx = (int)(u % K);
+      const int yy = (int)((u / K) % D.ny);
+      cl = (int)(u / ((int64_t)K * D.ny));
+      i = lx[xk * Kx0 + kx];
+      j = yk ? 2 * yy + 1 : 2 * yy + 2;
+      ok = yy < nyf;
+    } else {
+      const int K = yk ? Ky1 : Ky0;
+      const int xx = (int)(u % D.nx);
+      const int ky = (int)((u / D.nx) % K);
+      cl = (int)(u / ((int64_t)K * D.nx));
+      j = ly[yk * Ky0 + ky];
+      i = xk ? 2 * xx + 1 : 2 * xx + 2;
+      ok = xx < nxf && !isx[i];
+    }
+    if (ok) {
+      const int c = cl / D.nlev[f], lev = cl % D.nlev[f];
+      const int k = f < 2 ? 2 * lev + 2 : 2 * lev + 1;
+      const int64_t o = (((int64_t)c * D.Nz + k) * D.Ny + j) * D.Nx + i;
+      const double2 a = H[o], b = w[(part == 0 ? cxo[f] : cyo[f]) + u];
+      H[o] = make_double2(a.x + b.x, a.y + b.y);
+    }
+  }
+}
+
+// E_l on the interior R nodes: on an interface plane the true E = rho curl_h H (H = v + w on the
+// layers), elsewhere rho curl_h H_b with H_b = H on the plane P nodes only (nonzero next to a
+// plane).  Then f2 = f - curl_h E_l on the interior P nodes off the planes.
+__global__ void k_mw2_elift(MwDev D, const double2* __restrict__ H, double2* __restrict__ E,
+                            const unsigned char* __restrict__ plx, const unsigned char* __restrict__ ply) {
+  const int64_t N = (int64_t)D.Nz * D.Ny * D.Nx;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % D.Nx);
+    const int j = (int)((t / D.Nx) % D.Ny), k = (int)(t / ((int64_t)D.Nx * D.Ny));
+    cx ex = mk(0, 0), ey = ex, ez = ex;
+    if (((i + j + k) & 1) && i > 0 && j > 0 && k > 0 && i < D.Nx - 1 && j < D.Ny - 1 && k < D.Nz - 1) {
+      const bool on = plx[i] || ply[j];
+      const int64_t sx = 1, sy = D.Nx, sz = (int64_t)D.Nx * D.Ny;
+      const cx ix = cinv(ld(D.dxx + i)), iy = cinv(ld(D.dyy + j)), iz = cinv(ld(D.dzz + k));
+      // neighbour (di, dj, dk) is usable if interior and (on ? any : on a plane)
+      auto use = [&](int ii, int jj, int kk) {
+        if (ii <= 0 || jj <= 0 || kk <= 0 || ii >= D.Nx - 1 || jj >= D.Ny - 1 || kk >= D.Nz - 1) return false;
+        return on || plx[ii] || ply[jj];
+      };
+      auto d = [&](int c, int di, int dj, int dk, int64_t s, cx inv) {
+        const cx a = use(i + di, j + dj, k + dk) ? ld(H + c * N + t + s) : mk(0, 0);
+        const cx b = use(i - di, j - dj, k - dk) ? ld(H + c * N + t - s) : mk(0, 0);
+        return (a - b) * inv;
+      };
+      ex = ld(D.lev + 4 * k + 1) * (d(2, 0, 1, 0, sy, iy) - d(1, 0, 0, 1, sz, iz));
+      ey = ld(D.lev + 4 * k + 2) * (d(0, 0, 0, 1, sz, iz) - d(2, 1, 0, 0, sx, ix));
+      ez = ld(D.lev + 4 * k + 3) * (d(1, 1, 0, 0, sx, ix) - d(0, 0, 1, 0, sy, iy));
+    }
+    st(E + t, ex);
+    st(E + N + t, ey);
+    st(E + 2 * N + t, ez);
+  }
+}
+
+__global__ void k_mw2_flift(MwDev D, const double2* __restrict__ E, const double2* __restrict__ F,
+                            double2* __restrict__ F2, const unsigned char* __restrict__ plx,
+                            const unsigned char* __restrict__ ply) {
+  const int64_t N = (int64_t)D.Nz * D.Ny * D.Nx;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % D.Nx);
+    const int j = (int)((t / D.Nx) % D.Ny), k = (int)(t / ((int64_t)D.Nx * D.Ny));
+    cx rx = mk(0, 0), ry = rx, rz = rx;
+    if (!((i + j + k) & 1) && i > 0 && j > 0 && k > 0 && i < D.Nx - 1 && j < D.Ny - 1 && k < D.Nz - 1 && !plx[i] &&
+        !ply[j]) {
+      const int64_t sx = 1, sy = D.Nx, sz = (int64_t)D.Nx * D.Ny;
+      const cx ix = cinv(ld(D.dxx + i)), iy = cinv(ld(D.dyy + j)), iz = cinv(ld(D.dzz + k));
+      auto d = [&](int c, int64_t s, cx inv) { return (ld(E + c * N + t + s) - ld(E + c * N + t - s)) * inv; };
+      rx = ld(F + t) - (d(2, sy, iy) - d(1, sz, iz));
+      ry = ld(F + N + t) - (d(0, sz, iz) - d(2, sx, ix));
+      rz = ld(F + 2 * N + t) - (d(1, sx, ix) - d(0, sy, iy));
+    }
+    st(F2 + t, rx);
+    st(F2 + N + t, ry);
+    st(F2 + 2 * N + t, rz);
+  }
+}
+
+}  // namespace
+
+struct lfds_mw2 {
+  lfds_mw* glob = nullptr;  // global grid: MwDev tables (lam, nu, levels, steps) and residual kernels
+  struct Blk {
+    lfds_mw* plan = nullptr;
+    int x0, x1, y0, y1;  // box nodes (inclusive): its boundary nodes lie on planes / dOmega
+  };
+  std::vector<Blk> blk;
+  bool realx = true, realy = true;
+  char* d_tab = nullptr;            // step-5 matrices + layer tables
+  lfds::GemmDesc* d_desc = nullptr;  // 8 groups of 4
+  int Kx[2] = {0, 0}, Ky[2] = {0, 0};
+  const int* d_lx = nullptr;
+  const int* d_ly = nullptr;
+  const unsigned char *d_isx = nullptr, *d_plx = nullptr, *d_ply = nullptr;
+  const int64_t *d_cxo = nullptr, *d_cyo = nullptr;
+  int64_t compact = 0;               // complex elements of one compact slot (>= 1)
+  int64_t compact_used = 0;          // of which in use (0 without interfaces)
+  int gM[8] = {}, gKc[8] = {}, gReal[8] = {};
+  int64_t gN[8] = {};
+  size_t sub_elems = 0, sub_ws = 0;
+};
+
+extern "C" {
+
+void lfds_mw2_destroy(lfds_mw2* P) {
+  if (!P) return;
+  if (P->glob) lfds_mw_destroy(P->glob);
+  for (auto& b : P->blk)
+    if (b.plan) lfds_mw_destroy(b.plan);
+  cudaFree(P->d_tab);
+  cudaFree(P->d_desc);
+  delete P;
+}
+
+int lfds_mw2_setup(int Nx, const lfds_z* hx, int Ny, const lfds_z* hy, int Nz, const lfds_z* hz, const lfds_z* c1,
+                   const lfds_z* c2, const lfds_z* c3, lfds_z mu, double omega, int n_ix, const int* ix, int n_iy,
+                   const int* iy, int device, lfds_mw2** out) {
+  if (!out) return mwfail(LFDS_EINVAL, "out is NULL");
+  *out = nullptr;
+  auto check_if = [&](int N, int n, const int* I, const char* ax) -> int {
+    int prev = 0;
+    for (int a = 0; a < n; ++a) {
+      if (I[a] % 2 || I[a] - prev < 4) return mwfail(LFDS_EINVAL, "%s interface %d: even nodes >= 4 apart", ax, I[a]);
+      prev = I[a];
+    }
+    if (N - 1 - prev < 4) return mwfail(LFDS_EINVAL, "%s: last block narrower than 5 nodes", ax);
+    return LFDS_OK;
+  };
+  int rc;
+  if ((rc = check_if(Nx, n_ix, ix, "x")) || (rc = check_if(Ny, n_iy, iy, "y"))) return rc;
+  std::unique_ptr<lfds_mw2> P(new lfds_mw2());
+  auto bail = [&](int code) {
+    lfds_mw2_destroy(P.release());
+    return code;
+  };
+  if ((rc = lfds_mw_setup(Nx, hx, Ny, hy, Nz, hz, c1, c2, c3, mu, omega, device, 0, &P->glob))) return bail(rc);
+  const MwDev& D = P->glob->D;
+  // blocks and their plans (sub-grids of the steps)
+  std::vector<int> xs = {0}, ys = {0};
+  xs.insert(xs.end(), ix, ix + n_ix); xs.push_back(Nx - 1);
+  ys.insert(ys.end(), iy, iy + n_iy); ys.push_back(Ny - 1);
+  for (size_t b = 0; b + 1 < ys.size(); ++b)
+    for (size_t a = 0; a + 1 < xs.size(); ++a) {
+      lfds_mw2::Blk B{nullptr, xs[a], xs[a + 1], ys[b], ys[b + 1]};
+      if ((rc = lfds_mw_setup(B.x1 - B.x0 + 1, hx + B.x0, B.y1 - B.y0 + 1, hy + B.y0, Nz, hz, c1, c2, c3, mu, omega,
+                              device, 0, &B.plan))) {
+        P->blk.push_back(B);
+        return bail(rc);
+      }
+      P->blk.push_back(B);
+      P->sub_elems = std::max(P->sub_elems, (size_t)3 * Nz * (B.y1 - B.y0 + 1) * (B.x1 - B.x0 + 1));
+      P->sub_ws = std::max(P->sub_ws, lfds_mw_workspace_bytes(B.plan));
+    }
+  // global axis bases again (host), restricted to the layer nodes
+  Axis1 X, Y;
+  if ((rc = axis_setup(Nx, hx, "x", X)) || (rc = axis_setup(Ny, hy, "y", Y))) return bail(rc);
+  P->realx = X.real;
+  P->realy = Y.real;
+  // layer lists per kind (packed node index within the family axis): primary I -> I/2 - 1,
+  // dual I -+ 1 -> (I-2)/2, I/2;  and the node lists used by the kernels
+  std::vector<int> lxp, lxd, lyp, lyd, nxl, nyl;  // packed indices; node ids (primary list then dual)
+  std::vector<unsigned char> isx(Nx, 0), plx(Nx, 0), ply(Ny, 0);
+  for (int a = 0; a < n_ix; ++a) {
+    const int I = ix[a];
+    lxp.push_back(I / 2 - 1);
+    lxd.push_back((I - 2) / 2);
+    lxd.push_back(I / 2);
+    isx[I - 1] = isx[I] = isx[I + 1] = 1;
+    plx[I] = 1;
+  }
+  for (int b = 0; b < n_iy; ++b) {
+    const int J = iy[b];
+    lyp.push_back(J / 2 - 1);
+    lyd.push_back((J - 2) / 2);
+    lyd.push_back(J / 2);
+    ply[J] = 1;
+  }
+  P->Kx[0] = (int)lxp.size(); P->Kx[1] = (int)lxd.size();
+  P->Ky[0] = (int)lyp.size(); P->Ky[1] = (int)lyd.size();
+  for (int v : lxp) nxl.push_back(2 * v + 2);
+  for (int v : lxd) nxl.push_back(2 * v + 1);
+  for (int v : lyp) nyl.push_back(2 * v + 2);
+  for (int v : lyd) nyl.push_back(2 * v + 1);
+  // matrices: full F/I per axis and kind, and their layer sub-matrices
+  const int nx = D.nx, ny = D.ny;
+  auto sub_cols = [](const std::vector<zc>& F, int rows, int cols, const std::vector<int>& idx) {
+    std::vector<zc> o((size_t)rows * idx.size());  // F[:, idx]
+    for (int r = 0; r < rows; ++r)
+      for (size_t q = 0; q < idx.size(); ++q) o[(size_t)r * idx.size() + q] = F[(size_t)r * cols + idx[q]];
+    return o;
+  };
+  auto sub_rows = [](const std::vector<zc>& I, int cols, const std::vector<int>& idx) {
+    std::vector<zc> o((size_t)idx.size() * cols);  // I[idx, :]
+    for (size_t q = 0; q < idx.size(); ++q)
+      for (int c = 0; c < cols; ++c) o[q * cols + c] = I[(size_t)idx[q] * cols + c];
+    return o;
+  };
+  struct M { std::vector<zc> v; bool real; size_t off; };
+  std::vector<M> mats;
+  auto add = [&](std::vector<zc> v, bool real) { mats.push_back(M{std::move(v), real, 0}); return (int)mats.size() - 1; };
+  const int npx = nx - 1, npy = ny - 1;
+  const int mFx[2] = {add(X.Fp, X.real), add(X.Fd, X.real)}, mIx[2] = {add(X.Ip, X.real), add(X.Id, X.real)};
+  const int mFy[2] = {add(Y.Fp, Y.real), add(Y.Fd, Y.real)}, mIy[2] = {add(Y.Ip, Y.real), add(Y.Id, Y.real)};
+  const int mFxs[2] = {add(sub_cols(X.Fp, npx, npx, lxp), X.real), add(sub_cols(X.Fd, nx, nx, lxd), X.real)};
+  const int mIxs[2] = {add(sub_rows(X.Ip, npx, lxp), X.real), add(sub_rows(X.Id, nx, lxd), X.real)};
+  const int mFys[2] = {add(sub_cols(Y.Fp, npy, npy, lyp), Y.real), add(sub_cols(Y.Fd, ny, ny, lyd), Y.real)};
+  const int mIys[2] = {add(sub_rows(Y.Ip, npy, lyp), Y.real), add(sub_rows(Y.Id, ny, lyd), Y.real)};
+  size_t o = 0;
+  for (auto& m : mats) {
+    m.off = o;
+    o += al256(std::max<size_t>(1, m.v.size()) * (m.real ? 8 : 16));
+  }
+  // compact slot layout: x-part [f][3 nlev][ny][Kx], then y-part [f][3 nlev][Ky][nx]
+  int64_t cxo[4], cyo[4], c = 0;
+  for (int f = 0; f < 4; ++f) { cxo[f] = c; c += (int64_t)3 * D.nlev[f] * ny * P->Kx[fam_xk(f)]; }
+  for (int f = 0; f < 4; ++f) { cyo[f] = c; c += (int64_t)3 * D.nlev[f] * P->Ky[fam_yk(f)] * nx; }
+  P->compact = std::max<int64_t>(c, 1);
+  P->compact_used = c;
+  const size_t oCxo = o; o += al256(sizeof(int64_t) * 4);
+  const size_t oCyo = o; o += al256(sizeof(int64_t) * 4);
+  const size_t oLx = o; o += al256(sizeof(int) * std::max<size_t>(1, nxl.size()));
+  const size_t oLy = o; o += al256(sizeof(int) * std::max<size_t>(1, nyl.size()));
+  const size_t oIsx = o; o += al256(Nx);
+  const size_t oPlx = o; o += al256(Nx);
+  const size_t oPly = o; o += al256(Ny);
+  std::vector<char> h(o, 0);
+  for (auto& m : mats) {
+    if (m.real) {
+      double* d = reinterpret_cast<double*>(h.data() + m.off);
+      for (size_t q = 0; q < m.v.size(); ++q) d[q] = m.v[q].real();
+    } else {
+      double2* d = reinterpret_cast<double2*>(h.data() + m.off);
+      for (size_t q = 0; q < m.v.size(); ++q) d[q] = make_double2(m.v[q].real(), m.v[q].imag());
+    }
+  }
+  memcpy(h.data() + oCxo, cxo, sizeof cxo);
+  memcpy(h.data() + oCyo, cyo, sizeof cyo);
+  if (!nxl.empty()) memcpy(h.data() + oLx, nxl.data(), sizeof(int) * nxl.size());
+  if (!nyl.empty()) memcpy(h.data() + oLy, nyl.data(), sizeof(int) * nyl.size());
+  memcpy(h.data() + oIsx, isx.data(), Nx);
+  memcpy(h.data() + oPlx, plx.data(), Nx);
+  memcpy(h.data() + oPly, ply.data(), Ny);
+  if (cudaMalloc(&P->d_tab, o) != cudaSuccess || cudaMemcpy(P->d_tab, h.data(), o, cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(mwfail(LFDS_ENOMEM, "step-5 tables"));
+  P->d_cxo = reinterpret_cast<const int64_t*>(P->d_tab + oCxo);
+  P->d_cyo = reinterpret_cast<const int64_t*>(P->d_tab + oCyo);
+  P->d_lx = reinterpret_cast<const int*>(P->d_tab + oLx);
+  P->d_ly = reinterpret_cast<const int*>(P->d_tab + oLy);
+  P->d_isx = reinterpret_cast<const unsigned char*>(P->d_tab + oIsx);
+  P->d_plx = reinterpret_cast<const unsigned char*>(P->d_tab + oPlx);
+  P->d_ply = reinterpret_cast<const unsigned char*>(P->d_tab + oPly);
+  // descriptors: buffers B_F = compact r, B_U = stage-1 compact, B_IF = inverse stage-1 compact,
+  // B_RED = compact w, B_MS = coefficients (x-part), B_T1 = coefficients (y-part)
+  auto ao = [&](int m) { return (int64_t)(mats[m].off / (mats[m].real ? 8 : 16)); };
+  std::vector<lfds::GemmDesc> desc;
+  const int64_t pl = D.plane;
+  for (int g = 0; g < 8; ++g) {
+    for (int f = 0; f < 4; ++f) {
+      const int xk = fam_xk(f), yk = fam_yk(f);
+      const int nxf = xk ? nx : nx - 1, nyf = yk ? ny : ny - 1;
+      const int Kx = P->Kx[xk], Ky = P->Ky[yk];
+      const int64_t nl = 3 * D.nlev[f];
+      lfds::GemmDesc d{};
+      d.N1 = (int)nl;
+      switch (g) {
+        case 0:  // XA: Y1[m][kx] = Fy RXc
+          d.a_off = ao(mFy[yk]); d.sAi = nyf; d.sAj = 1; d.M = d.K = nyf;
+          d.b_buf = lfds::B_F; d.b_off = cxo[f]; d.sBj = Kx; d.sB1 = (int64_t)ny * Kx; d.sB2 = 1; d.N2 = Kx;
+          d.c_buf = lfds::B_U; d.c_off = cxo[f] + (yk ? 0 : Kx); d.sCi = Kx; d.sC1 = (int64_t)ny * Kx; d.sC2 = 1;
+          break;
+        case 1:  // XB: coef[m][l] = sum_kx Y1[m][kx] Fx[l, layer kx]
+          d.a_off = ao(mFxs[xk]); d.sAi = Kx; d.sAj = 1; d.M = nxf; d.K = Kx;
+          d.b_buf = lfds::B_U; d.b_off = cxo[f]; d.sBj = 1; d.sB1 = (int64_t)ny * Kx; d.sB2 = Kx; d.N2 = ny;
+          d.c_buf = lfds::B_MS; d.c_off = D.fam_off[f] + (xk ? 0 : 1); d.sCi = 1; d.sC1 = pl; d.sC2 = nx;
+          break;
+        case 2:  // YA: X1[ky][l] = RYc Fx^T
+          d.a_off = ao(mFx[xk]); d.sAi = nxf; d.sAj = 1; d.M = d.K = nxf;
+          d.b_buf = lfds::B_F; d.b_off = cyo[f]; d.sBj = 1; d.sB1 = (int64_t)Ky * nx; d.sB2 = nx; d.N2 = Ky;
+          d.c_buf = lfds::B_U; d.c_off = cyo[f] + (xk ? 0 : 1); d.sCi = 1; d.sC1 = (int64_t)Ky * nx; d.sC2 = nx;
+          break;
+        case 3:  // YB: coef2[m][l] = sum_ky Fy[m, layer ky] X1[ky][l]
+          d.a_off = ao(mFys[yk]); d.sAi = Ky; d.sAj = 1; d.M = nyf; d.K = Ky;
+          d.b_buf = lfds::B_U; d.b_off = cyo[f]; d.sBj = nx; d.sB1 = (int64_t)Ky * nx; d.sB2 = 1; d.N2 = nx;
+          d.c_buf = lfds::B_T1; d.c_off = D.fam_off[f] + (yk ? 0 : nx); d.sCi = nx; d.sC1 = pl; d.sC2 = 1;
+          break;
+        case 4:  // IXA: Z1[m][kx] = sum_l Ix[layer kx, l] w~[m][l]
+          d.a_off = ao(mIxs[xk]); d.sAi = nxf; d.sAj = 1; d.M = Kx; d.K = nxf;
+          d.b_buf = lfds::B_MS; d.b_off = D.fam_off[f] + (xk ? 0 : 1); d.sBj = 1; d.sB1 = pl; d.sB2 = nx; d.N2 = ny;
+          d.c_buf = lfds::B_IF; d.c_off = cxo[f]; d.sCi = 1; d.sC1 = (int64_t)ny * Kx; d.sC2 = Kx;
+          break;
+        case 5:  // IXB: WXc[y][kx] = Iy Z1
+          d.a_off = ao(mIy[yk]); d.sAi = nyf; d.sAj = 1; d.M = d.K = nyf;
+          d.b_buf = lfds::B_IF; d.b_off = cxo[f] + (yk ? 0 : Kx); d.sBj = Kx; d.sB1 = (int64_t)ny * Kx; d.sB2 = 1;
+          d.N2 = Kx;
+          d.c_buf = lfds::B_RED; d.c_off = cxo[f]; d.sCi = Kx; d.sC1 = (int64_t)ny * Kx; d.sC2 = 1;
+          break;
+        case 6:  // IYA: Z2[ky][l] = sum_m Iy[layer ky, m] w~[m][l]
+          d.a_off = ao(mIys[yk]); d.sAi = nyf; d.sAj = 1; d.M = Ky; d.K = nyf;
+          d.b_buf = lfds::B_MS; d.b_off = D.fam_off[f] + (yk ? 0 : nx); d.sBj = nx; d.sB1 = pl; d.sB2 = 1; d.N2 = nx;
+          d.c_buf = lfds::B_IF; d.c_off = cyo[f]; d.sCi = nx; d.sC1 = (int64_t)Ky * nx; d.sC2 = 1;
+          break;
+        default:  // IYB: WYc[ky][x] = Z2 Ix^T
+          d.a_off = ao(mIx[xk]); d.sAi = nxf; d.sAj = 1; d.M = d.K = nxf;
+          d.b_buf = lfds::B_IF; d.b_off = cyo[f] + (xk ? 0 : 1); d.sBj = 1; d.sB1 = (int64_t)Ky * nx; d.sB2 = nx;
+          d.N2 = Ky;
+          d.c_buf = lfds::B_RED; d.c_off = cyo[f]; d.sCi = 1; d.sC1 = (int64_t)Ky * nx; d.sC2 = nx;
+          break;
+      }
+      desc.push_back(d);
+      P->gM[g] = std::max(P->gM[g], d.M);
+      P->gN[g] = std::max<int64_t>(P->gN[g], (int64_t)d.N1 * d.N2);
+    }
+    const bool xaxis = g == 1 || g == 2 || g == 4 || g == 7;  // contractions along x use x's bases
+    P->gReal[g] = xaxis ? X.real : Y.real;
+    P->gKc[g] = (g == 1 || g == 2 || g == 4 || g == 7);     // K index contiguous in B
+  }
+  if (cudaMalloc(&P->d_desc, desc.size() * sizeof(lfds::GemmDesc)) != cudaSuccess ||
+      cudaMemcpy(P->d_desc, desc.data(), desc.size() * sizeof(lfds::GemmDesc), cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(mwfail(LFDS_ECUDA, "descriptor upload"));
+  *out = P.release();
+  return LFDS_OK;
+}
+
+static size_t mw2_layout(const lfds_mw2* P, size_t off[8]) {
+  const MwDev& D = P->glob->D;
+  const size_t full = al256((size_t)3 * D.Nz * D.Ny * D.Nx * 16);
+  const size_t fam = al256(P->glob->fam_elems * 16), cp = al256(P->glob->cp_elems * 16);
+  const size_t cmp = al256((size_t)P->compact * 16), sub = al256(P->sub_elems * 16);
+  size_t o = 0;
+  off[0] = o; o += full;          // r, then f2
+  off[1] = o; o += full;          // E
+  off[2] = o; o += 2 * fam + cp;  // coef, coef2, Thomas scratch
+  off[3] = o; o += 4 * cmp;       // compact slots
+  off[4] = o; o += sub;           // block f
+  off[5] = o; o += sub;           // block H
+  off[6] = o; o += al256(P->sub_ws);
+  return o;
+}
+
+size_t lfds_mw2_workspace_bytes(const lfds_mw2* P) {
+  if (!P) return 0;
+  size_t off[8];
+  return mw2_layout(P, off);
+}
+
+static cudaError_t box_copy(const lfds_mw2::Blk& B, const MwDev& D, void* full, void* packed, bool to_packed,
+                            bool interior, cudaStream_t st) {
+  const int bx = B.x1 - B.x0 + 1, by = B.y1 - B.y0 + 1;
+  const int e = interior ? 1 : 0;
+  cudaMemcpy3DParms p{};
+  p.extent = make_cudaExtent((size_t)(bx - 2 * e) * 16, by - 2 * e, (size_t)3 * D.Nz);
+  p.kind = cudaMemcpyDeviceToDevice;
+  cudaPitchedPtr F = make_cudaPitchedPtr(full, (size_t)D.Nx * 16, (size_t)D.Nx * 16, D.Ny);
+  cudaPitchedPtr S = make_cudaPitchedPtr(packed, (size_t)bx * 16, (size_t)bx * 16, by);
+  const cudaPos pf = make_cudaPos((size_t)(B.x0 + e) * 16, B.y0 + e, 0), ps = make_cudaPos((size_t)e * 16, e, 0);
+  if (to_packed) { p.srcPtr = F; p.srcPos = pf; p.dstPtr = S; p.dstPos = ps; }
+  else { p.srcPtr = S; p.srcPos = ps; p.dstPtr = F; p.dstPos = pf; }
+  return cudaMemcpy3DAsync(&p, st);
+}
+
+int lfds_mw2_solve(lfds_mw2* P, const void* f_dev, void* h_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (!P || !f_dev || !h_dev || !ws) return mwfail(LFDS_EINVAL, "bad arguments");
+  size_t off[8];
+  if (ws_bytes < mw2_layout(P, off)) return mwfail(LFDS_EINVAL, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  (void)cudaGetLastError();
+  const MwDev& D = P->glob->D;
+  char* w = static_cast<char*>(ws);
+  double2* R = reinterpret_cast<double2*>(w + off[0]);
+  double2* E = reinterpret_cast<double2*>(w + off[1]);
+  double2* coef = reinterpret_cast<double2*>(w + off[2]);
+  double2* coef2 = coef + al256(P->glob->fam_elems * 16) / 16;
+  double2* cp = coef2 + al256(P->glob->fam_elems * 16) / 16;
+  const size_t cmp = al256((size_t)P->compact * 16);
+  char* sf = w + off[4];
+  char* sh = w + off[5];
+  void* sws = w + off[6];
+  double2* H = static_cast<double2*>(h_dev);
+  const double2* F = static_cast<const double2*>(f_dev);
+  const int64_t N = (int64_t)D.Nz * D.Ny * D.Nx;
+  const unsigned gs = (unsigned)std::min<int64_t>((N + 255) / 256, 148 * 16);
+  int rc;
+  auto cuda = [&](cudaError_t x) { return x == cudaSuccess ? LFDS_OK : mwfail(LFDS_ECUDA, "two-level: %s", cudaGetErrorString(x)); };
+  auto blocks = [&](const void* src) -> int {
+    for (auto& B : P->blk) {
+      int q;
+      if ((q = cuda(box_copy(B, D, const_cast<void*>(src), sf, true, false, st)))) return q;
+      if ((q = lfds_mw_solve(B.plan, sf, sh, sws, P->sub_ws, stream))) return q;
+      if ((q = cuda(box_copy(B, D, H, sh, false, true, st)))) return q;
+    }
+    return LFDS_OK;
+  };
+  // 1-3: v on every block, zero on the planes
+  if ((rc = cuda(cudaMemsetAsync(H, 0, (size_t)3 * N * 16, st)))) return rc;
+  if ((rc = blocks(F))) return rc;
+  // 4: r = f - A_h v
+  k_mw_curlh<<<gs, 256, 0, st>>>(D, H, E);
+  k_mw_curle<<<gs, 256, 0, st>>>(D, E, H, F, R);
+  // 5: w on the layers
+  lfds::Bufs b{};
+  b.p[lfds::B_TAB] = P->d_tab;
+  b.p[lfds::B_F] = w + off[3];
+  b.p[lfds::B_U] = w + off[3] + cmp;
+  b.p[lfds::B_IF] = w + off[3] + 2 * cmp;
+  b.p[lfds::B_RED] = w + off[3] + 3 * cmp;
+  b.p[lfds::B_MS] = coef;
+  b.p[lfds::B_T1] = coef2;
+  const int64_t ctot = P->compact_used;
+  const unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ctot + 255) / 256, 148 * 16));
+  if (ctot) k_mw2_gather_r<<<gc, 256, 0, st>>>(D, R, static_cast<double2*>(b.p[lfds::B_F]), P->d_cxo, P->d_cyo, P->d_lx,
+                                     P->d_ly, P->Kx[0], P->Kx[1], P->Ky[0], P->Ky[1], P->d_isx, ctot);
+  if ((rc = cuda(cudaGetLastError()))) return rc;
+  auto group = [&](int g) {  // (empty when the axis has no interfaces; XB / YB then write zeros)
+    if (P->gM[g] == 0 || P->gN[g] == 0) return cudaSuccess;
+    return lfds::launch_xform(P->d_desc + 4 * g, 4, P->gM[g], P->gN[g], P->gReal[g], P->gKc[g], b, st);
+  };
+  for (int g = 0; g < 4; ++g)
+    if ((rc = cuda(group(g)))) return rc;
+  k_mw_zsolve<<<(unsigned)((4 * D.plane + 127) / 128), 128, 0, st>>>(D, coef, cp, coef2);
+  if ((rc = cuda(cudaGetLastError()))) return rc;
+  for (int g = 4; g < 8; ++g)
+    if ((rc = cuda(group(g)))) return rc;
+  if (ctot) k_mw2_add_w<<<gc, 256, 0, st>>>(D, static_cast<const double2*>(b.p[lfds::B_RED]), H, P->d_cxo, P->d_cyo, P->d_lx,
+                                  P->d_ly, P->Kx[0], P->Kx[1], P->Ky[0], P->Ky[1], P->d_isx, ctot);
+  // 6: interface data lifted into the right side (into R)
+  k_mw2_elift<<<gs, 256, 0, st>>>(D, H, E, P->d_plx, P->d_ply);
+  k_mw2_flift<<<gs, 256, 0, st>>>(D, E, F, R, P->d_plx, P->d_ply);
+  if ((rc = cuda(cudaGetLastError()))) return rc;
+  // 7: every block with its interface data; H = w stays on the plane P nodes
+  if ((rc = blocks(R))) return rc;
+  return cuda(cudaGetLastError());
+}
+
+int lfds_mw2_blocks(const lfds_mw2* P, int* n) {
+  if (!P || !n) return mwfail(LFDS_EINVAL, "bad arguments");
+  *n = (int)P->blk.size();
   return LFDS_OK;
 }
 

@@ -126,6 +126,13 @@ _lib.lfds_mw_kernel_name.restype = ctypes.c_char_p
 _lib.lfds_mw_kernel_times.argtypes = [_P, _P, _P]
 _lib.lfds_mw_destroy.argtypes = [_P]
 _lib.lfds_mw_last_error.restype = ctypes.c_char_p
+_lib.lfds_mw2_setup.argtypes = [ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P, _P, _P, _Z, ctypes.c_double,
+                                ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P]
+_lib.lfds_mw2_workspace_bytes.argtypes = [_P]
+_lib.lfds_mw2_workspace_bytes.restype = ctypes.c_size_t
+_lib.lfds_mw2_solve.argtypes = [_P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.lfds_mw2_blocks.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
+_lib.lfds_mw2_destroy.argtypes = [_P]
 
 EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
             "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_get_report",
@@ -138,7 +145,8 @@ EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "
             "lfds_ml_solve", "lfds_ml_get_plans", "lfds_ml_destroy", "lfds_ml_last_error",
             "lfds_mw_setup", "lfds_mw_workspace_bytes", "lfds_mw_solve", "lfds_mw_residual",
             "lfds_mw_kernel_count", "lfds_mw_kernel_name", "lfds_mw_kernel_times", "lfds_mw_destroy",
-            "lfds_mw_last_error"]
+            "lfds_mw_last_error", "lfds_mw2_setup", "lfds_mw2_workspace_bytes", "lfds_mw2_solve",
+            "lfds_mw2_blocks", "lfds_mw2_destroy"]
 
 
 def _check(rc):
@@ -597,6 +605,64 @@ class MWPlan:
             self.close()
         except Exception:
             pass
+
+
+class MW2Plan(MWPlan):
+    """Two-level (blocked) Maxwell solve, lfds_mw2_setup: x-interfaces ix and
+    y-interfaces iy (even node indices) split the grid into blocks; H = H^1 + H^2."""
+
+    def __init__(self, hx, hy, hz, c1, c2, c3, mu, omega: float, ix=(), iy=(), *, device: int = 0):
+        hx_, px = _zarr(hx); hy_, py = _zarr(hy); hz_, pz = _zarr(hz)
+        a1, p1 = _zarr(c1); a2, p2 = _zarr(c2); a3, p3 = _zarr(c3)
+        ix_ = np.ascontiguousarray(np.asarray(list(ix), dtype=np.int32))
+        iy_ = np.ascontiguousarray(np.asarray(list(iy), dtype=np.int32))
+        mu = complex(mu)
+        h = _P()
+        _mw_check(_lib.lfds_mw2_setup(len(hx_) + 1, px, len(hy_) + 1, py, len(hz_) + 1, pz, p1, p2, p3,
+                                      _Z(mu.real, mu.imag), float(omega), len(ix_), ix_.ctypes.data_as(_P),
+                                      len(iy_), iy_.ctypes.data_as(_P), int(device), ctypes.byref(h)))
+        self._h = h
+        self.device = int(device)
+        self.shape = (3, len(hz_) + 1, len(hy_) + 1, len(hx_) + 1)
+        self._ws = None
+
+    @classmethod
+    def from_problem(cls, p, ix=(), iy=(), **kw):
+        return cls(p.hx, p.hy, p.hz, p.c1, p.c2, p.c3, p.mu, p.omega, ix, iy, **kw)
+
+    def n_blocks(self) -> int:
+        n = ctypes.c_int()
+        _mw_check(_lib.lfds_mw2_blocks(self._h, ctypes.byref(n)))
+        return n.value
+
+    def workspace(self):
+        import torch
+        nb = int(_lib.lfds_mw2_workspace_bytes(self._h))
+        if self._ws is None or self._ws.numel() < nb:
+            self._ws = torch.empty(nb, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        return self._ws
+
+    def solve(self, f, out=None, stream=None):
+        import torch
+        self._chk(f, "f")
+        H = torch.empty_like(f) if out is None else out
+        self._chk(H, "out")
+        ws = self.workspace()
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _mw_check(_lib.lfds_mw2_solve(self._h, _P(f.data_ptr()), _P(H.data_ptr()), _P(ws.data_ptr()), ws.numel(),
+                                      _P(st)))
+        return H
+
+    def residual(self, H, f, out=None, stream=None):
+        raise NotImplementedError("use an MWPlan of the same grid for residuals")
+
+    def kernel_times(self) -> dict:
+        return {}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lfds_mw2_destroy(self._h)
+            self._h = None
 
 
 def setup_grid(hx, hy, hz, sigma_node, sigma_edge, lam, iface_x=(), iface_y=(), **kw) -> Plan:

@@ -140,3 +140,33 @@ def test_maxwell_rejects_even_node_counts():
     p = make_mw("mw_tiny")
     with pytest.raises(LfdsError, match="odd"):
         MWPlan(np.ones(7), p.hy, p.hz, p.c1, p.c2, p.c3, p.mu, p.omega)
+
+
+@pytest.mark.parametrize("name,ix,iy", [
+    ("mw_s", [8], [6]),          # 2 x 2 blocks
+    ("mw_s2", [8, 16], [10]),    # 3 x 2 blocks, PML in the outer blocks
+    ("mw_s", [4, 10], []),       # x-interfaces only (a 5-node block)
+    ("mw_s2", [], [6, 12]),      # y-interfaces only
+    ("mw_s", [], []),            # one block: step 5 has nothing to do
+])
+def test_two_level_maxwell_matches_oracle(name, ix, iy):
+    """H = H^1 + H^2 through lfds_mw2_*: the oracle's sparse-LU solution to
+    the 1e-9 bar, and the layered (single-block) GPU solve to 1e-11."""
+    from paper_1909_01299_b200 import MW2Plan
+    p = make_mw(name)
+    f = p.rhs()
+    g, ref = _oracle(p, f)
+    plan = MW2Plan.from_problem(p, ix, iy)
+    assert plan.n_blocks() == (len(ix) + 1) * (len(iy) + 1)
+    fd = torch.from_numpy(f).cuda()
+    H = plan.solve(fd).cpu().numpy()
+    _check(p, g, H, ref)
+    H1 = _plan(p).solve(fd).cpu().numpy()
+    assert np.linalg.norm(H - H1) / np.linalg.norm(H1) < 1e-11
+
+
+def test_two_level_maxwell_rejects_odd_interfaces():
+    from paper_1909_01299_b200 import MW2Plan, LfdsError
+    p = make_mw("mw_s")
+    with pytest.raises(LfdsError, match="even"):
+        MW2Plan.from_problem(p, [7], [])

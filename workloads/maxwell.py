@@ -112,3 +112,31 @@ def make_mw(name: str) -> MWProblem:
     c3 = rv[layer].astype(np.complex128)
     omega = 2.0 * rh.min() / delta ** 2
     return MWProblem(name, hx, hy, hz, c1, c2, c3, 1.0 + 0j, float(omega), nsrc, cfg)
+
+
+def rhs_torch(p: MWProblem, device="cuda"):
+    """The same recipe as MWProblem.rhs() drawn on the device with torch's generator (seed
+    1909 * 1000 + cfg): full-size fields (3 x 257 x 513 x 513 complex128 = 3.2 GB) are not built
+    in numpy.  Only the layout (interior P nodes) is used, no arithmetic of the method."""
+    import torch
+    nz, ny, nx = p.shape
+    g = torch.Generator(device=device)
+    g.manual_seed(1909 * 1000 + p.cfg)
+    f = torch.randn((3, nz, ny, nx), dtype=torch.complex128, device=device, generator=g) * 1e-3
+    k = torch.arange(nz, device=device)[:, None, None]
+    j = torch.arange(ny, device=device)[None, :, None]
+    i = torch.arange(nx, device=device)[None, None, :]
+    unk = ((i + j + k) % 2 == 0) & (i > 0) & (i < nx - 1) & (j > 0) & (j < ny - 1) & (k > 0) & (k < nz - 1)
+    f *= unk
+    rs = _rng(p.cfg, 3)
+    placed = 0
+    while placed < p.nsrc:
+        c = int(rs.integers(0, 3))
+        kk = int(rs.integers(1, nz - 1))
+        jj = int(rs.integers(max(1, ny // 4), max(2, 3 * ny // 4)))
+        ii = int(rs.integers(max(1, nx // 4), max(2, 3 * nx // 4)))
+        if (ii + jj + kk) % 2:
+            continue
+        f[c, kk, jj, ii] += complex(rs.standard_normal(), rs.standard_normal())
+        placed += 1
+    return f
