@@ -72,13 +72,9 @@ __device__ __forceinline__ cx operator-(cx a, cx b) { return cx{a.x - b.x, a.y -
 __device__ __forceinline__ cx operator-(cx a) { return cx{-a.x, -a.y}; }
 __device__ __forceinline__ cx operator*(cx a, cx b) { return cx{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
 __device__ __forceinline__ cx cinv(cx a) {
-  // Smith-style scaling against overflow / underflow
-  if (fabs(a.x) >= fabs(a.y)) {
-    const double r = a.y / a.x, d = a.x + a.y * r;
-    return cx{1.0 / d, -r / d};
-  }
-  const double r = a.x / a.y, d = a.y + a.x * r;
-  return cx{r / d, -1.0 / d};
+  // one division: |a|^2 of the z-system entries stays far inside the double range
+  const double r = 1.0 / fma(a.x, a.x, a.y * a.y);
+  return cx{a.x * r, -a.y * r};
 }
 struct m2 {  // 2x2 complex matrix [[a, b], [c, d]]
   cx a, b, c, d;
@@ -114,6 +110,7 @@ struct MwDev {
   const double2* lam;  // nx (lambda_l, lambda_0 = 0)
   const double2* nu;   // ny
   const double2* lev;  // per level k: [dz_k, c1, c2, c3] (4 Nz)
+  const double2* idz;  // 1 / dz_k (Nz)
   const double2* dxx;  // x_{i+1} - x_{i-1} per node (Nx), dyy (Ny), dzz (Nz)
   const double2* dyy;
   const double2* dzz;
@@ -220,7 +217,7 @@ __global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict_
   v2 Yprev{};
   for (int r = 0; r < nX; ++r) {
     const int k = k0 + 2 * r;
-    const cx dz = ld(D.lev + 4 * k), idz = cinv(dz);
+    const cx idz = ld(D.idz + k);
     const bool gp = interior(k + 1);
     Lev Lp{};
     cx fzp = zero;
@@ -230,11 +227,11 @@ __global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict_
     }
     m2 Ap{zero, zero, zero, zero}, Am{zero, zero, zero, zero};
     if (gp) {
-      const cx w = idz * cinv(ld(D.lev + 4 * (k + 1)));
+      const cx w = idz * ld(D.idz + k + 1);
       Ap = m2{Lp.SQ.a * w, Lp.SQ.b * w, Lp.SQ.c * w, Lp.SQ.d * w};
     }
     if (gm) {
-      const cx w = idz * cinv(ld(D.lev + 4 * (k - 1)));
+      const cx w = idz * ld(D.idz + k - 1);
       Am = m2{Lm.SQ.a * w, Lm.SQ.b * w, Lm.SQ.c * w, Lm.SQ.d * w};
     }
     const cx c3 = ld(D.lev + 4 * k + 3);
@@ -265,7 +262,7 @@ __global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict_
   // backward sweep, H_z at the level between X(k) and X(k + 2) (and below the first X level)
   auto hz_at = [&](int kz, v2 Xlo, v2 Xhi) {  // X at kz - 1, kz + 1
     const Lev L = level_terms(D, kz, sx, sy);
-    const cx idz = cinv(ld(D.lev + 4 * kz));
+    const cx idz = ld(D.idz + kz);
     const cx dzx = (Xhi.x - Xlo.x) * idz, dzy = (Xhi.y - Xlo.y) * idz;
     const cx v = (rdz(kz) + sx * L.c2 * dzx + sy * L.c1 * dzy) * L.idel;
     st(FZ + (int64_t)lev_of(fz, kz) * D.plane, az ? zero : v);
@@ -526,6 +523,7 @@ int lfds_mw_setup(int Nx, const lfds_z* hx, int Ny, const lfds_z* hy, int Nz, co
   const size_t oDx = o; o += al256(16 * (size_t)Nx);
   const size_t oDy = o; o += al256(16 * (size_t)Ny);
   const size_t oDz = o; o += al256(16 * (size_t)Nz);
+  const size_t oIdz = o; o += al256(16 * (size_t)Nz);
   std::vector<char> h(o, 0);
   auto put = [&](size_t at, const std::vector<zc>& v, bool real) {
     if (real) {
@@ -540,11 +538,17 @@ int lfds_mw_setup(int Nx, const lfds_z* hx, int Ny, const lfds_z* hy, int Nz, co
   put(oFpy, Y.Fp, Y.real); put(oIpy, Y.Ip, Y.real); put(oFdy, Y.Fd, Y.real); put(oIdy, Y.Id, Y.real);
   put(oLam, X.lam, false); put(oNu, Y.lam, false); put(oLev, lev, false);
   put(oDx, X.dnode, false); put(oDy, Y.dnode, false); put(oDz, Z.dnode, false);
+  {
+    std::vector<zc> idz(Nz);
+    for (int k = 0; k < Nz; ++k) idz[k] = 1.0 / Z.dnode[k];
+    put(oIdz, idz, false);
+  }
   if (cudaMalloc(&P->d_mem, o) != cudaSuccess) return mwfail(LFDS_ENOMEM, "device tables (%zu bytes)", o);
   if (cudaMemcpy(P->d_mem, h.data(), o, cudaMemcpyHostToDevice) != cudaSuccess)
     return mwfail(LFDS_ECUDA, "table upload");
   auto dp = [&](size_t at) { return reinterpret_cast<const double2*>(P->d_mem + at); };
   D.lam = dp(oLam); D.nu = dp(oNu); D.lev = dp(oLev); D.dxx = dp(oDx); D.dyy = dp(oDy); D.dzz = dp(oDz);
+  D.idz = dp(oIdz);
   // transform descriptors (lfds_internal.h GemmDesc: C(i, n) = sum_j S(i, j) B(j, n)); the
   // buffers are B_MS = FAM (node data / coefficients) and B_T1 = T (half-transformed)
   std::vector<lfds::GemmDesc> desc;

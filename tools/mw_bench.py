@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--config", default="mw1")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--two-level", type=int, nargs="*", default=[], dest="two",
+                    help="also time the two-level solve with B x B blocks for each B given")
     a = ap.parse_args()
     p = make_mw(a.config)
     nz, ny, nx = p.shape
@@ -65,6 +67,32 @@ def main():
         prof.solve(f, out=H)
     kt = prof.kernel_times()
     prof.close()
+    two = {}
+    for B in a.two:
+        from paper_1909_01299_b200 import MW2Plan
+        step = (nx - 1) // B
+        ix = [b * step - (b * step) % 2 for b in range(1, B)]
+        stepy = (ny - 1) // B
+        iy = [b * stepy - (b * stepy) % 2 for b in range(1, B)]
+        p2 = MW2Plan.from_problem(p, ix, iy)
+        H2 = torch.empty_like(f)
+        for _ in range(a.warmup):
+            p2.solve(f, out=H2)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(a.steps):
+            p2.solve(f, out=H2)
+        e1.record()
+        torch.cuda.synchronize()
+        ms2 = e0.elapsed_time(e1) / a.steps
+        r2 = plan.residual(H2, f)
+        two[f"{B}x{B}"] = {"ix": ix, "iy": iy, "ms": ms2, "rel_residual": float(torch.linalg.vector_norm(r2) /
+                                                                              torch.linalg.vector_norm(f)),
+                           "rel_diff_vs_layered": float(torch.linalg.vector_norm(H2 - H) / torch.linalg.vector_norm(H)),
+                           "workspace_gb": p2.workspace().numel() / 1e9}
+        del r2, H2
+        p2.close()
+        torch.cuda.empty_cache()
     plan.close()
     n = (nx - 1) // 2, (ny - 1) // 2, (nz - 1) // 2
     # unknowns: 3 components on the interior P nodes (i + j + k even, 1 <= i <= N - 2)
@@ -107,7 +135,7 @@ def main():
            "config": {"workload": a.config, "grid_nodes": [nx, ny, nz], "unknowns": unknowns,
                       "real_bases": [realx, realy], "rel_residual": rel, "l2": "inputs > L2 (3.2 GB fields)"},
            "roofline": dict(kernels[dom], kernel=dom), "kernels": kernels, "fp64_peak_tflops_in_run": peak_fp64,
-           "hbm_peak_source": hsrc, "kernel_times_from": "CUDA events per launch group, profiled solves after the timed region"}
+           "hbm_peak_source": hsrc, "two_level": two, "kernel_times_from": "CUDA events per launch group, profiled solves after the timed region"}
     print(json.dumps(out))
 
 
