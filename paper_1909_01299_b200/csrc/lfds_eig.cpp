@@ -25,7 +25,9 @@ namespace lfds {
 using lc = std::complex<long double>;
 static inline long double abs1(lc z) { return std::fabs(z.real()) + std::fabs(z.imag()); }
 
-// implicit QL on (d, e), e[i] couples i and i+1; returns false on non-convergence/breakdown
+// implicit QL on (d, e), e[i] couples i and i+1; returns false on non-convergence/breakdown.
+// The textbook implicit-shift QL iteration (the EISPACK tql1 / Numerical Recipes tqli loop
+// structure), here complexified for complex-symmetric pencils and run in long double.
 static bool ql_values(std::vector<lc>& d, std::vector<lc> e) {
   const int n = (int)d.size();
   if (n <= 1) return true;
@@ -79,7 +81,9 @@ static bool ql_values(std::vector<lc>& d, std::vector<lc> e) {
   return true;
 }
 
-// one eigenvector of the tridiagonal (d, e) at eigenvalue mu by inverse iteration
+// one eigenvector of the tridiagonal (d, e) at eigenvalue mu by inverse iteration; the shifted
+// matrix is factored by LU with partial pivoting in the dl / d / du / du2 band layout of LAPACK's
+// zgttrf (the standard algorithm, written out here in long double).
 static void inverse_iteration(const std::vector<lc>& d, const std::vector<lc>& e, lc mu, long double snorm,
                               std::vector<lc>& x, int seed, int iters, bool fresh) {
   const int n = (int)d.size();
