@@ -273,7 +273,15 @@ constexpr int X3_THREADS = 256;
 template <bool KCONTIG>
 __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __restrict__ descs, int gm, Bufs bufs) {
   extern __shared__ __align__(16) double xsm[];
-  const GemmDesc& D = descs[blockIdx.z];
+  // the descriptor in shared memory: read from global memory it is re-fetched after every
+  // barrier (the compiler cannot keep it in registers at the 128-register cap; ncu: ~10 % of
+  // the stall samples were integer ops waiting on those loads)
+  __shared__ GemmDesc sD;
+  __shared__ int64_t sboff[4][X3_THREADS];  // KCONTIG: this thread's four B column offsets
+  if (threadIdx.x < (int)(sizeof(GemmDesc) / 8))
+    reinterpret_cast<int64_t*>(&sD)[threadIdx.x] = reinterpret_cast<const int64_t*>(descs + blockIdx.z)[threadIdx.x];
+  __syncthreads();
+  const GemmDesc& D = sD;
   const int M = D.M, K = D.K;
   const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
   const int i0 = (int)(blockIdx.x % gm) * XT_M;  // row tiles fastest (B tile reuse in L2)
@@ -288,14 +296,20 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
   // A: 64 x 16 -> thread row tid/4, 4 consecutive j
   const int ai = tid >> 2, aj0 = (tid & 3) * 4;
   const bool arow_ok = (i0 + ai) < M;
-  // KCONTIG: thread -> j = tid % 16, columns tid/16 + 16e (e < 4), offsets stepped from the
-  // first column in every chunk (no per-column registers to keep: this kernel is at the
-  // 128-register cap of two CTAs per SM); otherwise thread -> column tid % 64, rows tid/64 + 4e
+  // KCONTIG: thread -> j = tid % 16, columns tid/16 + 16e (e < 4), their offsets in shared
+  // memory (no registers to keep them in: this kernel is at the 128-register cap of two CTAs
+  // per SM); otherwise thread -> column tid % 64, rows tid/64 + 4e
   int bj, bn0;
   int64_t bcol0, bn1_0, bn2_0;
   if (KCONTIG) {
     bj = tid & 15;
     bn0 = tid >> 4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t n = n0 + bn0 + 16 * e;
+      const int64_t n1 = n / N2, n2 = n - n1 * N2;
+      sboff[e][tid] = n < N ? n1 * D.sB1 + n2 * D.sB2 : -1;
+    }
   } else {
     bj = tid >> 6;
     bn0 = tid & 63;
@@ -317,18 +331,11 @@ __global__ void __launch_bounds__(X3_THREADS, 2) k_xform3m(const GemmDesc* __res
     }
     if (KCONTIG) {
       const int j = j0 + bj;
-      int64_t n = n0 + bn0, n1 = bn1_0, n2 = bn2_0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const bool ok = n < N && j < K;
-        cp_async16(Bs + bj * LDB_C + bn0 + 16 * e, ok ? B + n1 * D.sB1 + n2 * D.sB2 + j : B, ok);
-        n += 16;
-        if (N2 == 1) {  // plane transforms: one column per n1
-          n1 += 16;
-        } else {        // block transforms (N2 = block height >= 16: one wrap at most)
-          n2 += 16;
-          while (n2 >= N2) { n2 -= N2; ++n1; }
-        }
+        const int64_t o = sboff[e][tid];
+        const bool ok = o >= 0 && j < K;
+        cp_async16(Bs + bj * LDB_C + bn0 + 16 * e, ok ? B + o + j : B, ok);
       }
     } else {
 #pragma unroll
