@@ -370,71 +370,92 @@ __device__ __forceinline__ zdd zmul_zd(zdd a, cplx b) {  // dd x double complex
   return zdd{dd_add(m(a.x, b.x), dd_neg(m(a.y, b.y))), dd_add(m(a.x, b.y), m(a.y, b.x))};
 }
 
-// One thread per node: grid (x-tiles of 128, y, r*nz + k).  The double-double path evaluates
-// the residual in f-units, r_f = f - (A u)/V with V = hx^ hy^ hz^:
+// One thread per (i, j) column of a z-chunk: grid (x-tiles of 128, y, r * nchunks + chunk); the
+// thread marches k through its chunk of RZ_CHUNK planes with u(k-1), u(k), u(k+1) in registers,
+// so u is read from HBM about once (the x / y neighbours of a plane come from L1 / L2) and the
+// norms are reduced per column.  The double-double path evaluates the residual in f-units,
+// r_f = f - (A u)/V with V = hx^ hy^ hz^:
 //   (A u)/V = sigma_k [cxr (u_{i+1} - u_i) - cxl (u_i - u_{i-1}) + cyr (..) - cyl (..)]
 //           + czr (u_{k+1} - u_k) - czl (u_k - u_{k-1}) + lambda u_i,
 // cxl_i = 1/(h_{i-1} hx^_i), cxr_i = 1/(h_i hx^_i), czl_k = sigma_{k-1/2}/(h_{k-1} hz^_k), ...
 // from the plan's long-double tables (Eq. (fd) divided by the control volume, term by term).
+constexpr int RZ_CHUNK = 32;
 __global__ void __launch_bounds__(128) k_residual(ResParams P, const void* __restrict__ u, const void* __restrict__ f,
                                                   double2* __restrict__ rout, double* norms, Bufs bufs) {
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const int nx = P.nx, ny = P.ny, nz = P.nz;
+  const int nch = (nz + RZ_CHUNK - 1) / RZ_CHUNK;
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
-  const int r = blockIdx.z / nz, k = blockIdx.z - r * nz;
+  const int r = blockIdx.z / nch, kc = blockIdx.z - r * nch;
+  const int kb = kc * RZ_CHUNK, ke = min(nz, kb + RZ_CHUNK);
   const int64_t plane = (int64_t)nx * ny;
   double acc_r = 0, acc_b = 0;
-  if (i < nx) {
-    const int64_t t = ((int64_t)r * nz + k) * plane + (int64_t)j * nx + i;
-    const cplx uc = load_u(u, P.dtype, t);
-    const cplx ul = i > 0 ? load_u(u, P.dtype, t - 1) : mk(0, 0);
-    const cplx ur = i < nx - 1 ? load_u(u, P.dtype, t + 1) : mk(0, 0);
-    const cplx us = j > 0 ? load_u(u, P.dtype, t - nx) : mk(0, 0);
-    const cplx un = j < ny - 1 ? load_u(u, P.dtype, t + nx) : mk(0, 0);
-    const cplx ub = k > 0 ? load_u(u, P.dtype, t - plane) : mk(0, 0);
-    const cplx ut = k < nz - 1 ? load_u(u, P.dtype, t + plane) : mk(0, 0);
-    const cplx cx = ld(TAB + P.hhx + i), cy = ld(TAB + P.hhy + j), cz = ld(TAB + P.hhz + k);
-    const cplx sg = ld(TAB + P.sig + k);
+  // every lane runs the loop (the x neighbours of a plane come from the neighbouring lanes'
+  // registers by shuffles); lanes past the row end only take part in the shuffles
+  const bool ok = i < nx;
+  const int lane = threadIdx.x & 31;
+  {
+    const int ii = ok ? i : nx - 1;
+    const int64_t col = (int64_t)r * nz * plane + (int64_t)j * nx + ii;
+    const cplx cx = ld(TAB + P.hhx + ii), cy = ld(TAB + P.hhy + j);
     const cplx lam = mk(P.lam.x, P.lam.y);
-    const cplx fv = P.has_f ? load_f(f, P.dtype, t) : mk(0, 0);
-    const cplx V = cx * cy * cz;
-    cplx res, bnorm;
-    if (!P.dd) {
-      // fp64: the same f-units evaluation from the per-node stencil tables (their leading
-      // doubles), no per-point reciprocals
-      auto t64 = [&](int64_t off, int n, int e) {
-        const double2 a = __ldg(TAB + off + 4 * n + 2 * e), b = __ldg(TAB + off + 4 * n + 2 * e + 1);
-        return mk(a.x, b.x);
-      };
-      const cplx hx = (ur - uc) * t64(P.rxd, i, 1) - (uc - ul) * t64(P.rxd, i, 0);
-      const cplx hy = (un - uc) * t64(P.ryd, j, 1) - (uc - us) * t64(P.ryd, j, 0);
-      const cplx hz = (ut - uc) * t64(P.szd, k, 1) - (uc - ub) * t64(P.szd, k, 0);
-      const cplx Lu = sg * (hx + hy) + hz + lam * uc;
-      const cplx rf = fv - Lu;
-      res = P.to_f ? rf : rf * V;
-      bnorm = fv * V;
-    } else {
-      auto tdd = [&](int64_t off, int n, int e) {  // node table: [n][cl, cr], 2 slots each
-        const double2 a = __ldg(TAB + off + 4 * n + 2 * e), b = __ldg(TAB + off + 4 * n + 2 * e + 1);
-        return zdd{dd{a.x, a.y}, dd{b.x, b.y}};
-      };
-      const zdd Uc = zfrom(uc);
-      zdd h = zsub(zmul(zsub(zfrom(ur), Uc), tdd(P.rxd, i, 1)), zmul(zsub(Uc, zfrom(ul)), tdd(P.rxd, i, 0)));
-      h = zadd(h, zsub(zmul(zsub(zfrom(un), Uc), tdd(P.ryd, j, 1)), zmul(zsub(Uc, zfrom(us)), tdd(P.ryd, j, 0))));
-      zdd Lu = zmul_zd(h, sg);
-      Lu = zadd(Lu, zsub(zmul(zsub(zfrom(ut), Uc), tdd(P.szd, k, 1)), zmul(zsub(Uc, zfrom(ub)), tdd(P.szd, k, 0))));
-      Lu = zadd(Lu, zmul_zd(zfrom(uc), lam));
-      const zdd rf = zsub(zfrom(fv), Lu);
-      const cplx rfc = mk(rf.x.hi + rf.x.lo, rf.y.hi + rf.y.lo);
-      res = P.to_f ? rfc : rfc * V;
-      bnorm = fv * V;
+    cplx ub = kb > 0 ? load_u(u, P.dtype, col + (int64_t)(kb - 1) * plane) : mk(0, 0);
+    cplx uc = load_u(u, P.dtype, col + (int64_t)kb * plane);
+    for (int k = kb; k < ke; ++k) {
+      const int64_t t = col + (int64_t)k * plane;
+      const cplx ut = k < nz - 1 ? load_u(u, P.dtype, t + plane) : mk(0, 0);
+      cplx ul = mk(__shfl_up_sync(0xffffffffu, uc.x, 1), __shfl_up_sync(0xffffffffu, uc.y, 1));
+      cplx ur = mk(__shfl_down_sync(0xffffffffu, uc.x, 1), __shfl_down_sync(0xffffffffu, uc.y, 1));
+      if (lane == 0) ul = i > 0 && ok ? load_u(u, P.dtype, t - 1) : mk(0, 0);
+      if (lane == 31 || i >= nx - 1) ur = i < nx - 1 ? load_u(u, P.dtype, t + 1) : mk(0, 0);
+      const cplx us = j > 0 ? load_u(u, P.dtype, t - nx) : mk(0, 0);
+      const cplx un = j < ny - 1 ? load_u(u, P.dtype, t + nx) : mk(0, 0);
+      const cplx cz = ld(TAB + P.hhz + k);
+      const cplx sg = ld(TAB + P.sig + k);
+      const cplx fv = P.has_f ? load_f(f, P.dtype, t) : mk(0, 0);
+      const cplx V = cx * cy * cz;
+      cplx res, bnorm;
+      if (!P.dd) {
+        // fp64: the same f-units evaluation from the per-node stencil tables (their leading
+        // doubles), no per-point reciprocals
+        auto t64 = [&](int64_t off, int n, int e) {
+          const double2 a = __ldg(TAB + off + 4 * n + 2 * e), b = __ldg(TAB + off + 4 * n + 2 * e + 1);
+          return mk(a.x, b.x);
+        };
+        const cplx hx = (ur - uc) * t64(P.rxd, i, 1) - (uc - ul) * t64(P.rxd, i, 0);
+        const cplx hy = (un - uc) * t64(P.ryd, j, 1) - (uc - us) * t64(P.ryd, j, 0);
+        const cplx hz = (ut - uc) * t64(P.szd, k, 1) - (uc - ub) * t64(P.szd, k, 0);
+        const cplx Lu = sg * (hx + hy) + hz + lam * uc;
+        const cplx rf = fv - Lu;
+        res = P.to_f ? rf : rf * V;
+        bnorm = fv * V;
+      } else {
+        auto tdd = [&](int64_t off, int n, int e) {  // node table: [n][cl, cr], 2 slots each
+          const double2 a = __ldg(TAB + off + 4 * n + 2 * e), b = __ldg(TAB + off + 4 * n + 2 * e + 1);
+          return zdd{dd{a.x, a.y}, dd{b.x, b.y}};
+        };
+        const zdd Uc = zfrom(uc);
+        zdd h = zsub(zmul(zsub(zfrom(ur), Uc), tdd(P.rxd, i, 1)), zmul(zsub(Uc, zfrom(ul)), tdd(P.rxd, i, 0)));
+        h = zadd(h, zsub(zmul(zsub(zfrom(un), Uc), tdd(P.ryd, j, 1)), zmul(zsub(Uc, zfrom(us)), tdd(P.ryd, j, 0))));
+        zdd Lu = zmul_zd(h, sg);
+        Lu = zadd(Lu, zsub(zmul(zsub(zfrom(ut), Uc), tdd(P.szd, k, 1)), zmul(zsub(Uc, zfrom(ub)), tdd(P.szd, k, 0))));
+        Lu = zadd(Lu, zmul_zd(zfrom(uc), lam));
+        const zdd rf = zsub(zfrom(fv), Lu);
+        const cplx rfc = mk(rf.x.hi + rf.x.lo, rf.y.hi + rf.y.lo);
+        res = P.to_f ? rfc : rfc * V;
+        bnorm = fv * V;
+      }
+      if (ok) {
+        if (rout) rout[t] = make_double2(res.x, res.y);
+        const cplx rb = P.to_f ? res * V : res;
+        acc_r += rb.x * rb.x + rb.y * rb.y;
+        acc_b += bnorm.x * bnorm.x + bnorm.y * bnorm.y;
+      }
+      ub = uc;
+      uc = ut;
     }
-    if (rout) rout[t] = make_double2(res.x, res.y);
-    const cplx rb = P.to_f ? res * V : res;
-    acc_r = rb.x * rb.x + rb.y * rb.y;
-    acc_b = bnorm.x * bnorm.x + bnorm.y * bnorm.y;
   }
-  if (norms) {  // warp sums, one atomic pair per warp
+  if (norms) {  // warp sums, one atomic pair per warp and chunk
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       acc_r += __shfl_xor_sync(0xffffffffu, acc_r, o);
@@ -453,8 +474,9 @@ cudaError_t launch_residual(int nx, int ny, int nz, int R, int dtype, int ddm, i
                             double* d_norms, const Bufs& bufs, cudaStream_t st) {
   ResParams P{nx, ny, nz, R, dtype, ddm, has_f, to_f_units, hx, hy, hz, hhx, hhy, hhz, sig, sige, lam,
               ddtabs[0], ddtabs[1], ddtabs[2]};
-  if ((int64_t)nz * R > 65535 || ny > 65535) return cudaErrorInvalidValue;
-  k_residual<<<dim3((unsigned)((nx + 127) / 128), (unsigned)ny, (unsigned)(nz * R)), 128, 0, st>>>(P, u, f, r, d_norms,
+  const int64_t nch = (nz + RZ_CHUNK - 1) / RZ_CHUNK;
+  if (nch * R > 65535 || ny > 65535) return cudaErrorInvalidValue;
+  k_residual<<<dim3((unsigned)((nx + 127) / 128), (unsigned)ny, (unsigned)(nch * R)), 128, 0, st>>>(P, u, f, r, d_norms,
                                                                                                     bufs);
   return cudaGetLastError();
 }

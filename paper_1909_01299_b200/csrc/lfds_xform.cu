@@ -77,7 +77,11 @@ __global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict
   constexpr int TM = SMALLM ? 32 : XT_M;
   constexpr int NJ = SMALLM ? 4 : 8;  // real-view 8-column tiles per warp
   extern __shared__ __align__(16) double xsm[];
-  const GemmDesc& D = descs[blockIdx.z];
+  __shared__ GemmDesc sD;  // (see k_xform3m: global-memory descriptor fields are re-read after barriers)
+  if (threadIdx.x < (int)(sizeof(GemmDesc) / 8))
+    reinterpret_cast<int64_t*>(&sD)[threadIdx.x] = reinterpret_cast<const int64_t*>(descs + blockIdx.z)[threadIdx.x];
+  __syncthreads();
+  const GemmDesc& D = sD;
   const int M = D.M, K = D.K;
   const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
   // row tiles fastest: the CTAs of one column tile run together and share its B tile in L2

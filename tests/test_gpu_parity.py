@@ -241,6 +241,32 @@ def test_residual_kernel_matches_oracle_stencil():
         assert abs(norms[0, 0] / np.linalg.norm(ref) - 1) < 1e-12
 
 
+@pytest.mark.parametrize("shape", [(70, 37, 45), (33, 5, 33), (1, 3, 1), (65, 1, 130)])
+def test_residual_kernel_z_chunks_and_ragged_rows(shape):
+    """The residual kernel marches z in chunks of 32 planes with u(k-1), u(k), u(k+1) in
+    registers and takes the x neighbours by warp shuffles: ragged chunk tails (nz = 70, 33, 65),
+    one plane, rows shorter than a warp and rows spanning several warps with a ragged end, vs
+    the oracle's literal stencil (Eq. (fd)) in fp64 and double-double, with 2 right-hand sides."""
+    Plan = _lib()
+    nz, ny, nx = shape
+    rng = np.random.default_rng(sum(shape))
+    hx = rng.uniform(0.5, 2, nx + 1) + 0.3j * rng.uniform(0, 1, nx + 1)
+    hy = rng.uniform(0.5, 2, ny + 1)
+    p = _steps_problem(hx, hy, nz, [nx // 2 + 1] if nx >= 3 else [], [ny // 2 + 1] if ny >= 3 else [])
+    plan = Plan.from_problem(p)
+    u = rng.standard_normal((2,) + p.shape) + 1j * rng.standard_normal((2,) + p.shape)
+    f = rng.standard_normal((2,) + p.shape) + 1j * rng.standard_normal((2,) + p.shape)
+    ut = torch.from_numpy(u).cuda()
+    ft = torch.from_numpy(f).cuda()
+    for dd in (False, True):
+        r, norms = plan.residual(ut, ft, dd=dd)
+        for q in range(2):
+            ref = oracle.mass_rhs(p, f[q]) - oracle.apply_stencil(p, u[q])
+            assert rel(r[q].cpu().numpy(), ref) < 1e-14
+            assert abs(norms[q, 0] / np.linalg.norm(ref) - 1) < 1e-12
+    plan.close()
+
+
 @pytest.mark.parametrize("nz", [1, 2, 3, 33, 70])
 def test_edge_sizes(nz):
     """Degenerate and ragged z sizes (identity padding rows in the warp solver), blocks of 1 node."""
