@@ -184,7 +184,8 @@ __device__ __forceinline__ Lev level_terms(const MwDev& D, int k, cx sx, cx sy) 
 
 // fam2 (optional, the two-level step 5): a second right-hand-side array in the same layout,
 // added to fam's on reading (the x-plane and y-plane parts of the transformed residual).
-__global__ void __launch_bounds__(128) k_mw_zsolve(MwDev D, double2* __restrict__ fam, double2* __restrict__ cp,
+// (128, 4): capped at 128 registers, 16 warps per SM (2.94 -> 2.70 ms at mw1)
+__global__ void __launch_bounds__(128, 4) k_mw_zsolve(MwDev D, double2* __restrict__ fam, double2* __restrict__ cp,
                                                    const double2* __restrict__ fam2) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)4 * D.plane) return;
