@@ -72,7 +72,9 @@ struct XSmem {
 // SMALLM (real S, M <= 32: blocks of at most 32 nodes): a 32-row tile, every warp 32 rows x
 // 16 complex columns, so no warp works on the all-zero rows 32..63 of the 64-row tile.
 template <bool REAL_S, bool KCONTIG, bool SMALLM = false>
-__global__ void __launch_bounds__(XT_THREADS) k_xform(const GemmDesc* __restrict__ descs, int gm, Bufs bufs) {
+// min blocks: 3 CTAs per SM for the 64-row tiles (168 registers instead of 194: C4q step-5 z-transforms
+// 1.23 -> 1.17 ms), 4 for SMALLM (its 116-128 registers unchanged)
+__global__ void __launch_bounds__(XT_THREADS, SMALLM ? 4 : 3) k_xform(const GemmDesc* __restrict__ descs, int gm, Bufs bufs) {
   static_assert(REAL_S || !SMALLM, "SMALLM: real S only");
   constexpr int TM = SMALLM ? 32 : XT_M;
   constexpr int NJ = SMALLM ? 4 : 8;  // real-view 8-column tiles per warp
