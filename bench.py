@@ -487,8 +487,8 @@ def run_ours(args, rank, world, local_rank):
     pw = dataclasses.replace(p, nrhs=nrhs * (1 if blocks else world))
     rhs0 = 0 if blocks else rank * nrhs
     refine = REFINE.get(args.config, 0) if args.refine is None else args.refine
-    if blocks and refine:
-        raise SystemExit("block-sharded solves do not refine; use --shard rhs for " + args.config)
+    # block-sharded refinement runs in dist.solve_sharded_refined (u completed by a sum over the
+    # ranks between the passes); the library plan itself does not refine then
     t0 = time.perf_counter()
     # the timed solve replays a CUDA graph of its launches (options.graph; stage events are graph
     # nodes); the sharded path runs phase by phase with the exchanges in between
@@ -496,7 +496,8 @@ def run_ours(args, rank, world, local_rank):
     # per-kernel events inside the timed region for the long steps; for the short (launch-bound)
     # configs they would perturb the step, so the kernel table comes from separate profiled steps
     kprof_timed = args.config not in SHORT_STEP
-    plan = Plan.from_problem(p, device=local_rank, refine=refine, residual_dd=res_dd, profile=2 if kprof_timed else 1,
+    plan = Plan.from_problem(p, device=local_rank, refine=0 if blocks else refine, residual_dd=res_dd,
+                             profile=2 if kprof_timed else 1,
                              graph=not blocks, rhs_chunk=0 if blocks else RHS_CHUNK.get(args.config, 0),
                              plane_dst=bool(args.plane_dst), dst_tma=bool(args.dst_tma))
     setup_s = time.perf_counter() - t0
@@ -518,9 +519,15 @@ def run_ours(args, rank, world, local_rank):
     u = torch.zeros_like(f)
     ws = plan.workspace(nrhs) if blocks else None
 
+    def sharded_solve(f_, u_):
+        if refine:
+            lfds_dist.solve_sharded_refined(plan, f_, u_, ws, refine, allreduce, dd=res_dd)
+        else:
+            lfds_dist.solve_sharded(plan, f_, u_, ws, allreduce)
+
     def step():
         if blocks:
-            lfds_dist.solve_sharded(plan, f, u, ws, allreduce)
+            sharded_solve(f, u)
         else:
             plan.solve(f, out=u)
     stream = torch.cuda.current_stream()
@@ -564,7 +571,7 @@ def run_ours(args, rank, world, local_rank):
     # correctness of what was timed: relative residual in double-double (sharded: the ranks'
     # parts of u are disjoint, their sum is the solution)
     if blocks:
-        if world > 1:
+        if world > 1 and not refine:  # (the refined path leaves the whole u on every rank)
             dist.all_reduce(u)
         plan.set_partition(None)
     rel_res = 0.0
@@ -590,7 +597,7 @@ def run_ours(args, rank, world, local_rank):
         def step_host(i):
             if blocks:  # H2D of f, sharded solve, D2H of u (this rank's part)
                 f.copy_(fh, non_blocking=True)
-                lfds_dist.solve_sharded(plan, f, u, ws, allreduce)
+                sharded_solve(f, u)
                 uhs[0].copy_(u, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             else:

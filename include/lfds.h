@@ -184,6 +184,21 @@ int lfds_residual(lfds_plan* plan, const void* u_dev, const void* f_dev, lfds_z*
                   int dd, double* norms, void* cuda_stream);
 
 /*
+ * Refinement pieces for callers that run the passes themselves (block-sharded solves, whose
+ * u is completed by a sum over the ranks between the passes; reading R13 of DESIGN.md):
+ *  lfds_residual_f  r = f - M^{-1} A u in f-units (the right side whose solve is the correction
+ *                   u_exact - u), device pointers, stream-ordered, no synchronisation; u_dev and
+ *                   f_dev in the plan dtype, r_dev complex128 [nrhs][nz][ny][nx]; dd = 1
+ *                   evaluates in double-double.
+ *  lfds_axpy        u += delta over nrhs fields (u in the plan dtype: the real part is added for
+ *                   LFDS_F64 plans), stream-ordered.
+ * Errors: LFDS_EINVAL (NULL pointers, nrhs < 1), LFDS_ENODEVICE, LFDS_ECUDA.
+ */
+int lfds_residual_f(lfds_plan* plan, const void* u_dev, const void* f_dev, lfds_z* r_dev, int nrhs, int dd,
+                    void* cuda_stream);
+int lfds_axpy(lfds_plan* plan, const lfds_z* delta_dev, void* u_dev, int nrhs, void* cuda_stream);
+
+/*
  * Block sharding across ranks (BASELINE.json north_star: "partitioned across the 8 B200s by
  * blocks S^ij, with NCCL over NVLink only for the interface exchange").  Every rank builds the
  * same plan, then lfds_set_partition tells it which blocks it computes in the two block passes
@@ -202,7 +217,9 @@ int lfds_residual(lfds_plan* plan, const void* u_dev, const void* f_dev, lfds_z*
  * on its segments of the interface planes (the segment of an x-plane in a block row belongs to
  * the owner of the block on its left, of a y-plane in a block column to the owner of the block
  * below, the plane intersections to the rank0 rank); other entries are not written.  Phased
- * solves take all nrhs right-hand sides in one pass and do not refine (LFDS_EINVAL otherwise).
+ * solves take all nrhs right-hand sides in one pass and do not refine (LFDS_EINVAL otherwise):
+ * a caller refines by summing u over the ranks, then lfds_residual_f, a phased solve of the
+ * residual, a sum of the correction and lfds_axpy (paper_1909_01299_b200/dist.py).
  */
 int lfds_set_partition(lfds_plan* plan, const int* block_owned, int l_begin, int l_end, int rank0);
 /*

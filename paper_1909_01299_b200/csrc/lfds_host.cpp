@@ -2255,6 +2255,36 @@ int lfds_residual(lfds_plan* P, const void* u_dev, const void* f_dev, lfds_z* r_
   return LFDS_OK;
 }
 
+int lfds_residual_f(lfds_plan* P, const void* u_dev, const void* f_dev, lfds_z* r_dev, int nrhs, int dd,
+                    void* stream) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  if (!u_dev || !f_dev || !r_dev || nrhs < 1) return fail(LFDS_EINVAL, "bad residual arguments");
+  (void)cudaGetLastError();  // (stale non-sticky errors of the caller)
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
+  Bufs b{};
+  b.p[B_TAB] = P->d_tab;
+  const Axis& X = P->ax[0];
+  const Axis& Y = P->ax[1];
+  CUDA_TRY(launch_residual(X.N, Y.N, P->nz, nrhs, dt, dd, 1, X.hoff, Y.hoff, P->t_hz, X.hhoff, Y.hhoff, P->t_hhz,
+                           P->t_sig, P->t_sige, make_double2(P->lam.real(), P->lam.imag()), P->t_dd, u_dev, f_dev,
+                           reinterpret_cast<double2*>(r_dev), 1, nullptr, b, st));
+  return LFDS_OK;
+}
+
+int lfds_axpy(lfds_plan* P, const lfds_z* delta_dev, void* u_dev, int nrhs, void* stream) {
+  if (!P) return fail(LFDS_EINVAL, "plan is NULL");
+  if (!P->d_tab) return fail(LFDS_ENODEVICE, "host-only plan (options.device < 0)");
+  if (!delta_dev || !u_dev || nrhs < 1) return fail(LFDS_EINVAL, "bad axpy arguments");
+  (void)cudaGetLastError();  // (stale non-sticky errors of the caller)
+  const int dt = P->opt.dtype == LFDS_F64 ? 1 : 0;
+  const int64_t n = (int64_t)P->ax[0].N * P->ax[1].N * P->nz * nrhs;
+  CUDA_TRY(launch_axpy_u(n, dt, reinterpret_cast<const double2*>(delta_dev), u_dev,
+                         reinterpret_cast<cudaStream_t>(stream)));
+  return LFDS_OK;
+}
+
 int lfds_get_report(const lfds_plan* cP, lfds_report* rep) {
   if (!cP || !rep) return fail(LFDS_EINVAL, "NULL argument");
   lfds_plan* P = const_cast<lfds_plan*>(cP);

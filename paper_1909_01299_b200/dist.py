@@ -161,3 +161,33 @@ def solve_sharded(plan, f, u, ws, allreduce: Optional[Callable] = None, stream=N
     allreduce(plan.exchange_view(ws, nrhs, 2))
     plan.solve_phase(3, f, u, ws, stream)
     return u
+
+
+def solve_sharded_refined(plan, f, u, ws, passes: int, allreduce: Optional[Callable] = None, stream=None,
+                          dd: bool = False):
+    """Block-sharded solve with `passes` refinement passes (reading R13: u += S(f - M^-1 A u)).
+
+    A sharded solve writes u only on the rank's blocks and its segments of the interface planes
+    (lfds_solve_phase), so u starts at zero and one sum over the ranks completes it; every rank
+    then forms the f-units residual of the whole grid (lfds_residual_f, the stencil reads u
+    across the block boundaries), solves for the correction with the same block sharding, and
+    completes the correction by a second sum before adding it (lfds_axpy).  Two volume sums per
+    pass: meant for the small, refinement-needing configs (C2: 17 MB per field)."""
+    import torch
+    if allreduce is None:
+        import torch.distributed as dist
+
+        def allreduce(t):
+            dist.all_reduce(t)
+    real = torch.view_as_real if u.is_complex() else (lambda t: t)
+    u.zero_()
+    solve_sharded(plan, f, u, ws, None if getattr(plan, "has_comm", False) else allreduce, stream)
+    allreduce(real(u))
+    for _ in range(passes):
+        r = plan.residual_f(u, f, dd=dd, stream=stream)
+        rf = r if u.is_complex() else r.real.contiguous()
+        d = torch.zeros_like(u)
+        solve_sharded(plan, rf, d, ws, None if getattr(plan, "has_comm", False) else allreduce, stream)
+        allreduce(real(d))
+        plan.axpy(d.to(torch.complex128) if not d.is_complex() else d, u, stream=stream)
+    return u

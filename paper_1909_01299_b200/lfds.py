@@ -77,6 +77,8 @@ _lib.lfds_solve.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
 _lib.lfds_solve_host.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
 _lib.lfds_solve_host_async.argtypes = [_P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _P]
 _lib.lfds_residual.argtypes = [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P]
+_lib.lfds_residual_f.argtypes = [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P]
+_lib.lfds_axpy.argtypes = [_P, _P, _P, ctypes.c_int, _P]
 _lib.lfds_get_report.argtypes = [_P, ctypes.POINTER(Report)]
 _lib.lfds_get_info.argtypes = [_P, ctypes.POINTER(Info)]
 _lib.lfds_get_basis.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
@@ -135,7 +137,8 @@ _lib.lfds_mw2_blocks.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
 _lib.lfds_mw2_destroy.argtypes = [_P]
 
 EXPORTED = ["lfds_default_options", "lfds_setup_grid", "lfds_workspace_bytes", "lfds_solve",
-            "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_get_report",
+            "lfds_workspace_bytes_host", "lfds_solve_host", "lfds_solve_host_async", "lfds_residual", "lfds_residual_f",
+            "lfds_axpy", "lfds_get_report",
             "lfds_get_info", "lfds_get_basis", "lfds_destroy", "lfds_last_error", "lfds_version",
             "lfds_stage_count", "lfds_stage_name", "lfds_stage_times", "lfds_set_partition",
             "lfds_exchange_layout", "lfds_solve_phase", "lfds_gmres_workspace_bytes", "lfds_gmres",
@@ -427,6 +430,31 @@ class Plan:
         _check(_lib.lfds_residual(self._h, _P(U.data_ptr()), None if F is None else _P(F.data_ptr()),
                                   _P(r.data_ptr()), nrhs, int(dd), norms.ctypes.data_as(_P), _P(st)))
         return (r[0] if single else r), norms.reshape(nrhs, 2)
+
+    def residual_f(self, u, f, dd: bool = False, stream=None):
+        """r = f - M^{-1} A u (f-units: the right side of the correction solve), complex128,
+        stream-ordered (lfds_residual_f)."""
+        torch = self._torch()
+        U = u.unsqueeze(0) if u.dim() == 3 else u
+        F = f.unsqueeze(0) if f.dim() == 3 else f
+        if U.shape != F.shape or not (U.is_cuda and F.is_cuda and U.is_contiguous() and F.is_contiguous()):
+            raise ValueError("u, f: contiguous device tensors of the same shape")
+        r = torch.empty(U.shape, dtype=torch.complex128, device=U.device)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _check(_lib.lfds_residual_f(self._h, _P(U.data_ptr()), _P(F.data_ptr()), _P(r.data_ptr()), U.shape[0],
+                                    int(dd), _P(st)))
+        return r if u.dim() == 4 else r[0]
+
+    def axpy(self, delta, u, stream=None):
+        """u += delta in place (lfds_axpy); delta complex128 of u's shape."""
+        torch = self._torch()
+        D = delta.unsqueeze(0) if delta.dim() == 3 else delta
+        U = u.unsqueeze(0) if u.dim() == 3 else u
+        if D.shape != U.shape or D.dtype != torch.complex128 or not (D.is_contiguous() and U.is_contiguous()):
+            raise ValueError("delta: contiguous complex128 of u's shape")
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _check(_lib.lfds_axpy(self._h, _P(D.data_ptr()), _P(U.data_ptr()), U.shape[0], _P(st)))
+        return u
 
     def close(self):
         if getattr(self, "_h", None):

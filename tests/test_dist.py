@@ -147,3 +147,76 @@ def test_exchange1_sums_the_ranks_partial_interface_residuals_gloo_world2():
     out = mgr.dict()
     mp.spawn(_oracle_worker, args=(2, port, out), nprocs=2, join=True)
     assert out[0] < 1e-13 and out[1] < 1e-13, dict(out)
+
+
+class _RefinePlan:
+    """Stand-in for the refinement protocol of dist.solve_sharded_refined: its sharded 'solve' is
+    the ORACLE's direct solve scaled by (1 + 1e-6) (an approximate inverse, so that refinement
+    has work to do), written only on this rank's slab of x nodes (the disjoint support a sharded
+    solve leaves in u); residual_f is the oracle's f - M^-1 A u on the whole grid."""
+
+    def __init__(self, p, rank, world):
+        self.p, self.rank, self.world = p, rank, world
+        self.has_comm = False
+        n = p.nx
+        self.x0, self.x1 = rank * n // world, (rank + 1) * n // world
+
+    def solve_phase(self, phase, f, u, ws, stream=None):
+        if phase == 3:  # (the separable oracle: scipy's splu runs ~100x slower in spawned workers)
+            import oracle
+            from oracle.solve import global_bases
+            self.g = getattr(self, "g", None) or global_bases(self.p)
+            sol = oracle.solve_separable(self.p, oracle.mass_rhs(self.p, f.numpy()[0]), self.g) * (1 + 1e-6)
+            u[0, :, :, self.x0:self.x1] = torch.from_numpy(np.ascontiguousarray(sol[:, :, self.x0:self.x1]))
+
+    def exchange_view(self, ws, nrhs, which):
+        return torch.zeros(4, dtype=torch.float64)
+
+    def residual_f(self, u, f, dd=False, stream=None):
+        import oracle
+        U, Fv = u.numpy()[0], f.numpy()[0]
+        V = oracle.mass_rhs(self.p, np.ones(self.p.shape, complex))
+        r = (oracle.mass_rhs(self.p, Fv) - oracle.apply_stencil(self.p, U)) / V
+        return torch.from_numpy(r[None].astype(np.complex128))
+
+    def axpy(self, d, u, stream=None):
+        u += d
+        return u
+
+
+def _refine_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist_mod.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)  # two ranks' BLAS / SuperLU thread pools on one host would oversubscribe it
+        torch.set_num_threads(1)
+        from workloads import shrunken
+        p = shrunken("c2", nrhs=1)
+        f = torch.from_numpy(p.rhs_all())
+        u = torch.full_like(f, 7.0)  # garbage: the protocol must zero it first
+        dist.solve_sharded_refined(_RefinePlan(p, rank, world), f, u, None, passes=1)
+        out[rank] = u.numpy()
+    finally:
+        dist_mod.destroy_process_group()
+
+
+def test_solve_sharded_refined_protocol_gloo_world2():
+    """Two gloo ranks: u completed by a sum over the ranks, the whole-grid f-units residual, the
+    sharded correction solve and its sum: one pass takes the 1e-6 approximate inverse to the
+    oracle's solution at ~1e-12 on every rank."""
+    import oracle
+    from workloads import shrunken
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_refine_worker, args=(2, port, out), nprocs=2, join=True)
+    p = shrunken("c2", nrhs=1)
+    ref = oracle.solve(p, p.rhs(0))  # separable + 80-bit refinement
+    for r in range(2):
+        u = out[r][0]
+        err = np.linalg.norm(u - ref) / np.linalg.norm(ref)
+        assert err < 1e-11, (r, err)
+    assert np.array_equal(out[0], out[1])

@@ -450,6 +450,71 @@ def test_full_size_c5_chunked_vs_oracle():
     assert_parity(p, U[1], ref)
 
 
+@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 3), ("c4", 2)])
+def test_block_sharded_refined_solve(name, world):
+    """Block sharding with refinement (dist.solve_sharded_refined: u completed by a sum over the
+    ranks, the whole-grid f-units residual lfds_residual_f, the sharded correction solve, its sum,
+    lfds_axpy): `world` ranks emulated by threads on one GPU with an in-process all-reduce summed
+    in rank order.  Every rank ends with the refined u: equal to the unsharded refined solve and
+    to the oracle's 80-bit-refined solution at the refined bar (C2 needs its pass, R12/R13)."""
+    import threading
+    from paper_1909_01299_b200 import Plan, dist
+    p = shrunken(name, nrhs=1)
+    F = p.rhs_all()
+    f = torch.from_numpy(F).cuda()
+    plans, ws = [], []
+    for r in range(world):
+        pl = Plan.from_problem(p)
+        dist.shard(pl, r, world)
+        plans.append(pl)
+        ws.append(pl.workspace(1))
+    bar = threading.Barrier(world)
+    slots, shared = [None] * world, {}
+
+    def make_allreduce(r):
+        def allreduce(t):
+            torch.cuda.synchronize()
+            slots[r] = t
+            bar.wait()
+            if r == 0:
+                tot = torch.zeros_like(slots[0])
+                for s_ in slots:
+                    tot += s_
+                shared["tot"] = tot
+            bar.wait()
+            t.copy_(shared["tot"])
+            torch.cuda.synchronize()
+            bar.wait()
+        return allreduce
+
+    out, errs = [None] * world, []
+
+    def run(r):
+        try:
+            u = torch.empty_like(f)
+            dist.solve_sharded_refined(plans[r], f, u, ws[r], passes=1, allreduce=make_allreduce(r))
+            torch.cuda.synchronize()
+            out[r] = u.cpu().numpy()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t_ in th:
+        t_.start()
+    for t_ in th:
+        t_.join()
+    assert not errs, errs
+    ref_plan = Plan.from_problem(p, refine=1, residual_dd=False)
+    u_ref = ref_plan.solve(f).cpu().numpy()
+    ref = oracle.solve(p, F[0])
+    for r in range(world):
+        assert rel(out[r], u_ref) < 1e-12, (r, rel(out[r], u_ref))
+        assert_parity(p, out[r][0], ref, tol=1e-12)
+    for pl in plans + [ref_plan]:
+        pl.close()
+
+
 @pytest.mark.parametrize("name,world", [("c2", 2), ("c5", 3), ("c4", 4)])
 def test_block_sharded_solve_matches_single_device(name, world):
     """Block sharding (north_star: blocks over ranks, one interface exchange): `world` ranks
