@@ -25,6 +25,12 @@ namespace {
 
 constexpr int RB = 4;  // rows per batch
 
+__device__ __forceinline__ void cp16p(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+
 template <int N>  // N doubles (power of two, 2..32) reduced over the warp; lane ends with one
 __device__ __forceinline__ double reduce_scatter(double (&v)[N], int& idx) {
   const int lane = threadIdx.x & 31;
@@ -156,10 +162,14 @@ __global__ void __launch_bounds__(512) k_proj(const PDesc* __restrict__ descs, B
 // m = w, w + NW, ... and each lane holds LPW columns, so a row sum of G is complete inside
 // the warp (reduce-scatter) and the CTA needs no barrier in its row loop; H (column sums)
 // accumulates per warp and is combined once per plane through shared memory, in warp order.
+// Rows arrive through a per-warp cp.async ring PNST rows deep (each lane copies and later reads
+// only its own columns, so a per-thread wait_group orders them; no warp or CTA barrier): PNST-1
+// rows per warp in flight without holding them in registers.
+constexpr int PNST = 4;
 template <int E, int LPW>
-__global__ void __launch_bounds__(128) k_proj_rows(const PDesc* __restrict__ descs, Bufs bufs) {
-  constexpr int N = 2 * E, NW = 4;
-  __shared__ double2 hs[NW][E][32 * LPW];
+__global__ void __launch_bounds__(128, 4) k_proj_rows(const PDesc* __restrict__ descs, Bufs bufs) {
+  constexpr int N = 2 * E, NW = 4, RW = 32 * LPW;
+  extern __shared__ __align__(16) double2 psm[];  // ring[NW][PNST][RW], then hs[NW][E][RW]
   const PDesc& D = descs[blockIdx.y];
   const int p = blockIdx.x;
   if (p >= D.nplanes) return;
@@ -168,6 +178,15 @@ __global__ void __launch_bounds__(128) k_proj_rows(const PDesc* __restrict__ des
   const double2* TAB = reinterpret_cast<const double2*>(bufs.p[B_TAB]);
   const double2* X = reinterpret_cast<const double2*>(bufs.p[D.x_buf]) + D.x_off + (int64_t)p * D.ps;
   double2* IF = reinterpret_cast<double2*>(bufs.p[B_IF]);
+  double2* ring = psm + warp * PNST * RW;
+  double2 (*hs)[E][RW] = reinterpret_cast<double2 (*)[E][RW]>(psm + NW * PNST * RW);
+  double2* wcs = psm + NW * PNST * RW + NW * E * RW;  // Wc[e][m], staged once per plane
+  const bool wsm = ny <= RW;  // Wc fits its staging area (else read through L1 per row)
+  if (wsm)
+    for (int c = threadIdx.x; c < E * ny; c += blockDim.x) {
+      const int e = c / ny, m = c - e * ny;
+      cp16p(wcs + c, TAB + D.wc + (int64_t)e * D.wc_es + m, e < E2);
+    }
   double2 wr[LPW][E], h[LPW][E];
 #pragma unroll
   for (int j = 0; j < LPW; ++j) {
@@ -178,23 +197,37 @@ __global__ void __launch_bounds__(128) k_proj_rows(const PDesc* __restrict__ des
       h[j][e] = make_double2(0, 0);
     }
   }
-  double2 xc[LPW], xn[LPW];
-  auto load = [&](double2 (&xb)[LPW], int m) {
+  // row i of this warp is m = warp + NW*i, in slot i % PNST
+  const int nrow = ny > warp ? (ny - warp + NW - 1) / NW : 0;
+  auto issue = [&](int i) {
+    if (i < nrow) {
+      const int m = warp + NW * i;
+      double2* d = ring + (i % PNST) * RW;
 #pragma unroll
-    for (int j = 0; j < LPW; ++j) {
-      const int l = lane + 32 * j;
-      xb[j] = (m < ny && l < nx) ? __ldg(X + (int64_t)m * nx + l) : make_double2(0, 0);
+      for (int j = 0; j < LPW; ++j) {
+        const int l = lane + 32 * j;
+        const bool ok = l < nx;
+        cp16p(d + l, ok ? X + (int64_t)m * nx + l : X, ok);  // zero-fill past nx
+      }
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  load(xn, warp);
-  for (int m = warp; m < ny; m += NW) {
 #pragma unroll
-    for (int j = 0; j < LPW; ++j) xc[j] = xn[j];
-    load(xn, m + NW);
+  for (int q = 0; q < PNST - 1; ++q) issue(q);
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(PNST - 2) : "memory");  // Wc rows (in the first group)
+  __syncthreads();
+  for (int i = 0; i < nrow; ++i) {
+    const int m = warp + NW * i;
+    issue(i + PNST - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(PNST - 1) : "memory");
+    double2 xc[LPW];
+    const double2* s = ring + (i % PNST) * RW;
+#pragma unroll
+    for (int j = 0; j < LPW; ++j) xc[j] = s[lane + 32 * j];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e < E2) {
-        const double2 w = __ldg(TAB + D.wc + (int64_t)e * D.wc_es + m);
+        const double2 w = wsm ? wcs[e * ny + m] : __ldg(TAB + D.wc + (int64_t)e * D.wc_es + m);
 #pragma unroll
         for (int j = 0; j < LPW; ++j) {
           h[j][e].x = fma(w.x, xc[j].x, fma(-w.y, xc[j].y, h[j][e].x));
@@ -215,17 +248,18 @@ __global__ void __launch_bounds__(128) k_proj_rows(const PDesc* __restrict__ des
       g[2 * e + 1] = gy;
     }
     int idx;
-    const double s = reduce_scatter<N>(g, idx);
+    const double sum = reduce_scatter<N>(g, idx);
     if (((lane & (32 / N - 1)) == 0 || N >= 32) && (idx >> 1) < E1)
-      reinterpret_cast<double*>(IF + D.g_off + (int64_t)(idx >> 1) * D.g_es + (int64_t)p * D.g_ps + m)[idx & 1] = s;
+      reinterpret_cast<double*>(IF + D.g_off + (int64_t)(idx >> 1) * D.g_es + (int64_t)p * D.g_ps + m)[idx & 1] = sum;
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 #pragma unroll
   for (int j = 0; j < LPW; ++j)
 #pragma unroll
     for (int e = 0; e < E; ++e) hs[warp][e][lane + 32 * j] = h[j][e];
   __syncthreads();
-  for (int t = threadIdx.x; t < E * 32 * LPW; t += blockDim.x) {
-    const int e = t / (32 * LPW), l = t % (32 * LPW);
+  for (int t = threadIdx.x; t < E * RW; t += blockDim.x) {
+    const int e = t / RW, l = t % RW;
     if (e < E2 && l < nx) {
       double2 acc = hs[0][e][l];
 #pragma unroll
@@ -263,10 +297,13 @@ cudaError_t launch_proj(const PDesc* d_descs, int ndesc, int max_nx, int maxE, i
   if (ndesc > 65535 || max_nx > 1024) return cudaErrorInvalidValue;
   if (maxE <= 2 && max_nx > 32 && max_nx <= 160) {  // wide block planes: row-per-warp variant
     const dim3 grid((unsigned)maxplanes, (unsigned)ndesc);
-#define PR(LPW)                                                   \
-  {                                                               \
-    k_proj_rows<2, LPW><<<grid, 128, 0, st>>>(d_descs, bufs);     \
-    return cudaGetLastError();                                    \
+#define PR(LPW)                                                                                   \
+  {                                                                                               \
+    const int sm = ((4 * PNST + 4 * 2) * 32 * LPW + 2 * 32 * LPW) * (int)sizeof(double2);        \
+    cudaError_t e = cudaFuncSetAttribute(k_proj_rows<2, LPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+    if (e != cudaSuccess) return e;                                                               \
+    k_proj_rows<2, LPW><<<grid, 128, sm, st>>>(d_descs, bufs);                                    \
+    return cudaGetLastError();                                                                    \
   }
     if (max_nx <= 64) PR(2)
     if (max_nx <= 128) PR(4)
@@ -296,11 +333,6 @@ __device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
-}
-__device__ __forceinline__ void cp16p(void* dst, const void* src, bool ok) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(ok ? 16 : 0)
-               : "memory");
 }
 struct C3 {  // 3M accumulators of one 8x8 complex tile (2 values per thread)
   double t1[2], t2[2], t3[2];
