@@ -120,36 +120,45 @@ struct MwDev {
 __device__ __forceinline__ int lev_of(int f, int k) { return f < 2 ? (k >> 1) - 1 : (k - 1) >> 1; }
 
 // ---------------------------------------------------------------- gather / scatter
+// One row (component c, level k, y index j) of the field per CTA iteration: the row's family,
+// packed y index and destination row are fixed (the P nodes of a row have i = j + k mod 2), so
+// the element loop carries no index divisions.
 __global__ void k_mw_gather(MwDev D, const double2* __restrict__ F, double2* __restrict__ fam) {
-  const int64_t total = (int64_t)3 * D.Nz * D.Ny * D.Nx;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(t % D.Nx);
-    int64_t r = t / D.Nx;
-    const int j = (int)(r % D.Ny);
-    r /= D.Ny;
-    const int k = (int)(r % D.Nz), c = (int)(r / D.Nz);
-    if (((i + j + k) & 1) || i == 0 || j == 0 || k == 0 || i == D.Nx - 1 || j == D.Ny - 1 || k == D.Nz - 1) continue;
-    const int xk = i & 1, yk = j & 1, f = fam_of(xk, yk);
-    const int xx = xk ? (i - 1) >> 1 : (i >> 1) - 1, yy = yk ? (j - 1) >> 1 : (j >> 1) - 1;
-    fam[D.fam_off[f] + (((int64_t)c * D.nlev[f] + lev_of(f, k)) * D.ny + yy) * D.nx + xx] = F[t];
+  const int64_t rows = (int64_t)3 * D.Nz * D.Ny;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int j = (int)(row % D.Ny);
+    const int64_t rk = row / D.Ny;
+    const int k = (int)(rk % D.Nz), c = (int)(rk / D.Nz);
+    if (j == 0 || k == 0 || j == D.Ny - 1 || k == D.Nz - 1) continue;  // uniform over the CTA
+    const int xk = (j + k) & 1, yk = j & 1, f = fam_of(xk, yk);
+    const int yy = yk ? (j - 1) >> 1 : (j >> 1) - 1;
+    double2* dst = fam + D.fam_off[f] + (((int64_t)c * D.nlev[f] + lev_of(f, k)) * D.ny + yy) * D.nx;
+    const double2* src = F + row * D.Nx;
+    for (int q = threadIdx.x;; q += blockDim.x) {  // i = 2q + xk, interior i in [1, Nx - 2]
+      const int i = 2 * q + xk;
+      if (i > D.Nx - 2) break;
+      if (i > 0) dst[xk ? q : q - 1] = src[i];
+    }
   }
 }
 
 __global__ void k_mw_scatter(MwDev D, const double2* __restrict__ fam, double2* __restrict__ H) {
-  const int64_t total = (int64_t)3 * D.Nz * D.Ny * D.Nx;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(t % D.Nx);
-    int64_t r = t / D.Nx;
-    const int j = (int)(r % D.Ny);
-    r /= D.Ny;
-    const int k = (int)(r % D.Nz), c = (int)(r / D.Nz);
-    double2 v = make_double2(0, 0);
-    if (!((i + j + k) & 1) && i > 0 && j > 0 && k > 0 && i < D.Nx - 1 && j < D.Ny - 1 && k < D.Nz - 1) {
-      const int xk = i & 1, yk = j & 1, f = fam_of(xk, yk);
-      const int xx = xk ? (i - 1) >> 1 : (i >> 1) - 1, yy = yk ? (j - 1) >> 1 : (j >> 1) - 1;
-      v = fam[D.fam_off[f] + (((int64_t)c * D.nlev[f] + lev_of(f, k)) * D.ny + yy) * D.nx + xx];
+  const int64_t rows = (int64_t)3 * D.Nz * D.Ny;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int j = (int)(row % D.Ny);
+    const int64_t rk = row / D.Ny;
+    const int k = (int)(rk % D.Nz), c = (int)(rk / D.Nz);
+    const bool rok = j > 0 && k > 0 && j < D.Ny - 1 && k < D.Nz - 1;
+    const int xk = (j + k) & 1, yk = j & 1, f = fam_of(xk, yk);
+    const int yy = yk ? (j - 1) >> 1 : (j >> 1) - 1;
+    const double2* src =
+        rok ? fam + D.fam_off[f] + (((int64_t)c * D.nlev[f] + lev_of(f, k)) * D.ny + yy) * D.nx : fam;
+    double2* dst = H + row * D.Nx;
+    for (int i = threadIdx.x; i < D.Nx; i += blockDim.x) {
+      double2 v = make_double2(0, 0);
+      if (rok && (i & 1) == xk && i > 0 && i < D.Nx - 1) v = src[xk ? (i - 1) >> 1 : (i >> 1) - 1];
+      dst[i] = v;
     }
-    H[t] = v;
   }
 }
 
@@ -184,8 +193,10 @@ __device__ __forceinline__ Lev level_terms(const MwDev& D, int k, cx sx, cx sy) 
 
 // fam2 (optional, the two-level step 5): a second right-hand-side array in the same layout,
 // added to fam's on reading (the x-plane and y-plane parts of the transformed residual).
-// (128, 4): capped at 128 registers, 16 warps per SM (2.94 -> 2.70 ms at mw1)
-__global__ void __launch_bounds__(128, 4) k_mw_zsolve(MwDev D, double2* __restrict__ fam, double2* __restrict__ cp,
+// (128, 3): 164 registers, no spills with the one-row-ahead loads (2.15 ms at the
+// 128-register cap of 4 CTAs per SM, 2.00 ms here)
+template <bool SUM>  // SUM: fam2 given (its values added on reading)
+__global__ void __launch_bounds__(128, 3) k_mw_zsolve(MwDev D, double2* __restrict__ fam, double2* __restrict__ cp,
                                                    const double2* __restrict__ fam2) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)4 * D.plane) return;
@@ -205,26 +216,51 @@ __global__ void __launch_bounds__(128, 4) k_mw_zsolve(MwDev D, double2* __restri
   double2* CP = cp + (int64_t)s * (D.nz) * 4 * D.plane + hoff;
   const cx zero = mk(0, 0);
   const cx iwm = mk(D.iwm.x, D.iwm.y);
-  const int64_t d2 = fam2 ? (int64_t)(fam2 - fam) : 0;  // element offset of the second array
-  auto rd = [&](const double2* p) -> cx { return fam2 ? ldw(p) + ldw(p + d2) : ldw(p); };
-  auto rdz = [&](int k) -> cx { return az ? zero : rd(FZ + (int64_t)lev_of(fz, k) * D.plane); };
+  const int64_t d2 = SUM ? (int64_t)(fam2 - fam) : 0;  // element offset of the second array
+  auto rd = [&](const double2* p) -> cx { return SUM ? ldw(p) + ldw(p + d2) : ldw(p); };
   auto interior = [&](int k) { return k >= 1 && k <= D.Nz - 2; };
+  // The volume loads of row r + 1 are issued before row r is eliminated (raw values: with fam2
+  // the two parts are summed at use), so each row's memory latency overlaps the previous row's
+  // arithmetic instead of serialising the sweep.
+  struct Raw {
+    cx x, y, z, x2, y2, z2;
+  };
+  auto fetch = [&](int k, Raw& v) {  // f_x, f_y at the X level k, f_z at k + 1
+    const double2* px = FX + (int64_t)lev_of(fx, k) * D.plane;
+    const double2* py = FY + (int64_t)lev_of(fy, k) * D.plane;
+    const bool hz = !az && interior(k + 1);
+    const double2* pz = FZ + (int64_t)lev_of(fz, k + 1) * D.plane;
+    v.x = ax ? zero : ldw(px);
+    v.y = ay ? zero : ldw(py);
+    v.z = hz ? ldw(pz) : zero;
+    if (SUM) {
+      v.x2 = ax ? zero : ldw(px + d2);
+      v.y2 = ay ? zero : ldw(py + d2);
+      v.z2 = hz ? ldw(pz + d2) : zero;
+    } else {
+      v.x2 = v.y2 = v.z2 = zero;
+    }
+  };
   // forward sweep
   Lev Lm{};
   bool gm = interior(k0 - 1);
   if (gm) Lm = level_terms(D, k0 - 1, sx, sy);
-  cx fzm = gm ? rdz(k0 - 1) : zero;
+  cx fzm = gm && !az ? rd(FZ + (int64_t)lev_of(fz, k0 - 1) * D.plane) : zero;
   m2 Cprev{};
   v2 Yprev{};
+  Raw nx_;
+  fetch(k0, nx_);
   for (int r = 0; r < nX; ++r) {
     const int k = k0 + 2 * r;
+    const Raw cur = nx_;
+    if (r + 1 < nX) fetch(k + 2, nx_);
     const cx idz = ld(D.idz + k);
     const bool gp = interior(k + 1);
     Lev Lp{};
     cx fzp = zero;
     if (gp) {
       Lp = level_terms(D, k + 1, sx, sy);
-      fzp = rdz(k + 1);
+      fzp = cur.z + cur.z2;
     }
     m2 Ap{zero, zero, zero, zero}, Am{zero, zero, zero, zero};
     if (gp) {
@@ -239,7 +275,7 @@ __global__ void __launch_bounds__(128, 4) k_mw_zsolve(MwDev D, double2* __restri
     m2 Dg{c3 * sy * sy - iwm, -(c3 * sx * sy), -(c3 * sx * sy), c3 * sx * sx - iwm};
     Dg = msub(msub(Dg, Ap), Am);
     const int lx = lev_of(fx, k), ly = lev_of(fy, k);
-    v2 rhs{ax ? zero : rd(FX + (int64_t)lx * D.plane), ay ? zero : rd(FY + (int64_t)ly * D.plane)};
+    v2 rhs{cur.x + cur.x2, cur.y + cur.y2};
     if (gp) rhs = vsub(rhs, v2{Lp.sqx * fzp * idz, Lp.sqy * fzp * idz});
     if (gm) rhs = v2{rhs.x + Lm.sqx * fzm * idz, rhs.y + Lm.sqy * fzm * idz};
     if (r > 0) {
@@ -261,34 +297,57 @@ __global__ void __launch_bounds__(128, 4) k_mw_zsolve(MwDev D, double2* __restri
     fzm = fzp;
   }
   // backward sweep, H_z at the level between X(k) and X(k + 2) (and below the first X level)
-  auto hz_at = [&](int kz, v2 Xlo, v2 Xhi) {  // X at kz - 1, kz + 1
+  auto hz_at = [&](int kz, v2 Xlo, v2 Xhi, cx fzv) {  // X at kz - 1, kz + 1; fzv = f_z(kz)
     const Lev L = level_terms(D, kz, sx, sy);
     const cx idz = ld(D.idz + kz);
     const cx dzx = (Xhi.x - Xlo.x) * idz, dzy = (Xhi.y - Xlo.y) * idz;
-    const cx v = (rdz(kz) + sx * L.c2 * dzx + sy * L.c1 * dzy) * L.idel;
+    const cx v = (fzv + sx * L.c2 * dzx + sy * L.c1 * dzy) * L.idel;
     st(FZ + (int64_t)lev_of(fz, kz) * D.plane, az ? zero : v);
   };
+  auto rdz = [&](int k) -> cx { return az ? zero : rd(FZ + (int64_t)lev_of(fz, k) * D.plane); };
   v2 Xn = Yprev;  // X at the last X level
   {
     const int k = k0 + 2 * (nX - 1);
     st(FX + (int64_t)lev_of(fx, k) * D.plane, ax ? zero : Xn.x);
     st(FY + (int64_t)lev_of(fy, k) * D.plane, ay ? zero : Xn.y);
-    if (interior(k + 1)) hz_at(k + 1, Xn, v2{zero, zero});
+    if (interior(k + 1)) hz_at(k + 1, Xn, v2{zero, zero}, rdz(k + 1));
   }
   CP -= 4 * D.plane;  // (row nX - 1's C' multiplies nothing)
+  // row r of the backward sweep reads C'(r), Y(r) and f_z(k + 1); those of row r - 1 are in flight
+  struct Back {
+    m2 C;
+    v2 Y;
+    cx z, z2;
+  };
+  auto fetchb = [&](int r, const double2* cpr, Back& v) {
+    const int k = k0 + 2 * r;
+    v.C = m2{ldw(cpr), ldw(cpr + D.plane), ldw(cpr + 2 * D.plane), ldw(cpr + 3 * D.plane)};
+    v.Y = v2{ldw(FX + (int64_t)lev_of(fx, k) * D.plane), ldw(FY + (int64_t)lev_of(fy, k) * D.plane)};
+    const double2* pz = FZ + (int64_t)lev_of(fz, k + 1) * D.plane;
+    v.z = az ? zero : ldw(pz);
+    v.z2 = (az || !SUM) ? zero : ldw(pz + d2);
+  };
+  Back nb;
+  if (nX >= 2) fetchb(nX - 2, CP - 4 * D.plane, nb);
   for (int r = nX - 2; r >= 0; --r) {
     const int k = k0 + 2 * r;
     CP -= 4 * D.plane;
-    const m2 C{ldw(CP), ldw(CP + D.plane), ldw(CP + 2 * D.plane), ldw(CP + 3 * D.plane)};
+    const Back cb = nb;
+    if (r > 0) fetchb(r - 1, CP - 4 * D.plane, nb);
     const int lx = lev_of(fx, k), ly = lev_of(fy, k);
-    const v2 Y{ldw(FX + (int64_t)lx * D.plane), ldw(FY + (int64_t)ly * D.plane)};
-    const v2 X = vsub(Y, mvec(C, Xn));
+    const v2 X = vsub(cb.Y, mvec(cb.C, Xn));
     st(FX + (int64_t)lx * D.plane, ax ? zero : X.x);
     st(FY + (int64_t)ly * D.plane, ay ? zero : X.y);
-    hz_at(k + 1, X, Xn);
+    hz_at(k + 1, X, Xn, cb.z + cb.z2);
     Xn = X;
   }
-  if (interior(k0 - 1)) hz_at(k0 - 1, v2{zero, zero}, Xn);
+  if (interior(k0 - 1)) hz_at(k0 - 1, v2{zero, zero}, Xn, rdz(k0 - 1));
+}
+
+void mw_zsolve_launch(const MwDev& D, double2* fam, double2* cp, const double2* fam2, cudaStream_t st) {
+  const unsigned grid = (unsigned)((4 * D.plane + 127) / 128);
+  if (fam2) k_mw_zsolve<true><<<grid, 128, 0, st>>>(D, fam, cp, fam2);
+  else k_mw_zsolve<false><<<grid, 128, 0, st>>>(D, fam, cp, nullptr);
 }
 
 // ---------------------------------------------------------------- residual r = f - A_h H
@@ -617,8 +676,7 @@ int lfds_mw_solve(lfds_mw* P, const void* f_dev, void* h_dev, void* ws, size_t w
   b.p[lfds::B_TAB] = P->d_mem;
   b.p[lfds::B_MS] = fam;
   b.p[lfds::B_T1] = T;
-  const int64_t total = (int64_t)3 * P->D.Nz * P->D.Ny * P->D.Nx;
-  const unsigned gs = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  const unsigned gs = (unsigned)std::min<int64_t>((int64_t)3 * P->D.Nz * P->D.Ny, 148 * 16);  // rows
   cudaError_t e = cudaSuccess;
   auto mark = [&](int i) {
     if (P->profile) cudaEventRecord(P->ev[i], st);
@@ -632,8 +690,7 @@ int lfds_mw_solve(lfds_mw* P, const void* f_dev, void* h_dev, void* ws, size_t w
   if (!e) e = lfds::launch_xform(P->d_desc + 4, 4, P->maxMy, P->maxNy, P->realy, false, b, st);
   mark(3);
   if (!e) {
-    const int64_t nt = 4 * P->D.plane;
-    k_mw_zsolve<<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(P->D, fam, cp, nullptr);
+    mw_zsolve_launch(P->D, fam, cp, nullptr, st);
     e = cudaGetLastError();
   }
   mark(4);
@@ -1207,7 +1264,7 @@ int lfds_mw2_solve(lfds_mw2* P, const void* f_dev, void* h_dev, void* ws, size_t
   };
   for (int g = 0; g < 4; ++g)
     if ((rc = cuda(group(g)))) return rc;
-  k_mw_zsolve<<<(unsigned)((4 * D.plane + 127) / 128), 128, 0, st>>>(D, coef, cp, coef2);
+  mw_zsolve_launch(D, coef, cp, coef2, st);
   if ((rc = cuda(cudaGetLastError()))) return rc;
   for (int g = 4; g < 8; ++g)
     if ((rc = cuda(group(g)))) return rc;
