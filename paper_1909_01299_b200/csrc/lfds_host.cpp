@@ -161,9 +161,15 @@ static inline void prof_record(cudaEvent_t e, cudaStream_t st) {
   else cudaEventRecord(e, st);
 }
 
+// experiment knob: LFDS_XSMALL=0 runs the small real-basis block transforms through k_xform
+static bool xsmall_on() {
+  static const bool on = !(getenv("LFDS_XSMALL") && atoi(getenv("LFDS_XSMALL")) == 0);
+  return on;
+}
+
 struct StageDescs {
   int64_t off = 0;  // index of the first desc in the device desc array
-  int n = 0, maxM = 0;
+  int n = 0, maxM = 0, maxK = 0;
   int64_t maxN = 0;
 };
 
@@ -402,9 +408,11 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     s.off = (int64_t)D.size();
     s.n = (int)v.size();
     s.maxM = 0;
+    s.maxK = 0;
     s.maxN = 0;
     for (auto& d : v) {
       s.maxM = std::max(s.maxM, d.M);
+      s.maxK = std::max(s.maxK, d.K);
       s.maxN = std::max(s.maxN, (int64_t)d.N1 * d.N2);
       D.push_back(d);
     }
@@ -894,6 +902,8 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
         return launch_xform(pp.d_descs + sc.off, sc.n, sc.maxM, sc.maxN, false, kcontig, bufs, st); }));
     if (sr.n)
       CUDA_TRY(kern(K_XFORM, nl(sr.n), [&] {
+        if (sr.maxM <= 32 && sr.maxK <= 32 && xsmall_on())
+          return launch_xform_small(pp.d_descs + sr.off, sr.n, sr.maxK, sr.maxN, kcontig, bufs, st);
         return launch_xform(pp.d_descs + sr.off, sr.n, sr.maxM, sr.maxN, true, kcontig, bufs, st); }));
     end();
     return LFDS_OK;

@@ -140,6 +140,9 @@ cudaError_t launch_projm(const ProjM& P, const Bufs& bufs, cudaStream_t st);
 // launchers (lfds_kernels.cu); return cudaGetLastError()
 cudaError_t launch_gemm(const GemmDesc* d_descs, int ndesc, int maxM, int maxN, int ldB_hint,
                         const Bufs& bufs, cudaStream_t st);
+// persistent form for real bases of at most 32 nodes (maxM, maxK <= 32; k_xsmall)
+cudaError_t launch_xform_small(const GemmDesc* d_descs, int ndesc, int maxK, int64_t maxN, bool kcontig,
+                               const Bufs& bufs, cudaStream_t st);
 cudaError_t launch_xform(const GemmDesc* d_descs, int ndesc, int maxM, int64_t maxN, bool real_s, bool kcontig,
                          const Bufs& bufs, cudaStream_t st);
 bool dst_supported(int n);

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "lfds_internal.h"
 
 namespace lfds {
@@ -268,6 +270,173 @@ cudaError_t launch_one(const GemmDesc* d, int ndesc, int maxM, int64_t maxN, con
   return launch_one_t<REAL_S, KCONTIG, false>(d, ndesc, maxM, maxN, bufs, st);
 }
 
+
+// ---------------------------------------------------------------- persistent small real-S form
+// Blocks of at most 32 nodes with a real basis (R / U blocks of C3, C5): S is at most 32 x 32, so
+// k_xform's CTAs were short (two K chunks of 16, then the epilogue) and re-staged S per 64-column
+// tile.  k_xsmall keeps S in shared memory for the CTA's life and streams its column tiles (all K
+// rows of 64 complex columns at once) through a three-stage cp.async ring: two tiles in flight
+// while one is contracted.  Same warp tiling (32 rows x 16 complex columns per warp), arithmetic
+// order and epilogue as k_xform<true, *, true>, so the result is bit-identical.
+template <int KS>
+struct XsSmem {
+  static constexpr int NST = 3;
+  static constexpr int LDA = 36;                  // S rows (<= 32) padded, == 4 mod 16
+  static constexpr int A = KS * LDA;              // doubles
+  static constexpr int B = KS * LDB_C * 2;        // doubles per stage
+  static constexpr size_t BYTES = (size_t)(A + NST * B) * sizeof(double);
+};
+
+template <bool KCONTIG, int KS>
+__global__ void __launch_bounds__(XT_THREADS, 2) k_xsmall(const GemmDesc* __restrict__ descs, Bufs bufs) {
+  using SM = XsSmem<KS>;
+  constexpr int NST = SM::NST, NJ = 4;
+  extern __shared__ __align__(16) double xsm[];
+  __shared__ GemmDesc sD;
+  if (threadIdx.x < (int)(sizeof(GemmDesc) / 8))
+    reinterpret_cast<int64_t*>(&sD)[threadIdx.x] = reinterpret_cast<const int64_t*>(descs + blockIdx.y)[threadIdx.x];
+  __syncthreads();
+  const GemmDesc& D = sD;
+  const int M = D.M, K = D.K;
+  const int64_t N2 = D.N2, N = (int64_t)D.N1 * D.N2;
+  const int64_t ntiles = (N + XT_N - 1) / XT_N;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wn = warp * 16, g = lane >> 2, q = lane & 3;
+  double* As = xsm;
+  double* Bsm = xsm + SM::A;
+  {  // S once: As[j][i] = S(i, j), zero outside M x K
+    const double* A = reinterpret_cast<const double*>(bufs.p[B_TAB]) + D.a_off;
+    for (int c = tid; c < KS * 32; c += XT_THREADS) {
+      const int j = c >> 5, i = c & 31;
+      As[j * SM::LDA + i] = (i < M && j < K) ? __ldg(A + (int64_t)i * D.sAi + (int64_t)j * D.sAj) : 0.0;
+    }
+  }
+  const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off;
+  const int bj = KCONTIG ? (tid & 15) : (tid >> 6), bn0 = KCONTIG ? (tid >> 4) : (tid & 63);
+  const ColStep c8(8, N2);
+  auto issue = [&](int64_t t, int stage) {
+    if (t < ntiles) {
+      double2* Bs = reinterpret_cast<double2*>(Bsm + stage * SM::B);
+      if (KCONTIG) {  // 16 threads per 256-byte column segment, columns bn0 + 8e
+        int64_t n = t * XT_N + bn0;
+        int64_t n1 = n / N2, n2 = n - n1 * N2;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const bool nok = n < N;
+          const int64_t col = n1 * D.sB1 + n2 * D.sB2;
+#pragma unroll
+          for (int h = 0; h < KS / 16; ++h) {
+            const int j = bj + 16 * h;
+            const bool ok = nok && j < K;
+            cp_async16(Bs + j * LDB_C + bn0 + 8 * e, ok ? B + col + j : B, ok);
+          }
+          n += 8;
+          c8.advance(n1, n2, N2);
+        }
+      } else {  // 64 consecutive columns of one row per 64 threads, rows bj + 2e
+        const int64_t n = t * XT_N + bn0;
+        const int64_t n1 = n / N2, n2 = n - n1 * N2;
+        const int64_t col = n1 * D.sB1 + n2 * D.sB2;
+#pragma unroll
+        for (int e = 0; e < KS / 2; ++e) {
+          const int j = bj + 2 * e;
+          const bool ok = n < N && j < K;
+          cp_async16(Bs + j * LDB_C + bn0, ok ? B + col + (int64_t)j * D.sBj : B, ok);
+        }
+      }
+    }
+    cp_commit();
+  };
+  const int64_t G = gridDim.x;
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) issue(blockIdx.x + s * G, s);
+  double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
+  const ColStep c1(1, N2), c4(4, N2);
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+    __syncthreads();  // stage (k - 1) % NST read by every warp before it is refilled
+    issue(t + (NST - 1) * G, (k + NST - 1) % NST);
+    cp_wait<NST - 1>();
+    __syncthreads();  // tile t landed for every thread
+    const double* Bs = Bsm + (k % NST) * SM::B;
+    double acc[4][NJ][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < NJ; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KS; kk += 4) {
+      double a[4], b[NJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[(kk + q) * SM::LDA + 8 * i + g];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[j] = Bs[(kk + q) * (2 * LDB_C) + 2 * wn + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    // epilogue (k_xform's real-S order): columns wn + 4j + q, rows 8i + g
+    int64_t n = t * XT_N + wn + q;
+    int64_t n1 = n / N2, n2 = n - n1 * N2;
+#pragma unroll
+    for (int e = 0; e < NJ; ++e) {
+      if (n < N) {
+        const int64_t off = n1 * D.sC1 + n2 * D.sC2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = 8 * i + g;
+          if (row < M) C[(int64_t)row * D.sCi + off] = make_double2(acc[i][e][0], acc[i][e][1]);
+        }
+      }
+      n += 4;
+      c4.advance(n1, n2, N2);
+    }
+  }
+  cp_wait<0>();
+}
+
+template <bool KCONTIG, int KS>
+cudaError_t launch_xsmall_t(const GemmDesc* d, int ndesc, int64_t maxN, const Bufs& bufs, cudaStream_t st) {
+  const size_t sm = XsSmem<KS>::BYTES;
+  auto kern = k_xsmall<KCONTIG, KS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, XT_THREADS, sm)) != cudaSuccess) return e;
+  const int64_t ntiles = (maxN + XT_N - 1) / XT_N;
+  for (int y0 = 0; y0 < ndesc; y0 += 65535) {
+    const int ny = ndesc - y0 < 65535 ? ndesc - y0 : 65535;
+    // persistent CTAs over all descriptors of the launch, a whole number of waves (equal CTAs:
+    // a partial last wave would leave SMs idle for a whole CTA lifetime); else many waves
+    const int64_t cap = (int64_t)std::max(1, per) * sms;
+    int64_t per_desc = 0;
+    for (int64_t p = std::max<int64_t>(1, cap / ny); p <= std::max<int64_t>(1, 16 * cap / ny); ++p)
+      if ((p * ny) % cap == 0) { per_desc = p; break; }
+    if (!per_desc) per_desc = std::max<int64_t>(1, 16 * cap / ny);
+    per_desc = std::min<int64_t>(per_desc, ntiles);
+    kern<<<dim3((unsigned)per_desc, (unsigned)ny), XT_THREADS, sm, st>>>(d + y0, bufs);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// block transforms with a real basis of at most 32 nodes (S at most 32 x 32): persistent k_xsmall
+cudaError_t launch_xform_small(const GemmDesc* d_descs, int ndesc, int maxK, int64_t maxN, bool kcontig,
+                               const Bufs& bufs, cudaStream_t st) {
+  if (ndesc <= 0) return cudaSuccess;
+  if (maxK <= 16) return kcontig ? launch_xsmall_t<true, 16>(d_descs, ndesc, maxN, bufs, st)
+                                 : launch_xsmall_t<false, 16>(d_descs, ndesc, maxN, bufs, st);
+  if (maxK <= 32) return kcontig ? launch_xsmall_t<true, 32>(d_descs, ndesc, maxN, bufs, st)
+                                 : launch_xsmall_t<false, 32>(d_descs, ndesc, maxN, bufs, st);
+  return cudaErrorInvalidValue;
+}
+
+namespace {
 
 // ---------------------------------------------------------------- complex S, 3 real products
 // Complex eigenvector matrices (C blocks, global PML bases) with the 3-multiplication form
