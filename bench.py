@@ -57,6 +57,8 @@ DEFAULT_SHARD = {"c5": "rhs"}
 # FP64 peaks: derived 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 TF/s;
 # measured on this pool (profiles/r01_fp64_peaks.log): DMMA 37.1, DFMA 34.2 TF/s.
 FP64_PEAK_TFLOPS = 37.2
+# LFDS_XPLANE=0 (A/B knob of the library): no plane dense transforms (k_xplane)
+XPLANE = os.environ.get("LFDS_XPLANE", "1") != "0"
 
 
 def _peaks():
@@ -197,6 +199,8 @@ def stage_algorithmic(p, R: int, plan=None):
         for i in range(len(bx)):
             for j in range(len(by)):
                 k, n = (kinds[i], bx[i]) if axis == 0 else (kinds[j], by[j])
+                if xfused(i, j):
+                    continue
                 if p.real or not is_sine(k, n):  # the f64 path has no sine kernels
                     e = bx[i] * by[j] * nz * R
                     fl += (2.0 if p.real else 8.0 if k == 2 else 4.0) * n * e
@@ -208,6 +212,10 @@ def stage_algorithmic(p, R: int, plan=None):
     def fused(i, j):  # mirrors fused2() in lfds_host.cpp / dst2_supported() in lfds_dst.cu
         return (plane_dst and not p.real and is_sine(kx[i], bx[i]) and is_sine(ky[j], by[j])
                 and bx[i] == by[j] and 2 * (bx[i] + 1) in (32, 64, 128))
+
+    def xfused(i, j):  # mirrors xplane() in lfds_host.cpp: two real bases of <= 32 nodes, no sine form
+        return (XPLANE and not p.real and not fused(i, j) and kx[i] != 2 and ky[j] != 2
+                and not is_sine(kx[i], bx[i]) and not is_sine(ky[j], by[j]) and bx[i] <= 32 and by[j] <= 32)
 
     def sine(kinds, axis):
         el = 0.0
@@ -224,6 +232,14 @@ def stage_algorithmic(p, R: int, plan=None):
     nf = plan.info().get("n_plane_dst") if plan else None
     if nf is not None and nf != sum(fused(i, j) for i in range(len(bx)) for j in range(len(by))):
         raise RuntimeError(f"plane-transform block count {nf} (library) != bench accounting")
+    nxf = plan.info().get("n_plane_dense") if plan else None
+    if nxf is not None and nxf != sum(xfused(i, j) for i in range(len(bx)) for j in range(len(by))):
+        raise RuntimeError(f"plane-dense block count {nxf} (library) != bench accounting")
+    # plane dense transform (k_xplane: real bases on both axes, one pass): 4 (nx + ny) flops and
+    # 32 B per element
+    pdense = (sum(4.0 * (bx[i] + by[j]) * bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by))
+                  if xfused(i, j)) or None,
+              32.0 * sum(bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by)) if xfused(i, j)))
     el_blk = sum(nx * ny * nz * R for nx in bx for ny in by)
     el_all = p.nx * p.ny * nz * R
     nifx, nify = len(p.iface_x), len(p.iface_y)
@@ -248,6 +264,7 @@ def stage_algorithmic(p, R: int, plan=None):
         "step6_zsolve_lift": (None, 2 * esz * el_blk),
         "step7_y_sine": ys, "step7_y_dense": yd, "step7_x_sine": xs, "step7_x_dense": xd,
         "step1_plane_sine": psine, "step7_plane_sine": psine,
+        "step1_plane_dense": pdense, "step7_plane_dense": pdense,
         # refinement: r = Mf - Au reads u and f and writes r; u += r reads both, writes u
         "refine_residual": (None, 48.0 * el_all), "refine_axpy": (None, 48.0 * el_all),
     }
@@ -278,10 +295,18 @@ def kernel_algorithmic(p, R: int, plan=None):
         L = 2 * (n + 1)
         return kind == 0 and (L in (16, 32, 64, 128, 256, 512) or (L % 16 == 0 and L // 16 in (3, 5, 6, 10, 12, 20)))
 
+    def xfused(i, j):  # stage_algorithmic's rule (k_xplane blocks)
+        fz = (bool(getattr(plan, "plane_dst", True)) if plan else True) and is_sine(kx[i], bx[i]) \
+            and is_sine(ky[j], by[j]) and bx[i] == by[j] and 2 * (bx[i] + 1) in (32, 64, 128)
+        return (XPLANE and not p.real and not fz and kx[i] != 2 and ky[j] != 2
+                and not is_sine(kx[i], bx[i]) and not is_sine(ky[j], by[j]) and bx[i] <= 32 and by[j] <= 32)
+
     fc = bc = fr = br = 0.0  # complex-S / real-S dense passes (4 per block: x, y forward + inverse)
     for i in range(len(bx)):
         for j in range(len(by)):
             e = bx[i] * by[j] * nz * R
+            if xfused(i, j):
+                continue
             for k, n in ((kx[i], bx[i]), (ky[j], by[j])):
                 if p.real or is_sine(k, n):
                     continue
@@ -317,6 +342,7 @@ def kernel_algorithmic(p, R: int, plan=None):
         "k_dst": (None, (alg["step1_y_sine"][1] or 0) + (alg["step7_y_sine"][1] or 0) or None),
         "k_dstt": (None, (alg["step1_y_sine"][1] or 0) + (alg["step7_y_sine"][1] or 0) or None),
         "k_dst2": (None, (alg["step1_plane_sine"][1] or 0) + (alg["step7_plane_sine"][1] or 0) or None),
+        "k_xplane": (2 * (alg["step1_plane_dense"][0] or 0) or None, 2 * (alg["step1_plane_dense"][1] or 0) or None),
         "k_zs1": alg["step2_zsolve"], "k_zsw": alg["step2_zsolve"], "k_zs2": alg["step6_zsolve_lift"],
         "k_proj_rows": alg["step3_edge_projection"],
         "k_s5m": (alg["step5_global_zsolve"][0], None) if modal else (None, None),

@@ -124,20 +124,21 @@ struct Axis {
 
 // one stage per kernel kind (sine = FFT-based DST on uniform blocks, dense = DMMA contraction)
 enum Stage { ST_X1S, ST_X1D, ST_Y1S, ST_Y1D, ST_Z1, ST_EPROJ, ST_EDGE, ST_IFRES, ST_GFWD, ST_GSWEEP, ST_GPROJ,
-             ST_GPLANE, ST_FACE, ST_Z2, ST_Y7S, ST_Y7D, ST_X7S, ST_X7D, ST_WRITE, ST_RESID, ST_AXPY, ST_P1S, ST_P7S, ST_COUNT };
+             ST_GPLANE, ST_FACE, ST_Z2, ST_Y7S, ST_Y7D, ST_X7S, ST_X7D, ST_WRITE, ST_RESID, ST_AXPY, ST_P1S, ST_P7S, ST_P1D, ST_P7D, ST_COUNT };
 const char* kStageNames[ST_COUNT] = {
     "step1_x_sine", "step1_x_dense", "step1_y_sine", "step1_y_dense", "step2_zsolve", "step3_edge_projection",
     "step3_edge_values", "step4_iface_residual", "step5_plane_forward", "step5_global_zsolve", "step5_projection",
     "step5_plane_inverse", "step6_face_transform", "step6_zsolve_lift", "step7_y_sine", "step7_y_dense",
     "step7_x_sine", "step7_x_dense", "step7_write_iface", "refine_residual", "refine_axpy", "step1_plane_sine",
-    "step7_plane_sine"};
+    "step7_plane_sine", "step1_plane_dense", "step7_plane_dense"};
 
 // kernel kinds (per-kernel device time: the roofline of the dominant kernel, bench.py)
 enum Kern { K_XFORM3M, K_XFORM, K_DSTW, K_DST, K_DST2, K_ZS1, K_ZS2, K_ZS3, K_PROJ, K_PROJM, K_S5M, K_IFRES,
-            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_ZSW, K_DSTT, K_FOLD, K_COUNT };
+            K_WRITE, K_RESID, K_AXPY, K_GEMM, K_ZSW, K_DSTT, K_FOLD, K_XPLANE, K_COUNT };
 const char* kKernNames[K_COUNT] = {
     "k_xform3m", "k_xform", "k_dstw", "k_dst", "k_dst2", "k_zs1", "k_zs2", "k_zs3", "k_proj_rows", "k_projm",
-    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm", "k_zsw", "k_dstt", "k_fold"};
+    "k_s5m", "k_iface_res", "k_write_iface", "k_residual", "k_axpy", "k_gemm", "k_zsw", "k_dstt", "k_fold",
+    "k_xplane"};
 
 struct Profiler {
   // stage < ST_COUNT: a stage record; stage = ST_COUNT + k: a record of kernel kind k
@@ -161,6 +162,12 @@ static inline void prof_record(cudaEvent_t e, cudaStream_t st) {
   else cudaEventRecord(e, st);
 }
 
+// experiment knob: LFDS_XPLANE=0 runs the blocks with two small real bases through an x pass and a
+// y pass (k_xsmall) instead of the plane transform k_xplane
+static bool xplane_on() {
+  static const bool on = !(getenv("LFDS_XPLANE") && atoi(getenv("LFDS_XPLANE")) == 0);
+  return on;
+}
 // experiment knob: LFDS_XSMALL=0 runs the small real-basis block transforms through k_xform
 static bool xsmall_on() {
   static const bool on = !(getenv("LFDS_XSMALL") && atoi(getenv("LFDS_XSMALL")) == 0);
@@ -211,6 +218,10 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   struct Dst2Group { int n; int64_t off; int count; };
   std::vector<Dst2Group> p1s, p7s;
   Dst2Desc* d_dst2 = nullptr;
+  // plane transforms of blocks with two real bases of at most 32 nodes (k_xplane): forward
+  // descriptors d_xpl[0, n_xpl), inverse d_xpl[n_xpl, 2 n_xpl)
+  XPlaneDesc* d_xpl = nullptr;
+  int n_xpl = 0;
   bool use_xform = false;
   int max_systems = 0, max_systems_global = 0;
   // workspace layout (bytes)
@@ -235,6 +246,7 @@ void free_pass(PassPlan& pp) {
   cudaFree(pp.d_own);
   cudaFree(pp.d_wmask);
   cudaFree(pp.d_dst2);
+  cudaFree(pp.d_xpl);
   cudaFree(pp.d_zwo);
 }
 
@@ -665,6 +677,36 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
     return P->opt.plane_dst && bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
   };
+  // blocks with real bases of at most 32 nodes on both axes (no fast sine transform): steps 1
+  // and 7 as plane transforms (k_xplane)
+  auto xplane = [&](int b) {
+    const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
+    return xplane_on() && !fused2(b) && bx.Fr >= 0 && by.Fr >= 0 && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
+  };
+  if (pp.use_xform) {
+    std::vector<XPlaneDesc> fw, iv;
+    for (int b : blk_ids) {
+      if (!xplane(b)) continue;
+      const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
+      const int64_t pl = (int64_t)bx.n * by.n, g0 = (int64_t)(by.lo - 1) * Nx + (bx.lo - 1);
+      XPlaneDesc d{};
+      d.nx = bx.n; d.ny = by.n; d.nplanes = (int)RZ;
+      d.b_buf = B_F; d.b_off = g0; d.sB1 = (int64_t)Nx * Ny; d.sBr = Nx;       // f[rk][y0+q][x0+p]
+      d.c_buf = B_MS; d.c_off = ms[b]; d.sC1 = pl; d.sCr = bx.n;                // MS[rk][m][l]
+      d.ax = bx.Fr; d.ay = by.Fr;
+      fw.push_back(d);
+      d.b_buf = B_MS; d.b_off = ms[b]; d.sB1 = pl; d.sBr = bx.n;
+      d.c_buf = B_U; d.c_off = g0; d.sC1 = (int64_t)Nx * Ny; d.sCr = Nx;        // u[rk][y0+q][x0+p]
+      d.ax = bx.Wr; d.ay = by.Wr;
+      iv.push_back(d);
+    }
+    pp.n_xpl = (int)fw.size();
+    if (pp.n_xpl) {
+      fw.insert(fw.end(), iv.begin(), iv.end());
+      CUDA_TRY(cudaMalloc(&pp.d_xpl, sizeof(XPlaneDesc) * fw.size()));
+      CUDA_TRY(cudaMemcpy(pp.d_xpl, fw.data(), sizeof(XPlaneDesc) * fw.size(), cudaMemcpyHostToDevice));
+    }
+  }
   if (pp.use_xform) {
     std::map<int, std::vector<Dst2Desc>> f2, i2;  // per length n
     for (int b : blk_ids) {
@@ -705,7 +747,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
         const int b = blk_ids[q];
         const AxisBlock& ab = xaxis ? X.blocks[b % nbx] : Y.blocks[b / nbx];
         const int64_t roff = fwd ? ab.Fr : ab.Wr;
-        if (fused2(b)) continue;  // k_dst2 (both axes at once)
+        if (fused2(b) || xplane(b)) continue;  // k_dst2 / k_xplane (both axes at once)
         if (ab.dst) {
           d.scale = fwd ? ab.dst_fwd : ab.dst_inv;
           d.a_off = P->t_tw.at(2 * (ab.n + 1));  // twiddles W_L^j of the odd-extension FFT
@@ -909,6 +951,15 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     return LFDS_OK;
   };
   // plane sine transforms (uniform x uniform blocks), one launch per block length
+  // plane transforms of the blocks with two small real bases (k_xplane)
+  auto planex = [&](bool fwd) -> int {
+    if (!pp.n_xpl) return LFDS_OK;
+    begin(fwd ? ST_P1D : ST_P7D);
+    CUDA_TRY(kern(K_XPLANE, nl(pp.n_xpl), [&] {
+      return launch_xplane(pp.d_xpl + (fwd ? 0 : pp.n_xpl), pp.n_xpl, (int)((int64_t)R * Nz), bufs, st); }));
+    end();
+    return LFDS_OK;
+  };
   auto plane2 = [&](const std::vector<PassPlan::Dst2Group>& gs, int stg) -> int {
     if (gs.empty()) return LFDS_OK;
     begin(stg);
@@ -943,6 +994,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   // pass 1
   if (phases & PH_1) {
   if ((rc = plane2(pp.p1s, ST_P1S))) return rc;
+  if ((rc = planex(true))) return rc;
   if ((rc = xform(pp.x1c, pp.x1r, pp.s1x, true, &pp.x1s, ST_X1S, ST_X1D))) return rc;
   if ((rc = xform(pp.y1c, pp.y1r, pp.s1y, false, &pp.y1s, ST_Y1S, ST_Y1D))) return rc;
   begin(ST_Z1);
@@ -1084,6 +1136,7 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   }
   // step 7
   if ((rc = plane2(pp.p7s, ST_P7S))) return rc;
+  if ((rc = planex(false))) return rc;
   if ((rc = xform(pp.y7c, pp.y7r, pp.s7y, false, &pp.y7s, ST_Y7S, ST_Y7D))) return rc;
   if ((rc = xform(pp.x7c, pp.x7r, pp.s7x, true, &pp.x7s, ST_X7S, ST_X7D))) return rc;
   if (has_if) {  // (sharded: every rank writes its own segments of the planes, pp.d_wmask)
@@ -1585,6 +1638,13 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
   if (P->opt.plane_dst && P->opt.dtype != LFDS_F64)
     for (auto& by : Y.blocks)
       for (auto& bx : X.blocks) I.n_plane_dst += bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
+  I.n_plane_dense = 0;  // the xplane() rule of build_pass (complex data only)
+  if (xplane_on() && P->opt.dtype != LFDS_F64)
+    for (auto& by : Y.blocks)
+      for (auto& bx : X.blocks) {
+        const bool f2 = P->opt.plane_dst && bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
+        I.n_plane_dense += !f2 && bx.Fr >= 0 && by.Fr >= 0 && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
+      }
   *out = P.release();
   return LFDS_OK;
 }

@@ -159,6 +159,19 @@ struct Dst2Desc {
   double ax, ay;             // DST-I scales of the two axes (dst_fwd or dst_inv)
 };
 bool dst2_supported(int n);
+// Plane (2-D) transform of a block whose x and y bases are both real and at most 32 nodes long
+// (R / U blocks of C5, C3): per plane r < nplanes,
+//   C[r][m][l] = sum_q Ay[m][q] ( sum_p B[r][q][p] Ax[l][p] )
+// (steps 1 and 7 of PAPER.md:66 / :72 in ONE pass over the block: the x-transformed plane stays
+// in shared memory).  Ax, Ay: real matrices [out][in] in B_TAB (offsets in doubles), rows q/m
+// strided by sBr/sCr, p/l contiguous.
+struct XPlaneDesc {
+  int64_t b_off, sB1, sBr;
+  int64_t c_off, sC1, sCr;
+  int64_t ax, ay;
+  int nx, ny, nplanes, b_buf, c_buf, pad;
+};
+cudaError_t launch_xplane(const XPlaneDesc* d_descs, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st);
 // y (strided) sine passes fed by TMA (k_dstt): one 128-byte tensor map per descriptor, built on
 // the host for the descriptor's current input buffer (the map embeds its address)
 bool dst_tma_supported(int n);

@@ -423,7 +423,142 @@ cudaError_t launch_xsmall_t(const GemmDesc* d, int ndesc, int64_t maxN, const Bu
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- plane form, both bases real
+// Blocks whose x AND y bases are real and at most 32 nodes long (the R x R blocks of C5 / C3):
+// steps 1 and 7 as ONE pass over the block instead of an x pass and a y pass,
+//   Out[m][l] = sum_q Ay[m][q] T[q][l],   T[q][l] = sum_p In[q][p] Ax[l][p],
+// with the x-transformed plane T kept in shared memory (32 B per element of HBM traffic per
+// direction instead of 64).  A CTA owns one block (Ax, Ay staged once, K-major like k_xsmall)
+// and streams its planes through a three-stage cp.async ring; per plane two DMMA phases with
+// the complex data viewed as real (re, im) columns:
+//   phase 1: rows l (Ax as the A operand), columns (q, re/im): warp w takes q = 4w .. 4w + 3;
+//   phase 2: rows m (Ay),                  columns (l, re/im): warp w takes l = 4w .. 4w + 3.
+// Same K order (p, q ascending in steps of 4) and DMMA shapes as the two k_xsmall passes, so
+// the result is bit-identical to theirs.  The output is staged in the consumed input buffer and
+// stored by rows (coalesced).  Strides: In rows 36 units (B fragments of phase 1 conflict-free:
+// 2 * 36 == 8 mod 16), T rows 34 (phase-2 B fragments: 2 * 34 == 4 mod 16; phase-1 stores hit
+// four 32-B bank groups).
+constexpr int XP_THREADS = 256, XP_LDA = 36, XP_LDI = 36, XP_LDT = 34, XP_NST = 3;
+constexpr size_t XP_BYTES = (size_t)(2 * 32 * XP_LDA + 2 * (XP_NST * 32 * XP_LDI + 32 * XP_LDT)) * sizeof(double);
+
+__global__ void __launch_bounds__(XP_THREADS, 2) k_xplane(const XPlaneDesc* __restrict__ descs, Bufs bufs) {
+  extern __shared__ __align__(16) double xsm[];
+  __shared__ XPlaneDesc sD;
+  static_assert(sizeof(XPlaneDesc) % 8 == 0, "descriptor copied as 64-bit words");
+  if (threadIdx.x < (int)(sizeof(XPlaneDesc) / 8))
+    reinterpret_cast<int64_t*>(&sD)[threadIdx.x] = reinterpret_cast<const int64_t*>(descs + blockIdx.y)[threadIdx.x];
+  __syncthreads();
+  const XPlaneDesc& D = sD;
+  const int nx = D.nx, ny = D.ny, np = D.nplanes;
+  if ((int)blockIdx.x >= np) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  double* AsX = xsm;                   // AsX[p][l] = Ax(l, p)
+  double* AsY = xsm + 32 * XP_LDA;     // AsY[q][m] = Ay(m, q)
+  double2* Ins = reinterpret_cast<double2*>(xsm + 2 * 32 * XP_LDA);  // [NST][32][LDI]
+  double2* Ts = Ins + XP_NST * 32 * XP_LDI;                          // [32][LDT]: T[q][l]
+  {
+    const double* TABd = reinterpret_cast<const double*>(bufs.p[B_TAB]);
+    for (int c = tid; c < 32 * 32; c += XP_THREADS) {
+      const int i = c >> 5, j = c & 31;  // (out, in)
+      AsX[j * XP_LDA + i] = (i < nx && j < nx) ? __ldg(TABd + D.ax + (int64_t)i * nx + j) : 0.0;
+      AsY[j * XP_LDA + i] = (i < ny && j < ny) ? __ldg(TABd + D.ay + (int64_t)i * ny + j) : 0.0;
+    }
+  }
+  const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off;
+  double2* C = reinterpret_cast<double2*>(bufs.p[D.c_buf]) + D.c_off;
+  // plane r into ring slot `stage`: 32 x 32 slots, zero outside ny x nx (a lane per column)
+  auto issue = [&](int r, int stage) {
+    if (r < np) {
+      double2* dst = Ins + stage * 32 * XP_LDI;
+      const double2* src = B + (int64_t)r * D.sB1;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int row = (tid >> 5) + 8 * e, col = lane;
+        const bool ok = row < ny && col < nx;
+        cp_async16(dst + row * XP_LDI + col, ok ? src + (int64_t)row * D.sBr + col : B, ok);
+      }
+    }
+    cp_commit();
+  };
+  const int G = gridDim.x;
+#pragma unroll
+  for (int s = 0; s < XP_NST - 1; ++s) issue((int)blockIdx.x + s * G, s);
+  int k = 0;
+  for (int r = blockIdx.x; r < np; r += G, ++k) {
+    __syncthreads();  // slot (k - 1) % NST stored out by every thread before it is refilled
+    issue(r + (XP_NST - 1) * G, (k + XP_NST - 1) % XP_NST);
+    cp_wait<XP_NST - 1>();
+    __syncthreads();  // plane r landed for every thread (and AsX / AsY on the first plane)
+    double2* In = Ins + (k % XP_NST) * 32 * XP_LDI;
+    double acc[4][2];
+    {  // ---- phase 1: T[q][l], rows l = 8i + g, complex column q = 4 warp + (lane & 3)
+      const double* Ind = reinterpret_cast<const double*>(In);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        double a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = AsX[(kk + q) * XP_LDA + 8 * i + g];
+        const double b = Ind[((4 * warp + (g >> 1)) * XP_LDI + kk + q) * 2 + (g & 1)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma(acc[i][0], acc[i][1], a[i], b);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Ts[(4 * warp + q) * XP_LDT + 8 * i + g] = make_double2(acc[i][0], acc[i][1]);
+    }
+    __syncthreads();  // T complete; the input plane is consumed
+    {  // ---- phase 2: Out[m][l], rows m = 8i + g, complex column l = 4 warp + (lane & 3)
+      const double* Td = reinterpret_cast<const double*>(Ts);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        double a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = AsY[(kk + q) * XP_LDA + 8 * i + g];
+        const double b = Td[(kk + q) * (2 * XP_LDT) + 8 * warp + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma(acc[i][0], acc[i][1], a[i], b);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) In[(8 * i + g) * XP_LDI + 4 * warp + q] = make_double2(acc[i][0], acc[i][1]);
+    }
+    __syncthreads();  // output plane staged (and T consumed)
+    double2* dst = C + (int64_t)r * D.sC1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int row = (tid >> 5) + 8 * e, col = lane;
+      if (row < ny && col < nx) dst[(int64_t)row * D.sCr + col] = In[row * XP_LDI + col];
+    }
+  }
+  cp_wait<0>();
+}
+
 }  // namespace
+
+// plane transforms of blocks with two real bases of at most 32 nodes: persistent CTAs per block,
+// a whole number of waves over the launch (see launch_xsmall_t)
+cudaError_t launch_xplane(const XPlaneDesc* d, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st) {
+  if (ndesc <= 0 || nplanes <= 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_xplane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XP_BYTES);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_xplane, XP_THREADS, XP_BYTES)) != cudaSuccess) return e;
+  for (int y0 = 0; y0 < ndesc; y0 += 65535) {
+    const int ny = ndesc - y0 < 65535 ? ndesc - y0 : 65535;
+    const int64_t cap = (int64_t)std::max(1, per) * sms;
+    int64_t per_desc = 0;
+    for (int64_t p = std::max<int64_t>(1, cap / ny); p <= std::max<int64_t>(1, 16 * cap / ny); ++p)
+      if ((p * ny) % cap == 0) { per_desc = p; break; }
+    if (!per_desc) per_desc = std::max<int64_t>(1, 16 * cap / ny);
+    per_desc = std::min<int64_t>(per_desc, nplanes);
+    k_xplane<<<dim3((unsigned)per_desc, (unsigned)ny), XP_THREADS, XP_BYTES, st>>>(d + y0, bufs);
+  }
+  return cudaGetLastError();
+}
 
 // block transforms with a real basis of at most 32 nodes (S at most 32 x 32): persistent k_xsmall
 cudaError_t launch_xform_small(const GemmDesc* d_descs, int ndesc, int maxK, int64_t maxN, bool kcontig,

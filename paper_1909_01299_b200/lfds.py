@@ -62,7 +62,7 @@ class Info(ctypes.Structure):
                 ("margin_global_lmt", ctypes.c_int * 3),
                 ("margin_block", ctypes.c_double), ("margin_block_rel", ctypes.c_double),
                 ("margin_block_ij", ctypes.c_int * 2), ("margin_block_lmt", ctypes.c_int * 3),
-                ("global_fold", ctypes.c_int)]
+                ("global_fold", ctypes.c_int), ("n_plane_dense", ctypes.c_int)]
 
 
 _P = ctypes.c_void_p

@@ -353,6 +353,38 @@ def test_plane_sine_lengths(n):
     assert rel(U[0], U1[0]) < 1e-12
 
 
+@pytest.mark.parametrize("sizes", [((31, 32, 9), (17, 31, 5)), ((32, 32), (32, 1)), ((5, 30), (31, 31, 31))])
+def test_plane_dense_blocks(sizes):
+    """Plane transform k_xplane of blocks whose x and y bases are both real and at most 32 nodes
+    long (graded real steps: no sine form), ragged and unequal sizes on the two axes (rows /
+    columns of the 32 x 32 tile left empty), several right-hand sides, next to thin complex PML
+    blocks on the 1-D passes: element-wise against the oracle; the plane stages must have run
+    and the library must count the blocks."""
+    rng = np.random.default_rng(4242 + sum(sizes[0]))
+
+    def axis(blocks):
+        steps, ifc, node = [1.0 + 0.5j, 1.0 + 0.5j, 1.0 + 0.5j], [3], 3  # 2 PML nodes, interface at 3
+        for n in blocks:
+            steps += list(1.0 + 0.3 * rng.random(n + 1))   # graded real steps: R blocks
+            node += n + 1
+            ifc.append(node)
+        steps += [1.0 + 0.5j, 1.0 + 0.5j, 1.0 + 0.5j]              # interface `node`, then 2 PML nodes
+        return np.asarray(steps, dtype=np.complex128), ifc
+
+    hx, ifx = axis(sizes[0])
+    hy, ify = axis(sizes[1])
+    p = _steps_problem(hx, hy, 5, ifx, ify)
+    F = rng.standard_normal((3,) + p.shape) + 1j * rng.standard_normal((3,) + p.shape)
+    F[:, :, : p.shape[1] // 3, :] *= 3.0
+    plan, U = gpu_solve(p, F, profile=True)
+    assert plan.info()["n_plane_dense"] == len(sizes[0]) * len(sizes[1]), plan.info()
+    st = plan.stage_times()
+    assert st["step1_plane_dense"][1] >= 1 and st["step7_plane_dense"][1] >= 1, st
+    for r in range(3):
+        ref = oracle.solve_direct(p, oracle.mass_rhs(p, F[r]))
+        assert_parity(p, U[r], ref)
+
+
 def test_plane_sine_under_graph_capture_and_rhs_chunks():
     """The plane transform (cluster launch) replays bit-identically from a captured CUDA graph
     and gives the same result with RHS chunking (planes = chunk x N_z per launch)."""

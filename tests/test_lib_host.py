@@ -204,3 +204,24 @@ def test_plane_transform_block_count(lfds):
     # bench.py's byte accounting agrees with the library's rule (it raises otherwise)
     alg = bench.stage_algorithmic(q, 1, pq)
     assert alg["step1_plane_sine"][1] == 32.0 * 900 * 31 * 31 * q.nz
+
+
+def test_plane_dense_block_count(lfds):
+    """lfds_info.n_plane_dense: the blocks whose steps 1 and 7 run as one plane transform on DMMA
+    (k_xplane) — real bases of at most 32 nodes on both axes and no sine form (C5: its 14 x 14
+    graded real blocks of 31 nodes; C4: none, its blocks have 127 nodes; C4q: none, its core
+    blocks take the plane sine transform; the f64 path: none).  bench.py's accounting follows the
+    same rule (it raises when the counts differ)."""
+    import bench
+    from workloads import make_problem
+    c5 = make_problem("c5")
+    p5 = host_plan(c5)
+    assert p5.info()["n_plane_dense"] == 14 * 14
+    assert host_plan(make_problem("c4")).info()["n_plane_dense"] == 0
+    assert host_plan(make_problem("c4q")).info()["n_plane_dense"] == 0
+    assert host_plan(shrunken("c1")).info()["n_plane_dense"] == 0
+    alg = bench.stage_algorithmic(c5, 1, p5)
+    el = 14 * 14 * 31 * 31 * c5.nz  # (the 32-node last block of each axis holds the PML: complex)
+    assert alg["step1_plane_dense"][1] == 32.0 * el
+    ka = bench.kernel_algorithmic(c5, 1, p5)
+    assert ka["k_xplane"][1] == 2 * 32.0 * el
