@@ -164,10 +164,11 @@ static inline void prof_record(cudaEvent_t e, cudaStream_t st) {
 
 // experiment knob: LFDS_XPLANE=0 runs the blocks with two small real bases through an x pass and a
 // y pass (k_xsmall) instead of the plane transform k_xplane
-static bool xplane_on() {
-  static const bool on = !(getenv("LFDS_XPLANE") && atoi(getenv("LFDS_XPLANE")) == 0);
-  return on;
+static int xplane_mode() {  // 0: off; 1 (default): 2-stage ring, 3 CTAs per SM; 4: 3-stage ring, 2 CTAs per SM
+  static const int mode = getenv("LFDS_XPLANE") ? atoi(getenv("LFDS_XPLANE")) : 1;
+  return mode;
 }
+static bool xplane_on() { return xplane_mode() != 0; }
 // experiment knob: LFDS_XSMALL=0 runs the small real-basis block transforms through k_xform
 static bool xsmall_on() {
   static const bool on = !(getenv("LFDS_XSMALL") && atoi(getenv("LFDS_XSMALL")) == 0);
@@ -956,7 +957,8 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
     if (!pp.n_xpl) return LFDS_OK;
     begin(fwd ? ST_P1D : ST_P7D);
     CUDA_TRY(kern(K_XPLANE, nl(pp.n_xpl), [&] {
-      return launch_xplane(pp.d_xpl + (fwd ? 0 : pp.n_xpl), pp.n_xpl, (int)((int64_t)R * Nz), bufs, st); }));
+      return launch_xplane(pp.d_xpl + (fwd ? 0 : pp.n_xpl), pp.n_xpl, (int)((int64_t)R * Nz), bufs, st,
+                           xplane_mode()); }));
     end();
     return LFDS_OK;
   };

@@ -171,7 +171,9 @@ struct XPlaneDesc {
   int64_t ax, ay;
   int nx, ny, nplanes, b_buf, c_buf, pad;
 };
-cudaError_t launch_xplane(const XPlaneDesc* d_descs, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st);
+// mode: 1 = two-stage ring at 3 CTAs per SM (default), 4 = three-stage ring at 2 CTAs per SM
+cudaError_t launch_xplane(const XPlaneDesc* d_descs, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st,
+                          int mode = 1);
 // y (strided) sine passes fed by TMA (k_dstt): one 128-byte tensor map per descriptor, built on
 // the host for the descriptor's current input buffer (the map embeds its address)
 bool dst_tma_supported(int n);

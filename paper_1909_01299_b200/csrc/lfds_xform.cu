@@ -429,7 +429,7 @@ cudaError_t launch_xsmall_t(const GemmDesc* d, int ndesc, int64_t maxN, const Bu
 //   Out[m][l] = sum_q Ay[m][q] T[q][l],   T[q][l] = sum_p In[q][p] Ax[l][p],
 // with the x-transformed plane T kept in shared memory (32 B per element of HBM traffic per
 // direction instead of 64).  A CTA owns one block (Ax, Ay staged once, K-major like k_xsmall)
-// and streams its planes through a three-stage cp.async ring; per plane two DMMA phases with
+// and streams its planes through a cp.async ring (two stages at three CTAs per SM); per plane two DMMA phases with
 // the complex data viewed as real (re, im) columns:
 //   phase 1: rows l (Ax as the A operand), columns (q, re/im): warp w takes q = 4w .. 4w + 3;
 //   phase 2: rows m (Ay),                  columns (l, re/im): warp w takes l = 4w .. 4w + 3.
@@ -438,10 +438,12 @@ cudaError_t launch_xsmall_t(const GemmDesc* d, int ndesc, int64_t maxN, const Bu
 // stored by rows (coalesced).  Strides: In rows 36 units (B fragments of phase 1 conflict-free:
 // 2 * 36 == 8 mod 16), T rows 34 (phase-2 B fragments: 2 * 34 == 4 mod 16; phase-1 stores hit
 // four 32-B bank groups).
-constexpr int XP_THREADS = 256, XP_LDA = 36, XP_LDI = 36, XP_LDT = 34, XP_NST = 3;
-constexpr size_t XP_BYTES = (size_t)(2 * 32 * XP_LDA + 2 * (XP_NST * 32 * XP_LDI + 32 * XP_LDT)) * sizeof(double);
+constexpr int XP_THREADS = 256, XP_LDA = 36, XP_LDI = 36, XP_LDT = 34;
+template <int XP_NST>
+constexpr size_t xp_bytes() { return (size_t)(2 * 32 * XP_LDA + 2 * (XP_NST * 32 * XP_LDI + 32 * XP_LDT)) * sizeof(double); }
 
-__global__ void __launch_bounds__(XP_THREADS, 2) k_xplane(const XPlaneDesc* __restrict__ descs, Bufs bufs) {
+template <int XP_NST, int MINB>
+__global__ void __launch_bounds__(XP_THREADS, MINB) k_xplane(const XPlaneDesc* __restrict__ descs, Bufs bufs) {
   extern __shared__ __align__(16) double xsm[];
   __shared__ XPlaneDesc sD;
   static_assert(sizeof(XPlaneDesc) % 8 == 0, "descriptor copied as 64-bit words");
@@ -539,14 +541,16 @@ __global__ void __launch_bounds__(XP_THREADS, 2) k_xplane(const XPlaneDesc* __re
 
 // plane transforms of blocks with two real bases of at most 32 nodes: persistent CTAs per block,
 // a whole number of waves over the launch (see launch_xsmall_t)
-cudaError_t launch_xplane(const XPlaneDesc* d, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st) {
-  if (ndesc <= 0 || nplanes <= 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_xplane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XP_BYTES);
+template <class K>
+static cudaError_t launch_xplane_k(K kern, int threads, size_t sm, int planes_per_cta_iter, const XPlaneDesc* d,
+                                   int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_xplane, XP_THREADS, XP_BYTES)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, sm)) != cudaSuccess) return e;
+  const int64_t items = (nplanes + planes_per_cta_iter - 1) / planes_per_cta_iter;
   for (int y0 = 0; y0 < ndesc; y0 += 65535) {
     const int ny = ndesc - y0 < 65535 ? ndesc - y0 : 65535;
     const int64_t cap = (int64_t)std::max(1, per) * sms;
@@ -554,10 +558,18 @@ cudaError_t launch_xplane(const XPlaneDesc* d, int ndesc, int nplanes, const Buf
     for (int64_t p = std::max<int64_t>(1, cap / ny); p <= std::max<int64_t>(1, 16 * cap / ny); ++p)
       if ((p * ny) % cap == 0) { per_desc = p; break; }
     if (!per_desc) per_desc = std::max<int64_t>(1, 16 * cap / ny);
-    per_desc = std::min<int64_t>(per_desc, nplanes);
-    k_xplane<<<dim3((unsigned)per_desc, (unsigned)ny), XP_THREADS, XP_BYTES, st>>>(d + y0, bufs);
+    per_desc = std::min<int64_t>(per_desc, items);
+    kern<<<dim3((unsigned)per_desc, (unsigned)ny), threads, sm, st>>>(d + y0, bufs);
   }
   return cudaGetLastError();
+}
+
+// mode 1 (default): a two-stage ring at three CTAs per SM (73 KB each); 4: a three-stage ring at two
+// CTAs per SM (A/B: 97.3 vs 95.7 ms per C5 step for mode 1, profiles/r02/xplane_modes)
+cudaError_t launch_xplane(const XPlaneDesc* d, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st, int mode) {
+  if (ndesc <= 0 || nplanes <= 0) return cudaSuccess;
+  if (mode == 4) return launch_xplane_k(k_xplane<3, 2>, XP_THREADS, xp_bytes<3>(), 1, d, ndesc, nplanes, bufs, st);
+  return launch_xplane_k(k_xplane<2, 3>, XP_THREADS, xp_bytes<2>(), 1, d, ndesc, nplanes, bufs, st);
 }
 
 // block transforms with a real basis of at most 32 nodes (S at most 32 x 32): persistent k_xsmall
