@@ -213,8 +213,8 @@ def stage_algorithmic(p, R: int, plan=None):
         return (plane_dst and not p.real and is_sine(kx[i], bx[i]) and is_sine(ky[j], by[j])
                 and bx[i] == by[j] and 2 * (bx[i] + 1) in (32, 64, 128))
 
-    def xfused(i, j):  # mirrors xplane() in lfds_host.cpp: two real bases of <= 32 nodes, no sine form
-        return (XPLANE and not p.real and not fused(i, j) and kx[i] != 2 and ky[j] != 2
+    def xfused(i, j):  # mirrors xplane() in lfds_host.cpp: two bases of <= 32 nodes, no sine form
+        return (XPLANE and not p.real and not fused(i, j)
                 and not is_sine(kx[i], bx[i]) and not is_sine(ky[j], by[j]) and bx[i] <= 32 and by[j] <= 32)
 
     def sine(kinds, axis):
@@ -235,9 +235,10 @@ def stage_algorithmic(p, R: int, plan=None):
     nxf = plan.info().get("n_plane_dense") if plan else None
     if nxf is not None and nxf != sum(xfused(i, j) for i in range(len(bx)) for j in range(len(by))):
         raise RuntimeError(f"plane-dense block count {nxf} (library) != bench accounting")
-    # plane dense transform (k_xplane: real bases on both axes, one pass): 4 (nx + ny) flops and
-    # 32 B per element
-    pdense = (sum(4.0 * (bx[i] + by[j]) * bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by))
+    # plane dense transform (k_xplane: both axes in one pass): 4 n flops per element for a real
+    # basis, 8 n for a complex one, and 32 B per element
+    pdense = (sum(((8.0 if kx[i] == 2 else 4.0) * bx[i] + (8.0 if ky[j] == 2 else 4.0) * by[j])
+                  * bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by))
                   if xfused(i, j)) or None,
               32.0 * sum(bx[i] * by[j] * nz * R for i in range(len(bx)) for j in range(len(by)) if xfused(i, j)))
     el_blk = sum(nx * ny * nz * R for nx in bx for ny in by)
@@ -298,7 +299,7 @@ def kernel_algorithmic(p, R: int, plan=None):
     def xfused(i, j):  # stage_algorithmic's rule (k_xplane blocks)
         fz = (bool(getattr(plan, "plane_dst", True)) if plan else True) and is_sine(kx[i], bx[i]) \
             and is_sine(ky[j], by[j]) and bx[i] == by[j] and 2 * (bx[i] + 1) in (32, 64, 128)
-        return (XPLANE and not p.real and not fz and kx[i] != 2 and ky[j] != 2
+        return (XPLANE and not p.real and not fz
                 and not is_sine(kx[i], bx[i]) and not is_sine(ky[j], by[j]) and bx[i] <= 32 and by[j] <= 32)
 
     fc = bc = fr = br = 0.0  # complex-S / real-S dense passes (4 per block: x, y forward + inverse)

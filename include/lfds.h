@@ -303,8 +303,8 @@ typedef struct {
                                /* step-5 plane transforms along that axis run on folded data at  */
                                /* half length (even / odd modes)                  */
   int n_plane_dense;           /* blocks whose steps 1 and 7 run as one plane  */
-                               /* transform on DMMA (k_xplane): real bases of at most 32 nodes   */
-                               /* on both axes, no fast sine transform, complex data             */
+                               /* transform on DMMA (k_xplane): at most 32 nodes on both axes,    */
+                               /* neither axis on the fast sine transform, complex data          */
 } lfds_info;
 int lfds_get_info(const lfds_plan* plan, lfds_info* info);
 

@@ -219,10 +219,12 @@ struct PassPlan {  // descriptors for one (R, in_real, out_real)
   struct Dst2Group { int n; int64_t off; int count; };
   std::vector<Dst2Group> p1s, p7s;
   Dst2Desc* d_dst2 = nullptr;
-  // plane transforms of blocks with two real bases of at most 32 nodes (k_xplane): forward
-  // descriptors d_xpl[0, n_xpl), inverse d_xpl[n_xpl, 2 n_xpl)
+  // plane transforms of blocks with two bases of at most 32 nodes and no sine form (k_xplane),
+  // grouped by the kind of the two matrices (real / complex): forward descriptors of group t in
+  // d_xpl[xp_off[t], + xp_cnt[t]), the inverse ones n_xpl further
   XPlaneDesc* d_xpl = nullptr;
   int n_xpl = 0;
+  int xp_off[4] = {0, 0, 0, 0}, xp_cnt[4] = {0, 0, 0, 0};  // t = cx + 2 cy
   bool use_xform = false;
   int max_systems = 0, max_systems_global = 0;
   // workspace layout (bytes)
@@ -678,28 +680,34 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
     const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
     return P->opt.plane_dst && bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
   };
-  // blocks with real bases of at most 32 nodes on both axes (no fast sine transform): steps 1
-  // and 7 as plane transforms (k_xplane)
+  // blocks of at most 32 nodes on both axes without a fast sine transform (real or complex
+  // bases): steps 1 and 7 as plane transforms (k_xplane)
   auto xplane = [&](int b) {
     const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
-    return xplane_on() && !fused2(b) && bx.Fr >= 0 && by.Fr >= 0 && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
+    return xplane_on() && !fused2(b) && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
   };
   if (pp.use_xform) {
     std::vector<XPlaneDesc> fw, iv;
-    for (int b : blk_ids) {
-      if (!xplane(b)) continue;
-      const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
-      const int64_t pl = (int64_t)bx.n * by.n, g0 = (int64_t)(by.lo - 1) * Nx + (bx.lo - 1);
-      XPlaneDesc d{};
-      d.nx = bx.n; d.ny = by.n; d.nplanes = (int)RZ;
-      d.b_buf = B_F; d.b_off = g0; d.sB1 = (int64_t)Nx * Ny; d.sBr = Nx;       // f[rk][y0+q][x0+p]
-      d.c_buf = B_MS; d.c_off = ms[b]; d.sC1 = pl; d.sCr = bx.n;                // MS[rk][m][l]
-      d.ax = bx.Fr; d.ay = by.Fr;
-      fw.push_back(d);
-      d.b_buf = B_MS; d.b_off = ms[b]; d.sB1 = pl; d.sBr = bx.n;
-      d.c_buf = B_U; d.c_off = g0; d.sC1 = (int64_t)Nx * Ny; d.sCr = Nx;        // u[rk][y0+q][x0+p]
-      d.ax = bx.Wr; d.ay = by.Wr;
-      iv.push_back(d);
+    for (int t = 0; t < 4; ++t) {  // groups: t = cx + 2 cy
+      pp.xp_off[t] = (int)fw.size();
+      for (int b : blk_ids) {
+        if (!xplane(b)) continue;
+        const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
+        const bool cx = bx.Fr < 0, cy = by.Fr < 0;  // complex matrix: offsets in complex units
+        if ((cx ? 1 : 0) + (cy ? 2 : 0) != t) continue;
+        const int64_t pl = (int64_t)bx.n * by.n, g0 = (int64_t)(by.lo - 1) * Nx + (bx.lo - 1);
+        XPlaneDesc d{};
+        d.nx = bx.n; d.ny = by.n; d.nplanes = (int)RZ;
+        d.b_buf = B_F; d.b_off = g0; d.sB1 = (int64_t)Nx * Ny; d.sBr = Nx;       // f[rk][y0+q][x0+p]
+        d.c_buf = B_MS; d.c_off = ms[b]; d.sC1 = pl; d.sCr = bx.n;                // MS[rk][m][l]
+        d.ax = cx ? bx.F : bx.Fr; d.ay = cy ? by.F : by.Fr;
+        fw.push_back(d);
+        d.b_buf = B_MS; d.b_off = ms[b]; d.sB1 = pl; d.sBr = bx.n;
+        d.c_buf = B_U; d.c_off = g0; d.sC1 = (int64_t)Nx * Ny; d.sCr = Nx;        // u[rk][y0+q][x0+p]
+        d.ax = cx ? bx.W : bx.Wr; d.ay = cy ? by.W : by.Wr;
+        iv.push_back(d);
+      }
+      pp.xp_cnt[t] = (int)fw.size() - pp.xp_off[t];
     }
     pp.n_xpl = (int)fw.size();
     if (pp.n_xpl) {
@@ -956,9 +964,11 @@ static int run_pass(lfds_plan* P, PassPlan& pp, Bufs bufs, int R, int in_dtype, 
   auto planex = [&](bool fwd) -> int {
     if (!pp.n_xpl) return LFDS_OK;
     begin(fwd ? ST_P1D : ST_P7D);
-    CUDA_TRY(kern(K_XPLANE, nl(pp.n_xpl), [&] {
-      return launch_xplane(pp.d_xpl + (fwd ? 0 : pp.n_xpl), pp.n_xpl, (int)((int64_t)R * Nz), bufs, st,
-                           xplane_mode()); }));
+    for (int t = 0; t < 4; ++t)
+      if (pp.xp_cnt[t])
+        CUDA_TRY(kern(K_XPLANE, nl(pp.xp_cnt[t]), [&] {
+          return launch_xplane(pp.d_xpl + (fwd ? 0 : pp.n_xpl) + pp.xp_off[t], pp.xp_cnt[t], (int)((int64_t)R * Nz),
+                               bufs, st, xplane_mode(), (t & 1) != 0, (t & 2) != 0); }));
     end();
     return LFDS_OK;
   };
@@ -1645,7 +1655,7 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
     for (auto& by : Y.blocks)
       for (auto& bx : X.blocks) {
         const bool f2 = P->opt.plane_dst && bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
-        I.n_plane_dense += !f2 && bx.Fr >= 0 && by.Fr >= 0 && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
+        I.n_plane_dense += !f2 && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
       }
   *out = P.release();
   return LFDS_OK;

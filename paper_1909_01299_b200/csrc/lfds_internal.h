@@ -159,8 +159,8 @@ struct Dst2Desc {
   double ax, ay;             // DST-I scales of the two axes (dst_fwd or dst_inv)
 };
 bool dst2_supported(int n);
-// Plane (2-D) transform of a block whose x and y bases are both real and at most 32 nodes long
-// (R / U blocks of C5, C3): per plane r < nplanes,
+// Plane (2-D) transform of a block whose x and y bases are both at most 32 nodes long and have no
+// sine form (R / C blocks of C5, C3; real or complex matrices per axis): per plane r < nplanes,
 //   C[r][m][l] = sum_q Ay[m][q] ( sum_p B[r][q][p] Ax[l][p] )
 // (steps 1 and 7 of PAPER.md:66 / :72 in ONE pass over the block: the x-transformed plane stays
 // in shared memory).  Ax, Ay: real matrices [out][in] in B_TAB (offsets in doubles), rows q/m
@@ -172,8 +172,10 @@ struct XPlaneDesc {
   int nx, ny, nplanes, b_buf, c_buf, pad;
 };
 // mode: 1 = two-stage ring at 3 CTAs per SM (default), 4 = three-stage ring at 2 CTAs per SM
+// cx / cy: the x / y matrices of every descriptor of the launch are complex ([out][in] in B_TAB,
+// offsets ax / ay in complex units)
 cudaError_t launch_xplane(const XPlaneDesc* d_descs, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st,
-                          int mode = 1);
+                          int mode = 1, bool cx = false, bool cy = false);
 // y (strided) sine passes fed by TMA (k_dstt): one 128-byte tensor map per descriptor, built on
 // the host for the descriptor's current input buffer (the map embeds its address)
 bool dst_tma_supported(int n);

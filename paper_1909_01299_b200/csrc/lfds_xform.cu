@@ -439,10 +439,16 @@ cudaError_t launch_xsmall_t(const GemmDesc* d, int ndesc, int64_t maxN, const Bu
 // 2 * 36 == 8 mod 16), T rows 34 (phase-2 B fragments: 2 * 34 == 4 mod 16; phase-1 stores hit
 // four 32-B bank groups).
 constexpr int XP_THREADS = 256, XP_LDA = 36, XP_LDI = 36, XP_LDT = 34;
-template <int XP_NST>
-constexpr size_t xp_bytes() { return (size_t)(2 * 32 * XP_LDA + 2 * (XP_NST * 32 * XP_LDI + 32 * XP_LDT)) * sizeof(double); }
+// A complex basis on an axis (CX / CY: C blocks of at most 32 nodes next to the real ones, and
+// C x C corner blocks) takes a second real matrix Im A and a second DMMA per step against the
+// data with its (re, im) slots swapped and the re slot negated:
+//   (Ar + i Ai)(Br + i Bi):  re = Ar Br + Ai (-Bi),  im = Ar Bi + Ai Br.
+template <int XP_NST, bool CX, bool CY>
+constexpr size_t xp_bytes() {
+  return (size_t)((2 + CX + CY) * 32 * XP_LDA + 2 * (XP_NST * 32 * XP_LDI + 32 * XP_LDT)) * sizeof(double);
+}
 
-template <int XP_NST, int MINB>
+template <int XP_NST, int MINB, bool CX, bool CY>
 __global__ void __launch_bounds__(XP_THREADS, MINB) k_xplane(const XPlaneDesc* __restrict__ descs, Bufs bufs) {
   extern __shared__ __align__(16) double xsm[];
   __shared__ XPlaneDesc sD;
@@ -456,14 +462,29 @@ __global__ void __launch_bounds__(XP_THREADS, MINB) k_xplane(const XPlaneDesc* _
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   double* AsX = xsm;                   // AsX[p][l] = Ax(l, p)
   double* AsY = xsm + 32 * XP_LDA;     // AsY[q][m] = Ay(m, q)
-  double2* Ins = reinterpret_cast<double2*>(xsm + 2 * 32 * XP_LDA);  // [NST][32][LDI]
+  double* AsXi = xsm + 2 * 32 * XP_LDA;              // imaginary parts (CX / CY)
+  double* AsYi = xsm + (2 + CX) * 32 * XP_LDA;
+  double2* Ins = reinterpret_cast<double2*>(xsm + (2 + CX + CY) * 32 * XP_LDA);  // [NST][32][LDI]
   double2* Ts = Ins + XP_NST * 32 * XP_LDI;                          // [32][LDT]: T[q][l]
   {
     const double* TABd = reinterpret_cast<const double*>(bufs.p[B_TAB]);
     for (int c = tid; c < 32 * 32; c += XP_THREADS) {
       const int i = c >> 5, j = c & 31;  // (out, in)
-      AsX[j * XP_LDA + i] = (i < nx && j < nx) ? __ldg(TABd + D.ax + (int64_t)i * nx + j) : 0.0;
-      AsY[j * XP_LDA + i] = (i < ny && j < ny) ? __ldg(TABd + D.ay + (int64_t)i * ny + j) : 0.0;
+      const double2* TABz = reinterpret_cast<const double2*>(TABd);  // complex matrices: offsets in complex units
+      if constexpr (CX) {
+        const double2 z = (i < nx && j < nx) ? __ldg(TABz + D.ax + (int64_t)i * nx + j) : make_double2(0.0, 0.0);
+        AsX[j * XP_LDA + i] = z.x;
+        AsXi[j * XP_LDA + i] = z.y;
+      } else {
+        AsX[j * XP_LDA + i] = (i < nx && j < nx) ? __ldg(TABd + D.ax + (int64_t)i * nx + j) : 0.0;
+      }
+      if constexpr (CY) {
+        const double2 z = (i < ny && j < ny) ? __ldg(TABz + D.ay + (int64_t)i * ny + j) : make_double2(0.0, 0.0);
+        AsY[j * XP_LDA + i] = z.x;
+        AsYi[j * XP_LDA + i] = z.y;
+      } else {
+        AsY[j * XP_LDA + i] = (i < ny && j < ny) ? __ldg(TABd + D.ay + (int64_t)i * ny + j) : 0.0;
+      }
     }
   }
   const double2* B = reinterpret_cast<const double2*>(bufs.p[D.b_buf]) + D.b_off;
@@ -483,6 +504,7 @@ __global__ void __launch_bounds__(XP_THREADS, MINB) k_xplane(const XPlaneDesc* _
     cp_commit();
   };
   const int G = gridDim.x;
+  const double sgn = (g & 1) ? 1.0 : -1.0;  // swapped-slot operand of a complex basis: (-Bi, Br)
 #pragma unroll
   for (int s = 0; s < XP_NST - 1; ++s) issue((int)blockIdx.x + s * G, s);
   int k = 0;
@@ -502,9 +524,15 @@ __global__ void __launch_bounds__(XP_THREADS, MINB) k_xplane(const XPlaneDesc* _
         double a[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = AsX[(kk + q) * XP_LDA + 8 * i + g];
-        const double b = Ind[((4 * warp + (g >> 1)) * XP_LDI + kk + q) * 2 + (g & 1)];
+        const int ad = ((4 * warp + (g >> 1)) * XP_LDI + kk + q) * 2 + (g & 1);
+        const double b = Ind[ad];
 #pragma unroll
         for (int i = 0; i < 4; ++i) dmma(acc[i][0], acc[i][1], a[i], b);
+        if constexpr (CX) {
+          const double bp = sgn * Ind[ad ^ 1];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dmma(acc[i][0], acc[i][1], AsXi[(kk + q) * XP_LDA + 8 * i + g], bp);
+        }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) Ts[(4 * warp + q) * XP_LDT + 8 * i + g] = make_double2(acc[i][0], acc[i][1]);
@@ -519,9 +547,15 @@ __global__ void __launch_bounds__(XP_THREADS, MINB) k_xplane(const XPlaneDesc* _
         double a[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = AsY[(kk + q) * XP_LDA + 8 * i + g];
-        const double b = Td[(kk + q) * (2 * XP_LDT) + 8 * warp + g];
+        const int ad = (kk + q) * (2 * XP_LDT) + 8 * warp + g;
+        const double b = Td[ad];
 #pragma unroll
         for (int i = 0; i < 4; ++i) dmma(acc[i][0], acc[i][1], a[i], b);
+        if constexpr (CY) {
+          const double bp = sgn * Td[ad ^ 1];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dmma(acc[i][0], acc[i][1], AsYi[(kk + q) * XP_LDA + 8 * i + g], bp);
+        }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) In[(8 * i + g) * XP_LDI + 4 * warp + q] = make_double2(acc[i][0], acc[i][1]);
@@ -565,11 +599,20 @@ static cudaError_t launch_xplane_k(K kern, int threads, size_t sm, int planes_pe
 }
 
 // mode 1 (default): a two-stage ring at three CTAs per SM (73 KB each); 4: a three-stage ring at two
-// CTAs per SM (A/B: 97.3 vs 95.7 ms per C5 step for mode 1, profiles/r02/xplane_modes)
-cudaError_t launch_xplane(const XPlaneDesc* d, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st, int mode) {
+// CTAs per SM (A/B: 97.3 vs 95.7 ms per C5 step for mode 1, profiles/r02/xplane_modes).  cx / cy: the
+// basis of that axis is complex (offsets ax / ay in complex units); those forms run two CTAs per SM.
+cudaError_t launch_xplane(const XPlaneDesc* d, int ndesc, int nplanes, const Bufs& bufs, cudaStream_t st, int mode,
+                          bool cx, bool cy) {
   if (ndesc <= 0 || nplanes <= 0) return cudaSuccess;
-  if (mode == 4) return launch_xplane_k(k_xplane<3, 2>, XP_THREADS, xp_bytes<3>(), 1, d, ndesc, nplanes, bufs, st);
-  return launch_xplane_k(k_xplane<2, 3>, XP_THREADS, xp_bytes<2>(), 1, d, ndesc, nplanes, bufs, st);
+  if (cx && cy)
+    return launch_xplane_k(k_xplane<2, 2, true, true>, XP_THREADS, xp_bytes<2, true, true>(), 1, d, ndesc, nplanes, bufs, st);
+  if (cx)
+    return launch_xplane_k(k_xplane<2, 2, true, false>, XP_THREADS, xp_bytes<2, true, false>(), 1, d, ndesc, nplanes, bufs, st);
+  if (cy)
+    return launch_xplane_k(k_xplane<2, 2, false, true>, XP_THREADS, xp_bytes<2, false, true>(), 1, d, ndesc, nplanes, bufs, st);
+  if (mode == 4)
+    return launch_xplane_k(k_xplane<3, 2, false, false>, XP_THREADS, xp_bytes<3, false, false>(), 1, d, ndesc, nplanes, bufs, st);
+  return launch_xplane_k(k_xplane<2, 3, false, false>, XP_THREADS, xp_bytes<2, false, false>(), 1, d, ndesc, nplanes, bufs, st);
 }
 
 // block transforms with a real basis of at most 32 nodes (S at most 32 x 32): persistent k_xsmall

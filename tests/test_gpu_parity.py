@@ -355,11 +355,11 @@ def test_plane_sine_lengths(n):
 
 @pytest.mark.parametrize("sizes", [((31, 32, 9), (17, 31, 5)), ((32, 32), (32, 1)), ((5, 30), (31, 31, 31))])
 def test_plane_dense_blocks(sizes):
-    """Plane transform k_xplane of blocks whose x and y bases are both real and at most 32 nodes
-    long (graded real steps: no sine form), ragged and unequal sizes on the two axes (rows /
-    columns of the 32 x 32 tile left empty), several right-hand sides, next to thin complex PML
-    blocks on the 1-D passes: element-wise against the oracle; the plane stages must have run
-    and the library must count the blocks."""
+    """Plane transform k_xplane of blocks of at most 32 nodes on both axes without a sine form:
+    graded real steps (R blocks), ragged and unequal sizes on the two axes (rows / columns of the
+    32 x 32 tile left empty), several right-hand sides, next to thin complex PML blocks (the
+    complex-basis forms C x R, R x C, C x C): element-wise against the oracle; the plane stages
+    must have run and the library must count the blocks."""
     rng = np.random.default_rng(4242 + sum(sizes[0]))
 
     def axis(blocks):
@@ -377,7 +377,9 @@ def test_plane_dense_blocks(sizes):
     F = rng.standard_normal((3,) + p.shape) + 1j * rng.standard_normal((3,) + p.shape)
     F[:, :, : p.shape[1] // 3, :] *= 3.0
     plan, U = gpu_solve(p, F, profile=True)
-    assert plan.info()["n_plane_dense"] == len(sizes[0]) * len(sizes[1]), plan.info()
+    # every block qualifies: the graded real ones (R x R), the 2-node PML blocks next to them
+    # (C x R, R x C: the complex-basis forms of the kernel) and the four C x C corners
+    assert plan.info()["n_plane_dense"] == (len(sizes[0]) + 2) * (len(sizes[1]) + 2), plan.info()
     st = plan.stage_times()
     assert st["step1_plane_dense"][1] >= 1 and st["step7_plane_dense"][1] >= 1, st
     for r in range(3):

@@ -208,20 +208,29 @@ def test_plane_transform_block_count(lfds):
 
 def test_plane_dense_block_count(lfds):
     """lfds_info.n_plane_dense: the blocks whose steps 1 and 7 run as one plane transform on DMMA
-    (k_xplane) — real bases of at most 32 nodes on both axes and no sine form (C5: its 14 x 14
-    graded real blocks of 31 nodes; C4: none, its blocks have 127 nodes; C4q: none, its core
-    blocks take the plane sine transform; the f64 path: none).  bench.py's accounting follows the
-    same rule (it raises when the counts differ)."""
+    (k_xplane) — at most 32 nodes on both axes, neither axis on the fast sine transform (C5: all
+    16 x 16 blocks, 14 x 14 graded real ones and the PML ones with a complex basis on an axis; C4:
+    none, its blocks have 127 nodes; C4q: the four complex corner blocks, its other blocks have a
+    sine axis; the f64 path: none).  bench.py's accounting follows the same rule (it raises when
+    the counts differ)."""
     import bench
     from workloads import make_problem
     c5 = make_problem("c5")
     p5 = host_plan(c5)
-    assert p5.info()["n_plane_dense"] == 14 * 14
+    assert p5.info()["n_plane_dense"] == 16 * 16
     assert host_plan(make_problem("c4")).info()["n_plane_dense"] == 0
-    assert host_plan(make_problem("c4q")).info()["n_plane_dense"] == 0
+    q = make_problem("c4q")
+    pq = host_plan(q)
+    assert pq.info()["n_plane_dense"] == 4
+    bench.stage_algorithmic(q, 1, pq)
     assert host_plan(shrunken("c1")).info()["n_plane_dense"] == 0
     alg = bench.stage_algorithmic(c5, 1, p5)
-    el = 14 * 14 * 31 * 31 * c5.nz  # (the 32-node last block of each axis holds the PML: complex)
-    assert alg["step1_plane_dense"][1] == 32.0 * el
+    assert alg["step1_plane_dense"][1] == 32.0 * c5.unknowns - 32.0 * c5.nz * (2 * 15 * 512 - 15 * 15)
+    n = [31] * 15 + [32]
+    k = [2] + [1] * 14 + [2]
+    fl = sum(((8.0 if k[i] == 2 else 4.0) * n[i] + (8.0 if k[j] == 2 else 4.0) * n[j]) * n[i] * n[j]
+             for i in range(16) for j in range(16)) * c5.nz
+    assert alg["step1_plane_dense"][0] == fl
     ka = bench.kernel_algorithmic(c5, 1, p5)
-    assert ka["k_xplane"][1] == 2 * 32.0 * el
+    assert ka["k_xplane"] == (2 * fl, 2 * alg["step1_plane_dense"][1])
+    assert ka["k_xform"][0] == 2 * 4.0 * c5.nz * (15 * 512 * 2) * c5.nz  # only the step-5 z-transforms are left

@@ -11,11 +11,11 @@ import os
 import re
 import sys
 
-KINDS = [(r"k_xform3m<", "k_xform3m"), (r"k_xform<", "k_xform"), (r"k_dstw<", "k_dstw"), (r"k_dst2<", "k_dst2"), (r"k_dstt<", "k_dstt"),
+KINDS = [(r"k_xform3m<", "k_xform3m"), (r"k_xform<|k_xsmall<", "k_xform"), (r"k_xplane<", "k_xplane"), (r"k_dstw<", "k_dstw"), (r"k_dst2<", "k_dst2"), (r"k_dstt<", "k_dstt"),
          (r"k_dst<", "k_dst"), (r"k_zs1<", "k_zs1"), (r"k_zs2<", "k_zs2"), (r"k_zs3<", "k_zs3"),
          (r"k_proj_rows<|k_proj<", "k_proj_rows"), (r"k_projm", "k_projm"), (r"k_s5m<|k_p2sum", "k_s5m"),
          (r"k_iface_res", "k_iface_res"), (r"k_write_iface", "k_write_iface"), (r"k_gemm", "k_gemm"),
-         (r"k_zsw", "k_zsw"), (r"k_fold|k_unfold", "k_fold")]
+         (r"k_zsw", "k_zsw"), (r"k_fold|k_unfold", "k_fold"), (r"k_residual", "k_residual"), (r"k_axpy", "k_axpy")]
 
 
 def kind_of(name):
