@@ -213,9 +213,15 @@ def stage_algorithmic(p, R: int, plan=None):
         return (plane_dst and not p.real and is_sine(kx[i], bx[i]) and is_sine(ky[j], by[j])
                 and bx[i] == by[j] and 2 * (bx[i] + 1) in (32, 64, 128))
 
-    def xfused(i, j):  # mirrors xplane() in lfds_host.cpp: two bases of <= 32 nodes, no sine form
+    def xcand(i, j):  # mirrors xplane() in lfds_host.cpp: two bases of <= 32 nodes, no sine form
         return (XPLANE and not p.real and not fused(i, j)
                 and not is_sine(kx[i], bx[i]) and not is_sine(ky[j], by[j]) and bx[i] <= 32 and by[j] <= 32)
+    # ... used when such blocks hold at least half of the block unknowns (lfds_host.cpp, setup)
+    xp_ok = 2 * sum(bx[i] * by[j] for i in range(len(bx)) for j in range(len(by)) if xcand(i, j)) \
+        >= sum(bx[i] * by[j] for i in range(len(bx)) for j in range(len(by)))
+
+    def xfused(i, j):
+        return xp_ok and xcand(i, j)
 
     def sine(kinds, axis):
         el = 0.0
@@ -301,6 +307,12 @@ def kernel_algorithmic(p, R: int, plan=None):
             and is_sine(ky[j], by[j]) and bx[i] == by[j] and 2 * (bx[i] + 1) in (32, 64, 128)
         return (XPLANE and not p.real and not fz
                 and not is_sine(kx[i], bx[i]) and not is_sine(ky[j], by[j]) and bx[i] <= 32 and by[j] <= 32)
+    xcand = xfused
+    xp_ok = 2 * sum(bx[i] * by[j] for i in range(len(bx)) for j in range(len(by)) if xcand(i, j)) \
+        >= sum(bx[i] * by[j] for i in range(len(bx)) for j in range(len(by)))
+
+    def xfused(i, j):  # noqa: F811 (the rule above, gated by the plan-level share test)
+        return xp_ok and xcand(i, j)
 
     fc = bc = fr = br = 0.0  # complex-S / real-S dense passes (4 per block: x, y forward + inverse)
     for i in range(len(bx)):

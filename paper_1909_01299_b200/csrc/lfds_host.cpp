@@ -271,6 +271,7 @@ struct lfds_plan {
   // step-5 z-modal form (real z tables): Z^T (t x k) and Z (k x t) as real tables (offsets in
   // doubles), theta_t (complex slots)
   bool s5m = false;
+  bool xplane_ok = false;  // steps 1 and 7 of the small non-sine blocks as plane transforms (k_xplane)
   int64_t t_zt = 0, t_zf = 0, t_theta = 0;
   int64_t t_dd[3] = {0, 0, 0};  // double-double stencil tables (x, y, z) for the residual
   int64_t t_hz = 0, t_hhz = 0, t_sig = 0, t_sige = 0, t_ifx = 0, t_ify = 0, t_bx = 0, t_by = 0, t_xlo = 0, t_ylo = 0;
@@ -684,7 +685,7 @@ static int build_pass(lfds_plan* P, int R, int in_real, int out_real, PassPlan& 
   // bases): steps 1 and 7 as plane transforms (k_xplane)
   auto xplane = [&](int b) {
     const AxisBlock &bx = X.blocks[b % nbx], &by = Y.blocks[b / nbx];
-    return xplane_on() && !fused2(b) && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
+    return P->xplane_ok && !fused2(b) && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
   };
   if (pp.use_xform) {
     std::vector<XPlaneDesc> fw, iv;
@@ -1650,13 +1651,24 @@ int lfds_setup_grid(int nx, const lfds_z* hx, int ny, const lfds_z* hy, int nz, 
   if (P->opt.plane_dst && P->opt.dtype != LFDS_F64)
     for (auto& by : Y.blocks)
       for (auto& bx : X.blocks) I.n_plane_dst += bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
-  I.n_plane_dense = 0;  // the xplane() rule of build_pass (complex data only)
-  if (xplane_on() && P->opt.dtype != LFDS_F64)
+  // the xplane() rule of build_pass (complex data only).  The plane form pays when the blocks it
+  // applies to carry the solve (C5: every block); a few small corner blocks among sine or large
+  // blocks (C3, C2, C4q, C4j) only add launches to launch-bound steps (C3 1.32 -> 1.41 ms), so it
+  // is used when those blocks hold at least half of the block unknowns.
+  I.n_plane_dense = 0;
+  if (xplane_on() && P->opt.dtype != LFDS_F64) {
+    int64_t el_x = 0, el_all = 0;
+    int cnt = 0;
     for (auto& by : Y.blocks)
       for (auto& bx : X.blocks) {
         const bool f2 = P->opt.plane_dst && bx.dst && by.dst && bx.n == by.n && dst2_supported(bx.n);
-        I.n_plane_dense += !f2 && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
+        const bool xp = !f2 && !bx.dst && !by.dst && bx.n <= 32 && by.n <= 32;
+        el_all += (int64_t)bx.n * by.n;
+        if (xp) { el_x += (int64_t)bx.n * by.n; ++cnt; }
       }
+    P->xplane_ok = 2 * el_x >= el_all && cnt > 0;
+    if (P->xplane_ok) I.n_plane_dense = cnt;
+  }
   *out = P.release();
   return LFDS_OK;
 }
