@@ -305,6 +305,9 @@ typedef struct {
   int n_plane_dense;           /* blocks whose steps 1 and 7 run as one plane  */
                                /* transform on DMMA (k_xplane): at most 32 nodes on both axes,    */
                                /* neither axis on the fast sine transform, complex data          */
+                               /* and those blocks holding at least half of the block unknowns   */
+                               /* (0 otherwise; the environment variable LFDS_XPLANE=0 forces the */
+                               /* x pass + y pass form for A/B runs)              */
 } lfds_info;
 int lfds_get_info(const lfds_plan* plan, lfds_info* info);
 
